@@ -1,0 +1,318 @@
+/*
+ * veloreg_gpu.h -- C ABI of the B200-native (sm_100a) operator layer for the
+ * CLAIRE / veloreg Gauss-Newton-Krylov registration hot path.
+ *
+ * The reference (/root/reference/proj, "veloreg") has no FFI: its operator
+ * boundary is the C++ template API Objective<T> (include/veloreg/objective.hpp:56-102),
+ * the free functions of transport.hpp / spectral.hpp / interp.hpp / field_ops.hpp,
+ * and the solver entry points of solver.hpp:100-164. Every function below names
+ * the reference interface it replaces. A C++ adapter rethrows
+ * status codes as the matching veloreg::Error subclasses.
+ *
+ * Conventions
+ *  - All arithmetic is IEEE fp64 (the reference precision for parity).
+ *  - Field arguments are DEVICE pointers (double*), laid out exactly like the
+ *    reference: scalar field = N = n1*n2*n3 doubles, row-major, axis 0 slowest,
+ *    linear index (i1*n2+i2)*n3+i3 (grid.hpp:17-19); vector field = 3 scalar
+ *    fields back to back (component c at ptr + c*N; VectorField SoA, field.hpp:101-126);
+ *    time series = (n_t+1) scalar fields back to back (field.hpp:129-151).
+ *    Spectra are complex128 interleaved (re,im), dims (n1, n2, n3/2+1) row-major
+ *    (fft.hpp:12-23).
+ *  - Functions ending in _host take HOST pointers and include the H2D/D2H copies.
+ *  - Every call is ordered on the context's CUDA stream; calls that return host
+ *    scalars synchronize that stream.
+ *  - Return value: 0 on success, else a veloreg::ErrorCategory value
+ *    (errors.hpp:9-17); vr_last_error() gives the thread-local message and
+ *    vr_last_error_class() the exception subclass to rethrow.
+ *  - Grids: every axis a power of two in [4, 1024] (the GPU FFT's domain).
+ */
+#ifndef VELOREG_GPU_H
+#define VELOREG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VR_ABI_VERSION 1
+
+/* ---- status codes: veloreg::ErrorCategory (errors.hpp:9-17) ---------------- */
+enum {
+    VR_OK = 0,
+    VR_ERR_IO = 2,
+    VR_ERR_FORMAT = 3,
+    VR_ERR_ARGUMENT = 4,
+    VR_ERR_NUMERICS = 5,
+    VR_ERR_CONVERGENCE = 6,
+    VR_ERR_RESOURCE = 7,
+    VR_ERR_LOGIC = 8
+};
+/* exception subclass of the last error (errors.hpp:32-67) */
+enum {
+    VR_EXC_NONE = 0,
+    VR_EXC_IO = 1,
+    VR_EXC_FORMAT = 2,
+    VR_EXC_ARGUMENT = 3,
+    VR_EXC_DIMENSION = 4, /* DimensionError : ArgumentError */
+    VR_EXC_NUMERIC = 5,
+    VR_EXC_CONVERGENCE = 6,
+    VR_EXC_RESOURCE = 7,
+    VR_EXC_LOGIC = 8
+};
+const char* vr_last_error(void);
+int vr_last_error_class(void);
+int vr_abi_version(void);
+
+/* ---- model / solver parameter PODs ---------------------------------------- */
+/* RegKind, spectral.hpp:71 */
+enum { VR_REG_H1 = 0, VR_REG_H2 = 1, VR_REG_H3 = 2, VR_REG_HELMHOLTZ = 3 };
+/* RegOpMode, spectral.hpp:104 */
+enum { VR_REGOP_APPLY = 0, VR_REGOP_INVERSE = 1, VR_REGOP_INVERSE_SQRT = 2 };
+/* ProjectionKind, spectral.hpp:115 */
+enum { VR_PROJ_IDENTITY = 0, VR_PROJ_INCOMPRESSIBLE = 1, VR_PROJ_NEAR_INCOMPRESSIBLE = 2 };
+/* TraceDirection, transport.hpp:17 */
+enum { VR_TRACE_BACKWARD = 0, VR_TRACE_FORWARD = 1 };
+/* StopReason, solver.hpp:35-41 */
+enum {
+    VR_STOP_ZERO_GRADIENT = 0,
+    VR_STOP_CONVERGED_REL = 1,
+    VR_STOP_CONVERGED_ABS = 2,
+    VR_STOP_MAX_ITERATIONS = 3,
+    VR_STOP_LINE_SEARCH_FAILURE = 4
+};
+/* Krylov preconditioner choice (solver.hpp:130-150) */
+enum { VR_PRECOND_NONE = 0, VR_PRECOND_SPECTRAL = 1 };
+
+/* RegNorm, spectral.hpp:75-102 (defaults: H2, gamma 1, squared, no penalty, beta_w 1e-4) */
+typedef struct {
+    int kind;
+    double gamma;
+    int helmholtz_squared;
+    int div_penalty;
+    double beta_w;
+} vr_regnorm;
+
+/* RegModel, objective.hpp:11-23 (defaults: K = identity, beta_v 1e-2, n_t 4, GN) */
+typedef struct {
+    vr_regnorm norm;
+    int projection;
+    double beta_v;
+    int nt;
+    int gauss_newton;
+} vr_model;
+
+/* SolverParams, solver.hpp:13-33 */
+typedef struct {
+    double eps_opt;
+    double abs_grad_tol;
+    int max_newton;
+    int max_krylov;
+    double armijo_c1;
+    double armijo_backtrack;
+    int armijo_max_trials;
+    int squared_norm_stop;
+} vr_solver_params;
+
+/* SolveCounters, objective.hpp:26-31 */
+typedef struct {
+    long objective_evals;
+    long gradient_evals;
+    long hessian_matvecs;
+    long pde_solves;
+} vr_counters;
+
+/* IterationRecord, solver.hpp:45-58 */
+typedef struct {
+    int k;
+    double objective;
+    double mismatch_rel;
+    double grad_norm;
+    double grad_rel;
+    double step_length;
+    double forcing;
+    int inner_iterations;
+    long fine_matvecs;
+    long coarse_matvecs;
+    long pde_solves;
+    double wall_time_s;
+} vr_iteration_record;
+
+/* SolveReport, solver.hpp:60-75 (records returned separately) */
+typedef struct {
+    int stop;
+    int success;
+    int outer_iterations;
+    double grad0;
+    double final_grad_rel;
+    double final_mismatch_rel;
+    double final_objective;
+    double wall_time_s;
+    vr_counters fine;
+    vr_counters coarse;
+    int n_records; /* number of IterationRecords produced */
+} vr_solve_report;
+
+/* PcgStats, solver.hpp:87-93 */
+typedef struct {
+    int iterations;
+    double rel_residual;
+    int converged;
+    int negative_curvature;
+    int hit_max_iterations;
+} vr_pcg_stats;
+
+void vr_model_default(vr_model* m);
+void vr_solver_params_default(vr_solver_params* p);
+/* RegModel::validate / RegNorm::validate / SolverParams::validate */
+int vr_model_validate(const vr_model* m);
+int vr_solver_params_validate(const vr_solver_params* p);
+
+/* ---- context: one grid, one device, one stream ---------------------------- */
+typedef struct vr_ctx vr_ctx;
+/* Grid3 ctor (grid.hpp:24-31): DimensionError for dims < 4 or not a power of two <= 1024 */
+int vr_ctx_create(int n1, int n2, int n3, int device, vr_ctx** out);
+int vr_ctx_destroy(vr_ctx* ctx);
+int vr_ctx_synchronize(vr_ctx* ctx);
+void* vr_ctx_stream(vr_ctx* ctx); /* cudaStream_t */
+int vr_ctx_grid(const vr_ctx* ctx, int dims[3]);
+/* kernels launched on this ctx since creation / last reset (evidence counter) */
+long long vr_ctx_kernel_launches(const vr_ctx* ctx);
+void vr_ctx_reset_kernel_launches(vr_ctx* ctx);
+
+/* device / pinned memory plumbing */
+int vr_device_alloc(vr_ctx* ctx, size_t bytes, void** out);
+int vr_device_free(vr_ctx* ctx, void* p);
+int vr_host_alloc_pinned(size_t bytes, void** out);
+int vr_host_free_pinned(void* p);
+int vr_memcpy_h2d(vr_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes); /* async */
+int vr_memcpy_d2h(vr_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes); /* syncs */
+int vr_memcpy_d2d(vr_ctx* ctx, void* dst_dev, const void* src_dev, size_t bytes); /* async */
+int vr_memset_zero(vr_ctx* ctx, void* dst_dev, size_t bytes);                     /* async */
+
+/* ---- BLAS-1 with deterministic reductions (field_ops.hpp:14-111) --------- */
+/* ncomp = 1 (ScalarField) or 3 (VectorField); 'n' fields of the grid */
+int vr_scale(vr_ctx* ctx, double* x, int ncomp, double a);                               /* scale */
+int vr_add_scaled(vr_ctx* ctx, double* y, double a, const double* x, int ncomp);          /* add_scaled */
+int vr_lin_comb(vr_ctx* ctx, double* out, double a, const double* x, double b, const double* y,
+                int ncomp);                                                              /* lin_comb */
+int vr_dot_l2(vr_ctx* ctx, const double* a, const double* b, int ncomp, double* out);    /* dot_l2 */
+int vr_norm_l2(vr_ctx* ctx, const double* a, int ncomp, double* out);                    /* norm_l2 */
+int vr_max_abs(vr_ctx* ctx, const double* a, int ncomp, double* out);                    /* max_abs */
+int vr_max_magnitude(vr_ctx* ctx, const double* v3, double* out);                        /* max_magnitude */
+int vr_all_finite(vr_ctx* ctx, const double* a, int ncomp, int* out);                    /* all_finite */
+/* weighted h1*h2*h3 * sum a*b (spectral.cpp:47-62) */
+int vr_inner_product(vr_ctx* ctx, const double* a, const double* b, int ncomp, double* out);
+
+/* ---- spectral operators (fft.hpp, spectral.hpp) ---------------------------- */
+/* fft_forward_raw (fft.cpp:66-73): unnormalized r2c */
+int vr_fft_r2c(vr_ctx* ctx, const double* in, double* out_spectrum);
+/* fft_inverse_raw (fft.cpp:75-83): c2r including the 1/N scale */
+int vr_fft_c2r(vr_ctx* ctx, const double* spectrum, double* out);
+int vr_gradient(vr_ctx* ctx, const double* f, double* out3);              /* spectral.cpp:108-122 */
+int vr_divergence(vr_ctx* ctx, const double* v3, double* out);            /* spectral.cpp:124-140 */
+int vr_laplacian(vr_ctx* ctx, const double* f, double* out, int ncomp);   /* spectral.cpp:142-153 */
+int vr_helmholtz1_apply(vr_ctx* ctx, const double* f, double* out);       /* spectral.cpp:155-160 */
+int vr_gaussian_smooth(vr_ctx* ctx, const double* f, double* out, int ncomp,
+                       const double sigma_voxels[3]);                     /* spectral.cpp:84-106 */
+int vr_apply_reg_operator(vr_ctx* ctx, const double* v3, double* out3, const vr_regnorm* norm,
+                          int mode, double beta);                         /* spectral.cpp:166-184 */
+int vr_apply_projection(vr_ctx* ctx, const double* f3, double* out3, int kind, double beta_v,
+                        double beta_w);                                   /* spectral.cpp:190-222 */
+int vr_rescale_intensity(vr_ctx* ctx, const double* f, double* out, int* degenerate); /* spectral.cpp:64-78 */
+
+/* ---- semi-Lagrangian transport (interp.hpp, transport.hpp) ------------------ */
+int vr_tricubic_interpolate(vr_ctx* ctx, const double* f, const double* points3, double* out,
+                            int nfields /* 1..3: f holds nfields fields */); /* interp.hpp:80-126 */
+int vr_trace_characteristics(vr_ctx* ctx, const double* v3, int nt, int direction,
+                             double* departure3);                              /* transport.cpp:11-42 */
+int vr_continuity_factor(vr_ctx* ctx, const double* div_v, const double* departure3, double dt,
+                         double* factor);                                      /* transport.cpp:44-55 */
+int vr_solve_state(vr_ctx* ctx, const double* m_T, const double* v3, int nt,
+                   double* history);                                           /* transport.cpp:72-86 */
+/* solve_adjoint (transport.cpp:115-124); history (nt+1 fields) may be NULL, initial may be NULL */
+int vr_solve_adjoint(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
+                     double* history, double* initial);
+int vr_gradient_dot(vr_ctx* ctx, const double* f, const double* w3, double* out); /* transport.cpp:126-148 */
+int vr_solve_inc_state(vr_ctx* ctx, const double* m_history, const double* v3, const double* vt3,
+                       int nt, double* mt_history);                            /* transport.cpp:150-180 */
+/* Gauss-Newton branch of solve_inc_adjoint (transport.cpp:182-191, :228-237) */
+int vr_solve_inc_adjoint(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
+                         double* history, double* initial);
+
+/* ---- Objective (objective.hpp:56-102) -------------------------------------- */
+typedef struct vr_objective vr_objective;
+typedef struct vr_state vr_state;
+/* Objective ctor (objective.cpp:35-45); m_R, m_T are device pointers that must
+ * outlive the objective (the reference holds non-owning pointers, objective.hpp:97-98).
+ * counters may be NULL (then the objective keeps none, like counters_ == nullptr). */
+int vr_objective_create(vr_ctx* ctx, const double* m_R, const double* m_T, const vr_model* model,
+                        vr_objective** out);
+int vr_objective_destroy(vr_objective* obj);
+int vr_objective_initial_mismatch(const vr_objective* obj, double* out);
+int vr_objective_counters(const vr_objective* obj, vr_counters* out);
+int vr_objective_reset_counters(vr_objective* obj);
+int vr_objective_set_beta(vr_objective* obj, double beta_v); /* continuation levels */
+
+/* evaluate (objective.cpp:47-75): state solve + J. 1 PDE solve. */
+int vr_evaluate(vr_objective* obj, const double* v3, vr_state** out_state);
+int vr_state_destroy(vr_state* s);
+/* EvalState scalars (objective.hpp:37-54) */
+int vr_state_scalars(const vr_state* s, double* objective, double* mismatch, double* mismatch_rel,
+                     int* has_gradient, int* has_adjoint_ctx);
+/* copies of the frozen EvalState fields for parity checks */
+enum {
+    VR_STATE_V = 0,          /* 3 fields */
+    VR_STATE_X_BWD = 1,      /* 3 fields */
+    VR_STATE_X_FWD = 2,      /* 3 fields (after the gradient) */
+    VR_STATE_FACTOR = 3,     /* 1 field  (after the gradient) */
+    VR_STATE_M_HISTORY = 4,  /* nt+1 fields */
+    VR_STATE_GRADIENT = 5,   /* 3 fields (after the gradient) */
+    VR_STATE_GRAD_M = 6      /* 3*(nt+1) fields: d_a m_j at [j*3 + a] (after the gradient) */
+};
+int vr_state_get(const vr_state* s, int which, double* out_dev);
+/* compute_gradient (objective.cpp:77-112): adjoint sweep with fused accumulation. 1 PDE solve.
+ * g3 (device, may be NULL) receives a copy of the gradient. */
+int vr_compute_gradient(vr_objective* obj, vr_state* s, double* g3);
+/* hessian_matvec (objective.cpp:114-121): H vt = H_data vt + beta_v A vt. 2 PDE solves. */
+int vr_hessian_matvec(vr_objective* obj, const vr_state* s, const double* vt3, double* out3);
+/* same, HOST buffers in and out (H2D + matvec + D2H): the end-to-end entry */
+int vr_hessian_matvec_host(vr_objective* obj, const vr_state* s, const double* vt3_host,
+                           double* out3_host);
+/* hessian_data_matvec (objective.cpp:123-156) */
+int vr_hessian_data_matvec(vr_objective* obj, const vr_state* s, const double* vt3, double* out3);
+/* apply_reg / apply_K (objective.cpp:178-186) */
+int vr_objective_apply_reg(vr_objective* obj, const double* u3, int mode, double* out3);
+int vr_objective_apply_K(vr_objective* obj, const double* u3, double* out3);
+
+/* ---- solvers (solver.hpp:78-164; host driver over the device operators) ---- */
+int vr_compute_forcing(double grad_norm, double grad0_norm, double* out); /* solver.cpp:23-27 */
+/* pcg_solve on the GN Hessian of (obj, s) with the chosen preconditioner (solver.cpp:51-100) */
+int vr_pcg_solve(vr_objective* obj, const vr_state* s, const double* rhs3, double rel_tol,
+                 int max_iter, int precond, double* x3, vr_pcg_stats* stats);
+/* gauss_newton_solve (solver.cpp:154-269): all pointers device; v_out may alias nothing.
+ * records (host, may be NULL) receives up to max_records IterationRecords. */
+int vr_gauss_newton_solve(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                          const vr_model* model, const vr_solver_params* params, int precond,
+                          double* v_out, vr_solve_report* report, vr_iteration_record* records,
+                          int max_records);
+/* Parameter continuation in beta_v: levels 1, 1e-1, ... down to
+ * model->beta_v (last level snapped to the target), each warm-started from the
+ * previous velocity. reports[level] / records (concatenated) are filled for
+ * up to max_levels levels; *n_levels receives the number of levels run. */
+int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                              const vr_model* model, const vr_solver_params* params, int precond,
+                              double* v_out, vr_solve_report* reports, int max_levels,
+                              int* n_levels, vr_iteration_record* records, int max_records);
+
+/* ---- synthetic inputs (synthetic.cpp:10-34) -------------------------------- */
+/* m_T, v* analytic on the grid; m_R = solve_state(m_T, v*, nt).final() on the GPU */
+int vr_generate_synthetic(vr_ctx* ctx, int nt, double amplitude, double* m_R, double* m_T,
+                          double* v_star);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VELOREG_GPU_H */

@@ -1,0 +1,433 @@
+"""oracle/ref.py -- TEST INFRASTRUCTURE ONLY: ctypes access to the compiled reference.
+
+Loads oracle/_ref/libveloreg_ref.so (the UNMODIFIED reference sources from
+/root/reference/proj/src compiled with the FFTW/doctest shims plus the
+ref_capi.cpp harness, see oracle/Makefile) and exposes the reference's
+operators on host numpy arrays with the same names as the product's Python
+mirror (paper_1808_04487_b200.veloreg). Only tests/, __graft_entry__.smoke()
+and bench.py's CPU-baseline legs may import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libveloreg_ref.so")
+sys.path.insert(0, os.path.dirname(_HERE))
+from paper_1808_04487_b200 import _lib as _gpu_lib_types  # noqa: E402  (POD layouts only)
+
+RegNorm = _gpu_lib_types.RegNorm
+Model = _gpu_lib_types.Model
+SolverParams = _gpu_lib_types.SolverParams
+Counters = _gpu_lib_types.Counters
+SolveReport = _gpu_lib_types.SolveReport
+IterationRecord = _gpu_lib_types.IterationRecord
+PcgStats = _gpu_lib_types.PcgStats
+
+_lib = None
+P, D, I = C.c_void_p, C.c_double, C.c_int
+DIMS = C.POINTER(C.c_int)
+_SIG = {
+    "vref_last_error": (C.c_char_p, []),
+    "vref_last_error_class": (I, []),
+    "vref_set_workers": (None, [I]),
+    "vref_workers": (I, []),
+    "vref_fft_r2c": (I, [DIMS, P, P]),
+    "vref_fft_c2r": (I, [DIMS, P, P]),
+    "vref_gradient": (I, [DIMS, P, P]),
+    "vref_divergence": (I, [DIMS, P, P]),
+    "vref_laplacian": (I, [DIMS, P, P]),
+    "vref_helmholtz1_apply": (I, [DIMS, P, P]),
+    "vref_gaussian_smooth": (I, [DIMS, P, P, C.POINTER(D)]),
+    "vref_apply_reg_operator": (I, [DIMS, P, P, C.POINTER(RegNorm), I, D]),
+    "vref_apply_projection": (I, [DIMS, P, P, I, D, D]),
+    "vref_rescale_intensity": (I, [DIMS, P, P, C.POINTER(C.c_int)]),
+    "vref_inner_product": (I, [DIMS, P, P, I, C.POINTER(D)]),
+    "vref_dot_l2": (I, [DIMS, P, P, I, C.POINTER(D)]),
+    "vref_max_magnitude": (I, [DIMS, P, C.POINTER(D)]),
+    "vref_tricubic_interpolate": (I, [DIMS, P, P, P, I]),
+    "vref_trace_characteristics": (I, [DIMS, P, I, I, P]),
+    "vref_continuity_factor": (I, [DIMS, P, P, D, P]),
+    "vref_solve_state": (I, [DIMS, P, P, I, P]),
+    "vref_solve_adjoint": (I, [DIMS, P, P, I, P, P]),
+    "vref_gradient_dot": (I, [DIMS, P, P, P]),
+    "vref_solve_inc_state": (I, [DIMS, P, P, P, I, I, P]),
+    "vref_solve_inc_adjoint": (I, [DIMS, P, P, I, P, P]),
+    "vref_objective_create": (I, [DIMS, P, P, C.POINTER(Model), C.POINTER(P)]),
+    "vref_objective_destroy": (None, [P]),
+    "vref_objective_initial_mismatch": (I, [P, C.POINTER(D)]),
+    "vref_objective_counters": (I, [P, C.POINTER(Counters)]),
+    "vref_evaluate": (I, [P, P, C.POINTER(P)]),
+    "vref_state_destroy": (None, [P]),
+    "vref_state_scalars": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(C.c_int),
+                               C.POINTER(C.c_int)]),
+    "vref_state_get": (I, [P, I, P]),
+    "vref_compute_gradient": (I, [P, P, P]),
+    "vref_hessian_matvec": (I, [P, P, P, P]),
+    "vref_hessian_data_matvec": (I, [P, P, P, P]),
+    "vref_objective_apply_reg": (I, [P, P, I, P]),
+    "vref_objective_apply_K": (I, [P, P, P]),
+    "vref_pcg_solve": (I, [P, P, P, D, I, I, P, C.POINTER(PcgStats)]),
+    "vref_gauss_newton_solve": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I, P,
+                                    C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
+    "vref_parameter_continuation": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I,
+                                        P, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
+                                        C.POINTER(IterationRecord), I]),
+    "vref_generate_synthetic": (I, [DIMS, I, D, P, P, P]),
+    "vref_random_smooth_scalar": (I, [DIMS, I, C.c_ulonglong, D, P]),
+    "vref_random_smooth_vector": (I, [DIMS, I, C.c_ulonglong, D, P]),
+    "vref_random_rough_scalar": (I, [DIMS, C.c_ulonglong, P]),
+}
+
+
+class RefError(RuntimeError):
+    def __init__(self, status, cls, msg):
+        super().__init__(msg)
+        self.status, self.cls = status, cls
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise ImportError(f"{LIB_PATH} not built (make -C oracle lib)")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIG.items():
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = lib
+    return _lib
+
+
+def _call(name, *args):
+    lib = load()
+    st = getattr(lib, name)(*args)
+    if st:
+        raise RefError(st, lib.vref_last_error_class(), lib.vref_last_error().decode())
+
+
+def _dims(shape):
+    return (C.c_int * 3)(*shape[-3:])
+
+
+def _a(x):
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def set_workers(n: int):
+    load().vref_set_workers(int(n))
+
+
+# ---- operators (host numpy in / out) --------------------------------------------
+def fft_forward(f):
+    f = _a(f)
+    n1, n2, n3 = f.shape
+    out = np.empty((n1, n2, n3 // 2 + 1), dtype=np.complex128)
+    _call("vref_fft_r2c", _dims(f.shape), f.ctypes.data, out.ctypes.data)
+    return out
+
+
+def fft_inverse(spec, shape):
+    s = np.ascontiguousarray(spec, dtype=np.complex128)
+    out = np.empty(shape)
+    _call("vref_fft_c2r", _dims(shape), s.ctypes.data, out.ctypes.data)
+    return out
+
+
+def _unary(name, f, out_fields):
+    f = _a(f)
+    shape = f.shape[-3:]
+    out = np.empty((out_fields,) + shape if out_fields > 1 else shape)
+    _call(name, _dims(shape), f.ctypes.data, out.ctypes.data)
+    return out
+
+
+def gradient(f):
+    return _unary("vref_gradient", f, 3)
+
+
+def divergence(v):
+    return _unary("vref_divergence", v, 1)
+
+
+def laplacian(f):
+    return _unary("vref_laplacian", f, 1)
+
+
+def helmholtz1_apply(f):
+    return _unary("vref_helmholtz1_apply", f, 1)
+
+
+def gaussian_smooth(f, sigma):
+    f = _a(f)
+    out = np.empty_like(f)
+    _call("vref_gaussian_smooth", _dims(f.shape), f.ctypes.data, out.ctypes.data,
+          (C.c_double * 3)(*sigma))
+    return out
+
+
+def apply_reg_operator(v, norm, mode, beta=1.0):
+    v = _a(v)
+    out = np.empty_like(v)
+    _call("vref_apply_reg_operator", _dims(v.shape), v.ctypes.data, out.ctypes.data, C.byref(norm),
+          mode, beta)
+    return out
+
+
+def apply_projection(v, kind, beta_v=0.0, beta_w=0.0):
+    v = _a(v)
+    out = np.empty_like(v)
+    _call("vref_apply_projection", _dims(v.shape), v.ctypes.data, out.ctypes.data, kind, beta_v, beta_w)
+    return out
+
+
+def rescale_intensity(f):
+    f = _a(f)
+    out = np.empty_like(f)
+    deg = C.c_int()
+    _call("vref_rescale_intensity", _dims(f.shape), f.ctypes.data, out.ctypes.data, C.byref(deg))
+    return out, bool(deg.value)
+
+
+def inner_product(a, b):
+    a, b = _a(a), _a(b)
+    r = C.c_double()
+    _call("vref_inner_product", _dims(a.shape), a.ctypes.data, b.ctypes.data, 3 if a.ndim == 4 else 1,
+          C.byref(r))
+    return r.value
+
+
+def dot_l2(a, b):
+    a, b = _a(a), _a(b)
+    r = C.c_double()
+    _call("vref_dot_l2", _dims(a.shape), a.ctypes.data, b.ctypes.data, 3 if a.ndim == 4 else 1, C.byref(r))
+    return r.value
+
+
+def max_magnitude(v):
+    v = _a(v)
+    r = C.c_double()
+    _call("vref_max_magnitude", _dims(v.shape), v.ctypes.data, C.byref(r))
+    return r.value
+
+
+def tricubic_interpolate(f, points):
+    f, p = _a(f), _a(points)
+    nf = 1 if f.ndim == 3 else f.shape[0]
+    out = np.empty_like(f)
+    _call("vref_tricubic_interpolate", _dims(p.shape), f.ctypes.data, p.ctypes.data, out.ctypes.data, nf)
+    return out
+
+
+def trace_characteristics(v, nt, direction="backward"):
+    v = _a(v)
+    out = np.empty_like(v)
+    _call("vref_trace_characteristics", _dims(v.shape), v.ctypes.data, nt,
+          0 if direction == "backward" else 1, out.ctypes.data)
+    return out
+
+
+def continuity_factor(div_v, departure, dt):
+    d, p = _a(div_v), _a(departure)
+    out = np.empty_like(d)
+    _call("vref_continuity_factor", _dims(d.shape), d.ctypes.data, p.ctypes.data, dt, out.ctypes.data)
+    return out
+
+
+def solve_state(m_T, v, nt):
+    m, v = _a(m_T), _a(v)
+    out = np.empty((nt + 1,) + m.shape)
+    _call("vref_solve_state", _dims(m.shape), m.ctypes.data, v.ctypes.data, nt, out.ctypes.data)
+    return out
+
+
+def solve_adjoint(terminal, v, nt, needs_history=False):
+    t, v = _a(terminal), _a(v)
+    init = np.empty_like(t)
+    hist = np.empty((nt + 1,) + t.shape) if needs_history else None
+    _call("vref_solve_adjoint", _dims(t.shape), t.ctypes.data, v.ctypes.data, nt,
+          hist.ctypes.data if hist is not None else None, init.ctypes.data)
+    return init, hist
+
+
+def solve_inc_adjoint(terminal, v, nt, needs_history=False):
+    t, v = _a(terminal), _a(v)
+    init = np.empty_like(t)
+    hist = np.empty((nt + 1,) + t.shape) if needs_history else None
+    _call("vref_solve_inc_adjoint", _dims(t.shape), t.ctypes.data, v.ctypes.data, nt,
+          hist.ctypes.data if hist is not None else None, init.ctypes.data)
+    return init, hist
+
+
+def gradient_dot(f, w):
+    f, w = _a(f), _a(w)
+    out = np.empty_like(f)
+    _call("vref_gradient_dot", _dims(f.shape), f.ctypes.data, w.ctypes.data, out.ctypes.data)
+    return out
+
+
+def solve_inc_state(m_history, v, v_tilde, nt):
+    m, v, vt = _a(m_history), _a(v), _a(v_tilde)
+    out = np.empty((nt + 1,) + m.shape[-3:])
+    _call("vref_solve_inc_state", _dims(m.shape), m.ctypes.data, v.ctypes.data, vt.ctypes.data, nt,
+          m.shape[0], out.ctypes.data)
+    return out
+
+
+def generate_synthetic(shape, nt, amplitude=1.0):
+    mR, mT = np.empty(shape), np.empty(shape)
+    vs = np.empty((3,) + tuple(shape))
+    _call("vref_generate_synthetic", _dims(shape), nt, amplitude, mR.ctypes.data, mT.ctypes.data,
+          vs.ctypes.data)
+    return mR, mT, vs
+
+
+def random_smooth_scalar(shape, max_mode, seed, amplitude):
+    out = np.empty(shape)
+    _call("vref_random_smooth_scalar", _dims(shape), max_mode, seed, amplitude, out.ctypes.data)
+    return out
+
+
+def random_smooth_vector(shape, max_mode, seed, amplitude):
+    out = np.empty((3,) + tuple(shape))
+    _call("vref_random_smooth_vector", _dims(shape), max_mode, seed, amplitude, out.ctypes.data)
+    return out
+
+
+def random_rough_scalar(shape, seed):
+    out = np.empty(shape)
+    _call("vref_random_rough_scalar", _dims(shape), seed, out.ctypes.data)
+    return out
+
+
+# ---- objective ------------------------------------------------------------------
+class State:
+    def __init__(self, obj, h):
+        self.obj, self._h = obj, h
+
+    def scalars(self):
+        J, mis, rel = C.c_double(), C.c_double(), C.c_double()
+        hg, hc = C.c_int(), C.c_int()
+        _call("vref_state_scalars", self._h, C.byref(J), C.byref(mis), C.byref(rel), C.byref(hg), C.byref(hc))
+        return {"objective": J.value, "mismatch": mis.value, "mismatch_rel": rel.value,
+                "has_gradient": bool(hg.value), "has_adjoint_ctx": bool(hc.value)}
+
+    def get(self, which):
+        nt = self.obj.model.nt
+        nf = {0: 3, 1: 3, 2: 3, 3: 1, 4: nt + 1, 5: 3}[which]
+        out = np.empty((nf,) + self.obj.shape if nf > 1 else self.obj.shape)
+        _call("vref_state_get", self._h, which, out.ctypes.data)
+        return out
+
+    def __del__(self):
+        if _lib is not None and getattr(self, "_h", None):
+            _lib.vref_state_destroy(self._h)
+            self._h = None
+
+
+class Objective:
+    def __init__(self, m_R, m_T, model):
+        self.shape = tuple(np.shape(m_R))
+        self.model = model
+        r, t = _a(m_R), _a(m_T)
+        h = C.c_void_p()
+        _call("vref_objective_create", _dims(self.shape), r.ctypes.data, t.ctypes.data, C.byref(model), C.byref(h))
+        self._h = h
+
+    def initial_mismatch(self):
+        r = C.c_double()
+        _call("vref_objective_initial_mismatch", self._h, C.byref(r))
+        return r.value
+
+    def counters(self):
+        c = Counters()
+        _call("vref_objective_counters", self._h, C.byref(c))
+        return {k: getattr(c, k) for k, _ in Counters._fields_}
+
+    def evaluate(self, v):
+        v = _a(v)
+        h = C.c_void_p()
+        _call("vref_evaluate", self._h, v.ctypes.data, C.byref(h))
+        return State(self, h)
+
+    def compute_gradient(self, s):
+        g = np.empty((3,) + self.shape)
+        _call("vref_compute_gradient", self._h, s._h, g.ctypes.data)
+        return g
+
+    def hessian_matvec(self, s, vt):
+        vt = _a(vt)
+        out = np.empty_like(vt)
+        _call("vref_hessian_matvec", self._h, s._h, vt.ctypes.data, out.ctypes.data)
+        return out
+
+    def hessian_data_matvec(self, s, vt):
+        vt = _a(vt)
+        out = np.empty_like(vt)
+        _call("vref_hessian_data_matvec", self._h, s._h, vt.ctypes.data, out.ctypes.data)
+        return out
+
+    def apply_reg(self, u, mode):
+        u = _a(u)
+        out = np.empty_like(u)
+        _call("vref_objective_apply_reg", self._h, u.ctypes.data, mode, out.ctypes.data)
+        return out
+
+    def apply_K(self, u):
+        u = _a(u)
+        out = np.empty_like(u)
+        _call("vref_objective_apply_K", self._h, u.ctypes.data, out.ctypes.data)
+        return out
+
+    def pcg_solve(self, s, rhs, rel_tol, max_iter, precond=1):
+        rhs = _a(rhs)
+        x = np.empty_like(rhs)
+        st = PcgStats()
+        _call("vref_pcg_solve", self._h, s._h, rhs.ctypes.data, rel_tol, max_iter, precond, x.ctypes.data, C.byref(st))
+        return x, {k: getattr(st, k) for k, _ in PcgStats._fields_}
+
+    def __del__(self):
+        if _lib is not None and getattr(self, "_h", None):
+            _lib.vref_objective_destroy(self._h)
+            self._h = None
+
+
+def _report(r):
+    d = {k: getattr(r, k) for k, _ in SolveReport._fields_ if k not in ("fine", "coarse")}
+    for nm in ("fine", "coarse"):
+        c = getattr(r, nm)
+        d[nm] = {k: getattr(c, k) for k, _ in Counters._fields_}
+    return d
+
+
+def gauss_newton_solve(m_R, m_T, v0, model, params, precond=1, max_records=512):
+    r, t, v0 = _a(m_R), _a(m_T), _a(v0)
+    vout = np.empty_like(v0)
+    rep = SolveReport()
+    recs = (IterationRecord * max_records)()
+    _call("vref_gauss_newton_solve", _dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data,
+          C.byref(model), C.byref(params), precond, vout.ctypes.data, C.byref(rep), recs, max_records)
+    n = min(rep.n_records, max_records)
+    return vout, _report(rep), [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
+
+
+def parameter_continuation(m_R, m_T, v0, model, params, precond=1, max_levels=16, max_records=1024):
+    r, t, v0 = _a(m_R), _a(m_T), _a(v0)
+    vout = np.empty_like(v0)
+    reps = (SolveReport * max_levels)()
+    recs = (IterationRecord * max_records)()
+    nl = C.c_int()
+    _call("vref_parameter_continuation", _dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data,
+          C.byref(model), C.byref(params), precond, vout.ctypes.data, reps, max_levels, C.byref(nl),
+          recs, max_records)
+    reports = [_report(reps[i]) for i in range(min(nl.value, max_levels))]
+    n = min(sum(x["n_records"] for x in reports), max_records)
+    return vout, reports, [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]

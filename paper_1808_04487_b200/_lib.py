@@ -1,0 +1,238 @@
+"""ctypes binding of the C ABI in include/veloreg_gpu.h (libveloreg_gpu.so).
+
+The shared library is built in-tree (``make -C paper_1808_04487_b200``). There is
+no CPU fallback: importing the package without the library, or calling it
+without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libveloreg_gpu.so")
+
+# ---- error hierarchy mirroring veloreg::Error (proj/include/veloreg/errors.hpp:9-67)
+
+
+class VelouregError(RuntimeError):
+    category = 0
+
+
+class IoError(VelouregError):
+    category = 2
+
+
+class FormatError(VelouregError):
+    category = 3
+
+
+class ArgumentError(VelouregError):
+    category = 4
+
+
+class DimensionError(ArgumentError):
+    pass
+
+
+class NumericError(VelouregError):
+    category = 5
+
+
+class ConvergenceError(VelouregError):
+    category = 6
+
+
+class ResourceError(VelouregError):
+    category = 7
+
+
+class LogicError(VelouregError):
+    category = 8
+
+
+_EXC_BY_CLASS = {
+    1: IoError,
+    2: FormatError,
+    3: ArgumentError,
+    4: DimensionError,
+    5: NumericError,
+    6: ConvergenceError,
+    7: ResourceError,
+    8: LogicError,
+}
+_EXC_BY_STATUS = {2: IoError, 3: FormatError, 4: ArgumentError, 5: NumericError,
+                  6: ConvergenceError, 7: ResourceError, 8: LogicError}
+
+# ---- POD mirrors ------------------------------------------------------------
+
+
+class RegNorm(C.Structure):
+    _fields_ = [("kind", C.c_int), ("gamma", C.c_double), ("helmholtz_squared", C.c_int),
+                ("div_penalty", C.c_int), ("beta_w", C.c_double)]
+
+
+class Model(C.Structure):
+    _fields_ = [("norm", RegNorm), ("projection", C.c_int), ("beta_v", C.c_double),
+                ("nt", C.c_int), ("gauss_newton", C.c_int)]
+
+
+class SolverParams(C.Structure):
+    _fields_ = [("eps_opt", C.c_double), ("abs_grad_tol", C.c_double), ("max_newton", C.c_int),
+                ("max_krylov", C.c_int), ("armijo_c1", C.c_double),
+                ("armijo_backtrack", C.c_double), ("armijo_max_trials", C.c_int),
+                ("squared_norm_stop", C.c_int)]
+
+
+class Counters(C.Structure):
+    _fields_ = [("objective_evals", C.c_long), ("gradient_evals", C.c_long),
+                ("hessian_matvecs", C.c_long), ("pde_solves", C.c_long)]
+
+
+class IterationRecord(C.Structure):
+    _fields_ = [("k", C.c_int), ("objective", C.c_double), ("mismatch_rel", C.c_double),
+                ("grad_norm", C.c_double), ("grad_rel", C.c_double),
+                ("step_length", C.c_double), ("forcing", C.c_double),
+                ("inner_iterations", C.c_int), ("fine_matvecs", C.c_long),
+                ("coarse_matvecs", C.c_long), ("pde_solves", C.c_long),
+                ("wall_time_s", C.c_double)]
+
+
+class SolveReport(C.Structure):
+    _fields_ = [("stop", C.c_int), ("success", C.c_int), ("outer_iterations", C.c_int),
+                ("grad0", C.c_double), ("final_grad_rel", C.c_double),
+                ("final_mismatch_rel", C.c_double), ("final_objective", C.c_double),
+                ("wall_time_s", C.c_double), ("fine", Counters), ("coarse", Counters),
+                ("n_records", C.c_int)]
+
+
+class PcgStats(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("rel_residual", C.c_double), ("converged", C.c_int),
+                ("negative_curvature", C.c_int), ("hit_max_iterations", C.c_int)]
+
+
+# constants (veloreg_gpu.h)
+REG_H1, REG_H2, REG_H3, REG_HELMHOLTZ = 0, 1, 2, 3
+REGOP_APPLY, REGOP_INVERSE, REGOP_INVERSE_SQRT = 0, 1, 2
+PROJ_IDENTITY, PROJ_INCOMPRESSIBLE, PROJ_NEAR_INCOMPRESSIBLE = 0, 1, 2
+TRACE_BACKWARD, TRACE_FORWARD = 0, 1
+PRECOND_NONE, PRECOND_SPECTRAL = 0, 1
+STOP_NAMES = ["zero_gradient", "converged_rel", "converged_abs", "max_iterations",
+              "line_search_failure"]
+STATE_V, STATE_X_BWD, STATE_X_FWD, STATE_FACTOR, STATE_M_HISTORY, STATE_GRADIENT, STATE_GRAD_M = range(7)
+
+P = C.c_void_p
+D = C.c_double
+I = C.c_int
+DP = C.c_void_p  # device pointer
+HP = C.c_void_p  # host pointer
+
+# name -> (restype, argtypes); all status-returning functions have restype int
+SIGNATURES = {
+    "vr_last_error": (C.c_char_p, []),
+    "vr_last_error_class": (I, []),
+    "vr_abi_version": (I, []),
+    "vr_model_default": (None, [C.POINTER(Model)]),
+    "vr_solver_params_default": (None, [C.POINTER(SolverParams)]),
+    "vr_model_validate": (I, [C.POINTER(Model)]),
+    "vr_solver_params_validate": (I, [C.POINTER(SolverParams)]),
+    "vr_ctx_create": (I, [I, I, I, I, C.POINTER(P)]),
+    "vr_ctx_destroy": (I, [P]),
+    "vr_ctx_synchronize": (I, [P]),
+    "vr_ctx_stream": (P, [P]),
+    "vr_ctx_grid": (I, [P, C.POINTER(C.c_int)]),
+    "vr_ctx_kernel_launches": (C.c_longlong, [P]),
+    "vr_ctx_reset_kernel_launches": (None, [P]),
+    "vr_device_alloc": (I, [P, C.c_size_t, C.POINTER(P)]),
+    "vr_device_free": (I, [P, P]),
+    "vr_host_alloc_pinned": (I, [C.c_size_t, C.POINTER(P)]),
+    "vr_host_free_pinned": (I, [P]),
+    "vr_memcpy_h2d": (I, [P, DP, HP, C.c_size_t]),
+    "vr_memcpy_d2h": (I, [P, HP, DP, C.c_size_t]),
+    "vr_memcpy_d2d": (I, [P, DP, DP, C.c_size_t]),
+    "vr_memset_zero": (I, [P, DP, C.c_size_t]),
+    "vr_scale": (I, [P, DP, I, D]),
+    "vr_add_scaled": (I, [P, DP, D, DP, I]),
+    "vr_lin_comb": (I, [P, DP, D, DP, D, DP, I]),
+    "vr_dot_l2": (I, [P, DP, DP, I, C.POINTER(D)]),
+    "vr_norm_l2": (I, [P, DP, I, C.POINTER(D)]),
+    "vr_max_abs": (I, [P, DP, I, C.POINTER(D)]),
+    "vr_max_magnitude": (I, [P, DP, C.POINTER(D)]),
+    "vr_all_finite": (I, [P, DP, I, C.POINTER(C.c_int)]),
+    "vr_inner_product": (I, [P, DP, DP, I, C.POINTER(D)]),
+    "vr_fft_r2c": (I, [P, DP, DP]),
+    "vr_fft_c2r": (I, [P, DP, DP]),
+    "vr_gradient": (I, [P, DP, DP]),
+    "vr_divergence": (I, [P, DP, DP]),
+    "vr_laplacian": (I, [P, DP, DP, I]),
+    "vr_helmholtz1_apply": (I, [P, DP, DP]),
+    "vr_gaussian_smooth": (I, [P, DP, DP, I, C.POINTER(D)]),
+    "vr_apply_reg_operator": (I, [P, DP, DP, C.POINTER(RegNorm), I, D]),
+    "vr_apply_projection": (I, [P, DP, DP, I, D, D]),
+    "vr_rescale_intensity": (I, [P, DP, DP, C.POINTER(C.c_int)]),
+    "vr_tricubic_interpolate": (I, [P, DP, DP, DP, I]),
+    "vr_trace_characteristics": (I, [P, DP, I, I, DP]),
+    "vr_continuity_factor": (I, [P, DP, DP, D, DP]),
+    "vr_solve_state": (I, [P, DP, DP, I, DP]),
+    "vr_solve_adjoint": (I, [P, DP, DP, I, DP, DP]),
+    "vr_gradient_dot": (I, [P, DP, DP, DP]),
+    "vr_solve_inc_state": (I, [P, DP, DP, DP, I, DP]),
+    "vr_solve_inc_adjoint": (I, [P, DP, DP, I, DP, DP]),
+    "vr_objective_create": (I, [P, DP, DP, C.POINTER(Model), C.POINTER(P)]),
+    "vr_objective_destroy": (I, [P]),
+    "vr_objective_initial_mismatch": (I, [P, C.POINTER(D)]),
+    "vr_objective_counters": (I, [P, C.POINTER(Counters)]),
+    "vr_objective_reset_counters": (I, [P]),
+    "vr_objective_set_beta": (I, [P, D]),
+    "vr_evaluate": (I, [P, DP, C.POINTER(P)]),
+    "vr_state_destroy": (I, [P]),
+    "vr_state_scalars": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(C.c_int),
+                             C.POINTER(C.c_int)]),
+    "vr_state_get": (I, [P, I, DP]),
+    "vr_compute_gradient": (I, [P, P, DP]),
+    "vr_hessian_matvec": (I, [P, P, DP, DP]),
+    "vr_hessian_matvec_host": (I, [P, P, HP, HP]),
+    "vr_hessian_data_matvec": (I, [P, P, DP, DP]),
+    "vr_objective_apply_reg": (I, [P, DP, I, DP]),
+    "vr_objective_apply_K": (I, [P, DP, DP]),
+    "vr_compute_forcing": (I, [D, D, C.POINTER(D)]),
+    "vr_pcg_solve": (I, [P, P, DP, D, I, I, DP, C.POINTER(PcgStats)]),
+    "vr_gauss_newton_solve": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I,
+                                  DP, C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
+    "vr_parameter_continuation": (I, [P, DP, DP, DP, C.POINTER(Model),
+                                      C.POINTER(SolverParams), I, DP, C.POINTER(SolveReport), I,
+                                      C.POINTER(C.c_int), C.POINTER(IterationRecord), I]),
+    "vr_generate_synthetic": (I, [P, I, D, DP, DP, DP]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libveloreg_gpu.so and declare every exported symbol. Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `make -C {_HERE}` (no CPU fallback exists)")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    lib = load()
+    msg = lib.vr_last_error().decode(errors="replace")
+    cls = _EXC_BY_CLASS.get(lib.vr_last_error_class(), _EXC_BY_STATUS.get(status, VelouregError))
+    raise cls(msg)
+
+
+def call(name: str, *args):
+    fn = getattr(load(), name)
+    check(fn(*args))

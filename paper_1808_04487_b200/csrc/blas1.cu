@@ -1,0 +1,206 @@
+// blas1.cu -- fused pointwise updates and deterministic reductions.
+//
+// Replaces the reference's BLAS-1 layer (proj/include/veloreg/field_ops.hpp:14-111)
+// and its deterministic 64-chunk CPU reductions (parallel.hpp:68-97). Here the
+// reduction order is fixed by a constant grid of kRedBlocks blocks with a
+// shuffle tree per block and an ordered final pass, so results are bitwise
+// reproducible run to run (though not bitwise equal to the CPU chunk order).
+#include <cfloat>
+
+#include "vr_common.cuh"
+
+namespace vr {
+namespace {
+
+__global__ void k_scale(double* __restrict__ x, long long n, double a) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        x[i] = x[i] * a;
+}
+__global__ void k_add_scaled(double* __restrict__ y, double a, const double* __restrict__ x,
+                             long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = y[i] + a * x[i];
+}
+// out may alias x or y (elementwise)
+__global__ void k_lin_comb(double* out, double a, const double* x, double b, const double* y,
+                           long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = a * x[i] + b * y[i];
+}
+__global__ void k_affine(const double* __restrict__ x, double* __restrict__ out, long long n,
+                         double lo, double s) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = (x[i] - lo) * s;
+}
+
+enum class RedOp { dot, sumsq_diff, maxabs, maxmag2, nonfinite, minval, maxval };
+
+template <RedOp OP>
+__device__ __forceinline__ double red_term(const double* a, const double* b, long long i,
+                                           long long n) {
+    if constexpr (OP == RedOp::dot) return a[i] * b[i];
+    if constexpr (OP == RedOp::sumsq_diff) {
+        double d = a[i] - b[i];
+        return d * d;
+    }
+    if constexpr (OP == RedOp::maxabs) return fabs(a[i]);
+    if constexpr (OP == RedOp::maxmag2) {
+        double x = a[i], y = a[i + n], z = a[i + 2 * n];
+        return x * x + y * y + z * z;
+    }
+    if constexpr (OP == RedOp::nonfinite) return isfinite(a[i]) ? 0.0 : 1.0;
+    if constexpr (OP == RedOp::minval) return -a[i];
+    if constexpr (OP == RedOp::maxval) return a[i];
+    return 0.0;
+}
+template <RedOp OP>
+constexpr bool is_max() {
+    return OP == RedOp::maxabs || OP == RedOp::maxmag2 || OP == RedOp::minval ||
+           OP == RedOp::maxval;
+}
+
+template <RedOp OP>
+__device__ __forceinline__ double combine(double x, double y) {
+    if constexpr (is_max<OP>()) return fmax(x, y);
+    return x + y;
+}
+
+// grid (kRedBlocks, ncomp): component c reduces a + c*n, b + c*n
+template <RedOp OP>
+__global__ void __launch_bounds__(kRedThreads) k_reduce(const double* __restrict__ a,
+                                                        const double* __restrict__ b, long long n,
+                                                        double* __restrict__ partials) {
+    const int c = blockIdx.y;
+    const double* ac = a + (OP == RedOp::maxmag2 ? 0 : c * n);
+    const double* bc = b ? b + c * n : nullptr;
+    double acc = is_max<OP>() ? -1e300 : 0.0;
+    for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < n;
+         i += (long long)gridDim.x * kRedThreads)
+        acc = combine<OP>(acc, red_term<OP>(ac, bc, i, n));
+    __shared__ double sh[kRedThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) acc = combine<OP>(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = sh[0];
+        for (int w = 1; w < kRedThreads / 32; ++w) s = combine<OP>(s, sh[w]);
+        partials[c * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+// one block per component: ordered sum of nblocks partials
+template <bool MAX>
+__global__ void k_finalize(const double* __restrict__ partials, int nblocks,
+                           double* __restrict__ out) {
+    const int c = blockIdx.x;
+    double acc = MAX ? -1e300 : 0.0;
+    for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
+        double v = partials[c * nblocks + i];
+        acc = MAX ? fmax(acc, v) : acc + v;
+    }
+    __shared__ double sh[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        double v = __shfl_down_sync(0xffffffffu, acc, o);
+        acc = MAX ? fmax(acc, v) : acc + v;
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = sh[0];
+        for (int w = 1; w < (int)(blockDim.x / 32); ++w) s = MAX ? fmax(s, sh[w]) : s + sh[w];
+        out[c] = s;
+    }
+}
+
+template <RedOp OP>
+void reduce(vr_ctx* ctx, const double* a, const double* b, long long n, int ncomp,
+            double* host_out) {
+    const int nb = static_cast<int>(std::min<long long>(kRedBlocks, (n + kRedThreads - 1) / kRedThreads));
+    k_reduce<OP><<<dim3(nb, ncomp), kRedThreads, 0, ctx->stream>>>(a, b, n, ctx->red_partials);
+    check_launch();
+    k_finalize<is_max<OP>()><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nb, ctx->red_out);
+    check_launch();
+    count_launch(ctx, 2);
+    VR_CUDA(cudaMemcpyAsync(ctx->red_host, ctx->red_out, sizeof(double) * ncomp,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < ncomp; ++c) host_out[c] = ctx->red_host[c];
+}
+
+unsigned ew_grid(long long n) {
+    return static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148LL * 16));
+}
+
+}  // namespace
+
+void scale(vr_ctx* ctx, double* x, long long n, double a) {
+    k_scale<<<ew_grid(n), 256, 0, ctx->stream>>>(x, n, a);
+    check_launch();
+    count_launch(ctx);
+}
+void add_scaled(vr_ctx* ctx, double* y, double a, const double* x, long long n) {
+    k_add_scaled<<<ew_grid(n), 256, 0, ctx->stream>>>(y, a, x, n);
+    check_launch();
+    count_launch(ctx);
+}
+void lin_comb(vr_ctx* ctx, double* out, double a, const double* x, double b, const double* y,
+              long long n) {
+    k_lin_comb<<<ew_grid(n), 256, 0, ctx->stream>>>(out, a, x, b, y, n);
+    check_launch();
+    count_launch(ctx);
+}
+void affine(vr_ctx* ctx, const double* x, double* out, long long n, double lo, double s) {
+    k_affine<<<ew_grid(n), 256, 0, ctx->stream>>>(x, out, n, lo, s);
+    check_launch();
+    count_launch(ctx);
+}
+void dot_components(vr_ctx* ctx, const double* a, const double* b, long long n, int ncomp,
+                    double* results) {
+    reduce<RedOp::dot>(ctx, a, b, n, ncomp, results);
+}
+double max_abs(vr_ctx* ctx, const double* a, long long n) {
+    if (n == 0) return 0.0;
+    double r;
+    reduce<RedOp::maxabs>(ctx, a, nullptr, n, 1, &r);
+    return r;
+}
+double max_magnitude(vr_ctx* ctx, const double* v3, long long n) {
+    double r;
+    reduce<RedOp::maxmag2>(ctx, v3, nullptr, n, 1, &r);
+    return std::sqrt(r);
+}
+bool all_finite(vr_ctx* ctx, const double* a, long long n) {
+    double r;
+    reduce<RedOp::nonfinite>(ctx, a, nullptr, n, 1, &r);
+    return r == 0.0;
+}
+double sum_sq_diff(vr_ctx* ctx, const double* a, const double* b, long long n) {
+    double r;
+    reduce<RedOp::sumsq_diff>(ctx, a, b, n, 1, &r);
+    return r;
+}
+double min_value(vr_ctx* ctx, const double* a, long long n) {
+    double r;
+    reduce<RedOp::minval>(ctx, a, nullptr, n, 1, &r);
+    return -r;
+}
+double max_value(vr_ctx* ctx, const double* a, long long n) {
+    double r;
+    reduce<RedOp::maxval>(ctx, a, nullptr, n, 1, &r);
+    return r;
+}
+void finalize_sums(vr_ctx* ctx, int nblocks, int ncomp, double* host_out) {
+    k_finalize<false><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nblocks, ctx->red_out);
+    check_launch();
+    count_launch(ctx);
+    VR_CUDA(cudaMemcpyAsync(ctx->red_host, ctx->red_out, sizeof(double) * ncomp,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < ncomp; ++c) host_out[c] = ctx->red_host[c];
+}
+
+}  // namespace vr

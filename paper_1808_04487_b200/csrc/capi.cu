@@ -1,0 +1,818 @@
+// capi.cu -- extern "C" boundary (include/veloreg_gpu.h). Every entry point
+// catches vr::Error and maps it to the veloreg::ErrorCategory status code
+// (errors.hpp:9-17) plus a thread-local message, so a C++ adapter can rethrow
+// the reference's typed exception.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "objective.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_cls = VR_EXC_NONE;
+
+template <typename Fn>
+int guard(Fn&& fn) {
+    try {
+        fn();
+        return VR_OK;
+    } catch (const vr::Error& e) {
+        g_err = e.what();
+        g_cls = e.cls;
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("host allocation failed: ") + e.what();
+        g_cls = VR_EXC_RESOURCE;
+        return VR_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_cls = VR_EXC_LOGIC;
+        return VR_ERR_LOGIC;
+    }
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) vr::throw_argument(std::string(what) + ": null argument");
+}
+void set_dev(vr_ctx* ctx) {
+    need(ctx != nullptr, "context");
+    VR_CUDA(cudaSetDevice(ctx->device));
+}
+void check_ncomp(int ncomp) {
+    if (ncomp != 1 && ncomp != 3) vr::throw_argument("ncomp must be 1 or 3");
+}
+bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+}  // namespace
+
+namespace vr {
+
+double* spec_buf(vr_ctx* ctx, int i) {
+    if (static_cast<int>(ctx->spec_scratch.size()) <= i) ctx->spec_scratch.resize(i + 1, nullptr);
+    if (!ctx->spec_scratch[i]) {
+        void* p = nullptr;
+        VR_CUDA(cudaMalloc(&p, sizeof(double) * 2 * ctx->g.NC));
+        ctx->spec_scratch[i] = static_cast<double*>(p);
+    }
+    return ctx->spec_scratch[i];
+}
+double* field_buf(vr_ctx* ctx, int i) {
+    if (static_cast<int>(ctx->field_scratch.size()) <= i) ctx->field_scratch.resize(i + 1, nullptr);
+    if (!ctx->field_scratch[i]) {
+        void* p = nullptr;
+        VR_CUDA(cudaMalloc(&p, sizeof(double) * ctx->g.N));
+        ctx->field_scratch[i] = static_cast<double*>(p);
+    }
+    return ctx->field_scratch[i];
+}
+
+}  // namespace vr
+
+extern "C" {
+
+const char* vr_last_error(void) { return g_err.c_str(); }
+int vr_last_error_class(void) { return g_cls; }
+int vr_abi_version(void) { return VR_ABI_VERSION; }
+
+void vr_model_default(vr_model* m) {
+    m->norm.kind = VR_REG_H2;
+    m->norm.gamma = 1.0;
+    m->norm.helmholtz_squared = 1;
+    m->norm.div_penalty = 0;
+    m->norm.beta_w = 1e-4;
+    m->projection = VR_PROJ_IDENTITY;
+    m->beta_v = 1e-2;
+    m->nt = 4;
+    m->gauss_newton = 1;
+}
+void vr_solver_params_default(vr_solver_params* p) {
+    p->eps_opt = 5e-2;
+    p->abs_grad_tol = 1e-6;
+    p->max_newton = 50;
+    p->max_krylov = 100;
+    p->armijo_c1 = 1e-4;
+    p->armijo_backtrack = 0.5;
+    p->armijo_max_trials = 20;
+    p->squared_norm_stop = 1;
+}
+int vr_model_validate(const vr_model* m) {
+    return guard([&] {
+        need(m, "model");
+        vr::validate_model(*m);
+    });
+}
+int vr_solver_params_validate(const vr_solver_params* p) {
+    return guard([&] {
+        need(p, "params");
+        vr::validate_params(*p);
+    });
+}
+
+// ---- context -----------------------------------------------------------------
+int vr_ctx_create(int n1, int n2, int n3, int device, vr_ctx** out) {
+    return guard([&] {
+        need(out, "out");
+        const int d[3] = {n1, n2, n3};
+        for (int a = 0; a < 3; ++a)
+            if (d[a] < 4)
+                vr::throw_dimension("Grid3: every dimension must be >= 4, got " +
+                                    std::to_string(n1) + "x" + std::to_string(n2) + "x" +
+                                    std::to_string(n3));
+        for (int a = 0; a < 3; ++a)
+            if (!pow2(d[a]) || d[a] > 1024)
+                vr::throw_dimension("vr_ctx_create: GPU grids need power-of-two dims <= 1024, got " +
+                                    std::to_string(n1) + "x" + std::to_string(n2) + "x" +
+                                    std::to_string(n3));
+        int count = 0;
+        VR_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count)
+            vr::throw_resource("vr_ctx_create: no CUDA device " + std::to_string(device));
+        VR_CUDA(cudaSetDevice(device));
+        auto* ctx = new vr_ctx();
+        try {
+            ctx->device = device;
+            vr::GridDims& g = ctx->g;
+            g.n1 = n1;
+            g.n2 = n2;
+            g.n3 = n3;
+            g.nh = n3 / 2 + 1;
+            g.N = static_cast<long long>(n1) * n2 * n3;
+            g.NC = static_cast<long long>(n1) * n2 * g.nh;
+            g.h1 = vr::kTwoPi / n1;
+            g.h2 = vr::kTwoPi / n2;
+            g.h3 = vr::kTwoPi / n3;
+            VR_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            // keep freed blocks cached in the stream-ordered pool (no OS round trips)
+            cudaMemPool_t pool;
+            VR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t thr = UINT64_MAX;
+            VR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+            vr::fft_plan_create(ctx);
+            VR_CUDA(cudaMalloc(&ctx->red_partials, sizeof(double) * vr::kRedBlocks * 8));
+            VR_CUDA(cudaMalloc(&ctx->red_out, sizeof(double) * 8));
+            VR_CUDA(cudaMallocHost(&ctx->red_host, sizeof(double) * 8));
+            VR_CUDA(cudaMalloc(&ctx->flag_dev, sizeof(int) * 4));
+            VR_CUDA(cudaMallocHost(&ctx->flag_host, sizeof(int) * 4));
+        } catch (...) {
+            vr_ctx_destroy(ctx);
+            throw;
+        }
+        *out = ctx;
+    });
+}
+
+int vr_ctx_destroy(vr_ctx* ctx) {
+    if (!ctx) return VR_OK;
+    return guard([&] {
+        cudaSetDevice(ctx->device);
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        vr::fft_plan_destroy(ctx);
+        for (double* p : ctx->spec_scratch) cudaFree(p);
+        for (double* p : ctx->field_scratch) cudaFree(p);
+        cudaFree(ctx->red_partials);
+        cudaFree(ctx->red_out);
+        cudaFreeHost(ctx->red_host);
+        cudaFree(ctx->flag_dev);
+        cudaFreeHost(ctx->flag_host);
+        if (ctx->stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+int vr_ctx_synchronize(vr_ctx* ctx) {
+    return guard([&] {
+        set_dev(ctx);
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+void* vr_ctx_stream(vr_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+int vr_ctx_grid(const vr_ctx* ctx, int dims[3]) {
+    return guard([&] {
+        need(ctx && dims, "vr_ctx_grid");
+        dims[0] = ctx->g.n1;
+        dims[1] = ctx->g.n2;
+        dims[2] = ctx->g.n3;
+    });
+}
+long long vr_ctx_kernel_launches(const vr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void vr_ctx_reset_kernel_launches(vr_ctx* ctx) {
+    if (ctx) ctx->launches = 0;
+}
+
+// ---- memory -------------------------------------------------------------------
+int vr_device_alloc(vr_ctx* ctx, size_t bytes, void** out) {
+    return guard([&] {
+        set_dev(ctx);
+        need(out, "out");
+        VR_CUDA(cudaMalloc(out, bytes));
+    });
+}
+int vr_device_free(vr_ctx* ctx, void* p) {
+    return guard([&] {
+        set_dev(ctx);
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        VR_CUDA(cudaFree(p));
+    });
+}
+int vr_host_alloc_pinned(size_t bytes, void** out) {
+    return guard([&] {
+        need(out, "out");
+        VR_CUDA(cudaMallocHost(out, bytes));
+    });
+}
+int vr_host_free_pinned(void* p) { return guard([&] { VR_CUDA(cudaFreeHost(p)); }); }
+int vr_memcpy_h2d(vr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guard([&] {
+        set_dev(ctx);
+        VR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    });
+}
+int vr_memcpy_d2h(vr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guard([&] {
+        set_dev(ctx);
+        VR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int vr_memcpy_d2d(vr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guard([&] {
+        set_dev(ctx);
+        VR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    });
+}
+int vr_memset_zero(vr_ctx* ctx, void* dst, size_t bytes) {
+    return guard([&] {
+        set_dev(ctx);
+        VR_CUDA(cudaMemsetAsync(dst, 0, bytes, ctx->stream));
+    });
+}
+
+// ---- BLAS-1 ---------------------------------------------------------------------
+int vr_scale(vr_ctx* ctx, double* x, int ncomp, double a) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        vr::scale(ctx, x, ncomp * ctx->g.N, a);
+    });
+}
+int vr_add_scaled(vr_ctx* ctx, double* y, double a, const double* x, int ncomp) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        vr::add_scaled(ctx, y, a, x, ncomp * ctx->g.N);
+    });
+}
+int vr_lin_comb(vr_ctx* ctx, double* out, double a, const double* x, double b, const double* y,
+                int ncomp) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        vr::lin_comb(ctx, out, a, x, b, y, ncomp * ctx->g.N);
+    });
+}
+int vr_dot_l2(vr_ctx* ctx, const double* a, const double* b, int ncomp, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        double r[3];
+        vr::dot_components(ctx, a, b, ctx->g.N, ncomp, r);
+        double s = 0.0;
+        for (int c = 0; c < ncomp; ++c) s += r[c];
+        *out = s;
+    });
+}
+int vr_norm_l2(vr_ctx* ctx, const double* a, int ncomp, double* out) {
+    double d = 0.0;
+    int st = vr_dot_l2(ctx, a, a, ncomp, &d);
+    if (st == VR_OK) *out = std::sqrt(d);
+    return st;
+}
+int vr_max_abs(vr_ctx* ctx, const double* a, int ncomp, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        *out = vr::max_abs(ctx, a, ncomp * ctx->g.N);
+    });
+}
+int vr_max_magnitude(vr_ctx* ctx, const double* v3, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        *out = vr::max_magnitude(ctx, v3, ctx->g.N);
+    });
+}
+int vr_all_finite(vr_ctx* ctx, const double* a, int ncomp, int* out) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        *out = vr::all_finite(ctx, a, ncomp * ctx->g.N) ? 1 : 0;
+    });
+}
+int vr_inner_product(vr_ctx* ctx, const double* a, const double* b, int ncomp, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        *out = ncomp == 3 ? vr::inner_product_vec(ctx, a, b) : vr::inner_product_scalar(ctx, a, b);
+    });
+}
+
+// ---- spectral -------------------------------------------------------------------
+int vr_fft_r2c(vr_ctx* ctx, const double* in, double* out_spectrum) {
+    return guard([&] {
+        set_dev(ctx);
+        vr::fft_r2c(ctx, in, out_spectrum);
+    });
+}
+int vr_fft_c2r(vr_ctx* ctx, const double* spectrum, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        double* s = vr::spec_buf(ctx, 0);
+        VR_CUDA(cudaMemcpyAsync(s, spectrum, sizeof(double) * 2 * ctx->g.NC,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+        vr::fft_c2r(ctx, s, out, 1.0 / static_cast<double>(ctx->g.N), nullptr);
+    });
+}
+int vr_gradient(vr_ctx* ctx, const double* f, double* out3) {
+    return guard([&] {
+        set_dev(ctx);
+        vr::op_gradient(ctx, f, out3);
+    });
+}
+int vr_divergence(vr_ctx* ctx, const double* v3, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        vr::op_divergence(ctx, v3, out);
+    });
+}
+int vr_laplacian(vr_ctx* ctx, const double* f, double* out, int ncomp) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        vr::MultParams mp;
+        mp.kind = vr::Mult::laplacian;
+        for (int c = 0; c < ncomp; ++c)
+            vr::spectral_scalar_op(ctx, f + c * ctx->g.N, out + c * ctx->g.N, mp);
+    });
+}
+int vr_helmholtz1_apply(vr_ctx* ctx, const double* f, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        vr::MultParams mp;
+        mp.kind = vr::Mult::helmholtz1;
+        vr::spectral_scalar_op(ctx, f, out, mp);
+    });
+}
+int vr_gaussian_smooth(vr_ctx* ctx, const double* f, double* out, int ncomp,
+                       const double sigma[3]) {
+    return guard([&] {
+        set_dev(ctx);
+        check_ncomp(ncomp);
+        need(sigma, "sigma");
+        for (int a = 0; a < 3; ++a)
+            if (sigma[a] < 0.0) vr::throw_argument("gaussian_smooth: sigma must be >= 0");
+        vr::MultParams mp;
+        mp.kind = vr::Mult::gaussian;
+        const double h[3] = {ctx->g.h1, ctx->g.h2, ctx->g.h3};
+        for (int a = 0; a < 3; ++a) mp.sig2h2[a] = sigma[a] * sigma[a] * h[a] * h[a];
+        for (int c = 0; c < ncomp; ++c)
+            vr::spectral_scalar_op(ctx, f + c * ctx->g.N, out + c * ctx->g.N, mp);
+    });
+}
+int vr_apply_reg_operator(vr_ctx* ctx, const double* v3, double* out3, const vr_regnorm* norm,
+                          int mode, double beta) {
+    return guard([&] {
+        set_dev(ctx);
+        need(norm, "norm");
+        vr_model m;
+        vr_model_default(&m);
+        m.norm = *norm;
+        vr::validate_model(m);
+        if (beta <= 0.0) vr::throw_argument("apply_reg_operator: beta must be > 0");
+        if (mode < VR_REGOP_APPLY || mode > VR_REGOP_INVERSE_SQRT)
+            vr::throw_argument("apply_reg_operator: unknown mode");
+        vr::op_reg(ctx, v3, out3, *norm, mode, beta);
+    });
+}
+int vr_apply_projection(vr_ctx* ctx, const double* f3, double* out3, int kind, double beta_v,
+                        double beta_w) {
+    return guard([&] {
+        set_dev(ctx);
+        vr::op_projection(ctx, f3, out3, kind, beta_v, beta_w);
+    });
+}
+int vr_rescale_intensity(vr_ctx* ctx, const double* f, double* out, int* degenerate) {
+    return guard([&] {
+        set_dev(ctx);
+        const long long N = ctx->g.N;
+        const double lo = vr::min_value(ctx, f, N), hi = vr::max_value(ctx, f, N);
+        if (hi <= lo) {
+            VR_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * N, ctx->stream));
+            if (degenerate) *degenerate = 1;
+            return;
+        }
+        vr::affine(ctx, f, out, N, lo, 1.0 / (hi - lo));
+        if (degenerate) *degenerate = 0;
+    });
+}
+
+// ---- transport -------------------------------------------------------------------
+int vr_tricubic_interpolate(vr_ctx* ctx, const double* f, const double* pts3, double* out,
+                            int nfields) {
+    return guard([&] {
+        set_dev(ctx);
+        vr::sl_tricubic(ctx, f, nfields, pts3, out);
+    });
+}
+int vr_trace_characteristics(vr_ctx* ctx, const double* v3, int nt, int direction,
+                             double* dep3) {
+    return guard([&] {
+        set_dev(ctx);
+        if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
+        if (!vr::all_finite(ctx, v3, 3 * ctx->g.N))
+            vr::throw_numeric("trace_characteristics: velocity has non-finite values");
+        vr::sl_trace(ctx, v3, nt, direction, dep3);
+    });
+}
+int vr_continuity_factor(vr_ctx* ctx, const double* div_v, const double* dep3, double dt,
+                         double* factor) {
+    return guard([&] {
+        set_dev(ctx);
+        vr::sl_factor(ctx, div_v, dep3, 0.5 * dt, factor);
+    });
+}
+int vr_solve_state(vr_ctx* ctx, const double* m_T, const double* v3, int nt, double* history) {
+    return guard([&] {
+        set_dev(ctx);
+        const long long N = ctx->g.N;
+        if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
+        if (!vr::all_finite(ctx, v3, 3 * N))
+            vr::throw_numeric("trace_characteristics: velocity has non-finite values");
+        double* xb = vr::dev_alloc(ctx, 3 * N);
+        vr::sl_trace(ctx, v3, nt, VR_TRACE_BACKWARD, xb);
+        VR_CUDA(cudaMemcpyAsync(history, m_T, sizeof(double) * N, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        for (int j = 0; j < nt; ++j) vr::sl_advect(ctx, history + j * N, xb, history + (j + 1) * N);
+        vr::dev_free(ctx, xb);
+    });
+}
+static void adjoint_like(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
+                         double* history, double* initial) {
+    const long long N = ctx->g.N;
+    if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
+    if (!vr::all_finite(ctx, v3, 3 * N))
+        vr::throw_numeric("trace_characteristics: velocity has non-finite values");
+    double* xf = vr::dev_alloc(ctx, 3 * N);
+    double* factor = vr::dev_alloc(ctx, N);
+    double* work = vr::dev_alloc(ctx, 2 * N);
+    vr::sl_trace(ctx, v3, nt, VR_TRACE_FORWARD, xf);
+    double* div = vr::field_buf(ctx, 0);
+    vr::op_divergence(ctx, v3, div);
+    vr::sl_factor(ctx, div, xf, 0.5 / nt, factor);
+    const double* cur = terminal;
+    if (history)
+        VR_CUDA(cudaMemcpyAsync(history + nt * N, terminal, sizeof(double) * N,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    int pp = 0;
+    for (int j = nt - 1; j >= 0; --j) {
+        double* dst = history ? history + j * N : work + pp * N;
+        vr::sl_continuity(ctx, cur, xf, factor, dst);
+        cur = dst;
+        pp ^= 1;
+    }
+    if (initial)
+        VR_CUDA(cudaMemcpyAsync(initial, cur, sizeof(double) * N, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    vr::dev_free(ctx, xf);
+    vr::dev_free(ctx, factor);
+    vr::dev_free(ctx, work);
+}
+int vr_solve_adjoint(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
+                     double* history, double* initial) {
+    return guard([&] {
+        set_dev(ctx);
+        adjoint_like(ctx, terminal, v3, nt, history, initial);
+    });
+}
+int vr_solve_inc_adjoint(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
+                         double* history, double* initial) {
+    return guard([&] {
+        set_dev(ctx);
+        adjoint_like(ctx, terminal, v3, nt, history, initial);
+    });
+}
+int vr_gradient_dot(vr_ctx* ctx, const double* f, const double* w3, double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        double* gm = vr::dev_alloc(ctx, 3 * ctx->g.N);
+        vr::op_gradient(ctx, f, gm);
+        vr::sl_gradient_dot(ctx, gm, w3, out);
+        vr::dev_free(ctx, gm);
+    });
+}
+int vr_solve_inc_state(vr_ctx* ctx, const double* m_history, const double* v3, const double* vt3,
+                       int nt, double* mt_history) {
+    // step-by-step restatement of transport.cpp:150-173 (the fused matvec path
+    // lives in objective.cu; this entry point returns the whole mt history)
+    return guard([&] {
+        set_dev(ctx);
+        const long long N = ctx->g.N;
+        if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
+        double* xb = vr::dev_alloc(ctx, 3 * N);
+        double* gm = vr::dev_alloc(ctx, 3 * N);
+        double* q = vr::dev_alloc(ctx, 2 * N);
+        double* tmp = vr::dev_alloc(ctx, N);
+        vr::sl_trace(ctx, v3, nt, VR_TRACE_BACKWARD, xb);
+        const double hdt = 0.5 / nt;
+        double* qp = q;
+        double* qn = q + N;
+        vr::op_gradient(ctx, m_history, gm);
+        vr::sl_gradient_dot(ctx, gm, vt3, qp);
+        VR_CUDA(cudaMemsetAsync(mt_history, 0, sizeof(double) * N, ctx->stream));
+        for (int j = 0; j < nt; ++j) {
+            vr::op_gradient(ctx, m_history + (j + 1) * N, gm);
+            vr::sl_gradient_dot(ctx, gm, vt3, qn);
+            vr::lin_comb(ctx, tmp, 1.0, mt_history + j * N, -hdt, qp, N);
+            vr::sl_advect(ctx, tmp, xb, mt_history + (j + 1) * N);
+            vr::add_scaled(ctx, mt_history + (j + 1) * N, -hdt, qn, N);
+            std::swap(qp, qn);
+        }
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        vr::dev_free(ctx, xb);
+        vr::dev_free(ctx, gm);
+        vr::dev_free(ctx, q);
+        vr::dev_free(ctx, tmp);
+    });
+}
+
+// ---- objective -------------------------------------------------------------------
+int vr_objective_create(vr_ctx* ctx, const double* m_R, const double* m_T, const vr_model* model,
+                        vr_objective** out) {
+    return guard([&] {
+        set_dev(ctx);
+        need(m_R && m_T && model && out, "vr_objective_create");
+        *out = vr::objective_create(ctx, m_R, m_T, *model);
+    });
+}
+int vr_objective_destroy(vr_objective* obj) {
+    return guard([&] {
+        if (obj) {
+            cudaSetDevice(obj->ctx->device);
+            delete obj;
+        }
+    });
+}
+int vr_objective_initial_mismatch(const vr_objective* obj, double* out) {
+    return guard([&] {
+        need(obj && out, "vr_objective_initial_mismatch");
+        *out = obj->initial_mismatch;
+    });
+}
+int vr_objective_counters(const vr_objective* obj, vr_counters* out) {
+    return guard([&] {
+        need(obj && out, "vr_objective_counters");
+        *out = obj->counters;
+    });
+}
+int vr_objective_reset_counters(vr_objective* obj) {
+    return guard([&] {
+        need(obj, "vr_objective_reset_counters");
+        obj->counters = vr_counters{};
+    });
+}
+int vr_objective_set_beta(vr_objective* obj, double beta_v) {
+    return guard([&] {
+        need(obj, "vr_objective_set_beta");
+        if (beta_v <= 0.0) vr::throw_argument("RegModel: beta_v must be > 0");
+        obj->model.beta_v = beta_v;
+    });
+}
+int vr_evaluate(vr_objective* obj, const double* v3, vr_state** out_state) {
+    return guard([&] {
+        need(obj && v3 && out_state, "vr_evaluate");
+        set_dev(obj->ctx);
+        *out_state = vr::objective_evaluate(obj, v3);
+    });
+}
+int vr_state_destroy(vr_state* s) {
+    return guard([&] {
+        if (s) {
+            cudaSetDevice(s->obj->ctx->device);
+            delete s;
+        }
+    });
+}
+int vr_state_scalars(const vr_state* s, double* objective, double* mismatch, double* mismatch_rel,
+                     int* has_gradient, int* has_adjoint_ctx) {
+    return guard([&] {
+        need(s, "vr_state_scalars");
+        if (objective) *objective = s->objective;
+        if (mismatch) *mismatch = s->mismatch;
+        if (mismatch_rel) *mismatch_rel = s->mismatch_rel;
+        if (has_gradient) *has_gradient = s->has_gradient;
+        if (has_adjoint_ctx) *has_adjoint_ctx = s->has_adjoint_ctx;
+    });
+}
+int vr_state_get(const vr_state* s, int which, double* out) {
+    return guard([&] {
+        need(s && out, "vr_state_get");
+        vr_ctx* ctx = s->obj->ctx;
+        set_dev(ctx);
+        const long long N = ctx->g.N;
+        const double* src = nullptr;
+        long long n = 0;
+        switch (which) {
+            case VR_STATE_V: src = s->v; n = 3 * N; break;
+            case VR_STATE_X_BWD: src = s->xb; n = 3 * N; break;
+            case VR_STATE_X_FWD: src = s->xf; n = 3 * N; break;
+            case VR_STATE_FACTOR: src = s->factor; n = N; break;
+            case VR_STATE_M_HISTORY: src = s->mhist; n = (s->nt + 1) * N; break;
+            case VR_STATE_GRADIENT: src = s->has_gradient ? s->grad : nullptr; n = 3 * N; break;
+            case VR_STATE_GRAD_M: src = s->gradm; n = 3LL * (s->nt + 1) * N; break;
+            default: vr::throw_argument("vr_state_get: unknown field");
+        }
+        if (!src) vr::throw_logic("vr_state_get: field not computed yet");
+        VR_CUDA(cudaMemcpyAsync(out, src, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    });
+}
+int vr_compute_gradient(vr_objective* obj, vr_state* s, double* g3) {
+    return guard([&] {
+        need(obj && s, "vr_compute_gradient");
+        set_dev(obj->ctx);
+        vr::objective_gradient(obj, s);
+        if (g3)
+            VR_CUDA(cudaMemcpyAsync(g3, s->grad, sizeof(double) * 3 * obj->ctx->g.N,
+                                    cudaMemcpyDeviceToDevice, obj->ctx->stream));
+    });
+}
+int vr_hessian_matvec(vr_objective* obj, const vr_state* s, const double* vt3, double* out3) {
+    return guard([&] {
+        need(obj && s && vt3 && out3, "vr_hessian_matvec");
+        set_dev(obj->ctx);
+        vr::objective_matvec(obj, s, vt3, out3, true);
+    });
+}
+int vr_hessian_data_matvec(vr_objective* obj, const vr_state* s, const double* vt3, double* out3) {
+    return guard([&] {
+        need(obj && s && vt3 && out3, "vr_hessian_data_matvec");
+        set_dev(obj->ctx);
+        vr::objective_matvec(obj, s, vt3, out3, false);
+    });
+}
+int vr_hessian_matvec_host(vr_objective* obj, const vr_state* s, const double* vt3_host,
+                           double* out3_host) {
+    return guard([&] {
+        need(obj && s && vt3_host && out3_host, "vr_hessian_matvec_host");
+        vr_ctx* ctx = obj->ctx;
+        set_dev(ctx);
+        const size_t bytes = sizeof(double) * 3 * ctx->g.N;
+        double* vt = vr::dev_alloc(ctx, 3 * ctx->g.N);
+        double* out = vr::dev_alloc(ctx, 3 * ctx->g.N);
+        try {
+            VR_CUDA(cudaMemcpyAsync(vt, vt3_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+            vr::objective_matvec(obj, s, vt, out, true);
+            VR_CUDA(cudaMemcpyAsync(out3_host, out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            vr::dev_free(ctx, vt);
+            vr::dev_free(ctx, out);
+            throw;
+        }
+        vr::dev_free(ctx, vt);
+        vr::dev_free(ctx, out);
+    });
+}
+int vr_objective_apply_reg(vr_objective* obj, const double* u3, int mode, double* out3) {
+    return guard([&] {
+        need(obj && u3 && out3, "vr_objective_apply_reg");
+        set_dev(obj->ctx);
+        vr::objective_apply_reg(obj, u3, mode, out3);
+    });
+}
+int vr_objective_apply_K(vr_objective* obj, const double* u3, double* out3) {
+    return guard([&] {
+        need(obj && u3 && out3, "vr_objective_apply_K");
+        set_dev(obj->ctx);
+        vr::objective_apply_K(obj, u3, out3);
+    });
+}
+
+// ---- solvers ----------------------------------------------------------------------
+int vr_compute_forcing(double grad_norm, double grad0_norm, double* out) {
+    return guard([&] {
+        if (grad0_norm <= 0.0)
+            vr::throw_logic("compute_forcing: |g_0| = 0, the solver should have terminated");
+        *out = std::min(0.5, std::sqrt(grad_norm / grad0_norm));
+    });
+}
+int vr_pcg_solve(vr_objective* obj, const vr_state* s, const double* rhs3, double rel_tol,
+                 int max_iter, int precond, double* x3, vr_pcg_stats* stats) {
+    return guard([&] {
+        need(obj && s && rhs3 && x3 && stats, "vr_pcg_solve");
+        vr_ctx* ctx = obj->ctx;
+        set_dev(ctx);
+        const long long n3 = 3 * ctx->g.N;
+        vr::DevOp op = [&](const double* u, double* out) {
+            vr::objective_matvec(obj, s, u, out, true);
+        };
+        vr::DevOp pc = [&](const double* r, double* z) {
+            if (precond == VR_PRECOND_SPECTRAL)
+                vr::objective_apply_reg(obj, r, VR_REGOP_INVERSE, z);
+            else
+                VR_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * n3, cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+        };
+        *stats = vr::pcg_solve(ctx, op, rhs3, rel_tol, max_iter, pc, x3);
+    });
+}
+static void copy_records(const vr::GnResult& r, vr_iteration_record* recs, int max_recs,
+                         int offset) {
+    if (!recs) return;
+    for (size_t i = 0; i < r.records.size(); ++i) {
+        const int slot = offset + static_cast<int>(i);
+        if (slot >= max_recs) break;
+        recs[slot] = r.records[i];
+    }
+}
+int vr_gauss_newton_solve(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                          const vr_model* model, const vr_solver_params* params, int precond,
+                          double* v_out, vr_solve_report* report, vr_iteration_record* records,
+                          int max_records) {
+    return guard([&] {
+        set_dev(ctx);
+        need(m_R && m_T && v0 && model && params && v_out && report, "vr_gauss_newton_solve");
+        vr::GnResult r = vr::gauss_newton_solve(ctx, m_R, m_T, v0, *model, *params, precond, v_out);
+        *report = r.report;
+        copy_records(r, records, max_records, 0);
+    });
+}
+int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                              const vr_model* model, const vr_solver_params* params, int precond,
+                              double* v_out, vr_solve_report* reports, int max_levels,
+                              int* n_levels, vr_iteration_record* records, int max_records) {
+    return guard([&] {
+        set_dev(ctx);
+        need(m_R && m_T && v0 && model && params && v_out && n_levels, "vr_parameter_continuation");
+        if (!(model->beta_v <= 1.0))
+            vr::throw_argument("parameter continuation: target beta_v > 1");
+        std::vector<double> levels;
+        for (int i = 0;; ++i) {
+            const double b = std::pow(10.0, -i);
+            if (b <= model->beta_v * (1.0 + 1e-9)) break;
+            levels.push_back(b);
+        }
+        levels.push_back(model->beta_v);
+        const long long n3 = 3 * ctx->g.N;
+        double* v = vr::dev_alloc(ctx, n3);
+        VR_CUDA(cudaMemcpyAsync(v, v0, sizeof(double) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+        int off = 0;
+        *n_levels = 0;
+        try {
+            for (size_t l = 0; l < levels.size(); ++l) {
+                vr_model m = *model;
+                m.beta_v = levels[l];
+                vr::GnResult r = vr::gauss_newton_solve(ctx, m_R, m_T, v, m, *params, precond, v);
+                if (reports && static_cast<int>(l) < max_levels) reports[l] = r.report;
+                copy_records(r, records, max_records, off);
+                off += static_cast<int>(r.records.size());
+                *n_levels = static_cast<int>(l) + 1;
+                if (r.report.stop == VR_STOP_LINE_SEARCH_FAILURE) break;
+            }
+            VR_CUDA(cudaMemcpyAsync(v_out, v, sizeof(double) * n3, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+            VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            vr::dev_free(ctx, v);
+            throw;
+        }
+        vr::dev_free(ctx, v);
+    });
+}
+
+int vr_generate_synthetic(vr_ctx* ctx, int nt, double amplitude, double* m_R, double* m_T,
+                          double* v_star) {
+    return guard([&] {
+        set_dev(ctx);
+        need(m_R && m_T && v_star, "vr_generate_synthetic");
+        const long long N = ctx->g.N;
+        vr::synth_fill(ctx, amplitude, m_T, v_star);
+        double* xb = vr::dev_alloc(ctx, 3 * N);
+        double* a = vr::dev_alloc(ctx, N);
+        double* b = vr::dev_alloc(ctx, N);
+        vr::sl_trace(ctx, v_star, nt, VR_TRACE_BACKWARD, xb);
+        const double* cur = m_T;
+        double* bufs[2] = {a, b};
+        for (int j = 0; j < nt; ++j) {
+            double* dst = (j + 1 == nt) ? m_R : bufs[j & 1];
+            vr::sl_advect(ctx, cur, xb, dst);
+            cur = dst;
+        }
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        vr::dev_free(ctx, xb);
+        vr::dev_free(ctx, a);
+        vr::dev_free(ctx, b);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,767 @@
+// fft.cu -- hand-written fp64 3D r2c/c2r FFTs for power-of-two periodic grids,
+// fused with the spectral multipliers of the reference's spectral module.
+//
+// Replaces proj/src/fft.cpp (FFTW r2c/c2r 3D, forward unnormalized, inverse
+// scaled by 1/N after the c2r, fft.cpp:66-115) and the serial bin loops of
+// proj/src/spectral.cpp:13-214 (gradient, divergence, laplacian, (-lap+1),
+// beta*A^{1,-1,-1/2}, Leray / near-incompressible K, Gaussian).
+//
+// Decomposition (all passes HBM-streaming, each CTA owns whole 1D lines):
+//   x3 (contiguous):  k_r2c_rows / k_c2r_rows. A real row of n3 is packed as
+//                     n3/2 complex values, transformed in shared memory and
+//                     split/merged into the n3/2+1 half-spectrum bins.
+//   x2, x1 (strided): k_fft_axis. A CTA loads TB adjacent columns (coalesced
+//                     along the contiguous index) straight into registers,
+//                     runs a Stockham radix-16 FFT with shared-memory exchanges,
+//                     and stores straight back. The x1 pass optionally runs
+//                     forward -> multiplier -> inverse in one kernel, so a
+//                     scalar spectral operator costs 5 passes instead of 6.
+// In-register butterflies are radix-2 DIT networks of size <= 16 with
+// literal twiddles; inter-stage twiddles come from per-axis long-double
+// tables (exactly rounded), so the transform error is O(eps log n).
+#include <cmath>
+
+#include "vr_common.cuh"
+
+namespace vr {
+
+struct FftPlan {
+    double2* tw1 = nullptr;   // exp(2 pi i k / n1), k < n1 (cos, sin)
+    double2* tw2 = nullptr;   // n2
+    double2* tw3h = nullptr;  // n3 / 2
+    double2* tw3 = nullptr;   // n3
+};
+
+namespace {
+
+// --------------------------------------------------------------------------
+// complex helpers
+// --------------------------------------------------------------------------
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+constexpr int bitrev_c(int i, int r) {
+    int out = 0;
+    for (int b = 1; b < r; b <<= 1) {
+        out = (out << 1) | (i & 1);
+        i >>= 1;
+    }
+    return out;
+}
+
+// exp(DIR * 2 pi i k / 16), k in [0, 8)
+template <int DIR>
+__device__ __forceinline__ double2 w16(int k) {
+    constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173,
+                     R2 = 0.70710678118654752440;
+    const double c[8] = {1.0, C1, R2, S1, 0.0, -S1, -R2, -C1};
+    const double s[8] = {0.0, S1, R2, C1, 1.0, C1, R2, S1};
+    return make_double2(c[k], DIR * s[k]);
+}
+
+// In-register DFT of size R (<= 16): X[k] = sum_n x[n] exp(DIR 2 pi i n k / R)
+template <int R, int DIR>
+__device__ __forceinline__ void dft_reg(double2* x) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int j = bitrev_c(i, R);
+        if (j > i) {
+            double2 t = x[i];
+            x[i] = x[j];
+            x[j] = t;
+        }
+    }
+#pragma unroll
+    for (int len = 2; len <= R; len <<= 1) {
+#pragma unroll
+        for (int start = 0; start < R; start += len) {
+#pragma unroll
+            for (int k = 0; k < len / 2; ++k) {
+                const int widx = k * (16 / len);
+                double2 b = x[start + k + len / 2];
+                double2 t;
+                if (widx == 0) {
+                    t = b;
+                } else if (widx == 4) {
+                    t = make_double2(-DIR * b.y, DIR * b.x);  // b * (DIR i)
+                } else {
+                    t = cmul(b, w16<DIR>(widx));
+                }
+                const double2 a = x[start + k];
+                x[start + k] = cadd(a, t);
+                x[start + k + len / 2] = csub(a, t);
+            }
+        }
+    }
+}
+
+__host__ __device__ constexpr int rmax_of(int n) { return n < 16 ? n : 16; }
+
+// One Stockham stage of radix R for a length-N transform with Ns = product of
+// previous radices; this thread handles butterflies j = t + b*T, b < RMAX/R.
+// SRC(i) reads element i, DST(i, v) writes element i. Caller handles syncs.
+template <int N, int R, int DIR, class Src, class Dst>
+__device__ __forceinline__ void stockham_stage(int Ns, int t, const double2* __restrict__ tw,
+                                               Src src, Dst dst, bool sync_between) {
+    constexpr int RMAX = rmax_of(N);
+    constexpr int T = N / RMAX;
+    constexpr int NB = RMAX / R;
+    double2 x[RMAX];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int j = t + b * T;
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[b * R + r] = src(j + r * (N / R));
+    }
+    if (sync_between) __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int j = t + b * T;
+        const int k = j & (Ns - 1);
+        if (Ns > 1) {
+            const int step = N / (Ns * R);
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                double2 w = __ldg(tw + r * k * step);
+                if (DIR < 0) w.y = -w.y;
+                x[b * R + r] = cmul(x[b * R + r], w);
+            }
+        }
+        dft_reg<R, DIR>(x + b * R);
+        const int out = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst(out + r * Ns, x[b * R + r]);
+    }
+}
+
+// Full length-N transform. The first stage reads LOAD(i), the last writes
+// STORE(i, v); intermediate stages exchange through shared memory via SM(i)
+// (a reference to this column's element i). SRC_SM / DST_SM say whether LOAD /
+// STORE alias that shared buffer, which decides where barriers are needed.
+// Must be called by all threads of the CTA (barriers inside).
+template <int N, int DIR, bool SRC_SM, bool DST_SM, class Load, class Store, class Sm>
+__device__ __forceinline__ void fft_line(int t, const double2* __restrict__ tw, Load load,
+                                         Store store, Sm sm) {
+    auto sm_src = [&](int i) { return sm(i); };
+    auto sm_dst = [&](int i, double2 v) { sm(i) = v; };
+    int Ns = 1;
+    bool first = true;
+    while (Ns < N) {
+        const int rem = N / Ns;
+        const bool last = rem <= 16;
+        const int R = rem >= 16 ? 16 : rem;
+        const bool reads_sm = !first || SRC_SM;
+        const bool writes_sm = !last || DST_SM;
+        const bool sync_between = reads_sm && writes_sm;
+        // R is uniform across the CTA; dispatch to compile-time radices
+#define VR_STAGE(RR)                                                                           \
+    if (R == RR) {                                                                             \
+        if (first && last)                                                                     \
+            stockham_stage<N, RR, DIR>(Ns, t, tw, load, store, sync_between);                  \
+        else if (first)                                                                        \
+            stockham_stage<N, RR, DIR>(Ns, t, tw, load, sm_dst, sync_between);                 \
+        else if (last)                                                                         \
+            stockham_stage<N, RR, DIR>(Ns, t, tw, sm_src, store, sync_between);                \
+        else                                                                                   \
+            stockham_stage<N, RR, DIR>(Ns, t, tw, sm_src, sm_dst, sync_between);               \
+    }
+        if constexpr (N >= 16) { VR_STAGE(16) }
+        if constexpr (N >= 8) { VR_STAGE(8) }
+        if constexpr (N >= 4) { VR_STAGE(4) }
+        VR_STAGE(2)
+#undef VR_STAGE
+        if (!last) __syncthreads();
+        first = false;
+        Ns *= R;
+    }
+}
+
+// --------------------------------------------------------------------------
+// spectral multipliers (spectral.cpp:23-39, 84-184)
+// --------------------------------------------------------------------------
+struct MultDev {
+    int kind;
+    int reg_kind, reg_mode, helm_sq;
+    double gamma, beta;
+    double sig2h2[3];
+};
+
+__device__ __forceinline__ double symbol_dev(const MultDev& m, double k2) {
+    switch (m.reg_kind) {
+        case VR_REG_H1: return k2;
+        case VR_REG_H2: return k2 * k2;
+        case VR_REG_H3: return k2 * k2 * k2;
+        default: {
+            double s = k2 + m.gamma;
+            return m.helm_sq ? s * s : s;
+        }
+    }
+}
+
+// returns the complex multiplier at bin (i1, i2, i3)
+__device__ __forceinline__ double2 mult_at(const MultDev& m, const GridDims& g, int i1, int i2,
+                                           int i3) {
+    switch (m.kind) {
+        case static_cast<int>(Mult::deriv0): return make_double2(0.0, (double)deriv_freq(i1, g.n1));
+        case static_cast<int>(Mult::deriv1): return make_double2(0.0, (double)deriv_freq(i2, g.n2));
+        case static_cast<int>(Mult::deriv2): return make_double2(0.0, (double)deriv_freq(i3, g.n3));
+        default: break;
+    }
+    const double a = fft_freq(i1, g.n1), b = fft_freq(i2, g.n2), c = fft_freq(i3, g.n3);
+    const double k2 = a * a + b * b + c * c;
+    double v = 1.0;
+    switch (m.kind) {
+        case static_cast<int>(Mult::laplacian): v = -k2; break;
+        case static_cast<int>(Mult::helmholtz1): v = k2 + 1.0; break;
+        case static_cast<int>(Mult::reg): {
+            const double s = symbol_dev(m, k2);
+            if (m.reg_mode == VR_REGOP_APPLY)
+                v = m.beta * s;
+            else if (m.reg_mode == VR_REGOP_INVERSE)
+                v = 1.0 / (m.beta * (s == 0.0 ? 1.0 : s));
+            else
+                v = 1.0 / sqrt(m.beta * (s == 0.0 ? 1.0 : s));
+            break;
+        }
+        case static_cast<int>(Mult::gaussian): {
+            const double e = m.sig2h2[0] * a * a + m.sig2h2[1] * b * b + m.sig2h2[2] * c * c;
+            v = exp(-0.5 * e);
+            break;
+        }
+        default: break;
+    }
+    return make_double2(v, 0.0);
+}
+
+__device__ __forceinline__ double2 apply_mult(double2 m, double2 c) {
+    // real multipliers: c * m.x (exactly like complex<double> *= double);
+    // imaginary (derivative) multipliers: (0, k) * c
+    if (m.y == 0.0) return make_double2(c.x * m.x, c.y * m.x);
+    return cmul(m, c);
+}
+
+
+// --------------------------------------------------------------------------
+// strided-axis kernel (x1 / x2 passes)
+// --------------------------------------------------------------------------
+template <int N>
+struct AxisCfg {
+    static constexpr int RMAX = rmax_of(N);
+    static constexpr int T = N / RMAX;
+    static constexpr int TB0 = 256 / T;
+    static constexpr int TB = TB0 < 1 ? 1 : (TB0 > 64 ? 64 : TB0);
+    static constexpr int THREADS = TB * T;
+    static constexpr size_t SMEM = sizeof(double2) * N * TB;
+};
+
+// MODE 0: transform in direction DIR (src may equal dst)
+// MODE 1: forward -> multiplier -> inverse (x1 pass only), src -> dst (may alias)
+// MODE 2: like 1 but dst += result (accumulate)
+template <int N, int DIR, int MODE>
+__global__ void __launch_bounds__(AxisCfg<N>::THREADS)
+    k_fft_axis(const double2* src, double2* dst, long long inner, long long outer_stride,
+               const double2* __restrict__ tw, MultDev m, GridDims g) {
+    using C = AxisCfg<N>;
+    extern __shared__ double2 smem[];
+    const int col = threadIdx.x % C::TB;
+    const int t = threadIdx.x / C::TB;
+    const long long cc = blockIdx.x * (long long)C::TB + col;
+    const bool valid = cc < inner;
+    const long long off = blockIdx.y * outer_stride + (valid ? cc : 0);
+    const double2* s = src + off;
+    double2* d = dst + off;
+    auto sm = [&](int i) -> double2& { return smem[i * C::TB + col]; };
+    auto load = [&](int i) -> double2 {
+        return valid ? s[(long long)i * inner] : make_double2(0.0, 0.0);
+    };
+    auto store = [&](int i, double2 v) {
+        if (valid) {
+            if constexpr (MODE == 2)
+                d[(long long)i * inner] = cadd(d[(long long)i * inner], v);
+            else
+                d[(long long)i * inner] = v;
+        }
+    };
+    if constexpr (MODE == 0) {
+        fft_line<N, DIR, false, false>(t, tw, load, store, sm);
+    } else {
+        // x1 pass: column cc = i2 * nh + i3
+        const int i2 = static_cast<int>(cc / g.nh);
+        const int i3 = static_cast<int>(cc % g.nh);
+        auto store_mult = [&](int i, double2 v) { sm(i) = apply_mult(mult_at(m, g, i, i2, i3), v); };
+        fft_line<N, -1, false, true>(t, tw, load, store_mult, sm);
+        __syncthreads();
+        auto load_sm = [&](int i) -> double2 { return sm(i); };
+        fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
+    }
+}
+
+// --------------------------------------------------------------------------
+// x3 row kernels (real rows <-> half-spectrum rows)
+// --------------------------------------------------------------------------
+template <int M>
+struct RowCfg {
+    static constexpr int RMAX = rmax_of(M);
+    static constexpr int T = M / RMAX;
+    static constexpr int RB0 = 256 / T;
+    static constexpr int RB = RB0 < 1 ? 1 : (RB0 > 64 ? 64 : RB0);
+    static constexpr int THREADS = RB * T;
+    static constexpr int LD = (M + 1) + ((M + 1) >> 4) + 1;  // padded row length
+    static constexpr size_t SMEM = sizeof(double2) * LD * RB;
+};
+__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+
+// r2c along x3: in nrows x 2M reals -> out nrows x (M+1) complex.
+// z[m] = x[2m] + i x[2m+1]; Z = FFT_M(z); X[k] = A[k] + W_N^k B[k] with
+// A = (Z[k] + conj Z[M-k]) / 2, B = (Z[k] - conj Z[M-k]) / 2i.
+template <int M>
+__global__ void __launch_bounds__(RowCfg<M>::THREADS)
+    k_r2c_rows(const double* __restrict__ in, double2* __restrict__ out, long long nrows,
+               const double2* __restrict__ twM, const double2* __restrict__ twN) {
+    using C = RowCfg<M>;
+    extern __shared__ double2 smem[];
+    const long long row0 = blockIdx.x * (long long)C::RB;
+    const double2* src = reinterpret_cast<const double2*>(in) + row0 * M;
+    const long long avail = (nrows - row0) * M;
+    for (int e = threadIdx.x; e < C::RB * M; e += C::THREADS) {
+        const int r = e / M, i = e % M;
+        smem[r * C::LD + padi(i)] = (e < avail) ? src[e] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    {
+        const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
+        auto sm = [&](int i) -> double2& { return smem[r * C::LD + padi(i)]; };
+        auto load = [&](int i) -> double2 { return sm(i); };
+        auto store = [&](int i, double2 v) { sm(i) = v; };
+        fft_line<M, -1, true, true>(t, twM, load, store, sm);
+    }
+    __syncthreads();
+    double2* dstp = out + row0 * (M + 1);
+    const long long avail_out = (nrows - row0) * (M + 1);
+    for (int e = threadIdx.x; e < C::RB * (M + 1); e += C::THREADS) {
+        if (e >= avail_out) break;
+        const int r = e / (M + 1), k = e % (M + 1);
+        const double2* Z = smem + r * C::LD;
+        double2 X;
+        if (k == 0 || k == M) {
+            const double2 z0 = Z[0];
+            X = make_double2(k == 0 ? z0.x + z0.y : z0.x - z0.y, 0.0);
+        } else {
+            const double2 zk = Z[padi(k)];
+            const double2 zc = cconj(Z[padi(M - k)]);
+            const double2 A = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
+            const double2 D = make_double2(0.5 * (zk.x - zc.x), 0.5 * (zk.y - zc.y));
+            const double2 B = make_double2(D.y, -D.x);  // D / i
+            double2 w = __ldg(twN + k);
+            w.y = -w.y;  // exp(-2 pi i k / N)
+            X = cadd(A, cmul(w, B));
+        }
+        dstp[e] = X;
+    }
+}
+
+// c2r along x3: in nrows x (M+1) complex -> out nrows x 2M reals,
+// out = add + scale * x. Z[k] = E + i O, E = X[k] + conj X[M-k],
+// O = (X[k] - conj X[M-k]) exp(+2 pi i k / N); z = IFFT_M(Z); x[2m] = Re, x[2m+1] = Im.
+// Imaginary parts of the self-conjugate bins X[0], X[M] are ignored (c2r semantics).
+template <int M>
+__global__ void __launch_bounds__(RowCfg<M>::THREADS)
+    k_c2r_rows(const double2* __restrict__ in, double* __restrict__ out, long long nrows,
+               const double2* __restrict__ twM, const double2* __restrict__ twN, double scale,
+               const double* __restrict__ add) {
+    using C = RowCfg<M>;
+    extern __shared__ double2 smem[];
+    const long long row0 = blockIdx.x * (long long)C::RB;
+    const double2* src = in + row0 * (M + 1);
+    const long long avail = (nrows - row0) * (M + 1);
+    for (int e = threadIdx.x; e < C::RB * (M + 1); e += C::THREADS) {
+        const int r = e / (M + 1), i = e % (M + 1);
+        smem[r * C::LD + padi(i)] = (e < avail) ? src[e] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    // form Z in place: thread handles the pair (k, M-k), k in [0, M/2]
+    for (int e = threadIdx.x; e < C::RB * (M / 2 + 1); e += C::THREADS) {
+        const int r = e / (M / 2 + 1), k = e % (M / 2 + 1);
+        double2* X = smem + r * C::LD;
+        if (k == 0) {
+            const double a = X[0].x, b = X[padi(M)].x;
+            X[0] = make_double2(a + b, a - b);
+        } else {
+            const double2 xk = X[padi(k)], xm = X[padi(M - k)];
+            const double2 wk = __ldg(twN + k);      // exp(+2 pi i k / N)
+            const double2 wm = __ldg(twN + M - k);  // exp(+2 pi i (M-k) / N)
+            {
+                const double2 E = cadd(xk, cconj(xm));
+                const double2 O = cmul(csub(xk, cconj(xm)), wk);
+                X[padi(k)] = make_double2(E.x - O.y, E.y + O.x);
+            }
+            if (k != M - k) {
+                const double2 E = cadd(xm, cconj(xk));
+                const double2 O = cmul(csub(xm, cconj(xk)), wm);
+                X[padi(M - k)] = make_double2(E.x - O.y, E.y + O.x);
+            }
+        }
+    }
+    __syncthreads();
+    {
+        const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
+        auto sm = [&](int i) -> double2& { return smem[r * C::LD + padi(i)]; };
+        auto load = [&](int i) -> double2 { return sm(i); };
+        auto store = [&](int i, double2 v) { sm(i) = v; };
+        fft_line<M, +1, true, true>(t, twM, load, store, sm);
+    }
+    __syncthreads();
+    double2* dstp = reinterpret_cast<double2*>(out) + row0 * M;
+    const double2* addp = add ? reinterpret_cast<const double2*>(add) + row0 * M : nullptr;
+    const long long avail_out = (nrows - row0) * M;
+    for (int e = threadIdx.x; e < C::RB * M; e += C::THREADS) {
+        if (e >= avail_out) break;
+        const int r = e / M, i = e % M;
+        const double2 z = smem[r * C::LD + padi(i)];
+        double2 o;
+        if (addp) {
+            const double2 a = addp[e];
+            o = make_double2(a.x + scale * z.x, a.y + scale * z.y);
+        } else {
+            o = make_double2(z.x * scale, z.y * scale);
+        }
+        dstp[e] = o;
+    }
+}
+
+// --------------------------------------------------------------------------
+// elementwise spectral kernels on full (n1, n2, nh) spectra
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void bin_coords(long long b, const GridDims& g, int& i1, int& i2,
+                                           int& i3) {
+    i3 = static_cast<int>(b % g.nh);
+    long long r = b / g.nh;
+    i2 = static_cast<int>(r % g.n2);
+    i1 = static_cast<int>(r / g.n2);
+}
+
+__global__ void k_spec_mult(const double2* __restrict__ in, double2* __restrict__ out, MultDev m,
+                            GridDims g) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < g.NC;
+         b += (long long)gridDim.x * blockDim.x) {
+        int i1, i2, i3;
+        bin_coords(b, g, i1, i2, i3);
+        out[b] = apply_mult(mult_at(m, g, i1, i2, i3), in[b]);
+    }
+}
+
+// divergence (spectral.cpp:124-140): acc = sum_a i k_a c_a, deriv_freq
+__global__ void k_spec_div(const double2* __restrict__ c0, const double2* __restrict__ c1,
+                           const double2* __restrict__ c2, double2* __restrict__ out, GridDims g) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < g.NC;
+         b += (long long)gridDim.x * blockDim.x) {
+        int i1, i2, i3;
+        bin_coords(b, g, i1, i2, i3);
+        double2 acc = make_double2(0.0, 0.0);
+        acc = cadd(acc, cmul(make_double2(0.0, (double)deriv_freq(i1, g.n1)), c0[b]));
+        acc = cadd(acc, cmul(make_double2(0.0, (double)deriv_freq(i2, g.n2)), c1[b]));
+        acc = cadd(acc, cmul(make_double2(0.0, (double)deriv_freq(i3, g.n3)), c2[b]));
+        out[b] = acc;
+    }
+}
+
+// projections (spectral.cpp:190-214)
+__global__ void k_spec_project(double2* __restrict__ c0, double2* __restrict__ c1,
+                               double2* __restrict__ c2, GridDims g, int kind, double beta_v,
+                               double beta_w) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < g.NC;
+         b += (long long)gridDim.x * blockDim.x) {
+        int i1, i2, i3;
+        bin_coords(b, g, i1, i2, i3);
+        const double k[3] = {(double)deriv_freq(i1, g.n1), (double)deriv_freq(i2, g.n2),
+                             (double)deriv_freq(i3, g.n3)};
+        const double kk = k[0] * k[0] + k[1] * k[1] + k[2] * k[2];
+        if (kk == 0.0) continue;
+        double s = 1.0;
+        if (kind == VR_PROJ_NEAR_INCOMPRESSIBLE)
+            s = beta_w * (kk + 1.0) / (beta_v + beta_w * (kk + 1.0));
+        const double2 a0 = c0[b], a1 = c1[b], a2 = c2[b];
+        double2 kdotf = make_double2(k[0] * a0.x, k[0] * a0.y);
+        kdotf = cadd(kdotf, make_double2(k[1] * a1.x, k[1] * a1.y));
+        kdotf = cadd(kdotf, make_double2(k[2] * a2.x, k[2] * a2.y));
+        const double f = s / kk;
+        const double2 corr = make_double2(kdotf.x * f, kdotf.y * f);
+        c0[b] = csub(a0, make_double2(k[0] * corr.x, k[0] * corr.y));
+        c1[b] = csub(a1, make_double2(k[1] * corr.x, k[1] * corr.y));
+        c2[b] = csub(a2, make_double2(k[2] * corr.x, k[2] * corr.y));
+    }
+}
+
+MultDev to_dev(const MultParams& p) {
+    MultDev m;
+    m.kind = static_cast<int>(p.kind);
+    m.reg_kind = p.reg_kind;
+    m.reg_mode = p.reg_mode;
+    m.helm_sq = p.helm_sq;
+    m.gamma = p.gamma;
+    m.beta = p.beta;
+    for (int a = 0; a < 3; ++a) m.sig2h2[a] = p.sig2h2[a];
+    return m;
+}
+
+int ilog2(int n) {
+    int l = 0;
+    while ((1 << l) < n) ++l;
+    return l;
+}
+
+// ---- host-side launchers ----------------------------------------------------
+template <int N, int DIR, int MODE>
+void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inner, long long outer,
+                   long long outer_stride, const double2* tw, const MultDev& m) {
+    using C = AxisCfg<N>;
+    auto kern = k_fft_axis<N, DIR, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(C::SMEM)));
+        attr = true;
+    }
+    dim3 grid(static_cast<unsigned>((inner + C::TB - 1) / C::TB), static_cast<unsigned>(outer));
+    kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, dst, inner, outer_stride, tw, m, ctx->g);
+    check_launch();
+    count_launch(ctx);
+}
+
+template <int DIR, int MODE>
+void launch_axis(vr_ctx* ctx, int n, const double2* src, double2* dst, long long inner,
+                 long long outer, long long outer_stride, const double2* tw, const MultDev& m) {
+    switch (n) {
+#define VR_CASE(NN) \
+    case NN: launch_axis_t<NN, DIR, MODE>(ctx, src, dst, inner, outer, outer_stride, tw, m); break;
+        VR_CASE(4)
+        VR_CASE(8)
+        VR_CASE(16)
+        VR_CASE(32)
+        VR_CASE(64)
+        VR_CASE(128)
+        VR_CASE(256)
+        VR_CASE(512)
+        VR_CASE(1024)
+#undef VR_CASE
+        default: throw_dimension("fft: unsupported axis length " + std::to_string(n));
+    }
+}
+
+template <int M>
+void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double scale,
+                   const double* add) {
+    using C = RowCfg<M>;
+    const long long nrows = static_cast<long long>(ctx->g.n1) * ctx->g.n2;
+    const unsigned grid = static_cast<unsigned>((nrows + C::RB - 1) / C::RB);
+    if (forward) {
+        static bool attr = false;
+        if (!attr) {
+            VR_CUDA(cudaFuncSetAttribute(k_r2c_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::SMEM)));
+            attr = true;
+        }
+        k_r2c_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+            static_cast<const double*>(in), static_cast<double2*>(out), nrows, ctx->fft->tw3h,
+            ctx->fft->tw3);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            VR_CUDA(cudaFuncSetAttribute(k_c2r_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::SMEM)));
+            attr = true;
+        }
+        k_c2r_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+            static_cast<const double2*>(in), static_cast<double*>(out), nrows, ctx->fft->tw3h,
+            ctx->fft->tw3, scale, add);
+    }
+    check_launch();
+    count_launch(ctx);
+}
+
+void launch_rows(vr_ctx* ctx, bool forward, const void* in, void* out, double scale,
+                 const double* add) {
+    switch (ctx->g.n3 / 2) {
+#define VR_CASE(MM) \
+    case MM: launch_rows_t<MM>(ctx, forward, in, out, scale, add); break;
+        VR_CASE(2)
+        VR_CASE(4)
+        VR_CASE(8)
+        VR_CASE(16)
+        VR_CASE(32)
+        VR_CASE(64)
+        VR_CASE(128)
+        VR_CASE(256)
+        VR_CASE(512)
+#undef VR_CASE
+        default: throw_dimension("fft: unsupported n3 " + std::to_string(ctx->g.n3));
+    }
+}
+
+unsigned spec_grid(const GridDims& g) {
+    return static_cast<unsigned>(std::min<long long>((g.NC + 255) / 256, 148LL * 16));
+}
+
+// forward passes x2 then x1 on a spectrum in place
+void axes_forward(vr_ctx* ctx, double2* s) {
+    const GridDims& g = ctx->g;
+    MultDev none{};
+    launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+    launch_axis<-1, 0>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, none);
+}
+void axes_inverse(vr_ctx* ctx, double2* s) {
+    const GridDims& g = ctx->g;
+    MultDev none{};
+    launch_axis<+1, 0>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, none);
+    launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+}
+
+void upload_table(double2** dst, int n) {
+    std::vector<double2> h(n);
+    const long double two_pi_l = 6.283185307179586476925286766559005768L;
+    for (int k = 0; k < n; ++k) {
+        long double a = two_pi_l * static_cast<long double>(k) / static_cast<long double>(n);
+        h[k] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(sinl(a)));
+    }
+    VR_CUDA(cudaMalloc(dst, sizeof(double2) * n));
+    VR_CUDA(cudaMemcpy(*dst, h.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+
+// ============================================================================
+// public (namespace vr) entry points
+// ============================================================================
+void fft_plan_create(vr_ctx* ctx) {
+    auto* p = new FftPlan();
+    ctx->fft = p;
+    upload_table(&p->tw1, ctx->g.n1);
+    upload_table(&p->tw2, ctx->g.n2);
+    upload_table(&p->tw3h, ctx->g.n3 / 2);
+    upload_table(&p->tw3, ctx->g.n3);
+}
+void fft_plan_destroy(vr_ctx* ctx) {
+    if (!ctx->fft) return;
+    cudaFree(ctx->fft->tw1);
+    cudaFree(ctx->fft->tw2);
+    cudaFree(ctx->fft->tw3h);
+    cudaFree(ctx->fft->tw3);
+    delete ctx->fft;
+    ctx->fft = nullptr;
+}
+
+void fft_r2c(vr_ctx* ctx, const double* in, double* spec) {
+    auto* s = reinterpret_cast<double2*>(spec);
+    launch_rows(ctx, true, in, s, 1.0, nullptr);
+    axes_forward(ctx, s);
+}
+
+void fft_c2r(vr_ctx* ctx, double* spec, double* out, double scale, const double* add) {
+    auto* s = reinterpret_cast<double2*>(spec);
+    axes_inverse(ctx, s);
+    launch_rows(ctx, false, s, out, scale, add);
+}
+
+void spectral_scalar_op(vr_ctx* ctx, const double* in, double* out, const MultParams& mp,
+                        const double* add) {
+    const GridDims& g = ctx->g;
+    auto* s = reinterpret_cast<double2*>(spec_buf(ctx, 0));
+    MultDev none{}, m = to_dev(mp);
+    launch_rows(ctx, true, in, s, 1.0, nullptr);
+    launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+    launch_axis<-1, 1>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, m);
+    launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+    launch_rows(ctx, false, s, out, 1.0 / static_cast<double>(g.N), add);
+}
+
+void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
+    const GridDims& g = ctx->g;
+    auto* s0 = reinterpret_cast<double2*>(spec_buf(ctx, 0));
+    auto* s1 = reinterpret_cast<double2*>(spec_buf(ctx, 1));
+    MultDev none{};
+    launch_rows(ctx, true, f, s0, 1.0, nullptr);
+    launch_axis<-1, 0>(ctx, g.n2, s0, s0, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+    for (int a = 0; a < 3; ++a) {
+        MultParams mp;
+        mp.kind = static_cast<Mult>(static_cast<int>(Mult::deriv0) + a);
+        launch_axis<-1, 1>(ctx, g.n1, s0, s1, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1,
+                           to_dev(mp));
+        launch_axis<+1, 0>(ctx, g.n2, s1, s1, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2,
+                           none);
+        launch_rows(ctx, false, s1, out3 + a * g.N, 1.0 / static_cast<double>(g.N), nullptr);
+    }
+}
+
+void op_divergence(vr_ctx* ctx, const double* v3, double* out) {
+    const GridDims& g = ctx->g;
+    double2* s[3];
+    for (int a = 0; a < 3; ++a) {
+        s[a] = reinterpret_cast<double2*>(spec_buf(ctx, a));
+        fft_r2c(ctx, v3 + a * g.N, reinterpret_cast<double*>(s[a]));
+    }
+    auto* acc = reinterpret_cast<double2*>(spec_buf(ctx, 3));
+    k_spec_div<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], acc, g);
+    check_launch();
+    count_launch(ctx);
+    fft_c2r(ctx, reinterpret_cast<double*>(acc), out, 1.0 / static_cast<double>(g.N), nullptr);
+}
+
+void op_projection(vr_ctx* ctx, const double* in3, double* out3, int kind, double beta_v,
+                   double beta_w) {
+    const GridDims& g = ctx->g;
+    if (kind == VR_PROJ_IDENTITY) {
+        if (in3 != out3)
+            VR_CUDA(cudaMemcpyAsync(out3, in3, sizeof(double) * 3 * g.N, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+        return;
+    }
+    if (kind == VR_PROJ_NEAR_INCOMPRESSIBLE && (beta_v <= 0.0 || beta_w <= 0.0))
+        throw_argument("apply_projection: near-incompressible K needs beta_v, beta_w > 0");
+    if (kind != VR_PROJ_INCOMPRESSIBLE && kind != VR_PROJ_NEAR_INCOMPRESSIBLE)
+        throw_argument("apply_projection: unknown projection kind");
+    double2* s[3];
+    for (int a = 0; a < 3; ++a) {
+        s[a] = reinterpret_cast<double2*>(spec_buf(ctx, a));
+        fft_r2c(ctx, in3 + a * g.N, reinterpret_cast<double*>(s[a]));
+    }
+    k_spec_project<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], g, kind, beta_v,
+                                                           beta_w);
+    check_launch();
+    count_launch(ctx);
+    for (int a = 0; a < 3; ++a)
+        fft_c2r(ctx, reinterpret_cast<double*>(s[a]), out3 + a * g.N,
+                1.0 / static_cast<double>(g.N), nullptr);
+}
+
+double reg_symbol(const vr_regnorm& n, double k2) {
+    switch (n.kind) {
+        case VR_REG_H1: return k2;
+        case VR_REG_H2: return k2 * k2;
+        case VR_REG_H3: return k2 * k2 * k2;
+        case VR_REG_HELMHOLTZ: {
+            double s = k2 + n.gamma;
+            return n.helmholtz_squared ? s * s : s;
+        }
+    }
+    return 0.0;
+}
+
+void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm, int mode,
+            double beta, const double* add3) {
+    MultParams mp;
+    mp.kind = Mult::reg;
+    mp.reg_kind = norm.kind;
+    mp.reg_mode = mode;
+    mp.gamma = norm.gamma;
+    mp.helm_sq = norm.helmholtz_squared;
+    mp.beta = beta;
+    const long long N = ctx->g.N;
+    for (int c = 0; c < 3; ++c)
+        spectral_scalar_op(ctx, in3 + c * N, out3 + c * N, mp, add3 ? add3 + c * N : nullptr);
+}
+
+}  // namespace vr

@@ -1,0 +1,512 @@
+// objective.cu -- Objective<double> on the device (proj/src/objective.cpp:35-186)
+// and the C++ host driver: PCG, Armijo, Gauss-Newton (proj/src/solver.cpp:23-269).
+//
+// The host driver keeps the reference's algorithm and constants verbatim
+// (forcing min(0.5, sqrt(|g|/|g0|)), unweighted dots in PCG and the stop test,
+// weighted inner product for the Armijo slope, squared-norm relative stop);
+// every vector it touches stays in HBM and only scalars cross to the host.
+#include <chrono>
+#include <cmath>
+#include <string>
+
+#include "objective.cuh"
+
+vr_state::~vr_state() {
+    vr_ctx* ctx = obj ? obj->ctx : nullptr;
+    if (!ctx) return;
+    for (double* p : {v, xb, mhist, xf, factor, gradm, grad}) vr::dev_free(ctx, p);
+}
+
+vr_objective::~vr_objective() {
+    if (!ctx) return;
+    for (double* p : {ws_lam, ws_tmp, ws_b}) vr::dev_free(ctx, p);
+}
+
+namespace vr {
+
+double* dev_alloc(vr_ctx* ctx, long long n) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, sizeof(double) * static_cast<size_t>(n), ctx->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw_resource("device allocation of " + std::to_string(sizeof(double) * n) +
+                       " bytes failed: " + cudaGetErrorString(e));
+    }
+    return static_cast<double*>(p);
+}
+void dev_free(vr_ctx* ctx, double* p) {
+    if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+void validate_model(const vr_model& m) {
+    // RegNorm::validate (spectral.hpp:82-87), RegModel::validate (objective.hpp:18-22)
+    if (m.norm.kind < VR_REG_H1 || m.norm.kind > VR_REG_HELMHOLTZ)
+        throw_argument("RegNorm: unknown regularization kind");
+    if (m.norm.kind == VR_REG_HELMHOLTZ && m.norm.gamma <= 0.0)
+        throw_argument("RegNorm: helmholtz gamma must be > 0");
+    if (m.norm.div_penalty && m.norm.beta_w <= 0.0)
+        throw_argument("RegNorm: beta_w must be > 0 when the divergence penalty is on");
+    if (m.beta_v <= 0.0) throw_argument("RegModel: beta_v must be > 0");
+    if (m.nt < 1) throw_argument("RegModel: n_t must be >= 1");
+    if (m.projection < VR_PROJ_IDENTITY || m.projection > VR_PROJ_NEAR_INCOMPRESSIBLE)
+        throw_argument("RegModel: unknown projection kind");
+    if (!m.gauss_newton)
+        throw_argument("RegModel: the full-Newton Hessian is not implemented on the GPU path "
+                       "(Gauss-Newton only)");
+}
+
+void validate_params(const vr_solver_params& p) {
+    // SolverParams::validate (solver.hpp:24-32)
+    if (p.eps_opt <= 0 || p.abs_grad_tol <= 0 || p.armijo_c1 <= 0)
+        throw_argument("SolverParams: tolerances must be > 0");
+    if (p.max_newton < 1 || p.max_krylov < 1 || p.armijo_max_trials < 1)
+        throw_argument("SolverParams: iteration limits must be >= 1");
+    if (p.armijo_backtrack <= 0 || p.armijo_backtrack >= 1)
+        throw_argument("SolverParams: backtracking factor must be in (0,1)");
+}
+
+// ---------------------------------------------------------------------------
+// reductions with the reference's component order (field_ops.hpp:51-64,
+// spectral.cpp:47-62)
+// ---------------------------------------------------------------------------
+static double cell_volume(const GridDims& g) { return g.h1 * g.h2 * g.h3; }
+
+double dot_l2_vec(vr_ctx* ctx, const double* a, const double* b) {
+    double r[3];
+    dot_components(ctx, a, b, ctx->g.N, 3, r);
+    double s = 0.0;
+    for (int c = 0; c < 3; ++c) s += r[c];
+    return s;
+}
+double norm_l2_vec(vr_ctx* ctx, const double* a) { return std::sqrt(dot_l2_vec(ctx, a, a)); }
+double inner_product_vec(vr_ctx* ctx, const double* a, const double* b) {
+    double r[3];
+    dot_components(ctx, a, b, ctx->g.N, 3, r);
+    const double vol = cell_volume(ctx->g);
+    double s = 0.0;
+    for (int c = 0; c < 3; ++c) s += r[c] * vol;
+    return s;
+}
+double inner_product_scalar(vr_ctx* ctx, const double* a, const double* b) {
+    double r;
+    dot_components(ctx, a, b, ctx->g.N, 1, &r);
+    return r * cell_volume(ctx->g);
+}
+
+// ---------------------------------------------------------------------------
+// Objective
+// ---------------------------------------------------------------------------
+vr_objective* objective_create(vr_ctx* ctx, const double* mR, const double* mT,
+                               const vr_model& model) {
+    validate_model(model);
+    auto* o = new vr_objective();
+    o->ctx = ctx;
+    o->mR = mR;
+    o->mT = mT;
+    o->model = model;
+    const long long N = ctx->g.N;
+    try {
+        o->ws_lam = dev_alloc(ctx, (model.nt + 1) * N);
+        o->ws_tmp = dev_alloc(ctx, 2 * N);
+        o->ws_b = dev_alloc(ctx, 3 * N);
+        // initial_mismatch_ = <m_T - m_R, m_T - m_R>_h (objective.cpp:40-44)
+        o->initial_mismatch = sum_sq_diff(ctx, mT, mR, N) * cell_volume(ctx->g);
+    } catch (...) {
+        delete o;
+        throw;
+    }
+    return o;
+}
+
+vr_state* objective_evaluate(vr_objective* o, const double* v3) {
+    vr_ctx* ctx = o->ctx;
+    const GridDims& g = ctx->g;
+    const long long N = g.N;
+    const int nt = o->model.nt;
+    if (!all_finite(ctx, v3, 3 * N)) throw_numeric("evaluate_objective: non-finite velocity");
+
+    auto* s = new vr_state();
+    s->obj = o;
+    s->nt = nt;
+    try {
+        s->v = dev_alloc(ctx, 3 * N);
+        s->xb = dev_alloc(ctx, 3 * N);
+        s->mhist = dev_alloc(ctx, (nt + 1) * N);
+        VR_CUDA(cudaMemcpyAsync(s->v, v3, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        sl_trace(ctx, v3, nt, VR_TRACE_BACKWARD, s->xb);
+        // solve_state (transport.cpp:72-79)
+        VR_CUDA(cudaMemcpyAsync(s->mhist, o->mT, sizeof(double) * N, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        for (int j = 0; j < nt; ++j) sl_advect(ctx, s->mhist + j * N, s->xb, s->mhist + (j + 1) * N);
+        o->counters.pde_solves += 1;
+
+        s->mismatch = sum_sq_diff(ctx, s->mhist + nt * N, o->mR, N) * cell_volume(g);
+        s->mismatch_rel = o->initial_mismatch > 0.0 ? s->mismatch / o->initial_mismatch : 0.0;
+
+        // reg = 1/2 beta_v <A v, v>_h with A applied at beta = 1 (objective.cpp:63-64)
+        double* Av = o->ws_b;
+        op_reg(ctx, v3, Av, o->model.norm, VR_REGOP_APPLY, 1.0);
+        const double reg = 0.5 * o->model.beta_v * inner_product_vec(ctx, Av, v3);
+        double penalty = 0.0;
+        if (o->model.norm.div_penalty) {
+            double* w = o->ws_tmp;
+            double* hw = o->ws_tmp + N;
+            op_divergence(ctx, v3, w);
+            MultParams mp;
+            mp.kind = Mult::helmholtz1;
+            spectral_scalar_op(ctx, w, hw, mp);
+            penalty = 0.5 * o->model.norm.beta_w * inner_product_scalar(ctx, hw, w);
+        }
+        s->objective = 0.5 * s->mismatch + reg + penalty;
+        if (!std::isfinite(s->objective))
+            throw_numeric("evaluate_objective: objective is not finite");
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    o->counters.objective_evals += 1;
+    return s;
+}
+
+// prepare_adjoint_ctx (objective.cpp:77-84) + the grad m_j cache
+static void prepare_adjoint_ctx(vr_objective* o, vr_state* s) {
+    if (s->has_adjoint_ctx) return;
+    vr_ctx* ctx = o->ctx;
+    const long long N = ctx->g.N;
+    const int nt = s->nt;
+    const double dt = 1.0 / nt;
+    if (!s->xf) s->xf = dev_alloc(ctx, 3 * N);
+    if (!s->factor) s->factor = dev_alloc(ctx, N);
+    if (!s->gradm) s->gradm = dev_alloc(ctx, 3LL * (nt + 1) * N);
+    sl_trace(ctx, s->v, nt, VR_TRACE_FORWARD, s->xf);
+    double* div_v = field_buf(ctx, 0);
+    op_divergence(ctx, s->v, div_v);
+    sl_factor(ctx, div_v, s->xf, 0.5 * dt, s->factor);
+    for (int j = 0; j <= nt; ++j) op_gradient(ctx, s->mhist + j * N, s->gradm + 3LL * j * N);
+    s->has_adjoint_ctx = true;
+}
+
+void objective_gradient(vr_objective* o, vr_state* s) {
+    vr_ctx* ctx = o->ctx;
+    const long long N = ctx->g.N;
+    prepare_adjoint_ctx(o, s);
+    const int nt = s->nt;
+    const double dt = 1.0 / nt;
+    if (!s->grad) s->grad = dev_alloc(ctx, 3 * N);
+
+    // terminal lambda = m_R - m_nt and the observer at j = nt (objective.cpp:91-99)
+    double* lam[2] = {o->ws_tmp, o->ws_tmp + N};
+    double* b = o->ws_b;
+    sl_grad_terminal(ctx, o->mR, s->mhist + nt * N, s->gradm + 3LL * nt * N, 0.5 * dt, lam[0], b);
+    int cur = 0;
+    for (int j = nt - 1; j >= 0; --j) {
+        const double w = (j == 0) ? 0.5 * dt : dt;
+        sl_adjoint_step(ctx, lam[cur], s->xf, s->factor, lam[cur ^ 1], s->gradm + 3LL * j * N, w, b);
+        cur ^= 1;
+    }
+    o->counters.pde_solves += 1;
+    if (o->model.projection != VR_PROJ_IDENTITY)
+        op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+    // g = b + beta_v A v (objective.cpp:106-110), the add fused into the c2r epilogue
+    op_reg(ctx, s->v, s->grad, o->model.norm, VR_REGOP_APPLY, o->model.beta_v, b);
+    s->has_gradient = true;
+    o->counters.gradient_evals += 1;
+}
+
+// hessian_data_matvec (objective.cpp:123-156) [+ beta_v A vt, objective.cpp:114-121]
+void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, double* out3,
+                      bool add_reg) {
+    vr_ctx* ctx = o->ctx;
+    const long long N = ctx->g.N;
+    if (!s->has_adjoint_ctx)
+        throw_logic("hessian_matvec: evaluation context is missing the adjoint sweep data "
+                    "(compute the gradient first)");
+    const int nt = s->nt;
+    const double dt = 1.0 / nt;
+    const double hdt = 0.5 / nt;
+    VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, sizeof(int), ctx->stream));
+
+    // incremental state (transport.cpp:150-173), terminal = -mt_nt into lam[nt]
+    double* tmp[2] = {o->ws_tmp, o->ws_tmp + N};
+    double* lam = o->ws_lam;
+    sl_incstate_first(ctx, s->gradm, vt3, hdt, tmp[0]);
+    int cur = 0;
+    for (int j = 0; j < nt; ++j) {
+        const bool last = (j + 1 == nt);
+        sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
+                         last ? lam + nt * N : tmp[cur ^ 1], last ? 1 : 0);
+        cur ^= 1;
+    }
+    o->counters.pde_solves += 1;
+    // incremental adjoint, Gauss-Newton branch = plain continuity sweep (transport.cpp:188-190)
+    for (int j = nt - 1; j >= 0; --j)
+        sl_adjoint_step(ctx, lam + (j + 1) * N, s->xf, s->factor, lam + j * N, nullptr, 0.0,
+                        nullptr);
+    o->counters.pde_solves += 1;
+    double* b = o->ws_b;
+    sl_accumulate(ctx, lam, s->gradm, nt, dt, b);
+    if (o->model.projection != VR_PROJ_IDENTITY)
+        op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+    o->counters.hessian_matvecs += 1;
+    if (add_reg)
+        op_reg(ctx, vt3, out3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v, b);
+    else
+        VR_CUDA(cudaMemcpyAsync(out3, b, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->flag_host) throw_numeric("hessian_matvec: non-finite direction");
+}
+
+void objective_apply_reg(vr_objective* o, const double* u3, int mode, double* out3) {
+    if (mode < VR_REGOP_APPLY || mode > VR_REGOP_INVERSE_SQRT)
+        throw_argument("apply_reg: unknown mode");
+    op_reg(o->ctx, u3, out3, o->model.norm, mode, o->model.beta_v);
+}
+void objective_apply_K(vr_objective* o, const double* u3, double* out3) {
+    op_projection(o->ctx, u3, out3, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+}
+
+// ---------------------------------------------------------------------------
+// PCG (solver.cpp:51-100)
+// ---------------------------------------------------------------------------
+vr_pcg_stats pcg_solve(vr_ctx* ctx, const DevOp& apply, const double* rhs, double rel_tol,
+                       int max_iter, const DevOp& precond, double* x) {
+    const long long n3 = 3 * ctx->g.N;
+    vr_pcg_stats st{};
+    st.rel_residual = 1.0;
+    VR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n3, ctx->stream));
+    const double r0 = norm_l2_vec(ctx, rhs);
+    if (r0 == 0.0) {
+        st.converged = 1;
+        st.rel_residual = 0.0;
+        return st;
+    }
+    const double target = rel_tol * r0;
+    double* r = dev_alloc(ctx, n3);
+    double* z = dev_alloc(ctx, n3);
+    double* s = dev_alloc(ctx, n3);
+    double* Hs = dev_alloc(ctx, n3);
+    auto cleanup = [&] {
+        for (double* p : {r, z, s, Hs}) dev_free(ctx, p);
+    };
+    try {
+        VR_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+        precond(r, z);
+        VR_CUDA(cudaMemcpyAsync(s, z, sizeof(double) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+        double rz = dot_l2_vec(ctx, r, z);
+        for (int it = 0; it < max_iter; ++it) {
+            apply(s, Hs);
+            const double sHs = dot_l2_vec(ctx, s, Hs);
+            if (sHs <= 0.0) {
+                st.negative_curvature = 1;
+                if (it == 0)
+                    VR_CUDA(cudaMemcpyAsync(x, z, sizeof(double) * n3, cudaMemcpyDeviceToDevice,
+                                            ctx->stream));
+                st.iterations = it + 1;
+                st.rel_residual = norm_l2_vec(ctx, r) / r0;
+                cleanup();
+                return st;
+            }
+            const double kappa = rz / sHs;
+            add_scaled(ctx, x, kappa, s, n3);
+            add_scaled(ctx, r, -kappa, Hs, n3);
+            st.iterations = it + 1;
+            const double rn = norm_l2_vec(ctx, r);
+            st.rel_residual = rn / r0;
+            if (rn < target) {
+                st.converged = 1;
+                cleanup();
+                return st;
+            }
+            precond(r, z);
+            const double rz_new = dot_l2_vec(ctx, r, z);
+            const double mu = rz_new / rz;
+            rz = rz_new;
+            lin_comb(ctx, s, 1.0, z, mu, s, n3);
+        }
+        st.hit_max_iterations = 1;
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+    return st;
+}
+
+// ---------------------------------------------------------------------------
+// Armijo (solver.cpp:104-129) and Gauss-Newton (solver.cpp:154-269)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct LineSearch {
+    bool success = false;
+    double alpha = 0.0;
+    int trials = 0;
+    vr_state* state = nullptr;
+};
+
+LineSearch armijo_search(vr_objective* o, const vr_state* cur, const double* dir,
+                         const vr_solver_params& p) {
+    vr_ctx* ctx = o->ctx;
+    const long long n3 = 3 * ctx->g.N;
+    if (!cur->has_gradient) throw_logic("armijo_search: current state has no gradient");
+    const double slope = inner_product_vec(ctx, cur->grad, dir);
+    if (slope >= 0.0)
+        throw_argument("armijo_search: not a descent direction (slope = " + std::to_string(slope) +
+                       ")");
+    LineSearch res;
+    double alpha = 1.0;
+    double* trial_v = dev_alloc(ctx, n3);
+    try {
+        for (int t = 0; t < p.armijo_max_trials; ++t) {
+            lin_comb(ctx, trial_v, 1.0, cur->v, alpha, dir, n3);
+            vr_state* trial = objective_evaluate(o, trial_v);
+            res.trials = t + 1;
+            if (trial->objective <= cur->objective + p.armijo_c1 * alpha * slope) {
+                res.success = true;
+                res.alpha = alpha;
+                res.state = trial;
+                break;
+            }
+            delete trial;
+            alpha *= p.armijo_backtrack;
+        }
+    } catch (...) {
+        dev_free(ctx, trial_v);
+        throw;
+    }
+    dev_free(ctx, trial_v);
+    return res;
+}
+
+vr_iteration_record make_record(int k, const vr_state* s, double gn, double g0,
+                                const vr_counters& fine, double elapsed) {
+    vr_iteration_record r{};
+    r.k = k;
+    r.objective = s->objective;
+    r.mismatch_rel = s->mismatch_rel;
+    r.grad_norm = gn;
+    r.grad_rel = g0 > 0 ? gn / g0 : 0.0;
+    r.fine_matvecs = fine.hessian_matvecs;
+    r.coarse_matvecs = 0;
+    r.pde_solves = fine.pde_solves;
+    r.wall_time_s = elapsed;
+    return r;
+}
+
+}  // namespace
+
+GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, const double* v0,
+                            const vr_model& model, const vr_solver_params& params, int precond,
+                            double* v_out) {
+    validate_params(params);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    const long long n3 = 3 * ctx->g.N;
+    GnResult res;
+    vr_solve_report& rep = res.report;
+    rep.stop = VR_STOP_MAX_ITERATIONS;
+    vr_objective* obj = objective_create(ctx, mR, mT, model);
+    vr_state* state = nullptr;
+    double* dir = nullptr;
+    double* rhs = nullptr;
+    auto cleanup = [&] {
+        delete state;
+        dev_free(ctx, dir);
+        dev_free(ctx, rhs);
+        delete obj;
+    };
+    try {
+        state = objective_evaluate(obj, v0);
+        objective_gradient(obj, state);
+        const double g0 = norm_l2_vec(ctx, state->grad);
+        rep.grad0 = g0;
+        res.records.push_back(make_record(0, state, g0, g0, obj->counters, elapsed()));
+        if (g0 == 0.0) {
+            rep.stop = VR_STOP_ZERO_GRADIENT;
+            rep.success = 1;
+        } else {
+            dir = dev_alloc(ctx, n3);
+            rhs = dev_alloc(ctx, n3);
+            double gk = g0;
+            int k = 0;
+            for (;;) {
+                const bool rel_ok = params.squared_norm_stop ? (gk * gk <= params.eps_opt * g0 * g0)
+                                                             : (gk <= params.eps_opt * g0);
+                if (rel_ok) {
+                    rep.stop = VR_STOP_CONVERGED_REL;
+                    rep.success = 1;
+                    break;
+                }
+                if (gk <= params.abs_grad_tol) {
+                    rep.stop = VR_STOP_CONVERGED_ABS;
+                    rep.success = 1;
+                    break;
+                }
+                if (k >= params.max_newton) {
+                    rep.stop = VR_STOP_MAX_ITERATIONS;
+                    break;
+                }
+                const double eps_H = std::min(0.5, std::sqrt(gk / g0));  // compute_forcing
+                const vr_state* cs = state;
+                DevOp op = [&](const double* u, double* out) {
+                    objective_matvec(obj, cs, u, out, true);
+                };
+                DevOp pc = [&](const double* r, double* z) {
+                    if (precond == VR_PRECOND_SPECTRAL)
+                        objective_apply_reg(obj, r, VR_REGOP_INVERSE, z);
+                    else
+                        VR_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * n3,
+                                                cudaMemcpyDeviceToDevice, ctx->stream));
+                };
+                // rhs = -g (scale(rhs, -1.0))
+                lin_comb(ctx, rhs, -1.0, state->grad, 0.0, state->grad, n3);
+                vr_pcg_stats pcg = pcg_solve(ctx, op, rhs, eps_H, params.max_krylov, pc, dir);
+
+                const double slope = inner_product_vec(ctx, state->grad, dir);
+                if (slope >= 0.0) {
+                    rep.stop = VR_STOP_LINE_SEARCH_FAILURE;
+                    break;
+                }
+                LineSearch ls = armijo_search(obj, state, dir, params);
+                if (!ls.success) {
+                    rep.stop = VR_STOP_LINE_SEARCH_FAILURE;
+                    break;
+                }
+                delete state;
+                state = ls.state;
+                objective_gradient(obj, state);
+                gk = norm_l2_vec(ctx, state->grad);
+                ++k;
+                vr_iteration_record row = make_record(k, state, gk, g0, obj->counters, elapsed());
+                row.step_length = ls.alpha;
+                row.forcing = eps_H;
+                row.inner_iterations = pcg.iterations;
+                res.records.push_back(row);
+            }
+            rep.outer_iterations = k;
+        }
+        rep.final_objective = state->objective;
+        rep.final_mismatch_rel = state->mismatch_rel;
+        const double gfin = norm_l2_vec(ctx, state->grad);
+        rep.final_grad_rel = g0 > 0 ? gfin / g0 : 0.0;
+        rep.fine = obj->counters;
+        rep.n_records = static_cast<int>(res.records.size());
+        VR_CUDA(cudaMemcpyAsync(v_out, state->v, sizeof(double) * n3, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        rep.wall_time_s = elapsed();
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+    return res;
+}
+
+}  // namespace vr

@@ -1,0 +1,78 @@
+// objective.cuh -- device-resident Objective / EvalState (objective.hpp:11-122)
+// and the host-side Gauss-Newton-Krylov driver (solver.hpp:78-164).
+#pragma once
+
+#include <functional>
+
+#include "vr_common.cuh"
+
+struct vr_objective;
+
+// EvalState<T> (objective.hpp:37-54), device resident. Beyond the reference's
+// fields it caches grad m_j (3 (n_t+1) fields), built once per iterate in the
+// gradient: it makes every Hessian matvec FFT-free except the beta_v A term.
+struct vr_state {
+    vr_objective* obj = nullptr;
+    int nt = 0;
+    double* v = nullptr;       // 3N
+    double* xb = nullptr;      // 3N backward departure points
+    double* mhist = nullptr;   // (nt+1)N
+    double* xf = nullptr;      // 3N forward departure points (adjoint ctx)
+    double* factor = nullptr;  // N continuity factor (adjoint ctx)
+    double* gradm = nullptr;   // 3(nt+1)N, [j*3 + a]
+    double* grad = nullptr;    // 3N
+    double objective = 0.0, mismatch = 0.0, mismatch_rel = 0.0;
+    bool has_gradient = false, has_adjoint_ctx = false;
+    ~vr_state();
+};
+
+struct vr_objective {
+    vr_ctx* ctx = nullptr;
+    const double* mR = nullptr;  // non-owning (objective.hpp:97-98)
+    const double* mT = nullptr;
+    vr_model model{};
+    vr_counters counters{};
+    double initial_mismatch = 0.0;
+    // workspace reused by every call
+    double* ws_lam = nullptr;  // (nt+1)N
+    double* ws_tmp = nullptr;  // 2N
+    double* ws_b = nullptr;    // 3N
+    ~vr_objective();
+};
+
+namespace vr {
+
+double* dev_alloc(vr_ctx* ctx, long long ndoubles);
+void dev_free(vr_ctx* ctx, double* p);
+
+void validate_model(const vr_model& m);
+void validate_params(const vr_solver_params& p);
+
+vr_objective* objective_create(vr_ctx* ctx, const double* mR, const double* mT,
+                               const vr_model& model);
+vr_state* objective_evaluate(vr_objective* o, const double* v3);
+void objective_gradient(vr_objective* o, vr_state* s);
+void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, double* out3,
+                      bool add_reg);
+void objective_apply_reg(vr_objective* o, const double* u3, int mode, double* out3);
+void objective_apply_K(vr_objective* o, const double* u3, double* out3);
+
+// weighted / unweighted reductions on vector fields (component order as the reference)
+double dot_l2_vec(vr_ctx* ctx, const double* a, const double* b);
+double norm_l2_vec(vr_ctx* ctx, const double* a);
+double inner_product_vec(vr_ctx* ctx, const double* a, const double* b);
+double inner_product_scalar(vr_ctx* ctx, const double* a, const double* b);
+
+using DevOp = std::function<void(const double*, double*)>;
+vr_pcg_stats pcg_solve(vr_ctx* ctx, const DevOp& apply, const double* rhs, double rel_tol,
+                       int max_iter, const DevOp& precond, double* x);
+
+struct GnResult {
+    vr_solve_report report{};
+    std::vector<vr_iteration_record> records;
+};
+GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, const double* v0,
+                            const vr_model& model, const vr_solver_params& params, int precond,
+                            double* v_out);
+
+}  // namespace vr

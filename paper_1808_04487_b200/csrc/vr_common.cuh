@@ -1,0 +1,194 @@
+// vr_common.cuh -- shared types for the sm_100a operator layer.
+//
+// Layout contract (reference proj/include/veloreg/grid.hpp:17-19, field.hpp:101-151):
+// fp64 scalar fields are N = n1*n2*n3 doubles, row-major, axis 0 slowest; vector
+// fields are 3 scalar fields back to back; half spectra are (n1, n2, n3/2+1)
+// complex128 (fft.hpp:12-23).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "veloreg_gpu.h"
+
+namespace vr {
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+// ---------------------------------------------------------------------------
+// Errors: mirror veloreg::Error categories (errors.hpp:9-67)
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int status;
+    int cls;
+    Error(int s, int c, const std::string& m) : std::runtime_error(m), status(s), cls(c) {}
+};
+[[noreturn]] inline void throw_argument(const std::string& m) {
+    throw Error(VR_ERR_ARGUMENT, VR_EXC_ARGUMENT, m);
+}
+[[noreturn]] inline void throw_dimension(const std::string& m) {
+    throw Error(VR_ERR_ARGUMENT, VR_EXC_DIMENSION, m);
+}
+[[noreturn]] inline void throw_numeric(const std::string& m) {
+    throw Error(VR_ERR_NUMERICS, VR_EXC_NUMERIC, m);
+}
+[[noreturn]] inline void throw_logic(const std::string& m) {
+    throw Error(VR_ERR_LOGIC, VR_EXC_LOGIC, m);
+}
+[[noreturn]] inline void throw_resource(const std::string& m) {
+    throw Error(VR_ERR_RESOURCE, VR_EXC_RESOURCE, m);
+}
+
+#define VR_CUDA(call)                                                                          \
+    do {                                                                                       \
+        cudaError_t vr_e_ = (call);                                                            \
+        if (vr_e_ != cudaSuccess)                                                              \
+            ::vr::throw_resource(std::string(#call) + ": " + cudaGetErrorString(vr_e_));       \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Grid (Grid3, grid.hpp:20-56) as passed to kernels by value
+// ---------------------------------------------------------------------------
+struct GridDims {
+    int n1, n2, n3;
+    int nh;            // n3/2 + 1
+    long long N;       // n1*n2*n3
+    long long NC;      // n1*n2*nh spectral bins
+    double h1, h2, h3; // two_pi / n_a, exactly as Grid3::spacing
+};
+
+// Signed FFT frequency / odd-derivative frequency (grid.hpp:58-64)
+__host__ __device__ inline int fft_freq(int i, int n) { return (2 * i <= n) ? i : i - n; }
+__host__ __device__ inline int deriv_freq(int i, int n) {
+    return (n % 2 == 0 && 2 * i == n) ? 0 : fft_freq(i, n);
+}
+// wrap_coord (grid.hpp:66-71)
+__device__ __forceinline__ double wrap_coord(double x) {
+    double y = x - kTwoPi * floor(x / kTwoPi);
+    if (y >= kTwoPi) y -= kTwoPi;
+    return y >= 0.0 ? y : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+struct FftPlan;
+
+}  // namespace vr
+
+struct vr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    vr::GridDims g{};
+    vr::FftPlan* fft = nullptr;
+    // lazily allocated scratch: spectra (NC complex) and real fields (N doubles)
+    std::vector<double*> spec_scratch;
+    std::vector<double*> field_scratch;
+    // deterministic reductions
+    double* red_partials = nullptr;  // device, kRedBlocks * 4 doubles
+    double* red_out = nullptr;       // device, 8 doubles
+    double* red_host = nullptr;      // pinned host, 8 doubles
+    int* flag_dev = nullptr;         // device int flags (non-finite detection)
+    int* flag_host = nullptr;        // pinned
+    long long launches = 0;
+};
+
+namespace vr {
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs; fixed => deterministic partial order
+constexpr int kRedThreads = 256;
+
+double* spec_buf(vr_ctx* ctx, int i);   // NC complex (2*NC doubles)
+double* field_buf(vr_ctx* ctx, int i);  // N doubles
+inline void count_launch(vr_ctx* ctx, int n = 1) { ctx->launches += n; }
+inline void check_launch() { VR_CUDA(cudaGetLastError()); }
+
+inline unsigned grid_1d(long long n, int threads) {
+    return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+// ---- BLAS-1 / reductions (blas1.cu) ----
+void scale(vr_ctx* ctx, double* x, long long n, double a);
+void add_scaled(vr_ctx* ctx, double* y, double a, const double* x, long long n);
+void lin_comb(vr_ctx* ctx, double* out, double a, const double* x, double b, const double* y,
+              long long n);
+// sums over `ncomp` consecutive blocks of length n; results[c] per component (host)
+void dot_components(vr_ctx* ctx, const double* a, const double* b, long long n, int ncomp,
+                    double* results);
+double max_abs(vr_ctx* ctx, const double* a, long long n);
+double max_magnitude(vr_ctx* ctx, const double* v3, long long n);
+bool all_finite(vr_ctx* ctx, const double* a, long long n);
+double sum_sq_diff(vr_ctx* ctx, const double* a, const double* b, long long n);
+double min_value(vr_ctx* ctx, const double* a, long long n);
+double max_value(vr_ctx* ctx, const double* a, long long n);
+void affine(vr_ctx* ctx, const double* x, double* out, long long n, double lo, double s);
+// device-side partial reduction helper: finalize `nblocks` partial sums (ncomp
+// interleaved per block) into red_out[0..ncomp) and copy to host
+void finalize_sums(vr_ctx* ctx, int nblocks, int ncomp, double* host_out);
+
+// ---- FFT / spectral (fft.cu) ----
+enum class Mult : int {
+    none = 0,
+    deriv0,
+    deriv1,
+    deriv2,
+    laplacian,
+    helmholtz1,
+    reg,
+    gaussian,
+};
+struct MultParams {
+    Mult kind = Mult::none;
+    int reg_kind = VR_REG_H2;
+    int reg_mode = VR_REGOP_APPLY;
+    double gamma = 1.0;
+    int helm_sq = 1;
+    double beta = 1.0;
+    double sig2h2[3] = {0, 0, 0};  // sigma_d^2 * h_d^2 for the gaussian
+};
+void fft_plan_create(vr_ctx* ctx);
+void fft_plan_destroy(vr_ctx* ctx);
+void fft_r2c(vr_ctx* ctx, const double* in, double* spec);
+// c2r of spec (destroyed) -> out = add + scale*x (add may be null)
+void fft_c2r(vr_ctx* ctx, double* spec, double* out, double scale, const double* add);
+// out = c2r(mult * r2c(in)) / N (+ add), fused x1 pass; in may equal out
+void spectral_scalar_op(vr_ctx* ctx, const double* in, double* out, const MultParams& m,
+                        const double* add = nullptr);
+void op_gradient(vr_ctx* ctx, const double* f, double* out3);
+void op_divergence(vr_ctx* ctx, const double* v3, double* out);
+void op_projection(vr_ctx* ctx, const double* in3, double* out3, int kind, double beta_v,
+                   double beta_w);
+void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm, int mode,
+            double beta, const double* add3 = nullptr);
+double reg_symbol(const vr_regnorm& n, double k2);
+
+// ---- semi-Lagrangian (sl.cu) ----
+void sl_tricubic(vr_ctx* ctx, const double* f, int nfields, const double* pts3, double* out);
+void sl_trace(vr_ctx* ctx, const double* v3, int nt, int direction, double* dep3);
+void sl_factor(vr_ctx* ctx, const double* div_v, const double* dep3, double half_dt,
+               double* factor);
+void sl_advect(vr_ctx* ctx, const double* f, const double* dep3, double* out);
+void sl_continuity(vr_ctx* ctx, const double* f, const double* dep3, const double* factor,
+                   double* out);
+// incremental state fused step: g = I[src](X); m = g - hdt*q(gm, vt);
+// mode 0: dst = m - hdt*q (next tmp); mode 1: dst = -m (terminal)
+void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double hdt,
+                       double* tmp0);
+void sl_incstate_step(vr_ctx* ctx, const double* src, const double* dep3, const double* gm,
+                      const double* vt3, double hdt, double* dst, int mode);
+// adjoint step with optional gradient accumulation b_a += (w*lam) * gm_a
+void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const double* factor,
+                     double* dst, const double* gm, double w, double* b3);
+void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const double* gm,
+                      double w, double* lam, double* b3);
+// b_a = sum_{j=nt..0} (w_j lam_j) d_a m_j
+void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, int nt, double dt,
+                   double* b3);
+void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out);
+void synth_fill(vr_ctx* ctx, double amplitude, double* m_T, double* v3);
+
+}  // namespace vr

@@ -1,0 +1,568 @@
+"""Python mirror of the reference's operator API, running on the sm_100a C ABI.
+
+Names, argument meaning and error behaviour follow the reference veloreg C++
+API (/root/reference/proj/include/veloreg/*.hpp) so parity tests read like the
+reference's own tests:
+
+* spectral.hpp  -> gradient, divergence, laplacian, helmholtz1_apply,
+  gaussian_smooth, apply_reg_operator, apply_projection, inner_product,
+  rescale_intensity
+* interp.hpp / transport.hpp -> tricubic_interpolate, trace_characteristics,
+  continuity_factor, solve_state, solve_adjoint, gradient_dot, solve_inc_state,
+  solve_inc_adjoint
+* objective.hpp -> Objective (evaluate / compute_gradient / hessian_matvec /
+  hessian_data_matvec / apply_reg / apply_K / counters / initial_mismatch)
+* solver.hpp -> compute_forcing, pcg_solve, gauss_newton_solve, plus
+  parameter_continuation
+
+Every call goes through libveloreg_gpu.so; host numpy arrays are copied to the
+device and back. Shapes: scalar (n1,n2,n3), vector (3,n1,n2,n3), time series
+(nt+1,n1,n2,n3); all float64, C-contiguous (the reference's layout).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (ArgumentError, DimensionError, LogicError, NumericError,  # noqa: F401
+                   ResourceError, VelouregError)
+
+_KIND = {"h1": _lib.REG_H1, "h2": _lib.REG_H2, "h3": _lib.REG_H3, "helmholtz": _lib.REG_HELMHOLTZ}
+_PROJ = {"identity": _lib.PROJ_IDENTITY, "incompressible": _lib.PROJ_INCOMPRESSIBLE,
+         "near_incompressible": _lib.PROJ_NEAR_INCOMPRESSIBLE}
+_MODE = {"apply": _lib.REGOP_APPLY, "inverse": _lib.REGOP_INVERSE,
+         "inverse_sqrt": _lib.REGOP_INVERSE_SQRT}
+
+
+def _enum(table, v):
+    return table[v] if isinstance(v, str) else int(v)
+
+
+def make_norm(kind="h2", gamma=1.0, helmholtz_squared=True, div_penalty=False, beta_w=1e-4):
+    """RegNorm (spectral.hpp:75-102)."""
+    return _lib.RegNorm(_enum(_KIND, kind), gamma, int(helmholtz_squared), int(div_penalty), beta_w)
+
+
+def make_model(kind="h2", beta_v=1e-2, nt=4, projection="identity", gamma=1.0,
+               helmholtz_squared=True, div_penalty=False, beta_w=1e-4, gauss_newton=True):
+    """RegModel (objective.hpp:11-23); defaults are the reference's."""
+    m = _lib.Model()
+    m.norm = make_norm(kind, gamma, helmholtz_squared, div_penalty, beta_w)
+    m.projection = _enum(_PROJ, projection)
+    m.beta_v = beta_v
+    m.nt = nt
+    m.gauss_newton = int(gauss_newton)
+    return m
+
+
+def make_params(**kw):
+    """SolverParams (solver.hpp:13-33) with keyword overrides."""
+    p = _lib.SolverParams()
+    _lib.load().vr_solver_params_default(C.byref(p))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise ArgumentError(f"SolverParams has no field {k}")
+        setattr(p, k, int(v) if isinstance(getattr(p, k), int) else v)
+    return p
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """One grid on one device with its own CUDA stream (vr_ctx)."""
+
+    def __init__(self, dims, device: int = 0):
+        if isinstance(dims, int):
+            dims = (dims, dims, dims)
+        self.dims = tuple(int(d) for d in dims)
+        self.N = self.dims[0] * self.dims[1] * self.dims[2]
+        self.nh = self.dims[2] // 2 + 1
+        h = C.c_void_p()
+        _lib.call("vr_ctx_create", self.dims[0], self.dims[1], self.dims[2], device, C.byref(h))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return _lib.load().vr_ctx_stream(self._h) or 0
+
+    def synchronize(self):
+        _lib.call("vr_ctx_synchronize", self._h)
+
+    def kernel_launches(self) -> int:
+        return int(_lib.load().vr_ctx_kernel_launches(self._h))
+
+    def reset_kernel_launches(self):
+        _lib.load().vr_ctx_reset_kernel_launches(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.call("vr_ctx_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- device arrays
+    def empty(self, nfields: int, complex_spectrum: bool = False) -> "DeviceArray":
+        return DeviceArray(self, nfields, complex_spectrum)
+
+    def to_device(self, arr) -> "DeviceArray":
+        if isinstance(arr, DeviceArray):
+            return arr
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        nf = a.size // self.N
+        if nf * self.N != a.size:
+            raise DimensionError(f"array of size {a.size} is not a whole number of {self.dims} fields")
+        d = DeviceArray(self, nf)
+        _lib.call("vr_memcpy_h2d", self._h, d.ptr, a.ctypes.data, a.nbytes)
+        return d
+
+
+class DeviceArray:
+    """`nfields` consecutive fp64 fields (or spectra) in HBM."""
+
+    def __init__(self, ctx: Context, nfields: int, complex_spectrum: bool = False):
+        self.ctx = ctx
+        self.nfields = nfields
+        self.spectrum = complex_spectrum
+        per = ctx.dims[0] * ctx.dims[1] * ctx.nh * 2 if complex_spectrum else ctx.N
+        self.count = per * nfields
+        self.nbytes = 8 * self.count
+        p = C.c_void_p()
+        _lib.call("vr_device_alloc", ctx.handle, max(self.nbytes, 8), C.byref(p))
+        self.ptr = p
+        _lib.call("vr_memset_zero", ctx.handle, p, max(self.nbytes, 8))
+
+    def numpy(self) -> np.ndarray:
+        out = np.empty(self.count, dtype=np.float64)
+        _lib.call("vr_memcpy_d2h", self.ctx.handle, out.ctypes.data, self.ptr, self.nbytes)
+        d = self.ctx.dims
+        if self.spectrum:
+            c = out.view(np.complex128)
+            return c.reshape((self.nfields, d[0], d[1], self.ctx.nh)) if self.nfields > 1 else c.reshape(d[0], d[1], self.ctx.nh)
+        return out.reshape((self.nfields,) + d) if self.nfields > 1 else out.reshape(d)
+
+    def upload(self, arr):
+        a = np.ascontiguousarray(arr, dtype=np.complex128 if self.spectrum else np.float64)
+        if a.nbytes != self.nbytes:
+            raise DimensionError("upload: size mismatch")
+        _lib.call("vr_memcpy_h2d", self.ctx.handle, self.ptr, a.ctypes.data, a.nbytes)
+
+    def field(self, i: int) -> C.c_void_p:
+        per = self.count // self.nfields
+        return C.c_void_p(self.ptr.value + 8 * per * i)
+
+    def free(self):
+        if getattr(self, "ptr", None) is not None and self.ctx._h:
+            _lib.call("vr_device_free", self.ctx.handle, self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _dev(ctx, a):
+    return a if isinstance(a, DeviceArray) else ctx.to_device(a)
+
+
+def _ret(out: DeviceArray, host: bool):
+    return out.numpy() if host else out
+
+
+def _is_host(*arrs):
+    return any(not isinstance(a, DeviceArray) for a in arrs)
+
+
+# ---- BLAS-1 / quadrature (field_ops.hpp, spectral.cpp:47-62) ------------------
+def inner_product(ctx, a, b) -> float:
+    da, db = _dev(ctx, a), _dev(ctx, b)
+    r = C.c_double()
+    _lib.call("vr_inner_product", ctx.handle, da.ptr, db.ptr, da.nfields, C.byref(r))
+    return r.value
+
+
+def dot_l2(ctx, a, b) -> float:
+    da, db = _dev(ctx, a), _dev(ctx, b)
+    r = C.c_double()
+    _lib.call("vr_dot_l2", ctx.handle, da.ptr, db.ptr, da.nfields, C.byref(r))
+    return r.value
+
+
+def norm_l2(ctx, a) -> float:
+    return float(np.sqrt(dot_l2(ctx, a, a)))
+
+
+def max_abs(ctx, a) -> float:
+    da = _dev(ctx, a)
+    r = C.c_double()
+    _lib.call("vr_max_abs", ctx.handle, da.ptr, da.nfields, C.byref(r))
+    return r.value
+
+
+def max_magnitude(ctx, v) -> float:
+    dv = _dev(ctx, v)
+    r = C.c_double()
+    _lib.call("vr_max_magnitude", ctx.handle, dv.ptr, C.byref(r))
+    return r.value
+
+
+# ---- spectral ----------------------------------------------------------------
+def fft_forward(ctx, f):
+    """fft_forward_raw (fft.cpp:66-73): unnormalized half spectrum (n1, n2, n3/2+1)."""
+    df = _dev(ctx, f)
+    out = ctx.empty(1, complex_spectrum=True)
+    _lib.call("vr_fft_r2c", ctx.handle, df.ptr, out.ptr)
+    return _ret(out, _is_host(f))
+
+
+def fft_inverse(ctx, spec):
+    """fft_inverse_raw (fft.cpp:75-83), includes the 1/N scale."""
+    if isinstance(spec, DeviceArray):
+        ds = spec
+    else:
+        ds = ctx.empty(1, complex_spectrum=True)
+        ds.upload(spec)
+    out = ctx.empty(1)
+    _lib.call("vr_fft_c2r", ctx.handle, ds.ptr, out.ptr)
+    return _ret(out, _is_host(spec))
+
+
+def gradient(ctx, f):
+    df = _dev(ctx, f)
+    out = ctx.empty(3)
+    _lib.call("vr_gradient", ctx.handle, df.ptr, out.ptr)
+    return _ret(out, _is_host(f))
+
+
+def divergence(ctx, v):
+    dv = _dev(ctx, v)
+    out = ctx.empty(1)
+    _lib.call("vr_divergence", ctx.handle, dv.ptr, out.ptr)
+    return _ret(out, _is_host(v))
+
+
+def laplacian(ctx, f):
+    df = _dev(ctx, f)
+    out = ctx.empty(df.nfields)
+    _lib.call("vr_laplacian", ctx.handle, df.ptr, out.ptr, df.nfields)
+    return _ret(out, _is_host(f))
+
+
+def helmholtz1_apply(ctx, f):
+    df = _dev(ctx, f)
+    out = ctx.empty(1)
+    _lib.call("vr_helmholtz1_apply", ctx.handle, df.ptr, out.ptr)
+    return _ret(out, _is_host(f))
+
+
+def gaussian_smooth(ctx, f, sigma_voxels: Sequence[float]):
+    df = _dev(ctx, f)
+    out = ctx.empty(df.nfields)
+    sig = (C.c_double * 3)(*[float(s) for s in sigma_voxels])
+    _lib.call("vr_gaussian_smooth", ctx.handle, df.ptr, out.ptr, df.nfields, sig)
+    return _ret(out, _is_host(f))
+
+
+def apply_reg_operator(ctx, v, norm=None, mode="apply", beta=1.0):
+    dv = _dev(ctx, v)
+    out = ctx.empty(3)
+    norm = norm if norm is not None else make_norm()
+    _lib.call("vr_apply_reg_operator", ctx.handle, dv.ptr, out.ptr, C.byref(norm),
+              _enum(_MODE, mode), beta)
+    return _ret(out, _is_host(v))
+
+
+def apply_projection(ctx, v, kind="incompressible", beta_v=0.0, beta_w=0.0):
+    dv = _dev(ctx, v)
+    out = ctx.empty(3)
+    _lib.call("vr_apply_projection", ctx.handle, dv.ptr, out.ptr, _enum(_PROJ, kind), beta_v, beta_w)
+    return _ret(out, _is_host(v))
+
+
+def rescale_intensity(ctx, f):
+    df = _dev(ctx, f)
+    out = ctx.empty(1)
+    deg = C.c_int()
+    _lib.call("vr_rescale_intensity", ctx.handle, df.ptr, out.ptr, C.byref(deg))
+    return _ret(out, _is_host(f)), bool(deg.value)
+
+
+# ---- transport -------------------------------------------------------------------
+def tricubic_interpolate(ctx, f, points):
+    df, dp = _dev(ctx, f), _dev(ctx, points)
+    out = ctx.empty(df.nfields)
+    _lib.call("vr_tricubic_interpolate", ctx.handle, df.ptr, dp.ptr, out.ptr, df.nfields)
+    return _ret(out, _is_host(f, points))
+
+
+def trace_characteristics(ctx, v, nt, direction="backward"):
+    dv = _dev(ctx, v)
+    out = ctx.empty(3)
+    d = _lib.TRACE_BACKWARD if direction == "backward" else _lib.TRACE_FORWARD
+    _lib.call("vr_trace_characteristics", ctx.handle, dv.ptr, nt, d, out.ptr)
+    return _ret(out, _is_host(v))
+
+
+def continuity_factor(ctx, div_v, departure, dt):
+    dd, dp = _dev(ctx, div_v), _dev(ctx, departure)
+    out = ctx.empty(1)
+    _lib.call("vr_continuity_factor", ctx.handle, dd.ptr, dp.ptr, dt, out.ptr)
+    return _ret(out, _is_host(div_v, departure))
+
+
+def solve_state(ctx, m_T, v, nt):
+    dm, dv = _dev(ctx, m_T), _dev(ctx, v)
+    out = ctx.empty(nt + 1)
+    _lib.call("vr_solve_state", ctx.handle, dm.ptr, dv.ptr, nt, out.ptr)
+    return _ret(out, _is_host(m_T, v))
+
+
+def solve_adjoint(ctx, terminal, v, nt, needs_history=False):
+    dt_, dv = _dev(ctx, terminal), _dev(ctx, v)
+    init = ctx.empty(1)
+    hist = ctx.empty(nt + 1) if needs_history else None
+    _lib.call("vr_solve_adjoint", ctx.handle, dt_.ptr, dv.ptr, nt, hist.ptr if hist else None, init.ptr)
+    host = _is_host(terminal, v)
+    return _ret(init, host), (_ret(hist, host) if hist else None)
+
+
+def solve_inc_adjoint(ctx, terminal, v, nt, needs_history=False):
+    dt_, dv = _dev(ctx, terminal), _dev(ctx, v)
+    init = ctx.empty(1)
+    hist = ctx.empty(nt + 1) if needs_history else None
+    _lib.call("vr_solve_inc_adjoint", ctx.handle, dt_.ptr, dv.ptr, nt, hist.ptr if hist else None, init.ptr)
+    host = _is_host(terminal, v)
+    return _ret(init, host), (_ret(hist, host) if hist else None)
+
+
+def gradient_dot(ctx, f, w):
+    df, dw = _dev(ctx, f), _dev(ctx, w)
+    out = ctx.empty(1)
+    _lib.call("vr_gradient_dot", ctx.handle, df.ptr, dw.ptr, out.ptr)
+    return _ret(out, _is_host(f, w))
+
+
+def solve_inc_state(ctx, m_history, v, v_tilde, nt):
+    dm, dv, dvt = _dev(ctx, m_history), _dev(ctx, v), _dev(ctx, v_tilde)
+    if dm.nfields != nt + 1:
+        raise DimensionError(f"solve_inc_state: m_history has {dm.nfields} slices, expected {nt + 1}")
+    out = ctx.empty(nt + 1)
+    _lib.call("vr_solve_inc_state", ctx.handle, dm.ptr, dv.ptr, dvt.ptr, nt, out.ptr)
+    return _ret(out, _is_host(m_history, v, v_tilde))
+
+
+def generate_synthetic(ctx, nt, amplitude=1.0, host=True):
+    """generate_synthetic (synthetic.cpp:16-34) on the device: (m_R, m_T, v_star)."""
+    mR, mT, vs = ctx.empty(1), ctx.empty(1), ctx.empty(3)
+    _lib.call("vr_generate_synthetic", ctx.handle, nt, amplitude, mR.ptr, mT.ptr, vs.ptr)
+    return (mR.numpy(), mT.numpy(), vs.numpy()) if host else (mR, mT, vs)
+
+
+# ---- objective -----------------------------------------------------------------
+class EvalState:
+    """EvalState<T> (objective.hpp:37-54); device resident."""
+
+    def __init__(self, obj: "Objective", handle):
+        self.obj = obj
+        self._h = handle
+
+    def _scalars(self):
+        J, mis, rel = C.c_double(), C.c_double(), C.c_double()
+        hg, hc = C.c_int(), C.c_int()
+        _lib.call("vr_state_scalars", self._h, C.byref(J), C.byref(mis), C.byref(rel), C.byref(hg), C.byref(hc))
+        return J.value, mis.value, rel.value, bool(hg.value), bool(hc.value)
+
+    objective = property(lambda s: s._scalars()[0])
+    mismatch = property(lambda s: s._scalars()[1])
+    mismatch_rel = property(lambda s: s._scalars()[2])
+    has_gradient = property(lambda s: s._scalars()[3])
+    has_adjoint_ctx = property(lambda s: s._scalars()[4])
+
+    def get(self, which: int, host=True):
+        ctx = self.obj.ctx
+        nt = self.obj.model.nt
+        nf = {_lib.STATE_V: 3, _lib.STATE_X_BWD: 3, _lib.STATE_X_FWD: 3, _lib.STATE_FACTOR: 1,
+              _lib.STATE_M_HISTORY: nt + 1, _lib.STATE_GRADIENT: 3,
+              _lib.STATE_GRAD_M: 3 * (nt + 1)}[which]
+        out = ctx.empty(nf)
+        _lib.call("vr_state_get", self._h, which, out.ptr)
+        return out.numpy() if host else out
+
+    @property
+    def gradient(self):
+        return self.get(_lib.STATE_GRADIENT)
+
+    @property
+    def m_history(self):
+        return self.get(_lib.STATE_M_HISTORY)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.call("vr_state_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Objective:
+    """Objective<double> (objective.hpp:56-102) over device-resident images."""
+
+    def __init__(self, ctx: Context, m_R, m_T, model=None):
+        self.ctx = ctx
+        self.model = model if model is not None else make_model()
+        self._mR = _dev(ctx, m_R)  # kept alive: the C object holds non-owning pointers
+        self._mT = _dev(ctx, m_T)
+        h = C.c_void_p()
+        _lib.call("vr_objective_create", ctx.handle, self._mR.ptr, self._mT.ptr, C.byref(self.model), C.byref(h))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def initial_mismatch(self) -> float:
+        r = C.c_double()
+        _lib.call("vr_objective_initial_mismatch", self._h, C.byref(r))
+        return r.value
+
+    def counters(self) -> dict:
+        c = _lib.Counters()
+        _lib.call("vr_objective_counters", self._h, C.byref(c))
+        return {k: getattr(c, k) for k, _ in _lib.Counters._fields_}
+
+    def evaluate(self, v) -> EvalState:
+        dv = _dev(self.ctx, v)
+        h = C.c_void_p()
+        _lib.call("vr_evaluate", self._h, dv.ptr, C.byref(h))
+        return EvalState(self, h)
+
+    def compute_gradient(self, state: EvalState):
+        _lib.call("vr_compute_gradient", self._h, state._h, None)
+
+    def hessian_matvec(self, state: EvalState, v_tilde, out: Optional[DeviceArray] = None):
+        dv = _dev(self.ctx, v_tilde)
+        o = out if out is not None else self.ctx.empty(3)
+        _lib.call("vr_hessian_matvec", self._h, state._h, dv.ptr, o.ptr)
+        return _ret(o, _is_host(v_tilde) and out is None)
+
+    def hessian_data_matvec(self, state: EvalState, v_tilde):
+        dv = _dev(self.ctx, v_tilde)
+        o = self.ctx.empty(3)
+        _lib.call("vr_hessian_data_matvec", self._h, state._h, dv.ptr, o.ptr)
+        return _ret(o, _is_host(v_tilde))
+
+    def hessian_matvec_host(self, state: EvalState, vt_host: np.ndarray, out_host: np.ndarray):
+        """End-to-end entry: host buffers in/out (H2D + matvec + D2H)."""
+        _lib.call("vr_hessian_matvec_host", self._h, state._h, vt_host.ctypes.data, out_host.ctypes.data)
+        return out_host
+
+    def apply_reg(self, u, mode="apply"):
+        du = _dev(self.ctx, u)
+        o = self.ctx.empty(3)
+        _lib.call("vr_objective_apply_reg", self._h, du.ptr, _enum(_MODE, mode), o.ptr)
+        return _ret(o, _is_host(u))
+
+    def apply_K(self, u):
+        du = _dev(self.ctx, u)
+        o = self.ctx.empty(3)
+        _lib.call("vr_objective_apply_K", self._h, du.ptr, o.ptr)
+        return _ret(o, _is_host(u))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.call("vr_objective_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- solvers --------------------------------------------------------------------
+def compute_forcing(grad_norm, grad0_norm) -> float:
+    r = C.c_double()
+    _lib.call("vr_compute_forcing", grad_norm, grad0_norm, C.byref(r))
+    return r.value
+
+
+def pcg_solve(obj: Objective, state: EvalState, rhs, rel_tol, max_iter, precond="spectral"):
+    ctx = obj.ctx
+    drhs = _dev(ctx, rhs)
+    x = ctx.empty(3)
+    st = _lib.PcgStats()
+    pc = _lib.PRECOND_SPECTRAL if precond == "spectral" else _lib.PRECOND_NONE
+    _lib.call("vr_pcg_solve", obj.handle, state._h, drhs.ptr, rel_tol, max_iter, pc, x.ptr, C.byref(st))
+    stats = {k: getattr(st, k) for k, _ in _lib.PcgStats._fields_}
+    return _ret(x, _is_host(rhs)), stats
+
+
+@dataclass
+class SolveResult:
+    v: np.ndarray
+    report: dict
+    records: List[dict] = field(default_factory=list)
+
+
+def _report_dict(r: _lib.SolveReport) -> dict:
+    d = {k: getattr(r, k) for k, _ in _lib.SolveReport._fields_ if k not in ("fine", "coarse")}
+    d["stop_name"] = _lib.STOP_NAMES[r.stop]
+    for nm in ("fine", "coarse"):
+        c = getattr(r, nm)
+        d[nm] = {k: getattr(c, k) for k, _ in _lib.Counters._fields_}
+    return d
+
+
+def _records(recs, n) -> List[dict]:
+    return [{k: getattr(recs[i], k) for k, _ in _lib.IterationRecord._fields_} for i in range(n)]
+
+
+def gauss_newton_solve(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral",
+                       max_records=512):
+    """gauss_newton_solve (solver.hpp:159-164) with the C++ host driver."""
+    model = model if model is not None else make_model()
+    params = params if params is not None else make_params()
+    dR, dT, dv0 = _dev(ctx, m_R), _dev(ctx, m_T), _dev(ctx, v0)
+    vout = ctx.empty(3)
+    rep = _lib.SolveReport()
+    recs = (_lib.IterationRecord * max_records)()
+    pc = _lib.PRECOND_SPECTRAL if precond == "spectral" else _lib.PRECOND_NONE
+    _lib.call("vr_gauss_newton_solve", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
+              C.byref(params), pc, vout.ptr, C.byref(rep), recs, max_records)
+    return SolveResult(vout.numpy(), _report_dict(rep), _records(recs, min(rep.n_records, max_records)))
+
+
+def parameter_continuation(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral",
+                           max_levels=16, max_records=1024):
+    """beta_v continuation 1, 1e-1, ..., target with warm starts."""
+    model = model if model is not None else make_model()
+    params = params if params is not None else make_params()
+    dR, dT, dv0 = _dev(ctx, m_R), _dev(ctx, m_T), _dev(ctx, v0)
+    vout = ctx.empty(3)
+    reps = (_lib.SolveReport * max_levels)()
+    recs = (_lib.IterationRecord * max_records)()
+    nl = C.c_int()
+    pc = _lib.PRECOND_SPECTRAL if precond == "spectral" else _lib.PRECOND_NONE
+    _lib.call("vr_parameter_continuation", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
+              C.byref(params), pc, vout.ptr, reps, max_levels, C.byref(nl), recs, max_records)
+    reports = [_report_dict(reps[i]) for i in range(min(nl.value, max_levels))]
+    nrec = sum(r["n_records"] for r in reports)
+    return vout.numpy(), reports, _records(recs, min(nrec, max_records))

@@ -1,0 +1,141 @@
+"""GPU parity: Objective (evaluate / reduced gradient / GN Hessian matvec) vs the compiled reference.
+
+Reference: proj/src/objective.cpp:35-186, tests proj/tests/test_objective.cpp.
+Per-operator bar: relative L2 <= 1e-10 (fp64).
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+MODELS = {
+    "h2_default": dict(kind="h2", beta_v=1e-2, nt=4),
+    "h1div_nearinc": dict(kind="h1", beta_v=1e-3, nt=4, div_penalty=True, beta_w=1e-4,
+                          projection="near_incompressible"),
+    "h1_leray": dict(kind="h1", beta_v=1e-2, nt=4, projection="incompressible"),
+    "helmholtz": dict(kind="helmholtz", gamma=0.5, beta_v=5e-2, nt=2),
+    "h3_nt8": dict(kind="h3", beta_v=1e-3, nt=8),
+}
+
+
+def image_pair(ref, dims, max_mode, seed):
+    # test_objective.cpp:22-33
+    a = 0.5 + ref.random_smooth_scalar(dims, max_mode, seed, 0.3)
+    b = 0.5 + ref.random_smooth_scalar(dims, max_mode, seed + 1, 0.3)
+    return a, b
+
+
+@pytest.mark.parametrize("name", list(MODELS))
+@pytest.mark.parametrize("dims", [(16, 16, 16), (32, 16, 32)])
+def test_objective_parity(vr, ref, ctx, name, dims):
+    c = ctx(dims)
+    kw = MODELS[name]
+    model = vr.make_model(**kw)
+    mR, mT = image_pair(ref, dims, 2, 91)
+    v = ref.random_smooth_vector(dims, 2, 120, 0.3)
+    if kw.get("projection") == "incompressible":
+        v = ref.apply_projection(v, 1)
+    vt = ref.random_smooth_vector(dims, 2, 142, 1.0)
+
+    ro = ref.Objective(mR, mT, model)
+    go = vr.Objective(c, mR, mT, model)
+    assert abs(go.initial_mismatch() - ro.initial_mismatch()) <= 1e-12 * ro.initial_mismatch()
+
+    rs = ro.evaluate(v)
+    gs = go.evaluate(v)
+    sc = rs.scalars()
+    assert abs(gs.objective - sc["objective"]) <= 1e-10 * abs(sc["objective"])
+    assert abs(gs.mismatch - sc["mismatch"]) <= 1e-10 * abs(sc["mismatch"])
+    assert abs(gs.mismatch_rel - sc["mismatch_rel"]) <= 1e-10 * abs(sc["mismatch_rel"])
+    assert rel_l2(gs.m_history, rs.get(4)) < TOL
+
+    g_ref = ro.compute_gradient(rs)
+    go.compute_gradient(gs)
+    assert gs.has_gradient and gs.has_adjoint_ctx
+    assert rel_l2(gs.gradient, g_ref) < TOL
+    assert rel_l2(gs.get(3), rs.get(3)) < TOL  # continuity factor
+
+    assert rel_l2(go.hessian_matvec(gs, vt), ro.hessian_matvec(rs, vt)) < TOL
+    assert rel_l2(go.hessian_data_matvec(gs, vt), ro.hessian_data_matvec(rs, vt)) < TOL
+    for mode in (0, 1, 2):
+        assert rel_l2(go.apply_reg(vt, mode), ro.apply_reg(vt, mode)) < TOL
+    assert rel_l2(go.apply_K(vt), ro.apply_K(vt)) < TOL
+    assert go.counters() == ro.counters()
+
+
+def test_counters_and_pure_reg_limit(vr, ref, ctx):
+    # test_objective.cpp:160-184
+    dims = (16, 16, 16)
+    c = ctx(dims)
+    m = np.full(dims, 0.5)
+    model = vr.make_model("h2", beta_v=2.5e-3, nt=4)
+    o = vr.Objective(c, m, m, model)
+    s = o.evaluate(np.zeros((3,) + dims))
+    o.compute_gradient(s)
+    assert o.counters()["pde_solves"] == 2
+    vt = ref.random_smooth_vector(dims, 2, 90, 1.0)
+    hv = o.hessian_matvec(s, vt)
+    assert o.counters()["pde_solves"] == 4
+    reg = vr.apply_reg_operator(c, vt, model.norm, "apply", model.beta_v)
+    assert np.abs(hv - reg).max() < 1e-14
+    assert np.abs(o.hessian_matvec(s, np.zeros((3,) + dims))).max() == 0.0
+
+
+def test_gn_symmetry_psd(vr, ref, ctx):
+    # test_objective.cpp:186-215 on the GPU path
+    dims = (16, 16, 16)
+    c = ctx(dims)
+    mR, mT = image_pair(ref, dims, 2, 91)
+    o = vr.Objective(c, mR, mT, vr.make_model("h2", beta_v=1e-3, nt=4))
+    s0 = o.evaluate(np.zeros((3,) + dims))
+    o.compute_gradient(s0)
+    for probe in range(3):
+        u = ref.random_smooth_vector(dims, 2, 100 + 2 * probe, 1.0)
+        w = ref.random_smooth_vector(dims, 2, 101 + 2 * probe, 1.0)
+        Hu, Hw = o.hessian_matvec(s0, u), o.hessian_matvec(s0, w)
+        a, b = vr.inner_product(c, Hu, w), vr.inner_product(c, u, Hw)
+        assert abs(a - b) / max(abs(a), abs(b)) < 1e-6
+        q = vr.inner_product(c, Hu, u)
+        assert q >= -1e-10 * max(1.0, abs(q))
+
+
+def test_objective_errors(vr, ref, ctx):
+    dims = (16, 16, 16)
+    c = ctx(dims)
+    mR, mT = image_pair(ref, dims, 2, 51)
+    o = vr.Objective(c, mR, mT, vr.make_model())
+    v = np.zeros((3,) + dims)
+    v[1, 0, 0, 7] = np.nan
+    with pytest.raises(vr.NumericError):
+        o.evaluate(v)
+    s = o.evaluate(np.zeros((3,) + dims))
+    with pytest.raises(vr.LogicError):
+        o.hessian_matvec(s, np.ones((3,) + dims))
+    o.compute_gradient(s)
+    bad = np.ones((3,) + dims)
+    bad[2, 1, 1, 1] = np.inf
+    with pytest.raises(vr.NumericError):
+        o.hessian_matvec(s, bad)
+    with pytest.raises(vr.ArgumentError):
+        vr.Objective(c, mR, mT, vr.make_model(beta_v=-1.0))
+
+
+def test_matvec_host_entry(vr, ref, ctx):
+    dims = (32, 32, 32)
+    c = ctx(dims)
+    mR, mT, vs = ref.generate_synthetic(dims, 4)
+    model = vr.make_model()
+    o = vr.Objective(c, mR, mT, model)
+    s = o.evaluate(vs)
+    o.compute_gradient(s)
+    vt = ref.random_smooth_vector(dims, 2, 142, 1.0)
+    out = np.empty_like(vt)
+    o.hessian_matvec_host(s, vt, out)
+    ro = ref.Objective(mR, mT, model)
+    rs = ro.evaluate(vs)
+    ro.compute_gradient(rs)
+    assert rel_l2(out, ro.hessian_matvec(rs, vt)) < TOL
