@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- Gauss-Newton Hessian matvec throughput on B200 (BASELINE config 3).
+
+Workload (BASELINE.json configs[2], the 1-GPU config the metric is quoted on):
+256^3 seeded ellipsoid phantom, band-limited random stationary velocity
+(|k| <= 6, max displacement 0.08*2pi), H2 regularization, beta_v = 1e-2,
+n_t = 4, Gauss-Newton, K = identity. A "step" is one reduced-space GN Hessian
+matvec H vt (objective.cpp:114-156) at the generating velocity, with the
+EvalState (state, adjoint context, grad m cache) frozen as in a PCG solve.
+
+Arms:
+  default           our sm_100a path through the C ABI (libveloreg_gpu.so)
+  --impl reference  the reference C++ code (oracle/_ref, compiled unmodified
+                    from /root/reference/proj/src) on the host cores, rank 0 only
+
+Multi-GPU (torchrun, N > 1): the slab-sharded matvec is not built yet, so each
+rank runs an independent replica of the workload on its own GPU ("scaling":
+"weak"; value = all ranks' matvecs / max-over-ranks time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Hessian matvecs/s"
+UNIT = "matvec/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256, help="grid size (default: config 3, 256^3)")
+    ap.add_argument("--nt", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=90.0,
+                    help="wall budget for the reference arm's timed matvecs")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(n, nt):
+    from paper_1808_04487_b200 import phantom
+    cfg = phantom.CONFIGS[3]
+    m_T = phantom.ellipsoid_phantom(n)
+    v = phantom.bandlimited_velocity(n, cfg["kmax"], cfg["disp"])
+    vt = phantom.bandlimited_direction(n)
+    desc = (f"config3: {n}^3 ellipsoid phantom (40, seed 1808, sigma 2 vox), band-limited v "
+            f"(|k|<=6, max disp 0.08*2pi, seed 4487), GN Hessian matvec at v, H2 beta_v=1e-2, "
+            f"n_t={nt}, K=identity, spectral-precond solve setting")
+    return m_T, v, vt, desc
+
+
+def bytes_model(n, nt):
+    """Algorithmic bytes with F = 8N and F_c = 16 n^2 (n/2+1)."""
+    N = n ** 3
+    F = 8.0 * N
+    Fc = 16.0 * n * n * (n // 2 + 1)
+    per_matvec = 8.0 * N * (9 + 8 * (nt + 1) + 12 * nt) + 6 * Fc
+    per_launch = {
+        # our kernels' compulsory traffic per launch
+        "sl_incstate_step": 11 * F,   # X 3F + gather src 1F + grad m 3F + vt 3F + write 1F
+        "sl_adjoint_step": 6 * F,     # X 3F + gather src 1F + factor 1F + write 1F
+        "sl_accumulate": (4 * (nt + 1) + 3) * F,
+        "sl_pointwise": 7 * F,
+        "fft_x3_r2c": F + Fc,
+        "fft_axis": 2 * Fc,
+        "fft_x1_mult": 2 * Fc,
+        "fft_x3_c2r": Fc + 2 * F,     # spectrum in, add-field in, real out
+    }
+    return per_matvec, per_launch
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, p[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+def run_reference_matvecs(m_R, m_T, v, vt, nt, steps, warmup, budget_s):
+    """Reference CPU arm: the compiled reference (oracle/_ref) on the host cores."""
+    from oracle import ref
+    import paper_1808_04487_b200.veloreg as V
+    cores = os.cpu_count() or 1
+    ref.set_workers(cores)
+    model = V.make_model("h2", beta_v=1e-2, nt=nt)
+    t0 = time.perf_counter()
+    obj = ref.Objective(m_R, m_T, model)
+    s = obj.evaluate(v)
+    obj.compute_gradient(s)
+    setup = time.perf_counter() - t0
+    for _ in range(warmup):
+        obj.hessian_matvec(s, vt)
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(max(1, steps)):
+        t = time.perf_counter()
+        obj.hessian_matvec(s, vt)
+        times.append(time.perf_counter() - t)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    total = sum(times)
+    return {"value": len(times) / total, "steps": len(times), "seconds": total, "cores": cores,
+            "setup_s": setup}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    n, nt = args.n, args.nt
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        m_T, v, vt, desc = workload(n, nt)
+        from oracle import ref
+        ref.set_workers(os.cpu_count() or 1)
+        m_R = ref.solve_state(m_T, v, nt)[-1]
+        r = run_reference_matvecs(m_R, m_T, v, vt, nt, args.steps, min(args.warmup, 1), args.ref_budget_s)
+        sample = (f"{r['steps']} GN Hessian matvec(s) at {n}^3 after 1 untimed warm-up matvec and an "
+                  f"untimed evaluate+gradient ({r['setup_s']:.1f}s); capped at {args.ref_budget_s:.0f}s")
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": r["steps"],
+                "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * r["seconds"] / r["steps"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "impl": "reference",
+                "config": {"workload": desc, "grid": n, "nt": nt},
+                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import paper_1808_04487_b200 as vr
+    import paper_1808_04487_b200.veloreg as V
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = local
+
+    m_T, v, vt, desc = workload(n, nt)
+    ctx = vr.Context(n, device=dev)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev))
+    d_mT = ctx.to_device(m_T)
+    d_v = ctx.to_device(v)
+    d_vt = ctx.to_device(vt)
+    hist = V.solve_state(ctx, d_mT, d_v, nt)                       # m_R = m_T transported by v
+    d_mR = ctx.empty(1)
+    _ = V._lib.call("vr_memcpy_d2d", ctx.handle, d_mR.ptr, hist.field(nt), 8 * ctx.N)
+    model = V.make_model("h2", beta_v=1e-2, nt=nt)
+    obj = V.Objective(ctx, d_mR, d_mT, model)
+    st = obj.evaluate(d_v)
+    obj.compute_gradient(st)
+    out = ctx.empty(3)
+
+    for _ in range(max(3, args.warmup)):
+        obj.hessian_matvec(st, d_vt, out=out)
+    ctx.synchronize()
+
+    # ---- timed region: device-resident inputs ------------------------------
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ctx.set_profiling(True)
+    l0 = ctx.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            obj.hessian_matvec(st, d_vt, out=out)
+        e1.record(stream)
+        e1.synchronize()
+    launches = ctx.kernel_launches() - l0
+    prof = ctx.profile_read()
+    ctx.set_profiling(False)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public C ABI with host buffers -------------
+    e2e = None
+    if not args.no_e2e:
+        nbytes = 3 * ctx.N * 8
+        hp_in, hp_out = V.C.c_void_p(), V.C.c_void_p()
+        V._lib.call("vr_host_alloc_pinned", nbytes, V.C.byref(hp_in))
+        V._lib.call("vr_host_alloc_pinned", nbytes, V.C.byref(hp_out))
+        h_in = np.ctypeslib.as_array((V.C.c_double * (3 * ctx.N)).from_address(hp_in.value))
+        h_out = np.ctypeslib.as_array((V.C.c_double * (3 * ctx.N)).from_address(hp_out.value))
+        h_in[:] = vt.ravel()
+        obj.hessian_matvec_host(st, h_in, h_out)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        k_e2e = max(3, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(k_e2e):
+            obj.hessian_matvec_host(st, h_in, h_out)
+        e1.record(stream)
+        e1.synchronize()
+        ms_e2e = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms_e2e], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": world * k_e2e / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": k_e2e,
+               "path": "vr_hessian_matvec_host (pinned host vt in, H vt out)"}
+        V._lib.call("vr_host_free_pinned", hp_in)
+        V._lib.call("vr_host_free_pinned", hp_out)
+
+    # ---- roofline of the dominant kernel ------------------------------------
+    peak, peak_kind = measured_peak()
+    per_matvec_bytes, per_launch = bytes_model(n, nt)
+    kernels = {k: {"launches": c, "total_ms": t, "avg_ms": t / c if c else None,
+                   "share": t / ms if ms else None} for k, (c, t) in prof.items()}
+    dom = max((k for k in prof if k in per_launch), key=lambda k: prof[k][1], default=None)
+    roof = None
+    if dom is not None:
+        c, t = prof[dom]
+        avg_s = t / c / 1e3
+        ach = per_launch[dom] / avg_s / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None, "peak_source": peak_kind,
+                "bytes_per_launch": per_launch[dom], "avg_launch_ms": t / c}
+    matvec_roof = {"bytes_per_matvec": per_matvec_bytes,
+                   "achieved_GBps": per_matvec_bytes / (ms_per_step / 1e3) / 1e9,
+                   "frac_of_peak": per_matvec_bytes / (ms_per_step / 1e3) / 1e9 / peak}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            m_R_host = d_mR.numpy()
+            r = run_reference_matvecs(m_R_host, m_T, v, vt, nt, 1, 0, 60.0)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
+                   "sample": f"1 GN Hessian matvec at {n}^3 by the compiled reference (oracle/_ref) after "
+                             f"an untimed evaluate+gradient ({r['setup_s']:.1f}s)"}
+        except Exception as exc:  # the oracle must be built; report instead of dying
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "grid": n, "nt": nt, "l2": "inputs larger than L2 (each fp64 field "
+                           f"{8 * n ** 3 / 2 ** 20:.0f} MiB; ~{int(per_matvec_bytes / 8 / n ** 3)} fields touched per step)",
+                           "parallelism": "replicas" if world > 1 else "single"},
+                "e2e": e2e, "gpu_launches": launches, "roofline": roof, "matvec_roofline": matvec_roof,
+                "kernels": kernels, "cpu_baseline": cpu, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -143,6 +143,8 @@ SIGNATURES = {
     "vr_ctx_grid": (I, [P, C.POINTER(C.c_int)]),
     "vr_ctx_kernel_launches": (C.c_longlong, [P]),
     "vr_ctx_reset_kernel_launches": (None, [P]),
+    "vr_ctx_set_profiling": (I, [P, I]),
+    "vr_ctx_profile_read": (I, [P, C.c_char_p, C.c_size_t]),
     "vr_device_alloc": (I, [P, C.c_size_t, C.POINTER(P)]),
     "vr_device_free": (I, [P, P]),
     "vr_host_alloc_pinned": (I, [C.c_size_t, C.POINTER(P)]),

@@ -120,11 +120,8 @@ template <RedOp OP>
 void reduce(vr_ctx* ctx, const double* a, const double* b, long long n, int ncomp,
             double* host_out) {
     const int nb = static_cast<int>(std::min<long long>(kRedBlocks, (n + kRedThreads - 1) / kRedThreads));
-    k_reduce<OP><<<dim3(nb, ncomp), kRedThreads, 0, ctx->stream>>>(a, b, n, ctx->red_partials);
-    check_launch();
-    k_finalize<is_max<OP>()><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nb, ctx->red_out);
-    check_launch();
-    count_launch(ctx, 2);
+    VR_LAUNCH(ctx, "reduce", k_reduce<OP><<<dim3(nb, ncomp), kRedThreads, 0, ctx->stream>>>(a, b, n, ctx->red_partials));
+    VR_LAUNCH(ctx, "reduce", k_finalize<is_max<OP>()><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nb, ctx->red_out););
     VR_CUDA(cudaMemcpyAsync(ctx->red_host, ctx->red_out, sizeof(double) * ncomp,
                             cudaMemcpyDeviceToHost, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -138,25 +135,17 @@ unsigned ew_grid(long long n) {
 }  // namespace
 
 void scale(vr_ctx* ctx, double* x, long long n, double a) {
-    k_scale<<<ew_grid(n), 256, 0, ctx->stream>>>(x, n, a);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "blas1", k_scale<<<ew_grid(n), 256, 0, ctx->stream>>>(x, n, a););
 }
 void add_scaled(vr_ctx* ctx, double* y, double a, const double* x, long long n) {
-    k_add_scaled<<<ew_grid(n), 256, 0, ctx->stream>>>(y, a, x, n);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "blas1", k_add_scaled<<<ew_grid(n), 256, 0, ctx->stream>>>(y, a, x, n););
 }
 void lin_comb(vr_ctx* ctx, double* out, double a, const double* x, double b, const double* y,
               long long n) {
-    k_lin_comb<<<ew_grid(n), 256, 0, ctx->stream>>>(out, a, x, b, y, n);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "blas1", k_lin_comb<<<ew_grid(n), 256, 0, ctx->stream>>>(out, a, x, b, y, n););
 }
 void affine(vr_ctx* ctx, const double* x, double* out, long long n, double lo, double s) {
-    k_affine<<<ew_grid(n), 256, 0, ctx->stream>>>(x, out, n, lo, s);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "blas1", k_affine<<<ew_grid(n), 256, 0, ctx->stream>>>(x, out, n, lo, s););
 }
 void dot_components(vr_ctx* ctx, const double* a, const double* b, long long n, int ncomp,
                     double* results) {
@@ -194,9 +183,7 @@ double max_value(vr_ctx* ctx, const double* a, long long n) {
     return r;
 }
 void finalize_sums(vr_ctx* ctx, int nblocks, int ncomp, double* host_out) {
-    k_finalize<false><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nblocks, ctx->red_out);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "blas1", k_finalize<false><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nblocks, ctx->red_out););
     VR_CUDA(cudaMemcpyAsync(ctx->red_host, ctx->red_out, sizeof(double) * ncomp,
                             cudaMemcpyDeviceToHost, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));

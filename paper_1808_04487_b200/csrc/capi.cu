@@ -3,6 +3,7 @@
 // (errors.hpp:9-17) plus a thread-local message, so a C++ adapter can rethrow
 // the reference's typed exception.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -58,6 +59,15 @@ double* spec_buf(vr_ctx* ctx, int i) {
     }
     return ctx->spec_scratch[i];
 }
+cudaEvent_t prof_event(vr_ctx* ctx) {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        VR_CUDA(cudaEventCreate(&e));
+        ctx->ev_pool.push_back(e);
+    }
+    return ctx->ev_pool[ctx->ev_used++];
+}
+
 double* field_buf(vr_ctx* ctx, int i) {
     if (static_cast<int>(ctx->field_scratch.size()) <= i) ctx->field_scratch.resize(i + 1, nullptr);
     if (!ctx->field_scratch[i]) {
@@ -171,6 +181,7 @@ int vr_ctx_destroy(vr_ctx* ctx) {
         vr::fft_plan_destroy(ctx);
         for (double* p : ctx->spec_scratch) cudaFree(p);
         for (double* p : ctx->field_scratch) cudaFree(p);
+        for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         cudaFree(ctx->red_partials);
         cudaFree(ctx->red_out);
         cudaFreeHost(ctx->red_host);
@@ -198,6 +209,47 @@ int vr_ctx_grid(const vr_ctx* ctx, int dims[3]) {
 long long vr_ctx_kernel_launches(const vr_ctx* ctx) { return ctx ? ctx->launches : 0; }
 void vr_ctx_reset_kernel_launches(vr_ctx* ctx) {
     if (ctx) ctx->launches = 0;
+}
+
+int vr_ctx_set_profiling(vr_ctx* ctx, int on) {
+    return guard([&] {
+        set_dev(ctx);
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->profiling = on != 0;
+        ctx->prof.clear();
+        ctx->ev_used = 0;
+    });
+}
+int vr_ctx_profile_read(vr_ctx* ctx, char* buf, size_t len) {
+    return guard([&] {
+        set_dev(ctx);
+        need(buf && len > 0, "vr_ctx_profile_read");
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        struct Acc {
+            long long n = 0;
+            double ms = 0.0;
+        };
+        std::vector<std::pair<std::string, Acc>> acc;
+        for (const auto& r : ctx->prof) {
+            float ms = 0.f;
+            VR_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+            auto it = acc.begin();
+            for (; it != acc.end(); ++it)
+                if (it->first == r.cat) break;
+            if (it == acc.end()) {
+                acc.push_back({r.cat, Acc{}});
+                it = acc.end() - 1;
+            }
+            it->second.n += 1;
+            it->second.ms += ms;
+        }
+        std::string out;
+        for (const auto& a : acc)
+            out += a.first + "," + std::to_string(a.second.n) + "," + std::to_string(a.second.ms) + "\n";
+        std::snprintf(buf, len, "%s", out.c_str());
+        ctx->prof.clear();
+        ctx->ev_used = 0;
+    });
 }
 
 // ---- memory -------------------------------------------------------------------

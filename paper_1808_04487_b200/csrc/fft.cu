@@ -527,9 +527,7 @@ void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inne
         attr = true;
     }
     dim3 grid(static_cast<unsigned>((inner + C::TB - 1) / C::TB), static_cast<unsigned>(outer));
-    kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, dst, inner, outer_stride, tw, m, ctx->g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : "fft_x1_mult", kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, dst, inner, outer_stride, tw, m, ctx->g););
 }
 
 template <int DIR, int MODE>
@@ -565,9 +563,9 @@ void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double 
                                          static_cast<int>(C::SMEM)));
             attr = true;
         }
-        k_r2c_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+        VR_LAUNCH(ctx, "fft_x3_r2c", k_r2c_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double*>(in), static_cast<double2*>(out), nrows, ctx->fft->tw3h,
-            ctx->fft->tw3);
+            ctx->fft->tw3));
     } else {
         static bool attr = false;
         if (!attr) {
@@ -575,12 +573,10 @@ void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double 
                                          static_cast<int>(C::SMEM)));
             attr = true;
         }
-        k_c2r_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double2*>(in), static_cast<double*>(out), nrows, ctx->fft->tw3h,
-            ctx->fft->tw3, scale, add);
+            ctx->fft->tw3, scale, add));
     }
-    check_launch();
-    count_launch(ctx);
 }
 
 void launch_rows(vr_ctx* ctx, bool forward, const void* in, void* out, double scale,
@@ -704,9 +700,7 @@ void op_divergence(vr_ctx* ctx, const double* v3, double* out) {
         fft_r2c(ctx, v3 + a * g.N, reinterpret_cast<double*>(s[a]));
     }
     auto* acc = reinterpret_cast<double2*>(spec_buf(ctx, 3));
-    k_spec_div<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], acc, g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "fft_spectral", k_spec_div<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], acc, g););
     fft_c2r(ctx, reinterpret_cast<double*>(acc), out, 1.0 / static_cast<double>(g.N), nullptr);
 }
 
@@ -728,10 +722,8 @@ void op_projection(vr_ctx* ctx, const double* in3, double* out3, int kind, doubl
         s[a] = reinterpret_cast<double2*>(spec_buf(ctx, a));
         fft_r2c(ctx, in3 + a * g.N, reinterpret_cast<double*>(s[a]));
     }
-    k_spec_project<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], g, kind, beta_v,
-                                                           beta_w);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "fft_spectral", k_spec_project<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], g, kind, beta_v,
+                                                           beta_w););
     for (int a = 0; a < 3; ++a)
         fft_c2r(ctx, reinterpret_cast<double*>(s[a]), out3 + a * g.N,
                 1.0 / static_cast<double>(g.N), nullptr);

@@ -295,13 +295,11 @@ unsigned pgrid(const GridDims& g) { return grid_1d(g.N, kThreads); }
 void sl_tricubic(vr_ctx* ctx, const double* f, int nfields, const double* pts3, double* out) {
     const GridDims& g = ctx->g;
     switch (nfields) {
-        case 1: k_tricubic<1><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g); break;
-        case 2: k_tricubic<2><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g); break;
-        case 3: k_tricubic<3><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g); break;
+        case 1: VR_LAUNCH(ctx, "sl_gather", k_tricubic<1><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g)); break;
+        case 2: VR_LAUNCH(ctx, "sl_gather", k_tricubic<2><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g)); break;
+        case 3: VR_LAUNCH(ctx, "sl_gather", k_tricubic<3><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g)); break;
         default: throw_argument("tricubic_interpolate: nfields must be 1, 2 or 3");
     }
-    check_launch();
-    count_launch(ctx);
 }
 
 void sl_trace(vr_ctx* ctx, const double* v3, int nt, int direction, double* dep3) {
@@ -309,95 +307,70 @@ void sl_trace(vr_ctx* ctx, const double* v3, int nt, int direction, double* dep3
     const GridDims& g = ctx->g;
     const double dt = 1.0 / nt;
     const double sign = direction == VR_TRACE_BACKWARD ? -1.0 : 1.0;
-    k_trace<<<pgrid(g), kThreads, 0, ctx->stream>>>(v3, dep3, g, sign, dt);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_trace", k_trace<<<pgrid(g), kThreads, 0, ctx->stream>>>(v3, dep3, g, sign, dt));
 }
 
 void sl_factor(vr_ctx* ctx, const double* div_v, const double* dep3, double half_dt,
                double* factor) {
     const GridDims& g = ctx->g;
-    k_factor<<<pgrid(g), kThreads, 0, ctx->stream>>>(div_v, dep3, factor, g, half_dt);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_factor", k_factor<<<pgrid(g), kThreads, 0, ctx->stream>>>(div_v, dep3, factor, g, half_dt));
 }
 
 void sl_advect(vr_ctx* ctx, const double* f, const double* dep3, double* out) {
     const GridDims& g = ctx->g;
-    k_advect<false><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, dep3, nullptr, out, g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_state_step", k_advect<false><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, dep3, nullptr, out, g));
 }
 
 void sl_continuity(vr_ctx* ctx, const double* f, const double* dep3, const double* factor,
                    double* out) {
     const GridDims& g = ctx->g;
-    k_advect<true><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, dep3, factor, out, g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_adjoint_step", k_advect<true><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, dep3, factor, out, g));
 }
 
 void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double hdt,
                        double* tmp0) {
     const GridDims& g = ctx->g;
-    k_incstate_first<<<pgrid(g), kThreads, 0, ctx->stream>>>(gm0, vt3, tmp0, g, hdt,
-                                                              ctx->flag_dev);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_pointwise", k_incstate_first<<<pgrid(g), kThreads, 0, ctx->stream>>>(gm0, vt3, tmp0, g, hdt, ctx->flag_dev));
 }
 
 void sl_incstate_step(vr_ctx* ctx, const double* src, const double* dep3, const double* gm,
                       const double* vt3, double hdt, double* dst, int mode) {
     const GridDims& g = ctx->g;
     if (mode == 0)
-        k_incstate_step<0><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, gm, vt3, dst, g, hdt);
+        VR_LAUNCH(ctx, "sl_incstate_step", k_incstate_step<0><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, gm, vt3, dst, g, hdt));
     else
-        k_incstate_step<1><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, gm, vt3, dst, g, hdt);
-    check_launch();
-    count_launch(ctx);
+        VR_LAUNCH(ctx, "sl_incstate_step", k_incstate_step<1><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, gm, vt3, dst, g, hdt));
 }
 
 void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const double* factor,
                      double* dst, const double* gm, double w, double* b3) {
     const GridDims& g = ctx->g;
     if (b3)
-        k_adjoint_step<true><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, factor, dst, gm, w,
-                                                                     b3, g);
+        VR_LAUNCH(ctx, "sl_adjoint_step_acc", k_adjoint_step<true><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, factor, dst, gm, w, b3, g));
     else
-        k_adjoint_step<false><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, factor, dst,
-                                                                      nullptr, 0.0, nullptr, g);
-    check_launch();
-    count_launch(ctx);
+        VR_LAUNCH(ctx, "sl_adjoint_step", k_adjoint_step<false><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, factor, dst, nullptr, 0.0, nullptr, g));
 }
 
 void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const double* gm,
                       double w, double* lam, double* b3) {
     const GridDims& g = ctx->g;
-    k_grad_terminal<<<pgrid(g), kThreads, 0, ctx->stream>>>(mR, mfinal, gm, w, lam, b3, g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_pointwise", k_grad_terminal<<<pgrid(g), kThreads, 0, ctx->stream>>>(mR, mfinal, gm, w, lam, b3, g));
 }
 
 void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, int nt, double dt,
                    double* b3) {
     const GridDims& g = ctx->g;
-    k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, gm_hist, nt, dt, b3, g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_accumulate", k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, gm_hist, nt, dt, b3, g));
 }
 
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out) {
     const GridDims& g = ctx->g;
-    k_gradient_dot<<<pgrid(g), kThreads, 0, ctx->stream>>>(gm3, w3, out, g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "sl_pointwise", k_gradient_dot<<<pgrid(g), kThreads, 0, ctx->stream>>>(gm3, w3, out, g));
 }
 
 void synth_fill(vr_ctx* ctx, double amplitude, double* m_T, double* v3) {
     const GridDims& g = ctx->g;
-    k_synth<<<pgrid(g), kThreads, 0, ctx->stream>>>(amplitude, m_T, v3, g);
-    check_launch();
-    count_launch(ctx);
+    VR_LAUNCH(ctx, "synth", k_synth<<<pgrid(g), kThreads, 0, ctx->stream>>>(amplitude, m_T, v3, g));
 }
 
 }  // namespace vr

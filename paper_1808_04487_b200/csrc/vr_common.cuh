@@ -95,6 +95,15 @@ struct vr_ctx {
     int* flag_dev = nullptr;         // device int flags (non-finite detection)
     int* flag_host = nullptr;        // pinned
     long long launches = 0;
+    // optional per-launch CUDA-event timing (bench / roofline evidence)
+    bool profiling = false;
+    struct ProfRec {
+        const char* cat;
+        cudaEvent_t start, stop;
+    };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
 };
 
 namespace vr {
@@ -106,6 +115,29 @@ double* spec_buf(vr_ctx* ctx, int i);   // NC complex (2*NC doubles)
 double* field_buf(vr_ctx* ctx, int i);  // N doubles
 inline void count_launch(vr_ctx* ctx, int n = 1) { ctx->launches += n; }
 inline void check_launch() { VR_CUDA(cudaGetLastError()); }
+cudaEvent_t prof_event(vr_ctx* ctx);
+inline cudaEvent_t prof_begin(vr_ctx* ctx) {
+    if (!ctx->profiling) return nullptr;
+    cudaEvent_t e = prof_event(ctx);
+    VR_CUDA(cudaEventRecord(e, ctx->stream));
+    return e;
+}
+inline void prof_end(vr_ctx* ctx, const char* cat, cudaEvent_t start) {
+    ctx->launches += 1;
+    if (!start) return;
+    cudaEvent_t e = prof_event(ctx);
+    VR_CUDA(cudaEventRecord(e, ctx->stream));
+    ctx->prof.push_back({cat, start, e});
+}
+// Launch a kernel on ctx's stream, check it, count it, and (when profiling)
+// bracket it with CUDA events under category CAT.
+#define VR_LAUNCH(ctx, cat, ...)                                   \
+    do {                                                           \
+        cudaEvent_t vr_ev_ = ::vr::prof_begin(ctx);                \
+        __VA_ARGS__;                                               \
+        ::vr::check_launch();                                      \
+        ::vr::prof_end(ctx, cat, vr_ev_);                          \
+    } while (0)
 
 inline unsigned grid_1d(long long n, int threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);

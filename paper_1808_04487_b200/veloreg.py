@@ -101,6 +101,19 @@ class Context:
     def reset_kernel_launches(self):
         _lib.load().vr_ctx_reset_kernel_launches(self._h)
 
+    def set_profiling(self, on: bool):
+        _lib.call("vr_ctx_set_profiling", self._h, int(bool(on)))
+
+    def profile_read(self) -> dict:
+        """{category: (launches, total_ms)} since profiling was enabled / last read."""
+        buf = C.create_string_buffer(1 << 16)
+        _lib.call("vr_ctx_profile_read", self._h, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            cat, n, ms = line.split(",")
+            out[cat] = (int(n), float(ms))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             _lib.call("vr_ctx_destroy", self._h)
