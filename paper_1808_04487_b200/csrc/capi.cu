@@ -4,6 +4,7 @@
 // the reference's typed exception.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -153,6 +154,8 @@ int vr_ctx_create(int n1, int n2, int n3, int device, vr_ctx** out) {
             g.h1 = vr::kTwoPi / n1;
             g.h2 = vr::kTwoPi / n2;
             g.h3 = vr::kTwoPi / n3;
+            const char* slm = std::getenv("VR_SL_MODE");
+            g.sl_mode = slm ? std::atoi(slm) : 1;
             VR_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
             // keep freed blocks cached in the stream-ordered pool (no OS round trips)
             cudaMemPool_t pool;

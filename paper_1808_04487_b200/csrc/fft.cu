@@ -75,8 +75,10 @@ __device__ __forceinline__ void dft_reg(double2* x) {
             x[j] = t;
         }
     }
+    constexpr int LOG2R = R >= 16 ? 4 : R >= 8 ? 3 : R >= 4 ? 2 : 1;
 #pragma unroll
-    for (int len = 2; len <= R; len <<= 1) {
+    for (int s = 0; s < LOG2R; ++s) {  // constant trip count: fully unrolled, literal twiddles
+        const int len = 2 << s;
 #pragma unroll
         for (int start = 0; start < R; start += len) {
 #pragma unroll
@@ -126,7 +128,7 @@ __device__ __forceinline__ void stockham_stage(int Ns, int t, const double2* __r
             const int step = N / (Ns * R);
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                double2 w = __ldg(tw + r * k * step);
+                double2 w = tw[r * k * step];  // shared-memory table
                 if (DIR < 0) w.y = -w.y;
                 x[b * R + r] = cmul(x[b * R + r], w);
             }
@@ -255,18 +257,21 @@ struct AxisCfg {
     static constexpr int TB0 = 256 / T;
     static constexpr int TB = TB0 < 1 ? 1 : (TB0 > 64 ? 64 : TB0);
     static constexpr int THREADS = TB * T;
-    static constexpr size_t SMEM = sizeof(double2) * N * TB;
+    static constexpr size_t SMEM = sizeof(double2) * (N * TB + N);  // data + twiddle table
 };
 
 // MODE 0: transform in direction DIR (src may equal dst)
 // MODE 1: forward -> multiplier -> inverse (x1 pass only), src -> dst (may alias)
 // MODE 2: like 1 but dst += result (accumulate)
 template <int N, int DIR, int MODE>
-__global__ void __launch_bounds__(AxisCfg<N>::THREADS)
+__global__ void __launch_bounds__(AxisCfg<N>::THREADS, 2)
     k_fft_axis(const double2* src, double2* dst, long long inner, long long outer_stride,
-               const double2* __restrict__ tw, MultDev m, GridDims g) {
+               const double2* __restrict__ tw_g, MultDev m, GridDims g) {
     using C = AxisCfg<N>;
     extern __shared__ double2 smem[];
+    double2* tw = smem + N * C::TB;  // W_N table staged once per CTA (broadcast reads)
+    for (int i = threadIdx.x; i < N; i += C::THREADS) tw[i] = __ldg(tw_g + i);
+    __syncthreads();
     const int col = threadIdx.x % C::TB;
     const int t = threadIdx.x / C::TB;
     const long long cc = blockIdx.x * (long long)C::TB + col;
@@ -311,19 +316,32 @@ struct RowCfg {
     static constexpr int RB = RB0 < 1 ? 1 : (RB0 > 64 ? 64 : RB0);
     static constexpr int THREADS = RB * T;
     static constexpr int LD = (M + 1) + ((M + 1) >> 4) + 1;  // padded row length
-    static constexpr size_t SMEM = sizeof(double2) * LD * RB;
+    static constexpr size_t SMEM = sizeof(double2) * (LD * RB + 3 * M);  // rows + W_M, W_2M tables
 };
+// stage the W_M and W_N (N = 2M) twiddle tables in shared memory after the rows
+template <int M>
+__device__ __forceinline__ void stage_row_tables(double2* smem, const double2* twM_g,
+                                                 const double2* twN_g, double2*& twM,
+                                                 double2*& twN) {
+    using C = RowCfg<M>;
+    twM = smem + C::LD * C::RB;
+    twN = twM + M;
+    for (int i = threadIdx.x; i < M; i += C::THREADS) twM[i] = __ldg(twM_g + i);
+    for (int i = threadIdx.x; i < 2 * M; i += C::THREADS) twN[i] = __ldg(twN_g + i);
+}
 __device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
 
 // r2c along x3: in nrows x 2M reals -> out nrows x (M+1) complex.
 // z[m] = x[2m] + i x[2m+1]; Z = FFT_M(z); X[k] = A[k] + W_N^k B[k] with
 // A = (Z[k] + conj Z[M-k]) / 2, B = (Z[k] - conj Z[M-k]) / 2i.
 template <int M>
-__global__ void __launch_bounds__(RowCfg<M>::THREADS)
+__global__ void __launch_bounds__(RowCfg<M>::THREADS, 2)
     k_r2c_rows(const double* __restrict__ in, double2* __restrict__ out, long long nrows,
-               const double2* __restrict__ twM, const double2* __restrict__ twN) {
+               const double2* __restrict__ twM_g, const double2* __restrict__ twN_g) {
     using C = RowCfg<M>;
     extern __shared__ double2 smem[];
+    double2 *twM, *twN;
+    stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
     const long long row0 = blockIdx.x * (long long)C::RB;
     const double2* src = reinterpret_cast<const double2*>(in) + row0 * M;
     const long long avail = (nrows - row0) * M;
@@ -356,7 +374,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
             const double2 A = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
             const double2 D = make_double2(0.5 * (zk.x - zc.x), 0.5 * (zk.y - zc.y));
             const double2 B = make_double2(D.y, -D.x);  // D / i
-            double2 w = __ldg(twN + k);
+            double2 w = twN[k];
             w.y = -w.y;  // exp(-2 pi i k / N)
             X = cadd(A, cmul(w, B));
         }
@@ -369,12 +387,14 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
 // O = (X[k] - conj X[M-k]) exp(+2 pi i k / N); z = IFFT_M(Z); x[2m] = Re, x[2m+1] = Im.
 // Imaginary parts of the self-conjugate bins X[0], X[M] are ignored (c2r semantics).
 template <int M>
-__global__ void __launch_bounds__(RowCfg<M>::THREADS)
+__global__ void __launch_bounds__(RowCfg<M>::THREADS, 2)
     k_c2r_rows(const double2* __restrict__ in, double* __restrict__ out, long long nrows,
-               const double2* __restrict__ twM, const double2* __restrict__ twN, double scale,
+               const double2* __restrict__ twM_g, const double2* __restrict__ twN_g, double scale,
                const double* __restrict__ add) {
     using C = RowCfg<M>;
     extern __shared__ double2 smem[];
+    double2 *twM, *twN;
+    stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
     const long long row0 = blockIdx.x * (long long)C::RB;
     const double2* src = in + row0 * (M + 1);
     const long long avail = (nrows - row0) * (M + 1);
@@ -392,8 +412,8 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
             X[0] = make_double2(a + b, a - b);
         } else {
             const double2 xk = X[padi(k)], xm = X[padi(M - k)];
-            const double2 wk = __ldg(twN + k);      // exp(+2 pi i k / N)
-            const double2 wm = __ldg(twN + M - k);  // exp(+2 pi i (M-k) / N)
+            const double2 wk = twN[k];     // exp(+2 pi i k / N)
+            const double2 wm = twN[M - k]; // exp(+2 pi i (M-k) / N)
             {
                 const double2 E = cadd(xk, cconj(xm));
                 const double2 O = cmul(csub(xk, cconj(xm)), wk);

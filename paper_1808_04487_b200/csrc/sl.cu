@@ -6,15 +6,26 @@
 // proj/src/transport.cpp:11-237 (trace, factor, steps, sweeps),
 // proj/src/objective.cpp:9-32,96-99,143-148 (fused gradient accumulation).
 //
-// Every kernel is one thread per output grid point, consecutive threads along
-// the contiguous x3 axis, so departure-point loads are coalesced and the 4x4x4
-// stencil rows of neighbouring threads overlap in L1. The stencil arithmetic
-// follows interp.hpp:32-53 exactly (u = x / h, 1e-12 node snap, floor, wrapped
-// base (i-1) mod n); the gather keeps the reference's a -> b -> c nesting.
+// Tile gather. A CTA owns a t1 x t2 x t3 tile of output points (t3 = 32 along
+// the contiguous axis, so a warp is one x3 run). Every thread first computes
+// its stencil (u = x / h, 1e-12 node snap, floor, weights; interp.hpp:32-53);
+// the CTA then reduces the bounding box of all 4x4x4 stencils. Because the
+// velocity is smooth the box is only a few voxels larger than the tile, so the
+// CTA stages it in shared memory with coalesced loads (periodic wrap resolved
+// once per box element) and the 64-point gathers read shared memory instead of
+// going through L1/L2. If the box does not fit (arbitrary query points, huge
+// CFL) the CTA falls back to direct wrapped global gathers. Both paths keep the
+// reference's a -> b -> c summation order.
+#include <climits>
+
 #include "vr_common.cuh"
 
 namespace vr {
 namespace {
+
+constexpr int kTileThreads = 256;
+constexpr int kBoxCap = 6144;  // doubles of staged box per CTA (48 KB)
+constexpr int kThreads = 256;  // pointwise kernels
 
 // cubic_weights (interp.hpp:12-18)
 __device__ __forceinline__ void cubic_weights(double s, double* w) {
@@ -25,68 +36,199 @@ __device__ __forceinline__ void cubic_weights(double s, double* w) {
     w[3] = sp1 * s * sm1 * (1.0 / 6.0);
 }
 
+// Stencil with UNWRAPPED base index b = floor(u) - 1 per axis; the stencil
+// nodes are b..b+3 taken modulo n (== the reference's ((i-1) mod n + t) mod n).
 struct Stencil {
-    long long o1[4];  // i1 * n2
-    int i2[4];
-    int i3[4];
-    double w1[4], w2[4], w3[4];
-    bool contig3;  // i3 indices consecutive (no wrap)
+    int b[3];
+    double w[3][4];
 };
 
-// TricubicStencil ctor, per axis (interp.hpp:32-53)
-__device__ __forceinline__ void axis_stencil(double x, double h, int n, int* idx, double* w) {
+// `own` is the output point's grid index on this axis: the integer base is
+// shifted by a whole period to the image nearest to it (exact; the weights are
+// computed from the unshifted u exactly as the reference), so departure points
+// wrapped across the seam still give compact CTA boxes.
+__device__ __forceinline__ void axis_stencil(double x, double h, int n, int own, int& b,
+                                             double* w) {
     double u = x / h;
     const double r = rint(u);
     if (fabs(u - r) < 1e-12) u = r;
     const double fl = floor(u);
-    const double s = u - fl;
-    const int i = static_cast<int>(fl);
-    cubic_weights(s, w);
-    int base = i - 1;
-    base %= n;
-    if (base < 0) base += n;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-        const int j = base + t;
-        idx[t] = j < n ? j : j - n;
-    }
+    cubic_weights(u - fl, w);
+    b = static_cast<int>(fl) - 1;
+    const int d = b - own;
+    if (d > n / 2)
+        b -= n * ((d + n / 2) / n);
+    else if (d < -n / 2)
+        b += n * ((-d + n / 2) / n);
 }
 
 __device__ __forceinline__ void make_stencil(const GridDims& g, double x1, double x2, double x3,
-                                             Stencil& st) {
-    int i1[4];
-    axis_stencil(x1, g.h1, g.n1, i1, st.w1);
-    axis_stencil(x2, g.h2, g.n2, st.i2, st.w2);
-    axis_stencil(x3, g.h3, g.n3, st.i3, st.w3);
-#pragma unroll
-    for (int t = 0; t < 4; ++t) st.o1[t] = static_cast<long long>(i1[t]) * g.n2;
-    st.contig3 = st.i3[3] == st.i3[0] + 3;
+                                             int o1, int o2, int o3, Stencil& st) {
+    axis_stencil(x1, g.h1, g.n1, o1, st.b[0], st.w[0]);
+    axis_stencil(x2, g.h2, g.n2, o2, st.b[1], st.w[1]);
+    axis_stencil(x3, g.h3, g.n3, o3, st.b[2], st.w[2]);
 }
 
-// gather (interp.hpp:55-72): sum_a w1[a] sum_b w2[b] sum_c w3[c] f
-__device__ __forceinline__ double gather(const double* __restrict__ f, const GridDims& g,
-                                         const Stencil& st) {
+// power-of-two periodic wrap (two's complement handles negative j)
+__device__ __forceinline__ int wrapi(int j, int n) { return j & (n - 1); }
+
+// direct gather from global memory (fallback path)
+__device__ __forceinline__ double global_gather(const double* __restrict__ f, const GridDims& g,
+                                                const Stencil& st) {
+    int i3[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) i3[c] = wrapi(st.b[2] + c, g.n3);
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const long long o1 = static_cast<long long>(wrapi(st.b[0] + a, g.n1)) * g.n2;
+        double acc1 = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double* row = f + (o1 + wrapi(st.b[1] + b, g.n2)) * g.n3;
+            double acc2 = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc2 += st.w[2][c] * __ldg(row + i3[c]);
+            acc1 += st.w[1][b] * acc2;
+        }
+        acc += st.w[0][a] * acc1;
+    }
+    return acc;
+}
+
+struct Box {
+    int m[3];  // min unwrapped base per axis
+    int e[3];  // extents (max base - min base + 4)
+    int size;  // e0 * e1 * e2
+};
+
+// CTA-wide bounding box of the active threads' stencils (all threads call).
+__device__ __forceinline__ Box block_box(const Stencil& st, bool active) {
+    __shared__ int red[kTileThreads / 32][6];
+    __shared__ Box box_s;
+    int v[6];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        v[a] = active ? st.b[a] : INT_MAX;
+        v[3 + a] = active ? st.b[a] : INT_MIN;
+    }
+    const unsigned full = 0xffffffffu;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        v[a] = __reduce_min_sync(full, v[a]);
+        v[3 + a] = __reduce_max_sync(full, v[3 + a]);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+        for (int k = 0; k < 6; ++k) red[warp][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        int r[6];
+        for (int k = 0; k < 6; ++k) r[k] = red[0][k];
+        for (int w = 1; w < nw; ++w)
+            for (int a = 0; a < 3; ++a) {
+                r[a] = min(r[a], red[w][a]);
+                r[3 + a] = max(r[3 + a], red[w][3 + a]);
+            }
+        Box b;
+        long long size = 1;
+        for (int a = 0; a < 3; ++a) {
+            b.m[a] = r[a];
+            const long long e = static_cast<long long>(r[3 + a]) - r[a] + 4;
+            b.e[a] = static_cast<int>(e < INT_MAX ? e : INT_MAX);
+            size *= e;
+        }
+        b.size = static_cast<int>(size < INT_MAX ? size : INT_MAX);
+        box_s = b;
+    }
+    __syncthreads();
+    return box_s;
+}
+
+// stage one field's box in shared memory: one warp per (j1, j2) box row, lanes
+// along the contiguous x3 run (coalesced), no per-element integer division
+__device__ __forceinline__ void box_load(const double* __restrict__ f, const GridDims& g,
+                                         const Box& bx, double* __restrict__ sbox) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    const int rows = bx.e[0] * bx.e[1];
+    for (int row = warp; row < rows; row += nwarps) {
+        const int j1 = row / bx.e[1];
+        const int j2 = row - j1 * bx.e[1];
+        const double* src = f + (static_cast<long long>(wrapi(bx.m[0] + j1, g.n1)) * g.n2 +
+                                 wrapi(bx.m[1] + j2, g.n2)) * g.n3;
+        double* dst = sbox + row * bx.e[2];
+        for (int j3 = lane; j3 < bx.e[2]; j3 += 32) dst[j3] = __ldg(src + wrapi(bx.m[2] + j3, g.n3));
+    }
+}
+
+__device__ __forceinline__ double box_gather(const double* __restrict__ sbox, const Box& bx,
+                                             const Stencil& st) {
+    const int e3 = bx.e[2], e23 = bx.e[1] * bx.e[2];
+    const double* p0 = sbox + ((st.b[0] - bx.m[0]) * bx.e[1] + (st.b[1] - bx.m[1])) * e3 +
+                       (st.b[2] - bx.m[2]);
     double acc = 0.0;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         double acc1 = 0.0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const double* row = f + (st.o1[a] + st.i2[b]) * g.n3;
+            const double* p = p0 + a * e23 + b * e3;
             double acc2 = 0.0;
-            if (st.contig3) {
-                const double* p = row + st.i3[0];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc2 += st.w3[c] * __ldg(p + c);
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) acc2 += st.w3[c] * __ldg(row + st.i3[c]);
-            }
-            acc1 += st.w2[b] * acc2;
+            for (int c = 0; c < 4; ++c) acc2 += st.w[2][c] * p[c];
+            acc1 += st.w[1][b] * acc2;
         }
-        acc += st.w1[a] * acc1;
+        acc += st.w[0][a] * acc1;
     }
     return acc;
+}
+
+// Gather NF fields at this thread's stencil; all threads of the CTA must call.
+// g.sl_mode: 0 = stage the CTA box in shared memory, 1 = L1-cached global gathers
+template <int NF>
+__device__ __forceinline__ void tile_gather(const double* const (&f)[NF], const GridDims& g,
+                                            const Stencil& st, bool active, double (&out)[NF]) {
+    extern __shared__ double sbox[];
+    if (g.sl_mode == 1) {
+        if (active) {
+#pragma unroll
+            for (int q = 0; q < NF; ++q) out[q] = global_gather(f[q], g, st);
+        }
+        return;
+    }
+    const Box bx = block_box(st, active);
+    if (bx.size <= kBoxCap / NF) {  // uniform across the CTA
+#pragma unroll
+        for (int q = 0; q < NF; ++q) box_load(f[q], g, bx, sbox + q * bx.size);
+        __syncthreads();
+        if (active) {
+#pragma unroll
+            for (int q = 0; q < NF; ++q) out[q] = box_gather(sbox + q * bx.size, bx, st);
+        }
+    } else if (active) {
+#pragma unroll
+        for (int q = 0; q < NF; ++q) out[q] = global_gather(f[q], g, st);
+    }
+}
+
+// tile geometry: CTA (bx, by, bz) covers i3 in [bx t3, ...), i2 in [by t2, ...), i1 in [bz t1, ...)
+struct Tile {
+    int t1, t2, t3;
+};
+__device__ __forceinline__ bool tile_point(const GridDims& g, const Tile& t, int& i1, int& i2,
+                                           int& i3, long long& idx) {
+    const int tid = threadIdx.x;
+    const int l3 = tid % t.t3;
+    const int l2 = (tid / t.t3) % t.t2;
+    const int l1 = tid / (t.t3 * t.t2);
+    i3 = blockIdx.x * t.t3 + l3;
+    i2 = blockIdx.y * t.t2 + l2;
+    i1 = blockIdx.z * t.t1 + l1;
+    const bool ok = l1 < t.t1 && i1 < g.n1 && i2 < g.n2 && i3 < g.n3;
+    idx = ok ? (static_cast<long long>(i1) * g.n2 + i2) * g.n3 + i3 : 0;
+    return ok;
 }
 
 __device__ __forceinline__ void load_point(const double* __restrict__ dep, long long i,
@@ -96,73 +238,94 @@ __device__ __forceinline__ void load_point(const double* __restrict__ dep, long 
     x3 = __ldg(dep + 2 * N + i);
 }
 
-constexpr int kThreads = 256;
-
 // ---------------------------------------------------------------------------
+// tricubic_interpolate{,2,3} (interp.hpp:80-126)
 template <int NF>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kTileThreads, NF == 1 ? 3 : 2)
     k_tricubic(const double* __restrict__ f, const double* __restrict__ pts, double* __restrict__ out,
-               GridDims g) {
-    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
-    if (i >= g.N) return;
-    double x1, x2, x3;
-    load_point(pts, i, g.N, x1, x2, x3);
+               GridDims g, Tile t) {
+    int i1, i2, i3;
+    long long i;
+    const bool act = tile_point(g, t, i1, i2, i3, i);
+    double x1 = 0, x2 = 0, x3 = 0;
+    if (act) load_point(pts, i, g.N, x1, x2, x3);
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
+    make_stencil(g, x1, x2, x3, i1, i2, i3, st);
+    const double* fs[NF];
 #pragma unroll
-    for (int q = 0; q < NF; ++q) out[q * g.N + i] = gather(f + q * g.N, g, st);
+    for (int q = 0; q < NF; ++q) fs[q] = f + q * g.N;
+    double r[NF];
+    tile_gather<NF>(fs, g, st, act, r);
+    if (act) {
+#pragma unroll
+        for (int q = 0; q < NF; ++q) out[q * g.N + i] = r[q];
+    }
 }
 
-// trace_characteristics (transport.cpp:11-42)
-__global__ void __launch_bounds__(kThreads)
-    k_trace(const double* __restrict__ v, double* __restrict__ dep, GridDims g, double sign,
-            double dt) {
-    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
-    if (i >= g.N) return;
-    long long r = i;
-    const int i3 = static_cast<int>(r % g.n3);
-    r /= g.n3;
-    const int i2 = static_cast<int>(r % g.n2);
-    const int i1 = static_cast<int>(r / g.n2);
+// trace_characteristics (transport.cpp:11-42): midpoint from v at the grid
+// point, one 3-field gather of v there, wrapped departure point.
+__global__ void __launch_bounds__(kTileThreads, 2)
+    k_trace(const double* __restrict__ v, double* __restrict__ dep, GridDims g, Tile t,
+            double sign, double dt) {
+    int i1, i2, i3;
+    long long i;
+    const bool act = tile_point(g, t, i1, i2, i3, i);
     const double x[3] = {g.h1 * i1, g.h2 * i2, g.h3 * i3};
-    double mid[3];
+    double mid[3] = {0, 0, 0};
+    if (act) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) mid[c] = wrap_coord(x[c] + sign * 0.5 * dt * v[c * g.N + i]);
+        for (int c = 0; c < 3; ++c) mid[c] = wrap_coord(x[c] + sign * 0.5 * dt * v[c * g.N + i]);
+    }
     Stencil st;
-    make_stencil(g, mid[0], mid[1], mid[2], st);
+    make_stencil(g, mid[0], mid[1], mid[2], i1, i2, i3, st);
+    const double* fs[3] = {v, v + g.N, v + 2 * g.N};
+    double r[3];
+    tile_gather<3>(fs, g, st, act, r);
+    if (act) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-        dep[c * g.N + i] = wrap_coord(x[c] + sign * dt * gather(v + c * g.N, g, st));
+        for (int c = 0; c < 3; ++c) dep[c * g.N + i] = wrap_coord(x[c] + sign * dt * r[c]);
+    }
 }
 
 // continuity_factor (transport.cpp:44-55)
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kTileThreads, 3)
     k_factor(const double* __restrict__ div, const double* __restrict__ dep,
-             double* __restrict__ factor, GridDims g, double half_dt) {
-    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
-    if (i >= g.N) return;
-    double x1, x2, x3;
-    load_point(dep, i, g.N, x1, x2, x3);
+             double* __restrict__ factor, GridDims g, Tile t, double half_dt) {
+    int i1, i2, i3;
+    long long i;
+    const bool act = tile_point(g, t, i1, i2, i3, i);
+    double x1 = 0, x2 = 0, x3 = 0, d = 0;
+    if (act) {
+        load_point(dep, i, g.N, x1, x2, x3);
+        d = div[i];
+    }
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
-    const double at_dep = gather(div, g, st);
-    factor[i] = exp(half_dt * (div[i] + at_dep));
+    make_stencil(g, x1, x2, x3, i1, i2, i3, st);
+    const double* fs[1] = {div};
+    double r[1];
+    tile_gather<1>(fs, g, st, act, r);
+    if (act) factor[i] = exp(half_dt * (d + r[0]));
 }
 
 // advect_step / continuity_step (transport.cpp:57-68)
 template <bool FACTOR>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kTileThreads, 3)
     k_advect(const double* __restrict__ f, const double* __restrict__ dep,
-             const double* __restrict__ factor, double* __restrict__ out, GridDims g) {
-    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
-    if (i >= g.N) return;
-    double x1, x2, x3;
-    load_point(dep, i, g.N, x1, x2, x3);
+             const double* __restrict__ factor, double* __restrict__ out, GridDims g, Tile t) {
+    int i1, i2, i3;
+    long long i;
+    const bool act = tile_point(g, t, i1, i2, i3, i);
+    double x1 = 0, x2 = 0, x3 = 0, fac = 1.0;
+    if (act) {
+        load_point(dep, i, g.N, x1, x2, x3);
+        if (FACTOR) fac = factor[i];
+    }
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
-    double v = gather(f, g, st);
-    if (FACTOR) v = v * factor[i];
-    out[i] = v;
+    make_stencil(g, x1, x2, x3, i1, i2, i3, st);
+    const double* fs[1] = {f};
+    double r[1];
+    tile_gather<1>(fs, g, st, act, r);
+    if (act) out[i] = FACTOR ? r[0] * fac : r[0];
 }
 
 // q = grad m . vt (transport.cpp:126-148 accumulation order: ((0 + d0 w0) + d1 w1) + d2 w2)
@@ -190,40 +353,57 @@ __global__ void __launch_bounds__(kThreads)
 //   mt_{j+1} = I[tmp_j](X_bwd) - hdt q_{j+1};  MODE 0: tmp_{j+1} = mt_{j+1} - hdt q_{j+1}
 //   MODE 1 (last step): terminal = -mt_nt (objective.cpp:138-140)
 template <int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kTileThreads, 3)
     k_incstate_step(const double* __restrict__ src, const double* __restrict__ dep,
                     const double* __restrict__ gm, const double* __restrict__ vt,
-                    double* __restrict__ dst, GridDims g, double hdt) {
-    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
-    if (i >= g.N) return;
-    double x1, x2, x3;
-    load_point(dep, i, g.N, x1, x2, x3);
+                    double* __restrict__ dst, GridDims g, Tile t, double hdt) {
+    int i1, i2, i3;
+    long long i;
+    const bool act = tile_point(g, t, i1, i2, i3, i);
+    double x1 = 0, x2 = 0, x3 = 0, q = 0;
+    if (act) {
+        load_point(dep, i, g.N, x1, x2, x3);
+        q = qdot(gm, vt, i, g.N);  // independent loads issued before the box staging
+    }
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
-    const double adv = gather(src, g, st);
-    const double q = qdot(gm, vt, i, g.N);
-    const double m = adv + (-hdt) * q;
-    dst[i] = (MODE == 0) ? 1.0 * m + (-hdt) * q : -m;
+    make_stencil(g, x1, x2, x3, i1, i2, i3, st);
+    const double* fs[1] = {src};
+    double r[1];
+    tile_gather<1>(fs, g, st, act, r);
+    if (act) {
+        const double m = r[0] + (-hdt) * q;
+        dst[i] = (MODE == 0) ? 1.0 * m + (-hdt) * q : -m;
+    }
 }
 
 // continuity step + optional fused accumulation b_a += (w * lam) * d_a m_j
 template <bool ACC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kTileThreads, 3)
     k_adjoint_step(const double* __restrict__ src, const double* __restrict__ dep,
                    const double* __restrict__ factor, double* __restrict__ dst,
-                   const double* __restrict__ gm, double w, double* __restrict__ b, GridDims g) {
-    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
-    if (i >= g.N) return;
-    double x1, x2, x3;
-    load_point(dep, i, g.N, x1, x2, x3);
+                   const double* __restrict__ gm, double w, double* __restrict__ b, GridDims g,
+                   Tile t) {
+    int i1, i2, i3;
+    long long i;
+    const bool act = tile_point(g, t, i1, i2, i3, i);
+    double x1 = 0, x2 = 0, x3 = 0, fac = 0;
+    if (act) {
+        load_point(dep, i, g.N, x1, x2, x3);
+        fac = factor[i];
+    }
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
-    const double lam = gather(src, g, st) * factor[i];
-    dst[i] = lam;
-    if (ACC) {
-        const double wl = w * lam;
+    make_stencil(g, x1, x2, x3, i1, i2, i3, st);
+    const double* fs[1] = {src};
+    double r[1];
+    tile_gather<1>(fs, g, st, act, r);
+    if (act) {
+        const double lam = r[0] * fac;
+        dst[i] = lam;
+        if (ACC) {
+            const double wl = w * lam;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) b[a * g.N + i] = b[a * g.N + i] + wl * gm[a * g.N + i];
+            for (int a = 0; a < 3; ++a) b[a * g.N + i] = b[a * g.N + i] + wl * gm[a * g.N + i];
+        }
     }
 }
 
@@ -290,14 +470,52 @@ __global__ void __launch_bounds__(kThreads)
 
 unsigned pgrid(const GridDims& g) { return grid_1d(g.N, kThreads); }
 
+Tile tile_of(const GridDims& g) {
+    Tile t;
+    t.t3 = g.n3 < 32 ? g.n3 : 32;
+    t.t2 = g.n2 < 4 ? g.n2 : 4;
+    const int rest = kTileThreads / (t.t3 * t.t2);
+    t.t1 = g.n1 < rest ? g.n1 : rest;
+    return t;
+}
+dim3 tgrid(const GridDims& g, const Tile& t) {
+    return dim3(static_cast<unsigned>(g.n3 / t.t3), static_cast<unsigned>(g.n2 / t.t2),
+                static_cast<unsigned>(g.n1 / t.t1));
+}
+unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.t3); }
+constexpr size_t kBoxBytes = sizeof(double) * kBoxCap;
+
+// opt every tile kernel into > 48 KB of shared memory once per (kernel, device)
+template <class K>
+void set_box_smem(K kern) {
+    static std::vector<std::pair<const void*, int>> done;
+    int dev = 0;
+    VR_CUDA(cudaGetDevice(&dev));
+    const void* key = reinterpret_cast<const void*>(kern);
+    for (const auto& d : done)
+        if (d.first == key && d.second == dev) return;
+    VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kBoxBytes)));
+    done.emplace_back(key, dev);
+}
+
+#define VR_TILE_LAUNCH(ctx, cat, kern, ...)                                                       \
+    do {                                                                                         \
+        const GridDims& g_ = (ctx)->g;                                                           \
+        const Tile t_ = tile_of(g_);                                                             \
+        set_box_smem(kern);                                                                      \
+        VR_LAUNCH(ctx, cat, kern<<<tgrid(g_, t_), tthreads(t_), kBoxBytes, (ctx)->stream>>>(__VA_ARGS__)); \
+    } while (0)
+
 }  // namespace
 
 void sl_tricubic(vr_ctx* ctx, const double* f, int nfields, const double* pts3, double* out) {
     const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
     switch (nfields) {
-        case 1: VR_LAUNCH(ctx, "sl_gather", k_tricubic<1><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g)); break;
-        case 2: VR_LAUNCH(ctx, "sl_gather", k_tricubic<2><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g)); break;
-        case 3: VR_LAUNCH(ctx, "sl_gather", k_tricubic<3><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, pts3, out, g)); break;
+        case 1: VR_TILE_LAUNCH(ctx, "sl_gather", k_tricubic<1>, f, pts3, out, g, t); break;
+        case 2: VR_TILE_LAUNCH(ctx, "sl_gather", k_tricubic<2>, f, pts3, out, g, t); break;
+        case 3: VR_TILE_LAUNCH(ctx, "sl_gather", k_tricubic<3>, f, pts3, out, g, t); break;
         default: throw_argument("tricubic_interpolate: nfields must be 1, 2 or 3");
     }
 }
@@ -305,26 +523,30 @@ void sl_tricubic(vr_ctx* ctx, const double* f, int nfields, const double* pts3, 
 void sl_trace(vr_ctx* ctx, const double* v3, int nt, int direction, double* dep3) {
     if (nt < 1) throw_argument("trace_characteristics: n_t must be >= 1");
     const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
     const double dt = 1.0 / nt;
     const double sign = direction == VR_TRACE_BACKWARD ? -1.0 : 1.0;
-    VR_LAUNCH(ctx, "sl_trace", k_trace<<<pgrid(g), kThreads, 0, ctx->stream>>>(v3, dep3, g, sign, dt));
+    VR_TILE_LAUNCH(ctx, "sl_trace", k_trace, v3, dep3, g, t, sign, dt);
 }
 
 void sl_factor(vr_ctx* ctx, const double* div_v, const double* dep3, double half_dt,
                double* factor) {
     const GridDims& g = ctx->g;
-    VR_LAUNCH(ctx, "sl_factor", k_factor<<<pgrid(g), kThreads, 0, ctx->stream>>>(div_v, dep3, factor, g, half_dt));
+    const Tile t = tile_of(g);
+    VR_TILE_LAUNCH(ctx, "sl_factor", k_factor, div_v, dep3, factor, g, t, half_dt);
 }
 
 void sl_advect(vr_ctx* ctx, const double* f, const double* dep3, double* out) {
     const GridDims& g = ctx->g;
-    VR_LAUNCH(ctx, "sl_state_step", k_advect<false><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, dep3, nullptr, out, g));
+    const Tile t = tile_of(g);
+    VR_TILE_LAUNCH(ctx, "sl_state_step", k_advect<false>, f, dep3, nullptr, out, g, t);
 }
 
 void sl_continuity(vr_ctx* ctx, const double* f, const double* dep3, const double* factor,
                    double* out) {
     const GridDims& g = ctx->g;
-    VR_LAUNCH(ctx, "sl_adjoint_step", k_advect<true><<<pgrid(g), kThreads, 0, ctx->stream>>>(f, dep3, factor, out, g));
+    const Tile t = tile_of(g);
+    VR_TILE_LAUNCH(ctx, "sl_adjoint_step", k_advect<true>, f, dep3, factor, out, g, t);
 }
 
 void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double hdt,
@@ -336,19 +558,21 @@ void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double
 void sl_incstate_step(vr_ctx* ctx, const double* src, const double* dep3, const double* gm,
                       const double* vt3, double hdt, double* dst, int mode) {
     const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
     if (mode == 0)
-        VR_LAUNCH(ctx, "sl_incstate_step", k_incstate_step<0><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, gm, vt3, dst, g, hdt));
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", k_incstate_step<0>, src, dep3, gm, vt3, dst, g, t, hdt);
     else
-        VR_LAUNCH(ctx, "sl_incstate_step", k_incstate_step<1><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, gm, vt3, dst, g, hdt));
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", k_incstate_step<1>, src, dep3, gm, vt3, dst, g, t, hdt);
 }
 
 void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const double* factor,
                      double* dst, const double* gm, double w, double* b3) {
     const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
     if (b3)
-        VR_LAUNCH(ctx, "sl_adjoint_step_acc", k_adjoint_step<true><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, factor, dst, gm, w, b3, g));
+        VR_TILE_LAUNCH(ctx, "sl_adjoint_step_acc", k_adjoint_step<true>, src, dep3, factor, dst, gm, w, b3, g, t);
     else
-        VR_LAUNCH(ctx, "sl_adjoint_step", k_adjoint_step<false><<<pgrid(g), kThreads, 0, ctx->stream>>>(src, dep3, factor, dst, nullptr, 0.0, nullptr, g));
+        VR_TILE_LAUNCH(ctx, "sl_adjoint_step", k_adjoint_step<false>, src, dep3, factor, dst, nullptr, 0.0, nullptr, g, t);
 }
 
 void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const double* gm,

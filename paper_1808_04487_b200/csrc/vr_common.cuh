@@ -59,6 +59,7 @@ struct GridDims {
     long long N;       // n1*n2*n3
     long long NC;      // n1*n2*nh spectral bins
     double h1, h2, h3; // two_pi / n_a, exactly as Grid3::spacing
+    int sl_mode;       // semi-Lagrangian gather variant (VR_SL_MODE; see sl.cu)
 };
 
 // Signed FFT frequency / odd-derivative frequency (grid.hpp:58-64)

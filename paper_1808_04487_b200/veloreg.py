@@ -423,8 +423,10 @@ class EvalState:
         return self.get(_lib.STATE_M_HISTORY)
 
     def close(self):
+        # the C state points at its objective and context: only destroy it while both live
         if getattr(self, "_h", None):
-            _lib.call("vr_state_destroy", self._h)
+            if getattr(self.obj, "_h", None) and getattr(self.obj.ctx, "_h", None):
+                _lib.call("vr_state_destroy", self._h)
             self._h = None
 
     def __del__(self):
@@ -500,7 +502,8 @@ class Objective:
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.call("vr_objective_destroy", self._h)
+            if getattr(self.ctx, "_h", None):
+                _lib.call("vr_objective_destroy", self._h)
             self._h = None
 
     def __del__(self):
