@@ -1,0 +1,112 @@
+"""CPU-only: pin the oracle before trusting it.
+
+1. The reference's own doctest suite (proj/tests, compiled unmodified against the
+   FFTW/doctest shims into oracle/_ref) passes: this pins the FFTW shim and the
+   compiled reference by the reference's known-answer and property tests.
+2. The numpy restatement (oracle/veloreg_np.py) reproduces the golden vectors
+   generated from the compiled reference (tests/golden/make_golden.py).
+3. Where the compiled reference is present, the restatement matches it on
+   fresh seeded inputs too.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import periodic_diff, rel_l2
+from oracle import veloreg_np as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_BIN = os.path.join(ROOT, "oracle", "_ref")
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.mark.parametrize("suite", ["test_fields", "test_transport", "test_objective", "test_solver",
+                                   "test_precond"])
+def test_reference_suite_passes(suite):
+    exe = os.path.join(REF_BIN, suite)
+    if not os.path.exists(exe):
+        pytest.skip("reference test binaries not built (make -C oracle tests)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "0 failed" in r.stdout
+
+
+def test_reference_postprocess_suite_known_failures():
+    # postprocess is out of the hot-path scope; 2 of its 7 cases fail with the
+    # reference's own tolerances (det-grad FD oracle, label flips); pinned here
+    exe = os.path.join(REF_BIN, "test_postprocess")
+    if not os.path.exists(exe):
+        pytest.skip("reference test binaries not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert "test cases: 7 | 5 passed | 2 failed" in r.stdout
+
+
+@pytest.fixture(scope="module", params=["16", "8x16x32"])
+def gold(request):
+    return dict(np.load(os.path.join(GOLD, f"golden_{request.param}.npz")))
+
+
+def test_np_fft_and_spectral_vs_golden(gold):
+    f, v = gold["f"], gold["v"]
+    assert rel_l2(O.fft_forward(f).view(np.float64), gold["fft_r2c"].view(np.float64)) < 1e-13
+    assert rel_l2(O.gradient(f), gold["gradient"]) < 1e-12
+    assert rel_l2(O.divergence(v), gold["divergence"]) < 1e-12
+    assert rel_l2(O.laplacian(f), gold["laplacian"]) < 1e-12
+    assert rel_l2(O.gaussian_smooth(f, (1.0, 2.0, 1.5)), gold["gaussian_1_2_1p5"]) < 1e-12
+    for kind, nm in ((0, "h1"), (1, "h2"), (2, "h3"), (3, "helmholtz")):
+        for mode, mn in ((0, "apply"), (1, "inverse"), (2, "inverse_sqrt")):
+            out = O.apply_reg_operator(v, kind, mode, 3e-2, gamma=0.7)
+            assert rel_l2(out, gold[f"reg_{nm}_{mn}"]) < 1e-12, (nm, mn)
+    assert rel_l2(O.apply_projection(v, O.INCOMPRESSIBLE), gold["leray"]) < 1e-12
+    assert rel_l2(O.apply_projection(v, O.NEAR_INCOMPRESSIBLE, 1e-3, 1e-4), gold["nearinc"]) < 1e-12
+
+
+def test_np_transport_vs_golden(gold):
+    assert rel_l2(O.tricubic_interpolate(gold["f"], gold["pts"]), gold["tricubic"]) < 1e-13
+    mT, vs = gold["syn_mT"], gold["syn_v"]
+    assert periodic_diff(O.trace_characteristics(vs, 4, "backward"), gold["trace_bwd"]).max() < 1e-13
+    assert periodic_diff(O.trace_characteristics(vs, 4, "forward"), gold["trace_fwd"]).max() < 1e-13
+    assert rel_l2(O.solve_state(mT, vs, 4), gold["state"]) < 1e-13
+
+
+@pytest.mark.parametrize("name,kw", [("h2", dict()),
+                                     ("h1div", dict(kind=O.H1, beta_v=1e-3, projection=O.NEAR_INCOMPRESSIBLE,
+                                                    div_penalty=True))])
+def test_np_objective_vs_golden(gold, name, kw):
+    o = O.Objective(gold["syn_mR"], gold["syn_mT"], **kw)
+    s = o.evaluate(0.5 * gold["syn_v"])
+    J, mis, rel = gold[f"obj_{name}_J"]
+    assert abs(s["objective"] - J) <= 1e-12 * abs(J)
+    assert abs(s["mismatch"] - mis) <= 1e-12 * abs(mis)
+    g = o.compute_gradient(s)
+    assert rel_l2(g, gold[f"obj_{name}_grad"]) < 1e-11
+    assert rel_l2(s["factor"], gold[f"obj_{name}_factor"]) < 1e-12
+    assert rel_l2(o.hessian_matvec(s, gold["vt"]), gold[f"obj_{name}_matvec"]) < 1e-11
+    assert o.counters["pde_solves"] == 4
+
+
+def test_np_gn_solve_vs_golden(gold):
+    res = O.gauss_newton_solve(gold["syn_mR"], gold["syn_mT"], np.zeros_like(gold["syn_v"]), dict(), eps_opt=1e-2)
+    it, mis, grel, nmv, npde = gold["gn_report"]
+    assert res["outer_iterations"] == int(it)
+    assert abs(res["final_mismatch_rel"] - mis) <= 1e-6 * mis
+    assert abs(res["final_grad_rel"] - grel) <= 1e-6 * grel
+    assert [r["inner_iterations"] for r in res["records"]] == list(gold["gn_inner"])
+    assert res["counters"]["hessian_matvecs"] == int(nmv) and res["counters"]["pde_solves"] == int(npde)
+    assert rel_l2(res["v"], gold["gn_v"]) < 1e-9
+
+
+def test_np_vs_compiled_reference_fresh_inputs(ref):
+    shape = (16, 8, 16)
+    f = ref.random_rough_scalar(shape, 99)
+    v = ref.random_smooth_vector(shape, 2, 77, 0.6)
+    assert rel_l2(O.gradient(f), ref.gradient(f)) < 1e-12
+    assert rel_l2(O.solve_state(f, v, 3), ref.solve_state(f, v, 3)) < 1e-12
+    hist = ref.solve_state(f, v, 4)
+    vt = ref.random_smooth_vector(shape, 2, 78, 1.0)
+    assert rel_l2(O.solve_inc_state(hist, v, vt, 4)[1:], ref.solve_inc_state(hist, v, vt, 4)[1:]) < 1e-11
+    term = ref.random_smooth_scalar(shape, 2, 31, 1.0)
+    init, hist_r = ref.solve_adjoint(term, v, 4, needs_history=True)
+    assert rel_l2(O.solve_adjoint(term, v, 4), hist_r) < 1e-12
