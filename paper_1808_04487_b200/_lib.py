@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libveloreg_gpu.so")
+LIB_PATH = os.environ.get("VR_LIB", os.path.join(_HERE, "libveloreg_gpu.so"))
 
 # ---- error hierarchy mirroring veloreg::Error (proj/include/veloreg/errors.hpp:9-67)
 

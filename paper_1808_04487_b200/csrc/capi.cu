@@ -154,9 +154,10 @@ int vr_ctx_create(int n1, int n2, int n3, int device, vr_ctx** out) {
             g.h1 = vr::kTwoPi / n1;
             g.h2 = vr::kTwoPi / n2;
             g.h3 = vr::kTwoPi / n3;
-            const char* slm = std::getenv("VR_SL_MODE");
-            g.sl_mode = slm ? std::atoi(slm) : 1;
             VR_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            VR_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+            VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
             // keep freed blocks cached in the stream-ordered pool (no OS round trips)
             cudaMemPool_t pool;
             VR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -190,6 +191,10 @@ int vr_ctx_destroy(vr_ctx* ctx) {
         cudaFreeHost(ctx->red_host);
         cudaFree(ctx->flag_dev);
         cudaFreeHost(ctx->flag_host);
+        if (ctx->side) cudaStreamSynchronize(ctx->side);
+        if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+        if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+        if (ctx->side) cudaStreamDestroy(ctx->side);
         if (ctx->stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });

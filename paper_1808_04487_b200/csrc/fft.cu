@@ -776,4 +776,30 @@ void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm
         spectral_scalar_op(ctx, in3 + c * N, out3 + c * N, mp, add3 ? add3 + c * N : nullptr);
 }
 
+void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mode, double beta) {
+    const GridDims& g = ctx->g;
+    MultParams mp;
+    mp.kind = Mult::reg;
+    mp.reg_kind = norm.kind;
+    mp.reg_mode = mode;
+    mp.gamma = norm.gamma;
+    mp.helm_sq = norm.helmholtz_squared;
+    mp.beta = beta;
+    MultDev none{}, m = to_dev(mp);
+    for (int c = 0; c < 3; ++c) {
+        auto* s = reinterpret_cast<double2*>(spec_buf(ctx, 4 + c));
+        launch_rows(ctx, true, in3 + c * g.N, s, 1.0, nullptr);
+        launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+        launch_axis<-1, 1>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, m);
+        launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+    }
+}
+
+void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3) {
+    const GridDims& g = ctx->g;
+    for (int c = 0; c < 3; ++c)
+        launch_rows(ctx, false, spec_buf(ctx, 4 + c), out3 + c * g.N, 1.0 / static_cast<double>(g.N),
+                    add3 ? add3 + c * g.N : nullptr);
+}
+
 }  // namespace vr

@@ -194,6 +194,9 @@ void objective_gradient(vr_objective* o, vr_state* s) {
     const int nt = s->nt;
     const double dt = 1.0 / nt;
     if (!s->grad) s->grad = dev_alloc(ctx, 3 * N);
+    on_side_stream(ctx, [&] {  // beta_v A v overlaps the adjoint sweep
+        op_reg_begin(ctx, s->v, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+    });
 
     // terminal lambda = m_R - m_nt and the observer at j = nt (objective.cpp:91-99)
     double* lam[2] = {o->ws_tmp, o->ws_tmp + N};
@@ -209,7 +212,8 @@ void objective_gradient(vr_objective* o, vr_state* s) {
     if (o->model.projection != VR_PROJ_IDENTITY)
         op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
     // g = b + beta_v A v (objective.cpp:106-110), the add fused into the c2r epilogue
-    op_reg(ctx, s->v, s->grad, o->model.norm, VR_REGOP_APPLY, o->model.beta_v, b);
+    join_side(ctx);
+    op_reg_finish(ctx, s->grad, b);
     s->has_gradient = true;
     o->counters.gradient_evals += 1;
 }
@@ -226,6 +230,12 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     const double dt = 1.0 / nt;
     const double hdt = 0.5 / nt;
     VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, sizeof(int), ctx->stream));
+    // beta_v A vt depends only on vt: its FFT passes (HBM-bound) run on the side
+    // stream under the L1-bound transport sweeps; only the c2r + add waits for b
+    if (add_reg)
+        on_side_stream(ctx, [&] {
+            op_reg_begin(ctx, vt3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+        });
 
     // incremental state (transport.cpp:150-173), terminal = -mt_nt into lam[nt]
     double* tmp[2] = {o->ws_tmp, o->ws_tmp + N};
@@ -249,9 +259,10 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     if (o->model.projection != VR_PROJ_IDENTITY)
         op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
     o->counters.hessian_matvecs += 1;
-    if (add_reg)
-        op_reg(ctx, vt3, out3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v, b);
-    else
+    if (add_reg) {
+        join_side(ctx);
+        op_reg_finish(ctx, out3, b);  // out = b + beta_v A vt (objective.cpp:118-120)
+    } else
         VR_CUDA(cudaMemcpyAsync(out3, b, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
     VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, sizeof(int), cudaMemcpyDeviceToHost,

@@ -24,6 +24,9 @@ namespace {
 
 constexpr int kTileThreads = 256;
 constexpr int kThreads = 256;  // pointwise kernels
+#ifndef VR_SL_MINB
+#define VR_SL_MINB 3  // min resident CTAs/SM for the gather kernels (80-register cap)
+#endif
 
 // cubic_weights (interp.hpp:12-18)
 __device__ __forceinline__ void cubic_weights(double s, double* w) {
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
 
 // continuity_factor (transport.cpp:44-55)
 template <bool BIG>
-__global__ void __launch_bounds__(kTileThreads, 3)
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     k_factor(const double* __restrict__ div, const double* __restrict__ dep,
              double* __restrict__ factor, GridDims g, Tile t, double half_dt) {
     int i1, i2, i3;
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(kTileThreads, 3)
 
 // advect_step / continuity_step (transport.cpp:57-68)
 template <bool FACTOR, bool BIG>
-__global__ void __launch_bounds__(kTileThreads, 3)
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     k_advect(const double* __restrict__ f, const double* __restrict__ dep,
              const double* __restrict__ factor, double* __restrict__ out, GridDims g, Tile t) {
     int i1, i2, i3;
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(kThreads)
 //   mt_{j+1} = I[tmp_j](X_bwd) - hdt q_{j+1};  MODE 0: tmp_{j+1} = mt_{j+1} - hdt q_{j+1}
 //   MODE 1 (last step): terminal = -mt_nt (objective.cpp:138-140)
 template <int MODE, bool BIG>
-__global__ void __launch_bounds__(kTileThreads, 3)
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     k_incstate_step(const double* __restrict__ src, const double* __restrict__ dep,
                     const double* __restrict__ gm, const double* __restrict__ vt,
                     double* __restrict__ dst, GridDims g, Tile t, double hdt) {
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(kTileThreads, 3)
 
 // continuity step + optional fused accumulation b_a += (w * lam) * d_a m_j
 template <bool ACC, bool BIG>
-__global__ void __launch_bounds__(kTileThreads, 3)
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     k_adjoint_step(const double* __restrict__ src, const double* __restrict__ dep,
                    const double* __restrict__ factor, double* __restrict__ dst,
                    const double* __restrict__ gm, double w, double* __restrict__ b, GridDims g,

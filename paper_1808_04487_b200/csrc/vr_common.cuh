@@ -59,7 +59,6 @@ struct GridDims {
     long long N;       // n1*n2*n3
     long long NC;      // n1*n2*nh spectral bins
     double h1, h2, h3; // two_pi / n_a, exactly as Grid3::spacing
-    int sl_mode;       // semi-Lagrangian gather variant (VR_SL_MODE; see sl.cu)
 };
 
 // Signed FFT frequency / odd-derivative frequency (grid.hpp:58-64)
@@ -83,7 +82,9 @@ struct FftPlan;
 
 struct vr_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;   // all public calls are ordered on this stream
+    cudaStream_t side = nullptr;     // internal: overlaps independent spectral work
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     vr::GridDims g{};
     vr::FftPlan* fft = nullptr;
     // lazily allocated scratch: spectra (NC complex) and real fields (N doubles)
@@ -197,6 +198,28 @@ void op_projection(vr_ctx* ctx, const double* in3, double* out3, int kind, doubl
                    double beta_w);
 void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm, int mode,
             double beta, const double* add3 = nullptr);
+// split form of op_reg for overlap: begin leaves the three x2-inverse-transformed
+// spectra in spec_buf(ctx, 4..6); finish runs the c2r passes with out = add + x/N
+void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mode, double beta);
+void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3);
+// run `fn` (which launches on ctx->stream) on the side stream, forked from the
+// current point of ctx->stream; join_side() makes ctx->stream wait for it
+template <class Fn>
+void on_side_stream(vr_ctx* ctx, Fn&& fn) {
+    VR_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    VR_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->side;
+    try {
+        fn();
+    } catch (...) {
+        ctx->stream = main;
+        throw;
+    }
+    ctx->stream = main;
+    VR_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+}
+inline void join_side(vr_ctx* ctx) { VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0)); }
 double reg_symbol(const vr_regnorm& n, double k2);
 
 // ---- semi-Lagrangian (sl.cu) ----
