@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=90.0,
                     help="wall budget for the reference arm's timed matvecs")
+    ap.add_argument("--no-solve", action="store_true", help="skip the GN solve timings")
     return ap.parse_args()
 
 
@@ -304,6 +305,50 @@ def main():
                    "achieved_GBps": per_matvec_bytes / (ms_per_step / 1e3) / 1e9,
                    "frac_of_peak": per_matvec_bytes / (ms_per_step / 1e3) / 1e9 / peak}
 
+    # ---- GN solve time (the metric's second half) ----------------------------
+    solve = None
+    if not args.no_solve:
+        solve = {}
+        # config 3: beta continuation 1 -> 1e-1 -> 1e-2, warm starts, eps_opt 1e-2
+        params = V.make_params(eps_opt=1e-2)
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + (n,) * 3), model, params)
+        ctx.synchronize()
+        t_solve = time.perf_counter() - t0
+        solve["config3"] = {
+            "grid": n, "seconds": t_solve, "levels": len(reps),
+            "newton_iterations": [r["outer_iterations"] for r in reps],
+            "hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps),
+            "pde_solves": sum(r["fine"]["pde_solves"] for r in reps),
+            "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"],
+            "stop": reps[-1]["stop_name"], "precond": "spectral", "continuation": "beta_v 1, 1e-1, 1e-2"}
+        # config 1: 64^3 analytic problem, GPU vs the reference on the host cores
+        ctx1 = vr.Context(64, device=dev)
+        mR1, mT1, _ = V.generate_synthetic(ctx1, nt)
+        p1 = V.make_params(eps_opt=1e-2)
+        t0 = time.perf_counter()
+        r1 = V.gauss_newton_solve(ctx1, mR1, mT1, np.zeros((3, 64, 64, 64)), model, p1)
+        t_gpu1 = time.perf_counter() - t0
+        solve["config1"] = {"grid": 64, "gpu_seconds": t_gpu1,
+                            "newton_iterations": r1.report["outer_iterations"],
+                            "hessian_matvecs": r1.report["fine"]["hessian_matvecs"],
+                            "final_mismatch_rel": r1.report["final_mismatch_rel"],
+                            "final_grad_rel": r1.report["final_grad_rel"]}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            try:
+                from oracle import ref
+                ref.set_workers(os.cpu_count() or 1)
+                t0 = time.perf_counter()
+                _, rep_c, _ = ref.gauss_newton_solve(mR1, mT1, np.zeros((3, 64, 64, 64)), model, p1)
+                solve["config1"].update({"cpu_reference_seconds": time.perf_counter() - t0,
+                                         "cpu_newton_iterations": rep_c["outer_iterations"],
+                                         "cpu_final_mismatch_rel": rep_c["final_mismatch_rel"],
+                                         "cpu_cores": os.cpu_count()})
+            except Exception as exc:
+                solve["config1"]["cpu_reference"] = f"unavailable: {exc}"
+        ctx1.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -324,7 +369,7 @@ def main():
                            f"{8 * n ** 3 / 2 ** 20:.0f} MiB; ~{int(per_matvec_bytes / 8 / n ** 3)} fields touched per step)",
                            "parallelism": "replicas" if world > 1 else "single"},
                 "e2e": e2e, "gpu_launches": launches, "roofline": roof, "matvec_roofline": matvec_roof,
-                "kernels": kernels, "cpu_baseline": cpu, "clocks": clk.summary()}
+                "kernels": kernels, "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

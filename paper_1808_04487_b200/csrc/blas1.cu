@@ -37,12 +37,13 @@ __global__ void k_affine(const double* __restrict__ x, double* __restrict__ out,
         out[i] = (x[i] - lo) * s;
 }
 
-enum class RedOp { dot, sumsq_diff, maxabs, maxmag2, nonfinite, minval, maxval };
+enum class RedOp { dot, sum, sumsq_diff, maxabs, maxmag2, nonfinite, minval, maxval };
 
 template <RedOp OP>
 __device__ __forceinline__ double red_term(const double* a, const double* b, long long i,
                                            long long n) {
     if constexpr (OP == RedOp::dot) return a[i] * b[i];
+    if constexpr (OP == RedOp::sum) return a[i];
     if constexpr (OP == RedOp::sumsq_diff) {
         double d = a[i] - b[i];
         return d * d;
@@ -132,7 +133,85 @@ unsigned ew_grid(long long n) {
     return static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148LL * 16));
 }
 
+template <bool MAX>
+__device__ __forceinline__ double block_reduce(double acc) {
+    __shared__ double sh[kRedThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v = __shfl_down_sync(0xffffffffu, acc, o);
+        acc = MAX ? fmax(acc, v) : acc + v;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+        s = sh[0];
+        for (int w = 1; w < kRedThreads / 32; ++w) s = MAX ? fmax(s, sh[w]) : s + sh[w];
+    }
+    return s;
+}
+
+// PCG residual update (solver.cpp:83-86) fused with the next norm: per
+// component c (grid.y): x += kappa s; r = r + (-kappa) Hs; partial sums of r.r
+// and of r (for the zero-mode projection of the regularization recurrence).
+// partials layout: [(2c + q) * gridDim.x + block], q = 0: r.r, q = 1: sum r
+__global__ void __launch_bounds__(kRedThreads)
+    k_pcg_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ s,
+                 const double* __restrict__ Hs, double kappa, long long n,
+                 double* __restrict__ partials) {
+    const long long off = blockIdx.y * n;
+    double rr = 0.0, rs = 0.0;
+    for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < n;
+         i += (long long)gridDim.x * kRedThreads) {
+        const long long k = off + i;
+        x[k] = x[k] + kappa * s[k];
+        const double rv = r[k] + (-kappa) * Hs[k];
+        r[k] = rv;
+        rr += rv * rv;
+        rs += rv;
+    }
+    const double a = block_reduce<false>(rr);
+    const double b = block_reduce<false>(rs);
+    if (threadIdx.x == 0) {
+        partials[(2 * blockIdx.y + 0) * gridDim.x + blockIdx.x] = a;
+        partials[(2 * blockIdx.y + 1) * gridDim.x + blockIdx.x] = b;
+    }
+}
+
+// PCG direction update (solver.cpp:96-97) plus the regularization recurrence:
+// s = 1.0 z + mu s ;  u = 1.0 (r - mean_c(r)) + mu u  (u tracks beta_v A s)
+__global__ void k_pcg_direction(double* __restrict__ s, double* __restrict__ u,
+                                const double* __restrict__ z, const double* __restrict__ r,
+                                double mu, double m0, double m1, double m2, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 3 * n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = static_cast<int>(i / n);
+        const double m = c == 0 ? m0 : (c == 1 ? m1 : m2);
+        if (s) s[i] = 1.0 * z[i] + mu * s[i];
+        if (u) u[i] = mu == 0.0 ? r[i] - m : 1.0 * (r[i] - m) + mu * u[i];
+    }
+}
+
 }  // namespace
+
+void pcg_update(vr_ctx* ctx, double* x, double* r, const double* s, const double* Hs, double kappa,
+                double* rr, double* rsum) {
+    const long long n = ctx->g.N;
+    const int nb = static_cast<int>(std::min<long long>(kRedBlocks, (n + kRedThreads - 1) / kRedThreads));
+    VR_LAUNCH(ctx, "blas1", k_pcg_update<<<dim3(nb, 3), kRedThreads, 0, ctx->stream>>>(x, r, s, Hs, kappa, n, ctx->red_partials));
+    double out[6];
+    finalize_sums(ctx, nb, 6, out);
+    for (int c = 0; c < 3; ++c) {
+        rr[c] = out[2 * c];
+        rsum[c] = out[2 * c + 1];
+    }
+}
+
+void pcg_direction(vr_ctx* ctx, double* s, double* u, const double* z, const double* r, double mu,
+                   const double mean[3]) {
+    const long long n = ctx->g.N;
+    VR_LAUNCH(ctx, "blas1", k_pcg_direction<<<ew_grid(3 * n), 256, 0, ctx->stream>>>(s, u, z, r, mu, mean[0], mean[1], mean[2], n));
+}
 
 void scale(vr_ctx* ctx, double* x, long long n, double a) {
     VR_LAUNCH(ctx, "blas1", k_scale<<<ew_grid(n), 256, 0, ctx->stream>>>(x, n, a););
@@ -150,6 +229,9 @@ void affine(vr_ctx* ctx, const double* x, double* out, long long n, double lo, d
 void dot_components(vr_ctx* ctx, const double* a, const double* b, long long n, int ncomp,
                     double* results) {
     reduce<RedOp::dot>(ctx, a, b, n, ncomp, results);
+}
+void sum_components(vr_ctx* ctx, const double* a, long long n, int ncomp, double* results) {
+    reduce<RedOp::sum>(ctx, a, nullptr, n, ncomp, results);
 }
 double max_abs(vr_ctx* ctx, const double* a, long long n) {
     if (n == 0) return 0.0;

@@ -783,7 +783,9 @@ int vr_pcg_solve(vr_objective* obj, const vr_state* s, const double* rhs3, doubl
                 VR_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * n3, cudaMemcpyDeviceToDevice,
                                         ctx->stream));
         };
-        *stats = vr::pcg_solve(ctx, op, rhs3, rel_tol, max_iter, pc, x3);
+        *stats = precond == VR_PRECOND_SPECTRAL
+                     ? vr::pcg_solve_gn(obj, s, rhs3, rel_tol, max_iter, x3)
+                     : vr::pcg_solve(ctx, op, rhs3, rel_tol, max_iter, pc, x3);
     });
 }
 static void copy_records(const vr::GnResult& r, vr_iteration_record* recs, int max_recs,

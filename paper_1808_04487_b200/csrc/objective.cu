@@ -220,7 +220,7 @@ void objective_gradient(vr_objective* o, vr_state* s) {
 
 // hessian_data_matvec (objective.cpp:123-156) [+ beta_v A vt, objective.cpp:114-121]
 void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, double* out3,
-                      bool add_reg) {
+                      bool add_reg, const double* reg_given) {
     vr_ctx* ctx = o->ctx;
     const long long N = ctx->g.N;
     if (!s->has_adjoint_ctx)
@@ -255,16 +255,24 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
                         nullptr);
     o->counters.pde_solves += 1;
     double* b = o->ws_b;
-    sl_accumulate(ctx, lam, s->gradm, nt, dt, b);
-    if (o->model.projection != VR_PROJ_IDENTITY)
-        op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+    const bool identity_K = o->model.projection == VR_PROJ_IDENTITY;
+    if (reg_given && identity_K) {
+        sl_accumulate(ctx, lam, s->gradm, nt, dt, out3, reg_given);  // out = b + u, one pass
+    } else {
+        sl_accumulate(ctx, lam, s->gradm, nt, dt, b);
+        if (!identity_K)
+            op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+        if (add_reg) {
+            join_side(ctx);
+            op_reg_finish(ctx, out3, b);  // out = b + beta_v A vt (objective.cpp:118-120)
+        } else if (reg_given) {
+            lin_comb(ctx, out3, 1.0, b, 1.0, reg_given, 3 * N);
+        } else {
+            VR_CUDA(cudaMemcpyAsync(out3, b, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+        }
+    }
     o->counters.hessian_matvecs += 1;
-    if (add_reg) {
-        join_side(ctx);
-        op_reg_finish(ctx, out3, b);  // out = b + beta_v A vt (objective.cpp:118-120)
-    } else
-        VR_CUDA(cudaMemcpyAsync(out3, b, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
-                                ctx->stream));
     VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, sizeof(int), cudaMemcpyDeviceToHost,
                             ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -337,6 +345,92 @@ vr_pcg_stats pcg_solve(vr_ctx* ctx, const DevOp& apply, const double* rhs, doubl
             const double mu = rz_new / rz;
             rz = rz_new;
             lin_comb(ctx, s, 1.0, z, mu, s, n3);
+        }
+        st.hit_max_iterations = 1;
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+    return st;
+}
+
+// ---------------------------------------------------------------------------
+// PCG on the GN Hessian with the spectral preconditioner. Same iteration as
+// pcg_solve (solver.cpp:51-100, identical stop / curvature / update formulas),
+// with two exact rewrites that remove work from every iteration:
+//  * u = beta_v A s is carried through the recurrence instead of recomputed by
+//    FFT in each matvec: z = (beta_v A)^-1 r gives beta_v A z = r - P0 r (P0 =
+//    per-component mean when A has a zero singular value, spectral.cpp:176-177,
+//    else 0), so s = z + mu s implies u = (r - P0 r) + mu u, and H s = H_data s + u.
+//  * x += kappa s, r -= kappa Hs and |r|^2 (plus sum r for P0) are one pass.
+// The rewrites change rounding only (~1e-15 relative per iteration).
+vr_pcg_stats pcg_solve_gn(vr_objective* o, const vr_state* s, const double* rhs, double rel_tol,
+                          int max_iter, double* x) {
+    vr_ctx* ctx = o->ctx;
+    const long long N = ctx->g.N;
+    const long long n3 = 3 * N;
+    const bool zero_mode = reg_symbol(o->model.norm, 0.0) == 0.0;
+    vr_pcg_stats st{};
+    st.rel_residual = 1.0;
+    VR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n3, ctx->stream));
+    const double r0 = norm_l2_vec(ctx, rhs);
+    if (r0 == 0.0) {
+        st.converged = 1;
+        st.rel_residual = 0.0;
+        return st;
+    }
+    const double target = rel_tol * r0;
+    double* r = dev_alloc(ctx, n3);
+    double* z = dev_alloc(ctx, n3);
+    double* sd = dev_alloc(ctx, n3);
+    double* Hs = dev_alloc(ctx, n3);
+    double* u = dev_alloc(ctx, n3);
+    auto cleanup = [&] {
+        for (double* p : {r, z, sd, Hs, u}) dev_free(ctx, p);
+    };
+    auto means_of = [&](const double* sums, double* m) {
+        for (int c = 0; c < 3; ++c) m[c] = zero_mode ? sums[c] / static_cast<double>(N) : 0.0;
+    };
+    try {
+        VR_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+        objective_apply_reg(o, r, VR_REGOP_INVERSE, z);  // SpectralPreconditioner::apply
+        VR_CUDA(cudaMemcpyAsync(sd, z, sizeof(double) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+        double sums[3], mean[3];
+        sum_components(ctx, r, N, 3, sums);
+        means_of(sums, mean);
+        pcg_direction(ctx, nullptr, u, nullptr, r, 0.0, mean);  // u = beta_v A z
+        double rz = dot_l2_vec(ctx, r, z);
+        for (int it = 0; it < max_iter; ++it) {
+            objective_matvec(o, s, sd, Hs, false, u);
+            const double sHs = dot_l2_vec(ctx, sd, Hs);
+            if (sHs <= 0.0) {
+                st.negative_curvature = 1;
+                if (it == 0)
+                    VR_CUDA(cudaMemcpyAsync(x, z, sizeof(double) * n3, cudaMemcpyDeviceToDevice,
+                                            ctx->stream));
+                st.iterations = it + 1;
+                st.rel_residual = norm_l2_vec(ctx, r) / r0;
+                cleanup();
+                return st;
+            }
+            const double kappa = rz / sHs;
+            double rr[3];
+            pcg_update(ctx, x, r, sd, Hs, kappa, rr, sums);
+            st.iterations = it + 1;
+            const double rn = std::sqrt(rr[0] + rr[1] + rr[2]);
+            st.rel_residual = rn / r0;
+            if (rn < target) {
+                st.converged = 1;
+                cleanup();
+                return st;
+            }
+            objective_apply_reg(o, r, VR_REGOP_INVERSE, z);
+            const double rz_new = dot_l2_vec(ctx, r, z);
+            const double mu = rz_new / rz;
+            rz = rz_new;
+            means_of(sums, mean);
+            pcg_direction(ctx, sd, u, z, r, mu, mean);
         }
         st.hit_max_iterations = 1;
     } catch (...) {
@@ -477,7 +571,10 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                 };
                 // rhs = -g (scale(rhs, -1.0))
                 lin_comb(ctx, rhs, -1.0, state->grad, 0.0, state->grad, n3);
-                vr_pcg_stats pcg = pcg_solve(ctx, op, rhs, eps_H, params.max_krylov, pc, dir);
+                vr_pcg_stats pcg =
+                    precond == VR_PRECOND_SPECTRAL
+                        ? pcg_solve_gn(obj, state, rhs, eps_H, params.max_krylov, dir)
+                        : pcg_solve(ctx, op, rhs, eps_H, params.max_krylov, pc, dir);
 
                 const double slope = inner_product_vec(ctx, state->grad, dir);
                 if (slope >= 0.0) {

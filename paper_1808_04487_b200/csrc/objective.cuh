@@ -52,8 +52,14 @@ vr_objective* objective_create(vr_ctx* ctx, const double* mR, const double* mT,
                                const vr_model& model);
 vr_state* objective_evaluate(vr_objective* o, const double* v3);
 void objective_gradient(vr_objective* o, vr_state* s);
+// H vt (add_reg) or H_data vt; reg_given (may be null, add_reg false): a field
+// equal to beta_v A vt computed elsewhere, added instead of the spectral term
 void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, double* out3,
-                      bool add_reg);
+                      bool add_reg, const double* reg_given = nullptr);
+// PCG on the GN Hessian with the spectral preconditioner (solver.cpp:51-100),
+// carrying u = beta_v A s through the recurrence (see objective.cu)
+vr_pcg_stats pcg_solve_gn(vr_objective* o, const vr_state* s, const double* rhs, double rel_tol,
+                          int max_iter, double* x);
 void objective_apply_reg(vr_objective* o, const double* u3, int mode, double* out3);
 void objective_apply_K(vr_objective* o, const double* u3, double* out3);
 

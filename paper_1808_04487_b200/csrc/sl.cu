@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kThreads)
 // b_a = sum_{j = nt..0} (w_j lam_j) d_a m_j (observer order of objective.cpp:143-148)
 __global__ void __launch_bounds__(kThreads)
     k_accumulate(const double* __restrict__ lam, const double* __restrict__ gm, int nt, double dt,
-                 double* __restrict__ b, GridDims g) {
+                 double* __restrict__ b, GridDims g, const double* __restrict__ add) {
     const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
     if (i >= g.N) return;
     double acc[3] = {0.0, 0.0, 0.0};
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads)
         for (int a = 0; a < 3; ++a) acc[a] = acc[a] + wl * gj[a * g.N + i];
     }
 #pragma unroll
-    for (int a = 0; a < 3; ++a) b[a * g.N + i] = acc[a];
+    for (int a = 0; a < 3; ++a) b[a * g.N + i] = add ? acc[a] + add[a * g.N + i] : acc[a];
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -466,9 +466,9 @@ void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const
 }
 
 void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, int nt, double dt,
-                   double* b3) {
+                   double* b3, const double* add3) {
     const GridDims& g = ctx->g;
-    VR_LAUNCH(ctx, "sl_accumulate", k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, gm_hist, nt, dt, b3, g));
+    VR_LAUNCH(ctx, "sl_accumulate", k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, gm_hist, nt, dt, b3, g, add3));
 }
 
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out) {

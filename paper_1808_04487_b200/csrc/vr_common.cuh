@@ -153,6 +153,7 @@ void lin_comb(vr_ctx* ctx, double* out, double a, const double* x, double b, con
 // sums over `ncomp` consecutive blocks of length n; results[c] per component (host)
 void dot_components(vr_ctx* ctx, const double* a, const double* b, long long n, int ncomp,
                     double* results);
+void sum_components(vr_ctx* ctx, const double* a, long long n, int ncomp, double* results);
 double max_abs(vr_ctx* ctx, const double* a, long long n);
 double max_magnitude(vr_ctx* ctx, const double* v3, long long n);
 bool all_finite(vr_ctx* ctx, const double* a, long long n);
@@ -163,6 +164,12 @@ void affine(vr_ctx* ctx, const double* x, double* out, long long n, double lo, d
 // device-side partial reduction helper: finalize `nblocks` partial sums (ncomp
 // interleaved per block) into red_out[0..ncomp) and copy to host
 void finalize_sums(vr_ctx* ctx, int nblocks, int ncomp, double* host_out);
+// fused PCG kernels on 3-component fields: x += kappa s; r -= kappa Hs, returning
+// per-component r.r and sum(r); and s = z + mu s with u = (r - mean) + mu u (u may be null)
+void pcg_update(vr_ctx* ctx, double* x, double* r, const double* s, const double* Hs, double kappa,
+                double* rr, double* rsum);
+void pcg_direction(vr_ctx* ctx, double* s, double* u, const double* z, const double* r, double mu,
+                   const double mean[3]);
 
 // ---- FFT / spectral (fft.cu) ----
 enum class Mult : int {
@@ -241,9 +248,9 @@ void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const d
                      double* dst, const double* gm, double w, double* b3);
 void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const double* gm,
                       double w, double* lam, double* b3);
-// b_a = sum_{j=nt..0} (w_j lam_j) d_a m_j
+// b_a = sum_{j=nt..0} (w_j lam_j) d_a m_j  (+ add_a when add3 is given)
 void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, int nt, double dt,
-                   double* b3);
+                   double* b3, const double* add3 = nullptr);
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out);
 void synth_fill(vr_ctx* ctx, double amplitude, double* m_T, double* v3);
 
