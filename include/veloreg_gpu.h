@@ -312,6 +312,35 @@ int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T,
                               double* v_out, vr_solve_report* reports, int max_levels,
                               int* n_levels, vr_iteration_record* records, int max_records);
 
+/* ---- x1-slab decomposition across GPUs (no reference counterpart:
+ * the reference is single-process, the paper's CLAIRE used MPI pencils,
+ * PAPER.md:475-479). Rank r of P owns planes [r n1/P, (r+1) n1/P); n1 and n2 must
+ * be divisible by P. Field arguments of the objective / solver entry points are
+ * then this rank's slab (n1/P x n2 x n3, same row-major layout); reductions
+ * return global values on every rank. Per-operator entry points (FFT, tricubic,
+ * transport solves) stay one-GPU only and raise ArgumentError on a slab ctx.
+ * `halo` = x1 planes exchanged on each side of every gathered field; it must
+ * cover the largest per-step x1 displacement + 4 (checked per velocity). */
+/* NCCL unique id (128 bytes) created on one rank and broadcast by the caller */
+int vr_nccl_unique_id(unsigned char out[128]);
+/* one process per GPU: NCCL communicator over nranks, this process = rank */
+int vr_ctx_create_dist(int n1, int n2, int n3, int device, int rank, int nranks,
+                       const unsigned char uid[128], int halo, vr_ctx** out);
+int vr_ctx_slab(const vr_ctx* ctx, int* rank, int* nranks, int* planes, int* first_plane,
+                int* halo);
+/* Self tests of the slab path on ONE GPU: P virtual ranks (host threads, device
+ * copies between host barriers, no cross-rank kernel waits) run on slabs of the
+ * global HOST inputs; outputs are assembled into global HOST arrays.
+ * scalars[5] = J, mismatch, mismatch_rel, ||g||_2, <H vt, vt> (unweighted). */
+int vr_dist_selftest_objective(int P, int n1, int n2, int n3, int device, int halo,
+                               const vr_model* model, const double* m_R, const double* m_T,
+                               const double* v, const double* vt, double* grad_out,
+                               double* matvec_out, double* reg_out, double* scalars);
+int vr_dist_selftest_solve(int P, int n1, int n2, int n3, int device, int halo,
+                           const vr_model* model, const vr_solver_params* params,
+                           const double* m_R, const double* m_T, const double* v0, double* v_out,
+                           vr_solve_report* report);
+
 /* ---- synthetic inputs (synthetic.cpp:10-34) -------------------------------- */
 /* m_T, v* analytic on the grid; m_R = solve_state(m_T, v*, nt).final() on the GPU */
 int vr_generate_synthetic(vr_ctx* ctx, int nt, double amplitude, double* m_R, double* m_T,

@@ -205,6 +205,14 @@ SIGNATURES = {
                                       C.POINTER(SolverParams), I, DP, C.POINTER(SolveReport), I,
                                       C.POINTER(C.c_int), C.POINTER(IterationRecord), I]),
     "vr_generate_synthetic": (I, [P, I, D, DP, DP, DP]),
+    "vr_nccl_unique_id": (I, [C.c_char_p]),
+    "vr_ctx_create_dist": (I, [I, I, I, I, I, I, C.c_char_p, I, C.POINTER(P)]),
+    "vr_ctx_slab": (I, [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                        C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "vr_dist_selftest_objective": (I, [I, I, I, I, I, I, C.POINTER(Model), HP, HP, HP, HP, HP, HP,
+                                       HP, HP]),
+    "vr_dist_selftest_solve": (I, [I, I, I, I, I, I, C.POINTER(Model), C.POINTER(SolverParams),
+                                   HP, HP, HP, HP, C.POINTER(SolveReport)]),
 }
 
 _lib = None

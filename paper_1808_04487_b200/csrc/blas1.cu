@@ -127,6 +127,7 @@ void reduce(vr_ctx* ctx, const double* a, const double* b, long long n, int ncom
                             cudaMemcpyDeviceToHost, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int c = 0; c < ncomp; ++c) host_out[c] = ctx->red_host[c];
+    if (ctx->dist) ctx->dist->allreduce(ctx, host_out, ncomp, is_max<OP>());  // rank order
 }
 
 unsigned ew_grid(long long n) {
@@ -270,6 +271,7 @@ void finalize_sums(vr_ctx* ctx, int nblocks, int ncomp, double* host_out) {
                             cudaMemcpyDeviceToHost, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int c = 0; c < ncomp; ++c) host_out[c] = ctx->red_host[c];
+    if (ctx->dist) ctx->dist->allreduce(ctx, host_out, ncomp, false);
 }
 
 }  // namespace vr

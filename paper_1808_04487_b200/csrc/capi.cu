@@ -46,10 +46,21 @@ void check_ncomp(int ncomp) {
     if (ncomp != 1 && ncomp != 3) vr::throw_argument("ncomp must be 1 or 3");
 }
 bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+// per-operator entry points whose arguments are whole fields in the reference
+// layout: one GPU only (on x1 slabs use the objective / solver entry points)
+void set_dev_single(vr_ctx* ctx, const char* what) {
+    set_dev(ctx);
+    if (ctx->dist) vr::throw_argument(std::string(what) + ": not available on x1 slabs");
+}
 
 }  // namespace
 
 namespace vr {
+
+void set_last_error(int cls, const std::string& msg) {
+    g_err = msg;
+    g_cls = cls;
+}
 
 double* spec_buf(vr_ctx* ctx, int i) {
     if (static_cast<int>(ctx->spec_scratch.size()) <= i) ctx->spec_scratch.resize(i + 1, nullptr);
@@ -125,57 +136,89 @@ int vr_solver_params_validate(const vr_solver_params* p) {
 int vr_ctx_create(int n1, int n2, int n3, int device, vr_ctx** out) {
     return guard([&] {
         need(out, "out");
-        const int d[3] = {n1, n2, n3};
-        for (int a = 0; a < 3; ++a)
-            if (d[a] < 4)
-                vr::throw_dimension("Grid3: every dimension must be >= 4, got " +
-                                    std::to_string(n1) + "x" + std::to_string(n2) + "x" +
-                                    std::to_string(n3));
-        for (int a = 0; a < 3; ++a)
-            if (!pow2(d[a]) || d[a] > 1024)
-                vr::throw_dimension("vr_ctx_create: GPU grids need power-of-two dims <= 1024, got " +
-                                    std::to_string(n1) + "x" + std::to_string(n2) + "x" +
-                                    std::to_string(n3));
-        int count = 0;
-        VR_CUDA(cudaGetDeviceCount(&count));
-        if (device < 0 || device >= count)
-            vr::throw_resource("vr_ctx_create: no CUDA device " + std::to_string(device));
-        VR_CUDA(cudaSetDevice(device));
-        auto* ctx = new vr_ctx();
-        try {
-            ctx->device = device;
-            vr::GridDims& g = ctx->g;
-            g.n1 = n1;
-            g.n2 = n2;
-            g.n3 = n3;
-            g.nh = n3 / 2 + 1;
-            g.N = static_cast<long long>(n1) * n2 * n3;
-            g.NC = static_cast<long long>(n1) * n2 * g.nh;
-            g.h1 = vr::kTwoPi / n1;
-            g.h2 = vr::kTwoPi / n2;
-            g.h3 = vr::kTwoPi / n3;
-            VR_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-            VR_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-            VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-            VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
-            // keep freed blocks cached in the stream-ordered pool (no OS round trips)
-            cudaMemPool_t pool;
-            VR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-            uint64_t thr = UINT64_MAX;
-            VR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-            vr::fft_plan_create(ctx);
-            VR_CUDA(cudaMalloc(&ctx->red_partials, sizeof(double) * vr::kRedBlocks * 8));
-            VR_CUDA(cudaMalloc(&ctx->red_out, sizeof(double) * 8));
-            VR_CUDA(cudaMallocHost(&ctx->red_host, sizeof(double) * 8));
-            VR_CUDA(cudaMalloc(&ctx->flag_dev, sizeof(int) * 4));
-            VR_CUDA(cudaMallocHost(&ctx->flag_host, sizeof(int) * 4));
-        } catch (...) {
-            vr_ctx_destroy(ctx);
-            throw;
-        }
-        *out = ctx;
+        *out = vr::ctx_new(n1, n2, n3, device, nullptr, 0);
     });
 }
+
+}  // extern "C"
+
+namespace vr {
+
+// Grid3 checks (grid.hpp:24-31) plus the GPU FFT domain; with a transport of
+// size P > 1 the context owns the x1 slab of rank t->rank
+vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
+    const int d[3] = {n1, n2, n3};
+    for (int a = 0; a < 3; ++a)
+        if (d[a] < 4)
+            throw_dimension("Grid3: every dimension must be >= 4, got " + std::to_string(n1) +
+                            "x" + std::to_string(n2) + "x" + std::to_string(n3));
+    for (int a = 0; a < 3; ++a)
+        if (!pow2(d[a]) || d[a] > 1024)
+            throw_dimension("vr_ctx_create: GPU grids need power-of-two dims <= 1024, got " +
+                            std::to_string(n1) + "x" + std::to_string(n2) + "x" +
+                            std::to_string(n3));
+    const int P = t ? t->size : 1;
+    if (P > 1) {
+        if (n1 % P != 0 || n2 % P != 0 || n1 / P < 4)
+            throw_argument("x1 slabs: n1 and n2 must be divisible by the rank count, >= 4 planes each");
+        if (halo < 4 || halo > n1 / P)
+            throw_argument("x1 slabs: halo must be in [4, n1/P]");
+    }
+    int count = 0;
+    VR_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+        throw_resource("vr_ctx_create: no CUDA device " + std::to_string(device));
+    VR_CUDA(cudaSetDevice(device));
+    auto* ctx = new vr_ctx();
+    try {
+        ctx->device = device;
+        ctx->dist = P > 1 ? t : nullptr;
+        GridDims& g = ctx->g;
+        g.n1 = n1;
+        g.n2 = n2;
+        g.n3 = n3;
+        g.nh = n3 / 2 + 1;
+        g.dist = P > 1;
+        g.L = n1 / P;
+        g.off1 = (P > 1 ? t->rank : 0) * g.L;
+        g.halo = P > 1 ? halo : 0;
+        g.n2s = n2 / P;
+        g.k2_off = (P > 1 ? t->rank : 0) * g.n2s;
+        g.N = static_cast<long long>(g.L) * n2 * n3;
+        g.NC = static_cast<long long>(g.L) * n2 * g.nh;
+        g.Ng = static_cast<long long>(n1) * n2 * n3;
+        g.h1 = kTwoPi / n1;
+        g.h2 = kTwoPi / n2;
+        g.h3 = kTwoPi / n3;
+        ctx->hstride = static_cast<long long>(g.L + 2 * g.halo) * n2 * n3;
+        VR_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        VR_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        // keep freed blocks cached in the stream-ordered pool (no OS round trips)
+        cudaMemPool_t pool;
+        VR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        VR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        fft_plan_create(ctx);
+        VR_CUDA(cudaMalloc(&ctx->red_partials, sizeof(double) * kRedBlocks * 8));
+        VR_CUDA(cudaMalloc(&ctx->red_out, sizeof(double) * 8));
+        VR_CUDA(cudaMallocHost(&ctx->red_host, sizeof(double) * 8));
+        VR_CUDA(cudaMalloc(&ctx->flag_dev, sizeof(int) * 4));
+        VR_CUDA(cudaMemset(ctx->flag_dev, 0, sizeof(int) * 4));
+        VR_CUDA(cudaMallocHost(&ctx->flag_host, sizeof(int) * 4));
+        g.flags = ctx->flag_dev;
+    } catch (...) {
+        ctx->dist = nullptr;  // the transport belongs to the caller
+        vr_ctx_destroy(ctx);
+        throw;
+    }
+    return ctx;
+}
+
+}  // namespace vr
+
+extern "C" {
 
 int vr_ctx_destroy(vr_ctx* ctx) {
     if (!ctx) return VR_OK;
@@ -196,6 +239,7 @@ int vr_ctx_destroy(vr_ctx* ctx) {
         if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
         if (ctx->side) cudaStreamDestroy(ctx->side);
         if (ctx->stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->owns_dist) delete ctx->dist;
         delete ctx;
     });
 }
@@ -379,17 +423,17 @@ int vr_inner_product(vr_ctx* ctx, const double* a, const double* b, int ncomp, d
 // ---- spectral -------------------------------------------------------------------
 int vr_fft_r2c(vr_ctx* ctx, const double* in, double* out_spectrum) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_fft_r2c");
         vr::fft_r2c(ctx, in, out_spectrum);
     });
 }
 int vr_fft_c2r(vr_ctx* ctx, const double* spectrum, double* out) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_fft_c2r");
         double* s = vr::spec_buf(ctx, 0);
         VR_CUDA(cudaMemcpyAsync(s, spectrum, sizeof(double) * 2 * ctx->g.NC,
                                 cudaMemcpyDeviceToDevice, ctx->stream));
-        vr::fft_c2r(ctx, s, out, 1.0 / static_cast<double>(ctx->g.N), nullptr);
+        vr::fft_c2r(ctx, s, out, 1.0 / static_cast<double>(ctx->g.Ng), nullptr);
     });
 }
 int vr_gradient(vr_ctx* ctx, const double* f, double* out3) {
@@ -462,7 +506,7 @@ int vr_apply_projection(vr_ctx* ctx, const double* f3, double* out3, int kind, d
 }
 int vr_rescale_intensity(vr_ctx* ctx, const double* f, double* out, int* degenerate) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_rescale_intensity");
         const long long N = ctx->g.N;
         const double lo = vr::min_value(ctx, f, N), hi = vr::max_value(ctx, f, N);
         if (hi <= lo) {
@@ -479,36 +523,36 @@ int vr_rescale_intensity(vr_ctx* ctx, const double* f, double* out, int* degener
 int vr_tricubic_interpolate(vr_ctx* ctx, const double* f, const double* pts3, double* out,
                             int nfields) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_tricubic_interpolate");
         vr::sl_tricubic(ctx, f, nfields, pts3, out);
     });
 }
 int vr_trace_characteristics(vr_ctx* ctx, const double* v3, int nt, int direction,
                              double* dep3) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_trace_characteristics");
         if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
         if (!vr::all_finite(ctx, v3, 3 * ctx->g.N))
             vr::throw_numeric("trace_characteristics: velocity has non-finite values");
-        vr::sl_trace(ctx, v3, nt, direction, dep3);
+        vr::sl_trace(ctx, v3, ctx->g.N, nt, direction, dep3);
     });
 }
 int vr_continuity_factor(vr_ctx* ctx, const double* div_v, const double* dep3, double dt,
                          double* factor) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_continuity_factor");
         vr::sl_factor(ctx, div_v, dep3, 0.5 * dt, factor);
     });
 }
 int vr_solve_state(vr_ctx* ctx, const double* m_T, const double* v3, int nt, double* history) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_solve_state");
         const long long N = ctx->g.N;
         if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
         if (!vr::all_finite(ctx, v3, 3 * N))
             vr::throw_numeric("trace_characteristics: velocity has non-finite values");
         double* xb = vr::dev_alloc(ctx, 3 * N);
-        vr::sl_trace(ctx, v3, nt, VR_TRACE_BACKWARD, xb);
+        vr::sl_trace(ctx, v3, ctx->g.N, nt, VR_TRACE_BACKWARD, xb);
         VR_CUDA(cudaMemcpyAsync(history, m_T, sizeof(double) * N, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
         for (int j = 0; j < nt; ++j) vr::sl_advect(ctx, history + j * N, xb, history + (j + 1) * N);
@@ -524,7 +568,7 @@ static void adjoint_like(vr_ctx* ctx, const double* terminal, const double* v3, 
     double* xf = vr::dev_alloc(ctx, 3 * N);
     double* factor = vr::dev_alloc(ctx, N);
     double* work = vr::dev_alloc(ctx, 2 * N);
-    vr::sl_trace(ctx, v3, nt, VR_TRACE_FORWARD, xf);
+    vr::sl_trace(ctx, v3, ctx->g.N, nt, VR_TRACE_FORWARD, xf);
     double* div = vr::field_buf(ctx, 0);
     vr::op_divergence(ctx, v3, div);
     vr::sl_factor(ctx, div, xf, 0.5 / nt, factor);
@@ -550,20 +594,20 @@ static void adjoint_like(vr_ctx* ctx, const double* terminal, const double* v3, 
 int vr_solve_adjoint(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
                      double* history, double* initial) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_solve_adjoint");
         adjoint_like(ctx, terminal, v3, nt, history, initial);
     });
 }
 int vr_solve_inc_adjoint(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
                          double* history, double* initial) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_solve_inc_adjoint");
         adjoint_like(ctx, terminal, v3, nt, history, initial);
     });
 }
 int vr_gradient_dot(vr_ctx* ctx, const double* f, const double* w3, double* out) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_gradient_dot");
         double* gm = vr::dev_alloc(ctx, 3 * ctx->g.N);
         vr::op_gradient(ctx, f, gm);
         vr::sl_gradient_dot(ctx, gm, w3, out);
@@ -575,14 +619,14 @@ int vr_solve_inc_state(vr_ctx* ctx, const double* m_history, const double* v3, c
     // step-by-step restatement of transport.cpp:150-173 (the fused matvec path
     // lives in objective.cu; this entry point returns the whole mt history)
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_solve_inc_state");
         const long long N = ctx->g.N;
         if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
         double* xb = vr::dev_alloc(ctx, 3 * N);
         double* gm = vr::dev_alloc(ctx, 3 * N);
         double* q = vr::dev_alloc(ctx, 2 * N);
         double* tmp = vr::dev_alloc(ctx, N);
-        vr::sl_trace(ctx, v3, nt, VR_TRACE_BACKWARD, xb);
+        vr::sl_trace(ctx, v3, ctx->g.N, nt, VR_TRACE_BACKWARD, xb);
         const double hdt = 0.5 / nt;
         double* qp = q;
         double* qn = q + N;
@@ -686,7 +730,12 @@ int vr_state_get(const vr_state* s, int which, double* out) {
             case VR_STATE_X_BWD: src = s->xb; n = 3 * N; break;
             case VR_STATE_X_FWD: src = s->xf; n = 3 * N; break;
             case VR_STATE_FACTOR: src = s->factor; n = N; break;
-            case VR_STATE_M_HISTORY: src = s->mhist; n = (s->nt + 1) * N; break;
+            case VR_STATE_M_HISTORY:  // halo-padded series: copy slice by slice
+                for (int j = 0; j <= s->nt; ++j)
+                    VR_CUDA(cudaMemcpyAsync(out + j * N, vr::pslice(ctx, s->mhist, j),
+                                            sizeof(double) * N, cudaMemcpyDeviceToDevice,
+                                            ctx->stream));
+                return;
             case VR_STATE_GRADIENT: src = s->has_gradient ? s->grad : nullptr; n = 3 * N; break;
             case VR_STATE_GRAD_M: src = s->gradm; n = 3LL * (s->nt + 1) * N; break;
             default: vr::throw_argument("vr_state_get: unknown field");
@@ -855,14 +904,14 @@ int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T,
 int vr_generate_synthetic(vr_ctx* ctx, int nt, double amplitude, double* m_R, double* m_T,
                           double* v_star) {
     return guard([&] {
-        set_dev(ctx);
+        set_dev_single(ctx, "vr_generate_synthetic");
         need(m_R && m_T && v_star, "vr_generate_synthetic");
         const long long N = ctx->g.N;
         vr::synth_fill(ctx, amplitude, m_T, v_star);
         double* xb = vr::dev_alloc(ctx, 3 * N);
         double* a = vr::dev_alloc(ctx, N);
         double* b = vr::dev_alloc(ctx, N);
-        vr::sl_trace(ctx, v_star, nt, VR_TRACE_BACKWARD, xb);
+        vr::sl_trace(ctx, v_star, ctx->g.N, nt, VR_TRACE_BACKWARD, xb);
         const double* cur = m_T;
         double* bufs[2] = {a, b};
         for (int j = 0; j < nt; ++j) {

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 2)
         fft_line<N, DIR, false, false>(t, tw, load, store, sm);
     } else {
         // x1 pass: column cc = i2 * nh + i3
-        const int i2 = static_cast<int>(cc / g.nh);
+        const int i2 = static_cast<int>(cc / g.nh) + g.k2_off;  // k2-slab on x1 slabs
         const int i3 = static_cast<int>(cc % g.nh);
         auto store_mult = [&](int i, double2 v) { sm(i) = apply_mult(mult_at(m, g, i, i2, i3), v); };
         fft_line<N, -1, false, true>(t, tw, load, store_mult, sm);
@@ -454,24 +454,15 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS, 2)
 }
 
 // --------------------------------------------------------------------------
-// elementwise spectral kernels on full (n1, n2, nh) spectra
+// elementwise spectral kernels on fully transformed spectra in the x1-pass
+// layout [n1][n2s][nh] (== (n1, n2, nh) on one GPU)
 // --------------------------------------------------------------------------
 __device__ __forceinline__ void bin_coords(long long b, const GridDims& g, int& i1, int& i2,
                                            int& i3) {
     i3 = static_cast<int>(b % g.nh);
     long long r = b / g.nh;
-    i2 = static_cast<int>(r % g.n2);
-    i1 = static_cast<int>(r / g.n2);
-}
-
-__global__ void k_spec_mult(const double2* __restrict__ in, double2* __restrict__ out, MultDev m,
-                            GridDims g) {
-    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < g.NC;
-         b += (long long)gridDim.x * blockDim.x) {
-        int i1, i2, i3;
-        bin_coords(b, g, i1, i2, i3);
-        out[b] = apply_mult(mult_at(m, g, i1, i2, i3), in[b]);
-    }
+    i2 = static_cast<int>(r % g.n2s) + g.k2_off;
+    i1 = static_cast<int>(r / g.n2s);
 }
 
 // divergence (spectral.cpp:124-140): acc = sum_a i k_a c_a, deriv_freq
@@ -528,12 +519,6 @@ MultDev to_dev(const MultParams& p) {
     return m;
 }
 
-int ilog2(int n) {
-    int l = 0;
-    while ((1 << l) < n) ++l;
-    return l;
-}
-
 // ---- host-side launchers ----------------------------------------------------
 template <int N, int DIR, int MODE>
 void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inner, long long outer,
@@ -574,7 +559,7 @@ template <int M>
 void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double scale,
                    const double* add) {
     using C = RowCfg<M>;
-    const long long nrows = static_cast<long long>(ctx->g.n1) * ctx->g.n2;
+    const long long nrows = static_cast<long long>(ctx->g.L) * ctx->g.n2;  // local rows
     const unsigned grid = static_cast<unsigned>((nrows + C::RB - 1) / C::RB);
     if (forward) {
         static bool attr = false;
@@ -622,20 +607,6 @@ unsigned spec_grid(const GridDims& g) {
     return static_cast<unsigned>(std::min<long long>((g.NC + 255) / 256, 148LL * 16));
 }
 
-// forward passes x2 then x1 on a spectrum in place
-void axes_forward(vr_ctx* ctx, double2* s) {
-    const GridDims& g = ctx->g;
-    MultDev none{};
-    launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
-    launch_axis<-1, 0>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, none);
-}
-void axes_inverse(vr_ctx* ctx, double2* s) {
-    const GridDims& g = ctx->g;
-    MultDev none{};
-    launch_axis<+1, 0>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, none);
-    launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
-}
-
 void upload_table(double2** dst, int n) {
     std::vector<double2> h(n);
     const long double two_pi_l = 6.283185307179586476925286766559005768L;
@@ -650,7 +621,7 @@ void upload_table(double2** dst, int n) {
 }  // namespace
 
 // ============================================================================
-// public (namespace vr) entry points
+// pass-level primitives (spectral.cu composes them, incl. the slab transposes)
 // ============================================================================
 void fft_plan_create(vr_ctx* ctx) {
     auto* p = new FftPlan();
@@ -670,136 +641,47 @@ void fft_plan_destroy(vr_ctx* ctx) {
     ctx->fft = nullptr;
 }
 
-void fft_r2c(vr_ctx* ctx, const double* in, double* spec) {
-    auto* s = reinterpret_cast<double2*>(spec);
-    launch_rows(ctx, true, in, s, 1.0, nullptr);
-    axes_forward(ctx, s);
+void pass_rows_forward(vr_ctx* ctx, const double* in, double* spec) {
+    launch_rows(ctx, true, in, spec, 1.0, nullptr);
 }
-
-void fft_c2r(vr_ctx* ctx, double* spec, double* out, double scale, const double* add) {
-    auto* s = reinterpret_cast<double2*>(spec);
-    axes_inverse(ctx, s);
-    launch_rows(ctx, false, s, out, scale, add);
+void pass_rows_inverse(vr_ctx* ctx, const double* spec, double* out, double scale,
+                       const double* add) {
+    launch_rows(ctx, false, spec, out, scale, add);
 }
-
-void spectral_scalar_op(vr_ctx* ctx, const double* in, double* out, const MultParams& mp,
-                        const double* add) {
+void pass_x2(vr_ctx* ctx, double* spec, int dir) {
     const GridDims& g = ctx->g;
-    auto* s = reinterpret_cast<double2*>(spec_buf(ctx, 0));
-    MultDev none{}, m = to_dev(mp);
-    launch_rows(ctx, true, in, s, 1.0, nullptr);
-    launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
-    launch_axis<-1, 1>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, m);
-    launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
-    launch_rows(ctx, false, s, out, 1.0 / static_cast<double>(g.N), add);
-}
-
-void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
-    const GridDims& g = ctx->g;
-    auto* s0 = reinterpret_cast<double2*>(spec_buf(ctx, 0));
-    auto* s1 = reinterpret_cast<double2*>(spec_buf(ctx, 1));
+    auto* s = reinterpret_cast<double2*>(spec);
     MultDev none{};
-    launch_rows(ctx, true, f, s0, 1.0, nullptr);
-    launch_axis<-1, 0>(ctx, g.n2, s0, s0, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
-    for (int a = 0; a < 3; ++a) {
-        MultParams mp;
-        mp.kind = static_cast<Mult>(static_cast<int>(Mult::deriv0) + a);
-        launch_axis<-1, 1>(ctx, g.n1, s0, s1, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1,
-                           to_dev(mp));
-        launch_axis<+1, 0>(ctx, g.n2, s1, s1, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2,
-                           none);
-        launch_rows(ctx, false, s1, out3 + a * g.N, 1.0 / static_cast<double>(g.N), nullptr);
-    }
+    if (dir < 0)
+        launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.L, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+    else
+        launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.L, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
 }
-
-void op_divergence(vr_ctx* ctx, const double* v3, double* out) {
+void pass_x1(vr_ctx* ctx, const double* src, double* dst, int dir, const MultParams* mult) {
     const GridDims& g = ctx->g;
-    double2* s[3];
-    for (int a = 0; a < 3; ++a) {
-        s[a] = reinterpret_cast<double2*>(spec_buf(ctx, a));
-        fft_r2c(ctx, v3 + a * g.N, reinterpret_cast<double*>(s[a]));
-    }
-    auto* acc = reinterpret_cast<double2*>(spec_buf(ctx, 3));
-    VR_LAUNCH(ctx, "fft_spectral", k_spec_div<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], acc, g););
-    fft_c2r(ctx, reinterpret_cast<double*>(acc), out, 1.0 / static_cast<double>(g.N), nullptr);
+    const auto* s = reinterpret_cast<const double2*>(src);
+    auto* d = reinterpret_cast<double2*>(dst);
+    const long long inner = (long long)g.n2s * g.nh;
+    MultDev none{};
+    if (mult)
+        launch_axis<-1, 1>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, to_dev(*mult));
+    else if (dir < 0)
+        launch_axis<-1, 0>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, none);
+    else
+        launch_axis<+1, 0>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, none);
 }
-
-void op_projection(vr_ctx* ctx, const double* in3, double* out3, int kind, double beta_v,
-                   double beta_w) {
+void pass_spec_div(vr_ctx* ctx, const double* s0, const double* s1, const double* s2, double* acc) {
     const GridDims& g = ctx->g;
-    if (kind == VR_PROJ_IDENTITY) {
-        if (in3 != out3)
-            VR_CUDA(cudaMemcpyAsync(out3, in3, sizeof(double) * 3 * g.N, cudaMemcpyDeviceToDevice,
-                                    ctx->stream));
-        return;
-    }
-    if (kind == VR_PROJ_NEAR_INCOMPRESSIBLE && (beta_v <= 0.0 || beta_w <= 0.0))
-        throw_argument("apply_projection: near-incompressible K needs beta_v, beta_w > 0");
-    if (kind != VR_PROJ_INCOMPRESSIBLE && kind != VR_PROJ_NEAR_INCOMPRESSIBLE)
-        throw_argument("apply_projection: unknown projection kind");
-    double2* s[3];
-    for (int a = 0; a < 3; ++a) {
-        s[a] = reinterpret_cast<double2*>(spec_buf(ctx, a));
-        fft_r2c(ctx, in3 + a * g.N, reinterpret_cast<double*>(s[a]));
-    }
-    VR_LAUNCH(ctx, "fft_spectral", k_spec_project<<<spec_grid(g), 256, 0, ctx->stream>>>(s[0], s[1], s[2], g, kind, beta_v,
-                                                           beta_w););
-    for (int a = 0; a < 3; ++a)
-        fft_c2r(ctx, reinterpret_cast<double*>(s[a]), out3 + a * g.N,
-                1.0 / static_cast<double>(g.N), nullptr);
+    VR_LAUNCH(ctx, "fft_spectral", k_spec_div<<<spec_grid(g), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const double2*>(s0), reinterpret_cast<const double2*>(s1),
+        reinterpret_cast<const double2*>(s2), reinterpret_cast<double2*>(acc), g));
 }
-
-double reg_symbol(const vr_regnorm& n, double k2) {
-    switch (n.kind) {
-        case VR_REG_H1: return k2;
-        case VR_REG_H2: return k2 * k2;
-        case VR_REG_H3: return k2 * k2 * k2;
-        case VR_REG_HELMHOLTZ: {
-            double s = k2 + n.gamma;
-            return n.helmholtz_squared ? s * s : s;
-        }
-    }
-    return 0.0;
-}
-
-void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm, int mode,
-            double beta, const double* add3) {
-    MultParams mp;
-    mp.kind = Mult::reg;
-    mp.reg_kind = norm.kind;
-    mp.reg_mode = mode;
-    mp.gamma = norm.gamma;
-    mp.helm_sq = norm.helmholtz_squared;
-    mp.beta = beta;
-    const long long N = ctx->g.N;
-    for (int c = 0; c < 3; ++c)
-        spectral_scalar_op(ctx, in3 + c * N, out3 + c * N, mp, add3 ? add3 + c * N : nullptr);
-}
-
-void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mode, double beta) {
+void pass_spec_project(vr_ctx* ctx, double* s0, double* s1, double* s2, int kind, double beta_v,
+                       double beta_w) {
     const GridDims& g = ctx->g;
-    MultParams mp;
-    mp.kind = Mult::reg;
-    mp.reg_kind = norm.kind;
-    mp.reg_mode = mode;
-    mp.gamma = norm.gamma;
-    mp.helm_sq = norm.helmholtz_squared;
-    mp.beta = beta;
-    MultDev none{}, m = to_dev(mp);
-    for (int c = 0; c < 3; ++c) {
-        auto* s = reinterpret_cast<double2*>(spec_buf(ctx, 4 + c));
-        launch_rows(ctx, true, in3 + c * g.N, s, 1.0, nullptr);
-        launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
-        launch_axis<-1, 1>(ctx, g.n1, s, s, (long long)g.n2 * g.nh, 1, 0, ctx->fft->tw1, m);
-        launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.n1, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
-    }
-}
-
-void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3) {
-    const GridDims& g = ctx->g;
-    for (int c = 0; c < 3; ++c)
-        launch_rows(ctx, false, spec_buf(ctx, 4 + c), out3 + c * g.N, 1.0 / static_cast<double>(g.N),
-                    add3 ? add3 + c * g.N : nullptr);
+    VR_LAUNCH(ctx, "fft_spectral", k_spec_project<<<spec_grid(g), 256, 0, ctx->stream>>>(
+        reinterpret_cast<double2*>(s0), reinterpret_cast<double2*>(s1),
+        reinterpret_cast<double2*>(s2), g, kind, beta_v, beta_w));
 }
 
 }  // namespace vr

@@ -14,12 +14,12 @@
 vr_state::~vr_state() {
     vr_ctx* ctx = obj ? obj->ctx : nullptr;
     if (!ctx) return;
-    for (double* p : {v, xb, mhist, xf, factor, gradm, grad}) vr::dev_free(ctx, p);
+    for (double* p : {v, xb, mhist, xf, factor, gradm, grad, vpad}) vr::dev_free(ctx, p);
 }
 
 vr_objective::~vr_objective() {
     if (!ctx) return;
-    for (double* p : {ws_lam, ws_tmp, ws_b}) vr::dev_free(ctx, p);
+    for (double* p : {ws_lam, ws_tmp, ws_div, ws_b}) vr::dev_free(ctx, p);
 }
 
 namespace vr {
@@ -106,8 +106,9 @@ vr_objective* objective_create(vr_ctx* ctx, const double* mR, const double* mT,
     o->model = model;
     const long long N = ctx->g.N;
     try {
-        o->ws_lam = dev_alloc(ctx, (model.nt + 1) * N);
-        o->ws_tmp = dev_alloc(ctx, 2 * N);
+        o->ws_lam = dev_alloc(ctx, (model.nt + 1) * ctx->hstride);
+        o->ws_tmp = dev_alloc(ctx, 2 * ctx->hstride);
+        o->ws_div = dev_alloc(ctx, ctx->hstride);
         o->ws_b = dev_alloc(ctx, 3 * N);
         // initial_mismatch_ = <m_T - m_R, m_T - m_R>_h (objective.cpp:40-44)
         o->initial_mismatch = sum_sq_diff(ctx, mT, mR, N) * cell_volume(ctx->g);
@@ -116,6 +117,34 @@ vr_objective* objective_create(vr_ctx* ctx, const double* mR, const double* mT,
         throw;
     }
     return o;
+}
+
+// ---- halo-padded fields (x1 slabs) -------------------
+// A field that is a gather source is stored with `halo` planes on each side:
+// slice j of a padded series starts at base + j*hstride, its interior at +hoff.
+// On one GPU hstride = N and hoff = 0, i.e. the plain layout.
+long long hoff(const vr_ctx* ctx) {
+    return static_cast<long long>(ctx->g.halo) * ctx->g.n2 * ctx->g.n3;
+}
+double* pslice(const vr_ctx* ctx, double* base, int j) {
+    return base + j * ctx->hstride + hoff(ctx);
+}
+void exchange(vr_ctx* ctx, double* interior) {
+    if (ctx->dist)
+        ctx->dist->halo(ctx, interior, static_cast<size_t>(ctx->g.n2) * ctx->g.n3, ctx->g.L,
+                        ctx->g.halo);
+}
+// raise the per-call device flags: [0] non-finite direction, [1] departure beyond halo
+void check_flags(vr_ctx* ctx, const char* what) {
+    VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    double f[2] = {static_cast<double>(ctx->flag_host[0]), static_cast<double>(ctx->flag_host[1])};
+    if (ctx->dist) ctx->dist->allreduce(ctx, f, 2, true);
+    if (f[1] != 0.0)
+        throw_resource(std::string(what) + ": departure points beyond the x1 halo of " +
+                       std::to_string(ctx->g.halo) + " planes (use a wider halo or fewer ranks)");
+    if (f[0] != 0.0) throw_numeric(std::string(what) + ": non-finite direction");
 }
 
 vr_state* objective_evaluate(vr_objective* o, const double* v3) {
@@ -129,19 +158,42 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
     s->obj = o;
     s->nt = nt;
     try {
+        VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
         s->v = dev_alloc(ctx, 3 * N);
         s->xb = dev_alloc(ctx, 3 * N);
-        s->mhist = dev_alloc(ctx, (nt + 1) * N);
+        s->mhist = dev_alloc(ctx, (nt + 1) * ctx->hstride);
         VR_CUDA(cudaMemcpyAsync(s->v, v3, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
-        sl_trace(ctx, v3, nt, VR_TRACE_BACKWARD, s->xb);
+        const double* vg = s->v;  // gather source of the RK2 midpoint step
+        long long vstride = N;
+        if (ctx->dist) {
+            // the departure points of this velocity must stay within the halo
+            const double vmax = max_abs(ctx, v3, N);  // |v_1|, all ranks
+            const double need = std::ceil(1.1 * vmax / nt / g.h1) + 4.0;
+            if (need > g.halo)
+                throw_resource("evaluate: x1 displacement needs a halo of " +
+                               std::to_string(static_cast<int>(need)) + " planes, ctx has " +
+                               std::to_string(g.halo));
+            s->vpad = dev_alloc(ctx, 3 * ctx->hstride);
+            for (int c = 0; c < 3; ++c) {
+                VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->vpad, c), v3 + c * N, sizeof(double) * N,
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+                exchange(ctx, pslice(ctx, s->vpad, c));
+            }
+            vg = pslice(ctx, s->vpad, 0);
+            vstride = ctx->hstride;
+        }
+        sl_trace(ctx, vg, vstride, nt, VR_TRACE_BACKWARD, s->xb);
         // solve_state (transport.cpp:72-79)
-        VR_CUDA(cudaMemcpyAsync(s->mhist, o->mT, sizeof(double) * N, cudaMemcpyDeviceToDevice,
-                                ctx->stream));
-        for (int j = 0; j < nt; ++j) sl_advect(ctx, s->mhist + j * N, s->xb, s->mhist + (j + 1) * N);
+        VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->mhist, 0), o->mT, sizeof(double) * N,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+        for (int j = 0; j < nt; ++j) {
+            exchange(ctx, pslice(ctx, s->mhist, j));
+            sl_advect(ctx, pslice(ctx, s->mhist, j), s->xb, pslice(ctx, s->mhist, j + 1));
+        }
         o->counters.pde_solves += 1;
 
-        s->mismatch = sum_sq_diff(ctx, s->mhist + nt * N, o->mR, N) * cell_volume(g);
+        s->mismatch = sum_sq_diff(ctx, pslice(ctx, s->mhist, nt), o->mR, N) * cell_volume(g);
         s->mismatch_rel = o->initial_mismatch > 0.0 ? s->mismatch / o->initial_mismatch : 0.0;
 
         // reg = 1/2 beta_v <A v, v>_h with A applied at beta = 1 (objective.cpp:63-64)
@@ -150,8 +202,8 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
         const double reg = 0.5 * o->model.beta_v * inner_product_vec(ctx, Av, v3);
         double penalty = 0.0;
         if (o->model.norm.div_penalty) {
-            double* w = o->ws_tmp;
-            double* hw = o->ws_tmp + N;
+            double* w = pslice(ctx, o->ws_tmp, 0);
+            double* hw = pslice(ctx, o->ws_tmp, 1);
             op_divergence(ctx, v3, w);
             MultParams mp;
             mp.kind = Mult::helmholtz1;
@@ -161,6 +213,7 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
         s->objective = 0.5 * s->mismatch + reg + penalty;
         if (!std::isfinite(s->objective))
             throw_numeric("evaluate_objective: objective is not finite");
+        if (ctx->dist) check_flags(ctx, "evaluate_objective");
     } catch (...) {
         delete s;
         throw;
@@ -179,11 +232,17 @@ static void prepare_adjoint_ctx(vr_objective* o, vr_state* s) {
     if (!s->xf) s->xf = dev_alloc(ctx, 3 * N);
     if (!s->factor) s->factor = dev_alloc(ctx, N);
     if (!s->gradm) s->gradm = dev_alloc(ctx, 3LL * (nt + 1) * N);
-    sl_trace(ctx, s->v, nt, VR_TRACE_FORWARD, s->xf);
-    double* div_v = field_buf(ctx, 0);
+    VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
+    if (ctx->dist)
+        sl_trace(ctx, pslice(ctx, s->vpad, 0), ctx->hstride, nt, VR_TRACE_FORWARD, s->xf);
+    else
+        sl_trace(ctx, s->v, N, nt, VR_TRACE_FORWARD, s->xf);
+    double* div_v = pslice(ctx, o->ws_div, 0);
     op_divergence(ctx, s->v, div_v);
+    exchange(ctx, div_v);
     sl_factor(ctx, div_v, s->xf, 0.5 * dt, s->factor);
-    for (int j = 0; j <= nt; ++j) op_gradient(ctx, s->mhist + j * N, s->gradm + 3LL * j * N);
+    for (int j = 0; j <= nt; ++j)
+        op_gradient(ctx, pslice(ctx, s->mhist, j), s->gradm + 3LL * j * N);
     s->has_adjoint_ctx = true;
 }
 
@@ -199,16 +258,19 @@ void objective_gradient(vr_objective* o, vr_state* s) {
     });
 
     // terminal lambda = m_R - m_nt and the observer at j = nt (objective.cpp:91-99)
-    double* lam[2] = {o->ws_tmp, o->ws_tmp + N};
+    double* lam[2] = {pslice(ctx, o->ws_tmp, 0), pslice(ctx, o->ws_tmp, 1)};
     double* b = o->ws_b;
-    sl_grad_terminal(ctx, o->mR, s->mhist + nt * N, s->gradm + 3LL * nt * N, 0.5 * dt, lam[0], b);
+    sl_grad_terminal(ctx, o->mR, pslice(ctx, s->mhist, nt), s->gradm + 3LL * nt * N, 0.5 * dt,
+                     lam[0], b);
     int cur = 0;
     for (int j = nt - 1; j >= 0; --j) {
         const double w = (j == 0) ? 0.5 * dt : dt;
+        exchange(ctx, lam[cur]);
         sl_adjoint_step(ctx, lam[cur], s->xf, s->factor, lam[cur ^ 1], s->gradm + 3LL * j * N, w, b);
         cur ^= 1;
     }
     o->counters.pde_solves += 1;
+    if (ctx->dist) check_flags(ctx, "compute_gradient");
     if (o->model.projection != VR_PROJ_IDENTITY)
         op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
     // g = b + beta_v A v (objective.cpp:106-110), the add fused into the c2r epilogue
@@ -229,7 +291,7 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     const int nt = s->nt;
     const double dt = 1.0 / nt;
     const double hdt = 0.5 / nt;
-    VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, sizeof(int), ctx->stream));
+    VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
     // beta_v A vt depends only on vt: its FFT passes (HBM-bound) run on the side
     // stream under the L1-bound transport sweeps; only the c2r + add waits for b
     if (add_reg)
@@ -238,28 +300,31 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
         });
 
     // incremental state (transport.cpp:150-173), terminal = -mt_nt into lam[nt]
-    double* tmp[2] = {o->ws_tmp, o->ws_tmp + N};
-    double* lam = o->ws_lam;
+    double* tmp[2] = {pslice(ctx, o->ws_tmp, 0), pslice(ctx, o->ws_tmp, 1)};
+    double* lam0 = pslice(ctx, o->ws_lam, 0);
+    auto lam = [&](int j) { return pslice(ctx, o->ws_lam, j); };
     sl_incstate_first(ctx, s->gradm, vt3, hdt, tmp[0]);
     int cur = 0;
     for (int j = 0; j < nt; ++j) {
         const bool last = (j + 1 == nt);
+        exchange(ctx, tmp[cur]);
         sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
-                         last ? lam + nt * N : tmp[cur ^ 1], last ? 1 : 0);
+                         last ? lam(nt) : tmp[cur ^ 1], last ? 1 : 0);
         cur ^= 1;
     }
     o->counters.pde_solves += 1;
     // incremental adjoint, Gauss-Newton branch = plain continuity sweep (transport.cpp:188-190)
-    for (int j = nt - 1; j >= 0; --j)
-        sl_adjoint_step(ctx, lam + (j + 1) * N, s->xf, s->factor, lam + j * N, nullptr, 0.0,
-                        nullptr);
+    for (int j = nt - 1; j >= 0; --j) {
+        exchange(ctx, lam(j + 1));
+        sl_adjoint_step(ctx, lam(j + 1), s->xf, s->factor, lam(j), nullptr, 0.0, nullptr);
+    }
     o->counters.pde_solves += 1;
     double* b = o->ws_b;
     const bool identity_K = o->model.projection == VR_PROJ_IDENTITY;
     if (reg_given && identity_K) {
-        sl_accumulate(ctx, lam, s->gradm, nt, dt, out3, reg_given);  // out = b + u, one pass
+        sl_accumulate(ctx, lam0, s->gradm, nt, dt, out3, reg_given);  // out = b + u, one pass
     } else {
-        sl_accumulate(ctx, lam, s->gradm, nt, dt, b);
+        sl_accumulate(ctx, lam0, s->gradm, nt, dt, b);
         if (!identity_K)
             op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
         if (add_reg) {
@@ -273,10 +338,7 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
         }
     }
     o->counters.hessian_matvecs += 1;
-    VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, sizeof(int), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    VR_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (*ctx->flag_host) throw_numeric("hessian_matvec: non-finite direction");
+    check_flags(ctx, "hessian_matvec");
 }
 
 void objective_apply_reg(vr_objective* o, const double* u3, int mode, double* out3) {
@@ -390,7 +452,8 @@ vr_pcg_stats pcg_solve_gn(vr_objective* o, const vr_state* s, const double* rhs,
         for (double* p : {r, z, sd, Hs, u}) dev_free(ctx, p);
     };
     auto means_of = [&](const double* sums, double* m) {
-        for (int c = 0; c < 3; ++c) m[c] = zero_mode ? sums[c] / static_cast<double>(N) : 0.0;
+        for (int c = 0; c < 3; ++c)
+            m[c] = zero_mode ? sums[c] / static_cast<double>(ctx->g.Ng) : 0.0;  // global mean
     };
     try {
         VR_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * n3, cudaMemcpyDeviceToDevice, ctx->stream));

@@ -21,6 +21,7 @@ struct vr_state {
     double* factor = nullptr;  // N continuity factor (adjoint ctx)
     double* gradm = nullptr;   // 3(nt+1)N, [j*3 + a]
     double* grad = nullptr;    // 3N
+    double* vpad = nullptr;    // x1 slabs: halo-padded copy of v (gather source of the trace)
     double objective = 0.0, mismatch = 0.0, mismatch_rel = 0.0;
     bool has_gradient = false, has_adjoint_ctx = false;
     ~vr_state();
@@ -34,8 +35,9 @@ struct vr_objective {
     vr_counters counters{};
     double initial_mismatch = 0.0;
     // workspace reused by every call
-    double* ws_lam = nullptr;  // (nt+1)N
-    double* ws_tmp = nullptr;  // 2N
+    double* ws_lam = nullptr;  // (nt+1) halo-padded fields
+    double* ws_tmp = nullptr;  // 2 halo-padded fields
+    double* ws_div = nullptr;  // 1 halo-padded field (div v, gathered by the factor)
     double* ws_b = nullptr;    // 3N
     ~vr_objective();
 };
@@ -44,6 +46,10 @@ namespace vr {
 
 double* dev_alloc(vr_ctx* ctx, long long ndoubles);
 void dev_free(vr_ctx* ctx, double* p);
+// halo-padded field helpers (objective.cu)
+long long hoff(const vr_ctx* ctx);
+double* pslice(const vr_ctx* ctx, double* base, int j);
+void exchange(vr_ctx* ctx, double* interior);
 
 void validate_model(const vr_model& m);
 void validate_params(const vr_solver_params& p);

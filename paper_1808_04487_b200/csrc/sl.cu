@@ -53,11 +53,22 @@ __device__ __forceinline__ void axis_stencil(double x, double h, int& b, double*
     b = static_cast<int>(fl) - 1;
 }
 
+// i1 is the point's LOCAL plane. On x1 slabs the x1 base becomes slab-relative:
+// shifted by a whole period to the image nearest the point (departure points
+// are wrapped into [0, 2pi); the shift is exact, the weights are untouched) and
+// then offset by the slab origin, so gathers index the halo-padded slab directly.
 __device__ __forceinline__ void make_stencil(const GridDims& g, double x1, double x2, double x3,
-                                             Stencil& st) {
+                                             int i1, Stencil& st) {
     axis_stencil(x1, g.h1, st.b[0], st.w[0]);
     axis_stencil(x2, g.h2, st.b[1], st.w[1]);
     axis_stencil(x3, g.h3, st.b[2], st.w[2]);
+    if (g.dist) {
+        const int own = g.off1 + i1;
+        const int d = st.b[0] - own;
+        if (d > g.n1 / 2) st.b[0] -= g.n1;
+        if (d < -g.n1 / 2) st.b[0] += g.n1;
+        st.b[0] -= g.off1;
+    }
 }
 
 // power-of-two periodic wrap (two's complement handles negative j)
@@ -67,13 +78,21 @@ __device__ __forceinline__ int wrapi(int j, int n) { return j & (n - 1); }
 // 32-bit (a single field has N <= 2^30 elements), so each of the 16 stencil rows
 // costs one add + one address and its 4 x3-neighbours are immediate-offset
 // loads; only points whose x3 run crosses the periodic seam take the wrapped path.
+// On x1 slabs `f` points at the interior of a halo-padded field and x1 planes
+// b .. b+3 must lie in [-halo, L + halo); a violation raises flags[1] (checked
+// by the host after the sweep) and clamps.
 __device__ __forceinline__ double gather(const double* __restrict__ f, const GridDims& g,
                                          const Stencil& st) {
     const int n23 = g.n2 * g.n3;
+    int b1 = st.b[0];
+    if (g.dist && (b1 < -g.halo || b1 + 3 >= g.L + g.halo)) {
+        g.flags[1] = 1;
+        b1 = b1 < -g.halo ? -g.halo : g.L + g.halo - 4;
+    }
     int o12[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const int oa = wrapi(st.b[0] + a, g.n1) * n23;
+        const int oa = (g.dist ? b1 + a : wrapi(b1 + a, g.n1)) * n23;
 #pragma unroll
         for (int b = 0; b < 4; ++b) o12[a][b] = oa + wrapi(st.b[1] + b, g.n2) * g.n3;
     }
@@ -139,7 +158,7 @@ __device__ __forceinline__ bool tile_point(const GridDims& g, const Tile& t, int
     i3 = blockIdx.x * T3 + l3;
     i2 = blockIdx.y * T2 + l2;
     i1 = blockIdx.z * T1 + l1;
-    const bool ok = l1 < T1 && i1 < g.n1 && i2 < g.n2 && i3 < g.n3;
+    const bool ok = l1 < T1 && i1 < g.L && i2 < g.n2 && i3 < g.n3;
     idx = ok ? (static_cast<long long>(i1) * g.n2 + i2) * g.n3 + i3 : 0;
     return ok;
 }
@@ -163,7 +182,7 @@ __global__ void __launch_bounds__(kTileThreads, NF == 1 ? 3 : 2)
     double x1, x2, x3;
     load_point(pts, i, g.N, x1, x2, x3);
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
+    make_stencil(g, x1, x2, x3, i1, st);
 #pragma unroll
     for (int q = 0; q < NF; ++q) out[q * g.N + i] = gather(f + q * g.N, g, st);
 }
@@ -172,20 +191,21 @@ __global__ void __launch_bounds__(kTileThreads, NF == 1 ? 3 : 2)
 // point, one 3-field gather of v there, wrapped departure point.
 template <bool BIG>
 __global__ void __launch_bounds__(kTileThreads, 2)
-    k_trace(const double* __restrict__ v, double* __restrict__ dep, GridDims g, Tile t,
-            double sign, double dt) {
+    k_trace(const double* __restrict__ v, long long vs, double* __restrict__ dep, GridDims g,
+            Tile t, double sign, double dt) {
+    // v: component c at v + c*vs (vs = N, or the padded stride on x1 slabs)
     int i1, i2, i3;
     long long i;
     if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
-    const double x[3] = {g.h1 * i1, g.h2 * i2, g.h3 * i3};
+    const double x[3] = {g.h1 * (g.off1 + i1), g.h2 * i2, g.h3 * i3};
     double mid[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) mid[c] = wrap_coord(x[c] + sign * 0.5 * dt * v[c * g.N + i]);
+    for (int c = 0; c < 3; ++c) mid[c] = wrap_coord(x[c] + sign * 0.5 * dt * v[c * vs + i]);
     Stencil st;
-    make_stencil(g, mid[0], mid[1], mid[2], st);
+    make_stencil(g, mid[0], mid[1], mid[2], i1, st);
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-        dep[c * g.N + i] = wrap_coord(x[c] + sign * dt * gather(v + c * g.N, g, st));
+        dep[c * g.N + i] = wrap_coord(x[c] + sign * dt * gather(v + c * vs, g, st));
 }
 
 // continuity_factor (transport.cpp:44-55)
@@ -200,7 +220,7 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     load_point(dep, i, g.N, x1, x2, x3);
     const double d = div[i];
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
+    make_stencil(g, x1, x2, x3, i1, st);
     factor[i] = exp(half_dt * (d + gather(div, g, st)));
 }
 
@@ -216,7 +236,7 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     load_point(dep, i, g.N, x1, x2, x3);
     const double fac = FACTOR ? factor[i] : 1.0;
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
+    make_stencil(g, x1, x2, x3, i1, st);
     const double r = gather(f, g, st);
     out[i] = FACTOR ? r * fac : r;
 }
@@ -257,7 +277,7 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     load_point(dep, i, g.N, x1, x2, x3);
     const double q = qdot(gm, vt, i, g.N);
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
+    make_stencil(g, x1, x2, x3, i1, st);
     const double m = gather(src, g, st) + (-hdt) * q;
     dst[i] = (MODE == 0) ? 1.0 * m + (-hdt) * q : -m;
 }
@@ -276,7 +296,7 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     load_point(dep, i, g.N, x1, x2, x3);
     const double fac = factor[i];
     Stencil st;
-    make_stencil(g, x1, x2, x3, st);
+    make_stencil(g, x1, x2, x3, i1, st);
     const double lam = gather(src, g, st) * fac;
     dst[i] = lam;
     if (ACC) {
@@ -302,14 +322,15 @@ __global__ void __launch_bounds__(kThreads)
 
 // b_a = sum_{j = nt..0} (w_j lam_j) d_a m_j (observer order of objective.cpp:143-148)
 __global__ void __launch_bounds__(kThreads)
-    k_accumulate(const double* __restrict__ lam, const double* __restrict__ gm, int nt, double dt,
-                 double* __restrict__ b, GridDims g, const double* __restrict__ add) {
+    k_accumulate(const double* __restrict__ lam, long long ls, const double* __restrict__ gm,
+                 int nt, double dt, double* __restrict__ b, GridDims g,
+                 const double* __restrict__ add) {
     const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
     if (i >= g.N) return;
     double acc[3] = {0.0, 0.0, 0.0};
     for (int j = nt; j >= 0; --j) {
         const double w = (j == 0 || j == nt) ? 0.5 * dt : dt;
-        const double wl = w * lam[j * g.N + i];
+        const double wl = w * lam[j * ls + i];
         const double* gj = gm + 3LL * j * g.N;
 #pragma unroll
         for (int a = 0; a < 3; ++a) acc[a] = acc[a] + wl * gj[a * g.N + i];
@@ -336,7 +357,7 @@ __global__ void __launch_bounds__(kThreads)
     r /= g.n3;
     const int i2 = static_cast<int>(r % g.n2);
     const int i1 = static_cast<int>(r / g.n2);
-    const double x1 = g.h1 * i1, x2 = g.h2 * i2, x3 = g.h3 * i3;
+    const double x1 = g.h1 * (g.off1 + i1), x2 = g.h2 * i2, x3 = g.h3 * i3;
     const double s1 = sin(x1), s2 = sin(x2), s3 = sin(x3);
     mT[i] = (s1 * s1 + s2 * s2 + s3 * s3) / 3.0;
     const double v0 = sin(x3) * cos(x2) * sin(x2);
@@ -349,7 +370,7 @@ __global__ void __launch_bounds__(kThreads)
 
 unsigned pgrid(const GridDims& g) { return grid_1d(g.N, kThreads); }
 
-bool is_big(const GridDims& g) { return g.n3 >= 32 && g.n2 >= 4 && g.n1 >= 2; }
+bool is_big(const GridDims& g) { return g.n3 >= 32 && g.n2 >= 4 && g.L >= 2; }
 Tile tile_of(const GridDims& g) {
     Tile t;
     if (is_big(g)) {
@@ -359,12 +380,12 @@ Tile tile_of(const GridDims& g) {
     t.t3 = g.n3 < 32 ? g.n3 : 32;
     t.t2 = g.n2 < 4 ? g.n2 : 4;
     const int rest = kTileThreads / (t.t3 * t.t2);
-    t.t1 = g.n1 < rest ? g.n1 : rest;
+    t.t1 = g.L < rest ? g.L : rest;
     return t;
 }
 dim3 tgrid(const GridDims& g, const Tile& t) {
     return dim3(static_cast<unsigned>(g.n3 / t.t3), static_cast<unsigned>(g.n2 / t.t2),
-                static_cast<unsigned>(g.n1 / t.t1));
+                static_cast<unsigned>(g.L / t.t1));
 }
 unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.t3); }
 
@@ -404,13 +425,14 @@ void sl_tricubic(vr_ctx* ctx, const double* f, int nfields, const double* pts3, 
     }
 }
 
-void sl_trace(vr_ctx* ctx, const double* v3, int nt, int direction, double* dep3) {
+void sl_trace(vr_ctx* ctx, const double* v3, long long vstride, int nt, int direction,
+              double* dep3) {
     if (nt < 1) throw_argument("trace_characteristics: n_t must be >= 1");
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);
     const double dt = 1.0 / nt;
     const double sign = direction == VR_TRACE_BACKWARD ? -1.0 : 1.0;
-    VR_TILE_LAUNCH(ctx, "sl_trace", K_TRACE, v3, dep3, g, t, sign, dt);
+    VR_TILE_LAUNCH(ctx, "sl_trace", K_TRACE, v3, vstride, dep3, g, t, sign, dt);
 }
 
 void sl_factor(vr_ctx* ctx, const double* div_v, const double* dep3, double half_dt,
@@ -468,7 +490,7 @@ void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const
 void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, int nt, double dt,
                    double* b3, const double* add3) {
     const GridDims& g = ctx->g;
-    VR_LAUNCH(ctx, "sl_accumulate", k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, gm_hist, nt, dt, b3, g, add3));
+    VR_LAUNCH(ctx, "sl_accumulate", k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, ctx->hstride, gm_hist, nt, dt, b3, g, add3));
 }
 
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out) {

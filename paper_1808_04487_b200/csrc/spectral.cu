@@ -1,0 +1,203 @@
+// spectral.cu -- spectral operators (proj/src/spectral.cpp:84-222, fft.cpp:66-115)
+// composed from the FFT pass primitives of fft.cu, on one GPU or on x1 slabs.
+//
+// One GPU:  r2c(x3) -> x2 -> x1 [fused multiplier] -> x2 -> c2r(x3) on (n1, n2, nh).
+// x1 slabs: the x3 and x2 passes are local to the slab [L][n2][nh]; the x1 pass
+//           needs whole x1 columns, so an all-to-all transposes the slab into the
+//           k2-slab [n1][n2s][nh] (rank r keeps k2 in [r n2s, (r+1) n2s)), the x1
+//           kernel runs there (the multiplier decodes global k2 via k2_off), and a
+//           second all-to-all transposes back. Blocks to/from rank q are packed
+//           with 2D copies (one per peer), so the x1 layout needs no unpacking.
+#include "vr_common.cuh"
+
+namespace vr {
+namespace {
+
+double* sbuf(vr_ctx* ctx, int i) { return spec_buf(ctx, i); }
+
+// doubles in one complex row block [n2s][nh]
+size_t row_block(const GridDims& g) { return static_cast<size_t>(g.n2s) * g.nh * 2; }
+
+// slab [L][n2][nh] -> x1 layout [n1][n2s][nh]
+void transpose_to_x1(vr_ctx* ctx, const double* slab, double* xl) {
+    const GridDims& g = ctx->g;
+    const size_t row = row_block(g), pitch = static_cast<size_t>(g.n2) * g.nh * 2;
+    double* send = sbuf(ctx, 7);
+    for (int q = 0; q < ctx->dist->size; ++q)
+        VR_CUDA(cudaMemcpy2DAsync(send + q * g.L * row, row * sizeof(double), slab + q * row,
+                                  pitch * sizeof(double), row * sizeof(double), g.L,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->dist->alltoall(ctx, send, xl, g.L * row);
+}
+
+// x1 layout [n1][n2s][nh] -> slab [L][n2][nh]
+void transpose_from_x1(vr_ctx* ctx, const double* xl, double* slab) {
+    const GridDims& g = ctx->g;
+    const size_t row = row_block(g), pitch = static_cast<size_t>(g.n2) * g.nh * 2;
+    double* recv = sbuf(ctx, 7);
+    ctx->dist->alltoall(ctx, xl, recv, g.L * row);
+    for (int q = 0; q < ctx->dist->size; ++q)
+        VR_CUDA(cudaMemcpy2DAsync(slab + q * row, pitch * sizeof(double), recv + q * g.L * row,
+                                  row * sizeof(double), row * sizeof(double), g.L,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+double inv_n(const GridDims& g) { return 1.0 / static_cast<double>(g.Ng); }
+
+MultParams reg_mult(const vr_regnorm& norm, int mode, double beta) {
+    MultParams mp;
+    mp.kind = Mult::reg;
+    mp.reg_kind = norm.kind;
+    mp.reg_mode = mode;
+    mp.gamma = norm.gamma;
+    mp.helm_sq = norm.helmholtz_squared;
+    mp.beta = beta;
+    return mp;
+}
+
+// in (real slab) -> out (real slab) through the fused x1 multiplier; leaves the
+// x2-inverse-transformed slab spectrum in `s` when `out` is null
+void scalar_multiplier(vr_ctx* ctx, const double* in, double* s, double* out, const MultParams& mp,
+                       const double* add) {
+    pass_rows_forward(ctx, in, s);
+    pass_x2(ctx, s, -1);
+    if (ctx->dist) {
+        double* t = sbuf(ctx, 8);
+        transpose_to_x1(ctx, s, t);
+        pass_x1(ctx, t, t, 0, &mp);
+        transpose_from_x1(ctx, t, s);
+    } else {
+        pass_x1(ctx, s, s, 0, &mp);
+    }
+    pass_x2(ctx, s, +1);
+    if (out) pass_rows_inverse(ctx, s, out, inv_n(ctx->g), add);
+}
+
+}  // namespace
+
+// r2c: on slabs the result is left in the x1 layout (what the elementwise
+// spectral kernels and fft_c2r expect)
+void fft_r2c(vr_ctx* ctx, const double* in, double* spec) {
+    if (ctx->dist) {
+        double* s = sbuf(ctx, 8);
+        pass_rows_forward(ctx, in, s);
+        pass_x2(ctx, s, -1);
+        transpose_to_x1(ctx, s, spec);
+    } else {
+        pass_rows_forward(ctx, in, spec);
+        pass_x2(ctx, spec, -1);
+    }
+    pass_x1(ctx, spec, spec, -1, nullptr);
+}
+
+void fft_c2r(vr_ctx* ctx, double* spec, double* out, double scale, const double* add) {
+    pass_x1(ctx, spec, spec, +1, nullptr);
+    double* s = spec;
+    if (ctx->dist) {
+        s = sbuf(ctx, 8);
+        transpose_from_x1(ctx, spec, s);
+    }
+    pass_x2(ctx, s, +1);
+    pass_rows_inverse(ctx, s, out, scale, add);
+}
+
+void spectral_scalar_op(vr_ctx* ctx, const double* in, double* out, const MultParams& mp,
+                        const double* add) {
+    scalar_multiplier(ctx, in, sbuf(ctx, 0), out, mp, add);
+}
+
+void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
+    const GridDims& g = ctx->g;
+    double* s0 = sbuf(ctx, 0);
+    double* s1 = sbuf(ctx, 1);
+    pass_rows_forward(ctx, f, s0);
+    pass_x2(ctx, s0, -1);
+    double* src = s0;
+    if (ctx->dist) {
+        src = sbuf(ctx, 8);
+        transpose_to_x1(ctx, s0, src);
+    }
+    for (int a = 0; a < 3; ++a) {
+        MultParams mp;
+        mp.kind = static_cast<Mult>(static_cast<int>(Mult::deriv0) + a);
+        pass_x1(ctx, src, s1, 0, &mp);
+        double* s = s1;
+        if (ctx->dist) {
+            s = sbuf(ctx, 2);
+            transpose_from_x1(ctx, s1, s);
+        }
+        pass_x2(ctx, s, +1);
+        pass_rows_inverse(ctx, s, out3 + a * g.N, inv_n(g), nullptr);
+    }
+}
+
+void op_divergence(vr_ctx* ctx, const double* v3, double* out) {
+    const GridDims& g = ctx->g;
+    double* s[3];
+    for (int a = 0; a < 3; ++a) {
+        s[a] = sbuf(ctx, a);
+        fft_r2c(ctx, v3 + a * g.N, s[a]);
+    }
+    double* acc = sbuf(ctx, 3);
+    pass_spec_div(ctx, s[0], s[1], s[2], acc);
+    fft_c2r(ctx, acc, out, inv_n(g), nullptr);
+}
+
+void op_projection(vr_ctx* ctx, const double* in3, double* out3, int kind, double beta_v,
+                   double beta_w) {
+    const GridDims& g = ctx->g;
+    if (kind == VR_PROJ_IDENTITY) {
+        if (in3 != out3)
+            VR_CUDA(cudaMemcpyAsync(out3, in3, sizeof(double) * 3 * g.N, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+        return;
+    }
+    if (kind == VR_PROJ_NEAR_INCOMPRESSIBLE && (beta_v <= 0.0 || beta_w <= 0.0))
+        throw_argument("apply_projection: near-incompressible K needs beta_v, beta_w > 0");
+    if (kind != VR_PROJ_INCOMPRESSIBLE && kind != VR_PROJ_NEAR_INCOMPRESSIBLE)
+        throw_argument("apply_projection: unknown projection kind");
+    double* s[3];
+    for (int a = 0; a < 3; ++a) {
+        s[a] = sbuf(ctx, a);
+        fft_r2c(ctx, in3 + a * g.N, s[a]);
+    }
+    pass_spec_project(ctx, s[0], s[1], s[2], kind, beta_v, beta_w);
+    for (int a = 0; a < 3; ++a) fft_c2r(ctx, s[a], out3 + a * g.N, inv_n(g), nullptr);
+}
+
+double reg_symbol(const vr_regnorm& n, double k2) {
+    switch (n.kind) {
+        case VR_REG_H1: return k2;
+        case VR_REG_H2: return k2 * k2;
+        case VR_REG_H3: return k2 * k2 * k2;
+        case VR_REG_HELMHOLTZ: {
+            const double s = k2 + n.gamma;
+            return n.helmholtz_squared ? s * s : s;
+        }
+    }
+    return 0.0;
+}
+
+void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm, int mode,
+            double beta, const double* add3) {
+    const MultParams mp = reg_mult(norm, mode, beta);
+    const long long N = ctx->g.N;
+    for (int c = 0; c < 3; ++c)
+        scalar_multiplier(ctx, in3 + c * N, sbuf(ctx, 0), out3 + c * N, mp,
+                          add3 ? add3 + c * N : nullptr);
+}
+
+void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mode, double beta) {
+    const MultParams mp = reg_mult(norm, mode, beta);
+    for (int c = 0; c < 3; ++c)
+        scalar_multiplier(ctx, in3 + c * ctx->g.N, sbuf(ctx, 4 + c), nullptr, mp, nullptr);
+}
+
+void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3) {
+    const GridDims& g = ctx->g;
+    for (int c = 0; c < 3; ++c)
+        pass_rows_inverse(ctx, sbuf(ctx, 4 + c), out3 + c * g.N, inv_n(g),
+                          add3 ? add3 + c * g.N : nullptr);
+}
+
+}  // namespace vr

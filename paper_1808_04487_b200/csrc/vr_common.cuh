@@ -53,12 +53,24 @@ struct Error : std::runtime_error {
 // ---------------------------------------------------------------------------
 // Grid (Grid3, grid.hpp:20-56) as passed to kernels by value
 // ---------------------------------------------------------------------------
+// On one GPU L = n1, off1 = 0, halo = 0, n2s = n2, k2_off = 0, dist = 0. With P
+// x1 slabs rank r owns planes [off1, off1 + L), L = n1/P;
+// gathered fields carry `halo` planes on each side; the x1 FFT pass runs on the
+// k2-slab [n1][n2s][nh] (n2s = n2/P, first column k2_off).
 struct GridDims {
-    int n1, n2, n3;
-    int nh;            // n3/2 + 1
-    long long N;       // n1*n2*n3
-    long long NC;      // n1*n2*nh spectral bins
-    double h1, h2, h3; // two_pi / n_a, exactly as Grid3::spacing
+    int n1, n2, n3;     // global grid (Grid3)
+    int nh;             // n3/2 + 1
+    int L;              // x1 planes owned here
+    int off1;           // global index of the first owned plane
+    int halo;           // halo planes on each side of gathered fields
+    int n2s;            // k2 extent of the x1-pass spectrum layout
+    int k2_off;         // global k2 of its first column
+    int dist;           // 1 when x1-slab decomposed across ranks
+    long long N;        // local points L*n2*n3
+    long long NC;       // local spectral bins L*n2*nh (== n1*n2s*nh)
+    long long Ng;       // global points n1*n2*n3 (FFT normalisation)
+    double h1, h2, h3;  // two_pi / n_a, exactly as Grid3::spacing
+    int* flags;         // device flags: [0] non-finite input, [1] departure beyond halo
 };
 
 // Signed FFT frequency / odd-derivative frequency (grid.hpp:58-64)
@@ -78,6 +90,21 @@ __device__ __forceinline__ double wrap_coord(double x) {
 // ---------------------------------------------------------------------------
 struct FftPlan;
 
+// Exchange layer of the x1-slab decomposition (dist.cu): NCCL between processes,
+// or an in-process group of virtual ranks (host threads, one GPU) for tests.
+// Every rank calls the same sequence of operations.
+struct Transport {
+    int rank = 0, size = 1;
+    virtual ~Transport() = default;
+    // equal blocks: send + q*count -> rank q ; recv + q*count <- rank q (doubles)
+    virtual void alltoall(vr_ctx* ctx, const double* send, double* recv, size_t count) = 0;
+    // field interior at `interior` (L planes of `plane` doubles, halo H planes each
+    // side): lower halo <- previous rank's top H planes, upper <- next's bottom H
+    virtual void halo(vr_ctx* ctx, double* interior, size_t plane, int L, int H) = 0;
+    // combine k host doubles over ranks in rank order (sum, or max when `max`)
+    virtual void allreduce(vr_ctx* ctx, double* vals, int k, bool max) = 0;
+};
+
 }  // namespace vr
 
 struct vr_ctx {
@@ -87,6 +114,9 @@ struct vr_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     vr::GridDims g{};
     vr::FftPlan* fft = nullptr;
+    vr::Transport* dist = nullptr;  // null on one GPU
+    bool owns_dist = false;         // NCCL contexts own their transport
+    long long hstride = 0;          // doubles per halo-padded field ((L + 2 halo) n2 n3)
     // lazily allocated scratch: spectra (NC complex) and real fields (N doubles)
     std::vector<double*> spec_scratch;
     std::vector<double*> field_scratch;
@@ -113,6 +143,10 @@ namespace vr {
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs; fixed => deterministic partial order
 constexpr int kRedThreads = 256;
 
+// create a context for grid (n1, n2, n3) on `device`; with a transport of size
+// P > 1 it owns that rank's x1 slab with `halo` planes (capi.cu)
+vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo);
+void set_last_error(int cls, const std::string& msg);  // the C ABI's vr_last_error slot
 double* spec_buf(vr_ctx* ctx, int i);   // NC complex (2*NC doubles)
 double* field_buf(vr_ctx* ctx, int i);  // N doubles
 inline void count_launch(vr_ctx* ctx, int n = 1) { ctx->launches += n; }
@@ -193,6 +227,16 @@ struct MultParams {
 };
 void fft_plan_create(vr_ctx* ctx);
 void fft_plan_destroy(vr_ctx* ctx);
+// pass primitives (fft.cu): x3 rows on the local slab, x2 on the local slab,
+// x1 on the x1-pass layout [n1][n2s][nh] (mult: fused forward-multiply-inverse)
+void pass_rows_forward(vr_ctx* ctx, const double* in, double* spec);
+void pass_rows_inverse(vr_ctx* ctx, const double* spec, double* out, double scale,
+                       const double* add);
+void pass_x2(vr_ctx* ctx, double* spec, int dir);
+void pass_x1(vr_ctx* ctx, const double* src, double* dst, int dir, const MultParams* mult);
+void pass_spec_div(vr_ctx* ctx, const double* s0, const double* s1, const double* s2, double* acc);
+void pass_spec_project(vr_ctx* ctx, double* s0, double* s1, double* s2, int kind, double beta_v,
+                       double beta_w);
 void fft_r2c(vr_ctx* ctx, const double* in, double* spec);
 // c2r of spec (destroyed) -> out = add + scale*x (add may be null)
 void fft_c2r(vr_ctx* ctx, double* spec, double* out, double scale, const double* add);
@@ -211,8 +255,14 @@ void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mo
 void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3);
 // run `fn` (which launches on ctx->stream) on the side stream, forked from the
 // current point of ctx->stream; join_side() makes ctx->stream wait for it
+// (on x1 slabs the work stays on the main stream: its collectives must keep one
+// order on every rank)
 template <class Fn>
 void on_side_stream(vr_ctx* ctx, Fn&& fn) {
+    if (ctx->dist) {
+        fn();
+        return;
+    }
     VR_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
     VR_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     cudaStream_t main = ctx->stream;
@@ -226,12 +276,16 @@ void on_side_stream(vr_ctx* ctx, Fn&& fn) {
     ctx->stream = main;
     VR_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
 }
-inline void join_side(vr_ctx* ctx) { VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0)); }
+inline void join_side(vr_ctx* ctx) {
+    if (!ctx->dist) VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+}
 double reg_symbol(const vr_regnorm& n, double k2);
 
 // ---- semi-Lagrangian (sl.cu) ----
 void sl_tricubic(vr_ctx* ctx, const double* f, int nfields, const double* pts3, double* out);
-void sl_trace(vr_ctx* ctx, const double* v3, int nt, int direction, double* dep3);
+// v3: component c at v3 + c*vstride (N, or the halo-padded stride on x1 slabs)
+void sl_trace(vr_ctx* ctx, const double* v3, long long vstride, int nt, int direction,
+              double* dep3);
 void sl_factor(vr_ctx* ctx, const double* div_v, const double* dep3, double half_dt,
                double* factor);
 void sl_advect(vr_ctx* ctx, const double* f, const double* dep3, double* out);

@@ -78,6 +78,7 @@ class Context:
         if isinstance(dims, int):
             dims = (dims, dims, dims)
         self.dims = tuple(int(d) for d in dims)
+        self.local_dims = self.dims  # shape of this context's fields (a slab on x1 slabs)
         self.N = self.dims[0] * self.dims[1] * self.dims[2]
         self.nh = self.dims[2] // 2 + 1
         h = C.c_void_p()
@@ -148,7 +149,8 @@ class DeviceArray:
         self.ctx = ctx
         self.nfields = nfields
         self.spectrum = complex_spectrum
-        per = ctx.dims[0] * ctx.dims[1] * ctx.nh * 2 if complex_spectrum else ctx.N
+        ld = ctx.local_dims
+        per = ld[0] * ld[1] * ctx.nh * 2 if complex_spectrum else ctx.N
         self.count = per * nfields
         self.nbytes = 8 * self.count
         p = C.c_void_p()
@@ -159,7 +161,7 @@ class DeviceArray:
     def numpy(self) -> np.ndarray:
         out = np.empty(self.count, dtype=np.float64)
         _lib.call("vr_memcpy_d2h", self.ctx.handle, out.ctypes.data, self.ptr, self.nbytes)
-        d = self.ctx.dims
+        d = self.ctx.local_dims
         if self.spectrum:
             c = out.view(np.complex128)
             return c.reshape((self.nfields, d[0], d[1], self.ctx.nh)) if self.nfields > 1 else c.reshape(d[0], d[1], self.ctx.nh)
@@ -582,3 +584,65 @@ def parameter_continuation(ctx, m_R, m_T, v0, model=None, params=None, precond="
     reports = [_report_dict(reps[i]) for i in range(min(nl.value, max_levels))]
     nrec = sum(r["n_records"] for r in reports)
     return vout.numpy(), reports, _records(recs, min(nrec, max_records))
+
+
+# ---- x1-slab decomposition ---------------------------------
+def nccl_unique_id() -> bytes:
+    """NCCL unique id for vr_ctx_create_dist (create on one rank, broadcast)."""
+    buf = C.create_string_buffer(128)
+    _lib.call("vr_nccl_unique_id", buf)
+    return buf.raw
+
+
+class DistContext(Context):
+    """This process's x1 slab of a grid decomposed over `nranks` GPUs (NCCL)."""
+
+    def __init__(self, dims, rank: int, nranks: int, uid: bytes, device: int = 0, halo: int = 16):
+        if isinstance(dims, int):
+            dims = (dims, dims, dims)
+        self.dims = tuple(int(d) for d in dims)
+        h = C.c_void_p()
+        _lib.call("vr_ctx_create_dist", self.dims[0], self.dims[1], self.dims[2], device, rank,
+                  nranks, uid, halo, C.byref(h))
+        self._h = h
+        vals = [C.c_int() for _ in range(5)]
+        _lib.call("vr_ctx_slab", h, *[C.byref(x) for x in vals])
+        self.rank, self.nranks, self.planes, self.first_plane, self.halo = (x.value for x in vals)
+        self.local_dims = (self.planes, self.dims[1], self.dims[2])
+        self.N = self.planes * self.dims[1] * self.dims[2]
+        self.nh = self.dims[2] // 2 + 1
+
+    def slab(self, arr):
+        """This rank's planes of a global host array (scalar or vector field)."""
+        a = np.asarray(arr)
+        sl = slice(self.first_plane, self.first_plane + self.planes)
+        return np.ascontiguousarray(a[..., sl, :, :])
+
+
+def dist_selftest_objective(P, m_R, m_T, v, vt, model=None, halo=8, device=0):
+    """Evaluate + gradient + Hessian matvec + apply_reg on P virtual slab ranks on
+    one GPU; returns (gradient, matvec, reg, scalars) assembled over all slabs."""
+    dims = tuple(np.shape(m_R))
+    model = model if model is not None else make_model()
+    a = [np.ascontiguousarray(x, dtype=np.float64) for x in (m_R, m_T, v, vt)]
+    g, mv, rg = (np.empty((3,) + dims) for _ in range(3))
+    sc = np.empty(5)
+    _lib.call("vr_dist_selftest_objective", P, dims[0], dims[1], dims[2], device, halo,
+              C.byref(model), *[x.ctypes.data for x in a], g.ctypes.data, mv.ctypes.data,
+              rg.ctypes.data, sc.ctypes.data)
+    return g, mv, rg, dict(objective=sc[0], mismatch=sc[1], mismatch_rel=sc[2], grad_norm=sc[3],
+                           vt_H_vt=sc[4])
+
+
+def dist_selftest_solve(P, m_R, m_T, v0, model=None, params=None, halo=8, device=0):
+    """A full GN solve on P virtual slab ranks on one GPU."""
+    dims = tuple(np.shape(m_R))
+    model = model if model is not None else make_model()
+    params = params if params is not None else make_params()
+    a = [np.ascontiguousarray(x, dtype=np.float64) for x in (m_R, m_T, v0)]
+    vout = np.empty((3,) + dims)
+    rep = _lib.SolveReport()
+    _lib.call("vr_dist_selftest_solve", P, dims[0], dims[1], dims[2], device, halo,
+              C.byref(model), C.byref(params), *[x.ctypes.data for x in a], vout.ctypes.data,
+              C.byref(rep))
+    return vout, _report_dict(rep)
