@@ -13,9 +13,11 @@ Arms:
   --impl reference  the reference C++ code (oracle/_ref, compiled unmodified
                     from /root/reference/proj/src) on the host cores, rank 0 only
 
-Multi-GPU (torchrun, N > 1): the slab-sharded matvec is not built yet, so each
-rank runs an independent replica of the workload on its own GPU ("scaling":
-"weak"; value = all ranks' matvecs / max-over-ranks time).
+Multi-GPU (torchrun, N > 1): the same 256^3 problem is split into x1 slabs,
+one per rank (NCCL all-to-all FFT transposes, P2P halo exchange for the
+semi-Lagrangian gathers); "scaling": "strong", value = global matvecs /
+max-over-ranks time. If the slab path cannot start (e.g. no NCCL), every rank
+runs an independent replica instead ("parallelism": "replicas").
 """
 from __future__ import annotations
 
@@ -213,15 +215,39 @@ def main():
     dev = local
 
     m_T, v, vt, desc = workload(n, nt)
-    ctx = vr.Context(n, device=dev)
-    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev))
-    d_mT = ctx.to_device(m_T)
-    d_v = ctx.to_device(v)
-    d_vt = ctx.to_device(vt)
-    hist = V.solve_state(ctx, d_mT, d_v, nt)                       # m_R = m_T transported by v
-    d_mR = ctx.empty(1)
-    _ = V._lib.call("vr_memcpy_d2d", ctx.handle, d_mR.ptr, hist.field(nt), 8 * ctx.N)
     model = V.make_model("h2", beta_v=1e-2, nt=nt)
+    parallelism, scaling, slab_note = "single", "weak", None
+    ctx = None
+    if world > 1:
+        # x1 slabs over the ranks (NCCL all-to-all FFT transposes, P2P halos):
+        # the same 256^3 problem split across GPUs, i.e. strong scaling
+        try:
+            uid = [V.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx = V.DistContext(n, rank, world, uid[0], device=dev, halo=12)
+            d_mT, d_v, d_vt = (ctx.to_device(ctx.slab(a)) for a in (m_T, v, vt))
+            # m_R = m_T transported by v: the state history of an objective at v
+            tmp = V.Objective(ctx, d_mT, d_mT, model)
+            s0 = tmp.evaluate(d_v)
+            d_mR = ctx.to_device(s0.m_history[nt])
+            s0.close()
+            tmp.close()
+            parallelism, scaling = f"x1-slabs-{world}", "strong"
+        except Exception as exc:  # report and run per-GPU replicas instead
+            slab_note = f"slab path failed ({type(exc).__name__}: {exc}); ran replicas"
+            print(slab_note, file=sys.stderr, flush=True)
+            ctx = None
+    if ctx is None:
+        ctx = vr.Context(n, device=dev)
+        d_mT = ctx.to_device(m_T)
+        d_v = ctx.to_device(v)
+        d_vt = ctx.to_device(vt)
+        hist = V.solve_state(ctx, d_mT, d_v, nt)                   # m_R = m_T transported by v
+        d_mR = ctx.empty(1)
+        _ = V._lib.call("vr_memcpy_d2d", ctx.handle, d_mR.ptr, hist.field(nt), 8 * ctx.N)
+        if world > 1:
+            parallelism = "replicas"
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev))
     obj = V.Objective(ctx, d_mR, d_mT, model)
     st = obj.evaluate(d_v)
     obj.compute_gradient(st)
@@ -254,18 +280,19 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * args.steps / (ms / 1e3)
+    per_step_units = 1 if scaling == "strong" else world  # one global matvec vs one per replica
+    value = per_step_units * args.steps / (ms / 1e3)
 
     # ---- end to end through the public C ABI with host buffers -------------
     e2e = None
     if not args.no_e2e:
-        nbytes = 3 * ctx.N * 8
+        nbytes = 3 * ctx.N * 8  # this rank's vt in / H vt out
         hp_in, hp_out = V.C.c_void_p(), V.C.c_void_p()
         V._lib.call("vr_host_alloc_pinned", nbytes, V.C.byref(hp_in))
         V._lib.call("vr_host_alloc_pinned", nbytes, V.C.byref(hp_out))
         h_in = np.ctypeslib.as_array((V.C.c_double * (3 * ctx.N)).from_address(hp_in.value))
         h_out = np.ctypeslib.as_array((V.C.c_double * (3 * ctx.N)).from_address(hp_out.value))
-        h_in[:] = vt.ravel()
+        h_in[:] = (ctx.slab(vt) if scaling == "strong" else vt).ravel()
         obj.hessian_matvec_host(st, h_in, h_out)
         if dist is not None:
             dist.barrier()
@@ -281,8 +308,8 @@ def main():
             t = torch.tensor([ms_e2e], device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
-        e2e = {"value": world * k_e2e / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes, "steps": k_e2e,
+        e2e = {"value": per_step_units * k_e2e / (ms_e2e / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world, "steps": k_e2e,
                "path": "vr_hessian_matvec_host (pinned host vt in, H vt out)"}
         V._lib.call("vr_host_free_pinned", hp_in)
         V._lib.call("vr_host_free_pinned", hp_out)
@@ -290,6 +317,8 @@ def main():
     # ---- roofline of the dominant kernel ------------------------------------
     peak, peak_kind = measured_peak()
     per_matvec_bytes, per_launch = bytes_model(n, nt)
+    share = ctx.N / float(n ** 3)  # this rank's fraction of the grid (1 unless slabs)
+    per_launch = {k: b * share for k, b in per_launch.items()}
     kernels = {k: {"launches": c, "total_ms": t, "avg_ms": t / c if c else None,
                    "share": t / ms if ms else None} for k, (c, t) in prof.items()}
     dom = max((k for k in prof if k in per_launch), key=lambda k: prof[k][1], default=None)
@@ -313,7 +342,8 @@ def main():
         params = V.make_params(eps_opt=1e-2)
         ctx.synchronize()
         t0 = time.perf_counter()
-        vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + (n,) * 3), model, params)
+        vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + ctx.local_dims), model,
+                                                 params)
         ctx.synchronize()
         t_solve = time.perf_counter() - t0
         solve["config3"] = {
@@ -364,10 +394,10 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": desc, "grid": n, "nt": nt, "l2": "inputs larger than L2 (each fp64 field "
                            f"{8 * n ** 3 / 2 ** 20:.0f} MiB; ~{int(per_matvec_bytes / 8 / n ** 3)} fields touched per step)",
-                           "parallelism": "replicas" if world > 1 else "single"},
+                           "parallelism": parallelism, **({"note": slab_note} if slab_note else {})},
                 "e2e": e2e, "gpu_launches": launches, "roofline": roof, "matvec_roofline": matvec_roof,
                 "kernels": kernels, "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve}
         print(json.dumps(line), flush=True)

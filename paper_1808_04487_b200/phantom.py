@@ -37,7 +37,7 @@ def gaussian_smooth_np(f, sigma_voxels):
     h = (TWO_PI / n1, TWO_PI / n2, TWO_PI / n3)
     s = sigma_voxels
     e = (s[0] * s[0] * h[0] * h[0]) * k1 * k1 + (s[1] * s[1] * h[1] * h[1]) * k2 * k2 + (s[2] * s[2] * h[2] * h[2]) * k3 * k3
-    return np.fft.irfftn(np.fft.rfftn(f) * np.exp(-0.5 * e), s=f.shape)
+    return np.fft.irfftn(np.fft.rfftn(f) * np.exp(-0.5 * e), s=f.shape, axes=(0, 1, 2))
 
 
 def ellipsoid_phantom(n, count=40, seed=1808, sigma_voxels=2.0):
@@ -86,7 +86,7 @@ def bandlimited_velocity(n, kmax, max_disp, seed=4487):
         rng = np.random.default_rng(seed + 7919 * (c + 1))
         spec = np.zeros((n, n, n // 2 + 1), dtype=np.complex128)
         spec[mask] = rng.standard_normal(nnz) + 1j * rng.standard_normal(nnz)
-        v[c] = np.fft.irfftn(spec, s=(n, n, n))
+        v[c] = np.fft.irfftn(spec, s=(n, n, n), axes=(0, 1, 2))
     mag = np.sqrt((v * v).sum(axis=0)).max()
     return v * (max_disp / mag)
 
@@ -106,7 +106,7 @@ def bandlimited_direction(n, kmax_inf=2, seed=142):
         rng = np.random.default_rng(seed + 7919 * (c + 1))
         spec = np.zeros((n, n, n // 2 + 1), dtype=np.complex128)
         spec[mask] = rng.standard_normal(nnz) + 1j * rng.standard_normal(nnz)
-        f = np.fft.irfftn(spec, s=(n, n, n))
+        f = np.fft.irfftn(spec, s=(n, n, n), axes=(0, 1, 2))
         out[c] = f / np.abs(f).max()
     return out
 
