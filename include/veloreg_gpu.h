@@ -321,6 +321,16 @@ int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T,
  * transport solves) stay one-GPU only and raise ArgumentError on a slab ctx.
  * `halo` = x1 planes exchanged on each side of every gathered field; it must
  * cover the largest per-step x1 displacement + 4 (checked per velocity). */
+/* Host-only slab geometry (no GPU, no context): validates (n1,n2,n3,nranks,halo)
+ * as vr_ctx_create_dist does and fills out[VR_SLAB_FIELDS] =
+ * {planes L, first_plane off1, halo H, x2 rows per rank of the transposed
+ *  spectrum n2s, first x2 row k2_off, local points L n2 n3, local spectrum
+ *  L n2 (n3/2+1), halo-padded field stride (L+2H) n2 n3, global points}. */
+#define VR_SLAB_FIELDS 9
+int vr_slab_layout(int n1, int n2, int n3, int rank, int nranks, int halo, long long* out);
+/* Halo planes a velocity with max |v_1| = vmax_x1 needs at n_t steps on an n1
+ * grid (the check vr_evaluate applies on a slab context). */
+int vr_slab_halo_required(double vmax_x1, int nt, int n1, int* planes);
 /* NCCL unique id (128 bytes) created on one rank and broadcast by the caller */
 int vr_nccl_unique_id(unsigned char out[128]);
 /* one process per GPU: NCCL communicator over nranks, this process = rank */

@@ -206,6 +206,8 @@ SIGNATURES = {
                                       C.POINTER(C.c_int), C.POINTER(IterationRecord), I]),
     "vr_generate_synthetic": (I, [P, I, D, DP, DP, DP]),
     "vr_nccl_unique_id": (I, [C.c_char_p]),
+    "vr_slab_layout": (I, [I, I, I, I, I, I, C.POINTER(C.c_longlong)]),
+    "vr_slab_halo_required": (I, [C.c_double, I, I, C.POINTER(C.c_int)]),
     "vr_ctx_create_dist": (I, [I, I, I, I, I, I, C.c_char_p, I, C.POINTER(P)]),
     "vr_ctx_slab": (I, [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                         C.POINTER(C.c_int), C.POINTER(C.c_int)]),

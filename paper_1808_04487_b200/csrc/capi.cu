@@ -146,7 +146,8 @@ namespace vr {
 
 // Grid3 checks (grid.hpp:24-31) plus the GPU FFT domain; with a transport of
 // size P > 1 the context owns the x1 slab of rank t->rank
-vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
+// x1-slab geometry of rank `rank` of P; host only.
+void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& g) {
     const int d[3] = {n1, n2, n3};
     for (int a = 0; a < 3; ++a)
         if (d[a] < 4)
@@ -157,13 +158,42 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
             throw_dimension("vr_ctx_create: GPU grids need power-of-two dims <= 1024, got " +
                             std::to_string(n1) + "x" + std::to_string(n2) + "x" +
                             std::to_string(n3));
-    const int P = t ? t->size : 1;
+    if (P < 1 || rank < 0 || rank >= P) throw_argument("x1 slabs: rank must be in [0, nranks)");
     if (P > 1) {
         if (n1 % P != 0 || n2 % P != 0 || n1 / P < 4)
             throw_argument("x1 slabs: n1 and n2 must be divisible by the rank count, >= 4 planes each");
         if (halo < 4 || halo > n1 / P)
             throw_argument("x1 slabs: halo must be in [4, n1/P]");
     }
+    g.n1 = n1;
+    g.n2 = n2;
+    g.n3 = n3;
+    g.nh = n3 / 2 + 1;
+    g.dist = P > 1;
+    g.L = n1 / P;
+    g.off1 = rank * g.L;
+    g.halo = P > 1 ? halo : 0;
+    g.n2s = n2 / P;
+    g.k2_off = rank * g.n2s;
+    g.N = static_cast<long long>(g.L) * n2 * n3;
+    g.NC = static_cast<long long>(g.L) * n2 * g.nh;
+    g.Ng = static_cast<long long>(n1) * n2 * n3;
+    g.h1 = kTwoPi / n1;
+    g.h2 = kTwoPi / n2;
+    g.h3 = kTwoPi / n3;
+    g.flags = nullptr;
+}
+
+int halo_required(double vmax_x1, int nt, int n1) {
+    // RK2 departure points move at most dt max|v_1| (+10% for the midpoint
+    // interpolant's overshoot) and the stencil reaches 2 planes beyond floor(u) - 1
+    return static_cast<int>(std::ceil(1.1 * vmax_x1 / nt / (kTwoPi / n1))) + 4;
+}
+
+vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
+    const int P = t ? t->size : 1;
+    GridDims geo;
+    slab_geometry(n1, n2, n3, P, P > 1 ? t->rank : 0, halo, geo);
     int count = 0;
     VR_CUDA(cudaGetDeviceCount(&count));
     if (device < 0 || device >= count)
@@ -174,22 +204,7 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
         ctx->device = device;
         ctx->dist = P > 1 ? t : nullptr;
         GridDims& g = ctx->g;
-        g.n1 = n1;
-        g.n2 = n2;
-        g.n3 = n3;
-        g.nh = n3 / 2 + 1;
-        g.dist = P > 1;
-        g.L = n1 / P;
-        g.off1 = (P > 1 ? t->rank : 0) * g.L;
-        g.halo = P > 1 ? halo : 0;
-        g.n2s = n2 / P;
-        g.k2_off = (P > 1 ? t->rank : 0) * g.n2s;
-        g.N = static_cast<long long>(g.L) * n2 * n3;
-        g.NC = static_cast<long long>(g.L) * n2 * g.nh;
-        g.Ng = static_cast<long long>(n1) * n2 * n3;
-        g.h1 = kTwoPi / n1;
-        g.h2 = kTwoPi / n2;
-        g.h3 = kTwoPi / n3;
+        g = geo;
         ctx->hstride = static_cast<long long>(g.L + 2 * g.halo) * n2 * n3;
         VR_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         VR_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
@@ -219,6 +234,27 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
 }  // namespace vr
 
 extern "C" {
+
+int vr_slab_layout(int n1, int n2, int n3, int rank, int nranks, int halo, long long* out) {
+    return guard([&] {
+        need(out != nullptr, "vr_slab_layout");
+        vr::GridDims g;
+        vr::slab_geometry(n1, n2, n3, nranks, rank, halo, g);
+        const long long v[VR_SLAB_FIELDS] = {
+            g.L, g.off1, g.halo, g.n2s, g.k2_off, g.N, g.NC,
+            static_cast<long long>(g.L + 2 * g.halo) * n2 * n3, g.Ng};
+        for (int i = 0; i < VR_SLAB_FIELDS; ++i) out[i] = v[i];
+    });
+}
+
+int vr_slab_halo_required(double vmax_x1, int nt, int n1, int* planes) {
+    return guard([&] {
+        need(planes != nullptr, "vr_slab_halo_required");
+        if (nt < 1 || n1 < 4 || !(vmax_x1 >= 0.0) || !std::isfinite(vmax_x1))
+            vr::throw_argument("vr_slab_halo_required: need nt >= 1, n1 >= 4, finite vmax >= 0");
+        *planes = vr::halo_required(vmax_x1, nt, n1);
+    });
+}
 
 int vr_ctx_destroy(vr_ctx* ctx) {
     if (!ctx) return VR_OK;

@@ -169,10 +169,10 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
         if (ctx->dist) {
             // the departure points of this velocity must stay within the halo
             const double vmax = max_abs(ctx, v3, N);  // |v_1|, all ranks
-            const double need = std::ceil(1.1 * vmax / nt / g.h1) + 4.0;
+            const int need = halo_required(vmax, nt, g.n1);
             if (need > g.halo)
                 throw_resource("evaluate: x1 displacement needs a halo of " +
-                               std::to_string(static_cast<int>(need)) + " planes, ctx has " +
+                               std::to_string(need) + " planes, ctx has " +
                                std::to_string(g.halo));
             s->vpad = dev_alloc(ctx, 3 * ctx->hstride);
             for (int c = 0; c < 3; ++c) {

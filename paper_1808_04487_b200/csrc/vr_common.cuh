@@ -146,6 +146,8 @@ constexpr int kRedThreads = 256;
 // create a context for grid (n1, n2, n3) on `device`; with a transport of size
 // P > 1 it owns that rank's x1 slab with `halo` planes (capi.cu)
 vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo);
+void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& g);
+int halo_required(double vmax_x1, int nt, int n1);
 void set_last_error(int cls, const std::string& msg);  // the C ABI's vr_last_error slot
 double* spec_buf(vr_ctx* ctx, int i);   // NC complex (2*NC doubles)
 double* field_buf(vr_ctx* ctx, int i);  // N doubles

@@ -587,6 +587,25 @@ def parameter_continuation(ctx, m_R, m_T, v0, model=None, params=None, precond="
 
 
 # ---- x1-slab decomposition ---------------------------------
+SLAB_FIELDS = ("planes", "first_plane", "halo", "n2s", "k2_off", "points", "spectrum",
+               "padded_stride", "global_points")
+
+
+def slab_layout(dims, rank: int, nranks: int, halo: int) -> dict:
+    """x1-slab geometry of `rank` (host only, no GPU): vr_slab_layout."""
+    n1, n2, n3 = (dims,) * 3 if isinstance(dims, int) else tuple(dims)
+    out = (C.c_longlong * len(SLAB_FIELDS))()
+    _lib.call("vr_slab_layout", n1, n2, n3, rank, nranks, halo, out)
+    return dict(zip(SLAB_FIELDS, (int(x) for x in out)))
+
+
+def slab_halo_required(vmax_x1: float, nt: int, n1: int) -> int:
+    """Halo planes a velocity with max |v_1| = vmax_x1 needs (vr_slab_halo_required)."""
+    planes = C.c_int()
+    _lib.call("vr_slab_halo_required", float(vmax_x1), nt, n1, C.byref(planes))
+    return planes.value
+
+
 def nccl_unique_id() -> bytes:
     """NCCL unique id for vr_ctx_create_dist (create on one rank, broadcast)."""
     buf = C.create_string_buffer(128)
