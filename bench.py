@@ -261,7 +261,6 @@ def main():
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    ctx.set_profiling(True)
     l0 = ctx.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(dev) as clk:
@@ -271,14 +270,27 @@ def main():
         e1.record(stream)
         e1.synchronize()
     launches = ctx.kernel_launches() - l0
-    prof = ctx.profile_read()
-    ctx.set_profiling(False)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     if dist is not None:
         t = torch.tensor([ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+
+    # ---- per-kernel CUDA-event profile: a second pass of the same steps with
+    # every kernel bracketed by events on its launch stream (side-stream work
+    # serialised, so each interval is one kernel running alone) ------------------
+    k_prof = max(3, min(args.steps, 20))
+    ctx.set_profiling(True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(k_prof):
+        obj.hessian_matvec(st, d_vt, out=out)
+    p1.record(stream)
+    p1.synchronize()
+    prof = ctx.profile_read()
+    ctx.set_profiling(False)
+    ms_prof = p0.elapsed_time(p1)
     ms_per_step = ms / args.steps
     per_step_units = 1 if scaling == "strong" else world  # one global matvec vs one per replica
     value = per_step_units * args.steps / (ms / 1e3)
@@ -320,7 +332,7 @@ def main():
     share = ctx.N / float(n ** 3)  # this rank's fraction of the grid (1 unless slabs)
     per_launch = {k: b * share for k, b in per_launch.items()}
     kernels = {k: {"launches": c, "total_ms": t, "avg_ms": t / c if c else None,
-                   "share": t / ms if ms else None} for k, (c, t) in prof.items()}
+                   "share": t / ms_prof if ms_prof else None} for k, (c, t) in prof.items()}
     dom = max((k for k in prof if k in per_launch), key=lambda k: prof[k][1], default=None)
     roof = None
     if dom is not None:
@@ -399,7 +411,9 @@ def main():
                            f"{8 * n ** 3 / 2 ** 20:.0f} MiB; ~{int(per_matvec_bytes / 8 / n ** 3)} fields touched per step)",
                            "parallelism": parallelism, **({"note": slab_note} if slab_note else {})},
                 "e2e": e2e, "gpu_launches": launches, "roofline": roof, "matvec_roofline": matvec_roof,
-                "kernels": kernels, "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve}
+                "kernels": kernels, "kernel_profile": {"steps": k_prof, "ms_per_step": ms_prof / k_prof,
+                                                        "note": "separate serialised pass, events per kernel"},
+                "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -182,7 +182,9 @@ long long vr_ctx_kernel_launches(const vr_ctx* ctx);
 void vr_ctx_reset_kernel_launches(vr_ctx* ctx);
 
 /* Optional per-launch CUDA-event timing on the ctx stream (bench / roofline
- * evidence). vr_ctx_profile_read writes "category,launches,total_ms" lines
+ * evidence). While on, work that normally overlaps on the side stream runs
+ * in order on the ctx stream, so each event pair brackets one kernel running
+ * alone. vr_ctx_profile_read writes "category,launches,total_ms" lines
  * for the launches since profiling was enabled (or last read) and resets. */
 int vr_ctx_set_profiling(vr_ctx* ctx, int on);
 int vr_ctx_profile_read(vr_ctx* ctx, char* buf, size_t len);

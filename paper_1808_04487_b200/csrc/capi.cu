@@ -202,6 +202,8 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
     auto* ctx = new vr_ctx();
     try {
         ctx->device = device;
+        VR_CUDA(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+        if (const char* e = std::getenv("VR_OVERLAP")) ctx->overlap = std::atoi(e) != 0;
         ctx->dist = P > 1 ? t : nullptr;
         GridDims& g = ctx->g;
         g = geo;
@@ -303,6 +305,7 @@ int vr_ctx_set_profiling(vr_ctx* ctx, int on) {
     return guard([&] {
         set_dev(ctx);
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        VR_CUDA(cudaStreamSynchronize(ctx->side));
         ctx->profiling = on != 0;
         ctx->prof.clear();
         ctx->ev_used = 0;

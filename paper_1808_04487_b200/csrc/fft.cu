@@ -250,11 +250,20 @@ __device__ __forceinline__ double2 apply_mult(double2 m, double2 c) {
 // --------------------------------------------------------------------------
 // strided-axis kernel (x1 / x2 passes)
 // --------------------------------------------------------------------------
+#ifndef VR_AXIS_THREADS
+#define VR_AXIS_THREADS 256
+#endif
+#ifndef VR_AXIS_MINB
+#define VR_AXIS_MINB 2
+#endif
+#ifndef VR_ROW_THREADS
+#define VR_ROW_THREADS 128
+#endif
 template <int N>
 struct AxisCfg {
     static constexpr int RMAX = rmax_of(N);
     static constexpr int T = N / RMAX;
-    static constexpr int TB0 = 256 / T;
+    static constexpr int TB0 = VR_AXIS_THREADS / T;
     static constexpr int TB = TB0 < 1 ? 1 : (TB0 > 64 ? 64 : TB0);
     static constexpr int THREADS = TB * T;
     static constexpr size_t SMEM = sizeof(double2) * (N * TB + N);  // data + twiddle table
@@ -264,7 +273,7 @@ struct AxisCfg {
 // MODE 1: forward -> multiplier -> inverse (x1 pass only), src -> dst (may alias)
 // MODE 2: like 1 but dst += result (accumulate)
 template <int N, int DIR, int MODE>
-__global__ void __launch_bounds__(AxisCfg<N>::THREADS, 2)
+__global__ void __launch_bounds__(AxisCfg<N>::THREADS, VR_AXIS_MINB)
     k_fft_axis(const double2* src, double2* dst, long long inner, long long outer_stride,
                const double2* __restrict__ tw_g, MultDev m, GridDims g) {
     using C = AxisCfg<N>;
@@ -297,8 +306,13 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 2)
         // x1 pass: column cc = i2 * nh + i3
         const int i2 = static_cast<int>(cc / g.nh) + g.k2_off;  // k2-slab on x1 slabs
         const int i3 = static_cast<int>(cc % g.nh);
-        auto store_mult = [&](int i, double2 v) { sm(i) = apply_mult(mult_at(m, g, i, i2, i3), v); };
-        fft_line<N, -1, false, true>(t, tw, load, store_mult, sm);
+        auto store_sm = [&](int i, double2 v) { sm(i) = v; };
+        fft_line<N, -1, false, true>(t, tw, load, store_sm, sm);
+        __syncthreads();
+        // one (not unrolled) copy of the multiplier code: inlining mult_at into
+        // every butterfly store made this kernel ~40k instructions (i-cache bound)
+#pragma unroll 1
+        for (int i = t; i < N; i += C::T) sm(i) = apply_mult(mult_at(m, g, i, i2, i3), sm(i));
         __syncthreads();
         auto load_sm = [&](int i) -> double2 { return sm(i); };
         fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
@@ -308,15 +322,32 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 2)
 // --------------------------------------------------------------------------
 // x3 row kernels (real rows <-> half-spectrum rows)
 // --------------------------------------------------------------------------
+// Persistent CTAs walk tiles of RB rows with a two-stage cp.async pipeline: the
+// next tile's rows stream into the other shared-memory stage while this tile is
+// transformed, so HBM reads overlap the butterflies (the one-tile-per-CTA
+// version sat at ~2 TB/s, latency bound at 25% occupancy).
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc),
+                 "r"(pred ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 template <int M>
 struct RowCfg {
     static constexpr int RMAX = rmax_of(M);
     static constexpr int T = M / RMAX;
-    static constexpr int RB0 = 256 / T;
+    static constexpr int RB0 = VR_ROW_THREADS / T;
     static constexpr int RB = RB0 < 1 ? 1 : (RB0 > 64 ? 64 : RB0);
     static constexpr int THREADS = RB * T;
     static constexpr int LD = (M + 1) + ((M + 1) >> 4) + 1;  // padded row length
-    static constexpr size_t SMEM = sizeof(double2) * (LD * RB + 3 * M);  // rows + W_M, W_2M tables
+    static constexpr int STAGE = LD * RB;                     // one pipeline stage (double2)
+    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + 3 * M);  // 2 stages + W_M, W_2M
 };
 // stage the W_M and W_N (N = 2M) twiddle tables in shared memory after the rows
 template <int M>
@@ -324,61 +355,83 @@ __device__ __forceinline__ void stage_row_tables(double2* smem, const double2* t
                                                  const double2* twN_g, double2*& twM,
                                                  double2*& twN) {
     using C = RowCfg<M>;
-    twM = smem + C::LD * C::RB;
+    twM = smem + 2 * C::STAGE;
     twN = twM + M;
     for (int i = threadIdx.x; i < M; i += C::THREADS) twM[i] = __ldg(twM_g + i);
     for (int i = threadIdx.x; i < 2 * M; i += C::THREADS) twN[i] = __ldg(twN_g + i);
 }
 __device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
 
+// async copy of tile `tile` (RB rows of W double2 each, row-contiguous in src)
+// into a padded stage; rows past nrows are zero-filled
+template <int M, int W>
+__device__ __forceinline__ void load_rows_async(double2* stage, const double2* src, long long tile,
+                                                long long nrows) {
+    using C = RowCfg<M>;
+    const long long base = tile * C::RB * W;
+    const long long avail = (nrows - tile * C::RB) * W;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < C::RB * W; e += C::THREADS) {
+        const int r = e / W, i = e % W;
+        const bool ok = e < avail;
+        cp_async16(stage + r * C::LD + padi(i), src + base + (ok ? e : 0), ok);
+    }
+}
+
 // r2c along x3: in nrows x 2M reals -> out nrows x (M+1) complex.
 // z[m] = x[2m] + i x[2m+1]; Z = FFT_M(z); X[k] = A[k] + W_N^k B[k] with
 // A = (Z[k] + conj Z[M-k]) / 2, B = (Z[k] - conj Z[M-k]) / 2i.
 template <int M>
-__global__ void __launch_bounds__(RowCfg<M>::THREADS, 2)
+__global__ void __launch_bounds__(RowCfg<M>::THREADS)
     k_r2c_rows(const double* __restrict__ in, double2* __restrict__ out, long long nrows,
                const double2* __restrict__ twM_g, const double2* __restrict__ twN_g) {
     using C = RowCfg<M>;
     extern __shared__ double2 smem[];
     double2 *twM, *twN;
     stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
-    const long long row0 = blockIdx.x * (long long)C::RB;
-    const double2* src = reinterpret_cast<const double2*>(in) + row0 * M;
-    const long long avail = (nrows - row0) * M;
-    for (int e = threadIdx.x; e < C::RB * M; e += C::THREADS) {
-        const int r = e / M, i = e % M;
-        smem[r * C::LD + padi(i)] = (e < avail) ? src[e] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-    {
-        const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
-        auto sm = [&](int i) -> double2& { return smem[r * C::LD + padi(i)]; };
-        auto load = [&](int i) -> double2 { return sm(i); };
-        auto store = [&](int i, double2 v) { sm(i) = v; };
-        fft_line<M, -1, true, true>(t, twM, load, store, sm);
-    }
-    __syncthreads();
-    double2* dstp = out + row0 * (M + 1);
-    const long long avail_out = (nrows - row0) * (M + 1);
-    for (int e = threadIdx.x; e < C::RB * (M + 1); e += C::THREADS) {
-        if (e >= avail_out) break;
-        const int r = e / (M + 1), k = e % (M + 1);
-        const double2* Z = smem + r * C::LD;
-        double2 X;
-        if (k == 0 || k == M) {
-            const double2 z0 = Z[0];
-            X = make_double2(k == 0 ? z0.x + z0.y : z0.x - z0.y, 0.0);
-        } else {
-            const double2 zk = Z[padi(k)];
-            const double2 zc = cconj(Z[padi(M - k)]);
-            const double2 A = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
-            const double2 D = make_double2(0.5 * (zk.x - zc.x), 0.5 * (zk.y - zc.y));
-            const double2 B = make_double2(D.y, -D.x);  // D / i
-            double2 w = twN[k];
-            w.y = -w.y;  // exp(-2 pi i k / N)
-            X = cadd(A, cmul(w, B));
+    const double2* src = reinterpret_cast<const double2*>(in);
+    const long long ntiles = (nrows + C::RB - 1) / C::RB;
+    long long tile = blockIdx.x;
+    if (tile < ntiles) load_rows_async<M, M>(smem, src, tile, nrows);
+    cp_async_commit();
+    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
+        const long long next = tile + gridDim.x;
+        if (next < ntiles) load_rows_async<M, M>(smem + (b ^ 1) * C::STAGE, src, next, nrows);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        double2* buf = smem + b * C::STAGE;
+        {
+            const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
+            auto sm = [&](int i) -> double2& { return buf[r * C::LD + padi(i)]; };
+            auto load = [&](int i) -> double2 { return sm(i); };
+            auto store = [&](int i, double2 v) { sm(i) = v; };
+            fft_line<M, -1, true, true>(t, twM, load, store, sm);
         }
-        dstp[e] = X;
+        __syncthreads();
+        double2* dstp = out + tile * C::RB * (M + 1);
+        const long long avail_out = (nrows - tile * C::RB) * (M + 1);
+        for (int e = threadIdx.x; e < C::RB * (M + 1); e += C::THREADS) {
+            if (e >= avail_out) break;
+            const int r = e / (M + 1), k = e % (M + 1);
+            const double2* Z = buf + r * C::LD;
+            double2 X;
+            if (k == 0 || k == M) {
+                const double2 z0 = Z[0];
+                X = make_double2(k == 0 ? z0.x + z0.y : z0.x - z0.y, 0.0);
+            } else {
+                const double2 zk = Z[padi(k)];
+                const double2 zc = cconj(Z[padi(M - k)]);
+                const double2 A = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
+                const double2 D = make_double2(0.5 * (zk.x - zc.x), 0.5 * (zk.y - zc.y));
+                const double2 B = make_double2(D.y, -D.x);  // D / i
+                double2 w = twN[k];
+                w.y = -w.y;  // exp(-2 pi i k / N)
+                X = cadd(A, cmul(w, B));
+            }
+            dstp[e] = X;
+        }
+        __syncthreads();  // this stage is refilled by the next iteration's prefetch
     }
 }
 
@@ -387,69 +440,84 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS, 2)
 // O = (X[k] - conj X[M-k]) exp(+2 pi i k / N); z = IFFT_M(Z); x[2m] = Re, x[2m+1] = Im.
 // Imaginary parts of the self-conjugate bins X[0], X[M] are ignored (c2r semantics).
 template <int M>
-__global__ void __launch_bounds__(RowCfg<M>::THREADS, 2)
+__global__ void __launch_bounds__(RowCfg<M>::THREADS)
     k_c2r_rows(const double2* __restrict__ in, double* __restrict__ out, long long nrows,
                const double2* __restrict__ twM_g, const double2* __restrict__ twN_g, double scale,
                const double* __restrict__ add) {
     using C = RowCfg<M>;
+    constexpr int PER = C::RB * M / C::THREADS;  // output double2 per thread per tile
     extern __shared__ double2 smem[];
     double2 *twM, *twN;
     stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
-    const long long row0 = blockIdx.x * (long long)C::RB;
-    const double2* src = in + row0 * (M + 1);
-    const long long avail = (nrows - row0) * (M + 1);
-    for (int e = threadIdx.x; e < C::RB * (M + 1); e += C::THREADS) {
-        const int r = e / (M + 1), i = e % (M + 1);
-        smem[r * C::LD + padi(i)] = (e < avail) ? src[e] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-    // form Z in place: thread handles the pair (k, M-k), k in [0, M/2]
-    for (int e = threadIdx.x; e < C::RB * (M / 2 + 1); e += C::THREADS) {
-        const int r = e / (M / 2 + 1), k = e % (M / 2 + 1);
-        double2* X = smem + r * C::LD;
-        if (k == 0) {
-            const double a = X[0].x, b = X[padi(M)].x;
-            X[0] = make_double2(a + b, a - b);
-        } else {
-            const double2 xk = X[padi(k)], xm = X[padi(M - k)];
-            const double2 wk = twN[k];     // exp(+2 pi i k / N)
-            const double2 wm = twN[M - k]; // exp(+2 pi i (M-k) / N)
-            {
-                const double2 E = cadd(xk, cconj(xm));
-                const double2 O = cmul(csub(xk, cconj(xm)), wk);
-                X[padi(k)] = make_double2(E.x - O.y, E.y + O.x);
-            }
-            if (k != M - k) {
-                const double2 E = cadd(xm, cconj(xk));
-                const double2 O = cmul(csub(xm, cconj(xk)), wm);
-                X[padi(M - k)] = make_double2(E.x - O.y, E.y + O.x);
+    const long long ntiles = (nrows + C::RB - 1) / C::RB;
+    long long tile = blockIdx.x;
+    if (tile < ntiles) load_rows_async<M, M + 1>(smem, in, tile, nrows);
+    cp_async_commit();
+    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
+        const long long next = tile + gridDim.x;
+        if (next < ntiles) load_rows_async<M, M + 1>(smem + (b ^ 1) * C::STAGE, in, next, nrows);
+        cp_async_commit();
+        const long long avail_out = (nrows - tile * C::RB) * M;
+        double2* dstp = reinterpret_cast<double2*>(out) + tile * C::RB * M;
+        // the add field's loads are issued now and land while the rows transform
+        double2 addv[PER];
+        if (add) {
+            const double2* addp = reinterpret_cast<const double2*>(add) + tile * C::RB * M;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int e = threadIdx.x + j * C::THREADS;
+                addv[j] = e < avail_out ? __ldcs(addp + e) : make_double2(0.0, 0.0);
             }
         }
-    }
-    __syncthreads();
-    {
-        const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
-        auto sm = [&](int i) -> double2& { return smem[r * C::LD + padi(i)]; };
-        auto load = [&](int i) -> double2 { return sm(i); };
-        auto store = [&](int i, double2 v) { sm(i) = v; };
-        fft_line<M, +1, true, true>(t, twM, load, store, sm);
-    }
-    __syncthreads();
-    double2* dstp = reinterpret_cast<double2*>(out) + row0 * M;
-    const double2* addp = add ? reinterpret_cast<const double2*>(add) + row0 * M : nullptr;
-    const long long avail_out = (nrows - row0) * M;
-    for (int e = threadIdx.x; e < C::RB * M; e += C::THREADS) {
-        if (e >= avail_out) break;
-        const int r = e / M, i = e % M;
-        const double2 z = smem[r * C::LD + padi(i)];
-        double2 o;
-        if (addp) {
-            const double2 a = addp[e];
-            o = make_double2(a.x + scale * z.x, a.y + scale * z.y);
-        } else {
-            o = make_double2(z.x * scale, z.y * scale);
+        cp_async_wait<1>();
+        __syncthreads();
+        double2* buf = smem + b * C::STAGE;
+        // form Z in place: thread handles the pair (k, M-k), k in [0, M/2]
+        for (int e = threadIdx.x; e < C::RB * (M / 2 + 1); e += C::THREADS) {
+            const int r = e / (M / 2 + 1), k = e % (M / 2 + 1);
+            double2* X = buf + r * C::LD;
+            if (k == 0) {
+                const double a = X[0].x, bb = X[padi(M)].x;
+                X[0] = make_double2(a + bb, a - bb);
+            } else {
+                const double2 xk = X[padi(k)], xm = X[padi(M - k)];
+                const double2 wk = twN[k];     // exp(+2 pi i k / N)
+                const double2 wm = twN[M - k]; // exp(+2 pi i (M-k) / N)
+                {
+                    const double2 E = cadd(xk, cconj(xm));
+                    const double2 O = cmul(csub(xk, cconj(xm)), wk);
+                    X[padi(k)] = make_double2(E.x - O.y, E.y + O.x);
+                }
+                if (k != M - k) {
+                    const double2 E = cadd(xm, cconj(xk));
+                    const double2 O = cmul(csub(xm, cconj(xk)), wm);
+                    X[padi(M - k)] = make_double2(E.x - O.y, E.y + O.x);
+                }
+            }
         }
-        dstp[e] = o;
+        __syncthreads();
+        {
+            const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
+            auto sm = [&](int i) -> double2& { return buf[r * C::LD + padi(i)]; };
+            auto load = [&](int i) -> double2 { return sm(i); };
+            auto store = [&](int i, double2 v) { sm(i) = v; };
+            fft_line<M, +1, true, true>(t, twM, load, store, sm);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int e = threadIdx.x + j * C::THREADS;
+            if (e >= avail_out) break;
+            const int r = e / M, i = e % M;
+            const double2 z = buf[r * C::LD + padi(i)];
+            double2 o;
+            if (add)
+                o = make_double2(addv[j].x + scale * z.x, addv[j].y + scale * z.y);
+            else
+                o = make_double2(z.x * scale, z.y * scale);
+            dstp[e] = o;
+        }
+        __syncthreads();  // this stage is refilled by the next iteration's prefetch
     }
 }
 
@@ -525,11 +593,11 @@ void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inne
                    long long outer_stride, const double2* tw, const MultDev& m) {
     using C = AxisCfg<N>;
     auto kern = k_fft_axis<N, DIR, MODE>;
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {false};  // the attribute is per device
+    if (!attr[ctx->device & 63]) {
         VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(C::SMEM)));
-        attr = true;
+        attr[ctx->device & 63] = true;
     }
     dim3 grid(static_cast<unsigned>((inner + C::TB - 1) / C::TB), static_cast<unsigned>(outer));
     VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : "fft_x1_mult", kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, dst, inner, outer_stride, tw, m, ctx->g););
@@ -555,29 +623,39 @@ void launch_axis(vr_ctx* ctx, int n, const double2* src, double2* dst, long long
     }
 }
 
+// persistent grid: as many CTAs as fit on the device at once (<= one per tile).
+// `occ` is the caller's per-kernel cache (kernels of one signature share a
+// function-pointer type, so the cache cannot live in a template on K).
+template <class K>
+unsigned persistent_grid(vr_ctx* ctx, K kern, int threads, size_t smem, long long ntiles,
+                         int (&occ)[64]) {
+    const int d = ctx->device & 63;
+    if (!occ[d]) {
+        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        int o = 0;
+        VR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem));
+        occ[d] = o > 0 ? o : 1;
+    }
+    const long long g = static_cast<long long>(occ[d]) * ctx->sms;
+    return static_cast<unsigned>(ntiles < g ? ntiles : g);
+}
+
 template <int M>
 void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double scale,
                    const double* add) {
     using C = RowCfg<M>;
     const long long nrows = static_cast<long long>(ctx->g.L) * ctx->g.n2;  // local rows
-    const unsigned grid = static_cast<unsigned>((nrows + C::RB - 1) / C::RB);
+    const long long ntiles = (nrows + C::RB - 1) / C::RB;
     if (forward) {
-        static bool attr = false;
-        if (!attr) {
-            VR_CUDA(cudaFuncSetAttribute(k_r2c_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::SMEM)));
-            attr = true;
-        }
+        static int occ[64] = {0};
+        const unsigned grid = persistent_grid(ctx, k_r2c_rows<M>, C::THREADS, C::SMEM, ntiles, occ);
         VR_LAUNCH(ctx, "fft_x3_r2c", k_r2c_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double*>(in), static_cast<double2*>(out), nrows, ctx->fft->tw3h,
             ctx->fft->tw3));
     } else {
-        static bool attr = false;
-        if (!attr) {
-            VR_CUDA(cudaFuncSetAttribute(k_c2r_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::SMEM)));
-            attr = true;
-        }
+        static int occ[64] = {0};
+        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M>, C::THREADS, C::SMEM, ntiles, occ);
         VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double2*>(in), static_cast<double*>(out), nrows, ctx->fft->tw3h,
             ctx->fft->tw3, scale, add));

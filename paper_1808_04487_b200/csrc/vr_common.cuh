@@ -109,6 +109,7 @@ struct Transport {
 
 struct vr_ctx {
     int device = 0;
+    int sms = 0;                     // streaming multiprocessors of `device` (persistent grids)
     cudaStream_t stream = nullptr;   // all public calls are ordered on this stream
     cudaStream_t side = nullptr;     // internal: overlaps independent spectral work
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -129,6 +130,10 @@ struct vr_ctx {
     long long launches = 0;
     // optional per-launch CUDA-event timing (bench / roofline evidence)
     bool profiling = false;
+    // side-stream overlap of independent spectral work (VR_OVERLAP=1 enables).
+    // Off by default: the FFT kernels' shared memory shrinks the L1 that the
+    // concurrent gather kernels live on (measured 7.7 vs 6.9 ms per matvec).
+    bool overlap = false;
     struct ProfRec {
         const char* cat;
         cudaEvent_t start, stop;
@@ -258,10 +263,11 @@ void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3);
 // run `fn` (which launches on ctx->stream) on the side stream, forked from the
 // current point of ctx->stream; join_side() makes ctx->stream wait for it
 // (on x1 slabs the work stays on the main stream: its collectives must keep one
-// order on every rank)
+// order on every rank; while profiling too, so per-kernel event intervals do not
+// include time shared with a concurrent kernel)
 template <class Fn>
 void on_side_stream(vr_ctx* ctx, Fn&& fn) {
-    if (ctx->dist) {
+    if (ctx->dist || ctx->profiling || !ctx->overlap) {
         fn();
         return;
     }
@@ -279,7 +285,7 @@ void on_side_stream(vr_ctx* ctx, Fn&& fn) {
     VR_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
 }
 inline void join_side(vr_ctx* ctx) {
-    if (!ctx->dist) VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+    if (!ctx->dist && !ctx->profiling && ctx->overlap) VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
 }
 double reg_symbol(const vr_regnorm& n, double k2);
 
