@@ -204,6 +204,7 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
         ctx->device = device;
         VR_CUDA(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
         if (const char* e = std::getenv("VR_OVERLAP")) ctx->overlap = std::atoi(e) != 0;
+        if (const char* e = std::getenv("VR_FUSE_ACC")) ctx->fuse_acc = std::atoi(e) != 0;
         ctx->dist = P > 1 ? t : nullptr;
         GridDims& g = ctx->g;
         g = geo;

@@ -250,82 +250,10 @@ __device__ __forceinline__ double2 apply_mult(double2 m, double2 c) {
 // --------------------------------------------------------------------------
 // strided-axis kernel (x1 / x2 passes)
 // --------------------------------------------------------------------------
-#ifndef VR_AXIS_THREADS
-#define VR_AXIS_THREADS 256
-#endif
-#ifndef VR_AXIS_MINB
-#define VR_AXIS_MINB 2
-#endif
 #ifndef VR_ROW_THREADS
 #define VR_ROW_THREADS 128
 #endif
-template <int N>
-struct AxisCfg {
-    static constexpr int RMAX = rmax_of(N);
-    static constexpr int T = N / RMAX;
-    static constexpr int TB0 = VR_AXIS_THREADS / T;
-    static constexpr int TB = TB0 < 1 ? 1 : (TB0 > 64 ? 64 : TB0);
-    static constexpr int THREADS = TB * T;
-    static constexpr size_t SMEM = sizeof(double2) * (N * TB + N);  // data + twiddle table
-};
-
-// MODE 0: transform in direction DIR (src may equal dst)
-// MODE 1: forward -> multiplier -> inverse (x1 pass only), src -> dst (may alias)
-// MODE 2: like 1 but dst += result (accumulate)
-template <int N, int DIR, int MODE>
-__global__ void __launch_bounds__(AxisCfg<N>::THREADS, VR_AXIS_MINB)
-    k_fft_axis(const double2* src, double2* dst, long long inner, long long outer_stride,
-               const double2* __restrict__ tw_g, MultDev m, GridDims g) {
-    using C = AxisCfg<N>;
-    extern __shared__ double2 smem[];
-    double2* tw = smem + N * C::TB;  // W_N table staged once per CTA (broadcast reads)
-    for (int i = threadIdx.x; i < N; i += C::THREADS) tw[i] = __ldg(tw_g + i);
-    __syncthreads();
-    const int col = threadIdx.x % C::TB;
-    const int t = threadIdx.x / C::TB;
-    const long long cc = blockIdx.x * (long long)C::TB + col;
-    const bool valid = cc < inner;
-    const long long off = blockIdx.y * outer_stride + (valid ? cc : 0);
-    const double2* s = src + off;
-    double2* d = dst + off;
-    auto sm = [&](int i) -> double2& { return smem[i * C::TB + col]; };
-    auto load = [&](int i) -> double2 {
-        return valid ? s[(long long)i * inner] : make_double2(0.0, 0.0);
-    };
-    auto store = [&](int i, double2 v) {
-        if (valid) {
-            if constexpr (MODE == 2)
-                d[(long long)i * inner] = cadd(d[(long long)i * inner], v);
-            else
-                d[(long long)i * inner] = v;
-        }
-    };
-    if constexpr (MODE == 0) {
-        fft_line<N, DIR, false, false>(t, tw, load, store, sm);
-    } else {
-        // x1 pass: column cc = i2 * nh + i3
-        const int i2 = static_cast<int>(cc / g.nh) + g.k2_off;  // k2-slab on x1 slabs
-        const int i3 = static_cast<int>(cc % g.nh);
-        auto store_sm = [&](int i, double2 v) { sm(i) = v; };
-        fft_line<N, -1, false, true>(t, tw, load, store_sm, sm);
-        __syncthreads();
-        // one (not unrolled) copy of the multiplier code: inlining mult_at into
-        // every butterfly store made this kernel ~40k instructions (i-cache bound)
-#pragma unroll 1
-        for (int i = t; i < N; i += C::T) sm(i) = apply_mult(mult_at(m, g, i, i2, i3), sm(i));
-        __syncthreads();
-        auto load_sm = [&](int i) -> double2 { return sm(i); };
-        fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
-    }
-}
-
-// --------------------------------------------------------------------------
-// x3 row kernels (real rows <-> half-spectrum rows)
-// --------------------------------------------------------------------------
-// Persistent CTAs walk tiles of RB rows with a two-stage cp.async pipeline: the
-// next tile's rows stream into the other shared-memory stage while this tile is
-// transformed, so HBM reads overlap the butterflies (the one-tile-per-CTA
-// version sat at ~2 TB/s, latency bound at 25% occupancy).
+// async global -> shared copies (16 B, zero-fill when !pred) for the pipelined passes
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool pred) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc),
@@ -338,6 +266,93 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+#ifndef VR_AXIS_COLS
+#define VR_AXIS_COLS 2048  // TB = VR_AXIS_COLS / N columns per tile (8 at N = 256)
+#endif
+template <int N>
+struct AxisCfg {
+    static constexpr int RMAX = rmax_of(N);
+    static constexpr int T = N / RMAX;
+    static constexpr int TB0 = VR_AXIS_COLS / N;
+    static constexpr int TB = TB0 < 1 ? 1 : (TB0 > 64 ? 64 : TB0);
+    static constexpr int THREADS = TB * T;
+    static constexpr int STAGE = N * TB;  // one pipeline stage (double2)
+    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + N);  // 2 stages + W_N
+};
+
+// Strided-axis pass over tiles of TB adjacent columns x N elements, persistent
+// CTAs with a two-stage cp.async pipeline (the next tile streams in while this
+// one is transformed; the last butterfly stage stores straight to HBM).
+// MODE 0: transform in direction DIR (src may equal dst)
+// MODE 1: forward -> multiplier -> inverse (x1 pass only), src -> dst (may alias)
+template <int N, int DIR, int MODE>
+__global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
+    k_fft_axis(const double2* src, double2* dst, long long inner, long long outer,
+               long long outer_stride, const double2* __restrict__ tw_g, MultDev m, GridDims g) {
+    using C = AxisCfg<N>;
+    extern __shared__ double2 smem[];
+    double2* tw = smem + 2 * C::STAGE;  // W_N table staged once per CTA (broadcast reads)
+    for (int i = threadIdx.x; i < N; i += C::THREADS) tw[i] = __ldg(tw_g + i);
+    const long long ncb = (inner + C::TB - 1) / C::TB;
+    const long long ntiles = ncb * outer;
+    const int col = threadIdx.x % C::TB;
+    const int t = threadIdx.x / C::TB;
+    auto issue = [&](long long tile, double2* stage) {
+        const long long ob = tile / ncb, c0 = (tile - ob * ncb) * C::TB;
+        const double2* s = src + ob * outer_stride + c0;
+#pragma unroll 4
+        for (int e = threadIdx.x; e < C::STAGE; e += C::THREADS) {
+            const int i = e / C::TB, cl = e % C::TB;
+            const bool ok = c0 + cl < inner;
+            cp_async16(stage + e, s + (ok ? static_cast<long long>(i) * inner + cl : 0), ok);
+        }
+    };
+    long long tile = blockIdx.x;
+    if (tile < ntiles) issue(tile, smem);
+    cp_async_commit();
+    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
+        const long long next = tile + gridDim.x;
+        if (next < ntiles) issue(next, smem + (b ^ 1) * C::STAGE);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        double2* buf = smem + b * C::STAGE;
+        const long long ob = tile / ncb;
+        const long long cc = (tile - ob * ncb) * C::TB + col;
+        const bool valid = cc < inner;
+        double2* d = dst + ob * outer_stride + (valid ? cc : 0);
+        auto sm = [&](int i) -> double2& { return buf[i * C::TB + col]; };
+        auto load_sm = [&](int i) -> double2 { return sm(i); };
+        auto store = [&](int i, double2 v) {
+            if (valid) d[static_cast<long long>(i) * inner] = v;
+        };
+        if constexpr (MODE == 0) {
+            fft_line<N, DIR, true, false>(t, tw, load_sm, store, sm);
+        } else {
+            // x1 pass: column cc = i2 * nh + i3
+            const int i2 = static_cast<int>(cc / g.nh) + g.k2_off;  // k2-slab on x1 slabs
+            const int i3 = static_cast<int>(cc % g.nh);
+            auto store_sm = [&](int i, double2 v) { sm(i) = v; };
+            fft_line<N, -1, true, true>(t, tw, load_sm, store_sm, sm);
+            __syncthreads();
+            // one (not unrolled) copy of the multiplier code: inlining mult_at into
+            // every butterfly store made this kernel ~40k instructions (i-cache bound)
+#pragma unroll 1
+            for (int i = t; i < N; i += C::T) sm(i) = apply_mult(mult_at(m, g, i, i2, i3), sm(i));
+            __syncthreads();
+            fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
+        }
+        __syncthreads();  // this stage is refilled by the next iteration's prefetch
+    }
+}
+
+// --------------------------------------------------------------------------
+// x3 row kernels (real rows <-> half-spectrum rows)
+// --------------------------------------------------------------------------
+// Persistent CTAs walk tiles of RB rows with a two-stage cp.async pipeline: the
+// next tile's rows stream into the other shared-memory stage while this tile is
+// transformed, so HBM reads overlap the butterflies (the one-tile-per-CTA
+// version sat at ~2 TB/s, latency bound at 25% occupancy).
 template <int M>
 struct RowCfg {
     static constexpr int RMAX = rmax_of(M);
@@ -588,19 +603,35 @@ MultDev to_dev(const MultParams& p) {
 }
 
 // ---- host-side launchers ----------------------------------------------------
+// persistent grid: as many CTAs as fit on the device at once (<= one per tile).
+// `occ` is the caller's per-kernel cache (kernels of one signature share a
+// function-pointer type, so the cache cannot live in a template on K).
+template <class K>
+unsigned persistent_grid(vr_ctx* ctx, K kern, int threads, size_t smem, long long ntiles,
+                         int (&occ)[64]) {
+    const int d = ctx->device & 63;
+    if (!occ[d]) {
+        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        int o = 0;
+        VR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem));
+        occ[d] = o > 0 ? o : 1;
+    }
+    const long long g = static_cast<long long>(occ[d]) * ctx->sms;
+    return static_cast<unsigned>(ntiles < g ? ntiles : g);
+}
+
 template <int N, int DIR, int MODE>
 void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inner, long long outer,
                    long long outer_stride, const double2* tw, const MultDev& m) {
     using C = AxisCfg<N>;
-    auto kern = k_fft_axis<N, DIR, MODE>;
-    static bool attr[64] = {false};  // the attribute is per device
-    if (!attr[ctx->device & 63]) {
-        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(C::SMEM)));
-        attr[ctx->device & 63] = true;
-    }
-    dim3 grid(static_cast<unsigned>((inner + C::TB - 1) / C::TB), static_cast<unsigned>(outer));
-    VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : "fft_x1_mult", kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, dst, inner, outer_stride, tw, m, ctx->g););
+    static int occ[64] = {0};
+    const long long ntiles = (inner + C::TB - 1) / C::TB * outer;
+    const unsigned grid =
+        persistent_grid(ctx, k_fft_axis<N, DIR, MODE>, C::THREADS, C::SMEM, ntiles, occ);
+    VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : "fft_x1_mult",
+              k_fft_axis<N, DIR, MODE><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+                  src, dst, inner, outer, outer_stride, tw, m, ctx->g));
 }
 
 template <int DIR, int MODE>
@@ -621,24 +652,6 @@ void launch_axis(vr_ctx* ctx, int n, const double2* src, double2* dst, long long
 #undef VR_CASE
         default: throw_dimension("fft: unsupported axis length " + std::to_string(n));
     }
-}
-
-// persistent grid: as many CTAs as fit on the device at once (<= one per tile).
-// `occ` is the caller's per-kernel cache (kernels of one signature share a
-// function-pointer type, so the cache cannot live in a template on K).
-template <class K>
-unsigned persistent_grid(vr_ctx* ctx, K kern, int threads, size_t smem, long long ntiles,
-                         int (&occ)[64]) {
-    const int d = ctx->device & 63;
-    if (!occ[d]) {
-        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-        int o = 0;
-        VR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem));
-        occ[d] = o > 0 ? o : 1;
-    }
-    const long long g = static_cast<long long>(occ[d]) * ctx->sms;
-    return static_cast<unsigned>(ntiles < g ? ntiles : g);
 }
 
 template <int M>

@@ -303,28 +303,52 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     double* tmp[2] = {pslice(ctx, o->ws_tmp, 0), pslice(ctx, o->ws_tmp, 1)};
     double* lam0 = pslice(ctx, o->ws_lam, 0);
     auto lam = [&](int j) { return pslice(ctx, o->ws_lam, j); };
+    double* b = o->ws_b;
+    const bool identity_K = o->model.projection == VR_PROJ_IDENTITY;
+    // fused: b accumulates inside the sweep (observer order j = nt..0), lam_j ping-pongs
+    const bool fused = ctx->fuse_acc;
     sl_incstate_first(ctx, s->gradm, vt3, hdt, tmp[0]);
     int cur = 0;
     for (int j = 0; j < nt; ++j) {
         const bool last = (j + 1 == nt);
         exchange(ctx, tmp[cur]);
-        sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
-                         last ? lam(nt) : tmp[cur ^ 1], last ? 1 : 0);
+        if (last && fused)
+            sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * nt * N, vt3, hdt, lam(1), 2, b,
+                             0.5 * dt);
+        else
+            sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
+                             last ? lam(nt) : tmp[cur ^ 1], last ? 1 : 0);
         cur ^= 1;
     }
     o->counters.pde_solves += 1;
     // incremental adjoint, Gauss-Newton branch = plain continuity sweep (transport.cpp:188-190)
-    for (int j = nt - 1; j >= 0; --j) {
-        exchange(ctx, lam(j + 1));
-        sl_adjoint_step(ctx, lam(j + 1), s->xf, s->factor, lam(j), nullptr, 0.0, nullptr);
+    bool out_done = false;
+    if (fused) {
+        int lc = 1;  // lam_j alternates between lam(1) and lam(0)
+        for (int j = nt - 1; j >= 0; --j) {
+            const double w = (j == 0) ? 0.5 * dt : dt;
+            // the last step also adds u = beta_v A vt when it is given (out = b + u)
+            const bool fin = (j == 0) && reg_given && identity_K;
+            exchange(ctx, lam(lc));
+            sl_adjoint_step(ctx, lam(lc), s->xf, s->factor, lam(lc ^ 1), s->gradm + 3LL * j * N, w, b,
+                            fin ? reg_given : nullptr, fin ? out3 : b);
+            lc ^= 1;
+            out_done = fin;
+        }
+    } else {
+        for (int j = nt - 1; j >= 0; --j) {
+            exchange(ctx, lam(j + 1));
+            sl_adjoint_step(ctx, lam(j + 1), s->xf, s->factor, lam(j), nullptr, 0.0, nullptr);
+        }
+        if (reg_given && identity_K) {
+            sl_accumulate(ctx, lam0, s->gradm, nt, dt, out3, reg_given);  // out = b + u, one pass
+            out_done = true;
+        } else {
+            sl_accumulate(ctx, lam0, s->gradm, nt, dt, b);
+        }
     }
     o->counters.pde_solves += 1;
-    double* b = o->ws_b;
-    const bool identity_K = o->model.projection == VR_PROJ_IDENTITY;
-    if (reg_given && identity_K) {
-        sl_accumulate(ctx, lam0, s->gradm, nt, dt, out3, reg_given);  // out = b + u, one pass
-    } else {
-        sl_accumulate(ctx, lam0, s->gradm, nt, dt, b);
+    if (!out_done) {
         if (!identity_K)
             op_projection(ctx, b, b, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
         if (add_reg) {

@@ -6,9 +6,10 @@
 // proj/src/transport.cpp:11-237 (trace, factor, steps, sweeps),
 // proj/src/objective.cpp:9-32,96-99,143-148 (fused gradient accumulation).
 //
-// Mapping. A CTA owns a 2 x 4 x 32 tile of output points (x1 x x2 x x3; one warp
-// is one contiguous x3 run), so the 4x4x4 stencils of a CTA touch a compact,
-// heavily reused set of L1 lines (84% L1 hit rate measured at 256^3). Each
+// Mapping. A CTA owns a 1 x 4 x 32 tile of output points (x1 x x2 x x3; one warp
+// is one contiguous x3 run; 128 threads, ~28 resident warps/SM), so the 4x4x4
+// stencils of a CTA touch a compact, heavily reused set of L1 lines (84% L1 hit
+// rate measured at 256^3; the tile / occupancy sweep is in DESIGN.md). Each
 // thread computes its stencil once (u = x / h, 1e-12 node snap, floor, cubic
 // Lagrange weights; interp.hpp:32-53) and gathers through L1 with 32-bit
 // per-axis offsets and immediate-offset loads for the x3 run. The summation
@@ -22,11 +23,19 @@
 namespace vr {
 namespace {
 
-constexpr int kTileThreads = 256;
-constexpr int kThreads = 256;  // pointwise kernels
-#ifndef VR_SL_MINB
-#define VR_SL_MINB 3  // min resident CTAs/SM for the gather kernels (80-register cap)
+#ifndef VR_TILE_T2
+#define VR_TILE_T2 4  // x2 rows per CTA tile (x3 run of 32 per warp)
 #endif
+#ifndef VR_TILE_T1
+#define VR_TILE_T1 1  // x1 planes per CTA tile (1 x 4 x 32, 128 threads: measured best)
+#endif
+constexpr int kBigT1 = VR_TILE_T1, kBigT2 = VR_TILE_T2;
+constexpr int kTileThreads = 32 * kBigT1 * kBigT2;
+constexpr int kThreads = 256;  // pointwise kernels
+#ifndef VR_SL_WARPS
+#define VR_SL_WARPS 28  // resident warps/SM targeted by the gather kernels (72-register cap)
+#endif
+#define VR_SL_MINB (VR_SL_WARPS * 32 / kTileThreads)
 
 // cubic_weights (interp.hpp:12-18)
 __device__ __forceinline__ void cubic_weights(double s, double* w) {
@@ -134,7 +143,7 @@ __device__ __forceinline__ double gather(const double* __restrict__ f, const Gri
     return acc;
 }
 
-// Tile geometry. BIG: the 2 x 4 x 32 tile (grids with n3 >= 32, n2 >= 4, n1 >= 2);
+// Tile geometry. BIG: the T1 x T2 x 32 tile (grids with n3 >= 32, n2 >= T2, L >= T1);
 // otherwise a runtime tile that fits small test grids.
 struct Tile {
     int t1, t2, t3;
@@ -145,10 +154,10 @@ __device__ __forceinline__ bool tile_point(const GridDims& g, const Tile& t, int
     const int tid = threadIdx.x;
     int l1, l2, l3, T1, T2, T3;
     if (BIG) {
-        T1 = 2, T2 = 4, T3 = 32;
+        T1 = kBigT1, T2 = kBigT2, T3 = 32;
         l3 = tid & 31;
-        l2 = (tid >> 5) & 3;
-        l1 = tid >> 7;
+        l2 = (tid >> 5) % kBigT2;
+        l1 = (tid >> 5) / kBigT2;
     } else {
         T1 = t.t1, T2 = t.t2, T3 = t.t3;
         l3 = tid % T3;
@@ -173,7 +182,7 @@ __device__ __forceinline__ void load_point(const double* __restrict__ dep, long 
 // ---------------------------------------------------------------------------
 // tricubic_interpolate{,2,3} (interp.hpp:80-126)
 template <int NF, bool BIG>
-__global__ void __launch_bounds__(kTileThreads, NF == 1 ? 3 : 2)
+__global__ void __launch_bounds__(kTileThreads, NF == 1 ? VR_SL_MINB : VR_SL_MINB * 2 / 3)
     k_tricubic(const double* __restrict__ f, const double* __restrict__ pts, double* __restrict__ out,
                GridDims g, Tile t) {
     int i1, i2, i3;
@@ -190,7 +199,7 @@ __global__ void __launch_bounds__(kTileThreads, NF == 1 ? 3 : 2)
 // trace_characteristics (transport.cpp:11-42): midpoint from v at the grid
 // point, one 3-field gather of v there, wrapped departure point.
 template <bool BIG>
-__global__ void __launch_bounds__(kTileThreads, 2)
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
     k_trace(const double* __restrict__ v, long long vs, double* __restrict__ dep, GridDims g,
             Tile t, double sign, double dt) {
     // v: component c at v + c*vs (vs = N, or the padded stride on x1 slabs)
@@ -269,7 +278,8 @@ template <int MODE, bool BIG>
 __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     k_incstate_step(const double* __restrict__ src, const double* __restrict__ dep,
                     const double* __restrict__ gm, const double* __restrict__ vt,
-                    double* __restrict__ dst, GridDims g, Tile t, double hdt) {
+                    double* __restrict__ dst, GridDims g, Tile t, double hdt,
+                    double* __restrict__ b, double wb) {
     int i1, i2, i3;
     long long i;
     if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
@@ -279,16 +289,23 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     Stencil st;
     make_stencil(g, x1, x2, x3, i1, st);
     const double m = gather(src, g, st) + (-hdt) * q;
-    dst[i] = (MODE == 0) ? 1.0 * m + (-hdt) * q : -m;
+    const double r = (MODE == 0) ? 1.0 * m + (-hdt) * q : -m;
+    dst[i] = r;
+    if (MODE == 2) {  // b = 0 + (w lam_nt) grad m_nt (objective.cpp:143-148 at j = nt)
+        const double wl = wb * r;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) __stcs(b + a * g.N + i, 0.0 + wl * __ldcs(gm + a * g.N + i));
+    }
 }
 
-// continuity step + optional fused accumulation b_a += (w * lam) * d_a m_j
+// continuity step + optional fused accumulation bout_a = (b_a + (w * lam) * d_a m_j) [+ add_a]
+// (streaming loads / stores for b, gm, add keep L1 for the gather)
 template <bool ACC, bool BIG>
 __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     k_adjoint_step(const double* __restrict__ src, const double* __restrict__ dep,
                    const double* __restrict__ factor, double* __restrict__ dst,
-                   const double* __restrict__ gm, double w, double* __restrict__ b, GridDims g,
-                   Tile t) {
+                   const double* __restrict__ gm, double w, const double* b,
+                   const double* __restrict__ add, double* bout, GridDims g, Tile t) {
     int i1, i2, i3;
     long long i;
     if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
@@ -302,7 +319,11 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     if (ACC) {
         const double wl = w * lam;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) b[a * g.N + i] = b[a * g.N + i] + wl * gm[a * g.N + i];
+        for (int a = 0; a < 3; ++a) {
+            double v = __ldcs(b + a * g.N + i) + wl * __ldcs(gm + a * g.N + i);
+            if (add) v = v + __ldcs(add + a * g.N + i);
+            __stcs(bout + a * g.N + i, v);
+        }
     }
 }
 
@@ -370,11 +391,11 @@ __global__ void __launch_bounds__(kThreads)
 
 unsigned pgrid(const GridDims& g) { return grid_1d(g.N, kThreads); }
 
-bool is_big(const GridDims& g) { return g.n3 >= 32 && g.n2 >= 4 && g.L >= 2; }
+bool is_big(const GridDims& g) { return g.n3 >= 32 && g.n2 >= kBigT2 && g.L >= kBigT1; }
 Tile tile_of(const GridDims& g) {
     Tile t;
     if (is_big(g)) {
-        t.t1 = 2, t.t2 = 4, t.t3 = 32;
+        t.t1 = kBigT1, t.t2 = kBigT2, t.t3 = 32;
         return t;
     }
     t.t3 = g.n3 < 32 ? g.n3 : 32;
@@ -409,6 +430,7 @@ unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.
 #define K_CONTINUITY(B) k_advect<true, B>
 #define K_INCSTATE0(B) k_incstate_step<0, B>
 #define K_INCSTATE1(B) k_incstate_step<1, B>
+#define K_INCSTATE2(B) k_incstate_step<2, B>
 #define K_ADJ(B) k_adjoint_step<false, B>
 #define K_ADJ_ACC(B) k_adjoint_step<true, B>
 
@@ -462,23 +484,28 @@ void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double
 }
 
 void sl_incstate_step(vr_ctx* ctx, const double* src, const double* dep3, const double* gm,
-                      const double* vt3, double hdt, double* dst, int mode) {
+                      const double* vt3, double hdt, double* dst, int mode, double* b3, double wb) {
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);
     if (mode == 0)
-        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE0, src, dep3, gm, vt3, dst, g, t, hdt);
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE0, src, dep3, gm, vt3, dst, g, t, hdt, nullptr, 0.0);
+    else if (mode == 1)
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE1, src, dep3, gm, vt3, dst, g, t, hdt, nullptr, 0.0);
     else
-        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE1, src, dep3, gm, vt3, dst, g, t, hdt);
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE2, src, dep3, gm, vt3, dst, g, t, hdt, b3, wb);
 }
 
 void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const double* factor,
-                     double* dst, const double* gm, double w, double* b3) {
+                     double* dst, const double* gm, double w, double* b3, const double* add3,
+                     double* bout3) {
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);
     if (b3)
-        VR_TILE_LAUNCH(ctx, "sl_adjoint_step_acc", K_ADJ_ACC, src, dep3, factor, dst, gm, w, b3, g, t);
+        VR_TILE_LAUNCH(ctx, "sl_adjoint_step_acc", K_ADJ_ACC, src, dep3, factor, dst, gm, w, b3, add3,
+                       bout3 ? bout3 : b3, g, t);
     else
-        VR_TILE_LAUNCH(ctx, "sl_adjoint_step", K_ADJ, src, dep3, factor, dst, nullptr, 0.0, nullptr, g, t);
+        VR_TILE_LAUNCH(ctx, "sl_adjoint_step", K_ADJ, src, dep3, factor, dst, nullptr, 0.0, nullptr,
+                       nullptr, nullptr, g, t);
 }
 
 void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const double* gm,

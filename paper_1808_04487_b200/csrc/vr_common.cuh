@@ -134,6 +134,11 @@ struct vr_ctx {
     // Off by default: the FFT kernels' shared memory shrinks the L1 that the
     // concurrent gather kernels live on (measured 7.7 vs 6.9 ms per matvec).
     bool overlap = false;
+    // GN matvec: accumulate b inside the adjoint steps (HBM slack of the
+    // L1-bound gathers) instead of a separate pass over all lam_j (VR_FUSE_ACC)
+    // (measured slower at 256^3: 0.90 vs 0.63 + 0.11 ms per step, the extra
+    // streams compete with the gather for the LSU; off by default)
+    bool fuse_acc = false;
     struct ProfRec {
         const char* cat;
         cudaEvent_t start, stop;
@@ -300,14 +305,18 @@ void sl_advect(vr_ctx* ctx, const double* f, const double* dep3, double* out);
 void sl_continuity(vr_ctx* ctx, const double* f, const double* dep3, const double* factor,
                    double* out);
 // incremental state fused step: g = I[src](X); m = g - hdt*q(gm, vt);
-// mode 0: dst = m - hdt*q (next tmp); mode 1: dst = -m (terminal)
+// mode 0: dst = m - hdt*q (next tmp); mode 1: dst = -m (terminal);
+// mode 2: mode 1 and b3 = 0 + (wb * dst) * gm (first observer of the adjoint sweep)
 void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double hdt,
                        double* tmp0);
 void sl_incstate_step(vr_ctx* ctx, const double* src, const double* dep3, const double* gm,
-                      const double* vt3, double hdt, double* dst, int mode);
-// adjoint step with optional gradient accumulation b_a += (w*lam) * gm_a
+                      const double* vt3, double hdt, double* dst, int mode, double* b3 = nullptr,
+                      double wb = 0.0);
+// adjoint step with optional gradient accumulation bout_a = (b_a + (w*lam) * gm_a) [+ add_a]
+// (bout defaults to b3)
 void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const double* factor,
-                     double* dst, const double* gm, double w, double* b3);
+                     double* dst, const double* gm, double w, double* b3,
+                     const double* add3 = nullptr, double* bout3 = nullptr);
 void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const double* gm,
                       double w, double* lam, double* b3);
 // b_a = sum_{j=nt..0} (w_j lam_j) d_a m_j  (+ add_a when add3 is given)
