@@ -339,8 +339,18 @@ def main():
         c, t = prof[dom]
         avg_s = t / c / 1e3
         ach = per_launch[dom] / avg_s / 1e9
+        traffic = None
+        try:  # ncu-measured DRAM bytes per launch of this kernel (profiles/ncu_traffic.json)
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(dom)
+            if traffic is not None:
+                traffic = traffic * share
+        except Exception:
+            traffic = None
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": None, "peak_source": peak_kind,
+                "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
+                "limiter": "L1/LSU wavefronts of the 64-node fp64 gathers (ncu: L1/TEX 85 %, DRAM 29 %)"
+                           if dom.startswith("sl_") and "step" in dom else None,
                 "bytes_per_launch": per_launch[dom], "avg_launch_ms": t / c}
     matvec_roof = {"bytes_per_matvec": per_matvec_bytes,
                    "achieved_GBps": per_matvec_bytes / (ms_per_step / 1e3) / 1e9,
