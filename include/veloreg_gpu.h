@@ -82,8 +82,20 @@ enum {
     VR_STOP_MAX_ITERATIONS = 3,
     VR_STOP_LINE_SEARCH_FAILURE = 4
 };
-/* Krylov preconditioner choice (solver.hpp:130-150) */
-enum { VR_PRECOND_NONE = 0, VR_PRECOND_SPECTRAL = 1 };
+/* Krylov preconditioner choice (solver.hpp:130-150, precond.hpp:93-110) */
+enum { VR_PRECOND_NONE = 0, VR_PRECOND_SPECTRAL = 1, VR_PRECOND_TWO_LEVEL = 2 };
+
+/* TwoLevelOptions (precond.hpp:46-53; defaults: PCG(0.1) inner, CHEB(10), 500 inner
+ * iterations, 10 Lanczos steps, seed 1234) */
+enum { VR_INNER_PCG = 0, VR_INNER_CHEB = 1 };
+typedef struct {
+    int inner;
+    double kappa;
+    int cheb_iterations;
+    int max_inner_iterations;
+    int lanczos_iterations;
+    unsigned long long lanczos_seed;
+} vr_twolevel_options;
 
 /* RegNorm, spectral.hpp:75-102 (defaults: H2, gamma 1, squared, no penalty, beta_w 1e-4) */
 typedef struct {
@@ -164,6 +176,7 @@ typedef struct {
 } vr_pcg_stats;
 
 void vr_model_default(vr_model* m);
+void vr_twolevel_options_default(vr_twolevel_options* o);
 void vr_solver_params_default(vr_solver_params* p);
 /* RegModel::validate / RegNorm::validate / SolverParams::validate */
 int vr_model_validate(const vr_model* m);
@@ -313,6 +326,37 @@ int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T,
                               const vr_model* model, const vr_solver_params* params, int precond,
                               double* v_out, vr_solve_report* reports, int max_levels,
                               int* n_levels, vr_iteration_record* records, int max_records);
+
+/* ---- two-level preconditioner and grid transfer (one GPU) ---- */
+/* spectral_resample (spectral.cpp:340-356): field on src's grid -> dst's grid (coarser or
+ * finer on every axis, same device); ncomp 1 or 3 */
+int vr_spectral_resample(vr_ctx* src, const double* in, int ncomp, vr_ctx* dst, double* out);
+/* frequency_filter (spectral.cpp:358-385): band 0 = low (F_L), 1 = high (F_H) w.r.t. cutoff */
+int vr_frequency_filter(vr_ctx* ctx, const double* in, int ncomp, int band, const int cutoff[3],
+                        double* out);
+/* Objective::split_matvec (objective.cpp:158-176): (I + R H_data R) w, R = (beta_v A)^-1/2 */
+int vr_split_matvec(vr_objective* obj, const vr_state* state, const double* w3, double* out3);
+/* TwoLevelPreconditioner (precond.hpp:55-110): rebuild per outer iteration, apply = the
+ * approximate inverse of the split system; counters = the coarse SolveCounters */
+typedef struct vr_twolevel vr_twolevel;
+int vr_twolevel_create(const vr_twolevel_options* opts, vr_twolevel** out);
+int vr_twolevel_destroy(vr_twolevel* tl);
+int vr_twolevel_rebuild(vr_twolevel* tl, vr_objective* obj, const vr_state* state, double eps_H);
+int vr_twolevel_apply(vr_twolevel* tl, vr_ctx* ctx, const double* r3, double* z3);
+/* coarse split matvec on the coarse grid (dims via vr_twolevel_info) */
+int vr_twolevel_coarse_matvec(vr_twolevel* tl, const double* u3, double* out3);
+/* coarse dims[3], lanczos_runs, inner_diverged, eigenvalue bounds, coarse counters */
+int vr_twolevel_info(const vr_twolevel* tl, int dims[3], int* lanczos_runs, int* inner_diverged,
+                     double bounds[2], vr_counters* coarse);
+/* gauss_newton_solve with the two-level preconditioner (opts NULL = defaults): the
+ * outer PCG runs on the split system (solver.cpp:208-221); report->coarse and
+ * records[k].coarse_matvecs carry the coarse counters */
+int vr_gauss_newton_solve_two_level(vr_ctx* ctx, const double* m_R, const double* m_T,
+                                    const double* v0, const vr_model* model,
+                                    const vr_solver_params* params,
+                                    const vr_twolevel_options* opts, double* v_out,
+                                    vr_solve_report* report, vr_iteration_record* records,
+                                    int max_records);
 
 /* ---- x1-slab decomposition across GPUs (no reference counterpart:
  * the reference is single-process, the paper's CLAIRE used MPI pencils,

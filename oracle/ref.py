@@ -27,6 +27,7 @@ Counters = _gpu_lib_types.Counters
 SolveReport = _gpu_lib_types.SolveReport
 IterationRecord = _gpu_lib_types.IterationRecord
 PcgStats = _gpu_lib_types.PcgStats
+TwoLevelOptions = _gpu_lib_types.TwoLevelOptions
 
 _lib = None
 P, D, I = C.c_void_p, C.c_double, C.c_int
@@ -78,6 +79,20 @@ _SIG = {
                                         P, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
                                         C.POINTER(IterationRecord), I]),
     "vref_generate_synthetic": (I, [DIMS, I, D, P, P, P]),
+    "vref_spectral_resample": (I, [DIMS, P, I, DIMS, P]),
+    "vref_frequency_filter": (I, [DIMS, P, I, I, DIMS, P]),
+    "vref_split_matvec": (I, [P, P, P, P]),
+    "vref_twolevel_create": (I, [C.POINTER(TwoLevelOptions), C.POINTER(P)]),
+    "vref_twolevel_destroy": (None, [P]),
+    "vref_twolevel_rebuild": (I, [P, P, P, D]),
+    "vref_twolevel_apply": (I, [P, P, P]),
+    "vref_twolevel_coarse_matvec": (I, [P, P, P]),
+    "vref_twolevel_info": (I, [P, DIMS, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(D),
+                               C.POINTER(Counters)]),
+    "vref_gauss_newton_solve_two_level": (I, [DIMS, P, P, P, C.POINTER(Model),
+                                              C.POINTER(SolverParams), C.POINTER(TwoLevelOptions),
+                                              P, C.POINTER(SolveReport), C.POINTER(IterationRecord),
+                                              I]),
     "vref_random_smooth_scalar": (I, [DIMS, I, C.c_ulonglong, D, P]),
     "vref_random_smooth_vector": (I, [DIMS, I, C.c_ulonglong, D, P]),
     "vref_random_rough_scalar": (I, [DIMS, C.c_ulonglong, P]),
@@ -387,6 +402,12 @@ class Objective:
         _call("vref_objective_apply_K", self._h, u.ctypes.data, out.ctypes.data)
         return out
 
+    def split_matvec(self, s, w):
+        w = _a(w)
+        out = np.empty_like(w)
+        _call("vref_split_matvec", self._h, s._h, w.ctypes.data, out.ctypes.data)
+        return out
+
     def pcg_solve(self, s, rhs, rel_tol, max_iter, precond=1):
         rhs = _a(rhs)
         x = np.empty_like(rhs)
@@ -431,3 +452,75 @@ def parameter_continuation(m_R, m_T, v0, model, params, precond=1, max_levels=16
     reports = [_report(reps[i]) for i in range(min(nl.value, max_levels))]
     n = min(sum(x["n_records"] for x in reports), max_records)
     return vout, reports, [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
+
+
+# ---- two-level preconditioner / grid transfer (precond.hpp, spectral.hpp:131-153) ------
+def spectral_resample(f, shape):
+    f = _a(f)
+    nc = 3 if f.ndim == 4 else 1
+    out = np.empty(((3,) if nc == 3 else ()) + tuple(shape))
+    _call("vref_spectral_resample", _dims(f.shape), f.ctypes.data, nc, _dims(shape), out.ctypes.data)
+    return out
+
+
+def frequency_filter(f, band, cutoff):
+    f = _a(f)
+    nc = 3 if f.ndim == 4 else 1
+    out = np.empty_like(f)
+    b = {"low": 0, "high": 1}.get(band, band)
+    cut = (cutoff,) * 3 if isinstance(cutoff, int) else tuple(cutoff)
+    _call("vref_frequency_filter", _dims(f.shape), f.ctypes.data, nc, b, _dims(cut), out.ctypes.data)
+    return out
+
+
+class TwoLevelPreconditioner:
+    """TwoLevelPreconditioner<double> of the compiled reference (precond.hpp:93-110)."""
+
+    def __init__(self, options):
+        h = C.c_void_p()
+        _call("vref_twolevel_create", C.byref(options), C.byref(h))
+        self._h = h
+        self.shape = None
+
+    def rebuild(self, obj, state, eps_H):
+        self.shape = obj.shape
+        _call("vref_twolevel_rebuild", self._h, obj._h, state._h, eps_H)
+
+    def apply(self, r):
+        r = _a(r)
+        z = np.empty_like(r)
+        _call("vref_twolevel_apply", self._h, r.ctypes.data, z.ctypes.data)
+        return z
+
+    def coarse_matvec(self, u):
+        u = _a(u)
+        out = np.empty_like(u)
+        _call("vref_twolevel_coarse_matvec", self._h, u.ctypes.data, out.ctypes.data)
+        return out
+
+    def info(self):
+        dims = (C.c_int * 3)()
+        runs, div = C.c_int(), C.c_int()
+        b = (C.c_double * 2)()
+        c = Counters()
+        _call("vref_twolevel_info", self._h, dims, C.byref(runs), C.byref(div), b, C.byref(c))
+        return {"coarse_dims": tuple(dims), "lanczos_runs": runs.value,
+                "inner_diverged": bool(div.value), "bounds": (b[0], b[1]),
+                "coarse": {k: getattr(c, k) for k, _ in Counters._fields_}}
+
+    def __del__(self):
+        if _lib is not None and getattr(self, "_h", None):
+            _lib.vref_twolevel_destroy(self._h)
+            self._h = None
+
+
+def gauss_newton_solve_two_level(m_R, m_T, v0, model, params, options, max_records=512):
+    r, t, v0 = _a(m_R), _a(m_T), _a(v0)
+    vout = np.empty_like(v0)
+    rep = SolveReport()
+    recs = (IterationRecord * max_records)()
+    _call("vref_gauss_newton_solve_two_level", _dims(r.shape), r.ctypes.data, t.ctypes.data,
+          v0.ctypes.data, C.byref(model), C.byref(params), C.byref(options), vout.ctypes.data,
+          C.byref(rep), recs, max_records)
+    n = min(rep.n_records, max_records)
+    return vout, _report(rep), [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]

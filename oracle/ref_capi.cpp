@@ -20,6 +20,7 @@
 #include "veloreg/fft.hpp"
 #include "veloreg/objective.hpp"
 #include "veloreg/parallel.hpp"
+#include "veloreg/precond.hpp"
 #include "veloreg/solver.hpp"
 #include "veloreg/spectral.hpp"
 #include "veloreg/synthetic.hpp"
@@ -164,6 +165,22 @@ struct vref_objective {
 struct vref_state {
     EvalState<double> s;
 };
+struct vref_twolevel {
+    explicit vref_twolevel(const TwoLevelOptions& o) : pre(o) {}
+    TwoLevelPreconditioner<double> pre;
+    Grid3 fine;
+};
+static TwoLevelOptions to_tl(const vr_twolevel_options* o) {
+    TwoLevelOptions t;
+    if (!o) return t;
+    t.inner = o->inner == VR_INNER_CHEB ? TwoLevelOptions::Inner::cheb : TwoLevelOptions::Inner::pcg;
+    t.kappa = o->kappa;
+    t.cheb_iterations = o->cheb_iterations;
+    t.max_inner_iterations = o->max_inner_iterations;
+    t.lanczos_iterations = o->lanczos_iterations;
+    t.lanczos_seed = o->lanczos_seed;
+    return t;
+}
 
 extern "C" {
 
@@ -505,6 +522,81 @@ int vref_parameter_continuation(const int* d, const double* mR, const double* mT
             if (res.report.stop == StopReason::line_search_failure) break;
         }
         store(v, v_out);
+    });
+}
+
+// ---- two-level preconditioner / grid transfer (precond.hpp, spectral.hpp:131-153) ----
+int vref_spectral_resample(const int* ds, const double* in, int ncomp, const int* dd, double* out) {
+    return guard([&] {
+        Grid3 gs = grid_of(ds), gd = grid_of(dd);
+        if (ncomp == 3)
+            store(spectral_resample(load_vector(gs, in), gd), out);
+        else
+            store(spectral_resample(load_scalar(gs, in), gd), out);
+    });
+}
+int vref_frequency_filter(const int* d, const double* in, int ncomp, int band, const int* cutoff,
+                          double* out) {
+    return guard([&] {
+        Grid3 g = grid_of(d), c = grid_of(cutoff);
+        const FreqBand b = band == 0 ? FreqBand::low : FreqBand::high;
+        if (ncomp == 3)
+            store(frequency_filter(load_vector(g, in), b, c), out);
+        else
+            store(frequency_filter(load_scalar(g, in), b, c), out);
+    });
+}
+int vref_split_matvec(vref_objective* o, vref_state* s, const double* w3, double* out3) {
+    return guard([&] { store(o->obj->split_matvec(s->s, load_vector(o->g, w3)), out3); });
+}
+int vref_twolevel_create(const vr_twolevel_options* opts, vref_twolevel** out) {
+    return guard([&] { *out = new vref_twolevel(to_tl(opts)); });
+}
+void vref_twolevel_destroy(vref_twolevel* t) { delete t; }
+int vref_twolevel_rebuild(vref_twolevel* t, vref_objective* o, vref_state* s, double eps_H) {
+    return guard([&] {
+        t->fine = o->g;
+        t->pre.rebuild(*o->obj, s->s, eps_H);
+    });
+}
+int vref_twolevel_apply(vref_twolevel* t, const double* r3, double* z3) {
+    return guard([&] {
+        VectorField<double> z;
+        t->pre.apply(load_vector(t->fine, r3), z);
+        store(z, z3);
+    });
+}
+int vref_twolevel_coarse_matvec(vref_twolevel* t, const double* u3, double* out3) {
+    return guard([&] {
+        auto& c = t->pre.context();
+        store(c.coarse_matvec(load_vector(c.coarse_grid(), u3)), out3);
+    });
+}
+int vref_twolevel_info(vref_twolevel* t, int* dims, int* lanczos_runs, int* inner_diverged,
+                       double* bounds, vr_counters* coarse) {
+    return guard([&] {
+        auto& c = t->pre.context();
+        for (int a = 0; a < 3; ++a) dims[a] = c.ready() ? c.coarse_grid().dims[a] : 0;
+        *lanczos_runs = c.lanczos_runs();
+        *inner_diverged = c.inner_diverged();
+        bounds[0] = c.eig_bounds().first;
+        bounds[1] = c.eig_bounds().second;
+        fill_counters(*t->pre.coarse_counters(), coarse);
+    });
+}
+int vref_gauss_newton_solve_two_level(const int* d, const double* mR, const double* mT,
+                                      const double* v0, const vr_model* m,
+                                      const vr_solver_params* p, const vr_twolevel_options* opts,
+                                      double* v_out, vr_solve_report* rep,
+                                      vr_iteration_record* recs, int max_recs) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto R = load_scalar(g, mR), T = load_scalar(g, mT);
+        TwoLevelPreconditioner<double> pre(to_tl(opts));
+        auto res = gauss_newton_solve(R, T, load_vector(g, v0), to_model(*m), to_params(*p), pre,
+                                      pre.coarse_counters());
+        store(res.v, v_out);
+        fill_report(res.report, rep, recs, max_recs, 0);
     });
 }
 

@@ -106,6 +106,12 @@ class SolveReport(C.Structure):
                 ("n_records", C.c_int)]
 
 
+class TwoLevelOptions(C.Structure):
+    _fields_ = [("inner", C.c_int), ("kappa", C.c_double), ("cheb_iterations", C.c_int),
+                ("max_inner_iterations", C.c_int), ("lanczos_iterations", C.c_int),
+                ("lanczos_seed", C.c_ulonglong)]
+
+
 class PcgStats(C.Structure):
     _fields_ = [("iterations", C.c_int), ("rel_residual", C.c_double), ("converged", C.c_int),
                 ("negative_curvature", C.c_int), ("hit_max_iterations", C.c_int)]
@@ -116,7 +122,8 @@ REG_H1, REG_H2, REG_H3, REG_HELMHOLTZ = 0, 1, 2, 3
 REGOP_APPLY, REGOP_INVERSE, REGOP_INVERSE_SQRT = 0, 1, 2
 PROJ_IDENTITY, PROJ_INCOMPRESSIBLE, PROJ_NEAR_INCOMPRESSIBLE = 0, 1, 2
 TRACE_BACKWARD, TRACE_FORWARD = 0, 1
-PRECOND_NONE, PRECOND_SPECTRAL = 0, 1
+PRECOND_NONE, PRECOND_SPECTRAL, PRECOND_TWO_LEVEL = 0, 1, 2
+INNER_PCG, INNER_CHEB = 0, 1
 STOP_NAMES = ["zero_gradient", "converged_rel", "converged_abs", "max_iterations",
               "line_search_failure"]
 STATE_V, STATE_X_BWD, STATE_X_FWD, STATE_FACTOR, STATE_M_HISTORY, STATE_GRADIENT, STATE_GRAD_M = range(7)
@@ -205,6 +212,21 @@ SIGNATURES = {
                                       C.POINTER(SolverParams), I, DP, C.POINTER(SolveReport), I,
                                       C.POINTER(C.c_int), C.POINTER(IterationRecord), I]),
     "vr_generate_synthetic": (I, [P, I, D, DP, DP, DP]),
+    "vr_twolevel_options_default": (None, [C.POINTER(TwoLevelOptions)]),
+    "vr_spectral_resample": (I, [P, DP, I, P, DP]),
+    "vr_frequency_filter": (I, [P, DP, I, I, C.POINTER(C.c_int), DP]),
+    "vr_split_matvec": (I, [P, P, DP, DP]),
+    "vr_twolevel_create": (I, [C.POINTER(TwoLevelOptions), C.POINTER(P)]),
+    "vr_twolevel_destroy": (I, [P]),
+    "vr_twolevel_rebuild": (I, [P, P, P, D]),
+    "vr_twolevel_apply": (I, [P, P, DP, DP]),
+    "vr_twolevel_coarse_matvec": (I, [P, DP, DP]),
+    "vr_twolevel_info": (I, [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                             C.POINTER(D), C.POINTER(Counters)]),
+    "vr_gauss_newton_solve_two_level": (I, [P, DP, DP, DP, C.POINTER(Model),
+                                            C.POINTER(SolverParams), C.POINTER(TwoLevelOptions),
+                                            DP, C.POINTER(SolveReport),
+                                            C.POINTER(IterationRecord), I]),
     "vr_nccl_unique_id": (I, [C.c_char_p]),
     "vr_slab_layout": (I, [I, I, I, I, I, I, C.POINTER(C.c_longlong)]),
     "vr_slab_halo_required": (I, [C.c_double, I, I, C.POINTER(C.c_int)]),

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "objective.cuh"
+#include "twolevel.cuh"
 
 namespace {
 
@@ -90,6 +91,16 @@ double* field_buf(vr_ctx* ctx, int i) {
     return ctx->field_scratch[i];
 }
 
+vr_ctx* ctx_new_sibling(vr_ctx* parent, int n1, int n2, int n3) {
+    vr_ctx* c = ctx_new(n1, n2, n3, parent->device, nullptr, 0);
+    VR_CUDA(cudaStreamDestroy(c->stream));
+    c->stream = parent->stream;
+    c->owns_stream = false;
+    c->overlap = parent->overlap;
+    c->fuse_acc = parent->fuse_acc;
+    return c;
+}
+
 }  // namespace vr
 
 extern "C" {
@@ -108,6 +119,14 @@ void vr_model_default(vr_model* m) {
     m->beta_v = 1e-2;
     m->nt = 4;
     m->gauss_newton = 1;
+}
+void vr_twolevel_options_default(vr_twolevel_options* o) {
+    o->inner = VR_INNER_PCG;  // TwoLevelOptions (precond.hpp:46-53)
+    o->kappa = 0.1;
+    o->cheb_iterations = 10;
+    o->max_inner_iterations = 500;
+    o->lanczos_iterations = 10;
+    o->lanczos_seed = 1234;
 }
 void vr_solver_params_default(vr_solver_params* p) {
     p->eps_opt = 5e-2;
@@ -277,7 +296,7 @@ int vr_ctx_destroy(vr_ctx* ctx) {
         if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
         if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
         if (ctx->side) cudaStreamDestroy(ctx->side);
-        if (ctx->stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->stream && ctx->owns_stream) cudaStreamDestroy(ctx->stream);
         if (ctx->owns_dist) delete ctx->dist;
         delete ctx;
     });
@@ -938,6 +957,105 @@ int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T,
             throw;
         }
         vr::dev_free(ctx, v);
+    });
+}
+
+// ---- two-level preconditioner / grid transfer ----------------------------------
+struct vr_twolevel {
+    explicit vr_twolevel(const vr_twolevel_options& o) : tl(o) {}
+    vr::TwoLevel tl;
+};
+int vr_spectral_resample(vr_ctx* src, const double* in, int ncomp, vr_ctx* dst, double* out) {
+    return guard([&] {
+        set_dev(src);
+        need(dst && in && out, "vr_spectral_resample");
+        check_ncomp(ncomp);
+        for (int c = 0; c < ncomp; ++c)
+            vr::resample_scalar(src, in + c * src->g.N, dst, out + c * dst->g.N);
+    });
+}
+int vr_frequency_filter(vr_ctx* ctx, const double* in, int ncomp, int band, const int cutoff[3],
+                        double* out) {
+    return guard([&] {
+        set_dev(ctx);
+        need(in && out && cutoff, "vr_frequency_filter");
+        check_ncomp(ncomp);
+        if (band != 0 && band != 1) vr::throw_argument("frequency_filter: band must be 0 or 1");
+        for (int c = 0; c < ncomp; ++c)
+            vr::frequency_filter(ctx, in + c * ctx->g.N, band, cutoff, out + c * ctx->g.N);
+    });
+}
+int vr_split_matvec(vr_objective* obj, const vr_state* state, const double* w3, double* out3) {
+    return guard([&] {
+        need(obj && state && w3 && out3, "vr_split_matvec");
+        set_dev(obj->ctx);
+        if (!state->has_adjoint_ctx)
+            vr::throw_logic("split_matvec: evaluation context is missing the adjoint sweep data "
+                            "(compute the gradient first)");
+        vr::split_matvec(obj, state, w3, out3);
+    });
+}
+int vr_twolevel_create(const vr_twolevel_options* opts, vr_twolevel** out) {
+    return guard([&] {
+        need(out != nullptr, "vr_twolevel_create");
+        vr_twolevel_options d;
+        vr_twolevel_options_default(&d);
+        *out = new vr_twolevel(opts ? *opts : d);
+    });
+}
+int vr_twolevel_destroy(vr_twolevel* tl) {
+    return guard([&] { delete tl; });
+}
+int vr_twolevel_rebuild(vr_twolevel* tl, vr_objective* obj, const vr_state* state, double eps_H) {
+    return guard([&] {
+        need(tl && obj && state, "vr_twolevel_rebuild");
+        set_dev(obj->ctx);
+        tl->tl.rebuild(obj, state, eps_H);
+    });
+}
+int vr_twolevel_apply(vr_twolevel* tl, vr_ctx* ctx, const double* r3, double* z3) {
+    return guard([&] {
+        need(tl && r3 && z3, "vr_twolevel_apply");
+        set_dev(ctx);
+        tl->tl.apply(ctx, r3, z3);
+    });
+}
+int vr_twolevel_coarse_matvec(vr_twolevel* tl, const double* u3, double* out3) {
+    return guard([&] {
+        need(tl && u3 && out3, "vr_twolevel_coarse_matvec");
+        tl->tl.coarse_matvec(u3, out3);
+    });
+}
+int vr_twolevel_info(const vr_twolevel* tl, int dims[3], int* lanczos_runs, int* inner_diverged,
+                     double bounds[2], vr_counters* coarse) {
+    return guard([&] {
+        need(tl != nullptr, "vr_twolevel_info");
+        const vr::TwoLevel& t = tl->tl;
+        if (dims) {
+            dims[0] = t.cctx ? t.cctx->g.n1 : 0;
+            dims[1] = t.cctx ? t.cctx->g.n2 : 0;
+            dims[2] = t.cctx ? t.cctx->g.n3 : 0;
+        }
+        if (lanczos_runs) *lanczos_runs = t.lanczos_runs;
+        if (inner_diverged) *inner_diverged = t.inner_diverged;
+        if (bounds) bounds[0] = t.bounds.first, bounds[1] = t.bounds.second;
+        if (coarse) *coarse = t.counters();
+    });
+}
+int vr_gauss_newton_solve_two_level(vr_ctx* ctx, const double* m_R, const double* m_T,
+                                    const double* v0, const vr_model* model,
+                                    const vr_solver_params* params,
+                                    const vr_twolevel_options* opts, double* v_out,
+                                    vr_solve_report* report, vr_iteration_record* records,
+                                    int max_records) {
+    return guard([&] {
+        set_dev(ctx);
+        need(m_R && m_T && v0 && model && params && v_out && report,
+             "vr_gauss_newton_solve_two_level");
+        vr::GnResult r = vr::gauss_newton_solve(ctx, m_R, m_T, v0, *model, *params,
+                                                VR_PRECOND_TWO_LEVEL, v_out, opts);
+        *report = r.report;
+        copy_records(r, records, max_records, 0);
     });
 }
 

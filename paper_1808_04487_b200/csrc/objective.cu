@@ -9,7 +9,10 @@
 #include <cmath>
 #include <string>
 
+#include <memory>
+
 #include "objective.cuh"
+#include "twolevel.cuh"
 
 vr_state::~vr_state() {
     vr_ctx* ctx = obj ? obj->ctx : nullptr;
@@ -244,6 +247,35 @@ static void prepare_adjoint_ctx(vr_objective* o, vr_state* s) {
     for (int j = 0; j <= nt; ++j)
         op_gradient(ctx, pslice(ctx, s->mhist, j), s->gradm + 3LL * j * N);
     s->has_adjoint_ctx = true;
+}
+
+// An evaluation context assembled from given v and m history (the coarse
+// state of TwoLevelContext::rebuild, precond.cpp:177-196): backward
+// characteristics traced here, the adjoint context (X_fwd, factor, grad m
+// cache) built as for a gradient. One GPU.
+vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt) {
+    vr_ctx* ctx = o->ctx;
+    if (ctx->dist) throw_argument("state_from_history: one GPU only");
+    const long long N = ctx->g.N;
+    auto* s = new vr_state();
+    s->obj = o;
+    s->nt = nt;
+    try {
+        s->v = dev_alloc(ctx, 3 * N);
+        s->xb = dev_alloc(ctx, 3 * N);
+        s->mhist = dev_alloc(ctx, (nt + 1) * ctx->hstride);
+        VR_CUDA(cudaMemcpyAsync(s->v, v3, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        for (int j = 0; j <= nt; ++j)
+            VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->mhist, j), mhist + j * N, sizeof(double) * N,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+        sl_trace(ctx, s->v, N, nt, VR_TRACE_BACKWARD, s->xb);
+        prepare_adjoint_ctx(o, s);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    return s;
 }
 
 void objective_gradient(vr_objective* o, vr_state* s) {
@@ -575,7 +607,8 @@ LineSearch armijo_search(vr_objective* o, const vr_state* cur, const double* dir
 }
 
 vr_iteration_record make_record(int k, const vr_state* s, double gn, double g0,
-                                const vr_counters& fine, double elapsed) {
+                                const vr_counters& fine, const vr_counters& coarse,
+                                double elapsed) {
     vr_iteration_record r{};
     r.k = k;
     r.objective = s->objective;
@@ -583,7 +616,7 @@ vr_iteration_record make_record(int k, const vr_state* s, double gn, double g0,
     r.grad_norm = gn;
     r.grad_rel = g0 > 0 ? gn / g0 : 0.0;
     r.fine_matvecs = fine.hessian_matvecs;
-    r.coarse_matvecs = 0;
+    r.coarse_matvecs = coarse.hessian_matvecs;
     r.pde_solves = fine.pde_solves;
     r.wall_time_s = elapsed;
     return r;
@@ -593,8 +626,18 @@ vr_iteration_record make_record(int k, const vr_state* s, double gn, double g0,
 
 GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, const double* v0,
                             const vr_model& model, const vr_solver_params& params, int precond,
-                            double* v_out) {
+                            double* v_out, const vr_twolevel_options* tl_opts) {
     validate_params(params);
+    if (precond != VR_PRECOND_NONE && precond != VR_PRECOND_SPECTRAL &&
+        precond != VR_PRECOND_TWO_LEVEL)
+        throw_argument("gauss_newton_solve: unknown preconditioner");
+    std::unique_ptr<TwoLevel> tl;
+    if (precond == VR_PRECOND_TWO_LEVEL) {
+        vr_twolevel_options d;
+        vr_twolevel_options_default(&d);
+        tl.reset(new TwoLevel(tl_opts ? *tl_opts : d));
+    }
+    auto coarse = [&] { return tl ? tl->counters() : vr_counters{}; };
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] {
         return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -618,7 +661,7 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
         objective_gradient(obj, state);
         const double g0 = norm_l2_vec(ctx, state->grad);
         rep.grad0 = g0;
-        res.records.push_back(make_record(0, state, g0, g0, obj->counters, elapsed()));
+        res.records.push_back(make_record(0, state, g0, g0, obj->counters, coarse(), elapsed()));
         if (g0 == 0.0) {
             rep.stop = VR_STOP_ZERO_GRADIENT;
             rep.success = 1;
@@ -656,12 +699,23 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                         VR_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * n3,
                                                 cudaMemcpyDeviceToDevice, ctx->stream));
                 };
-                // rhs = -g (scale(rhs, -1.0))
-                lin_comb(ctx, rhs, -1.0, state->grad, 0.0, state->grad, n3);
-                vr_pcg_stats pcg =
-                    precond == VR_PRECOND_SPECTRAL
-                        ? pcg_solve_gn(obj, state, rhs, eps_H, params.max_krylov, dir)
-                        : pcg_solve(ctx, op, rhs, eps_H, params.max_krylov, pc, dir);
+                vr_pcg_stats pcg;
+                if (tl) {
+                    // split system (solver.cpp:208-221): (I + R H_data R) w = -R g, v~ = R w
+                    tl->rebuild(obj, state, eps_H);
+                    DevOp sop = [&](const double* w, double* out) { split_matvec(obj, cs, w, out); };
+                    DevOp spc = [&](const double* r, double* z) { tl->apply(ctx, r, z); };
+                    objective_apply_reg(obj, state->grad, VR_REGOP_INVERSE_SQRT, rhs);
+                    scale(ctx, rhs, n3, -1.0);
+                    pcg = pcg_solve(ctx, sop, rhs, eps_H, params.max_krylov, spc, dir);
+                    objective_apply_reg(obj, dir, VR_REGOP_INVERSE_SQRT, dir);
+                } else {
+                    // rhs = -g (scale(rhs, -1.0))
+                    lin_comb(ctx, rhs, -1.0, state->grad, 0.0, state->grad, n3);
+                    pcg = precond == VR_PRECOND_SPECTRAL
+                              ? pcg_solve_gn(obj, state, rhs, eps_H, params.max_krylov, dir)
+                              : pcg_solve(ctx, op, rhs, eps_H, params.max_krylov, pc, dir);
+                }
 
                 const double slope = inner_product_vec(ctx, state->grad, dir);
                 if (slope >= 0.0) {
@@ -678,7 +732,8 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                 objective_gradient(obj, state);
                 gk = norm_l2_vec(ctx, state->grad);
                 ++k;
-                vr_iteration_record row = make_record(k, state, gk, g0, obj->counters, elapsed());
+                vr_iteration_record row =
+                    make_record(k, state, gk, g0, obj->counters, coarse(), elapsed());
                 row.step_length = ls.alpha;
                 row.forcing = eps_H;
                 row.inner_iterations = pcg.iterations;
@@ -691,6 +746,7 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
         const double gfin = norm_l2_vec(ctx, state->grad);
         rep.final_grad_rel = g0 > 0 ? gfin / g0 : 0.0;
         rep.fine = obj->counters;
+        rep.coarse = coarse();
         rep.n_records = static_cast<int>(res.records.size());
         VR_CUDA(cudaMemcpyAsync(v_out, state->v, sizeof(double) * n3, cudaMemcpyDeviceToDevice,
                                 ctx->stream));

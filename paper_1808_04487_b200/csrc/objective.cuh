@@ -85,6 +85,8 @@ struct GnResult {
 };
 GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, const double* v0,
                             const vr_model& model, const vr_solver_params& params, int precond,
-                            double* v_out);
+                            double* v_out, const vr_twolevel_options* tl_opts = nullptr);
+// evaluation context from given v and m history (coarse state of the two-level preconditioner)
+vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt);
 
 }  // namespace vr

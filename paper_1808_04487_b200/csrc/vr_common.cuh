@@ -111,6 +111,7 @@ struct vr_ctx {
     int device = 0;
     int sms = 0;                     // streaming multiprocessors of `device` (persistent grids)
     cudaStream_t stream = nullptr;   // all public calls are ordered on this stream
+    bool owns_stream = true;         // false for siblings running on a parent's stream
     cudaStream_t side = nullptr;     // internal: overlaps independent spectral work
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     vr::GridDims g{};
@@ -156,6 +157,8 @@ constexpr int kRedThreads = 256;
 // create a context for grid (n1, n2, n3) on `device`; with a transport of size
 // P > 1 it owns that rank's x1 slab with `halo` planes (capi.cu)
 vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo);
+// a one-GPU context of another grid on parent's device that runs on parent's stream
+vr_ctx* ctx_new_sibling(vr_ctx* parent, int n1, int n2, int n3);
 void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& g);
 int halo_required(double vmax_x1, int nt, int n1);
 void set_last_error(int cls, const std::string& msg);  // the C ABI's vr_last_error slot

@@ -479,6 +479,13 @@ class Objective:
         _lib.call("vr_hessian_matvec", self._h, state._h, dv.ptr, o.ptr)
         return _ret(o, _is_host(v_tilde) and out is None)
 
+    def split_matvec(self, state: EvalState, w):
+        """Objective::split_matvec (objective.cpp:158-176): (I + R H_data R) w, R = (beta_v A)^-1/2."""
+        dw = _dev(self.ctx, w)
+        o = self.ctx.empty(3)
+        _lib.call("vr_split_matvec", self._h, state._h, dw.ptr, o.ptr)
+        return _ret(o, _is_host(w))
+
     def hessian_data_matvec(self, state: EvalState, v_tilde):
         dv = _dev(self.ctx, v_tilde)
         o = self.ctx.empty(3)
@@ -553,19 +560,124 @@ def _records(recs, n) -> List[dict]:
     return [{k: getattr(recs[i], k) for k, _ in _lib.IterationRecord._fields_} for i in range(n)]
 
 
+_PRECOND = {"none": _lib.PRECOND_NONE, "spectral": _lib.PRECOND_SPECTRAL,
+            "two_level": _lib.PRECOND_TWO_LEVEL}
+
+
 def gauss_newton_solve(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral",
-                       max_records=512):
-    """gauss_newton_solve (solver.hpp:159-164) with the C++ host driver."""
+                       max_records=512, twolevel=None):
+    """gauss_newton_solve (solver.hpp:159-164) with the C++ host driver. precond:
+    "spectral" (SpectralPreconditioner), "none", or "two_level" (TwoLevelPreconditioner,
+    options from make_twolevel_options / `twolevel`)."""
     model = model if model is not None else make_model()
     params = params if params is not None else make_params()
     dR, dT, dv0 = _dev(ctx, m_R), _dev(ctx, m_T), _dev(ctx, v0)
     vout = ctx.empty(3)
     rep = _lib.SolveReport()
     recs = (_lib.IterationRecord * max_records)()
-    pc = _lib.PRECOND_SPECTRAL if precond == "spectral" else _lib.PRECOND_NONE
-    _lib.call("vr_gauss_newton_solve", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
-              C.byref(params), pc, vout.ptr, C.byref(rep), recs, max_records)
+    pc = _enum(_PRECOND, precond)
+    if pc == _lib.PRECOND_TWO_LEVEL:
+        opts = twolevel if twolevel is not None else make_twolevel_options()
+        _lib.call("vr_gauss_newton_solve_two_level", ctx.handle, dR.ptr, dT.ptr, dv0.ptr,
+                  C.byref(model), C.byref(params), C.byref(opts), vout.ptr, C.byref(rep), recs,
+                  max_records)
+    else:
+        _lib.call("vr_gauss_newton_solve", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
+                  C.byref(params), pc, vout.ptr, C.byref(rep), recs, max_records)
     return SolveResult(vout.numpy(), _report_dict(rep), _records(recs, min(rep.n_records, max_records)))
+
+
+# ---- two-level preconditioner and grid transfer (precond.hpp, spectral.cpp:228-385) ----
+def make_twolevel_options(**kw):
+    """TwoLevelOptions (precond.hpp:46-53) with keyword overrides; inner "pcg" or "cheb"."""
+    o = _lib.TwoLevelOptions()
+    _lib.load().vr_twolevel_options_default(C.byref(o))
+    for k, v in kw.items():
+        if k == "inner":
+            v = {"pcg": _lib.INNER_PCG, "cheb": _lib.INNER_CHEB}.get(v, v)
+        if not hasattr(o, k):
+            raise ArgumentError(f"TwoLevelOptions has no field {k}")
+        setattr(o, k, v)
+    return o
+
+
+def spectral_resample(src: Context, f, dst: Context):
+    """spectral_resample (spectral.cpp:340-356): field on src's grid -> dst's grid."""
+    df = _dev(src, f)
+    nc = df.nfields
+    out = dst.empty(nc)
+    _lib.call("vr_spectral_resample", src.handle, df.ptr, nc, dst.handle, out.ptr)
+    return _ret(out, _is_host(f))
+
+
+def frequency_filter(ctx: Context, f, band, cutoff):
+    """frequency_filter (spectral.cpp:358-385): band "low" (F_L) or "high" (F_H)."""
+    df = _dev(ctx, f)
+    out = ctx.empty(df.nfields)
+    cut = (C.c_int * 3)(*((cutoff,) * 3 if isinstance(cutoff, int) else cutoff))
+    b = {"low": 0, "high": 1}.get(band, band)
+    _lib.call("vr_frequency_filter", ctx.handle, df.ptr, df.nfields, b, cut, out.ptr)
+    return _ret(out, _is_host(f))
+
+
+class TwoLevelPreconditioner:
+    """TwoLevelPreconditioner / TwoLevelContext (precond.hpp:55-110) on the device."""
+
+    def __init__(self, options=None, **kw):
+        self.options = options if options is not None else make_twolevel_options(**kw)
+        h = C.c_void_p()
+        _lib.call("vr_twolevel_create", C.byref(self.options), C.byref(h))
+        self._h = h
+        self.fine = None
+
+    def rebuild(self, obj: Objective, state: EvalState, eps_H: float):
+        self.fine = obj.ctx
+        _lib.call("vr_twolevel_rebuild", self._h, obj.handle, state._h, eps_H)
+
+    def apply(self, r):
+        dr = _dev(self.fine, r)
+        z = self.fine.empty(3)
+        _lib.call("vr_twolevel_apply", self._h, self.fine.handle, dr.ptr, z.ptr)
+        return _ret(z, _is_host(r))
+
+    def info(self) -> dict:
+        dims = (C.c_int * 3)()
+        runs, div = C.c_int(), C.c_int()
+        b = (C.c_double * 2)()
+        c = _lib.Counters()
+        _lib.call("vr_twolevel_info", self._h, dims, C.byref(runs), C.byref(div), b, C.byref(c))
+        return {"coarse_dims": tuple(dims), "lanczos_runs": runs.value,
+                "inner_diverged": bool(div.value), "bounds": (b[0], b[1]),
+                "coarse": {k: getattr(c, k) for k, _ in _lib.Counters._fields_}}
+
+    def coarse_matvec(self, u: np.ndarray) -> np.ndarray:
+        """Split-form GN matvec on the coarse grid (host arrays of the coarse shape)."""
+        dims = self.info()["coarse_dims"]
+        u = np.ascontiguousarray(u, dtype=np.float64).reshape((3,) + dims)
+        nb = 8 * u.size
+        ptr, out = C.c_void_p(), C.c_void_p()
+        _lib.call("vr_device_alloc", self.fine.handle, nb, C.byref(ptr))
+        _lib.call("vr_device_alloc", self.fine.handle, nb, C.byref(out))
+        try:
+            _lib.call("vr_memcpy_h2d", self.fine.handle, ptr, u.ctypes.data, nb)
+            _lib.call("vr_twolevel_coarse_matvec", self._h, ptr, out)
+            res = np.empty((3,) + dims)
+            _lib.call("vr_memcpy_d2h", self.fine.handle, res.ctypes.data, out, nb)
+        finally:
+            _lib.call("vr_device_free", self.fine.handle, ptr)
+            _lib.call("vr_device_free", self.fine.handle, out)
+        return res
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.call("vr_twolevel_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def parameter_continuation(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral",
@@ -578,7 +690,7 @@ def parameter_continuation(ctx, m_R, m_T, v0, model=None, params=None, precond="
     reps = (_lib.SolveReport * max_levels)()
     recs = (_lib.IterationRecord * max_records)()
     nl = C.c_int()
-    pc = _lib.PRECOND_SPECTRAL if precond == "spectral" else _lib.PRECOND_NONE
+    pc = _enum(_PRECOND, precond)
     _lib.call("vr_parameter_continuation", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
               C.byref(params), pc, vout.ptr, reps, max_levels, C.byref(nl), recs, max_records)
     reports = [_report_dict(reps[i]) for i in range(min(nl.value, max_levels))]
