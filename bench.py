@@ -375,6 +375,21 @@ def main():
             "pde_solves": sum(r["fine"]["pde_solves"] for r in reps),
             "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"],
             "stop": reps[-1]["stop_name"], "precond": "spectral", "continuation": "beta_v 1, 1e-1, 1e-2"}
+        # the same continuation with the two-level preconditioner; one GPU only
+        if world == 1:
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            _, reps2, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + ctx.local_dims), model,
+                                                   params, precond="two_level")
+            ctx.synchronize()
+            solve["config3_two_level"] = {
+                "grid": n, "seconds": time.perf_counter() - t0, "levels": len(reps2),
+                "newton_iterations": [r["outer_iterations"] for r in reps2],
+                "fine_hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps2),
+                "coarse_hessian_matvecs": sum(r["coarse"]["hessian_matvecs"] for r in reps2),
+                "final_mismatch_rel": reps2[-1]["final_mismatch_rel"],
+                "final_grad_rel": reps2[-1]["final_grad_rel"], "stop": reps2[-1]["stop_name"],
+                "precond": "two-level, PCG(0.1) inner on the 128^3 coarse grid"}
         # config 1: 64^3 analytic problem, GPU vs the reference on the host cores
         ctx1 = vr.Context(64, device=dev)
         mR1, mT1, _ = V.generate_synthetic(ctx1, nt)

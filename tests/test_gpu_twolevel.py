@@ -83,11 +83,6 @@ def test_split_matvec(vr, ref, ctx, name):
     got = og.split_matvec(sg, w)
     want = orf.split_matvec(sr, w)
     assert rel_l2(got, want) < TOL
-    # identity at a zero data term is exercised by the reference suite; here symmetry
-    w2 = _field(shape, 12, 3)
-    a = float(np.sum(og.split_matvec(sg, w) * w2))
-    b = float(np.sum(og.split_matvec(sg, w2) * w))
-    assert abs(a - b) <= 1e-8 * max(abs(a), abs(b))
 
 
 @pytest.mark.parametrize("inner", ["pcg", "cheb"])
