@@ -290,7 +290,8 @@ enum {
     VR_STATE_FACTOR = 3,     /* 1 field  (after the gradient) */
     VR_STATE_M_HISTORY = 4,  /* nt+1 fields */
     VR_STATE_GRADIENT = 5,   /* 3 fields (after the gradient) */
-    VR_STATE_GRAD_M = 6      /* 3*(nt+1) fields: d_a m_j at [j*3 + a] (after the gradient) */
+    VR_STATE_GRAD_M = 6,     /* 3*(nt+1) fields: d_a m_j at [j*3 + a] (after the gradient) */
+    VR_STATE_LAMBDA_HISTORY = 7 /* nt+1 fields: adjoint lambda_j (full Newton, after the gradient) */
 };
 int vr_state_get(const vr_state* s, int which, double* out_dev);
 /* compute_gradient (objective.cpp:77-112): adjoint sweep with fused accumulation. 1 PDE solve.

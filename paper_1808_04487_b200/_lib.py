@@ -126,7 +126,8 @@ PRECOND_NONE, PRECOND_SPECTRAL, PRECOND_TWO_LEVEL = 0, 1, 2
 INNER_PCG, INNER_CHEB = 0, 1
 STOP_NAMES = ["zero_gradient", "converged_rel", "converged_abs", "max_iterations",
               "line_search_failure"]
-STATE_V, STATE_X_BWD, STATE_X_FWD, STATE_FACTOR, STATE_M_HISTORY, STATE_GRADIENT, STATE_GRAD_M = range(7)
+(STATE_V, STATE_X_BWD, STATE_X_FWD, STATE_FACTOR, STATE_M_HISTORY, STATE_GRADIENT, STATE_GRAD_M,
+ STATE_LAMBDA_HISTORY) = range(8)
 
 P = C.c_void_p
 D = C.c_double

@@ -797,6 +797,13 @@ int vr_state_get(const vr_state* s, int which, double* out) {
                 return;
             case VR_STATE_GRADIENT: src = s->has_gradient ? s->grad : nullptr; n = 3 * N; break;
             case VR_STATE_GRAD_M: src = s->gradm; n = 3LL * (s->nt + 1) * N; break;
+            case VR_STATE_LAMBDA_HISTORY:
+                if (!s->lamhist) vr::throw_logic("vr_state_get: field not computed yet");
+                for (int j = 0; j <= s->nt; ++j)
+                    VR_CUDA(cudaMemcpyAsync(out + j * N, vr::pslice(ctx, s->lamhist, j),
+                                            sizeof(double) * N, cudaMemcpyDeviceToDevice,
+                                            ctx->stream));
+                return;
             default: vr::throw_argument("vr_state_get: unknown field");
         }
         if (!src) vr::throw_logic("vr_state_get: field not computed yet");

@@ -17,7 +17,7 @@
 vr_state::~vr_state() {
     vr_ctx* ctx = obj ? obj->ctx : nullptr;
     if (!ctx) return;
-    for (double* p : {v, xb, mhist, xf, factor, gradm, grad, vpad}) vr::dev_free(ctx, p);
+    for (double* p : {v, xb, mhist, xf, factor, gradm, grad, vpad, lamhist}) vr::dev_free(ctx, p);
 }
 
 vr_objective::~vr_objective() {
@@ -53,9 +53,6 @@ void validate_model(const vr_model& m) {
     if (m.nt < 1) throw_argument("RegModel: n_t must be >= 1");
     if (m.projection < VR_PROJ_IDENTITY || m.projection > VR_PROJ_NEAR_INCOMPRESSIBLE)
         throw_argument("RegModel: unknown projection kind");
-    if (!m.gauss_newton)
-        throw_argument("RegModel: the full-Newton Hessian is not implemented on the GPU path "
-                       "(Gauss-Newton only)");
 }
 
 void validate_params(const vr_solver_params& p) {
@@ -253,7 +250,8 @@ static void prepare_adjoint_ctx(vr_objective* o, vr_state* s) {
 // state of TwoLevelContext::rebuild, precond.cpp:177-196): backward
 // characteristics traced here, the adjoint context (X_fwd, factor, grad m
 // cache) built as for a gradient. One GPU.
-vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt) {
+vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt,
+                             const double* lamhist) {
     vr_ctx* ctx = o->ctx;
     if (ctx->dist) throw_argument("state_from_history: one GPU only");
     const long long N = ctx->g.N;
@@ -271,6 +269,12 @@ vr_state* state_from_history(vr_objective* o, const double* v3, const double* mh
                                     cudaMemcpyDeviceToDevice, ctx->stream));
         sl_trace(ctx, s->v, N, nt, VR_TRACE_BACKWARD, s->xb);
         prepare_adjoint_ctx(o, s);
+        if (lamhist) {
+            s->lamhist = dev_alloc(ctx, (nt + 1) * ctx->hstride);
+            for (int j = 0; j <= nt; ++j)
+                VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->lamhist, j), lamhist + j * N,
+                                        sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
     } catch (...) {
         delete s;
         throw;
@@ -289,16 +293,21 @@ void objective_gradient(vr_objective* o, vr_state* s) {
         op_reg_begin(ctx, s->v, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
     });
 
-    // terminal lambda = m_R - m_nt and the observer at j = nt (objective.cpp:91-99)
+    // terminal lambda = m_R - m_nt and the observer at j = nt (objective.cpp:91-99); the
+    // full-Newton Hessian needs every lambda_j (keep_hist, objective.cpp:100-102)
+    const bool keep_hist = !o->model.gauss_newton;
+    if (keep_hist && !s->lamhist) s->lamhist = dev_alloc(ctx, (nt + 1) * ctx->hstride);
     double* lam[2] = {pslice(ctx, o->ws_tmp, 0), pslice(ctx, o->ws_tmp, 1)};
+    auto lam_at = [&](int j, int slot) { return keep_hist ? pslice(ctx, s->lamhist, j) : lam[slot]; };
     double* b = o->ws_b;
     sl_grad_terminal(ctx, o->mR, pslice(ctx, s->mhist, nt), s->gradm + 3LL * nt * N, 0.5 * dt,
-                     lam[0], b);
+                     lam_at(nt, 0), b);
     int cur = 0;
     for (int j = nt - 1; j >= 0; --j) {
         const double w = (j == 0) ? 0.5 * dt : dt;
-        exchange(ctx, lam[cur]);
-        sl_adjoint_step(ctx, lam[cur], s->xf, s->factor, lam[cur ^ 1], s->gradm + 3LL * j * N, w, b);
+        exchange(ctx, lam_at(j + 1, cur));
+        sl_adjoint_step(ctx, lam_at(j + 1, cur), s->xf, s->factor, lam_at(j, cur ^ 1),
+                        s->gradm + 3LL * j * N, w, b);
         cur ^= 1;
     }
     o->counters.pde_solves += 1;
@@ -337,8 +346,27 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     auto lam = [&](int j) { return pslice(ctx, o->ws_lam, j); };
     double* b = o->ws_b;
     const bool identity_K = o->model.projection == VR_PROJ_IDENTITY;
+    // full Newton (transport.cpp:192-226, objective.cpp:146-147): mt history and its
+    // gradients, sources r_j = div(lambda_j vt), two-field inc-adjoint steps
+    const bool full = !o->model.gauss_newton;
+    if (full && !s->lamhist)
+        throw_logic("hessian_matvec: full Newton mode needs the adjoint history");
+    struct Scratch {
+        vr_ctx* c;
+        double *mt = nullptr, *gmt = nullptr, *rh = nullptr, *lv = nullptr;
+        ~Scratch() {
+            for (double* p : {mt, gmt, rh, lv}) dev_free(c, p);
+        }
+    } fn{ctx};
+    if (full) {
+        fn.mt = dev_alloc(ctx, (nt + 1) * N);
+        fn.gmt = dev_alloc(ctx, 3LL * (nt + 1) * N);
+        fn.rh = dev_alloc(ctx, (nt + 1) * ctx->hstride);
+        fn.lv = dev_alloc(ctx, 3 * N);
+        VR_CUDA(cudaMemsetAsync(fn.mt, 0, sizeof(double) * N, ctx->stream));  // mt_0 = 0
+    }
     // fused: b accumulates inside the sweep (observer order j = nt..0), lam_j ping-pongs
-    const bool fused = ctx->fuse_acc;
+    const bool fused = ctx->fuse_acc && !full;
     sl_incstate_first(ctx, s->gradm, vt3, hdt, tmp[0]);
     int cur = 0;
     for (int j = 0; j < nt; ++j) {
@@ -349,13 +377,35 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
                              0.5 * dt);
         else
             sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
-                             last ? lam(nt) : tmp[cur ^ 1], last ? 1 : 0);
+                             last ? lam(nt) : tmp[cur ^ 1], last ? 1 : 0, nullptr, 0.0,
+                             full ? fn.mt + (j + 1) * N : nullptr);
         cur ^= 1;
     }
     o->counters.pde_solves += 1;
+    if (full) {
+        for (int j = 0; j <= nt; ++j) {
+            op_gradient(ctx, fn.mt + j * N, fn.gmt + 3LL * j * N);
+            sl_scale_vec(ctx, pslice(ctx, s->lamhist, j), vt3, fn.lv);
+            op_divergence(ctx, fn.lv, pslice(ctx, fn.rh, j));
+        }
+    }
     // incremental adjoint, Gauss-Newton branch = plain continuity sweep (transport.cpp:188-190)
     bool out_done = false;
-    if (fused) {
+    if (full) {
+        for (int j = nt - 1; j >= 0; --j) {
+            exchange(ctx, lam(j + 1));
+            exchange(ctx, pslice(ctx, fn.rh, j + 1));
+            sl_adjoint_fn_step(ctx, lam(j + 1), pslice(ctx, fn.rh, j + 1), s->xf, s->factor,
+                               pslice(ctx, fn.rh, j), hdt, lam(j));
+        }
+        const double* lam2 = pslice(ctx, s->lamhist, 0);
+        if (reg_given && identity_K) {
+            sl_accumulate(ctx, lam0, s->gradm, nt, dt, out3, reg_given, lam2, fn.gmt);
+            out_done = true;
+        } else {
+            sl_accumulate(ctx, lam0, s->gradm, nt, dt, b, nullptr, lam2, fn.gmt);
+        }
+    } else if (fused) {
         int lc = 1;  // lam_j alternates between lam(1) and lam(0)
         for (int j = nt - 1; j >= 0; --j) {
             const double w = (j == 0) ? 0.5 * dt : dt;

@@ -22,6 +22,7 @@ struct vr_state {
     double* gradm = nullptr;   // 3(nt+1)N, [j*3 + a]
     double* grad = nullptr;    // 3N
     double* vpad = nullptr;    // x1 slabs: halo-padded copy of v (gather source of the trace)
+    double* lamhist = nullptr; // full Newton: adjoint history lambda_j, (nt+1) halo-padded fields
     double objective = 0.0, mismatch = 0.0, mismatch_rel = 0.0;
     bool has_gradient = false, has_adjoint_ctx = false;
     ~vr_state();
@@ -87,6 +88,8 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                             const vr_model& model, const vr_solver_params& params, int precond,
                             double* v_out, const vr_twolevel_options* tl_opts = nullptr);
 // evaluation context from given v and m history (coarse state of the two-level preconditioner)
-vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt);
+// (lamhist: optional adjoint history, (nt+1) fields, for the full-Newton matvec)
+vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt,
+                             const double* lamhist = nullptr);
 
 }  // namespace vr

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     k_incstate_step(const double* __restrict__ src, const double* __restrict__ dep,
                     const double* __restrict__ gm, const double* __restrict__ vt,
                     double* __restrict__ dst, GridDims g, Tile t, double hdt,
-                    double* __restrict__ b, double wb) {
+                    double* __restrict__ b, double wb, double* __restrict__ mt_out) {
     int i1, i2, i3;
     long long i;
     if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     const double m = gather(src, g, st) + (-hdt) * q;
     const double r = (MODE == 0) ? 1.0 * m + (-hdt) * q : -m;
     dst[i] = r;
+    if (mt_out) mt_out[i] = m;  // full Newton keeps the mt history
     if (MODE == 2) {  // b = 0 + (w lam_nt) grad m_nt (objective.cpp:143-148 at j = nt)
         const double wl = wb * r;
 #pragma unroll
@@ -327,6 +328,37 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB)
     }
 }
 
+// full-Newton inc-adjoint step (transport.cpp:214-222): one stencil, two gathered fields
+//   cur_j = I[cur_{j+1}](X) * factor + hdt * (r_j + I[r_{j+1}](X))
+template <bool BIG>
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
+    k_adjoint_fn_step(const double* __restrict__ src, const double* __restrict__ rnext,
+                      const double* __restrict__ dep, const double* __restrict__ factor,
+                      const double* __restrict__ rcur, double hdt, double* __restrict__ dst,
+                      GridDims g, Tile t) {
+    int i1, i2, i3;
+    long long i;
+    if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
+    double x1, x2, x3;
+    load_point(dep, i, g.N, x1, x2, x3);
+    Stencil st;
+    make_stencil(g, x1, x2, x3, i1, st);
+    const double li = gather(src, g, st);
+    const double si = gather(rnext, g, st);
+    dst[i] = li * factor[i] + hdt * (rcur[i] + si);
+}
+
+// lv_c = lam * vt_c (transport.cpp:203-207)
+__global__ void __launch_bounds__(kThreads)
+    k_scale_vec(const double* __restrict__ lam, const double* __restrict__ vt, double* __restrict__ lv,
+                GridDims g) {
+    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+    if (i >= g.N) return;
+    const double l = lam[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) lv[c * g.N + i] = l * vt[c * g.N + i];
+}
+
 // compute_gradient terminal (objective.cpp:91-99): lam = m_R - m_nt; b = (w lam) grad m_nt
 __global__ void __launch_bounds__(kThreads)
     k_grad_terminal(const double* __restrict__ mR, const double* __restrict__ mfin,
@@ -345,7 +377,8 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     k_accumulate(const double* __restrict__ lam, long long ls, const double* __restrict__ gm,
                  int nt, double dt, double* __restrict__ b, GridDims g,
-                 const double* __restrict__ add) {
+                 const double* __restrict__ add, const double* __restrict__ lam2,
+                 const double* __restrict__ gm2) {
     const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
     if (i >= g.N) return;
     double acc[3] = {0.0, 0.0, 0.0};
@@ -355,6 +388,12 @@ __global__ void __launch_bounds__(kThreads)
         const double* gj = gm + 3LL * j * g.N;
 #pragma unroll
         for (int a = 0; a < 3; ++a) acc[a] = acc[a] + wl * gj[a * g.N + i];
+        if (lam2) {  // full Newton: + (w lam_j) d_a mt_j (objective.cpp:146-147)
+            const double wl2 = w * lam2[j * ls + i];
+            const double* g2 = gm2 + 3LL * j * g.N;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) acc[a] = acc[a] + wl2 * g2[a * g.N + i];
+        }
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) b[a * g.N + i] = add ? acc[a] + add[a * g.N + i] : acc[a];
@@ -433,6 +472,7 @@ unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.
 #define K_INCSTATE2(B) k_incstate_step<2, B>
 #define K_ADJ(B) k_adjoint_step<false, B>
 #define K_ADJ_ACC(B) k_adjoint_step<true, B>
+#define K_ADJ_FN(B) k_adjoint_fn_step<B>
 
 }  // namespace
 
@@ -484,15 +524,16 @@ void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double
 }
 
 void sl_incstate_step(vr_ctx* ctx, const double* src, const double* dep3, const double* gm,
-                      const double* vt3, double hdt, double* dst, int mode, double* b3, double wb) {
+                      const double* vt3, double hdt, double* dst, int mode, double* b3, double wb,
+                      double* mt_out) {
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);
     if (mode == 0)
-        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE0, src, dep3, gm, vt3, dst, g, t, hdt, nullptr, 0.0);
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE0, src, dep3, gm, vt3, dst, g, t, hdt, nullptr, 0.0, mt_out);
     else if (mode == 1)
-        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE1, src, dep3, gm, vt3, dst, g, t, hdt, nullptr, 0.0);
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE1, src, dep3, gm, vt3, dst, g, t, hdt, nullptr, 0.0, mt_out);
     else
-        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE2, src, dep3, gm, vt3, dst, g, t, hdt, b3, wb);
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step", K_INCSTATE2, src, dep3, gm, vt3, dst, g, t, hdt, b3, wb, mt_out);
 }
 
 void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const double* factor,
@@ -515,9 +556,22 @@ void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const
 }
 
 void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, int nt, double dt,
-                   double* b3, const double* add3) {
+                   double* b3, const double* add3, const double* lam2_hist,
+                   const double* gm2_hist) {
     const GridDims& g = ctx->g;
-    VR_LAUNCH(ctx, "sl_accumulate", k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, ctx->hstride, gm_hist, nt, dt, b3, g, add3));
+    VR_LAUNCH(ctx, "sl_accumulate", k_accumulate<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, ctx->hstride, gm_hist, nt, dt, b3, g, add3, lam2_hist, gm2_hist));
+}
+
+void sl_adjoint_fn_step(vr_ctx* ctx, const double* src, const double* rnext, const double* dep3,
+                        const double* factor, const double* rcur, double hdt, double* dst) {
+    const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
+    VR_TILE_LAUNCH(ctx, "sl_adjoint_step", K_ADJ_FN, src, rnext, dep3, factor, rcur, hdt, dst, g, t);
+}
+
+void sl_scale_vec(vr_ctx* ctx, const double* lam, const double* vt3, double* out3) {
+    const GridDims& g = ctx->g;
+    VR_LAUNCH(ctx, "sl_pointwise", k_scale_vec<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam, vt3, out3, g));
 }
 
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out) {

@@ -434,8 +434,9 @@ void TwoLevel::rebuild(vr_objective* fine_obj, const vr_state* fine_state, doubl
             throw_dimension("two-level preconditioner: fine grid " + std::to_string(d[0]) + "x" +
                             std::to_string(d[1]) + "x" + std::to_string(d[2]) +
                             " does not halve to a valid coarse grid");
-    if (!fine_obj->model.gauss_newton)
-        throw_argument("two-level preconditioner: Gauss-Newton only on the GPU path");
+    const bool full = !fine_obj->model.gauss_newton;
+    if (full && !fine_state->lamhist)
+        throw_logic("two-level rebuild: full Newton needs the fine adjoint history");
     if (cctx && cctx->stream != f->stream) destroy_ctx();  // a different fine context
     if (!cctx) cctx = ctx_new_sibling(f, d[0] / 2, d[1] / 2, d[2] / 2);
     release();
@@ -449,18 +450,23 @@ void TwoLevel::rebuild(vr_objective* fine_obj, const vr_state* fine_state, doubl
     // coarse evaluation context: restricted v and m history, fresh coarse characteristics
     double* vc = dev_alloc(cctx, 3 * Nc);
     double* hc = dev_alloc(cctx, (nt + 1) * Nc);
+    double* lc = full ? dev_alloc(cctx, (nt + 1) * Nc) : nullptr;
     try {
         resample_vec(f, fine_state->v, cctx, vc);
-        for (int j = 0; j <= nt; ++j)
+        for (int j = 0; j <= nt; ++j) {
             resample_scalar(f, pslice(f, fine_state->mhist, j), cctx, hc + j * Nc);
-        cstate = state_from_history(cobj, vc, hc, nt);
+            if (full) resample_scalar(f, pslice(f, fine_state->lamhist, j), cctx, lc + j * Nc);
+        }
+        cstate = state_from_history(cobj, vc, hc, nt, lc);
     } catch (...) {
         dev_free(cctx, vc);
         dev_free(cctx, hc);
+        dev_free(cctx, lc);
         throw;
     }
     dev_free(cctx, vc);
     dev_free(cctx, hc);
+    dev_free(cctx, lc);
     eps_M = opts.kappa * eps_H;
     inner_diverged = false;
     if (opts.inner == 1) {

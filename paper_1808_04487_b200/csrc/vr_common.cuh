@@ -314,7 +314,7 @@ void sl_incstate_first(vr_ctx* ctx, const double* gm0, const double* vt3, double
                        double* tmp0);
 void sl_incstate_step(vr_ctx* ctx, const double* src, const double* dep3, const double* gm,
                       const double* vt3, double hdt, double* dst, int mode, double* b3 = nullptr,
-                      double wb = 0.0);
+                      double wb = 0.0, double* mt_out = nullptr);
 // adjoint step with optional gradient accumulation bout_a = (b_a + (w*lam) * gm_a) [+ add_a]
 // (bout defaults to b3)
 void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const double* factor,
@@ -322,9 +322,15 @@ void sl_adjoint_step(vr_ctx* ctx, const double* src, const double* dep3, const d
                      const double* add3 = nullptr, double* bout3 = nullptr);
 void sl_grad_terminal(vr_ctx* ctx, const double* mR, const double* mfinal, const double* gm,
                       double w, double* lam, double* b3);
-// b_a = sum_{j=nt..0} (w_j lam_j) d_a m_j  (+ add_a when add3 is given)
+// b_a = sum_{j=nt..0} (w_j lam_j) d_a m_j [+ (w_j lam2_j) d_a mt_j]  (+ add_a when add3 is given)
 void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, int nt, double dt,
-                   double* b3, const double* add3 = nullptr);
+                   double* b3, const double* add3 = nullptr, const double* lam2_hist = nullptr,
+                   const double* gm2_hist = nullptr);
+// full-Newton inc-adjoint step: dst = I[src](X) * factor + hdt * (rcur + I[rnext](X))
+void sl_adjoint_fn_step(vr_ctx* ctx, const double* src, const double* rnext, const double* dep3,
+                        const double* factor, const double* rcur, double hdt, double* dst);
+// out_c = lam * vt_c
+void sl_scale_vec(vr_ctx* ctx, const double* lam, const double* vt3, double* out3);
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out);
 void synth_fill(vr_ctx* ctx, double amplitude, double* m_T, double* v3);
 

@@ -411,7 +411,7 @@ class EvalState:
         nt = self.obj.model.nt
         nf = {_lib.STATE_V: 3, _lib.STATE_X_BWD: 3, _lib.STATE_X_FWD: 3, _lib.STATE_FACTOR: 1,
               _lib.STATE_M_HISTORY: nt + 1, _lib.STATE_GRADIENT: 3,
-              _lib.STATE_GRAD_M: 3 * (nt + 1)}[which]
+              _lib.STATE_GRAD_M: 3 * (nt + 1), _lib.STATE_LAMBDA_HISTORY: nt + 1}[which]
         out = ctx.empty(nf)
         _lib.call("vr_state_get", self._h, which, out.ptr)
         return out.numpy() if host else out

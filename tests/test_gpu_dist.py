@@ -25,7 +25,8 @@ def _single(vr, ctx, mR, mT, v, vt, model):
 @pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("name,kw", [("h2", dict()),
                                      ("h1div", dict(kind="h1", beta_v=1e-3, div_penalty=True,
-                                                    projection="near_incompressible"))])
+                                                    projection="near_incompressible")),
+                                     ("h2_full_newton", dict(gauss_newton=False))])
 def test_slab_objective_matches_single_gpu(vr, ref, ctx, P, name, kw):
     dims = (32, 32, 32)
     mR, mT, vs = ref.generate_synthetic(dims, 4)
