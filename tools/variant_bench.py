@@ -49,7 +49,11 @@ def main():
     ctx.synchronize()
     prof = ctx.profile_read()
     ctx.set_profiling(False)
-    res = {"lib": os.environ.get("VR_LIB", "default"), "ms_per_matvec": ms,
+    import hashlib
+    o = out.numpy()
+    res = {"lib": os.environ.get("VR_LIB", "default"), "gather": os.environ.get("VR_GATHER", "auto"),
+           "ms_per_matvec": ms, "out_sha1": hashlib.sha1(o.tobytes()).hexdigest()[:12],
+           "out_norm": float(np.linalg.norm(o)),
            "kernels_us": {k: round(1e3 * t / c, 1) for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
            "serial_ms_per_matvec": sum(t for c, t in prof.values()) / 10}
     print(json.dumps(res), flush=True)
