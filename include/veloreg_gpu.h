@@ -328,6 +328,78 @@ int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T,
                               double* v_out, vr_solve_report* reports, int max_levels,
                               int* n_levels, vr_iteration_record* records, int max_records);
 
+/* Grid continuation (not in the reference code): n_grid_levels grids,
+ * each axis halved per level (coarsest >= 16 points per axis). A coarse level solves on
+ * the spectrally restricted images smoothed with sigma = 1 voxel of that level, starting
+ * from the previous level's velocity prolonged spectrally (the coarsest starts from v0
+ * restricted); the finest level solves on the original images. One GPU. */
+int vr_grid_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                         const vr_model* model, const vr_solver_params* params, int precond,
+                         int n_grid_levels, double* v_out, vr_solve_report* reports,
+                         int max_levels, int* n_levels, vr_iteration_record* records,
+                         int max_records);
+/* Scale continuation: sigmas (voxels, strictly decreasing, >= 0; 0 =
+ * the unsmoothed images), images re-smoothed from the originals per level, warm starts */
+int vr_scale_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                          const vr_model* model, const vr_solver_params* params, int precond,
+                          const double* sigmas, int n_sigmas, double* v_out,
+                          vr_solve_report* reports, int max_levels, int* n_levels,
+                          vr_iteration_record* records, int max_records);
+/* BetaSearchParams: eps_J, bracket [beta_lo, beta_hi] (defaults
+ * 0.1 (H2, Table 2), [1e-5, 1]), at most max_bisections midpoints (10), stop below
+ * min_width_decades (0.25) */
+typedef struct {
+    double eps_J;
+    double beta_lo, beta_hi;
+    int max_bisections;
+    double min_width_decades;
+} vr_beta_search_params;
+void vr_beta_search_params_default(vr_beta_search_params* p);
+/* det grad y summary (DetStats, postprocess.hpp:23-27) */
+typedef struct {
+    double min, mean, max;
+} vr_det_summary;
+/* one trial of the search: beta_v, feasibility, det grad y of its velocity, its solve */
+typedef struct {
+    double beta;
+    int feasible;
+    vr_det_summary det;
+    vr_solve_report report;
+} vr_beta_trial;
+/* Beta search: trials at beta_hi, then beta_lo, then bisection on
+ * log10 beta_v; each warm-started from the previous trial's velocity. Returns the
+ * smallest feasible beta (*beta_out) and its velocity. No feasible beta in the bracket
+ * (beta_hi infeasible): VR_ERR_NUMERICS / NumericError with the trials filled in. */
+int vr_beta_search(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                   const vr_model* model, const vr_solver_params* params, int precond,
+                   const vr_beta_search_params* bp, double* beta_out, double* v_out,
+                   vr_beta_trial* trials, int max_trials, int* n_trials);
+
+/* ---- postprocess (postprocess.hpp:9-56; one GPU) ------------ */
+/* det_deformation_gradient (postprocess.cpp:13-29) */
+int vr_det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det);
+/* deformation_map (postprocess.cpp:31-60): displacement u, or y = wrap(x + u) */
+int vr_deformation_map(vr_ctx* ctx, const double* v3, int nt, int absolute, double* out3);
+/* det_stats (postprocess.cpp:62-81): foreground may be NULL (else voxels with
+ * foreground < threshold are skipped); all zero when nothing is counted */
+int vr_det_stats(vr_ctx* ctx, const double* det, const double* foreground, double threshold,
+                 vr_det_summary* out);
+/* transport_labels (postprocess.cpp:83-120): ResourceError above 64 distinct codes */
+int vr_transport_labels(vr_ctx* ctx, const double* labels, const double* v3, int nt,
+                        double* out);
+/* OverlapScores (postprocess.hpp:41-45) */
+typedef struct {
+    double dice;
+    double false_positive_rate;
+    double false_negative_rate;
+} vr_overlap;
+/* overlap_scores (postprocess.cpp:122-165): *n_labels = distinct nonzero codes of both
+ * maps (ascending); the first max_labels go to codes / per_label; mask may be NULL
+ * (else voxels with mask < 0.5 are skipped). Codes must span < 2^24 values. */
+int vr_overlap_scores(vr_ctx* ctx, const double* reference, const double* test,
+                      const double* mask, int max_labels, int* n_labels, int* codes,
+                      vr_overlap* per_label, vr_overlap* union_scores);
+
 /* ---- two-level preconditioner and grid transfer (one GPU) ---- */
 /* spectral_resample (spectral.cpp:340-356): field on src's grid -> dst's grid (coarser or
  * finer on every axis, same device); ncomp 1 or 3 */

@@ -28,6 +28,7 @@ SolveReport = _gpu_lib_types.SolveReport
 IterationRecord = _gpu_lib_types.IterationRecord
 PcgStats = _gpu_lib_types.PcgStats
 TwoLevelOptions = _gpu_lib_types.TwoLevelOptions
+BetaSearchParams = _gpu_lib_types.BetaSearchParams
 
 _lib = None
 P, D, I = C.c_void_p, C.c_double, C.c_int
@@ -79,6 +80,21 @@ _SIG = {
                                         P, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
                                         C.POINTER(IterationRecord), I]),
     "vref_generate_synthetic": (I, [DIMS, I, D, P, P, P]),
+    "vref_det_deformation_gradient": (I, [DIMS, P, I, P]),
+    "vref_deformation_map": (I, [DIMS, P, I, I, P]),
+    "vref_det_stats": (I, [DIMS, P, P, D, C.POINTER(D)]),
+    "vref_transport_labels": (I, [DIMS, P, P, I, P]),
+    "vref_overlap_scores": (I, [DIMS, P, P, P, I, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                C.POINTER(D), C.POINTER(D)]),
+    "vref_grid_continuation": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I, I,
+                                   P, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
+                                   C.POINTER(IterationRecord), I]),
+    "vref_scale_continuation": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I,
+                                    C.POINTER(D), I, P, C.POINTER(SolveReport), I,
+                                    C.POINTER(C.c_int), C.POINTER(IterationRecord), I]),
+    "vref_beta_search": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I,
+                             C.POINTER(BetaSearchParams), C.POINTER(D), P, C.POINTER(D),
+                             C.POINTER(SolveReport), I, C.POINTER(C.c_int)]),
     "vref_spectral_resample": (I, [DIMS, P, I, DIMS, P]),
     "vref_frequency_filter": (I, [DIMS, P, I, I, DIMS, P]),
     "vref_split_matvec": (I, [P, P, P, P]),
@@ -127,6 +143,15 @@ def _call(name, *args):
     st = getattr(lib, name)(*args)
     if st:
         raise RefError(st, lib.vref_last_error_class(), lib.vref_last_error().decode())
+
+
+def _lib_call_status(name, *args):
+    return getattr(load(), name)(*args)
+
+
+def _error(st):
+    lib = load()
+    return RefError(st, lib.vref_last_error_class(), lib.vref_last_error().decode())
 
 
 def _dims(shape):
@@ -452,6 +477,101 @@ def parameter_continuation(m_R, m_T, v0, model, params, precond=1, max_levels=16
     reports = [_report(reps[i]) for i in range(min(nl.value, max_levels))]
     n = min(sum(x["n_records"] for x in reports), max_records)
     return vout, reports, [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
+
+
+def _level_call(fn, args, vshape, max_levels, max_records):
+    vout = np.empty(vshape)
+    reps = (SolveReport * max_levels)()
+    recs = (IterationRecord * max_records)()
+    nl = C.c_int()
+    _call(fn, *args, vout.ctypes.data, reps, max_levels, C.byref(nl), recs, max_records)
+    reports = [_report(reps[i]) for i in range(min(nl.value, max_levels))]
+    n = min(sum(x["n_records"] for x in reports), max_records)
+    return vout, reports, [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
+
+
+def grid_continuation(m_R, m_T, v0, levels, model, params, precond=1, max_levels=16, max_records=1024):
+    """Restated grid continuation over the reference's solver (ref_capi.cpp)."""
+    r, t, v0 = _a(m_R), _a(m_T), _a(v0)
+    return _level_call("vref_grid_continuation",
+                       (_dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data, C.byref(model),
+                        C.byref(params), precond, int(levels)), v0.shape, max_levels, max_records)
+
+
+def scale_continuation(m_R, m_T, v0, sigmas, model, params, precond=1, max_levels=16, max_records=1024):
+    r, t, v0 = _a(m_R), _a(m_T), _a(v0)
+    sg = (C.c_double * len(sigmas))(*[float(x) for x in sigmas])
+    return _level_call("vref_scale_continuation",
+                       (_dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data, C.byref(model),
+                        C.byref(params), precond, sg, len(sigmas)), v0.shape, max_levels, max_records)
+
+
+def beta_search(m_R, m_T, v0, model, params, search, precond=1, max_trials=64):
+    """Restated beta search (ref_capi.cpp); returns (beta, v, trials)."""
+    r, t, v0 = _a(m_R), _a(m_T), _a(v0)
+    vout = np.empty_like(v0)
+    tr = np.zeros((max_trials, 5))
+    reps = (SolveReport * max_trials)()
+    n = C.c_int()
+    beta = C.c_double()
+    st = _lib_call_status("vref_beta_search", _dims(r.shape), r.ctypes.data, t.ctypes.data,
+                          v0.ctypes.data, C.byref(model), C.byref(params), precond, C.byref(search),
+                          C.byref(beta), vout.ctypes.data, tr.ctypes.data_as(C.POINTER(C.c_double)),
+                          reps, max_trials, C.byref(n))
+    trials = [{"beta": tr[i, 0], "feasible": bool(tr[i, 1]), "det_min": tr[i, 2], "det_mean": tr[i, 3],
+               "det_max": tr[i, 4], "report": _report(reps[i])} for i in range(min(n.value, max_trials))]
+    if st != 0:
+        e = _error(st)
+        e.trials = trials
+        raise e
+    return beta.value, vout, trials
+
+
+# ---- postprocess (postprocess.hpp:9-56) ----------------------------------------------
+def det_deformation_gradient(v, nt):
+    v = _a(v)
+    out = np.empty(v.shape[1:])
+    _call("vref_det_deformation_gradient", _dims(v.shape[1:]), v.ctypes.data, nt, out.ctypes.data)
+    return out
+
+
+def deformation_map(v, nt, absolute=False):
+    v = _a(v)
+    out = np.empty_like(v)
+    _call("vref_deformation_map", _dims(v.shape[1:]), v.ctypes.data, nt, 1 if absolute else 0,
+          out.ctypes.data)
+    return out
+
+
+def det_stats(det, foreground=None, threshold=0.05):
+    d = _a(det)
+    fg = _a(foreground) if foreground is not None else None
+    out = (C.c_double * 3)()
+    _call("vref_det_stats", _dims(d.shape), d.ctypes.data, fg.ctypes.data if fg is not None else None,
+          float(threshold), out)
+    return {"min": out[0], "mean": out[1], "max": out[2]}
+
+
+def transport_labels(labels, v, nt):
+    lab, v = _a(labels), _a(v)
+    out = np.empty_like(lab)
+    _call("vref_transport_labels", _dims(lab.shape), lab.ctypes.data, v.ctypes.data, nt, out.ctypes.data)
+    return out
+
+
+def overlap_scores(reference, test, mask=None, max_labels=4096):
+    a, b = _a(reference), _a(test)
+    m = _a(mask) if mask is not None else None
+    n = C.c_int()
+    codes = (C.c_int * max_labels)()
+    per = np.zeros((max_labels, 3))
+    uni = (C.c_double * 3)()
+    _call("vref_overlap_scores", _dims(a.shape), a.ctypes.data, b.ctypes.data,
+          m.ctypes.data if m is not None else None, max_labels, C.byref(n), codes,
+          per.ctypes.data_as(C.POINTER(C.c_double)), uni)
+    k = min(n.value, max_labels)
+    ov = lambda x: {"dice": x[0], "false_positive_rate": x[1], "false_negative_rate": x[2]}  # noqa: E731
+    return {"per_label": {codes[i]: ov(per[i]) for i in range(k)}, "union": ov(uni), "n_labels": n.value}
 
 
 # ---- two-level preconditioner / grid transfer (precond.hpp, spectral.hpp:131-153) ------

@@ -20,6 +20,7 @@
 #include "veloreg/fft.hpp"
 #include "veloreg/objective.hpp"
 #include "veloreg/parallel.hpp"
+#include "veloreg/postprocess.hpp"
 #include "veloreg/precond.hpp"
 #include "veloreg/solver.hpp"
 #include "veloreg/spectral.hpp"
@@ -522,6 +523,214 @@ int vref_parameter_continuation(const int* d, const double* mR, const double* mT
             if (res.report.stop == StopReason::line_search_failure) break;
         }
         store(v, v_out);
+    });
+}
+
+// ---- postprocess (postprocess.hpp:9-56): the reference functions as they are ----
+int vref_det_deformation_gradient(const int* d, const double* v, int nt, double* det) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        store(det_deformation_gradient(load_vector(g, v), nt), det);
+    });
+}
+int vref_deformation_map(const int* d, const double* v, int nt, int absolute, double* out) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        store(deformation_map(load_vector(g, v), nt, absolute != 0), out);
+    });
+}
+int vref_det_stats(const int* d, const double* det, const double* fg, double thr, double* out3) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto f = load_scalar(g, det);
+        DetStats st;
+        if (fg) {
+            auto m = load_scalar(g, fg);
+            st = det_stats(f, &m, thr);
+        } else {
+            st = det_stats(f, static_cast<const ScalarField<double>*>(nullptr), thr);
+        }
+        out3[0] = st.min, out3[1] = st.mean, out3[2] = st.max;
+    });
+}
+int vref_transport_labels(const int* d, const double* labels, const double* v, int nt, double* out) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        store(transport_labels(load_scalar(g, labels), load_vector(g, v), nt), out);
+    });
+}
+// per_label / uni: (dice, false_positive_rate, false_negative_rate) triples
+int vref_overlap_scores(const int* d, const double* ref, const double* test, const double* mask,
+                        int max_labels, int* n_labels, int* codes, double* per_label, double* uni) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto a = load_scalar(g, ref), b = load_scalar(g, test);
+        OverlapReport rep;
+        if (mask) {
+            auto m = load_scalar(g, mask);
+            rep = overlap_scores(a, b, &m);
+        } else {
+            rep = overlap_scores(a, b, static_cast<const ScalarField<double>*>(nullptr));
+        }
+        int k = 0;
+        for (const auto& [code, sc] : rep.per_label) {
+            if (k < max_labels) {
+                codes[k] = code;
+                per_label[3 * k] = sc.dice;
+                per_label[3 * k + 1] = sc.false_positive_rate;
+                per_label[3 * k + 2] = sc.false_negative_rate;
+            }
+            ++k;
+        }
+        *n_labels = k;
+        uni[0] = rep.union_scores.dice;
+        uni[1] = rep.union_scores.false_positive_rate;
+        uni[2] = rep.union_scores.false_negative_rate;
+    });
+}
+
+// ---- continuation, absent from the reference code: restated as
+// loops over the reference's own gauss_newton_solve, spectral_resample,
+// gaussian_smooth, det_deformation_gradient and det_stats ----
+namespace {
+struct PcHolder {
+    SpectralPreconditioner<double> spec;
+    IdentityPreconditioner ident;
+    KrylovPreconditioner<double>& get(int precond) {
+        return precond == VR_PRECOND_SPECTRAL ? static_cast<KrylovPreconditioner<double>&>(spec)
+                                              : static_cast<KrylovPreconditioner<double>&>(ident);
+    }
+};
+}  // namespace
+
+int vref_grid_continuation(const int* d, const double* mR, const double* mT, const double* v0,
+                           const vr_model* m, const vr_solver_params* p, int precond, int n_grid,
+                           double* v_out, vr_solve_report* reps, int max_levels, int* n_levels,
+                           vr_iteration_record* recs, int max_recs) {
+    return guard([&] {
+        if (n_grid < 1) throw ArgumentError("grid continuation: at least one level");
+        for (int a = 0; a < 3; ++a)
+            if ((d[a] >> (n_grid - 1)) < 16 || d[a] % (1 << (n_grid - 1)) != 0)
+                throw ArgumentError("grid continuation: the coarsest level must keep >= 16 points per axis");
+        Grid3 gf = grid_of(d);
+        auto R = load_scalar(gf, mR), T = load_scalar(gf, mT);
+        auto vf = load_vector(gf, v0);
+        PcHolder pc;
+        const int sh0 = n_grid - 1;
+        VectorField<double> v =
+            n_grid == 1 ? vf : spectral_resample(vf, Grid3(d[0] >> sh0, d[1] >> sh0, d[2] >> sh0));
+        int off = 0;
+        *n_levels = 0;
+        for (int l = 0; l < n_grid; ++l) {
+            const int s = n_grid - 1 - l;
+            auto res = [&] {
+                if (s == 0) return gauss_newton_solve(R, T, v, to_model(*m), to_params(*p), pc.get(precond));
+                Grid3 gl(d[0] >> s, d[1] >> s, d[2] >> s);
+                auto Rl = gaussian_smooth(spectral_resample(R, gl), {1.0, 1.0, 1.0});
+                auto Tl = gaussian_smooth(spectral_resample(T, gl), {1.0, 1.0, 1.0});
+                return gauss_newton_solve(Rl, Tl, v, to_model(*m), to_params(*p), pc.get(precond));
+            }();
+            if (l < max_levels) fill_report(res.report, &reps[l], recs, max_recs, off);
+            off += static_cast<int>(res.report.iterations.size());
+            *n_levels = l + 1;
+            if (s == 0) {
+                v = std::move(res.v);
+                break;
+            }
+            if (res.report.stop == StopReason::line_search_failure) {
+                v = spectral_resample(res.v, gf);
+                break;
+            }
+            const int s1 = s - 1;
+            v = spectral_resample(res.v, Grid3(d[0] >> s1, d[1] >> s1, d[2] >> s1));
+        }
+        store(v, v_out);
+    });
+}
+
+int vref_scale_continuation(const int* d, const double* mR, const double* mT, const double* v0,
+                            const vr_model* m, const vr_solver_params* p, int precond,
+                            const double* sigmas, int n, double* v_out, vr_solve_report* reps,
+                            int max_levels, int* n_levels, vr_iteration_record* recs, int max_recs) {
+    return guard([&] {
+        if (n < 1) throw ArgumentError("scale continuation: at least one level");
+        for (int l = 0; l < n; ++l) {
+            if (!(sigmas[l] >= 0.0)) throw ArgumentError("scale continuation: sigmas must be >= 0");
+            if (l > 0 && !(sigmas[l] < sigmas[l - 1]))
+                throw ArgumentError("scale continuation: sigmas must be strictly decreasing");
+        }
+        Grid3 g = grid_of(d);
+        auto R = load_scalar(g, mR), T = load_scalar(g, mT);
+        auto v = load_vector(g, v0);
+        PcHolder pc;
+        int off = 0;
+        *n_levels = 0;
+        for (int l = 0; l < n; ++l) {
+            const double sg = sigmas[l];
+            auto res = sg > 0.0 ? gauss_newton_solve(gaussian_smooth(R, {sg, sg, sg}),
+                                                     gaussian_smooth(T, {sg, sg, sg}), v,
+                                                     to_model(*m), to_params(*p), pc.get(precond))
+                                : gauss_newton_solve(R, T, v, to_model(*m), to_params(*p), pc.get(precond));
+            if (l < max_levels) fill_report(res.report, &reps[l], recs, max_recs, off);
+            off += static_cast<int>(res.report.iterations.size());
+            *n_levels = l + 1;
+            v = std::move(res.v);
+            if (res.report.stop == StopReason::line_search_failure) break;
+        }
+        store(v, v_out);
+    });
+}
+
+// trials: (beta, feasible, det min, det mean, det max) x n; reps: their solve reports
+int vref_beta_search(const int* d, const double* mR, const double* mT, const double* v0,
+                     const vr_model* m, const vr_solver_params* p, int precond,
+                     const vr_beta_search_params* bp, double* beta_out, double* v_out,
+                     double* trials, vr_solve_report* reps, int max_trials, int* n_trials) {
+    return guard([&] {
+        if (!(bp->eps_J > 0.0 && bp->eps_J < 1.0)) throw ArgumentError("beta search: eps_J must be in (0, 1)");
+        if (!(bp->beta_lo > 0.0 && bp->beta_lo < bp->beta_hi))
+            throw ArgumentError("beta search: need 0 < beta_lo < beta_hi");
+        if (bp->max_bisections < 0 || !(bp->min_width_decades > 0.0))
+            throw ArgumentError("beta search: max_bisections >= 0 and min_width_decades > 0");
+        Grid3 g = grid_of(d);
+        auto R = load_scalar(g, mR), T = load_scalar(g, mT);
+        auto vprev = load_vector(g, v0);
+        VectorField<double> vbest(g, 0.0);
+        PcHolder pc;
+        int k = 0;
+        double best = 0.0;
+        auto trial = [&](double beta) {
+            RegModel model = to_model(*m);
+            model.beta_v = beta;
+            auto res = gauss_newton_solve(R, T, vprev, model, to_params(*p), pc.get(precond));
+            auto det = det_deformation_gradient(res.v, m->nt);
+            DetStats st = det_stats(det, static_cast<const ScalarField<double>*>(nullptr), 0.0);
+            const bool feas = st.min >= bp->eps_J && st.max <= 1.0 / bp->eps_J;
+            if (k < max_trials) {
+                double* t = trials + 5 * k;
+                t[0] = beta, t[1] = feas ? 1.0 : 0.0, t[2] = st.min, t[3] = st.mean, t[4] = st.max;
+                fill_report(res.report, &reps[k], nullptr, 0, 0);
+            }
+            ++k;
+            vprev = res.v;
+            if (feas) best = beta, vbest = std::move(res.v);
+            return feas;
+        };
+        bool found = trial(bp->beta_hi);
+        if (found && !trial(bp->beta_lo)) {
+            double lo = std::log10(bp->beta_lo), hi = std::log10(bp->beta_hi);
+            for (int it = 0; it < bp->max_bisections && hi - lo >= bp->min_width_decades; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                if (trial(std::pow(10.0, mid)))
+                    hi = mid;
+                else
+                    lo = mid;
+            }
+        }
+        *n_trials = k;
+        *beta_out = best;
+        if (!found) throw NumericError("beta search: no feasible beta_v in the bracket");
+        store(vbest, v_out);
     });
 }
 

@@ -117,6 +117,25 @@ class PcgStats(C.Structure):
                 ("negative_curvature", C.c_int), ("hit_max_iterations", C.c_int)]
 
 
+class BetaSearchParams(C.Structure):
+    _fields_ = [("eps_J", C.c_double), ("beta_lo", C.c_double), ("beta_hi", C.c_double),
+                ("max_bisections", C.c_int), ("min_width_decades", C.c_double)]
+
+
+class DetSummary(C.Structure):
+    _fields_ = [("min", C.c_double), ("mean", C.c_double), ("max", C.c_double)]
+
+
+class BetaTrial(C.Structure):
+    _fields_ = [("beta", C.c_double), ("feasible", C.c_int), ("det", DetSummary),
+                ("report", SolveReport)]
+
+
+class Overlap(C.Structure):
+    _fields_ = [("dice", C.c_double), ("false_positive_rate", C.c_double),
+                ("false_negative_rate", C.c_double)]
+
+
 # constants (veloreg_gpu.h)
 REG_H1, REG_H2, REG_H3, REG_HELMHOLTZ = 0, 1, 2, 3
 REGOP_APPLY, REGOP_INVERSE, REGOP_INVERSE_SQRT = 0, 1, 2
@@ -213,6 +232,22 @@ SIGNATURES = {
                                       C.POINTER(SolverParams), I, DP, C.POINTER(SolveReport), I,
                                       C.POINTER(C.c_int), C.POINTER(IterationRecord), I]),
     "vr_generate_synthetic": (I, [P, I, D, DP, DP, DP]),
+    "vr_grid_continuation": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I, I,
+                                 DP, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
+                                 C.POINTER(IterationRecord), I]),
+    "vr_scale_continuation": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I,
+                                  C.POINTER(D), I, DP, C.POINTER(SolveReport), I,
+                                  C.POINTER(C.c_int), C.POINTER(IterationRecord), I]),
+    "vr_beta_search_params_default": (None, [C.POINTER(BetaSearchParams)]),
+    "vr_beta_search": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I,
+                           C.POINTER(BetaSearchParams), C.POINTER(D), DP, C.POINTER(BetaTrial), I,
+                           C.POINTER(C.c_int)]),
+    "vr_det_deformation_gradient": (I, [P, DP, I, DP]),
+    "vr_deformation_map": (I, [P, DP, I, I, DP]),
+    "vr_det_stats": (I, [P, DP, DP, D, C.POINTER(DetSummary)]),
+    "vr_transport_labels": (I, [P, DP, DP, I, DP]),
+    "vr_overlap_scores": (I, [P, DP, DP, DP, I, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                              C.POINTER(Overlap), C.POINTER(Overlap)]),
     "vr_twolevel_options_default": (None, [C.POINTER(TwoLevelOptions)]),
     "vr_spectral_resample": (I, [P, DP, I, P, DP]),
     "vr_frequency_filter": (I, [P, DP, I, I, C.POINTER(C.c_int), DP]),

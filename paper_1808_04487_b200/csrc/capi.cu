@@ -967,6 +967,108 @@ int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T,
     });
 }
 
+// ---- continuation / beta search / postprocess (postprocess.cu) ------------------
+static void copy_levels(const std::vector<vr::GnResult>& rs, vr_solve_report* reports, int max_levels,
+                        int* n_levels, vr_iteration_record* records, int max_records) {
+    int off = 0;
+    for (size_t l = 0; l < rs.size(); ++l) {
+        if (reports && static_cast<int>(l) < max_levels) reports[l] = rs[l].report;
+        copy_records(rs[l], records, max_records, off);
+        off += static_cast<int>(rs[l].records.size());
+    }
+    *n_levels = static_cast<int>(rs.size());
+}
+int vr_grid_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                         const vr_model* model, const vr_solver_params* params, int precond,
+                         int n_grid_levels, double* v_out, vr_solve_report* reports,
+                         int max_levels, int* n_levels, vr_iteration_record* records,
+                         int max_records) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_grid_continuation");
+        need(m_R && m_T && v0 && model && params && v_out && n_levels, "vr_grid_continuation");
+        copy_levels(vr::grid_continuation(ctx, m_R, m_T, v0, *model, *params, precond, n_grid_levels, v_out),
+                    reports, max_levels, n_levels, records, max_records);
+    });
+}
+int vr_scale_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                          const vr_model* model, const vr_solver_params* params, int precond,
+                          const double* sigmas, int n_sigmas, double* v_out,
+                          vr_solve_report* reports, int max_levels, int* n_levels,
+                          vr_iteration_record* records, int max_records) {
+    return guard([&] {
+        set_dev(ctx);
+        need(m_R && m_T && v0 && model && params && sigmas && v_out && n_levels, "vr_scale_continuation");
+        copy_levels(vr::scale_continuation(ctx, m_R, m_T, v0, *model, *params, precond, sigmas, n_sigmas, v_out),
+                    reports, max_levels, n_levels, records, max_records);
+    });
+}
+void vr_beta_search_params_default(vr_beta_search_params* p) {
+    p->eps_J = 0.1;  // H2 (Table 2); 0.25 for H1-div
+    p->beta_lo = 1e-5;
+    p->beta_hi = 1.0;
+    p->max_bisections = 10;
+    p->min_width_decades = 0.25;
+}
+int vr_beta_search(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
+                   const vr_model* model, const vr_solver_params* params, int precond,
+                   const vr_beta_search_params* bp, double* beta_out, double* v_out,
+                   vr_beta_trial* trials, int max_trials, int* n_trials) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_beta_search");
+        need(m_R && m_T && v0 && model && params && bp && beta_out && v_out && n_trials, "vr_beta_search");
+        vr::BetaSearch r = vr::beta_search(ctx, m_R, m_T, v0, *model, *params, precond, *bp, v_out);
+        *n_trials = static_cast<int>(r.trials.size());
+        for (int t = 0; t < *n_trials && t < max_trials; ++t) trials[t] = r.trials[t];
+        *beta_out = r.beta;
+        if (!r.found)
+            vr::throw_numeric("beta search: no feasible beta_v in [" + std::to_string(bp->beta_lo) + ", " +
+                              std::to_string(bp->beta_hi) + "] (det grad y bound " + std::to_string(bp->eps_J) + ")");
+    });
+}
+int vr_det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_det_deformation_gradient");
+        need(v3 && det, "vr_det_deformation_gradient");
+        vr::det_deformation_gradient(ctx, v3, nt, det);
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int vr_deformation_map(vr_ctx* ctx, const double* v3, int nt, int absolute, double* out3) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_deformation_map");
+        need(v3 && out3, "vr_deformation_map");
+        vr::deformation_map(ctx, v3, nt, absolute != 0, out3);
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int vr_det_stats(vr_ctx* ctx, const double* det, const double* foreground, double threshold,
+                 vr_det_summary* out) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_det_stats");
+        need(det && out, "vr_det_stats");
+        *out = vr::det_stats(ctx, det, foreground, threshold);
+    });
+}
+int vr_transport_labels(vr_ctx* ctx, const double* labels, const double* v3, int nt,
+                        double* out) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_transport_labels");
+        need(labels && v3 && out, "vr_transport_labels");
+        vr::transport_labels(ctx, labels, v3, nt, out);
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int vr_overlap_scores(vr_ctx* ctx, const double* reference, const double* test,
+                      const double* mask, int max_labels, int* n_labels, int* codes,
+                      vr_overlap* per_label, vr_overlap* union_scores) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_overlap_scores");
+        need(reference && test && n_labels, "vr_overlap_scores");
+        *n_labels = vr::overlap_scores(ctx, reference, test, mask, max_labels, codes, per_label,
+                                       union_scores);
+    });
+}
+
 // ---- two-level preconditioner / grid transfer ----------------------------------
 struct vr_twolevel {
     explicit vr_twolevel(const vr_twolevel_options& o) : tl(o) {}

@@ -92,4 +92,29 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
 vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt,
                              const double* lamhist = nullptr);
 
+// ---- postprocess / continuation (postprocess.cu) ----
+void det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det);
+void deformation_map(vr_ctx* ctx, const double* v3, int nt, bool absolute, double* out3);
+vr_det_summary det_stats(vr_ctx* ctx, const double* det, const double* fg, double threshold);
+void transport_labels(vr_ctx* ctx, const double* labels, const double* v3, int nt, double* out);
+// returns the number of distinct nonzero codes; fills the first max_labels
+int overlap_scores(vr_ctx* ctx, const double* ref, const double* test, const double* mask,
+                   int max_labels, int* codes_out, vr_overlap* per_label, vr_overlap* uni);
+std::vector<GnResult> grid_continuation(vr_ctx* ctx, const double* mR, const double* mT,
+                                        const double* v0, const vr_model& model,
+                                        const vr_solver_params& params, int precond,
+                                        int n_levels, double* v_out);
+std::vector<GnResult> scale_continuation(vr_ctx* ctx, const double* mR, const double* mT,
+                                         const double* v0, const vr_model& model,
+                                         const vr_solver_params& params, int precond,
+                                         const double* sigmas, int n, double* v_out);
+struct BetaSearch {
+    bool found = false;
+    double beta = 0.0;
+    std::vector<vr_beta_trial> trials;
+};
+BetaSearch beta_search(vr_ctx* ctx, const double* mR, const double* mT, const double* v0,
+                       const vr_model& model, const vr_solver_params& params, int precond,
+                       const vr_beta_search_params& bp, double* v_out);
+
 }  // namespace vr

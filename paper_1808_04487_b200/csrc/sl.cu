@@ -348,6 +348,27 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
     dst[i] = li * factor[i] + hdt * (rcur[i] + si);
 }
 
+// deformation_map step (postprocess.cpp:40-47): u <- I3[u](X) - half_dt (v(X) + v),
+// one stencil for the three components
+template <bool BIG>
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
+    k_defmap_step(const double* __restrict__ u, const double* __restrict__ dep,
+                  const double* __restrict__ vdep, const double* __restrict__ v, double half_dt,
+                  double* __restrict__ out, GridDims g, Tile t) {
+    int i1, i2, i3;
+    long long i;
+    if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
+    double x1, x2, x3;
+    load_point(dep, i, g.N, x1, x2, x3);
+    Stencil st;
+    make_stencil(g, x1, x2, x3, i1, st);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double ud = gather(u + c * g.N, g, st);
+        out[c * g.N + i] = ud - half_dt * (vdep[c * g.N + i] + v[c * g.N + i]);
+    }
+}
+
 // lv_c = lam * vt_c (transport.cpp:203-207)
 __global__ void __launch_bounds__(kThreads)
     k_scale_vec(const double* __restrict__ lam, const double* __restrict__ vt, double* __restrict__ lv,
@@ -473,6 +494,7 @@ unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.
 #define K_ADJ(B) k_adjoint_step<false, B>
 #define K_ADJ_ACC(B) k_adjoint_step<true, B>
 #define K_ADJ_FN(B) k_adjoint_fn_step<B>
+#define K_DEFMAP(B) k_defmap_step<B>
 
 }  // namespace
 
@@ -567,6 +589,13 @@ void sl_adjoint_fn_step(vr_ctx* ctx, const double* src, const double* rnext, con
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);
     VR_TILE_LAUNCH(ctx, "sl_adjoint_step", K_ADJ_FN, src, rnext, dep3, factor, rcur, hdt, dst, g, t);
+}
+
+void sl_defmap_step(vr_ctx* ctx, const double* u3, const double* dep3, const double* vdep3,
+                    const double* v3, double half_dt, double* out3) {
+    const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
+    VR_TILE_LAUNCH(ctx, "sl_defmap_step", K_DEFMAP, u3, dep3, vdep3, v3, half_dt, out3, g, t);
 }
 
 void sl_scale_vec(vr_ctx* ctx, const double* lam, const double* vt3, double* out3) {

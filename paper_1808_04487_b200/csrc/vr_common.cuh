@@ -329,6 +329,9 @@ void sl_accumulate(vr_ctx* ctx, const double* lam_hist, const double* gm_hist, i
 // full-Newton inc-adjoint step: dst = I[src](X) * factor + hdt * (rcur + I[rnext](X))
 void sl_adjoint_fn_step(vr_ctx* ctx, const double* src, const double* rnext, const double* dep3,
                         const double* factor, const double* rcur, double hdt, double* dst);
+// deformation_map step: out_c = I[u_c](X) - half_dt (vdep_c + v_c) (out must not alias u)
+void sl_defmap_step(vr_ctx* ctx, const double* u3, const double* dep3, const double* vdep3,
+                    const double* v3, double half_dt, double* out3);
 // out_c = lam * vt_c
 void sl_scale_vec(vr_ctx* ctx, const double* lam, const double* vt3, double* out3);
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out);

@@ -698,6 +698,137 @@ def parameter_continuation(ctx, m_R, m_T, v0, model=None, params=None, precond="
     return vout.numpy(), reports, _records(recs, min(nrec, max_records))
 
 
+def _levels(ctx, fn, args, max_levels, max_records):
+    vout = ctx.empty(3)
+    reps = (_lib.SolveReport * max_levels)()
+    recs = (_lib.IterationRecord * max_records)()
+    nl = C.c_int()
+    _lib.call(fn, *args, vout.ptr, reps, max_levels, C.byref(nl), recs, max_records)
+    reports = [_report_dict(reps[i]) for i in range(min(nl.value, max_levels))]
+    nrec = sum(r["n_records"] for r in reports)
+    return vout.numpy(), reports, _records(recs, min(nrec, max_records))
+
+
+def grid_continuation(ctx, m_R, m_T, v0, levels, model=None, params=None, precond="spectral",
+                      max_levels=16, max_records=1024):
+    """Coarse-to-fine solves over `levels` grids (vr_grid_continuation)."""
+    model = model if model is not None else make_model()
+    params = params if params is not None else make_params()
+    dR, dT, dv0 = _dev(ctx, m_R), _dev(ctx, m_T), _dev(ctx, v0)
+    return _levels(ctx, "vr_grid_continuation",
+                   (ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model), C.byref(params),
+                    _enum(_PRECOND, precond), int(levels)), max_levels, max_records)
+
+
+def scale_continuation(ctx, m_R, m_T, v0, sigmas, model=None, params=None, precond="spectral",
+                       max_levels=16, max_records=1024):
+    """Warm-started solves on images smoothed by decreasing sigmas."""
+    model = model if model is not None else make_model()
+    params = params if params is not None else make_params()
+    dR, dT, dv0 = _dev(ctx, m_R), _dev(ctx, m_T), _dev(ctx, v0)
+    sg = (C.c_double * len(sigmas))(*[float(x) for x in sigmas])
+    vout = ctx.empty(3)
+    reps = (_lib.SolveReport * max_levels)()
+    recs = (_lib.IterationRecord * max_records)()
+    nl = C.c_int()
+    _lib.call("vr_scale_continuation", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
+              C.byref(params), _enum(_PRECOND, precond), sg, len(sigmas), vout.ptr, reps,
+              max_levels, C.byref(nl), recs, max_records)
+    reports = [_report_dict(reps[i]) for i in range(min(nl.value, max_levels))]
+    nrec = sum(r["n_records"] for r in reports)
+    return vout.numpy(), reports, _records(recs, min(nrec, max_records))
+
+
+def beta_search_params(**kw) -> _lib.BetaSearchParams:
+    p = _lib.BetaSearchParams()
+    _lib.load().vr_beta_search_params_default(C.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+def _trial_dict(t) -> dict:
+    return {"beta": t.beta, "feasible": bool(t.feasible), "det_min": t.det.min,
+            "det_mean": t.det.mean, "det_max": t.det.max, "report": _report_dict(t.report)}
+
+
+def beta_search(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral", search=None,
+                max_trials=64):
+    """Smallest feasible beta_v by bisection on log10 beta (vr_beta_search).
+    Returns (beta, v, trials); NumericError (with .trials attached) when beta_hi is infeasible."""
+    model = model if model is not None else make_model()
+    params = params if params is not None else make_params()
+    search = search if search is not None else beta_search_params()
+    dR, dT, dv0 = _dev(ctx, m_R), _dev(ctx, m_T), _dev(ctx, v0)
+    vout = ctx.empty(3)
+    trials = (_lib.BetaTrial * max_trials)()
+    nt_ = C.c_int()
+    beta = C.c_double()
+    try:
+        _lib.call("vr_beta_search", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
+                  C.byref(params), _enum(_PRECOND, precond), C.byref(search), C.byref(beta), vout.ptr,
+                  trials, max_trials, C.byref(nt_))
+    except _lib.NumericError as e:
+        e.trials = [_trial_dict(trials[i]) for i in range(min(nt_.value, max_trials))]
+        raise
+    return beta.value, vout.numpy(), [_trial_dict(trials[i]) for i in range(min(nt_.value, max_trials))]
+
+
+# ---- postprocess (postprocess.hpp:9-56) -----------------------------------------
+def det_deformation_gradient(ctx, v, nt):
+    """det grad y by continuity transport (postprocess.cpp:13-29)."""
+    dv = _dev(ctx, v)
+    out = ctx.empty(1)
+    _lib.call("vr_det_deformation_gradient", ctx.handle, dv.ptr, nt, out.ptr)
+    return _ret(out, _is_host(v))
+
+
+def deformation_map(ctx, v, nt, absolute=False):
+    """Displacement u(., 1), or y = wrap(x + u) (postprocess.cpp:31-60)."""
+    dv = _dev(ctx, v)
+    out = ctx.empty(3)
+    _lib.call("vr_deformation_map", ctx.handle, dv.ptr, nt, 1 if absolute else 0, out.ptr)
+    return _ret(out, _is_host(v))
+
+
+def det_stats(ctx, det, foreground=None, threshold=0.05) -> dict:
+    """min / mean / max of det grad y, optionally on the foreground (postprocess.cpp:62-81)."""
+    dd = _dev(ctx, det)
+    fg = _dev(ctx, foreground) if foreground is not None else None
+    st = _lib.DetSummary()
+    _lib.call("vr_det_stats", ctx.handle, dd.ptr, fg.ptr if fg is not None else None, float(threshold),
+              C.byref(st))
+    return {"min": st.min, "mean": st.mean, "max": st.max}
+
+
+def transport_labels(ctx, labels, v, nt):
+    """Per-code label transport (postprocess.cpp:83-120)."""
+    dl, dv = _dev(ctx, labels), _dev(ctx, v)
+    out = ctx.empty(1)
+    _lib.call("vr_transport_labels", ctx.handle, dl.ptr, dv.ptr, nt, out.ptr)
+    return _ret(out, _is_host(labels))
+
+
+def _ov(o) -> dict:
+    return {"dice": o.dice, "false_positive_rate": o.false_positive_rate,
+            "false_negative_rate": o.false_negative_rate}
+
+
+def overlap_scores(ctx, reference, test, mask=None, max_labels=4096) -> dict:
+    """Dice / error rates per label and for the union (postprocess.cpp:122-165)."""
+    da, db = _dev(ctx, reference), _dev(ctx, test)
+    dm = _dev(ctx, mask) if mask is not None else None
+    n = C.c_int()
+    codes = (C.c_int * max_labels)()
+    per = (_lib.Overlap * max_labels)()
+    uni = _lib.Overlap()
+    _lib.call("vr_overlap_scores", ctx.handle, da.ptr, db.ptr, dm.ptr if dm is not None else None,
+              max_labels, C.byref(n), codes, per, C.byref(uni))
+    k = min(n.value, max_labels)
+    return {"per_label": {codes[i]: _ov(per[i]) for i in range(k)}, "union": _ov(uni),
+            "n_labels": n.value}
+
+
 # ---- x1-slab decomposition (DESIGN.md section 7) ---------------------------------
 SLAB_FIELDS = ("planes", "first_plane", "halo", "n2s", "k2_off", "points", "spectrum",
                "padded_stride", "global_points")

@@ -1,0 +1,185 @@
+"""GPU postprocess and continuation vs the compiled reference.
+
+Reference: proj/src/postprocess.cpp:13-167 (det grad y, deformation map,
+det_stats, label transport, overlap scores; tests proj/tests/test_postprocess.cpp)
+and SPEC.md:494-520 (grid / scale continuation and the beta search, which the
+reference code does not implement: the oracle restates them in
+oracle/ref_capi.cpp as loops over the reference's own solver and postprocess
+functions). Bars: fields 1e-10 relative L2 (fp64); labels and overlap scores
+exact; solves as in test_gpu_solver.py (Newton iterations +-1, final mismatch
+within 1%).
+"""
+import numpy as np
+import pytest
+
+from conftest import periodic_diff, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _compressible(ref, dims, amp=1.0):
+    # seeded band-limited field of the reference test support (test_support.hpp:90-97)
+    return ref.random_smooth_vector(dims, 2, 4487, amp)
+
+
+@pytest.mark.parametrize("n", [16, 32])
+def test_det_deformation_gradient(vr, ref, ctx, n):
+    dims = (n, n, n)
+    c = ctx(dims)
+    for v in (_compressible(ref, dims, 0.8), ref.generate_synthetic(dims, 4)[2], np.zeros((3,) + dims)):
+        g = vr.det_deformation_gradient(c, v, 4)
+        r = ref.det_deformation_gradient(v, 4)
+        assert rel_l2(g, r) <= 1e-10
+    assert np.all(vr.det_deformation_gradient(c, np.zeros((3,) + dims), 4) == 1.0)
+
+
+@pytest.mark.parametrize("absolute", [False, True])
+def test_deformation_map(vr, ref, ctx, absolute):
+    dims = (32, 32, 32)
+    c = ctx(dims)
+    v = _compressible(ref, dims, 0.6)
+    g = vr.deformation_map(c, v, 4, absolute=absolute)
+    r = ref.deformation_map(v, 4, absolute=absolute)
+    if absolute:
+        assert periodic_diff(g, r).max() <= 1e-12
+    else:
+        assert rel_l2(g, r) <= 1e-10
+
+
+def test_det_stats(vr, ref, ctx):
+    dims = (16, 16, 16)
+    c = ctx(dims)
+    mR, _, _ = ref.generate_synthetic(dims, 4)
+    det = ref.det_deformation_gradient(_compressible(ref, dims, 0.8), 4)
+    for fg in (None, mR):
+        g = vr.det_stats(c, det, fg, 0.05)
+        r = ref.det_stats(det, fg, 0.05)
+        assert g["min"] == r["min"] and g["max"] == r["max"]
+        assert abs(g["mean"] - r["mean"]) <= 1e-14 * abs(r["mean"])
+    # test_postprocess.cpp:70-88 masked extremes; nothing counted -> zeros
+    d = np.ones((8, 8, 8))
+    d.flat[0], d.flat[1] = 0.5, 2.0
+    fg = np.ones_like(d)
+    fg.flat[0] = fg.flat[1] = 0.0
+    c8 = ctx((8, 8, 8))
+    assert vr.det_stats(c8, d)["min"] == 0.5 and vr.det_stats(c8, d)["max"] == 2.0
+    m = vr.det_stats(c8, d, fg, 0.05)
+    assert m["min"] == 1.0 and m["max"] == 1.0
+    assert vr.det_stats(c8, d, np.zeros_like(d), 0.05) == {"min": 0.0, "mean": 0.0, "max": 0.0}
+
+
+def _labels(ref, dims):
+    mR, mT, vs = ref.generate_synthetic(dims, 4)
+    lab = np.round(mT * 4.0)  # codes 0..4 in nested shells
+    lab[lab == 2] = 7         # non-contiguous code
+    lab[0, 0, :4] = -3        # negative code
+    return lab, vs
+
+
+@pytest.mark.parametrize("n", [16, 32])
+def test_transport_labels(vr, ref, ctx, n):
+    dims = (n, n, n)
+    c = ctx(dims)
+    lab, vs = _labels(ref, dims)
+    for v in (vs, _compressible(ref, dims, 0.8), np.zeros((3,) + dims)):
+        g = vr.transport_labels(c, lab, v, 4)
+        r = ref.transport_labels(lab, v, 4)
+        assert np.array_equal(g, r)
+
+
+def test_transport_labels_limit(vr, ctx):
+    dims = (16, 16, 16)
+    lab = np.arange(16 ** 3, dtype=np.float64).reshape(dims) % 65 + 1  # 65 codes
+    with pytest.raises(vr.ResourceError):
+        vr.transport_labels(ctx(dims), lab, np.zeros((3,) + dims), 4)
+
+
+def test_overlap_scores(vr, ref, ctx):
+    dims = (32, 32, 32)
+    c = ctx(dims)
+    lab, vs = _labels(ref, dims)
+    moved = ref.transport_labels(lab, vs, 4)
+    mR, _, _ = ref.generate_synthetic(dims, 4)
+    mask = (mR > 0.3).astype(np.float64)
+    for m in (None, mask):
+        g = vr.overlap_scores(c, lab, moved, m)
+        r = ref.overlap_scores(lab, moved, m)
+        assert g["n_labels"] == r["n_labels"]
+        assert list(g["per_label"]) == list(r["per_label"])
+        for k in r["per_label"]:
+            assert g["per_label"][k] == pytest.approx(r["per_label"][k], rel=0, abs=0)
+        assert g["union"] == pytest.approx(r["union"], rel=0, abs=0)
+    # empty on both sides: dice 1, rates 0 (postprocess.hpp:52-53)
+    z = np.zeros(dims)
+    e = vr.overlap_scores(c, z, z)
+    assert e["n_labels"] == 0 and e["union"] == {"dice": 1.0, "false_positive_rate": 0.0,
+                                                  "false_negative_rate": 0.0}
+
+
+def _cmp_levels(rg, rr):
+    assert len(rg) == len(rr)
+    for a, b in zip(rg, rr):
+        assert a["stop"] == b["stop"]
+        assert abs(a["outer_iterations"] - b["outer_iterations"]) <= 1
+        assert abs(a["final_mismatch_rel"] - b["final_mismatch_rel"]) <= 1e-2 * b["final_mismatch_rel"]
+
+
+def test_grid_continuation(vr, ref, ctx):
+    dims = (32, 32, 32)
+    c = ctx(dims)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model(), vr.make_params()
+    v0 = np.zeros((3,) + dims)
+    vg, rg, _ = vr.grid_continuation(c, mR, mT, v0, 2, model, params)
+    vref, rr, _ = ref.grid_continuation(mR, mT, v0, 2, model, params)
+    _cmp_levels(rg, rr)
+    assert rel_l2(vg, vref) < 1e-6
+    # one level == the plain solve
+    v1, r1, _ = vr.grid_continuation(c, mR, mT, v0, 1, model, params)
+    plain = vr.gauss_newton_solve(c, mR, mT, v0, model, params)
+    assert np.array_equal(v1, plain.v) and r1[0]["outer_iterations"] == plain.report["outer_iterations"]
+    with pytest.raises(vr.ArgumentError):
+        vr.grid_continuation(c, mR, mT, v0, 3, model, params)  # coarsest would be 8^3
+
+
+def test_scale_continuation(vr, ref, ctx):
+    dims = (32, 32, 32)
+    c = ctx(dims)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model(), vr.make_params()
+    v0 = np.zeros((3,) + dims)
+    vg, rg, _ = vr.scale_continuation(c, mR, mT, v0, [4.0, 2.0, 1.0], model, params)
+    vref, rr, _ = ref.scale_continuation(mR, mT, v0, [4.0, 2.0, 1.0], model, params)
+    _cmp_levels(rg, rr)
+    assert rel_l2(vg, vref) < 1e-6
+    with pytest.raises(vr.ArgumentError):
+        vr.scale_continuation(c, mR, mT, v0, [1.0, 2.0], model, params)
+
+
+def test_beta_search(vr, ref, ctx):
+    dims = (16, 16, 16)
+    c = ctx(dims)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model(), vr.make_params()
+    v0 = np.zeros((3,) + dims)
+    sp = vr.beta_search_params(eps_J=0.9)
+    bg, vg, tg = vr.beta_search(c, mR, mT, v0, model, params, search=sp)
+    br, vref, tr = ref.beta_search(mR, mT, v0, model, params, sp)
+    assert [t["beta"] for t in tg] == pytest.approx([t["beta"] for t in tr], rel=1e-15)
+    assert [t["feasible"] for t in tg] == [t["feasible"] for t in tr]
+    assert len(tg) > 2 and bg == br
+    for a, b in zip(tg, tr):
+        assert abs(a["report"]["outer_iterations"] - b["report"]["outer_iterations"]) <= 1
+        assert a["det_min"] == pytest.approx(b["det_min"], rel=1e-6)
+        assert a["det_max"] == pytest.approx(b["det_max"], rel=1e-6)
+    assert rel_l2(vg, vref) < 1e-6
+    # the returned beta satisfies the bounds, a 10x smaller one does not
+    det = vr.det_deformation_gradient(c, vg, 4)
+    assert det.min() >= 0.9 and det.max() <= 1 / 0.9
+    # m_T == m_R: every beta feasible -> the bracket's lower end
+    b0, _, t0 = vr.beta_search(c, mT, mT, v0, model, params, search=sp)
+    assert b0 == sp.beta_lo and len(t0) == 2
+    # bound unreachable -> NumericError carrying the trials
+    with pytest.raises(vr.NumericError) as e:
+        vr.beta_search(c, mR, mT, v0, model, params, search=vr.beta_search_params(eps_J=0.9999999))
+    assert len(e.value.trials) == 1 and not e.value.trials[0]["feasible"]

@@ -110,3 +110,69 @@ def test_np_vs_compiled_reference_fresh_inputs(ref):
     term = ref.random_smooth_scalar(shape, 2, 31, 1.0)
     init, hist_r = ref.solve_adjoint(term, v, 4, needs_history=True)
     assert rel_l2(O.solve_adjoint(term, v, 4), hist_r) < 1e-12
+
+
+# ---- continuation restatements (oracle/ref_capi.cpp) ------------------
+def _ref_or_skip():
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref/libveloreg_ref.so not built (make -C oracle lib)")
+    return ref
+
+
+def _pods():
+    from paper_1808_04487_b200 import _lib as L
+    m = L.Model(L.RegNorm(L.REG_H2, 1.0, 1, 0, 1e-4), L.PROJ_IDENTITY, 1e-2, 4, 1)
+    p = L.SolverParams(1e-2, 1e-6, 50, 100, 1e-4, 0.5, 20, 1)
+    return L, m, p
+
+
+def test_oracle_single_level_continuations_equal_plain_solve():
+    ref = _ref_or_skip()
+    L, m, p = _pods()
+    dims = (16, 16, 16)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    v0 = np.zeros((3,) + dims)
+    plain, rep, _ = ref.gauss_newton_solve(mR, mT, v0, m, p)
+    vg, rg, _ = ref.grid_continuation(mR, mT, v0, 1, m, p)
+    vs, rs, _ = ref.scale_continuation(mR, mT, v0, [0.0], m, p)
+    assert np.array_equal(vg, plain) and np.array_equal(vs, plain)
+    assert rg[0]["outer_iterations"] == rs[0]["outer_iterations"] == rep["outer_iterations"]
+
+
+def test_oracle_grid_continuation_quality():
+    # two levels 16^3 -> 32^3 end within 1.5x of the single-level mismatch
+    ref = _ref_or_skip()
+    L, m, p = _pods()
+    dims = (32, 32, 32)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    v0 = np.zeros((3,) + dims)
+    _, rep, _ = ref.gauss_newton_solve(mR, mT, v0, m, p)
+    _, reps, _ = ref.grid_continuation(mR, mT, v0, 2, m, p)
+    assert len(reps) == 2 and all(r["success"] for r in reps)
+    assert reps[-1]["final_mismatch_rel"] <= 1.5 * rep["final_mismatch_rel"]
+
+
+def test_oracle_beta_search_contract():
+    ref = _ref_or_skip()
+    L, m, p = _pods()
+    dims = (16, 16, 16)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    v0 = np.zeros((3,) + dims)
+    sp = L.BetaSearchParams(0.9, 1e-5, 1.0, 10, 0.25)
+    beta, v, trials = ref.beta_search(mR, mT, v0, m, p, sp)
+    assert trials[0]["beta"] == 1.0 and trials[0]["feasible"]
+    assert trials[1]["beta"] == 1e-5 and not trials[1]["feasible"]
+    feas = [t["beta"] for t in trials if t["feasible"]]
+    assert beta == min(feas)
+    infeas_above = [t["beta"] for t in trials if not t["feasible"] and t["beta"] > beta]
+    assert not infeas_above  # monotone on this problem
+    det = ref.det_deformation_gradient(v, 4)
+    assert det.min() >= 0.9 and det.max() <= 1 / 0.9
+    # m_T == m_R: the lower end
+    b0, _, t0 = ref.beta_search(mT, mT, v0, m, p, sp)
+    assert b0 == 1e-5 and len(t0) == 2
+    # unreachable bound: error carrying the trace
+    with pytest.raises(ref.RefError) as e:
+        ref.beta_search(mR, mT, v0, m, p, L.BetaSearchParams(0.9999999, 1e-5, 1.0, 10, 0.25))
+    assert len(e.value.trials) == 1
