@@ -1,0 +1,51 @@
+"""solve_profile.py -- config-3 beta continuation with the spectral and the two-level
+preconditioner: wall time, per-iteration records and per-category kernel time
+(CUDA events per launch; the gap to wall time is host/launch overhead)."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1808_04487_b200 as vr  # noqa: E402
+import paper_1808_04487_b200.veloreg as V  # noqa: E402
+from paper_1808_04487_b200 import phantom  # noqa: E402
+
+
+def main():
+    n = int(os.environ.get("N", "256"))
+    cfg = phantom.CONFIGS[3]
+    m_T = phantom.ellipsoid_phantom(n)
+    v = phantom.bandlimited_velocity(n, cfg["kmax"], cfg["disp"])
+    ctx = vr.Context(n)
+    d_mT = ctx.to_device(m_T)
+    d_mR = ctx.to_device(np.asarray(V.solve_state(ctx, m_T, v, 4))[4])
+    model = V.make_model("h2", beta_v=1e-2, nt=4)
+    params = V.make_params(eps_opt=1e-2)
+    for pc in ("spectral", "two_level", "spectral", "two_level"):
+        for prof in (False, True):
+            ctx.synchronize()
+            ctx.set_profiling(prof)
+            t0 = time.perf_counter()
+            _, reps, recs = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3, n, n, n)), model, params,
+                                                     precond=pc)
+            ctx.synchronize()
+            wall = time.perf_counter() - t0
+            out = {"precond": pc, "profiling": prof, "wall_s": wall,
+                   "newton": [r["outer_iterations"] for r in reps],
+                   "fine_mv": sum(r["fine"]["hessian_matvecs"] for r in reps),
+                   "coarse_mv": sum(r["coarse"]["hessian_matvecs"] for r in reps),
+                   "records": [{k: rr[k] for k in ("k", "inner_iterations", "fine_matvecs", "coarse_matvecs",
+                                                   "wall_time_s")} for rr in recs]}
+            if prof:
+                p = ctx.profile_read()
+                out["kernel_ms"] = {k: round(t, 2) for k, (c, t) in sorted(p.items(), key=lambda kv: -kv[1][1])}
+                out["kernel_total_ms"] = sum(t for c, t in p.values())
+                ctx.set_profiling(False)
+            print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
