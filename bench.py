@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=90.0,
                     help="wall budget for the reference arm's timed matvecs")
     ap.add_argument("--no-solve", action="store_true", help="skip the GN solve timings")
+    ap.add_argument("--no-config4", action="store_true",
+                    help="skip the 512^3 (config 4, one GPU) matvec throughput")
     return ap.parse_args()
 
 
@@ -362,14 +364,17 @@ def main():
         solve = {}
         # config 3: beta continuation 1 -> 1e-1 -> 1e-2, warm starts, eps_opt 1e-2
         params = V.make_params(eps_opt=1e-2)
-        ctx.synchronize()
-        t0 = time.perf_counter()
-        vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + ctx.local_dims), model,
-                                                 params)
-        ctx.synchronize()
-        t_solve = time.perf_counter() - t0
+        t_runs = []
+        for _ in range(2):  # the first run also grows the stream-ordered memory pool
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + ctx.local_dims), model,
+                                                     params)
+            ctx.synchronize()
+            t_runs.append(time.perf_counter() - t0)
+        t_solve = t_runs[-1]
         solve["config3"] = {
-            "grid": n, "seconds": t_solve, "levels": len(reps),
+            "grid": n, "seconds": t_solve, "seconds_first_run": t_runs[0], "levels": len(reps),
             "newton_iterations": [r["outer_iterations"] for r in reps],
             "hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps),
             "pde_solves": sum(r["fine"]["pde_solves"] for r in reps),
@@ -377,13 +382,16 @@ def main():
             "stop": reps[-1]["stop_name"], "precond": "spectral", "continuation": "beta_v 1, 1e-1, 1e-2"}
         # the same continuation with the two-level preconditioner; one GPU only
         if world == 1:
-            ctx.synchronize()
-            t0 = time.perf_counter()
-            _, reps2, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + ctx.local_dims), model,
-                                                   params, precond="two_level")
-            ctx.synchronize()
+            t2 = []
+            for _ in range(2):  # first run: coarse context, plans and pool growth
+                ctx.synchronize()
+                t0 = time.perf_counter()
+                _, reps2, _ = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3,) + ctx.local_dims),
+                                                       model, params, precond="two_level")
+                ctx.synchronize()
+                t2.append(time.perf_counter() - t0)
             solve["config3_two_level"] = {
-                "grid": n, "seconds": time.perf_counter() - t0, "levels": len(reps2),
+                "grid": n, "seconds": t2[-1], "seconds_first_run": t2[0], "levels": len(reps2),
                 "newton_iterations": [r["outer_iterations"] for r in reps2],
                 "fine_hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps2),
                 "coarse_hessian_matvecs": sum(r["coarse"]["hessian_matvecs"] for r in reps2),
@@ -416,6 +424,45 @@ def main():
                 solve["config1"]["cpu_reference"] = f"unavailable: {exc}"
         ctx1.close()
 
+    # ---- config 4 on one GPU: 512^3 phantom (|k| <= 10), the P = 1 point of the
+    # strong-scaling curve; device-resident matvecs timed like the main line -----
+    cfg4 = None
+    if world == 1 and not args.no_config4 and n == 256:
+        from paper_1808_04487_b200 import phantom
+        n4 = phantom.CONFIGS[4]["n"]
+        m_T4, v4 = phantom.make_config_inputs(4)
+        vt4 = phantom.bandlimited_direction(n4)
+        c4 = vr.Context(n4, device=dev)
+        dT4, dv4, dvt4 = c4.to_device(m_T4), c4.to_device(v4), c4.to_device(vt4)
+        del m_T4, v4, vt4
+        h4 = V.solve_state(c4, dT4, dv4, nt)
+        dR4 = c4.empty(1)
+        V._lib.call("vr_memcpy_d2d", c4.handle, dR4.ptr, h4.field(nt), 8 * c4.N)
+        h4.free()
+        o4 = V.Objective(c4, dR4, dT4, model)
+        s4 = o4.evaluate(dv4)
+        o4.compute_gradient(s4)
+        out4 = c4.empty(3)
+        for _ in range(3):
+            o4.hessian_matvec(s4, dvt4, out=out4)
+        st4 = torch.cuda.ExternalStream(c4.stream, device=torch.device("cuda", dev))
+        k4 = max(3, min(args.steps, 20))
+        c4.synchronize()
+        e0.record(st4)
+        for _ in range(k4):
+            o4.hessian_matvec(s4, dvt4, out=out4)
+        e1.record(st4)
+        e1.synchronize()
+        ms4 = e0.elapsed_time(e1) / k4
+        b4, _ = bytes_model(n4, nt)
+        cfg4 = {"workload": f"config4 on one GPU: {n4}^3 ellipsoid phantom, band-limited v (|k|<=10, "
+                            "max disp 0.08*2pi), GN Hessian matvec at v", "grid": n4, "steps": k4,
+                "value": 1e3 / ms4, "unit": UNIT, "ms_per_step": ms4, "bytes_per_matvec": b4,
+                "achieved_GBps": b4 / (ms4 / 1e3) / 1e9, "frac_of_peak": b4 / (ms4 / 1e3) / 1e9 / peak}
+        s4.close()
+        o4.close()
+        c4.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -438,7 +485,8 @@ def main():
                 "e2e": e2e, "gpu_launches": launches, "roofline": roof, "matvec_roofline": matvec_roof,
                 "kernels": kernels, "kernel_profile": {"steps": k_prof, "ms_per_step": ms_prof / k_prof,
                                                         "note": "separate serialised pass, events per kernel"},
-                "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve}
+                "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve,
+                "config4_single_gpu": cfg4}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
