@@ -98,6 +98,14 @@ vr_ctx* ctx_new_sibling(vr_ctx* parent, int n1, int n2, int n3) {
     c->owns_stream = false;
     c->overlap = parent->overlap;
     c->fuse_acc = parent->fuse_acc;
+    c->parent = parent;
+    return c;
+}
+vr_ctx* ctx_sibling(vr_ctx* parent, int n1, int n2, int n3) {
+    for (vr_ctx* c : parent->siblings)
+        if (c->g.n1 == n1 && c->g.n2 == n2 && c->g.n3 == n3) return c;
+    vr_ctx* c = ctx_new_sibling(parent, n1, n2, n3);
+    parent->siblings.push_back(c);
     return c;
 }
 
@@ -283,6 +291,8 @@ int vr_ctx_destroy(vr_ctx* ctx) {
     return guard([&] {
         cudaSetDevice(ctx->device);
         if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        for (vr_ctx* c : ctx->siblings) vr_ctx_destroy(c);  // they share this stream
+        ctx->siblings.clear();
         vr::fft_plan_destroy(ctx);
         for (double* p : ctx->spec_scratch) cudaFree(p);
         for (double* p : ctx->field_scratch) cudaFree(p);
@@ -344,11 +354,12 @@ int vr_ctx_profile_read(vr_ctx* ctx, char* buf, size_t len) {
         for (const auto& r : ctx->prof) {
             float ms = 0.f;
             VR_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+            const std::string cat = (r.sibling ? "coarse_" : "") + std::string(r.cat);
             auto it = acc.begin();
             for (; it != acc.end(); ++it)
-                if (it->first == r.cat) break;
+                if (it->first == cat) break;
             if (it == acc.end()) {
-                acc.push_back({r.cat, Acc{}});
+                acc.push_back({cat, Acc{}});
                 it = acc.end() - 1;
             }
             it->second.n += 1;

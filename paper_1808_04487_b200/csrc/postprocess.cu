@@ -381,15 +381,11 @@ std::vector<GnResult> grid_continuation(vr_ctx* ctx, const double* mR, const dou
     const long long N = ctx->g.N;
     std::vector<vr_ctx*> lv(n_levels, nullptr);
     std::vector<GnResult> out;
-    auto cleanup = [&] {
-        for (int l = 0; l + 1 < n_levels; ++l)
-            if (lv[l]) vr_ctx_destroy(lv[l]);
-    };
-    try {
+    {
         lv[n_levels - 1] = ctx;
         for (int l = 0; l + 1 < n_levels; ++l) {
             const int s = n_levels - 1 - l;
-            lv[l] = ctx_new_sibling(ctx, d[0] >> s, d[1] >> s, d[2] >> s);
+            lv[l] = ctx_sibling(ctx, d[0] >> s, d[1] >> s, d[2] >> s);  // owned by ctx
         }
         // initial guess restricted to the coarsest level
         DevBuf v(lv[0], 3 * lv[0]->g.N);
@@ -424,11 +420,7 @@ std::vector<GnResult> grid_continuation(vr_ctx* ctx, const double* mR, const dou
             }
         }
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
-    } catch (...) {
-        cleanup();
-        throw;
     }
-    cleanup();
     return out;
 }
 

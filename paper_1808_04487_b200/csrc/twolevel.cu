@@ -417,8 +417,7 @@ vr_counters TwoLevel::counters() const {
 
 void TwoLevel::destroy_ctx() {
     release();
-    if (cctx) vr_ctx_destroy(cctx);
-    cctx = nullptr;
+    cctx = nullptr;  // the fine context owns its cached siblings
 }
 
 void TwoLevel::resample_vec(vr_ctx* src, const double* in, vr_ctx* dst, double* out) {
@@ -438,7 +437,7 @@ void TwoLevel::rebuild(vr_objective* fine_obj, const vr_state* fine_state, doubl
     if (full && !fine_state->lamhist)
         throw_logic("two-level rebuild: full Newton needs the fine adjoint history");
     if (cctx && cctx->stream != f->stream) destroy_ctx();  // a different fine context
-    if (!cctx) cctx = ctx_new_sibling(f, d[0] / 2, d[1] / 2, d[2] / 2);
+    if (!cctx) cctx = ctx_sibling(f, d[0] / 2, d[1] / 2, d[2] / 2);
     release();
     const long long Nc = cctx->g.N;
     const int nt = fine_state->nt;

@@ -143,7 +143,10 @@ struct vr_ctx {
     struct ProfRec {
         const char* cat;
         cudaEvent_t start, stop;
+        bool sibling;  // launched by a sibling context (reported as coarse_<cat>)
     };
+    vr_ctx* parent = nullptr;  // sibling contexts: launches are profiled by the parent
+    std::vector<vr_ctx*> siblings;  // cached siblings (other grids on this stream), owned
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -159,6 +162,9 @@ constexpr int kRedThreads = 256;
 vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo);
 // a one-GPU context of another grid on parent's device that runs on parent's stream
 vr_ctx* ctx_new_sibling(vr_ctx* parent, int n1, int n2, int n3);
+// the parent's cached sibling of that grid (created on first use, destroyed with the
+// parent): repeated solves do not pay for context / plan / scratch setup again
+vr_ctx* ctx_sibling(vr_ctx* parent, int n1, int n2, int n3);
 void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& g);
 int halo_required(double vmax_x1, int nt, int n1);
 void set_last_error(int cls, const std::string& msg);  // the C ABI's vr_last_error slot
@@ -167,18 +173,22 @@ double* field_buf(vr_ctx* ctx, int i);  // N doubles
 inline void count_launch(vr_ctx* ctx, int n = 1) { ctx->launches += n; }
 inline void check_launch() { VR_CUDA(cudaGetLastError()); }
 cudaEvent_t prof_event(vr_ctx* ctx);
+// the context that owns the profile (a sibling shares its parent's stream)
+inline vr_ctx* prof_owner(vr_ctx* ctx) { return ctx->parent ? ctx->parent : ctx; }
 inline cudaEvent_t prof_begin(vr_ctx* ctx) {
-    if (!ctx->profiling) return nullptr;
-    cudaEvent_t e = prof_event(ctx);
+    vr_ctx* p = prof_owner(ctx);
+    if (!p->profiling) return nullptr;
+    cudaEvent_t e = prof_event(p);
     VR_CUDA(cudaEventRecord(e, ctx->stream));
     return e;
 }
 inline void prof_end(vr_ctx* ctx, const char* cat, cudaEvent_t start) {
     ctx->launches += 1;
     if (!start) return;
-    cudaEvent_t e = prof_event(ctx);
+    vr_ctx* p = prof_owner(ctx);
+    cudaEvent_t e = prof_event(p);
     VR_CUDA(cudaEventRecord(e, ctx->stream));
-    ctx->prof.push_back({cat, start, e});
+    p->prof.push_back({cat, start, e, p != ctx});
 }
 // Launch a kernel on ctx's stream, check it, count it, and (when profiling)
 // bracket it with CUDA events under category CAT.

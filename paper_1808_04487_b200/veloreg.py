@@ -584,7 +584,8 @@ def gauss_newton_solve(ctx, m_R, m_T, v0, model=None, params=None, precond="spec
     else:
         _lib.call("vr_gauss_newton_solve", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
                   C.byref(params), pc, vout.ptr, C.byref(rep), recs, max_records)
-    return SolveResult(vout.numpy(), _report_dict(rep), _records(recs, min(rep.n_records, max_records)))
+    return SolveResult(_ret(vout, _is_host(m_R, m_T, v0)), _report_dict(rep),
+                       _records(recs, min(rep.n_records, max_records)))
 
 
 # ---- two-level preconditioner and grid transfer (precond.hpp, spectral.cpp:228-385) ----
@@ -695,7 +696,7 @@ def parameter_continuation(ctx, m_R, m_T, v0, model=None, params=None, precond="
               C.byref(params), pc, vout.ptr, reps, max_levels, C.byref(nl), recs, max_records)
     reports = [_report_dict(reps[i]) for i in range(min(nl.value, max_levels))]
     nrec = sum(r["n_records"] for r in reports)
-    return vout.numpy(), reports, _records(recs, min(nrec, max_records))
+    return _ret(vout, _is_host(m_R, m_T, v0)), reports, _records(recs, min(nrec, max_records))
 
 
 def _levels(ctx, fn, args, max_levels, max_records):

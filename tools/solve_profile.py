@@ -24,13 +24,16 @@ def main():
     d_mR = ctx.to_device(np.asarray(V.solve_state(ctx, m_T, v, 4))[4])
     model = V.make_model("h2", beta_v=1e-2, nt=4)
     params = V.make_params(eps_opt=1e-2)
-    for pc in ("spectral", "two_level", "spectral", "two_level"):
-        for prof in (False, True):
+    d_v0 = ctx.to_device(np.zeros((3, n, n, n)))
+    plan = [(pc, prof) for pc in ("spectral", "two_level", "spectral", "two_level") for prof in (False, True)]
+    if os.environ.get("REPEAT"):
+        plan = [("spectral", False)] * int(os.environ["REPEAT"])
+    for pc, prof in plan:
+        if True:
             ctx.synchronize()
             ctx.set_profiling(prof)
             t0 = time.perf_counter()
-            _, reps, recs = V.parameter_continuation(ctx, d_mR, d_mT, np.zeros((3, n, n, n)), model, params,
-                                                     precond=pc)
+            _, reps, recs = V.parameter_continuation(ctx, d_mR, d_mT, d_v0, model, params, precond=pc)
             ctx.synchronize()
             wall = time.perf_counter() - t0
             out = {"precond": pc, "profiling": prof, "wall_s": wall,
