@@ -302,6 +302,14 @@ int vr_hessian_matvec(vr_objective* obj, const vr_state* s, const double* vt3, d
 /* same, HOST buffers in and out (H2D + matvec + D2H): the end-to-end entry */
 int vr_hessian_matvec_host(vr_objective* obj, const vr_state* s, const double* vt3_host,
                            double* out3_host);
+/* pipelined form of vr_hessian_matvec_host for a stream of independent directions:
+ * returns once the work is queued; uploads (own stream), the matvec (ctx stream) and
+ * downloads (own stream) of consecutive calls overlap through two device slots. Host
+ * buffers (pinned for real overlap) must stay valid and vt3_host unmodified until
+ * vr_objective_wait returns; non-finite directions surface there as NumericError. */
+int vr_hessian_matvec_host_async(vr_objective* obj, const vr_state* s, const double* vt3_host,
+                                 double* out3_host);
+int vr_objective_wait(vr_objective* obj);
 /* hessian_data_matvec (objective.cpp:123-156) */
 int vr_hessian_data_matvec(vr_objective* obj, const vr_state* s, const double* vt3, double* out3);
 /* apply_reg / apply_K (objective.cpp:178-186) */

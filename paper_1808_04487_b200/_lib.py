@@ -222,6 +222,8 @@ SIGNATURES = {
     "vr_hessian_matvec": (I, [P, P, DP, DP]),
     "vr_hessian_matvec_host": (I, [P, P, HP, HP]),
     "vr_hessian_data_matvec": (I, [P, P, DP, DP]),
+    "vr_hessian_matvec_host_async": (I, [P, P, HP, HP]),
+    "vr_objective_wait": (I, [P]),
     "vr_objective_apply_reg": (I, [P, DP, I, DP]),
     "vr_objective_apply_K": (I, [P, DP, DP]),
     "vr_compute_forcing": (I, [D, D, C.POINTER(D)]),

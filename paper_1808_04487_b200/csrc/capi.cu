@@ -869,6 +869,21 @@ int vr_hessian_matvec_host(vr_objective* obj, const vr_state* s, const double* v
         vr::dev_free(ctx, out);
     });
 }
+int vr_hessian_matvec_host_async(vr_objective* obj, const vr_state* s, const double* vt3_host,
+                                 double* out3_host) {
+    return guard([&] {
+        need(obj && s && vt3_host && out3_host, "vr_hessian_matvec_host_async");
+        set_dev(obj->ctx);
+        vr::objective_matvec_host_async(obj, s, vt3_host, out3_host);
+    });
+}
+int vr_objective_wait(vr_objective* obj) {
+    return guard([&] {
+        need(obj, "vr_objective_wait");
+        set_dev(obj->ctx);
+        vr::objective_pipe_wait(obj);
+    });
+}
 int vr_objective_apply_reg(vr_objective* obj, const double* u3, int mode, double* out3) {
     return guard([&] {
         need(obj && u3 && out3, "vr_objective_apply_reg");

@@ -23,6 +23,19 @@ vr_state::~vr_state() {
 vr_objective::~vr_objective() {
     if (!ctx) return;
     for (double* p : {ws_lam, ws_tmp, ws_div, ws_b}) vr::dev_free(ctx, p);
+    if (pipe.h2d) {
+        cudaStreamSynchronize(pipe.h2d);
+        cudaStreamSynchronize(pipe.d2h);
+        for (int q = 0; q < 2; ++q) {
+            vr::dev_free(ctx, pipe.vt[q]);
+            vr::dev_free(ctx, pipe.out[q]);
+            cudaEventDestroy(pipe.up[q]);
+            cudaEventDestroy(pipe.done[q]);
+            cudaEventDestroy(pipe.down[q]);
+        }
+        cudaStreamDestroy(pipe.h2d);
+        cudaStreamDestroy(pipe.d2h);
+    }
 }
 
 namespace vr {
@@ -323,7 +336,7 @@ void objective_gradient(vr_objective* o, vr_state* s) {
 
 // hessian_data_matvec (objective.cpp:123-156) [+ beta_v A vt, objective.cpp:114-121]
 void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, double* out3,
-                      bool add_reg, const double* reg_given) {
+                      bool add_reg, const double* reg_given, bool check) {
     vr_ctx* ctx = o->ctx;
     const long long N = ctx->g.N;
     if (!s->has_adjoint_ctx)
@@ -332,7 +345,7 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     const int nt = s->nt;
     const double dt = 1.0 / nt;
     const double hdt = 0.5 / nt;
-    VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
+    if (check) VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
     // beta_v A vt depends only on vt: its FFT passes (HBM-bound) run on the side
     // stream under the L1-bound transport sweeps; only the c2r + add waits for b
     if (add_reg)
@@ -444,7 +457,58 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
         }
     }
     o->counters.hessian_matvecs += 1;
-    check_flags(ctx, "hessian_matvec");
+    if (check) check_flags(ctx, "hessian_matvec");
+}
+
+void objective_matvec_host_async(vr_objective* o, const vr_state* s, const double* vt3_host,
+                                 double* out3_host) {
+    vr_ctx* ctx = o->ctx;
+    if (ctx->dist) throw_argument("hessian_matvec_host_async: one GPU only");
+    if (!s->has_adjoint_ctx)
+        throw_logic("hessian_matvec: evaluation context is missing the adjoint sweep data "
+                    "(compute the gradient first)");
+    auto& P = o->pipe;
+    const long long n3 = 3 * ctx->g.N;
+    const size_t bytes = sizeof(double) * n3;
+    if (!P.h2d) {
+        VR_CUDA(cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking));
+        VR_CUDA(cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking));
+        for (int q = 0; q < 2; ++q) {
+            P.vt[q] = dev_alloc(ctx, n3);
+            P.out[q] = dev_alloc(ctx, n3);
+            VR_CUDA(cudaEventCreateWithFlags(&P.up[q], cudaEventDisableTiming));
+            VR_CUDA(cudaEventCreateWithFlags(&P.done[q], cudaEventDisableTiming));
+            VR_CUDA(cudaEventCreateWithFlags(&P.down[q], cudaEventDisableTiming));
+        }
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));  // slots allocated on the compute stream
+    }
+    if (P.issued == 0) VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
+    const int q = static_cast<int>(P.issued & 1);
+    // upload once the compute two calls back has finished reading this slot
+    VR_CUDA(cudaStreamWaitEvent(P.h2d, P.done[q], 0));
+    VR_CUDA(cudaMemcpyAsync(P.vt[q], vt3_host, bytes, cudaMemcpyHostToDevice, P.h2d));
+    VR_CUDA(cudaEventRecord(P.up[q], P.h2d));
+    // compute once uploaded and once the previous download of this slot's result is done
+    VR_CUDA(cudaStreamWaitEvent(ctx->stream, P.up[q], 0));
+    VR_CUDA(cudaStreamWaitEvent(ctx->stream, P.down[q], 0));
+    objective_matvec(o, s, P.vt[q], P.out[q], true, nullptr, false);
+    VR_CUDA(cudaEventRecord(P.done[q], ctx->stream));
+    VR_CUDA(cudaStreamWaitEvent(P.d2h, P.done[q], 0));
+    VR_CUDA(cudaMemcpyAsync(out3_host, P.out[q], bytes, cudaMemcpyDeviceToHost, P.d2h));
+    VR_CUDA(cudaEventRecord(P.down[q], P.d2h));
+    P.issued += 1;
+}
+
+void objective_pipe_wait(vr_objective* o) {
+    vr_ctx* ctx = o->ctx;
+    auto& P = o->pipe;
+    if (P.h2d) {
+        VR_CUDA(cudaStreamSynchronize(P.h2d));
+        VR_CUDA(cudaStreamSynchronize(P.d2h));
+    }
+    const bool any = P.issued > 0;
+    P.issued = 0;
+    if (any) check_flags(ctx, "hessian_matvec_host_async");
 }
 
 void objective_apply_reg(vr_objective* o, const double* u3, int mode, double* out3) {

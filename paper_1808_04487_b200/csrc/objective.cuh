@@ -40,6 +40,16 @@ struct vr_objective {
     double* ws_tmp = nullptr;  // 2 halo-padded fields
     double* ws_div = nullptr;  // 1 halo-padded field (div v, gathered by the factor)
     double* ws_b = nullptr;    // 3N
+    // pipelined host-buffer matvecs (vr_hessian_matvec_host_async): two device slots;
+    // H2D and D2H on their own streams so step k+1's upload and step k's download
+    // overlap step k / k+1 compute on the context's stream
+    struct Pipe {
+        double* vt[2] = {nullptr, nullptr};
+        double* out[2] = {nullptr, nullptr};
+        cudaStream_t h2d = nullptr, d2h = nullptr;
+        cudaEvent_t up[2] = {}, done[2] = {}, down[2] = {};
+        long long issued = 0;  // calls since the last wait
+    } pipe;
     ~vr_objective();
 };
 
@@ -62,7 +72,12 @@ void objective_gradient(vr_objective* o, vr_state* s);
 // H vt (add_reg) or H_data vt; reg_given (may be null, add_reg false): a field
 // equal to beta_v A vt computed elsewhere, added instead of the spectral term
 void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, double* out3,
-                      bool add_reg, const double* reg_given = nullptr);
+                      bool add_reg, const double* reg_given = nullptr, bool check = true);
+// pipelined H vt with host buffers (see vr_objective::Pipe); errors of the batch
+// (non-finite directions) surface in objective_pipe_wait
+void objective_matvec_host_async(vr_objective* o, const vr_state* s, const double* vt3_host,
+                                 double* out3_host);
+void objective_pipe_wait(vr_objective* o);
 // PCG on the GN Hessian with the spectral preconditioner (solver.cpp:51-100),
 // carrying u = beta_v A s through the recurrence (see objective.cu)
 vr_pcg_stats pcg_solve_gn(vr_objective* o, const vr_state* s, const double* rhs, double rel_tol,

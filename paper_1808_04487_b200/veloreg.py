@@ -497,6 +497,16 @@ class Objective:
         _lib.call("vr_hessian_matvec_host", self._h, state._h, vt_host.ctypes.data, out_host.ctypes.data)
         return out_host
 
+    def hessian_matvec_host_async(self, state: EvalState, vt_host: np.ndarray, out_host: np.ndarray):
+        """Pipelined host-buffer matvec (vr_hessian_matvec_host_async); results are valid
+        after wait(). Keep both arrays alive and vt_host unchanged until then."""
+        _lib.call("vr_hessian_matvec_host_async", self._h, state._h, vt_host.ctypes.data,
+                  out_host.ctypes.data)
+        return out_host
+
+    def wait(self):
+        _lib.call("vr_objective_wait", self._h)
+
     def apply_reg(self, u, mode="apply"):
         du = _dev(self.ctx, u)
         o = self.ctx.empty(3)

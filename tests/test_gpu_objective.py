@@ -139,3 +139,28 @@ def test_matvec_host_entry(vr, ref, ctx):
     rs = ro.evaluate(vs)
     ro.compute_gradient(rs)
     assert rel_l2(out, ro.hessian_matvec(rs, vt)) < TOL
+
+
+def test_matvec_host_async_pipeline(vr, ref, ctx):
+    # vr_hessian_matvec_host_async: a stream of independent directions through two
+    # device slots equals the synchronous call for each of them, bit for bit
+    dims = (32, 32, 32)
+    c = ctx(dims)
+    mR, mT, vs = ref.generate_synthetic(dims, 4)
+    o = vr.Objective(c, mR, mT, vr.make_model())
+    s = o.evaluate(0.5 * vs)
+    o.compute_gradient(s)
+    dirs = [ref.random_smooth_vector(dims, 2, 300 + k, 1.0) for k in range(5)]
+    outs = [np.empty_like(d) for d in dirs]
+    for d, out in zip(dirs, outs):
+        o.hessian_matvec_host_async(s, d, out)
+    o.wait()
+    for d, out in zip(dirs, outs):
+        assert np.array_equal(out, o.hessian_matvec(s, d))
+    bad = dirs[0].copy()
+    bad[0, 1, 2, 3] = np.nan
+    o.hessian_matvec_host_async(s, dirs[1], outs[1])
+    o.hessian_matvec_host_async(s, bad, outs[0])
+    with pytest.raises(vr.NumericError):
+        o.wait()
+    o.wait()  # nothing in flight: no error
