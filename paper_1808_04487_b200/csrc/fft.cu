@@ -285,6 +285,9 @@ struct AxisCfg {
 // one is transformed; the last butterfly stage stores straight to HBM).
 // MODE 0: transform in direction DIR (src may equal dst)
 // MODE 1: forward -> multiplier -> inverse (x1 pass only), src -> dst (may alias)
+// MODE 2: forward -> i deriv_freq(k) * m.beta -> inverse along this axis: the spectral
+//         derivative of a REAL field viewed as complex pairs (x3 = 2j, 2j+1 as re, im);
+//         i k (Nyquist 0) maps real lines to real lines, so the pair never mixes
 template <int N, int DIR, int MODE>
 __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
     k_fft_axis(const double2* src, double2* dst, long long inner, long long outer,
@@ -328,6 +331,17 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
         };
         if constexpr (MODE == 0) {
             fft_line<N, DIR, true, false>(t, tw, load_sm, store, sm);
+        } else if constexpr (MODE == 2) {
+            auto store_sm = [&](int i, double2 v) { sm(i) = v; };
+            fft_line<N, -1, true, true>(t, tw, load_sm, store_sm, sm);
+            __syncthreads();
+#pragma unroll 1
+            for (int i = t; i < N; i += C::T) {
+                const double2 c = cmul(make_double2(0.0, (double)deriv_freq(i, N)), sm(i));
+                sm(i) = make_double2(c.x * m.beta, c.y * m.beta);
+            }
+            __syncthreads();
+            fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
         } else {
             // x1 pass: column cc = i2 * nh + i3
             const int i2 = static_cast<int>(cc / g.nh) + g.k2_off;  // k2-slab on x1 slabs
@@ -548,6 +562,13 @@ __device__ __forceinline__ void bin_coords(long long b, const GridDims& g, int& 
     i1 = static_cast<int>(r / g.n2s);
 }
 
+// x3 derivative on the row spectrum [rows][nh]: c *= i deriv_freq(k3)
+__global__ void k_rows_deriv(double2* __restrict__ spec, long long nbins, int nh, int n3) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nbins;
+         b += (long long)gridDim.x * blockDim.x)
+        spec[b] = cmul(make_double2(0.0, (double)deriv_freq(static_cast<int>(b % nh), n3)), spec[b]);
+}
+
 // divergence (spectral.cpp:124-140): acc = sum_a i k_a c_a, deriv_freq
 __global__ void k_spec_div(const double2* __restrict__ c0, const double2* __restrict__ c1,
                            const double2* __restrict__ c2, double2* __restrict__ out, GridDims g) {
@@ -629,7 +650,7 @@ void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inne
     const long long ntiles = (inner + C::TB - 1) / C::TB * outer;
     const unsigned grid =
         persistent_grid(ctx, k_fft_axis<N, DIR, MODE>, C::THREADS, C::SMEM, ntiles, occ);
-    VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : "fft_x1_mult",
+    VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : (MODE == 1 ? "fft_x1_mult" : "fft_deriv"),
               k_fft_axis<N, DIR, MODE><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
                   src, dst, inner, outer, outer_stride, tw, m, ctx->g));
 }
@@ -760,6 +781,31 @@ void pass_x1(vr_ctx* ctx, const double* src, double* dst, int dir, const MultPar
         launch_axis<-1, 0>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, none);
     else
         launch_axis<+1, 0>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, none);
+}
+// d f / d x_axis of a real field on one GPU, one axis only: the derivative is a
+// 1D spectral operator along that axis (the other axes' transforms cancel), so x1
+// and x2 are one fused pass over f viewed as complex pairs and x3 is a row
+// r2c -> i k3 -> c2r round trip (spec: scratch of NC complex)
+void deriv_axis(vr_ctx* ctx, int axis, const double* f, double* out, double* spec) {
+    const GridDims& g = ctx->g;
+    const auto* s = reinterpret_cast<const double2*>(f);
+    auto* d = reinterpret_cast<double2*>(out);
+    const long long h3 = g.n3 / 2;
+    MultDev m{};
+    if (axis == 0) {
+        m.beta = 1.0 / g.n1;
+        launch_axis<-1, 2>(ctx, g.n1, s, d, static_cast<long long>(g.n2) * h3, 1, 0, ctx->fft->tw1, m);
+    } else if (axis == 1) {
+        m.beta = 1.0 / g.n2;
+        launch_axis<-1, 2>(ctx, g.n2, s, d, h3, g.L, static_cast<long long>(g.n2) * h3, ctx->fft->tw2,
+                           m);
+    } else {
+        launch_rows(ctx, true, f, spec, 1.0, nullptr);
+        const long long nb = static_cast<long long>(g.L) * g.n2 * g.nh;
+        VR_LAUNCH(ctx, "fft_spectral", k_rows_deriv<<<spec_grid(g), 256, 0, ctx->stream>>>(
+            reinterpret_cast<double2*>(spec), nb, g.nh, g.n3));
+        launch_rows(ctx, false, spec, out, 1.0 / g.n3, nullptr);
+    }
 }
 void pass_spec_div(vr_ctx* ctx, const double* s0, const double* s1, const double* s2, double* acc) {
     const GridDims& g = ctx->g;

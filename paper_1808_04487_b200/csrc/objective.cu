@@ -6,6 +6,8 @@
 // weighted inner product for the Armijo slope, squared-norm relative stop);
 // every vector it touches stays in HBM and only scalars cross to the host.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 
@@ -753,6 +755,17 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
     }
     auto coarse = [&] { return tl ? tl->counters() : vr_counters{}; };
     const auto t0 = std::chrono::steady_clock::now();
+    // VR_TIMING=1: host wall time per phase (stream drained at each boundary) on stderr
+    static const bool timing = std::getenv("VR_TIMING") != nullptr;
+    double ph[5] = {0, 0, 0, 0, 0};  // setup, pcg, line search, gradient, other
+    auto tp = std::chrono::steady_clock::now();
+    auto mark = [&](int phase) {
+        if (!timing) return;
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        const auto now = std::chrono::steady_clock::now();
+        ph[phase] += std::chrono::duration<double>(now - tp).count();
+        tp = now;
+    };
     auto elapsed = [&] {
         return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     };
@@ -774,6 +787,7 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
         state = objective_evaluate(obj, v0);
         objective_gradient(obj, state);
         const double g0 = norm_l2_vec(ctx, state->grad);
+        mark(0);
         rep.grad0 = g0;
         res.records.push_back(make_record(0, state, g0, g0, obj->counters, coarse(), elapsed()));
         if (g0 == 0.0) {
@@ -801,6 +815,7 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                     rep.stop = VR_STOP_MAX_ITERATIONS;
                     break;
                 }
+                mark(4);
                 const double eps_H = std::min(0.5, std::sqrt(gk / g0));  // compute_forcing
                 const vr_state* cs = state;
                 DevOp op = [&](const double* u, double* out) {
@@ -831,6 +846,7 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                               : pcg_solve(ctx, op, rhs, eps_H, params.max_krylov, pc, dir);
                 }
 
+                mark(1);
                 const double slope = inner_product_vec(ctx, state->grad, dir);
                 if (slope >= 0.0) {
                     rep.stop = VR_STOP_LINE_SEARCH_FAILURE;
@@ -841,10 +857,12 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                     rep.stop = VR_STOP_LINE_SEARCH_FAILURE;
                     break;
                 }
+                mark(2);
                 delete state;
                 state = ls.state;
                 objective_gradient(obj, state);
                 gk = norm_l2_vec(ctx, state->grad);
+                mark(3);
                 ++k;
                 vr_iteration_record row =
                     make_record(k, state, gk, g0, obj->counters, coarse(), elapsed());
@@ -866,6 +884,10 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
                                 ctx->stream));
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
         rep.wall_time_s = elapsed();
+        if (timing)
+            std::fprintf(stderr, "VR_TIMING gn_solve %.1f ms: setup %.1f pcg %.1f linesearch %.1f gradient %.1f other %.1f (%d iterations)\n",
+                         1e3 * rep.wall_time_s, 1e3 * ph[0], 1e3 * ph[1], 1e3 * ph[2], 1e3 * ph[3], 1e3 * ph[4],
+                         rep.outer_iterations);
     } catch (...) {
         cleanup();
         throw;

@@ -14,6 +14,8 @@ namespace vr {
 namespace {
 
 double* sbuf(vr_ctx* ctx, int i) { return spec_buf(ctx, i); }
+// the one-axis derivative passes move 16-byte pairs with cp.async
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // doubles in one complex row block [n2s][nh]
 size_t row_block(const GridDims& g) { return static_cast<size_t>(g.n2s) * g.nh * 2; }
@@ -108,6 +110,11 @@ void spectral_scalar_op(vr_ctx* ctx, const double* in, double* out, const MultPa
 
 void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
     const GridDims& g = ctx->g;
+    if (!ctx->dist && aligned16(f) && aligned16(out3)) {  // d_a f needs only transforms along a
+        // (gradient, spectral.cpp:108-122)
+        for (int a = 0; a < 3; ++a) deriv_axis(ctx, a, f, out3 + a * g.N, sbuf(ctx, 0));
+        return;
+    }
     double* s0 = sbuf(ctx, 0);
     double* s1 = sbuf(ctx, 1);
     pass_rows_forward(ctx, f, s0);
@@ -133,6 +140,16 @@ void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
 
 void op_divergence(vr_ctx* ctx, const double* v3, double* out) {
     const GridDims& g = ctx->g;
+    if (!ctx->dist && aligned16(v3) && aligned16(out)) {  // sum_a d_a v_a with one-axis
+        // derivatives (divergence, spectral.cpp:124-140)
+        double* t = field_buf(ctx, 9);
+        deriv_axis(ctx, 0, v3, t, sbuf(ctx, 0));
+        deriv_axis(ctx, 1, v3 + g.N, out, sbuf(ctx, 0));
+        add_scaled(ctx, out, 1.0, t, g.N);
+        deriv_axis(ctx, 2, v3 + 2 * g.N, t, sbuf(ctx, 0));
+        add_scaled(ctx, out, 1.0, t, g.N);
+        return;
+    }
     double* s[3];
     for (int a = 0; a < 3; ++a) {
         s[a] = sbuf(ctx, a);
