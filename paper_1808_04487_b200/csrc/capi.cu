@@ -836,6 +836,7 @@ int vr_hessian_matvec(vr_objective* obj, const vr_state* s, const double* vt3, d
     return guard([&] {
         need(obj && s && vt3 && out3, "vr_hessian_matvec");
         set_dev(obj->ctx);
+        if (obj->pipe.issued) vr::objective_pipe_wait(obj);  // drain pipelined calls first
         vr::objective_matvec(obj, s, vt3, out3, true);
     });
 }

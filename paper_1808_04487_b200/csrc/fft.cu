@@ -562,6 +562,33 @@ __device__ __forceinline__ void bin_coords(long long b, const GridDims& g, int& 
     i1 = static_cast<int>(r / g.n2s);
 }
 
+// <A v_c, v_c> per component by Parseval on the half spectrum (fft_freq symbol, bins with
+// 0 < k3 < n3/2 stand for their conjugate partner too); per-block partials, fixed grid
+__global__ void __launch_bounds__(kRedThreads)
+    k_reg_energy(const double2* __restrict__ s0, const double2* __restrict__ s1,
+                 const double2* __restrict__ s2, MultDev m, GridDims g, double* __restrict__ partials) {
+    const double2* sp = blockIdx.y == 0 ? s0 : (blockIdx.y == 1 ? s1 : s2);
+    double acc = 0.0;
+    for (long long b = blockIdx.x * (long long)kRedThreads + threadIdx.x; b < g.NC;
+         b += (long long)gridDim.x * kRedThreads) {
+        int i1, i2, i3;
+        bin_coords(b, g, i1, i2, i3);
+        const double a = fft_freq(i1, g.n1), c = fft_freq(i2, g.n2), d = fft_freq(i3, g.n3);
+        const double w = (i3 == 0 || 2 * i3 == g.n3) ? 1.0 : 2.0;
+        const double2 v = sp[b];
+        acc += w * symbol_dev(m, a * a + c * c + d * d) * (v.x * v.x + v.y * v.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    __shared__ double sh[kRedThreads / 32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = sh[0];
+        for (int q = 1; q < kRedThreads / 32; ++q) t += sh[q];
+        partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
 // x3 derivative on the row spectrum [rows][nh]: c *= i deriv_freq(k3)
 __global__ void k_rows_deriv(double2* __restrict__ spec, long long nbins, int nh, int n3) {
     for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nbins;
@@ -806,6 +833,27 @@ void deriv_axis(vr_ctx* ctx, int axis, const double* f, double* out, double* spe
             reinterpret_cast<double2*>(spec), nb, g.nh, g.n3));
         launch_rows(ctx, false, spec, out, 1.0 / g.n3, nullptr);
     }
+}
+// <A v, v>_h = h1 h2 h3 sum_c sum_x (A v_c) v_c (A at beta = 1, apply mode) by Parseval:
+// three forward transforms and a spectrum reduction instead of three transform round
+// trips and a real-space inner product (one GPU)
+double reg_energy(vr_ctx* ctx, const double* v3, const vr_regnorm& norm) {
+    const GridDims& g = ctx->g;
+    double* sp[3];
+    for (int c = 0; c < 3; ++c) {
+        sp[c] = spec_buf(ctx, 1 + c);
+        fft_r2c(ctx, v3 + c * g.N, sp[c]);
+    }
+    MultDev m{};
+    m.reg_kind = norm.kind;
+    m.gamma = norm.gamma;
+    m.helm_sq = norm.helmholtz_squared;
+    VR_LAUNCH(ctx, "reduce", k_reg_energy<<<dim3(kRedBlocks, 3), kRedThreads, 0, ctx->stream>>>(
+        reinterpret_cast<const double2*>(sp[0]), reinterpret_cast<const double2*>(sp[1]),
+        reinterpret_cast<const double2*>(sp[2]), m, g, ctx->red_partials));
+    double part[3];
+    finalize_sums(ctx, kRedBlocks, 3, part);
+    return (part[0] + part[1] + part[2]) / static_cast<double>(g.Ng) * (g.h1 * g.h2 * g.h3);
 }
 void pass_spec_div(vr_ctx* ctx, const double* s0, const double* s1, const double* s2, double* acc) {
     const GridDims& g = ctx->g;

@@ -211,10 +211,16 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
         s->mismatch = sum_sq_diff(ctx, pslice(ctx, s->mhist, nt), o->mR, N) * cell_volume(g);
         s->mismatch_rel = o->initial_mismatch > 0.0 ? s->mismatch / o->initial_mismatch : 0.0;
 
-        // reg = 1/2 beta_v <A v, v>_h with A applied at beta = 1 (objective.cpp:63-64)
-        double* Av = o->ws_b;
-        op_reg(ctx, v3, Av, o->model.norm, VR_REGOP_APPLY, 1.0);
-        const double reg = 0.5 * o->model.beta_v * inner_product_vec(ctx, Av, v3);
+        // reg = 1/2 beta_v <A v, v>_h with A applied at beta = 1 (objective.cpp:63-64);
+        // on one GPU by Parseval on the forward spectra (no inverse transforms)
+        double reg;
+        if (!ctx->dist) {
+            reg = 0.5 * o->model.beta_v * reg_energy(ctx, v3, o->model.norm);
+        } else {
+            double* Av = o->ws_b;
+            op_reg(ctx, v3, Av, o->model.norm, VR_REGOP_APPLY, 1.0);
+            reg = 0.5 * o->model.beta_v * inner_product_vec(ctx, Av, v3);
+        }
         double penalty = 0.0;
         if (o->model.norm.div_penalty) {
             double* w = pslice(ctx, o->ws_tmp, 0);

@@ -260,6 +260,8 @@ void pass_rows_inverse(vr_ctx* ctx, const double* spec, double* out, double scal
 void pass_x2(vr_ctx* ctx, double* spec, int dir);
 void pass_x1(vr_ctx* ctx, const double* src, double* dst, int dir, const MultParams* mult);
 void pass_spec_div(vr_ctx* ctx, const double* s0, const double* s1, const double* s2, double* acc);
+// <A v, v>_h at beta = 1 by Parseval (one GPU)
+double reg_energy(vr_ctx* ctx, const double* v3, const vr_regnorm& norm);
 // one-GPU spectral derivative along one axis (1D transforms only); spec: NC-complex scratch
 void deriv_axis(vr_ctx* ctx, int axis, const double* f, double* out, double* spec);
 void pass_spec_project(vr_ctx* ctx, double* s0, double* s1, double* s2, int kind, double beta_v,
