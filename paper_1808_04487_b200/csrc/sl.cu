@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(kThreads)
     if (i >= g.N) return;
     const double l = 1.0 * mR[i] + (-1.0) * mfin[i];
     lam[i] = l;
+    if (!b) return;  // the observer term is accumulated later (sl_accumulate)
     const double wl = w * l;
 #pragma unroll
     for (int a = 0; a < 3; ++a) b[a * g.N + i] = 0.0 + wl * gm[a * g.N + i];
