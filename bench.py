@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=90.0,
                     help="wall budget for the reference arm's timed matvecs")
     ap.add_argument("--no-solve", action="store_true", help="skip the GN solve timings")
+    ap.add_argument("--no-config2", action="store_true",
+                    help="skip the 128^3 (config 2) per-operator micro-benchmarks and solve")
     ap.add_argument("--no-config4", action="store_true",
                     help="skip the 512^3 (config 4, one GPU) matvec throughput")
     return ap.parse_args()
@@ -176,6 +178,96 @@ def run_reference_matvecs(m_R, m_T, v, vt, nt, steps, warmup, budget_s):
     total = sum(times)
     return {"value": len(times) / total, "steps": len(times), "seconds": total, "cores": cores,
             "setup_s": setup}
+
+
+def config2_block(vr, V, dev, nt, model, torch, with_cpu=True):
+    """BASELINE config 2: 128^3 section-4.2 problem. Per-operator GPU times (20 launches after
+    3 warm-ups, CUDA events on the library stream, outputs preallocated) with algorithmic
+    bytes, the reference's time for the same operator on the host cores, and the GN solve."""
+    n = 128
+    N = n ** 3
+    F, Fc = 8.0 * N, 16.0 * n * n * (n // 2 + 1)
+    c = vr.Context(n, device=dev)
+    mR, mT, vs = V.generate_synthetic(c, nt)
+    d_v, d_mT = c.to_device(vs), c.to_device(mT)
+    d_f = c.to_device(mT)
+    spec = c.empty(1, complex_spectrum=True)
+    o1, o3, x = c.empty(1), c.empty(3), c.empty(3)
+    L = V._lib
+    L.call("vr_trace_characteristics", c.handle, d_v.ptr, nt, 0, x.ptr)  # RK2 departure points of v*
+    ops = {
+        "fft_r2c": (lambda: L.call("vr_fft_r2c", c.handle, d_f.ptr, spec.ptr), F + Fc),
+        "fft_c2r": (lambda: L.call("vr_fft_c2r", c.handle, spec.ptr, o1.ptr), Fc + F),
+        "gradient": (lambda: L.call("vr_gradient", c.handle, d_f.ptr, o3.ptr), 4 * F),
+        "divergence": (lambda: L.call("vr_divergence", c.handle, d_v.ptr, o1.ptr), 4 * F),
+        "leray": (lambda: L.call("vr_apply_projection", c.handle, d_v.ptr, o3.ptr, 1, 0.0, 0.0), 6 * F),
+        "tricubic_3_fields": (lambda: L.call("vr_tricubic_interpolate", c.handle, d_v.ptr, x.ptr, o3.ptr, 3),
+                              9 * F),
+        "tricubic_1_field": (lambda: L.call("vr_tricubic_interpolate", c.handle, d_mT.ptr, x.ptr, o1.ptr, 1),
+                             5 * F),
+    }
+    st = torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", dev))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {}
+    for name, (fn, nbytes) in ops.items():
+        for _ in range(3):
+            fn()
+        c.synchronize()
+        e0.record(st)
+        for _ in range(20):
+            fn()
+        e1.record(st)
+        e1.synchronize()
+        us = e0.elapsed_time(e1) / 20 * 1e3
+        res[name] = {"gpu_us": us, "bytes": nbytes, "gpu_GBps": nbytes / (us * 1e-6) / 1e9}
+    params = V.make_params(eps_opt=1e-2)
+    d_mR = c.to_device(mR)
+    d_v0 = c.to_device(np.zeros((3, n, n, n)))
+    t_runs = []
+    for _ in range(2):
+        c.synchronize()
+        t0 = time.perf_counter()
+        r = V.gauss_newton_solve(c, d_mR, d_mT, d_v0, model, params)
+        c.synchronize()
+        t_runs.append(time.perf_counter() - t0)
+    solve = {"gpu_seconds": t_runs[-1], "gpu_seconds_first_run": t_runs[0],
+             "newton_iterations": r.report["outer_iterations"],
+             "hessian_matvecs": r.report["fine"]["hessian_matvecs"],
+             "final_mismatch_rel": r.report["final_mismatch_rel"], "final_grad_rel": r.report["final_grad_rel"]}
+    if with_cpu:
+        try:
+            from oracle import ref
+            ref.set_workers(os.cpu_count() or 1)
+            xh = x.numpy()
+            sp = ref.fft_forward(mT)
+            cpu_ops = {
+                "fft_r2c": lambda: ref.fft_forward(mT),
+                "fft_c2r": lambda: ref.fft_inverse(sp, (n, n, n)),
+                "gradient": lambda: ref.gradient(mT),
+                "divergence": lambda: ref.divergence(vs),
+                "leray": lambda: ref.apply_projection(vs, 1),
+                "tricubic_3_fields": lambda: ref.tricubic_interpolate(vs, xh),
+                "tricubic_1_field": lambda: ref.tricubic_interpolate(mT, xh),
+            }
+            for name, fn in cpu_ops.items():
+                fn()
+                t0 = time.perf_counter()
+                for _ in range(3):
+                    fn()
+                ms = (time.perf_counter() - t0) / 3 * 1e3
+                res[name]["cpu_ms"] = ms
+                res[name]["speedup"] = ms * 1e3 / res[name]["gpu_us"]
+            t0 = time.perf_counter()
+            _, rep_c, _ = ref.gauss_newton_solve(mR, mT, np.zeros((3, n, n, n)), model, params)
+            solve.update({"cpu_reference_seconds": time.perf_counter() - t0,
+                          "cpu_newton_iterations": rep_c["outer_iterations"],
+                          "cpu_final_mismatch_rel": rep_c["final_mismatch_rel"], "cpu_cores": os.cpu_count()})
+        except Exception as exc:
+            solve["cpu_reference"] = f"unavailable: {exc}"
+    c.close()
+    return {"grid": n, "workload": "config2: 128^3 synthetic problem (synthetic.cpp:16-34), H2 beta_v=1e-2, "
+            "n_t=4; operators on device-resident fields (tricubic at the RK2 departure points of v*)",
+            "operators": res, "solve": solve}
 
 
 def main():
@@ -479,6 +571,12 @@ def main():
         o4.close()
         c4.close()
 
+    # ---- config 2 (128^3 analytic problem): per-operator micro-benchmarks and the full
+    # GN solve, GPU (device-resident, CUDA events) next to the reference on the host cores --
+    cfg2 = None
+    if world == 1 and not args.no_config2:
+        cfg2 = config2_block(vr, V, dev, nt, model, torch, with_cpu=not args.no_cpu_baseline)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -502,7 +600,7 @@ def main():
                 "kernels": kernels, "kernel_profile": {"steps": k_prof, "ms_per_step": ms_prof / k_prof,
                                                         "note": "separate serialised pass, events per kernel"},
                 "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve,
-                "config4_single_gpu": cfg4}
+                "config4_single_gpu": cfg4, "config2": cfg2}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -14,6 +14,19 @@ import paper_1808_04487_b200.veloreg as V  # noqa: E402
 from paper_1808_04487_b200 import phantom  # noqa: E402
 
 
+def _pool_reserved():
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:
+        try:
+            from cuda import cudart as rt
+        except ImportError:
+            return None
+    err, pool = rt.cudaDeviceGetDefaultMemPool(0)
+    err, v = rt.cudaMemPoolGetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrReservedMemCurrent)
+    return int(v) / 1e9
+
+
 def main():
     n = int(os.environ.get("N", "256"))
     cfg = phantom.CONFIGS[3]
@@ -36,7 +49,7 @@ def main():
             _, reps, recs = V.parameter_continuation(ctx, d_mR, d_mT, d_v0, model, params, precond=pc)
             ctx.synchronize()
             wall = time.perf_counter() - t0
-            out = {"precond": pc, "profiling": prof, "wall_s": wall,
+            out = {"precond": pc, "profiling": prof, "wall_s": wall, "pool_reserved_GB": _pool_reserved(),
                    "newton": [r["outer_iterations"] for r in reps],
                    "fine_mv": sum(r["fine"]["hessian_matvecs"] for r in reps),
                    "coarse_mv": sum(r["coarse"]["hessian_matvecs"] for r in reps),
