@@ -180,6 +180,46 @@ def run_reference_matvecs(m_R, m_T, v, vt, nt, steps, warmup, budget_s):
             "setup_s": setup}
 
 
+def fp32_block(ctx, V, d_v, d_mT, nt, dev, torch):
+    """fp32 lane micro-benchmark at the bench grid: one tricubic gather of a scalar (a state
+    step) and of the 3 velocity components at the backward departure points, fp32 vs fp64."""
+    L = V._lib
+    N = ctx.N
+    x = ctx.empty(3)
+    L.call("vr_trace_characteristics", ctx.handle, d_v.ptr, nt, 0, x.ptr)
+    xf = V.DeviceBufferF32.from_host(ctx, x.numpy())
+    mf = V.DeviceBufferF32.from_host(ctx, d_mT.numpy())
+    vf = V.DeviceBufferF32.from_host(ctx, d_v.numpy())
+    o1, o3 = ctx.empty(1), ctx.empty(3)
+    of1, of3 = V.DeviceBufferF32(ctx, N), V.DeviceBufferF32(ctx, 3 * N)
+    ops = {
+        "state_step_f64": lambda: L.call("vr_tricubic_interpolate", ctx.handle, d_mT.ptr, x.ptr, o1.ptr, 1),
+        "state_step_f32": lambda: L.call("vr_tricubic_interpolate_f32", ctx.handle, mf.ptr, xf.ptr, of1.ptr, 1),
+        "velocity_3_fields_f64": lambda: L.call("vr_tricubic_interpolate", ctx.handle, d_v.ptr, x.ptr, o3.ptr, 3),
+        "velocity_3_fields_f32": lambda: L.call("vr_tricubic_interpolate_f32", ctx.handle, vf.ptr, xf.ptr,
+                                                of3.ptr, 3),
+    }
+    st = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {}
+    for name, fn in ops.items():
+        for _ in range(3):
+            fn()
+        ctx.synchronize()
+        e0.record(st)
+        for _ in range(20):
+            fn()
+        e1.record(st)
+        e1.synchronize()
+        res[name + "_us"] = e0.elapsed_time(e1) / 20 * 1e3
+    res["speedup_state_step"] = res["state_step_f64_us"] / res["state_step_f32_us"]
+    res["speedup_3_fields"] = res["velocity_3_fields_f64_us"] / res["velocity_3_fields_f32_us"]
+    res["note"] = "fp32 fields and departure points, fp64 weights and sums (the reference's float lane)"
+    for b in (xf, mf, vf, of1, of3):
+        b.free()
+    return res
+
+
 def config2_block(vr, V, dev, nt, model, torch, with_cpu=True):
     """BASELINE config 2: 128^3 section-4.2 problem. Per-operator GPU times (20 launches after
     3 warm-ups, CUDA events on the library stream, outputs preallocated) with algorithmic
@@ -569,7 +609,25 @@ def main():
                 "achieved_GBps": b4 / (ms4 / 1e3) / 1e9, "frac_of_peak": b4 / (ms4 / 1e3) / 1e9 / peak}
         s4.close()
         o4.close()
+        # the config-4 solve on one GPU (beta continuation, spectral preconditioner)
+        dv0 = c4.to_device(np.zeros((3, n4, n4, n4)))
+        c4.synchronize()
+        t0 = time.perf_counter()
+        _, reps4, _ = V.parameter_continuation(c4, dR4, dT4, dv0, model, V.make_params(eps_opt=1e-2))
+        c4.synchronize()
+        cfg4["gn_solve"] = {"seconds": time.perf_counter() - t0, "levels": len(reps4),
+                            "newton_iterations": [r["outer_iterations"] for r in reps4],
+                            "hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps4),
+                            "final_mismatch_rel": reps4[-1]["final_mismatch_rel"],
+                            "final_grad_rel": reps4[-1]["final_grad_rel"], "stop": reps4[-1]["stop_name"],
+                            "note": "single run (includes memory-pool growth)"}
         c4.close()
+
+    # ---- fp32 lane: the same tricubic gathers at the config-3 departure
+    # points with fp32 fields / points (fp64 stencil arithmetic), next to the fp64 kernel --
+    f32 = None
+    if world == 1:
+        f32 = fp32_block(ctx, V, d_v, d_mT, nt, dev, torch)
 
     # ---- config 2 (128^3 analytic problem): per-operator micro-benchmarks and the full
     # GN solve, GPU (device-resident, CUDA events) next to the reference on the host cores --
@@ -600,7 +658,7 @@ def main():
                 "kernels": kernels, "kernel_profile": {"steps": k_prof, "ms_per_step": ms_prof / k_prof,
                                                         "note": "separate serialised pass, events per kernel"},
                 "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve,
-                "config4_single_gpu": cfg4, "config2": cfg2}
+                "config4_single_gpu": cfg4, "config2": cfg2, "fp32_lane": f32}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

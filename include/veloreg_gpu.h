@@ -262,6 +262,16 @@ int vr_solve_inc_state(vr_ctx* ctx, const double* m_history, const double* v3, c
 int vr_solve_inc_adjoint(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
                          double* history, double* initial);
 
+/* ---- fp32 lane (one GPU): the float instantiations of the
+ * semi-Lagrangian operators (T = float in interp.hpp:80-126, transport.cpp:11-42, :72-86).
+ * Fields and departure points are fp32 device arrays; stencils and sums run in fp64 and
+ * results are rounded to fp32, as in the reference. */
+int vr_tricubic_interpolate_f32(vr_ctx* ctx, const float* f, const float* points3, float* out,
+                                int nfields);
+int vr_trace_characteristics_f32(vr_ctx* ctx, const float* v3, int nt, int direction,
+                                 float* departure3);
+int vr_solve_state_f32(vr_ctx* ctx, const float* m_T, const float* v3, int nt, float* history);
+
 /* ---- Objective (objective.hpp:56-102) -------------------------------------- */
 typedef struct vr_objective vr_objective;
 typedef struct vr_state vr_state;

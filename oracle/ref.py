@@ -81,6 +81,9 @@ _SIG = {
                                         C.POINTER(IterationRecord), I]),
     "vref_generate_synthetic": (I, [DIMS, I, D, P, P, P]),
     "vref_det_deformation_gradient": (I, [DIMS, P, I, P]),
+    "vref_tricubic_interpolate_f32": (I, [DIMS, P, P, P, I]),
+    "vref_trace_characteristics_f32": (I, [DIMS, P, I, I, P]),
+    "vref_solve_state_f32": (I, [DIMS, P, P, I, P]),
     "vref_deformation_map": (I, [DIMS, P, I, I, P]),
     "vref_det_stats": (I, [DIMS, P, P, D, C.POINTER(D)]),
     "vref_transport_labels": (I, [DIMS, P, P, I, P]),
@@ -525,6 +528,34 @@ def beta_search(m_R, m_T, v0, model, params, search, precond=1, max_trials=64):
         e.trials = trials
         raise e
     return beta.value, vout, trials
+
+
+# ---- fp32 lane: the reference's float instantiations ----------------------------------
+def _f(x):
+    return np.ascontiguousarray(x, dtype=np.float32)
+
+
+def tricubic_interpolate_f32(f, points):
+    f, p = _f(f), _f(points)
+    nf = 1 if f.ndim == 3 else f.shape[0]
+    out = np.empty_like(f)
+    _call("vref_tricubic_interpolate_f32", _dims(p.shape), f.ctypes.data, p.ctypes.data, out.ctypes.data, nf)
+    return out
+
+
+def trace_characteristics_f32(v, nt, direction="backward"):
+    v = _f(v)
+    out = np.empty_like(v)
+    _call("vref_trace_characteristics_f32", _dims(v.shape), v.ctypes.data, nt,
+          0 if direction == "backward" else 1, out.ctypes.data)
+    return out
+
+
+def solve_state_f32(m_T, v, nt):
+    m, v = _f(m_T), _f(v)
+    out = np.empty((nt + 1,) + m.shape, dtype=np.float32)
+    _call("vref_solve_state_f32", _dims(m.shape), m.ctypes.data, v.ctypes.data, nt, out.ctypes.data)
+    return out
 
 
 # ---- postprocess (postprocess.hpp:9-56) ----------------------------------------------

@@ -85,6 +85,22 @@ void store(const TimeSeries<double>& t, double* p) {
     for (int j = 0; j < t.slice_count(); ++j) store(t.slice(j), p + j * t.slice(0).size());
 }
 
+// fp32 lane: the reference's float instantiations (ScalarField<float>, ...)
+ScalarField<float> load_scalar_f(const Grid3& g, const float* p) {
+    ScalarField<float> f(g);
+    std::memcpy(f.data(), p, sizeof(float) * g.size());
+    return f;
+}
+VectorField<float> load_vector_f(const Grid3& g, const float* p) {
+    VectorField<float> v(g);
+    for (int c = 0; c < 3; ++c) std::memcpy(v[c].data(), p + c * g.size(), sizeof(float) * g.size());
+    return v;
+}
+void store_f(const ScalarField<float>& f, float* p) { std::memcpy(p, f.data(), sizeof(float) * f.size()); }
+void store_f(const VectorField<float>& v, float* p) {
+    for (int c = 0; c < 3; ++c) std::memcpy(p + c * v.size(), v[c].data(), sizeof(float) * v.size());
+}
+
 RegNorm to_norm(const vr_regnorm& n) {
     RegNorm r;
     r.kind = static_cast<RegKind>(n.kind);
@@ -308,6 +324,42 @@ int vref_trace_characteristics(const int* d, const double* v3, int nt, int dir, 
                                         dir == VR_TRACE_FORWARD ? TraceDirection::forward
                                                                 : TraceDirection::backward);
         store(ch.departure, dep3);
+    });
+}
+int vref_tricubic_interpolate_f32(const int* d, const float* f, const float* pts3, float* out,
+                                  int nfields) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto pts = load_vector_f(g, pts3);
+        const std::int64_t n = g.size();
+        if (nfields == 1) {
+            store_f(tricubic_interpolate(load_scalar_f(g, f), pts), out);
+        } else if (nfields == 2) {
+            ScalarField<float> o1, o2;
+            tricubic_interpolate2(load_scalar_f(g, f), load_scalar_f(g, f + n), pts, o1, o2);
+            store_f(o1, out);
+            store_f(o2, out + n);
+        } else {
+            VectorField<float> o;
+            tricubic_interpolate3(load_vector_f(g, f), pts, o);
+            store_f(o, out);
+        }
+    });
+}
+int vref_trace_characteristics_f32(const int* d, const float* v3, int nt, int dir, float* dep3) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto ch = trace_characteristics(load_vector_f(g, v3), nt,
+                                        dir == VR_TRACE_FORWARD ? TraceDirection::forward
+                                                                : TraceDirection::backward);
+        store_f(ch.departure, dep3);
+    });
+}
+int vref_solve_state_f32(const int* d, const float* mT, const float* v3, int nt, float* hist) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto h = solve_state(load_scalar_f(g, mT), load_vector_f(g, v3), nt);
+        for (int j = 0; j < h.slice_count(); ++j) store_f(h.slice(j), hist + j * g.size());
     });
 }
 int vref_continuity_factor(const int* d, const double* div_v, const double* dep3, double dt,

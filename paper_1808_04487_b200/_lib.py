@@ -223,6 +223,9 @@ SIGNATURES = {
     "vr_hessian_matvec_host": (I, [P, P, HP, HP]),
     "vr_hessian_data_matvec": (I, [P, P, DP, DP]),
     "vr_hessian_matvec_host_async": (I, [P, P, HP, HP]),
+    "vr_tricubic_interpolate_f32": (I, [P, DP, DP, DP, I]),
+    "vr_trace_characteristics_f32": (I, [P, DP, I, I, DP]),
+    "vr_solve_state_f32": (I, [P, DP, DP, I, DP]),
     "vr_objective_wait": (I, [P]),
     "vr_objective_apply_reg": (I, [P, DP, I, DP]),
     "vr_objective_apply_K": (I, [P, DP, DP]),

@@ -629,6 +629,44 @@ int vr_solve_state(vr_ctx* ctx, const double* m_T, const double* v3, int nt, dou
         vr::dev_free(ctx, xb);
     });
 }
+// ---- fp32 lane ------------------------------------------------------------------
+int vr_tricubic_interpolate_f32(vr_ctx* ctx, const float* f, const float* points3, float* out,
+                                int nfields) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_tricubic_interpolate_f32");
+        need(f && points3 && out, "vr_tricubic_interpolate_f32");
+        vr::sl_tricubic_f32(ctx, f, nfields, points3, out);
+    });
+}
+int vr_trace_characteristics_f32(vr_ctx* ctx, const float* v3, int nt, int direction,
+                                 float* departure3) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_trace_characteristics_f32");
+        need(v3 && departure3, "vr_trace_characteristics_f32");
+        if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
+        if (!vr::all_finite_f32(ctx, v3, 3 * ctx->g.N))
+            vr::throw_numeric("trace_characteristics: velocity has non-finite values");
+        vr::sl_trace_f32(ctx, v3, nt, direction, departure3);
+    });
+}
+int vr_solve_state_f32(vr_ctx* ctx, const float* m_T, const float* v3, int nt, float* history) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_solve_state_f32");
+        need(m_T && v3 && history, "vr_solve_state_f32");
+        const long long N = ctx->g.N;
+        if (nt < 1) vr::throw_argument("trace_characteristics: n_t must be >= 1");
+        if (!vr::all_finite_f32(ctx, v3, 3 * N))
+            vr::throw_numeric("trace_characteristics: velocity has non-finite values");
+        float* xb = nullptr;
+        VR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xb), sizeof(float) * 3 * N, ctx->stream));
+        vr::sl_trace_f32(ctx, v3, nt, VR_TRACE_BACKWARD, xb);
+        VR_CUDA(cudaMemcpyAsync(history, m_T, sizeof(float) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        for (int j = 0; j < nt; ++j) vr::sl_tricubic_f32(ctx, history + j * N, 1, xb, history + (j + 1) * N);
+        VR_CUDA(cudaFreeAsync(xb, ctx->stream));
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 static void adjoint_like(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
                          double* history, double* initial) {
     const long long N = ctx->g.N;

@@ -90,7 +90,11 @@ __device__ __forceinline__ int wrapi(int j, int n) { return j & (n - 1); }
 // On x1 slabs `f` points at the interior of a halo-padded field and x1 planes
 // b .. b+3 must lie in [-halo, L + halo); a violation raises flags[1] (checked
 // by the host after the sweep) and clamps.
-__device__ __forceinline__ double gather(const double* __restrict__ f, const GridDims& g,
+// TF = storage type of the gathered field (double, or float for the fp32 lane: the
+// reference's Objective<float> stores fields in fp32 and interpolates in fp64,
+// interp.hpp:55-70)
+template <class TF>
+__device__ __forceinline__ double gather(const TF* __restrict__ f, const GridDims& g,
                                          const Stencil& st) {
     const int n23 = g.n2 * g.n3;
     int b1 = st.b[0];
@@ -108,16 +112,16 @@ __device__ __forceinline__ double gather(const double* __restrict__ f, const Gri
     const int b3 = st.b[2];
     double acc = 0.0;
     if (b3 >= 0 && b3 + 3 < g.n3) {
-        const double* f3 = f + b3;
+        const TF* f3 = f + b3;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             double acc1 = 0.0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                const double* p = f3 + o12[a][b];
+                const TF* p = f3 + o12[a][b];
                 double acc2 = 0.0;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc2 += st.w[2][c] * __ldg(p + c);
+                for (int c = 0; c < 4; ++c) acc2 += st.w[2][c] * static_cast<double>(__ldg(p + c));
                 acc1 += st.w[1][b] * acc2;
             }
             acc += st.w[0][a] * acc1;
@@ -131,10 +135,10 @@ __device__ __forceinline__ double gather(const double* __restrict__ f, const Gri
             double acc1 = 0.0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                const double* p = f + o12[a][b];
+                const TF* p = f + o12[a][b];
                 double acc2 = 0.0;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc2 += st.w[2][c] * __ldg(p + i3[c]);
+                for (int c = 0; c < 4; ++c) acc2 += st.w[2][c] * static_cast<double>(__ldg(p + i3[c]));
                 acc1 += st.w[1][b] * acc2;
             }
             acc += st.w[0][a] * acc1;
@@ -172,11 +176,12 @@ __device__ __forceinline__ bool tile_point(const GridDims& g, const Tile& t, int
     return ok;
 }
 
-__device__ __forceinline__ void load_point(const double* __restrict__ dep, long long i,
+template <class TD>
+__device__ __forceinline__ void load_point(const TD* __restrict__ dep, long long i,
                                            long long N, double& x1, double& x2, double& x3) {
-    x1 = __ldg(dep + i);
-    x2 = __ldg(dep + N + i);
-    x3 = __ldg(dep + 2 * N + i);
+    x1 = static_cast<double>(__ldg(dep + i));
+    x2 = static_cast<double>(__ldg(dep + N + i));
+    x3 = static_cast<double>(__ldg(dep + 2 * N + i));
 }
 
 // ---------------------------------------------------------------------------
@@ -369,6 +374,43 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
     }
 }
 
+// ---- fp32 lane: the semi-Lagrangian operators of Objective<float>:
+// fields and departure points stored in fp32, stencils and sums in fp64, results
+// rounded to fp32 (interp.hpp:55-126, transport.cpp:11-42 with T = float) -----------
+template <int NF, bool BIG>
+__global__ void __launch_bounds__(kTileThreads, NF == 1 ? VR_SL_MINB : VR_SL_MINB * 2 / 3)
+    k_tricubic_f32(const float* __restrict__ f, const float* __restrict__ pts, float* __restrict__ out,
+                   GridDims g, Tile t) {
+    int i1, i2, i3;
+    long long i;
+    if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
+    double x1, x2, x3;
+    load_point(pts, i, g.N, x1, x2, x3);
+    Stencil st;
+    make_stencil(g, x1, x2, x3, i1, st);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) out[q * g.N + i] = static_cast<float>(gather(f + q * g.N, g, st));
+}
+
+template <bool BIG>
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
+    k_trace_f32(const float* __restrict__ v, float* __restrict__ dep, GridDims g, Tile t,
+                double sign, double dt) {
+    int i1, i2, i3;
+    long long i;
+    if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
+    const double x[3] = {g.h1 * i1, g.h2 * i2, g.h3 * i3};
+    double mid[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        mid[c] = wrap_coord(x[c] + sign * 0.5 * dt * static_cast<double>(v[c * g.N + i]));
+    Stencil st;
+    make_stencil(g, mid[0], mid[1], mid[2], i1, st);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        dep[c * g.N + i] = static_cast<float>(wrap_coord(x[c] + sign * dt * gather(v + c * g.N, g, st)));
+}
+
 // lv_c = lam * vt_c (transport.cpp:203-207)
 __global__ void __launch_bounds__(kThreads)
     k_scale_vec(const double* __restrict__ lam, const double* __restrict__ vt, double* __restrict__ lv,
@@ -496,6 +538,10 @@ unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.
 #define K_ADJ_ACC(B) k_adjoint_step<true, B>
 #define K_ADJ_FN(B) k_adjoint_fn_step<B>
 #define K_DEFMAP(B) k_defmap_step<B>
+#define K_TRICUBIC1F(B) k_tricubic_f32<1, B>
+#define K_TRICUBIC2F(B) k_tricubic_f32<2, B>
+#define K_TRICUBIC3F(B) k_tricubic_f32<3, B>
+#define K_TRACEF(B) k_trace_f32<B>
 
 }  // namespace
 
@@ -597,6 +643,36 @@ void sl_defmap_step(vr_ctx* ctx, const double* u3, const double* dep3, const dou
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);
     VR_TILE_LAUNCH(ctx, "sl_defmap_step", K_DEFMAP, u3, dep3, vdep3, v3, half_dt, out3, g, t);
+}
+
+void sl_tricubic_f32(vr_ctx* ctx, const float* f, int nfields, const float* pts3, float* out) {
+    const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
+    switch (nfields) {
+        case 1: VR_TILE_LAUNCH(ctx, "sl_gather_f32", K_TRICUBIC1F, f, pts3, out, g, t); break;
+        case 2: VR_TILE_LAUNCH(ctx, "sl_gather_f32", K_TRICUBIC2F, f, pts3, out, g, t); break;
+        case 3: VR_TILE_LAUNCH(ctx, "sl_gather_f32", K_TRICUBIC3F, f, pts3, out, g, t); break;
+        default: throw_argument("tricubic_interpolate: nfields must be 1, 2 or 3");
+    }
+}
+__global__ void __launch_bounds__(kThreads)
+    k_nonfinite_f32(const float* __restrict__ a, long long n, int* __restrict__ flag) {
+    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+    if (i < n && !isfinite(a[i])) *flag = 1;
+}
+bool all_finite_f32(vr_ctx* ctx, const float* a, long long n) {
+    VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, sizeof(int), ctx->stream));
+    VR_LAUNCH(ctx, "sl_pointwise", k_nonfinite_f32<<<grid_1d(n, kThreads), kThreads, 0, ctx->stream>>>(a, n, ctx->flag_dev));
+    VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ctx->flag_host[0] == 0;
+}
+void sl_trace_f32(vr_ctx* ctx, const float* v3, int nt, int direction, float* dep3) {
+    if (nt < 1) throw_argument("trace_characteristics: n_t must be >= 1");
+    const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
+    const double sign = direction == VR_TRACE_BACKWARD ? -1.0 : 1.0;
+    VR_TILE_LAUNCH(ctx, "sl_trace_f32", K_TRACEF, v3, dep3, g, t, sign, 1.0 / nt);
 }
 
 void sl_scale_vec(vr_ctx* ctx, const double* lam, const double* vt3, double* out3) {

@@ -346,6 +346,10 @@ void sl_adjoint_fn_step(vr_ctx* ctx, const double* src, const double* rnext, con
 // deformation_map step: out_c = I[u_c](X) - half_dt (vdep_c + v_c) (out must not alias u)
 void sl_defmap_step(vr_ctx* ctx, const double* u3, const double* dep3, const double* vdep3,
                     const double* v3, double half_dt, double* out3);
+// fp32 lane (one GPU): fields / points in fp32, stencil arithmetic in fp64
+void sl_tricubic_f32(vr_ctx* ctx, const float* f, int nfields, const float* pts3, float* out);
+void sl_trace_f32(vr_ctx* ctx, const float* v3, int nt, int direction, float* dep3);
+bool all_finite_f32(vr_ctx* ctx, const float* a, long long n);
 // out_c = lam * vt_c
 void sl_scale_vec(vr_ctx* ctx, const double* lam, const double* vt3, double* out3);
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out);

@@ -785,6 +785,69 @@ def beta_search(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral", 
     return beta.value, vout.numpy(), [_trial_dict(trials[i]) for i in range(min(nt_.value, max_trials))]
 
 
+# ---- fp32 lane: float fields, fp64 stencil arithmetic --------------
+class DeviceBufferF32:
+    """Raw fp32 device buffer (host round trips by explicit copies)."""
+
+    def __init__(self, ctx: Context, count: int):
+        self.ctx, self.count = ctx, int(count)
+        p = C.c_void_p()
+        _lib.call("vr_device_alloc", ctx.handle, 4 * self.count, C.byref(p))
+        self.ptr = p
+
+    @classmethod
+    def from_host(cls, ctx, a):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        b = cls(ctx, a.size)
+        _lib.call("vr_memcpy_h2d", ctx.handle, b.ptr, a.ctypes.data, 4 * a.size)
+        return b
+
+    def numpy(self, shape):
+        out = np.empty(shape, dtype=np.float32)
+        _lib.call("vr_memcpy_d2h", self.ctx.handle, out.ctypes.data, self.ptr, 4 * out.size)
+        return out
+
+    def free(self):
+        if getattr(self, "ptr", None):
+            _lib.call("vr_device_free", self.ctx.handle, self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def tricubic_interpolate_f32(ctx, f, points):
+    """tricubic_interpolate{,2,3}<float> (interp.hpp:80-126) on host float32 arrays."""
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    nf = 1 if f.ndim == 3 else f.shape[0]
+    df, dp = DeviceBufferF32.from_host(ctx, f), DeviceBufferF32.from_host(ctx, points)
+    out = DeviceBufferF32(ctx, f.size)
+    _lib.call("vr_tricubic_interpolate_f32", ctx.handle, df.ptr, dp.ptr, out.ptr, nf)
+    return out.numpy(f.shape)
+
+
+def trace_characteristics_f32(ctx, v, nt, direction="backward"):
+    """trace_characteristics<float> (transport.cpp:11-42): fp32 departure points."""
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    dv = DeviceBufferF32.from_host(ctx, v)
+    out = DeviceBufferF32(ctx, v.size)
+    _lib.call("vr_trace_characteristics_f32", ctx.handle, dv.ptr, nt,
+              _lib.TRACE_BACKWARD if direction == "backward" else _lib.TRACE_FORWARD, out.ptr)
+    return out.numpy(v.shape)
+
+
+def solve_state_f32(ctx, m_T, v, nt):
+    """solve_state<float> (transport.cpp:72-86): the fp32 state history (nt + 1 fields)."""
+    m = np.ascontiguousarray(m_T, dtype=np.float32)
+    dm, dv = DeviceBufferF32.from_host(ctx, m), DeviceBufferF32.from_host(ctx, v)
+    out = DeviceBufferF32(ctx, (nt + 1) * m.size)
+    _lib.call("vr_solve_state_f32", ctx.handle, dm.ptr, dv.ptr, nt, out.ptr)
+    return out.numpy((nt + 1,) + m.shape)
+
+
 # ---- postprocess (postprocess.hpp:9-56) -----------------------------------------
 def det_deformation_gradient(ctx, v, nt):
     """det grad y by continuity transport (postprocess.cpp:13-29)."""
