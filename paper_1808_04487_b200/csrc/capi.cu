@@ -225,6 +225,15 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
     VR_CUDA(cudaGetDeviceCount(&count));
     if (device < 0 || device >= count)
         throw_resource("vr_ctx_create: no CUDA device " + std::to_string(device));
+    // host waits spin instead of yielding (VR_SYNC=yield keeps the driver default): the solver
+    // drains the stream for every scalar, and a yielded waiter can be rescheduled late.
+    // Only takes effect if this call creates the device's primary context.
+    if (const char* e = std::getenv("VR_SYNC"); !e || std::string(e) != "yield") {
+        unsigned flags = 0;
+        if (cudaGetDeviceFlags(&flags) == cudaSuccess && !(flags & cudaDeviceScheduleMask))
+            (void)cudaSetDeviceFlags(cudaDeviceScheduleSpin);
+        (void)cudaGetLastError();
+    }
     VR_CUDA(cudaSetDevice(device));
     auto* ctx = new vr_ctx();
     try {
