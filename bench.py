@@ -608,9 +608,30 @@ def main():
                 "value": 1e3 / ms4, "unit": UNIT, "ms_per_step": ms4, "bytes_per_matvec": b4,
                 "achieved_GBps": b4 / (ms4 / 1e3) / 1e9, "frac_of_peak": b4 / (ms4 / 1e3) / 1e9 / peak}
         s4.close()
+        # 10 PCG iterations of the first Newton step (v = 0, beta_v 1e-2, spectral
+        # preconditioner; SURVEY 8(d) row C5's unit, here on one GPU at 512^3)
+        dv0 = c4.to_device(np.zeros((3, n4, n4, n4)))
+        s0 = o4.evaluate(dv0)
+        o4.compute_gradient(s0)
+        rhs = s0.get(V._lib.STATE_GRADIENT, host=False)
+        V._lib.call("vr_scale", c4.handle, rhs.ptr, 3, -1.0)
+        V.pcg_solve(o4, s0, rhs, 1e-30, 2)  # warm-up
+        c4.synchronize()
+        e0.record(st4)
+        _, pst = V.pcg_solve(o4, s0, rhs, 1e-30, 10)
+        e1.record(st4)
+        e1.synchronize()
+        ms_pcg = e0.elapsed_time(e1)
+        b_pcg = 148.0 * 8 * n4 ** 3  # B_mv + 39 F + 6 F_c ~ 148 F per PCG iteration
+        cfg4["pcg_10_iterations"] = {"ms": ms_pcg, "iterations": pst["iterations"],
+                                     "ms_per_iteration": ms_pcg / max(1, pst["iterations"]),
+                                     "bytes_per_iteration": b_pcg,
+                                     "frac_of_peak": b_pcg / (ms_pcg / max(1, pst["iterations"]) / 1e3) / 1e9 / peak,
+                                     "note": "first Newton step (v = 0); PCG carries beta_v A s, so an iteration "
+                                             "is a data matvec + the spectral preconditioner"}
+        s0.close()
         o4.close()
         # the config-4 solve on one GPU (beta continuation, spectral preconditioner)
-        dv0 = c4.to_device(np.zeros((3, n4, n4, n4)))
         c4.synchronize()
         t0 = time.perf_counter()
         _, reps4, _ = V.parameter_continuation(c4, dR4, dT4, dv0, model, V.make_params(eps_opt=1e-2))
