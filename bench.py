@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=90.0,
                     help="wall budget for the reference arm's timed matvecs")
     ap.add_argument("--no-solve", action="store_true", help="skip the GN solve timings")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-lane gather micro-benchmark")
     ap.add_argument("--no-config2", action="store_true",
                     help="skip the 128^3 (config 2) per-operator micro-benchmarks and solve")
     ap.add_argument("--no-config4", action="store_true",
@@ -647,7 +648,7 @@ def main():
     # ---- fp32 lane: the same tricubic gathers at the config-3 departure
     # points with fp32 fields / points (fp64 stencil arithmetic), next to the fp64 kernel --
     f32 = None
-    if world == 1:
+    if world == 1 and not args.no_fp32:
         f32 = fp32_block(ctx, V, d_v, d_mT, nt, dev, torch)
 
     # ---- config 2 (128^3 analytic problem): per-operator micro-benchmarks and the full
