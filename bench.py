@@ -515,13 +515,13 @@ def main():
         params = V.make_params(eps_opt=1e-2)
         d_v0 = ctx.to_device(np.zeros((3,) + ctx.local_dims))  # device-resident initial guess
         t_runs = []
-        for _ in range(4):  # the first run also grows the stream-ordered memory pool
+        for _ in range(6):  # the first run also grows the stream-ordered memory pool
             ctx.synchronize()
             t0 = time.perf_counter()
             vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, d_v0, model, params)
             ctx.synchronize()
             t_runs.append(time.perf_counter() - t0)
-        t_solve = float(np.median(t_runs[1:]))  # median of the 3 steady runs (host jitter)
+        t_solve = float(np.median(t_runs[1:]))  # median of the 5 steady runs (host jitter)
         solve["config3"] = {
             "grid": n, "seconds": t_solve, "seconds_runs": t_runs, "levels": len(reps),
             "newton_iterations": [r["outer_iterations"] for r in reps],
@@ -532,7 +532,7 @@ def main():
         # the same continuation with the two-level preconditioner; one GPU only
         if world == 1:
             t2 = []
-            for _ in range(4):  # first run: coarse context, plans and pool growth
+            for _ in range(6):  # first run: coarse context, plans and pool growth
                 ctx.synchronize()
                 t0 = time.perf_counter()
                 _, reps2, _ = V.parameter_continuation(ctx, d_mR, d_mT, d_v0, model, params,

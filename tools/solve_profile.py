@@ -28,6 +28,10 @@ def _pool_reserved():
 
 
 def main():
+    if os.environ.get("TORCH_FIRST"):  # the bench's order: torch owns the primary context
+        import torch
+        torch.cuda.set_device(0)
+        torch.zeros(1, device="cuda")
     n = int(os.environ.get("N", "256"))
     cfg = phantom.CONFIGS[3]
     m_T = phantom.ellipsoid_phantom(n)
@@ -38,6 +42,15 @@ def main():
     model = V.make_model("h2", beta_v=1e-2, nt=4)
     params = V.make_params(eps_opt=1e-2)
     d_v0 = ctx.to_device(np.zeros((3, n, n, n)))
+    if os.environ.get("HOT"):  # the bench's preamble: 100 matvecs at the generating velocity
+        o = V.Objective(ctx, d_mR, d_mT, V.make_model("h2", beta_v=1e-2, nt=4))
+        st = o.evaluate(ctx.to_device(v))
+        o.compute_gradient(st)
+        vt = ctx.to_device(phantom.bandlimited_direction(n))
+        out = ctx.empty(3)
+        for _ in range(100):
+            o.hessian_matvec(st, vt, out=out)
+        ctx.synchronize()
     plan = [(pc, prof) for pc in ("spectral", "two_level", "spectral", "two_level") for prof in (False, True)]
     if os.environ.get("REPEAT"):
         plan = [("spectral", False)] * int(os.environ["REPEAT"])
