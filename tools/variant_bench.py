@@ -51,7 +51,7 @@ def main():
     ctx.set_profiling(False)
     import hashlib
     o = out.numpy()
-    res = {"lib": os.environ.get("VR_LIB", "default"), "gather": os.environ.get("VR_GATHER", "auto"),
+    res = {"lib": os.environ.get("VR_LIB", "default"),
            "ms_per_matvec": ms, "out_sha1": hashlib.sha1(o.tobytes()).hexdigest()[:12],
            "out_norm": float(np.linalg.norm(o)),
            "kernels_us": {k: round(1e3 * t / c, 1) for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
