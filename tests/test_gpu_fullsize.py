@@ -112,3 +112,33 @@ def test_fullsize_spectral_round_trips(vr, ctx, config):
     rtn = rt.numpy() if hasattr(rt, "numpy") else rt
     rtm = rtn - rtn.mean(axis=(1, 2, 3), keepdims=True)
     assert rel_l2(rtm, fm) <= 1e-11
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("VR_FULLSIZE_512"),
+                    reason="~10 min of reference CPU time and ~90 GB host RAM; set VR_FULLSIZE_512=1")
+def test_config4_reference_parity(vr, ref, ctx):
+    """Config 4 (512^3) on one GPU against the reference on the host cores: one evaluate +
+    gradient + data matvec (same bars as config 3; run on demand, result in DESIGN.md)."""
+    from paper_1808_04487_b200 import phantom
+    c, n, m_R, m_T, v = _inputs(vr, ctx, 4)
+    vt = phantom.bandlimited_direction(n)
+    model = vr.make_model()
+    o = vr.Objective(c, m_R, m_T, model)
+    v_eval = 0.5 * v
+    s = o.evaluate(v_eval)
+    o.compute_gradient(s)
+    g, hdv = s.gradient, o.hessian_data_matvec(s, vt)
+    ro = ref.Objective(m_R, m_T, model)
+    rs = ro.evaluate(v_eval)
+    g_ref = ro.compute_gradient(rs)
+    hdv_ref = ro.hessian_data_matvec(rs, vt)
+    sc = rs.scalars()
+    reg = np.asarray(vr.apply_reg_operator(c, v_eval, model.norm, "apply", model.beta_v))
+    reg_ref = ref.apply_reg_operator(v_eval, model.norm, 0, model.beta_v)
+    errs = {"objective": abs(s.objective - sc["objective"]) / abs(sc["objective"]),
+            "gradient_data": rel_l2(g - reg, g_ref - reg_ref), "reg": rel_l2(reg, reg_ref),
+            "data_matvec": rel_l2(hdv, hdv_ref)}
+    print("config4 parity", errs)
+    assert errs["objective"] <= 1e-12
+    assert errs["gradient_data"] <= 1e-10 and errs["data_matvec"] <= 1e-10
+    assert errs["reg"] <= 2e-9 * (n / 256) ** 4
