@@ -377,8 +377,11 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
 // ---- fp32 lane: the semi-Lagrangian operators of Objective<float>:
 // fields and departure points stored in fp32, stencils and sums in fp64, results
 // rounded to fp32 (interp.hpp:55-126, transport.cpp:11-42 with T = float) -----------
+#ifndef VR_SL_MINB_F32
+#define VR_SL_MINB_F32 8  // resident CTAs/SM of the fp32 gathers (swept 4..8: 8 best, 480 vs 486-629 us)
+#endif
 template <int NF, bool BIG>
-__global__ void __launch_bounds__(kTileThreads, NF == 1 ? VR_SL_MINB : VR_SL_MINB * 2 / 3)
+__global__ void __launch_bounds__(kTileThreads, NF == 1 ? VR_SL_MINB_F32 : VR_SL_MINB_F32 * 2 / 3)
     k_tricubic_f32(const float* __restrict__ f, const float* __restrict__ pts, float* __restrict__ out,
                    GridDims g, Tile t) {
     int i1, i2, i3;
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(kTileThreads, NF == 1 ? VR_SL_MINB : VR_SL_MIN
 }
 
 template <bool BIG>
-__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB_F32 * 2 / 3)
     k_trace_f32(const float* __restrict__ v, float* __restrict__ dep, GridDims g, Tile t,
                 double sign, double dt) {
     int i1, i2, i3;
