@@ -271,6 +271,18 @@ int vr_tricubic_interpolate_f32(vr_ctx* ctx, const float* f, const float* points
 int vr_trace_characteristics_f32(vr_ctx* ctx, const float* v3, int nt, int direction,
                                  float* departure3);
 int vr_solve_state_f32(vr_ctx* ctx, const float* m_T, const float* v3, int nt, float* history);
+/* spectral operators with fp32 fields; the transforms run in fp64 and the half spectrum
+ * stays complex128 (fft.hpp:12-23: "f32 fields are converted at the boundary") */
+int vr_fft_r2c_f32(vr_ctx* ctx, const float* in, double* out_spectrum);
+int vr_fft_c2r_f32(vr_ctx* ctx, const double* spectrum, float* out);
+int vr_gradient_f32(vr_ctx* ctx, const float* f, float* out3);
+int vr_divergence_f32(vr_ctx* ctx, const float* v3, float* out);
+int vr_gaussian_smooth_f32(vr_ctx* ctx, const float* f, float* out, int ncomp,
+                           const double sigma_voxels[3]);
+int vr_apply_reg_operator_f32(vr_ctx* ctx, const float* v3, float* out3, const vr_regnorm* norm,
+                              int mode, double beta);
+int vr_apply_projection_f32(vr_ctx* ctx, const float* f3, float* out3, int kind, double beta_v,
+                            double beta_w);
 
 /* ---- Objective (objective.hpp:56-102) -------------------------------------- */
 typedef struct vr_objective vr_objective;

@@ -82,6 +82,13 @@ _SIG = {
     "vref_generate_synthetic": (I, [DIMS, I, D, P, P, P]),
     "vref_det_deformation_gradient": (I, [DIMS, P, I, P]),
     "vref_tricubic_interpolate_f32": (I, [DIMS, P, P, P, I]),
+    "vref_fft_r2c_f32": (I, [DIMS, P, P]),
+    "vref_fft_c2r_f32": (I, [DIMS, P, P]),
+    "vref_gradient_f32": (I, [DIMS, P, P]),
+    "vref_divergence_f32": (I, [DIMS, P, P]),
+    "vref_gaussian_smooth_f32": (I, [DIMS, P, P, C.POINTER(D)]),
+    "vref_apply_reg_operator_f32": (I, [DIMS, P, P, C.POINTER(RegNorm), I, D]),
+    "vref_apply_projection_f32": (I, [DIMS, P, P, I, D, D]),
     "vref_trace_characteristics_f32": (I, [DIMS, P, I, I, P]),
     "vref_solve_state_f32": (I, [DIMS, P, P, I, P]),
     "vref_deformation_map": (I, [DIMS, P, I, I, P]),
@@ -548,6 +555,48 @@ def trace_characteristics_f32(v, nt, direction="backward"):
     out = np.empty_like(v)
     _call("vref_trace_characteristics_f32", _dims(v.shape), v.ctypes.data, nt,
           0 if direction == "backward" else 1, out.ctypes.data)
+    return out
+
+
+def _f32_unary(name, a, nout, *extra):
+    a = _f(a)
+    shape = a.shape if a.ndim == 3 else a.shape[1:]
+    out = np.empty(((nout,) if nout > 1 else ()) + tuple(shape), dtype=np.float32)
+    _call(name, _dims(shape), a.ctypes.data, out.ctypes.data, *extra)
+    return out
+
+
+def gradient_f32(f):
+    return _f32_unary("vref_gradient_f32", f, 3)
+
+
+def divergence_f32(v):
+    return _f32_unary("vref_divergence_f32", v, 1)
+
+
+def apply_reg_operator_f32(v, norm, mode, beta=1.0):
+    return _f32_unary("vref_apply_reg_operator_f32", v, 3, C.byref(norm), mode, beta)
+
+
+def apply_projection_f32(v, kind, beta_v=0.0, beta_w=0.0):
+    return _f32_unary("vref_apply_projection_f32", v, 3, kind, beta_v, beta_w)
+
+
+def gaussian_smooth_f32(f, sigma):
+    return _f32_unary("vref_gaussian_smooth_f32", f, 1, (C.c_double * 3)(*sigma))
+
+
+def fft_forward_f32(f):
+    f = _f(f)
+    out = np.empty((f.shape[0], f.shape[1], f.shape[2] // 2 + 1), dtype=np.complex128)
+    _call("vref_fft_r2c_f32", _dims(f.shape), f.ctypes.data, out.ctypes.data)
+    return out
+
+
+def fft_inverse_f32(spec, shape):
+    s = np.ascontiguousarray(spec, dtype=np.complex128)
+    out = np.empty(shape, dtype=np.float32)
+    _call("vref_fft_c2r_f32", _dims(shape), s.ctypes.data, out.ctypes.data)
     return out
 
 

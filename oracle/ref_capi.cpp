@@ -362,6 +362,50 @@ int vref_solve_state_f32(const int* d, const float* mT, const float* v3, int nt,
         for (int j = 0; j < h.slice_count(); ++j) store_f(h.slice(j), hist + j * g.size());
     });
 }
+int vref_fft_r2c_f32(const int* d, const float* in, double* out) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        Spectrum sp;
+        fft_forward(load_scalar_f(g, in), sp);
+        std::memcpy(out, sp.data(), sizeof(std::complex<double>) * sp.size());
+    });
+}
+int vref_fft_c2r_f32(const int* d, const double* in, float* out) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        Spectrum sp(spectrum_size(g));
+        std::memcpy(sp.data(), in, sizeof(std::complex<double>) * sp.size());
+        ScalarField<float> f(g);
+        fft_inverse(g, sp, f);
+        store_f(f, out);
+    });
+}
+int vref_gradient_f32(const int* d, const float* f, float* out3) {
+    return guard([&] { store_f(gradient(load_scalar_f(grid_of(d), f)), out3); });
+}
+int vref_divergence_f32(const int* d, const float* v3, float* out) {
+    return guard([&] { store_f(divergence(load_vector_f(grid_of(d), v3)), out); });
+}
+int vref_gaussian_smooth_f32(const int* d, const float* f, float* out, const double* sigma) {
+    return guard([&] {
+        store_f(gaussian_smooth(load_scalar_f(grid_of(d), f), {sigma[0], sigma[1], sigma[2]}), out);
+    });
+}
+int vref_apply_reg_operator_f32(const int* d, const float* v3, float* out3, const vr_regnorm* n,
+                                int mode, double beta) {
+    return guard([&] {
+        store_f(apply_reg_operator(load_vector_f(grid_of(d), v3), to_norm(*n),
+                                   static_cast<RegOpMode>(mode), beta),
+                out3);
+    });
+}
+int vref_apply_projection_f32(const int* d, const float* v3, float* out3, int kind, double bv,
+                              double bw) {
+    return guard([&] {
+        store_f(apply_projection(load_vector_f(grid_of(d), v3), static_cast<ProjectionKind>(kind), bv, bw),
+                out3);
+    });
+}
 int vref_continuity_factor(const int* d, const double* div_v, const double* dep3, double dt,
                            double* factor) {
     return guard([&] {

@@ -226,6 +226,13 @@ SIGNATURES = {
     "vr_tricubic_interpolate_f32": (I, [P, DP, DP, DP, I]),
     "vr_trace_characteristics_f32": (I, [P, DP, I, I, DP]),
     "vr_solve_state_f32": (I, [P, DP, DP, I, DP]),
+    "vr_fft_r2c_f32": (I, [P, DP, DP]),
+    "vr_fft_c2r_f32": (I, [P, DP, DP]),
+    "vr_gradient_f32": (I, [P, DP, DP]),
+    "vr_divergence_f32": (I, [P, DP, DP]),
+    "vr_gaussian_smooth_f32": (I, [P, DP, DP, I, C.POINTER(D)]),
+    "vr_apply_reg_operator_f32": (I, [P, DP, DP, C.POINTER(RegNorm), I, D]),
+    "vr_apply_projection_f32": (I, [P, DP, DP, I, D, D]),
     "vr_objective_wait": (I, [P]),
     "vr_objective_apply_reg": (I, [P, DP, I, DP]),
     "vr_objective_apply_K": (I, [P, DP, DP]),

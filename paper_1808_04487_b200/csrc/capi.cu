@@ -676,6 +676,102 @@ int vr_solve_state_f32(vr_ctx* ctx, const float* m_T, const float* v3, int nt, f
     });
 }
 
+// fp32 fields through the fp64 spectral operators: convert at the boundary like the
+// reference's float lane (fft.hpp:12-17), one rounding to fp32 at the end
+extern "C++" template <class Fn>
+void via_f64(vr_ctx* ctx, const float* in, int nin, float* out, int nout, Fn&& fn) {
+    const long long N = ctx->g.N;
+    double* din = vr::dev_alloc(ctx, nin * N);
+    double* dout = out ? vr::dev_alloc(ctx, nout * N) : nullptr;
+    try {
+        if (in) vr::convert_f2d(ctx, in, din, nin * N);
+        fn(din, dout);
+        if (out) vr::convert_d2f(ctx, dout, out, nout * N);
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        vr::dev_free(ctx, din);
+        vr::dev_free(ctx, dout);
+        throw;
+    }
+    vr::dev_free(ctx, din);
+    vr::dev_free(ctx, dout);
+}
+int vr_fft_r2c_f32(vr_ctx* ctx, const float* in, double* out_spectrum) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_fft_r2c_f32");
+        need(in && out_spectrum, "vr_fft_r2c_f32");
+        via_f64(ctx, in, 1, nullptr, 0, [&](double* d, double*) { vr::fft_r2c(ctx, d, out_spectrum); });
+    });
+}
+int vr_fft_c2r_f32(vr_ctx* ctx, const double* spectrum, float* out) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_fft_c2r_f32");
+        need(spectrum && out, "vr_fft_c2r_f32");
+        via_f64(ctx, nullptr, 1, out, 1, [&](double*, double* o) {
+            double* s = vr::spec_buf(ctx, 0);
+            VR_CUDA(cudaMemcpyAsync(s, spectrum, sizeof(double) * 2 * ctx->g.NC,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+            vr::fft_c2r(ctx, s, o, 1.0 / static_cast<double>(ctx->g.Ng), nullptr);
+        });
+    });
+}
+int vr_gradient_f32(vr_ctx* ctx, const float* f, float* out3) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_gradient_f32");
+        need(f && out3, "vr_gradient_f32");
+        via_f64(ctx, f, 1, out3, 3, [&](double* d, double* o) { vr::op_gradient(ctx, d, o); });
+    });
+}
+int vr_divergence_f32(vr_ctx* ctx, const float* v3, float* out) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_divergence_f32");
+        need(v3 && out, "vr_divergence_f32");
+        via_f64(ctx, v3, 3, out, 1, [&](double* d, double* o) { vr::op_divergence(ctx, d, o); });
+    });
+}
+int vr_gaussian_smooth_f32(vr_ctx* ctx, const float* f, float* out, int ncomp,
+                           const double sigma[3]) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_gaussian_smooth_f32");
+        need(f && out && sigma, "vr_gaussian_smooth_f32");
+        check_ncomp(ncomp);
+        for (int a = 0; a < 3; ++a)
+            if (sigma[a] < 0.0) vr::throw_argument("gaussian_smooth: sigma must be >= 0");
+        vr::MultParams mp;
+        mp.kind = vr::Mult::gaussian;
+        const double h[3] = {ctx->g.h1, ctx->g.h2, ctx->g.h3};
+        for (int a = 0; a < 3; ++a) mp.sig2h2[a] = sigma[a] * sigma[a] * h[a] * h[a];
+        via_f64(ctx, f, ncomp, out, ncomp, [&](double* d, double* o) {
+            for (int c = 0; c < ncomp; ++c)
+                vr::spectral_scalar_op(ctx, d + c * ctx->g.N, o + c * ctx->g.N, mp);
+        });
+    });
+}
+int vr_apply_reg_operator_f32(vr_ctx* ctx, const float* v3, float* out3, const vr_regnorm* norm,
+                              int mode, double beta) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_apply_reg_operator_f32");
+        need(v3 && out3 && norm, "vr_apply_reg_operator_f32");
+        vr_model m;
+        vr_model_default(&m);
+        m.norm = *norm;
+        vr::validate_model(m);
+        if (beta <= 0.0) vr::throw_argument("apply_reg_operator: beta must be > 0");
+        if (mode < VR_REGOP_APPLY || mode > VR_REGOP_INVERSE_SQRT)
+            vr::throw_argument("apply_reg_operator: unknown mode");
+        via_f64(ctx, v3, 3, out3, 3, [&](double* d, double* o) { vr::op_reg(ctx, d, o, *norm, mode, beta); });
+    });
+}
+int vr_apply_projection_f32(vr_ctx* ctx, const float* f3, float* out3, int kind, double beta_v,
+                            double beta_w) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_apply_projection_f32");
+        need(f3 && out3, "vr_apply_projection_f32");
+        via_f64(ctx, f3, 3, out3, 3,
+                [&](double* d, double* o) { vr::op_projection(ctx, d, o, kind, beta_v, beta_w); });
+    });
+}
+
 static void adjoint_like(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
                          double* history, double* initial) {
     const long long N = ctx->g.N;

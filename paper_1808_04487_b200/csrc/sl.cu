@@ -663,6 +663,22 @@ __global__ void __launch_bounds__(kThreads)
     const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
     if (i < n && !isfinite(a[i])) *flag = 1;
 }
+__global__ void __launch_bounds__(kThreads)
+    k_f2d(const float* __restrict__ a, double* __restrict__ b, long long n) {
+    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+    if (i < n) b[i] = static_cast<double>(a[i]);
+}
+__global__ void __launch_bounds__(kThreads)
+    k_d2f(const double* __restrict__ a, float* __restrict__ b, long long n) {
+    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+    if (i < n) b[i] = static_cast<float>(a[i]);
+}
+void convert_f2d(vr_ctx* ctx, const float* a, double* b, long long n) {
+    VR_LAUNCH(ctx, "sl_pointwise", k_f2d<<<grid_1d(n, kThreads), kThreads, 0, ctx->stream>>>(a, b, n));
+}
+void convert_d2f(vr_ctx* ctx, const double* a, float* b, long long n) {
+    VR_LAUNCH(ctx, "sl_pointwise", k_d2f<<<grid_1d(n, kThreads), kThreads, 0, ctx->stream>>>(a, b, n));
+}
 bool all_finite_f32(vr_ctx* ctx, const float* a, long long n) {
     VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, sizeof(int), ctx->stream));
     VR_LAUNCH(ctx, "sl_pointwise", k_nonfinite_f32<<<grid_1d(n, kThreads), kThreads, 0, ctx->stream>>>(a, n, ctx->flag_dev));

@@ -350,6 +350,8 @@ void sl_defmap_step(vr_ctx* ctx, const double* u3, const double* dep3, const dou
 void sl_tricubic_f32(vr_ctx* ctx, const float* f, int nfields, const float* pts3, float* out);
 void sl_trace_f32(vr_ctx* ctx, const float* v3, int nt, int direction, float* dep3);
 bool all_finite_f32(vr_ctx* ctx, const float* a, long long n);
+void convert_f2d(vr_ctx* ctx, const float* a, double* b, long long n);
+void convert_d2f(vr_ctx* ctx, const double* a, float* b, long long n);
 // out_c = lam * vt_c
 void sl_scale_vec(vr_ctx* ctx, const double* lam, const double* vt3, double* out3);
 void sl_gradient_dot(vr_ctx* ctx, const double* gm3, const double* w3, double* out);

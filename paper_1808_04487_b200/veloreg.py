@@ -848,6 +848,60 @@ def solve_state_f32(ctx, m_T, v, nt):
     return out.numpy((nt + 1,) + m.shape)
 
 
+def _f32_op(ctx, fn, a, nout, *extra):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    din = DeviceBufferF32.from_host(ctx, a)
+    n = a.size if a.ndim == 3 else a[0].size
+    out = DeviceBufferF32(ctx, nout * n)
+    _lib.call(fn, ctx.handle, din.ptr, out.ptr, *extra)
+    shape = a.shape if a.ndim == 3 else a.shape[1:]
+    return out.numpy(((nout,) if nout > 1 else ()) + tuple(shape))
+
+
+def gradient_f32(ctx, f):
+    """gradient<float> (spectral.cpp:108-122): fp64 transforms, fp32 fields."""
+    return _f32_op(ctx, "vr_gradient_f32", f, 3)
+
+
+def divergence_f32(ctx, v):
+    return _f32_op(ctx, "vr_divergence_f32", v, 1)
+
+
+def apply_reg_operator_f32(ctx, v, norm=None, mode="apply", beta=1.0):
+    norm = norm if norm is not None else make_norm()
+    return _f32_op(ctx, "vr_apply_reg_operator_f32", v, 3, C.byref(norm), _enum(_MODE, mode), float(beta))
+
+
+def apply_projection_f32(ctx, v, kind="incompressible", beta_v=0.0, beta_w=0.0):
+    return _f32_op(ctx, "vr_apply_projection_f32", v, 3, _enum(_PROJ, kind), float(beta_v), float(beta_w))
+
+
+def gaussian_smooth_f32(ctx, f, sigma_voxels):
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    nc = 1 if f.ndim == 3 else f.shape[0]
+    sg = (C.c_double * 3)(*[float(x) for x in sigma_voxels])
+    return _f32_op(ctx, "vr_gaussian_smooth_f32", f, nc, nc, sg)
+
+
+def fft_forward_f32(ctx, f):
+    """fft_forward<float> (fft.hpp:28-29): complex128 half spectrum of an fp32 field."""
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    din = DeviceBufferF32.from_host(ctx, f)
+    out = ctx.empty(1, complex_spectrum=True)
+    _lib.call("vr_fft_r2c_f32", ctx.handle, din.ptr, out.ptr)
+    return out.numpy()
+
+
+def fft_inverse_f32(ctx, spec):
+    """fft_inverse<float> (fft.hpp:31-32): fp32 field from a complex128 half spectrum."""
+    ds = ctx.empty(1, complex_spectrum=True)
+    ds.upload(spec)
+    n1, n2, nh = np.shape(spec)
+    out = DeviceBufferF32(ctx, n1 * n2 * 2 * (nh - 1))
+    _lib.call("vr_fft_c2r_f32", ctx.handle, ds.ptr, out.ptr)
+    return out.numpy((n1, n2, 2 * (nh - 1)))
+
+
 # ---- postprocess (postprocess.hpp:9-56) -----------------------------------------
 def det_deformation_gradient(ctx, v, nt):
     """det grad y by continuity transport (postprocess.cpp:13-29)."""

@@ -53,3 +53,30 @@ def test_solve_state_f32(vr, ref, ctx):
     bad[0, 1, 2, 3] = np.inf
     with pytest.raises(vr.NumericError):
         vr.solve_state_f32(c, mT, bad, 4)
+
+
+@pytest.mark.parametrize("n", [16, 32])
+def test_spectral_f32(vr, ref, ctx, n):
+    # the reference's float instantiations of the spectral module (spectral.cpp:84-222):
+    # fp32 fields, fp64 transforms, one rounding at the end
+    dims = (n, n, n)
+    c = ctx(dims)
+    _, mT, vs = ref.generate_synthetic(dims, 4)
+    w = ref.random_smooth_vector(dims, 3, 55, 1.0)
+    model = vr.make_model()
+    cases = [
+        (vr.gradient_f32(c, mT), ref.gradient_f32(mT)),
+        (vr.divergence_f32(c, w), ref.divergence_f32(w)),
+        (vr.apply_projection_f32(c, w, "incompressible"), ref.apply_projection_f32(w, 1)),
+        (vr.gaussian_smooth_f32(c, mT, (1.0, 2.0, 0.5)), ref.gaussian_smooth_f32(mT, (1.0, 2.0, 0.5))),
+    ]
+    for mode, m in (("apply", 0), ("inverse", 1), ("inverse_sqrt", 2)):
+        cases.append((vr.apply_reg_operator_f32(c, w, model.norm, mode, 1e-2),
+                      ref.apply_reg_operator_f32(w, model.norm, m, 1e-2)))
+    for g, r in cases:
+        assert g.dtype == np.float32 and g.shape == r.shape
+        assert rel_l2(g, r) <= 1e-5
+    spec_g, spec_r = vr.fft_forward_f32(c, mT), ref.fft_forward_f32(mT)
+    # fp64 transform of the same fp32 input (compared as (re, im) pairs)
+    assert rel_l2(np.ascontiguousarray(spec_g).view(np.float64), spec_r.view(np.float64)) <= 1e-10
+    assert rel_l2(vr.fft_inverse_f32(c, spec_r), ref.fft_inverse_f32(spec_r, dims)) <= 1e-5
