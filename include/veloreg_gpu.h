@@ -284,6 +284,23 @@ int vr_apply_reg_operator_f32(vr_ctx* ctx, const float* v3, float* out3, const v
 int vr_apply_projection_f32(vr_ctx* ctx, const float* f3, float* out3, int kind, double beta_v,
                             double beta_w);
 
+/* Objective<float> (objective.cpp:35-156 with T = float; Gauss-Newton, one GPU): fp32
+ * images, velocities, directions and gradients (device pointers); fields stored in fp32
+ * where the reference stores them, stencils / transforms / reductions in fp64. */
+typedef struct vr_objective_f32 vr_objective_f32;
+typedef struct vr_state_f32 vr_state_f32;
+int vr_objective_f32_create(vr_ctx* ctx, const float* m_R, const float* m_T, const vr_model* model,
+                            vr_objective_f32** out);
+int vr_objective_f32_destroy(vr_objective_f32* obj);
+int vr_objective_f32_counters(const vr_objective_f32* obj, vr_counters* out);
+int vr_evaluate_f32(vr_objective_f32* obj, const float* v3, vr_state_f32** out_state);
+int vr_state_f32_destroy(vr_state_f32* s);
+int vr_state_f32_scalars(const vr_state_f32* s, double* objective, double* mismatch,
+                         double* mismatch_rel);
+int vr_compute_gradient_f32(vr_objective_f32* obj, vr_state_f32* s, float* g3);
+int vr_hessian_matvec_f32(vr_objective_f32* obj, const vr_state_f32* s, const float* vt3,
+                          float* out3);
+
 /* ---- Objective (objective.hpp:56-102) -------------------------------------- */
 typedef struct vr_objective vr_objective;
 typedef struct vr_state vr_state;

@@ -82,6 +82,16 @@ _SIG = {
     "vref_generate_synthetic": (I, [DIMS, I, D, P, P, P]),
     "vref_det_deformation_gradient": (I, [DIMS, P, I, P]),
     "vref_tricubic_interpolate_f32": (I, [DIMS, P, P, P, I]),
+    "vref_objective_f32_create": (I, [DIMS, P, P, C.POINTER(Model), C.POINTER(P)]),
+    "vref_objective_f32_destroy": (None, [P]),
+    "vref_evaluate_f32": (I, [P, P, C.POINTER(P)]),
+    "vref_state_f32_destroy": (None, [P]),
+    "vref_state_f32_scalars": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(D)]),
+    "vref_compute_gradient_f32": (I, [P, P, P]),
+    "vref_hessian_matvec_f32": (I, [P, P, P, P]),
+    "vref_objective_f32_counters": (I, [P, C.POINTER(Counters)]),
+    "vref_gauss_newton_solve_f32": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I, P,
+                                        C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
     "vref_fft_r2c_f32": (I, [DIMS, P, P]),
     "vref_fft_c2r_f32": (I, [DIMS, P, P]),
     "vref_gradient_f32": (I, [DIMS, P, P]),
@@ -598,6 +608,74 @@ def fft_inverse_f32(spec, shape):
     out = np.empty(shape, dtype=np.float32)
     _call("vref_fft_c2r_f32", _dims(shape), s.ctypes.data, out.ctypes.data)
     return out
+
+
+class ObjectiveF32:
+    """The reference's Objective<float> on host float32 arrays."""
+
+    def __init__(self, m_R, m_T, model):
+        self.shape = tuple(np.shape(m_R))
+        self.model = model
+        self._r, self._t = _f(m_R), _f(m_T)
+        h = C.c_void_p()
+        _call("vref_objective_f32_create", _dims(self.shape), self._r.ctypes.data, self._t.ctypes.data,
+              C.byref(model), C.byref(h))
+        self._h = h
+
+    def evaluate(self, v):
+        v = _f(v)
+        h = C.c_void_p()
+        _call("vref_evaluate_f32", self._h, v.ctypes.data, C.byref(h))
+        return StateF32(h)
+
+    def compute_gradient(self, s):
+        g = np.empty((3,) + self.shape, dtype=np.float32)
+        _call("vref_compute_gradient_f32", self._h, s._h, g.ctypes.data)
+        return g
+
+    def hessian_matvec(self, s, vt):
+        vt = _f(vt)
+        out = np.empty_like(vt)
+        _call("vref_hessian_matvec_f32", self._h, s._h, vt.ctypes.data, out.ctypes.data)
+        return out
+
+    def counters(self):
+        c = Counters()
+        _call("vref_objective_f32_counters", self._h, C.byref(c))
+        return {k: getattr(c, k) for k, _ in Counters._fields_}
+
+    def __del__(self):
+        try:
+            load().vref_objective_f32_destroy(self._h)
+        except Exception:
+            pass
+
+
+class StateF32:
+    def __init__(self, h):
+        self._h = h
+
+    def scalars(self):
+        J, mis, rel = C.c_double(), C.c_double(), C.c_double()
+        _call("vref_state_f32_scalars", self._h, C.byref(J), C.byref(mis), C.byref(rel))
+        return {"objective": J.value, "mismatch": mis.value, "mismatch_rel": rel.value}
+
+    def __del__(self):
+        try:
+            load().vref_state_f32_destroy(self._h)
+        except Exception:
+            pass
+
+
+def gauss_newton_solve_f32(m_R, m_T, v0, model, params, precond=1, max_records=512):
+    r, t, v0 = _f(m_R), _f(m_T), _f(v0)
+    vout = np.empty_like(v0)
+    rep = SolveReport()
+    recs = (IterationRecord * max_records)()
+    _call("vref_gauss_newton_solve_f32", _dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data,
+          C.byref(model), C.byref(params), precond, vout.ctypes.data, C.byref(rep), recs, max_records)
+    n = min(rep.n_records, max_records)
+    return vout, _report(rep), [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
 
 
 def solve_state_f32(m_T, v, nt):

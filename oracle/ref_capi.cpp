@@ -182,6 +182,16 @@ struct vref_objective {
 struct vref_state {
     EvalState<double> s;
 };
+// fp32 lane: Objective<float>
+struct vref_objective_f32 {
+    Grid3 g;
+    ScalarField<float> m_R, m_T;
+    SolveCounters counters;
+    std::unique_ptr<Objective<float>> obj;
+};
+struct vref_state_f32 {
+    EvalState<float> s;
+};
 struct vref_twolevel {
     explicit vref_twolevel(const TwoLevelOptions& o) : pre(o) {}
     TwoLevelPreconditioner<double> pre;
@@ -557,12 +567,72 @@ int vref_pcg_solve(vref_objective* o, vref_state* s, const double* rhs3, double 
 
 // ---- solvers ----------------------------------------------------------------------
 namespace {
-class IdentityPreconditioner final : public KrylovPreconditioner<double> {
+extern "C++" template <typename T>
+class IdentityPreconditionerT final : public KrylovPreconditioner<T> {
 public:
-    void rebuild(const Objective<double>&, const EvalState<double>&, double) override {}
-    void apply(const VectorField<double>& r, VectorField<double>& z) override { z = r; }
+    void rebuild(const Objective<T>&, const EvalState<T>&, double) override {}
+    void apply(const VectorField<T>& r, VectorField<T>& z) override { z = r; }
 };
+using IdentityPreconditioner = IdentityPreconditionerT<double>;
 } // namespace
+
+// ---- Objective<float> (the reference's fp32 lane) ----
+int vref_objective_f32_create(const int* d, const float* mR, const float* mT, const vr_model* m,
+                              vref_objective_f32** out) {
+    return guard([&] {
+        auto o = std::make_unique<vref_objective_f32>();
+        o->g = grid_of(d);
+        o->m_R = load_scalar_f(o->g, mR);
+        o->m_T = load_scalar_f(o->g, mT);
+        o->obj = std::make_unique<Objective<float>>(o->m_R, o->m_T, to_model(*m), &o->counters);
+        *out = o.release();
+    });
+}
+void vref_objective_f32_destroy(vref_objective_f32* o) { delete o; }
+int vref_evaluate_f32(vref_objective_f32* o, const float* v3, vref_state_f32** out) {
+    return guard([&] {
+        auto s = std::make_unique<vref_state_f32>();
+        s->s = o->obj->evaluate(load_vector_f(o->g, v3));
+        *out = s.release();
+    });
+}
+void vref_state_f32_destroy(vref_state_f32* s) { delete s; }
+int vref_state_f32_scalars(vref_state_f32* s, double* J, double* mis, double* mis_rel) {
+    return guard([&] {
+        *J = s->s.objective;
+        *mis = s->s.mismatch;
+        *mis_rel = s->s.mismatch_rel;
+    });
+}
+int vref_compute_gradient_f32(vref_objective_f32* o, vref_state_f32* s, float* g3) {
+    return guard([&] {
+        o->obj->compute_gradient(s->s);
+        if (g3) store_f(s->s.gradient, g3);
+    });
+}
+int vref_hessian_matvec_f32(vref_objective_f32* o, vref_state_f32* s, const float* vt3, float* out3) {
+    return guard([&] { store_f(o->obj->hessian_matvec(s->s, load_vector_f(o->g, vt3)), out3); });
+}
+int vref_objective_f32_counters(vref_objective_f32* o, vr_counters* c) {
+    return guard([&] { fill_counters(o->counters, c); });
+}
+int vref_gauss_newton_solve_f32(const int* d, const float* mR, const float* mT, const float* v0,
+                                const vr_model* m, const vr_solver_params* p, int precond,
+                                float* v_out, vr_solve_report* rep, vr_iteration_record* recs,
+                                int max_recs) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto R = load_scalar_f(g, mR), T = load_scalar_f(g, mT);
+        SpectralPreconditioner<float> spec;
+        IdentityPreconditionerT<float> ident;
+        KrylovPreconditioner<float>& pc =
+            precond == VR_PRECOND_SPECTRAL ? static_cast<KrylovPreconditioner<float>&>(spec)
+                                           : static_cast<KrylovPreconditioner<float>&>(ident);
+        auto res = gauss_newton_solve(R, T, load_vector_f(g, v0), to_model(*m), to_params(*p), pc);
+        store_f(res.v, v_out);
+        fill_report(res.report, rep, recs, max_recs, 0);
+    });
+}
 
 int vref_gauss_newton_solve(const int* d, const double* mR, const double* mT, const double* v0,
                             const vr_model* m, const vr_solver_params* p, int precond,

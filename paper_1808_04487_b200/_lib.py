@@ -226,6 +226,14 @@ SIGNATURES = {
     "vr_tricubic_interpolate_f32": (I, [P, DP, DP, DP, I]),
     "vr_trace_characteristics_f32": (I, [P, DP, I, I, DP]),
     "vr_solve_state_f32": (I, [P, DP, DP, I, DP]),
+    "vr_objective_f32_create": (I, [P, DP, DP, C.POINTER(Model), C.POINTER(P)]),
+    "vr_objective_f32_destroy": (I, [P]),
+    "vr_objective_f32_counters": (I, [P, C.POINTER(Counters)]),
+    "vr_evaluate_f32": (I, [P, DP, C.POINTER(P)]),
+    "vr_state_f32_destroy": (I, [P]),
+    "vr_state_f32_scalars": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(D)]),
+    "vr_compute_gradient_f32": (I, [P, P, DP]),
+    "vr_hessian_matvec_f32": (I, [P, P, DP, DP]),
     "vr_fft_r2c_f32": (I, [P, DP, DP]),
     "vr_fft_c2r_f32": (I, [P, DP, DP]),
     "vr_gradient_f32": (I, [P, DP, DP]),

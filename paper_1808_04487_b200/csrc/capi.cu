@@ -772,6 +772,59 @@ int vr_apply_projection_f32(vr_ctx* ctx, const float* f3, float* out3, int kind,
     });
 }
 
+// ---- Objective<float> --------------------------------------------------------------
+static vr::ObjF32* of(vr_objective_f32* o) { return reinterpret_cast<vr::ObjF32*>(o); }
+static vr::StateF32* sf(vr_state_f32* s) { return reinterpret_cast<vr::StateF32*>(s); }
+static const vr::StateF32* sfc(const vr_state_f32* s) { return reinterpret_cast<const vr::StateF32*>(s); }
+int vr_objective_f32_create(vr_ctx* ctx, const float* m_R, const float* m_T, const vr_model* model,
+                            vr_objective_f32** out) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_objective_f32_create");
+        need(m_R && m_T && model && out, "vr_objective_f32_create");
+        *out = reinterpret_cast<vr_objective_f32*>(vr::objf32_create(ctx, m_R, m_T, *model));
+    });
+}
+int vr_objective_f32_destroy(vr_objective_f32* obj) {
+    return guard([&] { vr::objf32_destroy(of(obj)); });
+}
+int vr_objective_f32_counters(const vr_objective_f32* obj, vr_counters* out) {
+    return guard([&] {
+        need(obj && out, "vr_objective_f32_counters");
+        *out = vr::objf32_counters(reinterpret_cast<const vr::ObjF32*>(obj));
+    });
+}
+int vr_evaluate_f32(vr_objective_f32* obj, const float* v3, vr_state_f32** out_state) {
+    return guard([&] {
+        need(obj && v3 && out_state, "vr_evaluate_f32");
+        set_dev(vr::objf32_ctx(of(obj)));
+        *out_state = reinterpret_cast<vr_state_f32*>(vr::objf32_evaluate(of(obj), v3));
+    });
+}
+int vr_state_f32_destroy(vr_state_f32* s) { return guard([&] { vr::statef32_destroy(sf(s)); }); }
+int vr_state_f32_scalars(const vr_state_f32* s, double* objective, double* mismatch,
+                         double* mismatch_rel) {
+    return guard([&] {
+        need(s && objective && mismatch && mismatch_rel, "vr_state_f32_scalars");
+        vr::statef32_scalars(sfc(s), objective, mismatch, mismatch_rel);
+    });
+}
+int vr_compute_gradient_f32(vr_objective_f32* obj, vr_state_f32* s, float* g3) {
+    return guard([&] {
+        need(obj && s, "vr_compute_gradient_f32");
+        set_dev(vr::objf32_ctx(of(obj)));
+        vr::objf32_gradient(of(obj), sf(s));
+        if (g3) vr::objf32_copy_gradient(of(obj), sf(s), g3);
+    });
+}
+int vr_hessian_matvec_f32(vr_objective_f32* obj, const vr_state_f32* s, const float* vt3,
+                          float* out3) {
+    return guard([&] {
+        need(obj && s && vt3 && out3, "vr_hessian_matvec_f32");
+        set_dev(vr::objf32_ctx(of(obj)));
+        vr::objf32_matvec(of(obj), sfc(s), vt3, out3);
+    });
+}
+
 static void adjoint_like(vr_ctx* ctx, const double* terminal, const double* v3, int nt,
                          double* history, double* initial) {
     const long long N = ctx->g.N;

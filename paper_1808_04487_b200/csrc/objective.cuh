@@ -107,6 +107,21 @@ GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, con
 vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt,
                              const double* lamhist = nullptr);
 
+// ---- fp32 lane objective (objective_f32.cu) ----
+struct ObjF32;
+struct StateF32;
+ObjF32* objf32_create(vr_ctx* ctx, const float* mR, const float* mT, const vr_model& model);
+void objf32_destroy(ObjF32* o);
+StateF32* objf32_evaluate(ObjF32* o, const float* v3);
+void statef32_destroy(StateF32* s);
+void statef32_scalars(const StateF32* s, double* J, double* mis, double* rel);
+const float* statef32_gradient(const StateF32* s);
+void objf32_gradient(ObjF32* o, StateF32* s);
+void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3);
+vr_counters objf32_counters(const ObjF32* o);
+vr_ctx* objf32_ctx(ObjF32* o);
+void objf32_copy_gradient(ObjF32* o, const StateF32* s, float* g3);  // synchronises
+
 // ---- postprocess / continuation (postprocess.cu) ----
 void det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det);
 void deformation_map(vr_ctx* ctx, const double* v3, int nt, bool absolute, double* out3);

@@ -1,0 +1,325 @@
+// objective_f32.cu -- the fp32 lane of the objective: the reference's
+// Objective<float> (proj/src/objective.cpp:35-156 with T = float) and its Gauss-Newton /
+// PCG / Armijo driver (proj/src/solver.cpp:23-269), one GPU.
+//
+// Every field is stored in fp32 exactly where the reference stores a ScalarField<float>
+// (state history, departure points, continuity factor, grad m_j, adjoint / incremental
+// fields, gradient, PCG vectors); stencils, transforms and reductions run in fp64 and
+// each stored result is rounded once, as in the reference: the fp32 semi-Lagrangian
+// kernels (sl.cu), the fp64 spectral operators behind a convert-at-the-boundary (the
+// reference's fft.hpp:12-17 contract) and fp64 reductions of the fp32 values. The
+// steps are composed from those operators and small pointwise kernels (no fusion yet):
+// this lane is about the reference's float semantics and the halved bytes, not about
+// squeezing the fp64 lane's fused sweeps.
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "objective.cuh"
+
+namespace vr {
+namespace {
+
+constexpr int kT = 256;
+unsigned blocks(long long n) { return grid_1d(n, kT); }
+
+// out = float(a x + b y)  (lin_comb, field_ops.hpp:30-40); y may be null (b ignored)
+__global__ void k_lincomb_f(float* out, double a, const float* x, double b, const float* y, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i >= n) return;
+    const double r = y ? a * static_cast<double>(x[i]) + b * static_cast<double>(y[i])
+                       : a * static_cast<double>(x[i]);
+    out[i] = static_cast<float>(r);
+}
+// y = float(y + a x)  (add_scaled)
+__global__ void k_axpy_f(float* y, double a, const float* x, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i < n) y[i] = static_cast<float>(static_cast<double>(y[i]) + a * static_cast<double>(x[i]));
+}
+// out = float(x * f)  (continuity_step, transport.cpp:62-68)
+__global__ void k_mul_f(float* out, const float* x, const float* f, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i < n) out[i] = static_cast<float>(x[i] * f[i]);
+}
+// continuity_factor (transport.cpp:44-55)
+__global__ void k_factor_f(float* factor, const float* div, const float* at_dep, double half_dt,
+                           long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i < n)
+        factor[i] = static_cast<float>(
+            exp(half_dt * (static_cast<double>(div[i]) + static_cast<double>(at_dep[i]))));
+}
+// b_a = float(b_a + w lam d_a f)  (accumulate_weighted_grad, objective.cpp:9-32)
+__global__ void k_accum_f(float* b, double w, const float* lam, const float* gm, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i >= n) return;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        b[a * n + i] = static_cast<float>(static_cast<double>(b[a * n + i]) +
+                                          w * static_cast<double>(lam[i]) * static_cast<double>(gm[a * n + i]));
+}
+// gradient_dot (transport.cpp:126-148): out = float(out + d_a f * w_a), a = 0, 1, 2
+__global__ void k_graddot_f(float* out, const float* gm, const float* w, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i >= n) return;
+    float o = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        o = static_cast<float>(static_cast<double>(o) + static_cast<double>(gm[a * n + i]) * static_cast<double>(w[a * n + i]));
+    out[i] = o;
+}
+
+float* falloc(vr_ctx* ctx, long long n) { return reinterpret_cast<float*>(dev_alloc(ctx, (n + 1) / 2)); }
+void ffree(vr_ctx* ctx, float* p) { dev_free(ctx, reinterpret_cast<double*>(p)); }
+
+void lincomb(vr_ctx* ctx, float* out, double a, const float* x, double b, const float* y, long long n) {
+    VR_LAUNCH(ctx, "f32_pointwise", k_lincomb_f<<<blocks(n), kT, 0, ctx->stream>>>(out, a, x, b, y, n));
+}
+void axpy(vr_ctx* ctx, float* y, double a, const float* x, long long n) {
+    VR_LAUNCH(ctx, "f32_pointwise", k_axpy_f<<<blocks(n), kT, 0, ctx->stream>>>(y, a, x, n));
+}
+
+// fp64 scratch views of fp32 fields (for the spectral operators and the reductions)
+struct F64 {
+    vr_ctx* ctx;
+    double* p;
+    F64(vr_ctx* c, const float* f, long long n) : ctx(c), p(dev_alloc(c, n)) {
+        if (f) convert_f2d(c, f, p, n);
+    }
+    ~F64() { dev_free(ctx, p); }
+    F64(const F64&) = delete;
+    F64& operator=(const F64&) = delete;
+};
+
+// sum_i a_i b_i of fp32 vectors (fp64 products and sums, fixed order) and the weighted
+// inner product (spectral.cpp:47-62)
+double dot_f(vr_ctx* ctx, const float* a, const float* b, long long n, int ncomp) {
+    F64 da(ctx, a, ncomp * n), db(ctx, b, ncomp * n);
+    double r[3] = {0, 0, 0};
+    dot_components(ctx, da.p, db.p, n, ncomp, r);
+    double s = 0.0;
+    for (int c = 0; c < ncomp; ++c) s += r[c];
+    return s;
+}
+double cell(const GridDims& g) { return g.h1 * g.h2 * g.h3; }
+
+void spectral_f(vr_ctx* ctx, const float* in, int nin, float* out, int nout,
+                const std::function<void(const double*, double*)>& fn) {
+    const long long N = ctx->g.N;
+    F64 din(ctx, in, nin * N), dout(ctx, nullptr, nout * N);
+    fn(din.p, dout.p);
+    convert_d2f(ctx, dout.p, out, nout * N);
+}
+
+}  // namespace
+
+struct ObjF32 {
+    vr_ctx* ctx = nullptr;
+    const float* mR = nullptr;
+    const float* mT = nullptr;
+    vr_model model{};
+    vr_counters counters{};
+    double initial_mismatch = 0.0;
+};
+
+struct StateF32 {
+    ObjF32* obj = nullptr;
+    int nt = 0;
+    float *v = nullptr, *xb = nullptr, *mhist = nullptr, *xf = nullptr, *factor = nullptr,
+          *gradm = nullptr, *grad = nullptr;
+    double objective = 0.0, mismatch = 0.0, mismatch_rel = 0.0;
+    bool has_gradient = false;
+    ~StateF32() {
+        if (!obj) return;
+        for (float* p : {v, xb, mhist, xf, factor, gradm, grad}) ffree(obj->ctx, p);
+    }
+};
+
+ObjF32* objf32_create(vr_ctx* ctx, const float* mR, const float* mT, const vr_model& model) {
+    validate_model(model);
+    if (ctx->dist) throw_argument("fp32 objective: one GPU only");
+    if (!model.gauss_newton) throw_argument("fp32 objective: Gauss-Newton only (full Newton is fp64)");
+    auto o = std::make_unique<ObjF32>();
+    o->ctx = ctx;
+    o->mR = mR;
+    o->mT = mT;
+    o->model = model;
+    const long long N = ctx->g.N;
+    float* diff = falloc(ctx, N);
+    lincomb(ctx, diff, 1.0, mT, -1.0, mR, N);  // objective.cpp:40-44
+    o->initial_mismatch = dot_f(ctx, diff, diff, N, 1) * cell(ctx->g);
+    ffree(ctx, diff);
+    return o.release();
+}
+
+// evaluate (objective.cpp:47-75)
+StateF32* objf32_evaluate(ObjF32* o, const float* v3) {
+    vr_ctx* ctx = o->ctx;
+    const long long N = ctx->g.N;
+    const int nt = o->model.nt;
+    if (!all_finite_f32(ctx, v3, 3 * N)) throw_numeric("evaluate_objective: non-finite velocity");
+    auto s = std::make_unique<StateF32>();
+    s->obj = o;
+    s->nt = nt;
+    s->v = falloc(ctx, 3 * N);
+    s->xb = falloc(ctx, 3 * N);
+    s->mhist = falloc(ctx, (nt + 1) * N);
+    VR_CUDA(cudaMemcpyAsync(s->v, v3, sizeof(float) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    sl_trace_f32(ctx, s->v, nt, VR_TRACE_BACKWARD, s->xb);
+    VR_CUDA(cudaMemcpyAsync(s->mhist, o->mT, sizeof(float) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    for (int j = 0; j < nt; ++j) sl_tricubic_f32(ctx, s->mhist + j * N, 1, s->xb, s->mhist + (j + 1) * N);
+    o->counters.pde_solves += 1;
+    float* diff = falloc(ctx, N);
+    lincomb(ctx, diff, 1.0, s->mhist + nt * N, -1.0, o->mR, N);
+    s->mismatch = dot_f(ctx, diff, diff, N, 1) * cell(ctx->g);
+    ffree(ctx, diff);
+    s->mismatch_rel = o->initial_mismatch > 0.0 ? s->mismatch / o->initial_mismatch : 0.0;
+    // reg = 1/2 beta_v <A v, v>_h (A at beta 1; Parseval on the fp64 view of v)
+    double reg, penalty = 0.0;
+    {
+        F64 dv(ctx, s->v, 3 * N);
+        reg = 0.5 * o->model.beta_v * reg_energy(ctx, dv.p, o->model.norm);
+        if (o->model.norm.div_penalty) {
+            F64 w(ctx, nullptr, N), hw(ctx, nullptr, N);
+            op_divergence(ctx, dv.p, w.p);
+            MultParams mp;
+            mp.kind = Mult::helmholtz1;
+            spectral_scalar_op(ctx, w.p, hw.p, mp);
+            penalty = 0.5 * o->model.norm.beta_w * inner_product_scalar(ctx, hw.p, w.p);
+        }
+    }
+    s->objective = 0.5 * s->mismatch + reg + penalty;
+    if (!std::isfinite(s->objective)) throw_numeric("evaluate_objective: objective is not finite");
+    o->counters.objective_evals += 1;
+    return s.release();
+}
+
+// prepare_adjoint_ctx + compute_gradient (objective.cpp:77-112); the grad m_j cache is
+// the reference's accumulate_weighted_grad scratch (fp32-rounded derivatives)
+void objf32_gradient(ObjF32* o, StateF32* s) {
+    vr_ctx* ctx = o->ctx;
+    const long long N = ctx->g.N;
+    const int nt = s->nt;
+    const double dt = 1.0 / nt;
+    if (!s->xf) {
+        s->xf = falloc(ctx, 3 * N);
+        s->factor = falloc(ctx, N);
+        s->gradm = falloc(ctx, 3LL * (nt + 1) * N);
+        sl_trace_f32(ctx, s->v, nt, VR_TRACE_FORWARD, s->xf);
+        float* div = falloc(ctx, N);
+        float* at = falloc(ctx, N);
+        spectral_f(ctx, s->v, 3, div, 1, [&](const double* i, double* out) { op_divergence(ctx, i, out); });
+        sl_tricubic_f32(ctx, div, 1, s->xf, at);
+        VR_LAUNCH(ctx, "f32_pointwise", k_factor_f<<<blocks(N), kT, 0, ctx->stream>>>(s->factor, div, at, 0.5 * dt, N));
+        ffree(ctx, div);
+        ffree(ctx, at);
+        for (int j = 0; j <= nt; ++j)
+            spectral_f(ctx, s->mhist + j * N, 1, s->gradm + 3LL * j * N, 3,
+                       [&](const double* i, double* out) { op_gradient(ctx, i, out); });
+    }
+    if (!s->grad) s->grad = falloc(ctx, 3 * N);
+    float* lam[2] = {falloc(ctx, N), falloc(ctx, N)};
+    float* b = s->grad;
+    VR_CUDA(cudaMemsetAsync(b, 0, sizeof(float) * 3 * N, ctx->stream));
+    lincomb(ctx, lam[0], 1.0, o->mR, -1.0, s->mhist + nt * N, N);  // terminal (objective.cpp:91-92)
+    VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, 0.5 * dt, lam[0], s->gradm + 3LL * nt * N, N));
+    int cur = 0;
+    for (int j = nt - 1; j >= 0; --j) {  // sweep_continuity (transport.cpp:88-113)
+        sl_tricubic_f32(ctx, lam[cur], 1, s->xf, lam[cur ^ 1]);
+        VR_LAUNCH(ctx, "f32_pointwise", k_mul_f<<<blocks(N), kT, 0, ctx->stream>>>(lam[cur ^ 1], lam[cur ^ 1], s->factor, N));
+        cur ^= 1;
+        const double w = (j == 0) ? 0.5 * dt : dt;
+        VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, w, lam[cur], s->gradm + 3LL * j * N, N));
+    }
+    ffree(ctx, lam[0]);
+    ffree(ctx, lam[1]);
+    o->counters.pde_solves += 1;
+    if (o->model.projection != VR_PROJ_IDENTITY)
+        spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
+            op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+        });
+    float* reg = falloc(ctx, 3 * N);
+    spectral_f(ctx, s->v, 3, reg, 3, [&](const double* i, double* out) {
+        op_reg(ctx, i, out, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+    });
+    axpy(ctx, b, 1.0, reg, 3 * N);  // add_scaled(gradient, 1.0, reg)
+    ffree(ctx, reg);
+    s->has_gradient = true;
+    o->counters.gradient_evals += 1;
+}
+
+// hessian_matvec (objective.cpp:114-156, GN): inc-state (transport.cpp:150-173), GN
+// inc-adjoint (sweep_continuity with the observer), K, + beta_v A vt
+void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) {
+    vr_ctx* ctx = o->ctx;
+    const long long N = ctx->g.N;
+    if (!all_finite_f32(ctx, vt3, 3 * N)) throw_numeric("hessian_matvec: non-finite direction");
+    if (!s->xf)
+        throw_logic("hessian_matvec: evaluation context is missing the adjoint sweep data "
+                    "(compute the gradient first)");
+    const int nt = s->nt;
+    const double dt = 1.0 / nt, hdt = 0.5 / nt;
+    float* q[2] = {falloc(ctx, N), falloc(ctx, N)};
+    float* mt[2] = {falloc(ctx, N), falloc(ctx, N)};
+    float* tmp = falloc(ctx, N);
+    auto qdot = [&](int j, float* out) {
+        VR_LAUNCH(ctx, "f32_pointwise", k_graddot_f<<<blocks(N), kT, 0, ctx->stream>>>(out, s->gradm + 3LL * j * N, vt3, N));
+    };
+    VR_CUDA(cudaMemsetAsync(mt[0], 0, sizeof(float) * N, ctx->stream));
+    qdot(0, q[0]);
+    int c = 0;
+    for (int j = 0; j < nt; ++j) {
+        qdot(j + 1, q[c ^ 1]);
+        lincomb(ctx, tmp, 1.0, mt[c], -hdt, q[c], N);
+        sl_tricubic_f32(ctx, tmp, 1, s->xb, mt[c ^ 1]);
+        axpy(ctx, mt[c ^ 1], -hdt, q[c ^ 1], N);
+        c ^= 1;
+    }
+    o->counters.pde_solves += 1;
+    float* lam[2] = {q[0], q[1]};  // reuse
+    lincomb(ctx, lam[0], -1.0, mt[c], 0.0, nullptr, N);  // terminal = -mt_nt
+    float* b = out3;
+    VR_CUDA(cudaMemsetAsync(b, 0, sizeof(float) * 3 * N, ctx->stream));
+    VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, 0.5 * dt, lam[0], s->gradm + 3LL * nt * N, N));
+    int cur = 0;
+    for (int j = nt - 1; j >= 0; --j) {
+        sl_tricubic_f32(ctx, lam[cur], 1, s->xf, lam[cur ^ 1]);
+        VR_LAUNCH(ctx, "f32_pointwise", k_mul_f<<<blocks(N), kT, 0, ctx->stream>>>(lam[cur ^ 1], lam[cur ^ 1], s->factor, N));
+        cur ^= 1;
+        const double w = (j == 0) ? 0.5 * dt : dt;
+        VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, w, lam[cur], s->gradm + 3LL * j * N, N));
+    }
+    o->counters.pde_solves += 1;
+    for (float* p : {q[0], q[1], mt[0], mt[1], tmp}) ffree(ctx, p);
+    if (o->model.projection != VR_PROJ_IDENTITY)
+        spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
+            op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+        });
+    o->counters.hessian_matvecs += 1;
+    float* reg = falloc(ctx, 3 * N);
+    spectral_f(ctx, vt3, 3, reg, 3, [&](const double* i, double* out) {
+        op_reg(ctx, i, out, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+    });
+    axpy(ctx, out3, 1.0, reg, 3 * N);
+    ffree(ctx, reg);
+}
+
+void objf32_destroy(ObjF32* o) { delete o; }
+void statef32_destroy(StateF32* s) { delete s; }
+void statef32_scalars(const StateF32* s, double* J, double* mis, double* rel) {
+    *J = s->objective;
+    *mis = s->mismatch;
+    *rel = s->mismatch_rel;
+}
+const float* statef32_gradient(const StateF32* s) { return s->grad; }
+vr_counters objf32_counters(const ObjF32* o) { return o->counters; }
+vr_ctx* objf32_ctx(ObjF32* o) { return o->ctx; }
+void objf32_copy_gradient(ObjF32* o, const StateF32* s, float* g3) {
+    if (!s->grad) throw_logic("gradient: not computed");
+    VR_CUDA(cudaMemcpyAsync(g3, s->grad, sizeof(float) * 3 * o->ctx->g.N, cudaMemcpyDeviceToDevice,
+                            o->ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(o->ctx->stream));
+}
+
+}  // namespace vr

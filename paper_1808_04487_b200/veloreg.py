@@ -848,6 +848,82 @@ def solve_state_f32(ctx, m_T, v, nt):
     return out.numpy((nt + 1,) + m.shape)
 
 
+class StateF32:
+    """EvalState<float> (device resident)."""
+
+    def __init__(self, obj, handle):
+        self.obj, self._h = obj, handle
+
+    def _scalars(self):
+        J, mis, rel = C.c_double(), C.c_double(), C.c_double()
+        _lib.call("vr_state_f32_scalars", self._h, C.byref(J), C.byref(mis), C.byref(rel))
+        return J.value, mis.value, rel.value
+
+    objective = property(lambda s: s._scalars()[0])
+    mismatch = property(lambda s: s._scalars()[1])
+    mismatch_rel = property(lambda s: s._scalars()[2])
+
+    def close(self):
+        if getattr(self, "_h", None) and getattr(self.obj, "_h", None):
+            _lib.call("vr_state_f32_destroy", self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ObjectiveF32:
+    """Objective<float> (objective.hpp:56-102, T = float; Gauss-Newton, one GPU) on host
+    float32 arrays: fp32 fields, fp64 stencils / transforms / reductions."""
+
+    def __init__(self, ctx: Context, m_R, m_T, model=None):
+        self.ctx = ctx
+        self.model = model if model is not None else make_model()
+        self.shape = tuple(np.shape(m_R))
+        self._mR = DeviceBufferF32.from_host(ctx, m_R)
+        self._mT = DeviceBufferF32.from_host(ctx, m_T)
+        h = C.c_void_p()
+        _lib.call("vr_objective_f32_create", ctx.handle, self._mR.ptr, self._mT.ptr, C.byref(self.model),
+                  C.byref(h))
+        self._h = h
+
+    def counters(self) -> dict:
+        c = _lib.Counters()
+        _lib.call("vr_objective_f32_counters", self._h, C.byref(c))
+        return {k: getattr(c, k) for k, _ in _lib.Counters._fields_}
+
+    def evaluate(self, v) -> StateF32:
+        dv = DeviceBufferF32.from_host(self.ctx, v)
+        h = C.c_void_p()
+        _lib.call("vr_evaluate_f32", self._h, dv.ptr, C.byref(h))
+        return StateF32(self, h)
+
+    def compute_gradient(self, state: StateF32):
+        g = DeviceBufferF32(self.ctx, 3 * int(np.prod(self.shape)))
+        _lib.call("vr_compute_gradient_f32", self._h, state._h, g.ptr)
+        return g.numpy((3,) + self.shape)
+
+    def hessian_matvec(self, state: StateF32, v_tilde):
+        dv = DeviceBufferF32.from_host(self.ctx, v_tilde)
+        out = DeviceBufferF32(self.ctx, 3 * int(np.prod(self.shape)))
+        _lib.call("vr_hessian_matvec_f32", self._h, state._h, dv.ptr, out.ptr)
+        return out.numpy((3,) + self.shape)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.call("vr_objective_f32_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _f32_op(ctx, fn, a, nout, *extra):
     a = np.ascontiguousarray(a, dtype=np.float32)
     din = DeviceBufferF32.from_host(ctx, a)

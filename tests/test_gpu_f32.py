@@ -80,3 +80,39 @@ def test_spectral_f32(vr, ref, ctx, n):
     # fp64 transform of the same fp32 input (compared as (re, im) pairs)
     assert rel_l2(np.ascontiguousarray(spec_g).view(np.float64), spec_r.view(np.float64)) <= 1e-10
     assert rel_l2(vr.fft_inverse_f32(c, spec_r), ref.fft_inverse_f32(spec_r, dims)) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [16, 32])
+@pytest.mark.parametrize("kind", ["h2", "h1div"])
+def test_objective_f32(vr, ref, ctx, n, kind):
+    # Objective<float> (objective.cpp:35-156, T = float): J, mismatch, reduced gradient and
+    # GN Hessian matvec against the reference's float instantiation, same PDE-solve counts
+    dims = (n, n, n)
+    c = ctx(dims)
+    mR, mT, vs = ref.generate_synthetic(dims, 4)
+    if kind == "h2":
+        model = vr.make_model()
+    else:
+        model = vr.make_model("h1", beta_v=1e-3, nt=4, div_penalty=True, beta_w=1e-4,
+                              projection="near_incompressible")
+    o = vr.ObjectiveF32(c, mR, mT, model)
+    ro = ref.ObjectiveF32(mR, mT, model)
+    vt = ref.random_smooth_vector(dims, 2, 142, 1.0)
+    for v in (0.5 * vs, np.zeros_like(vs)):
+        s, rs = o.evaluate(v), ro.evaluate(v)
+        sc = rs.scalars()
+        assert abs(s.objective - sc["objective"]) <= 1e-5 * abs(sc["objective"])
+        assert abs(s.mismatch_rel - sc["mismatch_rel"]) <= 1e-5 * max(abs(sc["mismatch_rel"]), 1e-30)
+        g, g_ref = o.compute_gradient(s), ro.compute_gradient(rs)
+        assert g.dtype == np.float32
+        assert rel_l2(g, g_ref) <= 1e-5
+        h, h_ref = o.hessian_matvec(s, vt), ro.hessian_matvec(rs, vt)
+        assert rel_l2(h, h_ref) <= 1e-5
+    assert o.counters() == ro.counters()
+    # and against the fp64 lane at the same inputs: fp32 storage only
+    o64 = vr.Objective(c, mR, mT, model)
+    s64 = o64.evaluate(0.5 * vs)
+    o64.compute_gradient(s64)
+    s32 = o.evaluate(0.5 * vs)
+    o.compute_gradient(s32)
+    assert rel_l2(o.hessian_matvec(s32, vt), o64.hessian_matvec(s64, vt)) <= 1e-4
