@@ -300,6 +300,12 @@ int vr_state_f32_scalars(const vr_state_f32* s, double* objective, double* misma
 int vr_compute_gradient_f32(vr_objective_f32* obj, vr_state_f32* s, float* g3);
 int vr_hessian_matvec_f32(vr_objective_f32* obj, const vr_state_f32* s, const float* vt3,
                           float* out3);
+/* gauss_newton_solve<float> (solver.cpp:154-269; PCG and Armijo on fp32 vectors with fp64
+ * scalars); precond VR_PRECOND_NONE or VR_PRECOND_SPECTRAL; fp32 device pointers */
+int vr_gauss_newton_solve_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
+                              const vr_model* model, const vr_solver_params* params, int precond,
+                              float* v_out, vr_solve_report* report, vr_iteration_record* records,
+                              int max_records);
 
 /* ---- Objective (objective.hpp:56-102) -------------------------------------- */
 typedef struct vr_objective vr_objective;

@@ -1147,6 +1147,19 @@ int vr_gauss_newton_solve(vr_ctx* ctx, const double* m_R, const double* m_T, con
         copy_records(r, records, max_records, 0);
     });
 }
+int vr_gauss_newton_solve_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
+                              const vr_model* model, const vr_solver_params* params, int precond,
+                              float* v_out, vr_solve_report* report, vr_iteration_record* records,
+                              int max_records) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_gauss_newton_solve_f32");
+        need(m_R && m_T && v0 && model && params && v_out && report, "vr_gauss_newton_solve_f32");
+        vr::GnResult r = vr::gauss_newton_solve_f32(ctx, m_R, m_T, v0, *model, *params, precond, v_out);
+        *report = r.report;
+        copy_records(r, records, max_records, 0);
+    });
+}
+
 int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
                               const vr_model* model, const vr_solver_params* params, int precond,
                               double* v_out, vr_solve_report* reports, int max_levels,

@@ -121,6 +121,9 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3);
 vr_counters objf32_counters(const ObjF32* o);
 vr_ctx* objf32_ctx(ObjF32* o);
 void objf32_copy_gradient(ObjF32* o, const StateF32* s, float* g3);  // synchronises
+GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, const float* v0,
+                                const vr_model& model, const vr_solver_params& params, int precond,
+                                float* v_out);
 
 // ---- postprocess / continuation (postprocess.cu) ----
 void det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det);

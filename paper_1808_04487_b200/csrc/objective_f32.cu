@@ -305,6 +305,177 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
     ffree(ctx, reg);
 }
 
+// ---- solver.cpp:51-269 on fp32 vectors (fp64 scalars) -------------------------------
+namespace {
+double norm_f(vr_ctx* ctx, const float* a, long long n) { return std::sqrt(dot_f(ctx, a, a, n, 1)); }
+
+vr_pcg_stats pcg_f32(ObjF32* o, const StateF32* s, const float* rhs, double rel_tol, int max_iter,
+                     int precond, float* x) {
+    vr_ctx* ctx = o->ctx;
+    const long long n3 = 3 * ctx->g.N;
+    vr_pcg_stats st{};
+    VR_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * n3, ctx->stream));
+    const double r0 = norm_f(ctx, rhs, n3);
+    if (r0 == 0.0) {
+        st.converged = 1;
+        return st;
+    }
+    const double target = rel_tol * r0;
+    float *r = falloc(ctx, n3), *z = falloc(ctx, n3), *sd = falloc(ctx, n3), *Hs = falloc(ctx, n3);
+    auto pc = [&](const float* in, float* out) {  // SpectralPreconditioner: (beta_v A)^-1
+        if (precond == VR_PRECOND_SPECTRAL)
+            spectral_f(ctx, in, 3, out, 3, [&](const double* i, double* oo) {
+                op_reg(ctx, i, oo, o->model.norm, VR_REGOP_INVERSE, o->model.beta_v);
+            });
+        else
+            VR_CUDA(cudaMemcpyAsync(out, in, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+    };
+    VR_CUDA(cudaMemcpyAsync(r, rhs, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+    pc(r, z);
+    VR_CUDA(cudaMemcpyAsync(sd, z, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+    double rz = dot_f(ctx, r, z, n3, 1);
+    bool done = false;
+    for (int it = 0; it < max_iter && !done; ++it) {
+        objf32_matvec(o, s, sd, Hs);
+        const double sHs = dot_f(ctx, sd, Hs, n3, 1);
+        if (sHs <= 0.0) {
+            st.negative_curvature = 1;
+            if (it == 0) VR_CUDA(cudaMemcpyAsync(x, z, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+            st.iterations = it + 1;
+            st.rel_residual = norm_f(ctx, r, n3) / r0;
+            done = true;
+            break;
+        }
+        const double kappa = rz / sHs;
+        axpy(ctx, x, kappa, sd, n3);
+        axpy(ctx, r, -kappa, Hs, n3);
+        st.iterations = it + 1;
+        const double rn = norm_f(ctx, r, n3);
+        st.rel_residual = rn / r0;
+        if (rn < target) {
+            st.converged = 1;
+            done = true;
+            break;
+        }
+        pc(r, z);
+        const double rz_new = dot_f(ctx, r, z, n3, 1);
+        const double mu = rz_new / rz;
+        rz = rz_new;
+        lincomb(ctx, sd, 1.0, z, mu, sd, n3);
+    }
+    if (!done) st.hit_max_iterations = 1;
+    for (float* p : {r, z, sd, Hs}) ffree(ctx, p);
+    return st;
+}
+}  // namespace
+
+GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, const float* v0,
+                                const vr_model& model, const vr_solver_params& params, int precond,
+                                float* v_out) {
+    validate_params(params);
+    if (precond != VR_PRECOND_NONE && precond != VR_PRECOND_SPECTRAL)
+        throw_argument("gauss_newton_solve_f32: preconditioner must be none or spectral");
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    const long long n3 = 3 * ctx->g.N;
+    const double hc = cell(ctx->g);
+    GnResult res;
+    vr_solve_report& rep = res.report;
+    rep.stop = VR_STOP_MAX_ITERATIONS;
+    std::unique_ptr<ObjF32> obj(objf32_create(ctx, mR, mT, model));
+    std::unique_ptr<StateF32> state(objf32_evaluate(obj.get(), v0));
+    objf32_gradient(obj.get(), state.get());
+    auto record = [&](int k, double gn, double g0) {
+        vr_iteration_record r{};
+        r.k = k;
+        r.objective = state->objective;
+        r.mismatch_rel = state->mismatch_rel;
+        r.grad_norm = gn;
+        r.grad_rel = g0 > 0 ? gn / g0 : 0.0;
+        r.fine_matvecs = obj->counters.hessian_matvecs;
+        r.pde_solves = obj->counters.pde_solves;
+        r.wall_time_s = elapsed();
+        return r;
+    };
+    const double g0 = norm_f(ctx, state->grad, n3);
+    rep.grad0 = g0;
+    res.records.push_back(record(0, g0, g0));
+    float* dir = falloc(ctx, n3);
+    float* rhs = falloc(ctx, n3);
+    float* trial_v = falloc(ctx, n3);
+    if (g0 == 0.0) {
+        rep.stop = VR_STOP_ZERO_GRADIENT;
+        rep.success = 1;
+    } else {
+        double gk = g0;
+        int k = 0;
+        for (;;) {
+            const bool rel_ok = params.squared_norm_stop ? (gk * gk <= params.eps_opt * g0 * g0)
+                                                         : (gk <= params.eps_opt * g0);
+            if (rel_ok) {
+                rep.stop = VR_STOP_CONVERGED_REL;
+                rep.success = 1;
+                break;
+            }
+            if (gk <= params.abs_grad_tol) {
+                rep.stop = VR_STOP_CONVERGED_ABS;
+                rep.success = 1;
+                break;
+            }
+            if (k >= params.max_newton) {
+                rep.stop = VR_STOP_MAX_ITERATIONS;
+                break;
+            }
+            const double eps_H = std::min(0.5, std::sqrt(gk / g0));  // compute_forcing
+            lincomb(ctx, rhs, -1.0, state->grad, 0.0, nullptr, n3);   // scale(rhs, -1)
+            const vr_pcg_stats pcg = pcg_f32(obj.get(), state.get(), rhs, eps_H, params.max_krylov,
+                                             precond, dir);
+            const double slope = dot_f(ctx, state->grad, dir, ctx->g.N, 3) * hc;  // inner_product
+            if (slope >= 0.0) {
+                rep.stop = VR_STOP_LINE_SEARCH_FAILURE;
+                break;
+            }
+            // armijo_search (solver.cpp:104-129)
+            double alpha = 1.0;
+            std::unique_ptr<StateF32> accepted;
+            for (int t = 0; t < params.armijo_max_trials; ++t) {
+                lincomb(ctx, trial_v, 1.0, state->v, alpha, dir, n3);
+                std::unique_ptr<StateF32> trial(objf32_evaluate(obj.get(), trial_v));
+                if (trial->objective <= state->objective + params.armijo_c1 * alpha * slope) {
+                    accepted = std::move(trial);
+                    break;
+                }
+                alpha *= params.armijo_backtrack;
+            }
+            if (!accepted) {
+                rep.stop = VR_STOP_LINE_SEARCH_FAILURE;
+                break;
+            }
+            state = std::move(accepted);
+            objf32_gradient(obj.get(), state.get());
+            gk = norm_f(ctx, state->grad, n3);
+            ++k;
+            vr_iteration_record row = record(k, gk, g0);
+            row.step_length = alpha;
+            row.forcing = eps_H;
+            row.inner_iterations = pcg.iterations;
+            res.records.push_back(row);
+        }
+        rep.outer_iterations = k;
+    }
+    for (float* p : {dir, rhs, trial_v}) ffree(ctx, p);
+    rep.final_objective = state->objective;
+    rep.final_mismatch_rel = state->mismatch_rel;
+    rep.final_grad_rel = g0 > 0 ? norm_f(ctx, state->grad, n3) / g0 : 0.0;
+    rep.fine = obj->counters;
+    rep.n_records = static_cast<int>(res.records.size());
+    VR_CUDA(cudaMemcpyAsync(v_out, state->v, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    rep.wall_time_s = elapsed();
+    state.reset();  // before the objective it points to
+    return res;
+}
+
 void objf32_destroy(ObjF32* o) { delete o; }
 void statef32_destroy(StateF32* s) { delete s; }
 void statef32_scalars(const StateF32* s, double* J, double* mis, double* rel) {

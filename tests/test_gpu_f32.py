@@ -116,3 +116,26 @@ def test_objective_f32(vr, ref, ctx, n, kind):
     s32 = o.evaluate(0.5 * vs)
     o.compute_gradient(s32)
     assert rel_l2(o.hessian_matvec(s32, vt), o64.hessian_matvec(s64, vt)) <= 1e-4
+
+
+@pytest.mark.parametrize("n", [16, 32])
+def test_gn_solve_f32(vr, ref, ctx, n):
+    # gauss_newton_solve<float>: Newton iterations +-1, final mismatch and |g| within 1 %
+    dims = (n, n, n)
+    c = ctx(dims)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model(), vr.make_params(eps_opt=1e-2)
+    v0 = np.zeros((3,) + dims)
+    res = vr.gauss_newton_solve_f32(c, mR, mT, v0, model, params)
+    v_ref, rep, _ = ref.gauss_newton_solve_f32(mR, mT, v0, model, params)
+    g = res.report
+    assert res.v.dtype == np.float32 and g["success"]
+    assert g["stop"] == rep["stop"]
+    assert abs(g["outer_iterations"] - rep["outer_iterations"]) <= 1
+    assert abs(g["final_mismatch_rel"] - rep["final_mismatch_rel"]) <= 1e-2 * rep["final_mismatch_rel"]
+    assert abs(g["final_grad_rel"] - rep["final_grad_rel"]) <= 1e-2 * rep["final_grad_rel"]
+    if g["outer_iterations"] == rep["outer_iterations"]:
+        assert rel_l2(res.v, v_ref) <= 1e-4
+    # the fp64 lane reaches the same iterate (the paper: fp32 converges identically)
+    r64 = vr.gauss_newton_solve(c, mR, mT, v0, model, params)
+    assert abs(r64.report["outer_iterations"] - g["outer_iterations"]) <= 1
