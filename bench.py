@@ -213,6 +213,31 @@ def fp32_block(ctx, V, d_v, d_mT, nt, dev, torch):
         e1.record(st)
         e1.synchronize()
         res[name + "_us"] = e0.elapsed_time(e1) / 20 * 1e3
+    # the fp32 objective's GN Hessian matvec at the same state (composed, not yet fused)
+    try:
+        of = V.ObjectiveF32(ctx, d_mT.numpy(), d_mT.numpy(), V.make_model("h2", beta_v=1e-2, nt=nt))
+        sf = of.evaluate(d_v.numpy())
+        of.compute_gradient(sf)
+        vt = V.DeviceBufferF32.from_host(ctx, d_v.numpy())
+        out = V.DeviceBufferF32(ctx, 3 * N)
+        mv = lambda: L.call("vr_hessian_matvec_f32", of._h, sf._h, vt.ptr, out.ptr)  # noqa: E731
+        for _ in range(2):
+            mv()
+        ctx.synchronize()
+        e0.record(st)
+        for _ in range(10):
+            mv()
+        e1.record(st)
+        e1.synchronize()
+        res["matvec_f32_ms"] = e0.elapsed_time(e1) / 10
+        res["matvec_f32_note"] = ("Objective<float> GN Hessian matvec at the generating velocity: fused fp32 sweep "
+                                  "steps, beta_v A vt through fp64 scratch views")
+        vt.free()
+        out.free()
+        sf.close()
+        of.close()
+    except Exception as exc:  # report, do not lose the line
+        res["matvec_f32_ms"] = f"unavailable: {exc}"
     res["speedup_state_step"] = res["state_step_f64_us"] / res["state_step_f32_us"]
     res["speedup_3_fields"] = res["velocity_3_fields_f64_us"] / res["velocity_3_fields_f32_us"]
     res["note"] = "fp32 fields and departure points, fp64 weights and sums (the reference's float lane)"

@@ -8,9 +8,9 @@
 // each stored result is rounded once, as in the reference: the fp32 semi-Lagrangian
 // kernels (sl.cu), the fp64 spectral operators behind a convert-at-the-boundary (the
 // reference's fft.hpp:12-17 contract) and fp64 reductions of the fp32 values. The
-// steps are composed from those operators and small pointwise kernels (no fusion yet):
-// this lane is about the reference's float semantics and the halved bytes, not about
-// squeezing the fp64 lane's fused sweeps.
+// steps are composed from those operators and small pointwise kernels;
+// the sweep steps are fused like the fp64 lane's (sl.cu *_f32 kernels), the spectral
+// terms go through fp64 scratch views.
 #include <chrono>
 #include <cmath>
 #include <memory>
@@ -37,11 +37,6 @@ __global__ void k_axpy_f(float* y, double a, const float* x, long long n) {
     const long long i = blockIdx.x * (long long)kT + threadIdx.x;
     if (i < n) y[i] = static_cast<float>(static_cast<double>(y[i]) + a * static_cast<double>(x[i]));
 }
-// out = float(x * f)  (continuity_step, transport.cpp:62-68)
-__global__ void k_mul_f(float* out, const float* x, const float* f, long long n) {
-    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
-    if (i < n) out[i] = static_cast<float>(x[i] * f[i]);
-}
 // continuity_factor (transport.cpp:44-55)
 __global__ void k_factor_f(float* factor, const float* div, const float* at_dep, double half_dt,
                            long long n) {
@@ -50,26 +45,6 @@ __global__ void k_factor_f(float* factor, const float* div, const float* at_dep,
         factor[i] = static_cast<float>(
             exp(half_dt * (static_cast<double>(div[i]) + static_cast<double>(at_dep[i]))));
 }
-// b_a = float(b_a + w lam d_a f)  (accumulate_weighted_grad, objective.cpp:9-32)
-__global__ void k_accum_f(float* b, double w, const float* lam, const float* gm, long long n) {
-    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
-    if (i >= n) return;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-        b[a * n + i] = static_cast<float>(static_cast<double>(b[a * n + i]) +
-                                          w * static_cast<double>(lam[i]) * static_cast<double>(gm[a * n + i]));
-}
-// gradient_dot (transport.cpp:126-148): out = float(out + d_a f * w_a), a = 0, 1, 2
-__global__ void k_graddot_f(float* out, const float* gm, const float* w, long long n) {
-    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
-    if (i >= n) return;
-    float o = 0.0f;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-        o = static_cast<float>(static_cast<double>(o) + static_cast<double>(gm[a * n + i]) * static_cast<double>(w[a * n + i]));
-    out[i] = o;
-}
-
 float* falloc(vr_ctx* ctx, long long n) { return reinterpret_cast<float*>(dev_alloc(ctx, (n + 1) / 2)); }
 void ffree(vr_ctx* ctx, float* p) { dev_free(ctx, reinterpret_cast<double*>(p)); }
 
@@ -219,21 +194,14 @@ void objf32_gradient(ObjF32* o, StateF32* s) {
                        [&](const double* i, double* out) { op_gradient(ctx, i, out); });
     }
     if (!s->grad) s->grad = falloc(ctx, 3 * N);
-    float* lam[2] = {falloc(ctx, N), falloc(ctx, N)};
+    // adjoint sweep keeping every lambda_j, then the observer accumulation in one pass
+    float* lamh = falloc(ctx, (nt + 1) * N);
     float* b = s->grad;
-    VR_CUDA(cudaMemsetAsync(b, 0, sizeof(float) * 3 * N, ctx->stream));
-    lincomb(ctx, lam[0], 1.0, o->mR, -1.0, s->mhist + nt * N, N);  // terminal (objective.cpp:91-92)
-    VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, 0.5 * dt, lam[0], s->gradm + 3LL * nt * N, N));
-    int cur = 0;
-    for (int j = nt - 1; j >= 0; --j) {  // sweep_continuity (transport.cpp:88-113)
-        sl_tricubic_f32(ctx, lam[cur], 1, s->xf, lam[cur ^ 1]);
-        VR_LAUNCH(ctx, "f32_pointwise", k_mul_f<<<blocks(N), kT, 0, ctx->stream>>>(lam[cur ^ 1], lam[cur ^ 1], s->factor, N));
-        cur ^= 1;
-        const double w = (j == 0) ? 0.5 * dt : dt;
-        VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, w, lam[cur], s->gradm + 3LL * j * N, N));
-    }
-    ffree(ctx, lam[0]);
-    ffree(ctx, lam[1]);
+    lincomb(ctx, lamh + nt * N, 1.0, o->mR, -1.0, s->mhist + nt * N, N);  // terminal (objective.cpp:91-92)
+    for (int j = nt - 1; j >= 0; --j)  // sweep_continuity (transport.cpp:88-113)
+        sl_continuity_f32(ctx, lamh + (j + 1) * N, s->xf, s->factor, lamh + j * N);
+    sl_accumulate_f32(ctx, lamh, s->gradm, nt, dt, b);
+    ffree(ctx, lamh);
     o->counters.pde_solves += 1;
     if (o->model.projection != VR_PROJ_IDENTITY)
         spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
@@ -260,38 +228,25 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
                     "(compute the gradient first)");
     const int nt = s->nt;
     const double dt = 1.0 / nt, hdt = 0.5 / nt;
-    float* q[2] = {falloc(ctx, N), falloc(ctx, N)};
-    float* mt[2] = {falloc(ctx, N), falloc(ctx, N)};
-    float* tmp = falloc(ctx, N);
-    auto qdot = [&](int j, float* out) {
-        VR_LAUNCH(ctx, "f32_pointwise", k_graddot_f<<<blocks(N), kT, 0, ctx->stream>>>(out, s->gradm + 3LL * j * N, vt3, N));
-    };
-    VR_CUDA(cudaMemsetAsync(mt[0], 0, sizeof(float) * N, ctx->stream));
-    qdot(0, q[0]);
+    // incremental state (transport.cpp:150-173) fused per step; the last step writes the
+    // inc-adjoint terminal -mt_nt into the history, whose sweep then keeps every lambda~_j
+    float* lamh = falloc(ctx, (nt + 1) * N);
+    float* tmp[2] = {falloc(ctx, N), falloc(ctx, N)};
+    sl_incstate_first_f32(ctx, s->gradm, vt3, hdt, tmp[0]);
     int c = 0;
     for (int j = 0; j < nt; ++j) {
-        qdot(j + 1, q[c ^ 1]);
-        lincomb(ctx, tmp, 1.0, mt[c], -hdt, q[c], N);
-        sl_tricubic_f32(ctx, tmp, 1, s->xb, mt[c ^ 1]);
-        axpy(ctx, mt[c ^ 1], -hdt, q[c ^ 1], N);
+        const bool last = j == nt - 1;
+        sl_incstate_step_f32(ctx, tmp[c], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
+                             last ? lamh + nt * N : tmp[c ^ 1], last);
         c ^= 1;
     }
     o->counters.pde_solves += 1;
-    float* lam[2] = {q[0], q[1]};  // reuse
-    lincomb(ctx, lam[0], -1.0, mt[c], 0.0, nullptr, N);  // terminal = -mt_nt
+    for (int j = nt - 1; j >= 0; --j)
+        sl_continuity_f32(ctx, lamh + (j + 1) * N, s->xf, s->factor, lamh + j * N);
     float* b = out3;
-    VR_CUDA(cudaMemsetAsync(b, 0, sizeof(float) * 3 * N, ctx->stream));
-    VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, 0.5 * dt, lam[0], s->gradm + 3LL * nt * N, N));
-    int cur = 0;
-    for (int j = nt - 1; j >= 0; --j) {
-        sl_tricubic_f32(ctx, lam[cur], 1, s->xf, lam[cur ^ 1]);
-        VR_LAUNCH(ctx, "f32_pointwise", k_mul_f<<<blocks(N), kT, 0, ctx->stream>>>(lam[cur ^ 1], lam[cur ^ 1], s->factor, N));
-        cur ^= 1;
-        const double w = (j == 0) ? 0.5 * dt : dt;
-        VR_LAUNCH(ctx, "f32_pointwise", k_accum_f<<<blocks(N), kT, 0, ctx->stream>>>(b, w, lam[cur], s->gradm + 3LL * j * N, N));
-    }
+    sl_accumulate_f32(ctx, lamh, s->gradm, nt, dt, b);
     o->counters.pde_solves += 1;
-    for (float* p : {q[0], q[1], mt[0], mt[1], tmp}) ffree(ctx, p);
+    for (float* p : {lamh, tmp[0], tmp[1]}) ffree(ctx, p);
     if (o->model.projection != VR_PROJ_IDENTITY)
         spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
             op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);

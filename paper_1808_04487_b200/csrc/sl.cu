@@ -414,6 +414,80 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB_F32 * 2 / 3)
         dep[c * g.N + i] = static_cast<float>(wrap_coord(x[c] + sign * dt * gather(v + c * g.N, g, st)));
 }
 
+// fp32-lane sweep steps, fused like the fp64 ones but with the reference's float
+// rounding points (transport.cpp:126-180, objective.cpp:9-32 with T = float)
+__device__ __forceinline__ float graddot_f32(const float* __restrict__ gm, const float* __restrict__ vt,
+                                             long long i, long long N) {
+    float o = 0.0f;  // gradient_dot<float>: out = float(out + d_a m * w_a), a = 0, 1, 2
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        o = static_cast<float>(static_cast<double>(o) +
+                               static_cast<double>(gm[a * N + i]) * static_cast<double>(vt[a * N + i]));
+    return o;
+}
+// tmp_0 = float(1.0 * 0 + (-hdt) q_0)
+__global__ void __launch_bounds__(kThreads)
+    k_incstate_first_f32(const float* __restrict__ gm0, const float* __restrict__ vt,
+                         float* __restrict__ tmp, long long N, double hdt) {
+    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+    if (i >= N) return;
+    const float q = graddot_f32(gm0, vt, i, N);
+    tmp[i] = static_cast<float>(1.0 * 0.0 + (-hdt) * static_cast<double>(q));
+}
+// mt_{j+1} = float(float(I[tmp_j](X)) + (-hdt) q_{j+1}); LAST: dst = float(-mt_nt) (terminal),
+// else dst = tmp_{j+1} = float(1.0 mt_{j+1} + (-hdt) q_{j+1})
+template <bool LAST, bool BIG>
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB_F32)
+    k_incstate_step_f32(const float* __restrict__ src, const float* __restrict__ dep,
+                        const float* __restrict__ gm, const float* __restrict__ vt,
+                        float* __restrict__ dst, GridDims g, Tile t, double hdt) {
+    int i1, i2, i3;
+    long long i;
+    if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
+    double x1, x2, x3;
+    load_point(dep, i, g.N, x1, x2, x3);
+    const float q = graddot_f32(gm, vt, i, g.N);
+    Stencil st;
+    make_stencil(g, x1, x2, x3, i1, st);
+    const float gv = static_cast<float>(gather(src, g, st));
+    const float m = static_cast<float>(static_cast<double>(gv) + (-hdt) * static_cast<double>(q));
+    dst[i] = LAST ? static_cast<float>(-m)
+                  : static_cast<float>(1.0 * static_cast<double>(m) + (-hdt) * static_cast<double>(q));
+}
+// continuity_step<float>: dst = float(I[src](X)) * factor (a float product)
+template <bool BIG>
+__global__ void __launch_bounds__(kTileThreads, VR_SL_MINB_F32)
+    k_continuity_f32(const float* __restrict__ src, const float* __restrict__ dep,
+                     const float* __restrict__ factor, float* __restrict__ dst, GridDims g, Tile t) {
+    int i1, i2, i3;
+    long long i;
+    if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
+    double x1, x2, x3;
+    load_point(dep, i, g.N, x1, x2, x3);
+    const float fac = factor[i];
+    Stencil st;
+    make_stencil(g, x1, x2, x3, i1, st);
+    dst[i] = static_cast<float>(gather(src, g, st)) * fac;
+}
+// b_a = sum over j = nt..0 of float(b_a + w_j lam_j d_a m_j), the observer order
+__global__ void __launch_bounds__(kThreads)
+    k_accumulate_f32(const float* __restrict__ lam, const float* __restrict__ gm, int nt, double dt,
+                     float* __restrict__ b, long long N) {
+    const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+    if (i >= N) return;
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+    for (int j = nt; j >= 0; --j) {
+        const double w = (j == 0 || j == nt) ? 0.5 * dt : dt;
+        const double wl = w * static_cast<double>(lam[j * N + i]);
+        const float* gj = gm + 3LL * j * N;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            acc[a] = static_cast<float>(static_cast<double>(acc[a]) + wl * static_cast<double>(gj[a * N + i]));
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) b[a * N + i] = acc[a];
+}
+
 // lv_c = lam * vt_c (transport.cpp:203-207)
 __global__ void __launch_bounds__(kThreads)
     k_scale_vec(const double* __restrict__ lam, const double* __restrict__ vt, double* __restrict__ lv,
@@ -545,6 +619,9 @@ unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.
 #define K_TRICUBIC2F(B) k_tricubic_f32<2, B>
 #define K_TRICUBIC3F(B) k_tricubic_f32<3, B>
 #define K_TRACEF(B) k_trace_f32<B>
+#define K_INCSTATEF0(B) k_incstate_step_f32<false, B>
+#define K_INCSTATEF1(B) k_incstate_step_f32<true, B>
+#define K_CONTINUITYF(B) k_continuity_f32<B>
 
 }  // namespace
 
@@ -685,6 +762,29 @@ bool all_finite_f32(vr_ctx* ctx, const float* a, long long n) {
     VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
     return ctx->flag_host[0] == 0;
+}
+void sl_incstate_first_f32(vr_ctx* ctx, const float* gm0, const float* vt3, double hdt, float* tmp0) {
+    const GridDims& g = ctx->g;
+    VR_LAUNCH(ctx, "sl_pointwise", k_incstate_first_f32<<<pgrid(g), kThreads, 0, ctx->stream>>>(gm0, vt3, tmp0, g.N, hdt));
+}
+void sl_incstate_step_f32(vr_ctx* ctx, const float* src, const float* dep3, const float* gm,
+                          const float* vt3, double hdt, float* dst, bool last) {
+    const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
+    if (last)
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step_f32", K_INCSTATEF1, src, dep3, gm, vt3, dst, g, t, hdt);
+    else
+        VR_TILE_LAUNCH(ctx, "sl_incstate_step_f32", K_INCSTATEF0, src, dep3, gm, vt3, dst, g, t, hdt);
+}
+void sl_continuity_f32(vr_ctx* ctx, const float* src, const float* dep3, const float* factor, float* dst) {
+    const GridDims& g = ctx->g;
+    const Tile t = tile_of(g);
+    VR_TILE_LAUNCH(ctx, "sl_adjoint_step_f32", K_CONTINUITYF, src, dep3, factor, dst, g, t);
+}
+void sl_accumulate_f32(vr_ctx* ctx, const float* lam_hist, const float* gm_hist, int nt, double dt,
+                       float* b3) {
+    const GridDims& g = ctx->g;
+    VR_LAUNCH(ctx, "sl_accumulate_f32", k_accumulate_f32<<<pgrid(g), kThreads, 0, ctx->stream>>>(lam_hist, gm_hist, nt, dt, b3, g.N));
 }
 void sl_trace_f32(vr_ctx* ctx, const float* v3, int nt, int direction, float* dep3) {
     if (nt < 1) throw_argument("trace_characteristics: n_t must be >= 1");

@@ -350,6 +350,12 @@ void sl_defmap_step(vr_ctx* ctx, const double* u3, const double* dep3, const dou
 void sl_tricubic_f32(vr_ctx* ctx, const float* f, int nfields, const float* pts3, float* out);
 void sl_trace_f32(vr_ctx* ctx, const float* v3, int nt, int direction, float* dep3);
 bool all_finite_f32(vr_ctx* ctx, const float* a, long long n);
+void sl_incstate_first_f32(vr_ctx* ctx, const float* gm0, const float* vt3, double hdt, float* tmp0);
+void sl_incstate_step_f32(vr_ctx* ctx, const float* src, const float* dep3, const float* gm,
+                          const float* vt3, double hdt, float* dst, bool last);
+void sl_continuity_f32(vr_ctx* ctx, const float* src, const float* dep3, const float* factor, float* dst);
+void sl_accumulate_f32(vr_ctx* ctx, const float* lam_hist, const float* gm_hist, int nt, double dt,
+                       float* b3);
 void convert_f2d(vr_ctx* ctx, const float* a, double* b, long long n);
 void convert_d2f(vr_ctx* ctx, const double* a, float* b, long long n);
 // out_c = lam * vt_c
