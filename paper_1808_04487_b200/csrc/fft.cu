@@ -20,6 +20,7 @@
 // literal twiddles; inter-stage twiddles come from per-axis long-double
 // tables (exactly rounded), so the transform error is O(eps log n).
 #include <cmath>
+#include <type_traits>
 
 #include "vr_common.cuh"
 
@@ -468,12 +469,14 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
 // out = add + scale * x. Z[k] = E + i O, E = X[k] + conj X[M-k],
 // O = (X[k] - conj X[M-k]) exp(+2 pi i k / N); z = IFFT_M(Z); x[2m] = Re, x[2m+1] = Im.
 // Imaginary parts of the self-conjugate bins X[0], X[M] are ignored (c2r semantics).
-template <int M>
+// TO = output / add element type (float for the fp32 lane: out = float(add + scale x))
+template <int M, class TO>
 __global__ void __launch_bounds__(RowCfg<M>::THREADS)
-    k_c2r_rows(const double2* __restrict__ in, double* __restrict__ out, long long nrows,
+    k_c2r_rows(const double2* __restrict__ in, TO* __restrict__ out, long long nrows,
                const double2* __restrict__ twM_g, const double2* __restrict__ twN_g, double scale,
-               const double* __restrict__ add) {
+               const TO* __restrict__ add) {
     using C = RowCfg<M>;
+    using TO2 = typename std::conditional<std::is_same<TO, float>::value, float2, double2>::type;
     constexpr int PER = C::RB * M / C::THREADS;  // output double2 per thread per tile
     extern __shared__ double2 smem[];
     double2 *twM, *twN;
@@ -487,15 +490,20 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
         if (next < ntiles) load_rows_async<M, M + 1>(smem + (b ^ 1) * C::STAGE, in, next, nrows);
         cp_async_commit();
         const long long avail_out = (nrows - tile * C::RB) * M;
-        double2* dstp = reinterpret_cast<double2*>(out) + tile * C::RB * M;
+        TO2* dstp = reinterpret_cast<TO2*>(out) + tile * C::RB * M;
         // the add field's loads are issued now and land while the rows transform
         double2 addv[PER];
         if (add) {
-            const double2* addp = reinterpret_cast<const double2*>(add) + tile * C::RB * M;
+            const TO2* addp = reinterpret_cast<const TO2*>(add) + tile * C::RB * M;
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
                 const int e = threadIdx.x + j * C::THREADS;
-                addv[j] = e < avail_out ? __ldcs(addp + e) : make_double2(0.0, 0.0);
+                if (e < avail_out) {
+                    const TO2 a = __ldcs(addp + e);
+                    addv[j] = make_double2(static_cast<double>(a.x), static_cast<double>(a.y));
+                } else {
+                    addv[j] = make_double2(0.0, 0.0);
+                }
             }
         }
         cp_async_wait<1>();
@@ -544,7 +552,10 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
                 o = make_double2(addv[j].x + scale * z.x, addv[j].y + scale * z.y);
             else
                 o = make_double2(z.x * scale, z.y * scale);
-            dstp[e] = o;
+            TO2 ot;
+            ot.x = static_cast<TO>(o.x);
+            ot.y = static_cast<TO>(o.y);
+            dstp[e] = ot;
         }
         __syncthreads();  // this stage is refilled by the next iteration's prefetch
     }
@@ -703,6 +714,17 @@ void launch_axis(vr_ctx* ctx, int n, const double2* src, double2* dst, long long
 }
 
 template <int M>
+void launch_rows_f32out(vr_ctx* ctx, const void* in, float* out, double scale, const float* add) {
+    using C = RowCfg<M>;
+    const long long nrows = static_cast<long long>(ctx->g.L) * ctx->g.n2;
+    const long long ntiles = (nrows + C::RB - 1) / C::RB;
+    static int occ[64] = {0};
+    const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, float>, C::THREADS, C::SMEM, ntiles, occ);
+    VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, float><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+        static_cast<const double2*>(in), out, nrows, ctx->fft->tw3h, ctx->fft->tw3, scale, add));
+}
+
+template <int M>
 void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double scale,
                    const double* add) {
     using C = RowCfg<M>;
@@ -716,8 +738,8 @@ void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double 
             ctx->fft->tw3));
     } else {
         static int occ[64] = {0};
-        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M>, C::THREADS, C::SMEM, ntiles, occ);
-        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, double>, C::THREADS, C::SMEM, ntiles, occ);
+        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, double><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double2*>(in), static_cast<double*>(out), nrows, ctx->fft->tw3h,
             ctx->fft->tw3, scale, add));
     }
@@ -786,6 +808,24 @@ void pass_rows_forward(vr_ctx* ctx, const double* in, double* spec) {
 void pass_rows_inverse(vr_ctx* ctx, const double* spec, double* out, double scale,
                        const double* add) {
     launch_rows(ctx, false, spec, out, scale, add);
+}
+void pass_rows_inverse_f32(vr_ctx* ctx, const double* spec, float* out, double scale,
+                           const float* add) {
+    switch (ctx->g.n3 / 2) {
+#define VR_CASE(MM) \
+    case MM: launch_rows_f32out<MM>(ctx, spec, out, scale, add); break;
+        VR_CASE(2)
+        VR_CASE(4)
+        VR_CASE(8)
+        VR_CASE(16)
+        VR_CASE(32)
+        VR_CASE(64)
+        VR_CASE(128)
+        VR_CASE(256)
+        VR_CASE(512)
+#undef VR_CASE
+        default: throw_dimension("fft: unsupported n3 " + std::to_string(ctx->g.n3));
+    }
 }
 void pass_x2(vr_ctx* ctx, double* spec, int dir) {
     const GridDims& g = ctx->g;

@@ -207,12 +207,11 @@ void objf32_gradient(ObjF32* o, StateF32* s) {
         spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
             op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
         });
-    float* reg = falloc(ctx, 3 * N);
-    spectral_f(ctx, s->v, 3, reg, 3, [&](const double* i, double* out) {
-        op_reg(ctx, i, out, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
-    });
-    axpy(ctx, b, 1.0, reg, 3 * N);  // add_scaled(gradient, 1.0, reg)
-    ffree(ctx, reg);
+    {  // g = float(b + beta_v A v): the add rides the c2r epilogue (add_scaled(gradient, 1.0, reg))
+        F64 dv(ctx, s->v, 3 * N);
+        op_reg_begin(ctx, dv.p, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+        op_reg_finish_f32(ctx, b, b);
+    }
     s->has_gradient = true;
     o->counters.gradient_evals += 1;
 }
@@ -252,12 +251,11 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
             op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
         });
     o->counters.hessian_matvecs += 1;
-    float* reg = falloc(ctx, 3 * N);
-    spectral_f(ctx, vt3, 3, reg, 3, [&](const double* i, double* out) {
-        op_reg(ctx, i, out, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
-    });
-    axpy(ctx, out3, 1.0, reg, 3 * N);
-    ffree(ctx, reg);
+    {  // out = float(b + beta_v A vt), the add fused into the c2r epilogue
+        F64 dvt(ctx, vt3, 3 * N);
+        op_reg_begin(ctx, dvt.p, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+        op_reg_finish_f32(ctx, out3, out3);
+    }
 }
 
 // ---- solver.cpp:51-269 on fp32 vectors (fp64 scalars) -------------------------------

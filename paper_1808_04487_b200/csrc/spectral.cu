@@ -210,6 +210,13 @@ void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mo
         scalar_multiplier(ctx, in3 + c * ctx->g.N, sbuf(ctx, 4 + c), nullptr, mp, nullptr);
 }
 
+void op_reg_finish_f32(vr_ctx* ctx, float* out3, const float* add3) {
+    const GridDims& g = ctx->g;
+    for (int c = 0; c < 3; ++c)
+        pass_rows_inverse_f32(ctx, sbuf(ctx, 4 + c), out3 + c * g.N, inv_n(g),
+                              add3 ? add3 + c * g.N : nullptr);
+}
+
 void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3) {
     const GridDims& g = ctx->g;
     for (int c = 0; c < 3; ++c)
