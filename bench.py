@@ -238,6 +238,33 @@ def fp32_block(ctx, V, d_v, d_mT, nt, dev, torch):
         of.close()
     except Exception as exc:  # report, do not lose the line
         res["matvec_f32_ms"] = f"unavailable: {exc}"
+    # the config-3 beta continuation in fp32 (device-resident fp32 images and initial guess)
+    try:
+        mR32 = V.DeviceBufferF32.from_host(ctx, V.solve_state(ctx, d_mT, d_v, nt).numpy()[nt])
+        mT32 = V.DeviceBufferF32.from_host(ctx, d_mT.numpy())
+        z32 = V.DeviceBufferF32.from_host(ctx, np.zeros((3,) + ctx.local_dims))
+        runs, reps = [], None
+        for _ in range(3):
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            vsol, reps, _ = V.parameter_continuation_f32(ctx, mR32, mT32, z32, V.make_model("h2", beta_v=1e-2, nt=nt),
+                                                         V.make_params(eps_opt=1e-2))
+            ctx.synchronize()
+            runs.append(time.perf_counter() - t0)
+            vsol.free()
+        res["config3_solve_f32"] = {"seconds": float(np.median(runs[1:])), "seconds_runs": runs,
+                                    "newton_iterations": [r["outer_iterations"] for r in reps],
+                                    "hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps),
+                                    "final_mismatch_rel": reps[-1]["final_mismatch_rel"],
+                                    "final_grad_rel": reps[-1]["final_grad_rel"],
+                                    "stop": reps[-1]["stop_name"],
+                                    "note": "the reference's float semantics at 256^3: fp32 round-off of v, amplified "
+                                            "by the H2 symbol |k|^4 (up to 2.4e9), floors the gradient near the "
+                                            "tolerance, so the beta = 1 level may stall (DESIGN.md section 9)"}
+        for b in (mR32, mT32, z32):
+            b.free()
+    except Exception as exc:
+        res["config3_solve_f32"] = f"unavailable: {exc}"
     res["speedup_state_step"] = res["state_step_f64_us"] / res["state_step_f32_us"]
     res["speedup_3_fields"] = res["velocity_3_fields_f64_us"] / res["velocity_3_fields_f32_us"]
     res["note"] = "fp32 fields and departure points, fp64 weights and sums (the reference's float lane)"

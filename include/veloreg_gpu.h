@@ -306,6 +306,12 @@ int vr_gauss_newton_solve_f32(vr_ctx* ctx, const float* m_R, const float* m_T, c
                               const vr_model* model, const vr_solver_params* params, int precond,
                               float* v_out, vr_solve_report* report, vr_iteration_record* records,
                               int max_records);
+/* parameter continuation over vr_gauss_newton_solve_f32 */
+int vr_parameter_continuation_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
+                                  const vr_model* model, const vr_solver_params* params,
+                                  int precond, float* v_out, vr_solve_report* reports,
+                                  int max_levels, int* n_levels, vr_iteration_record* records,
+                                  int max_records);
 
 /* ---- Objective (objective.hpp:56-102) -------------------------------------- */
 typedef struct vr_objective vr_objective;

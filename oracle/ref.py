@@ -92,6 +92,9 @@ _SIG = {
     "vref_objective_f32_counters": (I, [P, C.POINTER(Counters)]),
     "vref_gauss_newton_solve_f32": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I, P,
                                         C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
+    "vref_parameter_continuation_f32": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I,
+                                            P, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
+                                            C.POINTER(IterationRecord), I]),
     "vref_fft_r2c_f32": (I, [DIMS, P, P]),
     "vref_fft_c2r_f32": (I, [DIMS, P, P]),
     "vref_gradient_f32": (I, [DIMS, P, P]),
@@ -676,6 +679,19 @@ def gauss_newton_solve_f32(m_R, m_T, v0, model, params, precond=1, max_records=5
           C.byref(model), C.byref(params), precond, vout.ctypes.data, C.byref(rep), recs, max_records)
     n = min(rep.n_records, max_records)
     return vout, _report(rep), [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
+
+
+def parameter_continuation_f32(m_R, m_T, v0, model, params, precond=1, max_levels=16, max_records=1024):
+    r, t, v0 = _f(m_R), _f(m_T), _f(v0)
+    vout = np.empty_like(v0)
+    reps = (SolveReport * max_levels)()
+    recs = (IterationRecord * max_records)()
+    nl = C.c_int()
+    _call("vref_parameter_continuation_f32", _dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data,
+          C.byref(model), C.byref(params), precond, vout.ctypes.data, reps, max_levels, C.byref(nl),
+          recs, max_records)
+    reports = [_report(reps[i]) for i in range(min(nl.value, max_levels))]
+    return vout, reports
 
 
 def solve_state_f32(m_T, v, nt):

@@ -634,6 +634,43 @@ int vref_gauss_newton_solve_f32(const int* d, const float* mR, const float* mT, 
     });
 }
 
+int vref_parameter_continuation_f32(const int* d, const float* mR, const float* mT, const float* v0,
+                                    const vr_model* m, const vr_solver_params* p, int precond,
+                                    float* v_out, vr_solve_report* reps, int max_levels,
+                                    int* n_levels, vr_iteration_record* recs, int max_recs) {
+    return guard([&] {
+        if (!(m->beta_v <= 1.0)) throw ArgumentError("parameter continuation: target beta_v > 1");
+        std::vector<double> levels;
+        for (int i = 0;; ++i) {
+            double b = std::pow(10.0, -i);
+            if (b <= m->beta_v * (1.0 + 1e-9)) break;
+            levels.push_back(b);
+        }
+        levels.push_back(m->beta_v);
+        Grid3 g = grid_of(d);
+        auto R = load_scalar_f(g, mR), T = load_scalar_f(g, mT);
+        auto v = load_vector_f(g, v0);
+        SpectralPreconditioner<float> spec;
+        IdentityPreconditionerT<float> ident;
+        KrylovPreconditioner<float>& pc =
+            precond == VR_PRECOND_SPECTRAL ? static_cast<KrylovPreconditioner<float>&>(spec)
+                                           : static_cast<KrylovPreconditioner<float>&>(ident);
+        int off = 0;
+        *n_levels = 0;
+        for (std::size_t l = 0; l < levels.size(); ++l) {
+            RegModel model = to_model(*m);
+            model.beta_v = levels[l];
+            auto res = gauss_newton_solve(R, T, v, model, to_params(*p), pc);
+            if (static_cast<int>(l) < max_levels) fill_report(res.report, &reps[l], recs, max_recs, off);
+            off += static_cast<int>(res.report.iterations.size());
+            *n_levels = static_cast<int>(l) + 1;
+            v = std::move(res.v);
+            if (res.report.stop == StopReason::line_search_failure) break;
+        }
+        store_f(v, v_out);
+    });
+}
+
 int vref_gauss_newton_solve(const int* d, const double* mR, const double* mT, const double* v0,
                             const vr_model* m, const vr_solver_params* p, int precond,
                             double* v_out, vr_solve_report* rep, vr_iteration_record* recs,

@@ -1160,6 +1160,24 @@ int vr_gauss_newton_solve_f32(vr_ctx* ctx, const float* m_R, const float* m_T, c
     });
 }
 
+int vr_parameter_continuation_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
+                                  const vr_model* model, const vr_solver_params* params,
+                                  int precond, float* v_out, vr_solve_report* reports,
+                                  int max_levels, int* n_levels, vr_iteration_record* records,
+                                  int max_records) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_parameter_continuation_f32");
+        need(m_R && m_T && v0 && model && params && v_out && n_levels, "vr_parameter_continuation_f32");
+        auto rs = vr::parameter_continuation_f32(ctx, m_R, m_T, v0, *model, *params, precond, v_out);
+        int off = 0;
+        for (size_t l = 0; l < rs.size(); ++l) {
+            if (reports && static_cast<int>(l) < max_levels) reports[l] = rs[l].report;
+            copy_records(rs[l], records, max_records, off);
+            off += static_cast<int>(rs[l].records.size());
+        }
+        *n_levels = static_cast<int>(rs.size());
+    });
+}
 int vr_parameter_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, const double* v0,
                               const vr_model* model, const vr_solver_params* params, int precond,
                               double* v_out, vr_solve_report* reports, int max_levels,

@@ -124,6 +124,10 @@ void objf32_copy_gradient(ObjF32* o, const StateF32* s, float* g3);  // synchron
 GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, const float* v0,
                                 const vr_model& model, const vr_solver_params& params, int precond,
                                 float* v_out);
+std::vector<GnResult> parameter_continuation_f32(vr_ctx* ctx, const float* mR, const float* mT,
+                                                 const float* v0, const vr_model& model,
+                                                 const vr_solver_params& params, int precond,
+                                                 float* v_out);
 
 // ---- postprocess / continuation (postprocess.cu) ----
 void det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det);

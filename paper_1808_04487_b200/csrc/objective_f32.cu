@@ -429,6 +429,40 @@ GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, c
     return res;
 }
 
+// parameter continuation on the fp32 solve: beta_v 1, 1e-1, ... target
+std::vector<GnResult> parameter_continuation_f32(vr_ctx* ctx, const float* mR, const float* mT,
+                                                 const float* v0, const vr_model& model,
+                                                 const vr_solver_params& params, int precond,
+                                                 float* v_out) {
+    if (!(model.beta_v <= 1.0)) throw_argument("parameter continuation: target beta_v > 1");
+    std::vector<double> levels;
+    for (int i = 0;; ++i) {
+        const double b = std::pow(10.0, -i);
+        if (b <= model.beta_v * (1.0 + 1e-9)) break;
+        levels.push_back(b);
+    }
+    levels.push_back(model.beta_v);
+    const long long n3 = 3 * ctx->g.N;
+    float* v = falloc(ctx, n3);
+    VR_CUDA(cudaMemcpyAsync(v, v0, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+    std::vector<GnResult> out;
+    try {
+        for (double b : levels) {
+            vr_model m = model;
+            m.beta_v = b;
+            out.push_back(gauss_newton_solve_f32(ctx, mR, mT, v, m, params, precond, v));
+            if (out.back().report.stop == VR_STOP_LINE_SEARCH_FAILURE) break;
+        }
+        VR_CUDA(cudaMemcpyAsync(v_out, v, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        ffree(ctx, v);
+        throw;
+    }
+    ffree(ctx, v);
+    return out;
+}
+
 void objf32_destroy(ObjF32* o) { delete o; }
 void statef32_destroy(StateF32* s) { delete s; }
 void statef32_scalars(const StateF32* s, double* J, double* mis, double* rel) {

@@ -939,6 +939,28 @@ def gauss_newton_solve_f32(ctx, m_R, m_T, v0, model=None, params=None, precond="
     return SolveResult(vout.numpy(v0.shape), _report_dict(rep), _records(recs, min(rep.n_records, max_records)))
 
 
+def parameter_continuation_f32(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral",
+                               max_levels=16, max_records=1024):
+    """beta_v continuation over the fp32 solve on host float32 arrays, or on
+    DeviceBufferF32 inputs (then the result stays on the device)."""
+    model = model if model is not None else make_model()
+    params = params if params is not None else make_params()
+    bufs = [a if isinstance(a, DeviceBufferF32) else DeviceBufferF32.from_host(ctx, a) for a in (m_R, m_T, v0)]
+    host = not isinstance(v0, DeviceBufferF32)
+    n3 = bufs[2].count
+    vout = DeviceBufferF32(ctx, n3)
+    reps = (_lib.SolveReport * max_levels)()
+    recs = (_lib.IterationRecord * max_records)()
+    nl = C.c_int()
+    _lib.call("vr_parameter_continuation_f32", ctx.handle, bufs[0].ptr, bufs[1].ptr, bufs[2].ptr,
+              C.byref(model), C.byref(params), _enum(_PRECOND, precond), vout.ptr, reps, max_levels,
+              C.byref(nl), recs, max_records)
+    reports = [_report_dict(reps[i]) for i in range(min(nl.value, max_levels))]
+    nrec = sum(r["n_records"] for r in reports)
+    v = vout.numpy(np.shape(v0)) if host else vout
+    return v, reports, _records(recs, min(nrec, max_records))
+
+
 def _f32_op(ctx, fn, a, nout, *extra):
     a = np.ascontiguousarray(a, dtype=np.float32)
     din = DeviceBufferF32.from_host(ctx, a)

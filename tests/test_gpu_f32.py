@@ -139,3 +139,19 @@ def test_gn_solve_f32(vr, ref, ctx, n):
     # the fp64 lane reaches the same iterate (the paper: fp32 converges identically)
     r64 = vr.gauss_newton_solve(c, mR, mT, v0, model, params)
     assert abs(r64.report["outer_iterations"] - g["outer_iterations"]) <= 1
+
+
+def test_parameter_continuation_f32(vr, ref, ctx):
+    # beta continuation over the fp32 solve vs the restatement over gauss_newton_solve<float>
+    dims = (32, 32, 32)
+    c = ctx(dims)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model(), vr.make_params(eps_opt=1e-2)
+    v0 = np.zeros((3,) + dims)
+    vg, rg, _ = vr.parameter_continuation_f32(c, mR, mT, v0, model, params)
+    vref, rr = ref.parameter_continuation_f32(mR, mT, v0, model, params)
+    assert len(rg) == len(rr) == 3
+    for a, b in zip(rg, rr):
+        assert abs(a["outer_iterations"] - b["outer_iterations"]) <= 1
+        assert abs(a["final_mismatch_rel"] - b["final_mismatch_rel"]) <= 1e-2 * b["final_mismatch_rel"]
+    assert vg.dtype == np.float32 and rel_l2(vg, vref) <= 1e-3
