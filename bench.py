@@ -554,6 +554,14 @@ def main():
                 "limiter": "L1/LSU wavefronts of the 64-node fp64 gathers (ncu: L1/TEX 85 %, DRAM 29 %)"
                            if dom.startswith("sl_") and "step" in dom else None,
                 "bytes_per_launch": per_launch[dom], "avg_launch_ms": t / c}
+    # x1 slabs: NCCL exchange time per matvec (all-to-all transposes + halos run on the
+    # compute stream, so this is also the exposed communication time)
+    comm = None
+    if scaling == "strong":
+        cats = {k: v for k, v in prof.items() if k.startswith("comm_")}
+        comm = {"exposed_ms_per_matvec": sum(t for c, t in cats.values()) / k_prof,
+                "by_kind_ms_per_matvec": {k: t / k_prof for k, (c, t) in cats.items()},
+                "note": "exchanges on the compute stream (not overlapped): exposed = total"}
     matvec_roof = {"bytes_per_matvec": per_matvec_bytes,
                    "achieved_GBps": per_matvec_bytes / (ms_per_step / 1e3) / 1e9,
                    "frac_of_peak": per_matvec_bytes / (ms_per_step / 1e3) / 1e9 / peak}
@@ -732,7 +740,7 @@ def main():
                 "kernels": kernels, "kernel_profile": {"steps": k_prof, "ms_per_step": ms_prof / k_prof,
                                                         "note": "separate serialised pass, events per kernel"},
                 "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve,
-                "config4_single_gpu": cfg4, "config2": cfg2, "fp32_lane": f32}
+                "config4_single_gpu": cfg4, "config2": cfg2, "fp32_lane": f32, "comm": comm}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

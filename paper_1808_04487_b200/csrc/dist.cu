@@ -88,25 +88,38 @@ struct NcclTransport final : Transport {
         if (buf) cudaFree(buf);
         if (comm) nccl().commDestroy(comm);
     }
+    // exchange time as a profile category (library kernels: not counted as our launches);
+    // the exchanges run on the context stream, so their time is also the exposed time
+    static void comm_end(vr_ctx* ctx, const char* cat, cudaEvent_t start) {
+        if (!start) return;
+        vr_ctx* p = prof_owner(ctx);
+        cudaEvent_t e = prof_event(p);
+        VR_CUDA(cudaEventRecord(e, ctx->stream));
+        p->prof.push_back({cat, start, e, false});
+    }
     void alltoall(vr_ctx* ctx, const double* send, double* recv, size_t count) override {
         auto& api = nccl();
+        cudaEvent_t ev = prof_begin(ctx);
         nccl_check(api.groupStart(), "groupStart");
         for (int q = 0; q < size; ++q) {
             nccl_check(api.send(send + q * count, count, ncclDouble, q, comm, ctx->stream), "send");
             nccl_check(api.recv(recv + q * count, count, ncclDouble, q, comm, ctx->stream), "recv");
         }
         nccl_check(api.groupEnd(), "groupEnd");
+        comm_end(ctx, "comm_alltoall", ev);
     }
     void halo(vr_ctx* ctx, double* interior, size_t plane, int L, int H) override {
         auto& api = nccl();
         const int prev = (rank + size - 1) % size, next = (rank + 1) % size;
         const size_t n = static_cast<size_t>(H) * plane;
+        cudaEvent_t ev = prof_begin(ctx);
         nccl_check(api.groupStart(), "groupStart");
         nccl_check(api.send(interior, n, ncclDouble, prev, comm, ctx->stream), "send");
         nccl_check(api.recv(interior + L * plane, n, ncclDouble, next, comm, ctx->stream), "recv");
         nccl_check(api.send(interior + (L - H) * plane, n, ncclDouble, next, comm, ctx->stream), "send");
         nccl_check(api.recv(interior - n, n, ncclDouble, prev, comm, ctx->stream), "recv");
         nccl_check(api.groupEnd(), "groupEnd");
+        comm_end(ctx, "comm_halo", ev);
     }
     void allreduce(vr_ctx* ctx, double* vals, int k, bool max) override {
         VR_CUDA(cudaMemcpyAsync(buf, vals, sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
