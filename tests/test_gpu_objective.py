@@ -19,7 +19,17 @@ MODELS = {
     "h1_leray": dict(kind="h1", beta_v=1e-2, nt=4, projection="incompressible"),
     "helmholtz": dict(kind="helmholtz", gamma=0.5, beta_v=5e-2, nt=2),
     "h3_nt8": dict(kind="h3", beta_v=1e-3, nt=8),
+    "h2_nt1": dict(kind="h2", beta_v=1e-2, nt=1),
 }
+
+
+def reg_tol(kw, dims, max_mode=2):
+    """Bar for terms containing beta_v A: the symbol |k|^p amplifies the O(1e-16) round-off
+    two correct fp64 FFTs leave in the empty high modes of band-limited fields by up to
+    (k_max^2)^(p/2) against (3 max_mode^2)^(p/2) in the band (see test_gpu_fullsize.py)."""
+    p = {"h1": 1, "h2": 2, "h3": 3, "helmholtz": 2}[kw.get("kind", "h2")]
+    kmax2 = sum((n // 2) ** 2 for n in dims)
+    return max(TOL, 1e-15 * (kmax2 / (3.0 * max_mode ** 2)) ** p)
 
 
 def image_pair(ref, dims, max_mode, seed):
@@ -30,7 +40,7 @@ def image_pair(ref, dims, max_mode, seed):
 
 
 @pytest.mark.parametrize("name", list(MODELS))
-@pytest.mark.parametrize("dims", [(16, 16, 16), (32, 16, 32)])
+@pytest.mark.parametrize("dims", [(16, 16, 16), (32, 16, 32), (8, 32, 64), (64, 8, 16)])
 def test_objective_parity(vr, ref, ctx, name, dims):
     c = ctx(dims)
     kw = MODELS[name]
@@ -56,13 +66,14 @@ def test_objective_parity(vr, ref, ctx, name, dims):
     g_ref = ro.compute_gradient(rs)
     go.compute_gradient(gs)
     assert gs.has_gradient and gs.has_adjoint_ctx
-    assert rel_l2(gs.gradient, g_ref) < TOL
+    rt = reg_tol(kw, dims)
+    assert rel_l2(gs.gradient, g_ref) < rt
     assert rel_l2(gs.get(3), rs.get(3)) < TOL  # continuity factor
 
-    assert rel_l2(go.hessian_matvec(gs, vt), ro.hessian_matvec(rs, vt)) < TOL
+    assert rel_l2(go.hessian_matvec(gs, vt), ro.hessian_matvec(rs, vt)) < rt
     assert rel_l2(go.hessian_data_matvec(gs, vt), ro.hessian_data_matvec(rs, vt)) < TOL
     for mode in (0, 1, 2):
-        assert rel_l2(go.apply_reg(vt, mode), ro.apply_reg(vt, mode)) < TOL
+        assert rel_l2(go.apply_reg(vt, mode), ro.apply_reg(vt, mode)) < (rt if mode == 0 else TOL)
     assert rel_l2(go.apply_K(vt), ro.apply_K(vt)) < TOL
     assert go.counters() == ro.counters()
 
