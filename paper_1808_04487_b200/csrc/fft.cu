@@ -408,25 +408,48 @@ __device__ __forceinline__ void load_rows_async(double2* stage, const double2* s
     }
 }
 
+// r2c input rows into a stage: fp64 rows stream in with cp.async; fp32 rows (the fp32
+// lane) are loaded and widened to fp64 pairs in the same padded layout (synchronously)
+template <int M, class TI>
+__device__ __forceinline__ void load_rows_in(double2* stage, const TI* in, long long tile,
+                                             long long nrows) {
+    if constexpr (std::is_same<TI, double>::value) {
+        load_rows_async<M, M>(stage, reinterpret_cast<const double2*>(in), tile, nrows);
+    } else {
+        using C = RowCfg<M>;
+        const float2* src = reinterpret_cast<const float2*>(in);
+        const long long base = tile * C::RB * M;
+        const long long avail = (nrows - tile * C::RB) * M;
+        for (int e = threadIdx.x; e < C::RB * M; e += C::THREADS) {
+            const int r = e / M, i = e % M;
+            double2 v = make_double2(0.0, 0.0);
+            if (e < avail) {
+                const float2 f = __ldg(src + base + e);
+                v = make_double2(static_cast<double>(f.x), static_cast<double>(f.y));
+            }
+            stage[r * C::LD + padi(i)] = v;
+        }
+    }
+}
+
 // r2c along x3: in nrows x 2M reals -> out nrows x (M+1) complex.
 // z[m] = x[2m] + i x[2m+1]; Z = FFT_M(z); X[k] = A[k] + W_N^k B[k] with
 // A = (Z[k] + conj Z[M-k]) / 2, B = (Z[k] - conj Z[M-k]) / 2i.
-template <int M>
+template <int M, class TI>
 __global__ void __launch_bounds__(RowCfg<M>::THREADS)
-    k_r2c_rows(const double* __restrict__ in, double2* __restrict__ out, long long nrows,
+    k_r2c_rows(const TI* __restrict__ in, double2* __restrict__ out, long long nrows,
                const double2* __restrict__ twM_g, const double2* __restrict__ twN_g) {
     using C = RowCfg<M>;
     extern __shared__ double2 smem[];
     double2 *twM, *twN;
     stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
-    const double2* src = reinterpret_cast<const double2*>(in);
     const long long ntiles = (nrows + C::RB - 1) / C::RB;
     long long tile = blockIdx.x;
-    if (tile < ntiles) load_rows_async<M, M>(smem, src, tile, nrows);
+    if (tile < ntiles) load_rows_in<M, TI>(smem, in, tile, nrows);
     cp_async_commit();
     for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
         const long long next = tile + gridDim.x;
-        if (next < ntiles) load_rows_async<M, M>(smem + (b ^ 1) * C::STAGE, src, next, nrows);
+        if (next < ntiles) load_rows_in<M, TI>(smem + (b ^ 1) * C::STAGE, in, next, nrows);
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
@@ -714,6 +737,17 @@ void launch_axis(vr_ctx* ctx, int n, const double2* src, double2* dst, long long
 }
 
 template <int M>
+void launch_rows_f32in(vr_ctx* ctx, const float* in, double* spec) {
+    using C = RowCfg<M>;
+    const long long nrows = static_cast<long long>(ctx->g.L) * ctx->g.n2;
+    const long long ntiles = (nrows + C::RB - 1) / C::RB;
+    static int occ[64] = {0};
+    const unsigned grid = persistent_grid(ctx, k_r2c_rows<M, float>, C::THREADS, C::SMEM, ntiles, occ);
+    VR_LAUNCH(ctx, "fft_x3_r2c", k_r2c_rows<M, float><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+        in, reinterpret_cast<double2*>(spec), nrows, ctx->fft->tw3h, ctx->fft->tw3));
+}
+
+template <int M>
 void launch_rows_f32out(vr_ctx* ctx, const void* in, float* out, double scale, const float* add) {
     using C = RowCfg<M>;
     const long long nrows = static_cast<long long>(ctx->g.L) * ctx->g.n2;
@@ -732,8 +766,8 @@ void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double 
     const long long ntiles = (nrows + C::RB - 1) / C::RB;
     if (forward) {
         static int occ[64] = {0};
-        const unsigned grid = persistent_grid(ctx, k_r2c_rows<M>, C::THREADS, C::SMEM, ntiles, occ);
-        VR_LAUNCH(ctx, "fft_x3_r2c", k_r2c_rows<M><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+        const unsigned grid = persistent_grid(ctx, k_r2c_rows<M, double>, C::THREADS, C::SMEM, ntiles, occ);
+        VR_LAUNCH(ctx, "fft_x3_r2c", k_r2c_rows<M, double><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double*>(in), static_cast<double2*>(out), nrows, ctx->fft->tw3h,
             ctx->fft->tw3));
     } else {
@@ -808,6 +842,23 @@ void pass_rows_forward(vr_ctx* ctx, const double* in, double* spec) {
 void pass_rows_inverse(vr_ctx* ctx, const double* spec, double* out, double scale,
                        const double* add) {
     launch_rows(ctx, false, spec, out, scale, add);
+}
+void pass_rows_forward_f32(vr_ctx* ctx, const float* in, double* spec) {
+    switch (ctx->g.n3 / 2) {
+#define VR_CASE(MM) \
+    case MM: launch_rows_f32in<MM>(ctx, in, spec); break;
+        VR_CASE(2)
+        VR_CASE(4)
+        VR_CASE(8)
+        VR_CASE(16)
+        VR_CASE(32)
+        VR_CASE(64)
+        VR_CASE(128)
+        VR_CASE(256)
+        VR_CASE(512)
+#undef VR_CASE
+        default: throw_dimension("fft: unsupported n3 " + std::to_string(ctx->g.n3));
+    }
 }
 void pass_rows_inverse_f32(vr_ctx* ctx, const double* spec, float* out, double scale,
                            const float* add) {

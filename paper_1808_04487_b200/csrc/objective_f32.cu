@@ -207,11 +207,9 @@ void objf32_gradient(ObjF32* o, StateF32* s) {
         spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
             op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
         });
-    {  // g = float(b + beta_v A v): the add rides the c2r epilogue (add_scaled(gradient, 1.0, reg))
-        F64 dv(ctx, s->v, 3 * N);
-        op_reg_begin(ctx, dv.p, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
-        op_reg_finish_f32(ctx, b, b);
-    }
+    // g = float(b + beta_v A v): fp32 rows in, the add in the c2r epilogue (add_scaled(gradient, 1.0, reg))
+    op_reg_begin_f32(ctx, s->v, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+    op_reg_finish_f32(ctx, b, b);
     s->has_gradient = true;
     o->counters.gradient_evals += 1;
 }
@@ -251,11 +249,9 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
             op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
         });
     o->counters.hessian_matvecs += 1;
-    {  // out = float(b + beta_v A vt), the add fused into the c2r epilogue
-        F64 dvt(ctx, vt3, 3 * N);
-        op_reg_begin(ctx, dvt.p, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
-        op_reg_finish_f32(ctx, out3, out3);
-    }
+    // out = float(b + beta_v A vt): fp32 rows in, the add fused into the c2r epilogue
+    op_reg_begin_f32(ctx, vt3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+    op_reg_finish_f32(ctx, out3, out3);
 }
 
 // ---- solver.cpp:51-269 on fp32 vectors (fp64 scalars) -------------------------------
@@ -276,10 +272,10 @@ vr_pcg_stats pcg_f32(ObjF32* o, const StateF32* s, const float* rhs, double rel_
     const double target = rel_tol * r0;
     float *r = falloc(ctx, n3), *z = falloc(ctx, n3), *sd = falloc(ctx, n3), *Hs = falloc(ctx, n3);
     auto pc = [&](const float* in, float* out) {  // SpectralPreconditioner: (beta_v A)^-1
-        if (precond == VR_PRECOND_SPECTRAL)
-            spectral_f(ctx, in, 3, out, 3, [&](const double* i, double* oo) {
-                op_reg(ctx, i, oo, o->model.norm, VR_REGOP_INVERSE, o->model.beta_v);
-            });
+        if (precond == VR_PRECOND_SPECTRAL) {
+            op_reg_begin_f32(ctx, in, o->model.norm, VR_REGOP_INVERSE, o->model.beta_v);
+            op_reg_finish_f32(ctx, out, nullptr);
+        }
         else
             VR_CUDA(cudaMemcpyAsync(out, in, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
     };

@@ -210,6 +210,19 @@ void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mo
         scalar_multiplier(ctx, in3 + c * ctx->g.N, sbuf(ctx, 4 + c), nullptr, mp, nullptr);
 }
 
+// fp32 lane, one GPU: the forward half of op_reg on fp32 fields (rows widened in the
+// r2c pass), leaving the spectra in sbuf(4..6) for op_reg_finish_f32
+void op_reg_begin_f32(vr_ctx* ctx, const float* in3, const vr_regnorm& norm, int mode, double beta) {
+    const MultParams mp = reg_mult(norm, mode, beta);
+    for (int c = 0; c < 3; ++c) {
+        double* s = sbuf(ctx, 4 + c);
+        pass_rows_forward_f32(ctx, in3 + c * ctx->g.N, s);
+        pass_x2(ctx, s, -1);
+        pass_x1(ctx, s, s, 0, &mp);
+        pass_x2(ctx, s, +1);
+    }
+}
+
 void op_reg_finish_f32(vr_ctx* ctx, float* out3, const float* add3) {
     const GridDims& g = ctx->g;
     for (int c = 0; c < 3; ++c)

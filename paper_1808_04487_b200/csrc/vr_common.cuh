@@ -258,7 +258,8 @@ void pass_rows_forward(vr_ctx* ctx, const double* in, double* spec);
 void pass_rows_inverse(vr_ctx* ctx, const double* spec, double* out, double scale,
                        const double* add);
 void pass_x2(vr_ctx* ctx, double* spec, int dir);
-// fp32 lane: c2r rows writing out = float(add + scale x) (add: fp32 or null)
+// fp32 lane: r2c rows reading fp32; c2r rows writing out = float(add + scale x) (add: fp32 or null)
+void pass_rows_forward_f32(vr_ctx* ctx, const float* in, double* spec);
 void pass_rows_inverse_f32(vr_ctx* ctx, const double* spec, float* out, double scale,
                            const float* add);
 void pass_x1(vr_ctx* ctx, const double* src, double* dst, int dir, const MultParams* mult);
@@ -286,6 +287,7 @@ void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm
 void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mode, double beta);
 void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3);
 void op_reg_finish_f32(vr_ctx* ctx, float* out3, const float* add3);  // out = float(add + x/N)
+void op_reg_begin_f32(vr_ctx* ctx, const float* in3, const vr_regnorm& norm, int mode, double beta);
 // run `fn` (which launches on ctx->stream) on the side stream, forked from the
 // current point of ctx->stream; join_side() makes ctx->stream wait for it
 // (on x1 slabs the work stays on the main stream: its collectives must keep one
