@@ -13,11 +13,13 @@ Arms:
   --impl reference  the reference C++ code (oracle/_ref, compiled unmodified
                     from /root/reference/proj/src) on the host cores, rank 0 only
 
-Multi-GPU (torchrun, N > 1): the same 256^3 problem is split into x1 slabs,
-one per rank (NCCL all-to-all FFT transposes, P2P halo exchange for the
-semi-Lagrangian gathers); "scaling": "strong", value = global matvecs /
-max-over-ranks time. If the slab path cannot start (e.g. no NCCL), every rank
-runs an independent replica instead ("parallelism": "replicas").
+Multi-GPU (torchrun, N > 1): BASELINE config 4 (512^3, |k| <= 10) at N = 2..7
+and config 5 (1024^3, |k| <= 16, max displacement 0.05*2pi) at N = 8, split
+into x1 slabs, one per rank (NCCL all-to-all FFT transposes, P2P halo exchange
+for the semi-Lagrangian gathers, halo sized from the actual velocity); every
+rank generates only its own slab of the inputs. "scaling": "strong", value =
+global matvecs / max-over-ranks time. There is no fallback: if the slab path
+cannot start, the rank raises and torchrun tears the job down.
 """
 from __future__ import annotations
 
@@ -65,16 +67,38 @@ def dist_env():
     return rank, world, local
 
 
-def workload(n, nt):
+def config_for(world, n_arg):
+    """BASELINE config id and grid: config 3 (256^3) on one GPU, config 4 (512^3) on 2-7
+    GPUs, config 5 (1024^3) on 8; --n overrides the grid."""
+    cid = 3 if world == 1 else (5 if world >= 8 else 4)
+    from paper_1808_04487_b200 import phantom  # numpy only; does not load the product library
+    return cid, (n_arg or phantom.CONFIGS[cid]["n"])
+
+
+def workload_desc(cid, n, nt):
     from paper_1808_04487_b200 import phantom
-    cfg = phantom.CONFIGS[3]
+    c = phantom.CONFIGS[cid]
+    return (f"config{cid}: {n}^3 ellipsoid phantom (40, seed 1808, sigma 2 vox), band-limited v "
+            f"(|k|<={c['kmax']}, max disp {c['disp'] / (2 * np.pi):.2f}*2pi, seed 4487), GN Hessian matvec at v, "
+            f"H2 beta_v=1e-2, n_t={nt}, K=identity, spectral-precond solve setting")
+
+
+def workload(cid, n, nt):
+    """Global host arrays (one process: the single-GPU arm and the reference arm)."""
+    from paper_1808_04487_b200 import phantom
+    c = phantom.CONFIGS[cid]
     m_T = phantom.ellipsoid_phantom(n)
-    v = phantom.bandlimited_velocity(n, cfg["kmax"], cfg["disp"])
+    v = phantom.bandlimited_velocity(n, c["kmax"], c["disp"])
     vt = phantom.bandlimited_direction(n)
-    desc = (f"config3: {n}^3 ellipsoid phantom (40, seed 1808, sigma 2 vox), band-limited v "
-            f"(|k|<=6, max disp 0.08*2pi, seed 4487), GN Hessian matvec at v, H2 beta_v=1e-2, "
-            f"n_t={nt}, K=identity, spectral-precond solve setting")
-    return m_T, v, vt, desc
+    return m_T, v, vt, workload_desc(cid, n, nt)
+
+
+def bench_config(cid, n, nt, world):
+    """The `config` dict of the JSON line -- identical in both arms."""
+    return {"workload": workload_desc(cid, n, nt), "grid": n, "nt": nt,
+            "l2": f"inputs larger than L2 (each fp64 field {8 * n ** 3 / 2 ** 20:.0f} MiB of the global grid; "
+                  f"~{int(bytes_model(n, nt)[0] / 8 / n ** 3)} fields touched per step)",
+            "parallelism": "single" if world == 1 else f"x1-slabs-{world}"}
 
 
 def bytes_model(n, nt):
@@ -156,11 +180,10 @@ def measured_peak():
 # ---------------------------------------------------------------------------
 def run_reference_matvecs(m_R, m_T, v, vt, nt, steps, warmup, budget_s):
     """Reference CPU arm: the compiled reference (oracle/_ref) on the host cores."""
-    from oracle import ref
-    import paper_1808_04487_b200.veloreg as V
+    from oracle import ref  # the reference only: never maps libveloreg_gpu.so
     cores = os.cpu_count() or 1
     ref.set_workers(cores)
-    model = V.make_model("h2", beta_v=1e-2, nt=nt)
+    model = ref.make_model("h2", beta_v=1e-2, nt=nt)
     t0 = time.perf_counter()
     obj = ref.Objective(m_R, m_T, model)
     s = obj.evaluate(v)
@@ -363,16 +386,33 @@ def config2_block(vr, V, dev, nt, model, torch, with_cpu=True):
             "operators": res, "solve": solve}
 
 
+def ref_memory_ok(n):
+    """The reference keeps ~70 fp64 fields of the global grid (SURVEY 8(d) CPU baseline)."""
+    need = 70 * 8 * n ** 3
+    try:
+        import psutil
+        have = psutil.virtual_memory().available
+    except Exception:
+        have = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES")
+    return have >= need, need, have
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
-    n, nt = args.n, args.nt
+    nt = args.nt
+    cid, n = config_for(world, args.n)
 
     if args.impl == "reference":
         if rank != 0:
             return 0
-        m_T, v, vt, desc = workload(n, nt)
-        from oracle import ref
+        ok, need, have = ref_memory_ok(n)
+        if not ok:
+            print(json.dumps({"impl": "reference", "unavailable": f"the reference needs ~{need / 2 ** 30:.0f} GiB of "
+                              f"host RAM at {n}^3 (70 fp64 fields), {have / 2 ** 30:.0f} GiB available"}), flush=True)
+            return 0
+        m_T, v, vt, desc = workload(cid, n, nt)
+        from oracle import ref  # the reference only: never maps libveloreg_gpu.so
         ref.set_workers(os.cpu_count() or 1)
         m_R = ref.solve_state(m_T, v, nt)[-1]
         r = run_reference_matvecs(m_R, m_T, v, vt, nt, args.steps, min(args.warmup, 1), args.ref_budget_s)
@@ -380,9 +420,9 @@ def main():
                   f"untimed evaluate+gradient ({r['setup_s']:.1f}s); capped at {args.ref_budget_s:.0f}s")
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": r["steps"],
                 "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * r["seconds"] / r["steps"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "impl": "reference",
-                "config": {"workload": desc, "grid": n, "nt": nt},
+                "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": bench_config(cid, n, nt, world),
                 "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
                                  "sample": sample},
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -397,34 +437,45 @@ def main():
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = local
 
-    m_T, v, vt, desc = workload(n, nt)
     model = V.make_model("h2", beta_v=1e-2, nt=nt)
-    parallelism, scaling, slab_note = "single", "weak", None
-    ctx = None
+    desc = workload_desc(cid, n, nt)
+    scaling, comm_info = "weak", None
     if world > 1:
-        # x1 slabs over the ranks (NCCL all-to-all FFT transposes, P2P halos):
-        # the same 256^3 problem split across GPUs, i.e. strong scaling
-        try:
-            uid = [V.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            ctx = V.DistContext(n, rank, world, uid[0], device=dev, halo=12)
-            d_mT, d_v, d_vt = (ctx.to_device(ctx.slab(a)) for a in (m_T, v, vt))
-            # m_R = m_T transported by v: the state history of an objective at v
-            tmp = V.Objective(ctx, d_mT, d_mT, model)
-            s0 = tmp.evaluate(d_v)
-            d_mR = ctx.to_device(s0.m_history[nt])
-            s0.close()
-            tmp.close()
-            parallelism, scaling = f"x1-slabs-{world}", "strong"
-        except Exception as exc:  # report and run per-GPU replicas instead
-            slab_note = f"slab path failed ({type(exc).__name__}: {exc}); ran replicas"
-            print(slab_note, file=sys.stderr, flush=True)
-            ctx = None
-    if ctx is None:
+        # x1 slabs over the ranks (NCCL all-to-all FFT transposes, P2P halos): one global
+        # problem split across the GPUs, i.e. strong scaling. No fallback: any failure
+        # raises on this rank and torchrun tears the job down.
+        from paper_1808_04487_b200 import phantom
+
+        def _red(x, op):
+            t = torch.tensor([float(x)], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=op)
+            return float(t.item())
+        planes = n // world
+        first = rank * planes
+        m_T, v, vt, vmax1 = phantom.make_config_inputs_slab(
+            cid, first, planes, n=n, allreduce_max=lambda x: _red(x, dist.ReduceOp.MAX),
+            allreduce_min=lambda x: _red(x, dist.ReduceOp.MIN))
+        halo = V.slab_halo_required(vmax1, nt, n)
+        uid = [V.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = V.DistContext(n, rank, world, uid[0], device=dev, halo=halo)
+        assert (ctx.first_plane, ctx.planes) == (first, planes), "slab geometry mismatch"
+        d_mT, d_v, d_vt = (ctx.to_device(a) for a in (m_T, v, vt))
+        del m_T, v
+        # m_R = m_T transported by v: the state history of an objective at v
+        tmp = V.Objective(ctx, d_mT, d_mT, model)
+        s0 = tmp.evaluate(d_v)
+        d_mR = ctx.to_device(s0.m_history[nt])
+        s0.close()
+        tmp.close()
+        scaling = "strong"
+        comm_info = {"halo_planes": halo, "vmax_x1": vmax1, "planes_per_rank": planes}
+    else:
+        m_T, v, vt, desc = workload(cid, n, nt)
         ctx = vr.Context(n, device=dev)
         d_mT = ctx.to_device(m_T)
         d_v = ctx.to_device(v)
@@ -432,8 +483,6 @@ def main():
         hist = V.solve_state(ctx, d_mT, d_v, nt)                   # m_R = m_T transported by v
         d_mR = ctx.empty(1)
         _ = V._lib.call("vr_memcpy_d2d", ctx.handle, d_mR.ptr, hist.field(nt), 8 * ctx.N)
-        if world > 1:
-            parallelism = "replicas"
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev))
     obj = V.Objective(ctx, d_mR, d_mT, model)
     st = obj.evaluate(d_v)
@@ -479,7 +528,7 @@ def main():
     ctx.set_profiling(False)
     ms_prof = p0.elapsed_time(p1)
     ms_per_step = ms / args.steps
-    per_step_units = 1 if scaling == "strong" else world  # one global matvec vs one per replica
+    per_step_units = 1  # one global matvec per step (slabs split it; one GPU does all of it)
     value = per_step_units * args.steps / (ms / 1e3)
 
     # ---- end to end through the public C ABI with host buffers -------------
@@ -491,7 +540,7 @@ def main():
         V._lib.call("vr_host_alloc_pinned", nbytes, V.C.byref(hp_out))
         h_in = np.ctypeslib.as_array((V.C.c_double * (3 * ctx.N)).from_address(hp_in.value))
         h_out = np.ctypeslib.as_array((V.C.c_double * (3 * ctx.N)).from_address(hp_out.value))
-        h_in[:] = (ctx.slab(vt) if scaling == "strong" else vt).ravel()
+        h_in[:] = vt.ravel()  # this rank's slab (or the whole grid on one GPU)
         obj.hessian_matvec_host(st, h_in, h_out)
         if dist is not None:
             dist.barrier()
@@ -561,10 +610,19 @@ def main():
         cats = {k: v for k, v in prof.items() if k.startswith("comm_")}
         comm = {"exposed_ms_per_matvec": sum(t for c, t in cats.values()) / k_prof,
                 "by_kind_ms_per_matvec": {k: t / k_prof for k, (c, t) in cats.items()},
-                "note": "exchanges on the compute stream (not overlapped): exposed = total"}
+                "note": "serialised profile pass (rank 0): NCCL exchange time per matvec", **(comm_info or {})}
+    # per-matvec HBM bytes over the aggregate HBM bandwidth, plus (slabs) the
+    # all-to-all and halo bytes over NVLink (900 GB/s per direction per GPU)
+    nvl_bytes = 0.0
+    if world > 1:
+        Fc = 16.0 * n * n * (n // 2 + 1)
+        nvl_bytes = 6 * Fc * (world - 1) / world ** 2 + 2 * nt * 2 * comm_info["halo_planes"] * n * n * 8
+    t_roof = per_matvec_bytes / world / (peak * 1e9) + nvl_bytes / 900e9
     matvec_roof = {"bytes_per_matvec": per_matvec_bytes,
                    "achieved_GBps": per_matvec_bytes / (ms_per_step / 1e3) / 1e9,
-                   "frac_of_peak": per_matvec_bytes / (ms_per_step / 1e3) / 1e9 / peak}
+                   "frac_of_peak": per_matvec_bytes / (ms_per_step / 1e3) / 1e9 / (peak * world),
+                   "nvlink_bytes_per_gpu": nvl_bytes, "roofline_ms": t_roof * 1e3,
+                   "frac_of_roofline": t_roof * 1e3 / ms_per_step}
 
     # ---- GN solve time (the metric's second half) ----------------------------
     solve = None
@@ -582,7 +640,7 @@ def main():
             ctx.synchronize()
             t_runs.append(time.perf_counter() - t0)
         t_solve = float(np.median(t_runs[1:]))  # median of the 5 steady runs (host jitter)
-        solve["config3"] = {
+        solve[f"config{cid}"] = {
             "grid": n, "seconds": t_solve, "seconds_runs": t_runs, "levels": len(reps),
             "newton_iterations": [r["outer_iterations"] for r in reps],
             "hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps),
@@ -607,6 +665,7 @@ def main():
                 "final_mismatch_rel": reps2[-1]["final_mismatch_rel"],
                 "final_grad_rel": reps2[-1]["final_grad_rel"], "stop": reps2[-1]["stop_name"],
                 "precond": "two-level, PCG(0.1) inner on the 128^3 coarse grid"}
+    if not args.no_solve and world == 1:
         # config 1: 64^3 analytic problem, GPU vs the reference on the host cores
         ctx1 = vr.Context(64, device=dev)
         mR1, mT1, _ = V.generate_synthetic(ctx1, nt)
@@ -733,9 +792,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": desc, "grid": n, "nt": nt, "l2": "inputs larger than L2 (each fp64 field "
-                           f"{8 * n ** 3 / 2 ** 20:.0f} MiB; ~{int(per_matvec_bytes / 8 / n ** 3)} fields touched per step)",
-                           "parallelism": parallelism, **({"note": slab_note} if slab_note else {})},
+                "config": bench_config(cid, n, nt, world),
                 "e2e": e2e, "gpu_launches": launches, "roofline": roof, "matvec_roofline": matvec_roof,
                 "kernels": kernels, "kernel_profile": {"steps": k_prof, "ms_per_step": ms_prof / k_prof,
                                                         "note": "separate serialised pass, events per kernel"},

@@ -18,7 +18,12 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_ref", "libveloreg_ref.so")
 sys.path.insert(0, os.path.dirname(_HERE))
-from paper_1808_04487_b200 import _lib as _gpu_lib_types  # noqa: E402  (POD layouts only)
+# POD layouts only: _abi_types is pure ctypes declarations and the package __init__ is lazy,
+# so this import never maps libveloreg_gpu.so into a reference-arm process
+from paper_1808_04487_b200 import _abi_types as _gpu_lib_types  # noqa: E402
+
+make_model = _gpu_lib_types.make_model
+make_norm = _gpu_lib_types.make_norm
 
 RegNorm = _gpu_lib_types.RegNorm
 Model = _gpu_lib_types.Model

@@ -27,9 +27,11 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from . import _lib
+from . import _abi_types, _lib
 from ._lib import (ArgumentError, DimensionError, LogicError, NumericError,  # noqa: F401
                    ResourceError, VelouregError)
+
+_lib.load()  # no CPU fallback: importing the mirror without the built library raises
 
 _KIND = {"h1": _lib.REG_H1, "h2": _lib.REG_H2, "h3": _lib.REG_H3, "helmholtz": _lib.REG_HELMHOLTZ}
 _PROJ = {"identity": _lib.PROJ_IDENTITY, "incompressible": _lib.PROJ_INCOMPRESSIBLE,
@@ -42,21 +44,8 @@ def _enum(table, v):
     return table[v] if isinstance(v, str) else int(v)
 
 
-def make_norm(kind="h2", gamma=1.0, helmholtz_squared=True, div_penalty=False, beta_w=1e-4):
-    """RegNorm (spectral.hpp:75-102)."""
-    return _lib.RegNorm(_enum(_KIND, kind), gamma, int(helmholtz_squared), int(div_penalty), beta_w)
-
-
-def make_model(kind="h2", beta_v=1e-2, nt=4, projection="identity", gamma=1.0,
-               helmholtz_squared=True, div_penalty=False, beta_w=1e-4, gauss_newton=True):
-    """RegModel (objective.hpp:11-23); defaults are the reference's."""
-    m = _lib.Model()
-    m.norm = make_norm(kind, gamma, helmholtz_squared, div_penalty, beta_w)
-    m.projection = _enum(_PROJ, projection)
-    m.beta_v = beta_v
-    m.nt = nt
-    m.gauss_newton = int(gauss_newton)
-    return m
+make_norm = _abi_types.make_norm
+make_model = _abi_types.make_model
 
 
 def make_params(**kw):
@@ -189,8 +178,32 @@ class DeviceArray:
             pass
 
 
-def _dev(ctx, a):
-    return a if isinstance(a, DeviceArray) else ctx.to_device(a)
+def _dev(ctx, a, nfields: Optional[int] = None):
+    """Device view of `a` (host arrays are uploaded). With `nfields`, the argument must hold
+    exactly that many real fields of this context's grid: the C ABI takes bare pointers and
+    would otherwise read or write past a short buffer (DimensionError before any call)."""
+    if isinstance(a, DeviceArray):
+        if nfields is not None and (a.nfields != nfields or a.spectrum or a.ctx.N != ctx.N):
+            raise DimensionError(f"expected a device array of {nfields} real field(s) of {ctx.local_dims}, got "
+                                 f"{a.nfields} {'spectra' if a.spectrum else 'field(s)'} of {a.ctx.local_dims}")
+        return a
+    if nfields is not None and np.size(a) != nfields * ctx.N:
+        raise DimensionError(f"expected {nfields} field(s) of {ctx.local_dims} ({nfields * ctx.N} values), "
+                             f"got an array of shape {np.shape(a)}")
+    return ctx.to_device(a)
+
+
+def _host_buf(ctx, a, nfields: int, name: str, writeable: bool = False):
+    """Host buffer for the *_host entry points: float64, C-contiguous, exactly nfields*N
+    values (the C side copies nfields*N*8 bytes from / to the raw pointer)."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise DimensionError(f"{name}: need a C-contiguous float64 numpy array")
+    if a.size != nfields * ctx.N:
+        raise DimensionError(f"{name}: need {nfields * ctx.N} values ({nfields} field(s) of {ctx.local_dims}), "
+                             f"got {a.size}")
+    if writeable and not a.flags.writeable:
+        raise DimensionError(f"{name}: output array is read-only")
+    return a.ctypes.data
 
 
 def _ret(out: DeviceArray, host: bool):
@@ -203,14 +216,16 @@ def _is_host(*arrs):
 
 # ---- BLAS-1 / quadrature (field_ops.hpp, spectral.cpp:47-62) ------------------
 def inner_product(ctx, a, b) -> float:
-    da, db = _dev(ctx, a), _dev(ctx, b)
+    da = _dev(ctx, a)
+    db = _dev(ctx, b, da.nfields)
     r = C.c_double()
     _lib.call("vr_inner_product", ctx.handle, da.ptr, db.ptr, da.nfields, C.byref(r))
     return r.value
 
 
 def dot_l2(ctx, a, b) -> float:
-    da, db = _dev(ctx, a), _dev(ctx, b)
+    da = _dev(ctx, a)
+    db = _dev(ctx, b, da.nfields)
     r = C.c_double()
     _lib.call("vr_dot_l2", ctx.handle, da.ptr, db.ptr, da.nfields, C.byref(r))
     return r.value
@@ -228,7 +243,7 @@ def max_abs(ctx, a) -> float:
 
 
 def max_magnitude(ctx, v) -> float:
-    dv = _dev(ctx, v)
+    dv = _dev(ctx, v, 3)
     r = C.c_double()
     _lib.call("vr_max_magnitude", ctx.handle, dv.ptr, C.byref(r))
     return r.value
@@ -237,7 +252,7 @@ def max_magnitude(ctx, v) -> float:
 # ---- spectral ----------------------------------------------------------------
 def fft_forward(ctx, f):
     """fft_forward_raw (fft.cpp:66-73): unnormalized half spectrum (n1, n2, n3/2+1)."""
-    df = _dev(ctx, f)
+    df = _dev(ctx, f, 1)
     out = ctx.empty(1, complex_spectrum=True)
     _lib.call("vr_fft_r2c", ctx.handle, df.ptr, out.ptr)
     return _ret(out, _is_host(f))
@@ -256,14 +271,14 @@ def fft_inverse(ctx, spec):
 
 
 def gradient(ctx, f):
-    df = _dev(ctx, f)
+    df = _dev(ctx, f, 1)
     out = ctx.empty(3)
     _lib.call("vr_gradient", ctx.handle, df.ptr, out.ptr)
     return _ret(out, _is_host(f))
 
 
 def divergence(ctx, v):
-    dv = _dev(ctx, v)
+    dv = _dev(ctx, v, 3)
     out = ctx.empty(1)
     _lib.call("vr_divergence", ctx.handle, dv.ptr, out.ptr)
     return _ret(out, _is_host(v))
@@ -277,7 +292,7 @@ def laplacian(ctx, f):
 
 
 def helmholtz1_apply(ctx, f):
-    df = _dev(ctx, f)
+    df = _dev(ctx, f, 1)
     out = ctx.empty(1)
     _lib.call("vr_helmholtz1_apply", ctx.handle, df.ptr, out.ptr)
     return _ret(out, _is_host(f))
@@ -292,7 +307,7 @@ def gaussian_smooth(ctx, f, sigma_voxels: Sequence[float]):
 
 
 def apply_reg_operator(ctx, v, norm=None, mode="apply", beta=1.0):
-    dv = _dev(ctx, v)
+    dv = _dev(ctx, v, 3)
     out = ctx.empty(3)
     norm = norm if norm is not None else make_norm()
     _lib.call("vr_apply_reg_operator", ctx.handle, dv.ptr, out.ptr, C.byref(norm),
@@ -301,14 +316,14 @@ def apply_reg_operator(ctx, v, norm=None, mode="apply", beta=1.0):
 
 
 def apply_projection(ctx, v, kind="incompressible", beta_v=0.0, beta_w=0.0):
-    dv = _dev(ctx, v)
+    dv = _dev(ctx, v, 3)
     out = ctx.empty(3)
     _lib.call("vr_apply_projection", ctx.handle, dv.ptr, out.ptr, _enum(_PROJ, kind), beta_v, beta_w)
     return _ret(out, _is_host(v))
 
 
 def rescale_intensity(ctx, f):
-    df = _dev(ctx, f)
+    df = _dev(ctx, f, 1)
     out = ctx.empty(1)
     deg = C.c_int()
     _lib.call("vr_rescale_intensity", ctx.handle, df.ptr, out.ptr, C.byref(deg))
@@ -317,14 +332,16 @@ def rescale_intensity(ctx, f):
 
 # ---- transport -------------------------------------------------------------------
 def tricubic_interpolate(ctx, f, points):
-    df, dp = _dev(ctx, f), _dev(ctx, points)
+    df, dp = _dev(ctx, f), _dev(ctx, points, 3)
+    if df.nfields not in (1, 2, 3):
+        raise DimensionError(f"tricubic_interpolate: 1, 2 or 3 fields, got {df.nfields}")
     out = ctx.empty(df.nfields)
     _lib.call("vr_tricubic_interpolate", ctx.handle, df.ptr, dp.ptr, out.ptr, df.nfields)
     return _ret(out, _is_host(f, points))
 
 
 def trace_characteristics(ctx, v, nt, direction="backward"):
-    dv = _dev(ctx, v)
+    dv = _dev(ctx, v, 3)
     out = ctx.empty(3)
     d = _lib.TRACE_BACKWARD if direction == "backward" else _lib.TRACE_FORWARD
     _lib.call("vr_trace_characteristics", ctx.handle, dv.ptr, nt, d, out.ptr)
@@ -332,21 +349,21 @@ def trace_characteristics(ctx, v, nt, direction="backward"):
 
 
 def continuity_factor(ctx, div_v, departure, dt):
-    dd, dp = _dev(ctx, div_v), _dev(ctx, departure)
+    dd, dp = _dev(ctx, div_v, 1), _dev(ctx, departure, 3)
     out = ctx.empty(1)
     _lib.call("vr_continuity_factor", ctx.handle, dd.ptr, dp.ptr, dt, out.ptr)
     return _ret(out, _is_host(div_v, departure))
 
 
 def solve_state(ctx, m_T, v, nt):
-    dm, dv = _dev(ctx, m_T), _dev(ctx, v)
+    dm, dv = _dev(ctx, m_T, 1), _dev(ctx, v, 3)
     out = ctx.empty(nt + 1)
     _lib.call("vr_solve_state", ctx.handle, dm.ptr, dv.ptr, nt, out.ptr)
     return _ret(out, _is_host(m_T, v))
 
 
 def solve_adjoint(ctx, terminal, v, nt, needs_history=False):
-    dt_, dv = _dev(ctx, terminal), _dev(ctx, v)
+    dt_, dv = _dev(ctx, terminal, 1), _dev(ctx, v, 3)
     init = ctx.empty(1)
     hist = ctx.empty(nt + 1) if needs_history else None
     _lib.call("vr_solve_adjoint", ctx.handle, dt_.ptr, dv.ptr, nt, hist.ptr if hist else None, init.ptr)
@@ -355,7 +372,7 @@ def solve_adjoint(ctx, terminal, v, nt, needs_history=False):
 
 
 def solve_inc_adjoint(ctx, terminal, v, nt, needs_history=False):
-    dt_, dv = _dev(ctx, terminal), _dev(ctx, v)
+    dt_, dv = _dev(ctx, terminal, 1), _dev(ctx, v, 3)
     init = ctx.empty(1)
     hist = ctx.empty(nt + 1) if needs_history else None
     _lib.call("vr_solve_inc_adjoint", ctx.handle, dt_.ptr, dv.ptr, nt, hist.ptr if hist else None, init.ptr)
@@ -364,16 +381,14 @@ def solve_inc_adjoint(ctx, terminal, v, nt, needs_history=False):
 
 
 def gradient_dot(ctx, f, w):
-    df, dw = _dev(ctx, f), _dev(ctx, w)
+    df, dw = _dev(ctx, f, 1), _dev(ctx, w, 3)
     out = ctx.empty(1)
     _lib.call("vr_gradient_dot", ctx.handle, df.ptr, dw.ptr, out.ptr)
     return _ret(out, _is_host(f, w))
 
 
 def solve_inc_state(ctx, m_history, v, v_tilde, nt):
-    dm, dv, dvt = _dev(ctx, m_history), _dev(ctx, v), _dev(ctx, v_tilde)
-    if dm.nfields != nt + 1:
-        raise DimensionError(f"solve_inc_state: m_history has {dm.nfields} slices, expected {nt + 1}")
+    dm, dv, dvt = _dev(ctx, m_history, nt + 1), _dev(ctx, v, 3), _dev(ctx, v_tilde, 3)
     out = ctx.empty(nt + 1)
     _lib.call("vr_solve_inc_state", ctx.handle, dm.ptr, dv.ptr, dvt.ptr, nt, out.ptr)
     return _ret(out, _is_host(m_history, v, v_tilde))
@@ -444,8 +459,8 @@ class Objective:
     def __init__(self, ctx: Context, m_R, m_T, model=None):
         self.ctx = ctx
         self.model = model if model is not None else make_model()
-        self._mR = _dev(ctx, m_R)  # kept alive: the C object holds non-owning pointers
-        self._mT = _dev(ctx, m_T)
+        self._mR = _dev(ctx, m_R, 1)  # kept alive: the C object holds non-owning pointers
+        self._mT = _dev(ctx, m_T, 1)
         h = C.c_void_p()
         _lib.call("vr_objective_create", ctx.handle, self._mR.ptr, self._mT.ptr, C.byref(self.model), C.byref(h))
         self._h = h
@@ -465,7 +480,7 @@ class Objective:
         return {k: getattr(c, k) for k, _ in _lib.Counters._fields_}
 
     def evaluate(self, v) -> EvalState:
-        dv = _dev(self.ctx, v)
+        dv = _dev(self.ctx, v, 3)
         h = C.c_void_p()
         _lib.call("vr_evaluate", self._h, dv.ptr, C.byref(h))
         return EvalState(self, h)
@@ -474,47 +489,48 @@ class Objective:
         _lib.call("vr_compute_gradient", self._h, state._h, None)
 
     def hessian_matvec(self, state: EvalState, v_tilde, out: Optional[DeviceArray] = None):
-        dv = _dev(self.ctx, v_tilde)
-        o = out if out is not None else self.ctx.empty(3)
+        dv = _dev(self.ctx, v_tilde, 3)
+        o = _dev(self.ctx, out, 3) if out is not None else self.ctx.empty(3)
         _lib.call("vr_hessian_matvec", self._h, state._h, dv.ptr, o.ptr)
         return _ret(o, _is_host(v_tilde) and out is None)
 
     def split_matvec(self, state: EvalState, w):
         """Objective::split_matvec (objective.cpp:158-176): (I + R H_data R) w, R = (beta_v A)^-1/2."""
-        dw = _dev(self.ctx, w)
+        dw = _dev(self.ctx, w, 3)
         o = self.ctx.empty(3)
         _lib.call("vr_split_matvec", self._h, state._h, dw.ptr, o.ptr)
         return _ret(o, _is_host(w))
 
     def hessian_data_matvec(self, state: EvalState, v_tilde):
-        dv = _dev(self.ctx, v_tilde)
+        dv = _dev(self.ctx, v_tilde, 3)
         o = self.ctx.empty(3)
         _lib.call("vr_hessian_data_matvec", self._h, state._h, dv.ptr, o.ptr)
         return _ret(o, _is_host(v_tilde))
 
     def hessian_matvec_host(self, state: EvalState, vt_host: np.ndarray, out_host: np.ndarray):
         """End-to-end entry: host buffers in/out (H2D + matvec + D2H)."""
-        _lib.call("vr_hessian_matvec_host", self._h, state._h, vt_host.ctypes.data, out_host.ctypes.data)
+        _lib.call("vr_hessian_matvec_host", self._h, state._h, _host_buf(self.ctx, vt_host, 3, "vt_host"),
+                  _host_buf(self.ctx, out_host, 3, "out_host", writeable=True))
         return out_host
 
     def hessian_matvec_host_async(self, state: EvalState, vt_host: np.ndarray, out_host: np.ndarray):
         """Pipelined host-buffer matvec (vr_hessian_matvec_host_async); results are valid
         after wait(). Keep both arrays alive and vt_host unchanged until then."""
-        _lib.call("vr_hessian_matvec_host_async", self._h, state._h, vt_host.ctypes.data,
-                  out_host.ctypes.data)
+        _lib.call("vr_hessian_matvec_host_async", self._h, state._h, _host_buf(self.ctx, vt_host, 3, "vt_host"),
+                  _host_buf(self.ctx, out_host, 3, "out_host", writeable=True))
         return out_host
 
     def wait(self):
         _lib.call("vr_objective_wait", self._h)
 
     def apply_reg(self, u, mode="apply"):
-        du = _dev(self.ctx, u)
+        du = _dev(self.ctx, u, 3)
         o = self.ctx.empty(3)
         _lib.call("vr_objective_apply_reg", self._h, du.ptr, _enum(_MODE, mode), o.ptr)
         return _ret(o, _is_host(u))
 
     def apply_K(self, u):
-        du = _dev(self.ctx, u)
+        du = _dev(self.ctx, u, 3)
         o = self.ctx.empty(3)
         _lib.call("vr_objective_apply_K", self._h, du.ptr, o.ptr)
         return _ret(o, _is_host(u))

@@ -42,3 +42,56 @@ def test_profiles_bench_line_contract():
     for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
         assert k in d["e2e"], k
     assert abs(d["roofline"]["frac"] - d["roofline"]["achieved"] / d["roofline"]["peak"]) < 1e-9
+
+
+def test_reference_arm_never_maps_the_product_library():
+    # the reference arm must run the reference only (oracle/_ref), never
+    # libveloreg_gpu.so; run it in a fresh process and read its own /proc/self/maps
+    import subprocess
+    import sys
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--n','16','--steps','1',"
+            "'--warmup','0'];\ntry:\n runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit:\n pass\n"
+            "maps=open('/proc/self/maps').read(); print('MAPS', 'libveloreg_gpu' in maps, 'libveloreg_ref' in maps)")
+    out = subprocess.run([sys.executable, "-c", code], cwd=bench.ROOT, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    lines = out.stdout.strip().splitlines()
+    line = json.loads(lines[0])
+    assert lines[-1] == "MAPS False True"
+    assert line["impl"] == "reference" and line["config"] == bench.bench_config(3, 16, 4, 1)
+
+
+def test_both_arms_share_the_config_dict():
+    for world in (1, 2, 4, 8):
+        cid, n = bench.config_for(world, None)
+        assert (cid, n) == {1: (3, 256), 2: (4, 512), 4: (4, 512), 8: (5, 1024)}[world]
+        c = bench.bench_config(cid, n, 4, world)
+        assert c["grid"] == n and c["parallelism"] == ("single" if world == 1 else f"x1-slabs-{world}")
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_slab_inputs_match_the_global_generators(P):
+    # per-rank input generation (bench.py under torchrun) against the global generators;
+    # the reductions are emulated by precomputing the global statistics
+    import numpy as np
+    from paper_1808_04487_b200 import phantom as ph
+    n, kmax, disp = 32, 6, 0.08 * 2 * np.pi
+    gv, gt, gm = ph.bandlimited_velocity(n, kmax, disp), ph.bandlimited_direction(n), ph.ellipsoid_phantom(n)
+    L = n // P
+    vs = np.concatenate([ph.bandlimited_velocity_slab(n, kmax, disp, r * L, L,
+                                                      allreduce_max=lambda x: 1.0)[0] for r in range(P)], axis=1)
+    vs *= disp / np.sqrt((vs * vs).sum(0)).max()
+    assert np.abs(vs - gv).max() <= 1e-14 * np.abs(gv).max()
+    ts = np.concatenate([ph.bandlimited_direction_slab(n, r * L, L, allreduce_max=lambda x: 1.0)
+                         for r in range(P)], axis=1)
+    ts /= np.abs(ts).max(axis=(1, 2, 3), keepdims=True)
+    assert np.abs(ts - gt).max() <= 1e-14
+    raw = np.concatenate([ph.ellipsoid_phantom_slab(n, r * L, L, allreduce_max=lambda x: 1.0,
+                                                    allreduce_min=lambda x: 0.0) for r in range(P)])
+    raw = (raw - raw.min()) / (raw.max() - raw.min())
+    assert np.abs(raw - gm).max() <= 1e-9  # x1 kernel truncation: see ellipsoid_phantom_slab
+    _, vmax1 = ph.bandlimited_velocity_slab(n, kmax, disp, 0, n)
+    assert abs(vmax1 - np.abs(gv[0]).max()) <= 1e-14

@@ -1,8 +1,13 @@
 """GPU parity and size-independent properties at BASELINE's full single-GPU sizes.
 
 * config 3 (256^3, the bench workload): one evaluate + reduced gradient + GN
-  Hessian matvec (at half the generating velocity) against the compiled reference run on the host cores (the
-  reference's own objective.cpp:47-156 on the same arrays), relative L2 <= 1e-10.
+  Hessian matvec (at half the generating velocity) against the compiled reference run on
+  the host cores (the reference's own objective.cpp:47-156 on the same arrays): data parts
+  relative L2 <= 1e-10; the beta_v A terms against the exact (long-double) operator, GPU
+  error <= 1.5x the reference's (tests/exact.py).
+* the regularisation operator in all three modes at 256^3 and 512^3 against exact.
+* config 2 (128^3) full solve and config 3 (256^3) beta-continuation solve against the
+  reference: Newton iterations +-1, final mismatch and gradient within 1 %.
 * config 3 and config 4 (512^3 on one GPU): size-independent properties of the
   GN Hessian -- linearity, symmetry of the Gauss-Newton operator in the weighted
   inner product (test_objective.cpp:186-215), positive semi-definiteness, zero in
@@ -29,10 +34,14 @@ def _inputs(vr, ctx, config):
 
 
 def test_config3_reference_parity(vr, ref, ctx):
-    """Data parts at 1e-10. The beta_v A terms are compared at 2e-9: the H2 symbol |k|^4
-    reaches (128 sqrt 3)^4 ~ 2.4e9 at 256^3, so the O(1e-16) round-off two correct fp64
-    FFTs leave in the empty high modes of a band-limited field is amplified to ~1e-10 of
-    ||beta A v|| (measured 1.9e-10; 2e-15 at v = 0 where the term vanishes)."""
+    """Config 3 (the bench workload) against the reference on the host cores and against the
+    exact answer. Data parts (state, mismatch, the adjoint/incremental sweeps) GPU vs
+    reference at 1e-10. The beta_v A terms (proj/src/spectral.cpp:166-184) are measured
+    against beta_v A evaluated in long double on the same input (tests/exact.py): the H2
+    symbol |k|^4 reaches (128 sqrt 3)^4 ~ 2.4e9 at 256^3 and amplifies the round-off of any
+    fp64 FFT pair to ~1e-10 of ||beta A v||, the reference's included (measured: 1.4e-10 vs
+    exact). Bar: the GPU's error against exact is at most 1.5x the reference's."""
+    from exact import exact_reg, no_worse_than_reference, rel_err, sampled_max_err
     from paper_1808_04487_b200 import phantom
     c, n, m_R, m_T, v = _inputs(vr, ctx, 3)
     vt = phantom.bandlimited_direction(n)
@@ -53,12 +62,45 @@ def test_config3_reference_parity(vr, ref, ctx):
     assert abs(s.mismatch_rel - sc["mismatch_rel"]) <= 1e-12 * abs(sc["mismatch_rel"])
     reg = np.asarray(vr.apply_reg_operator(c, v_eval, model.norm, "apply", model.beta_v))
     reg_ref = ref.apply_reg_operator(v_eval, model.norm, 0, model.beta_v)
+    reg_ex = exact_reg(v_eval, "h2", model.beta_v)
+    vt_ex = exact_reg(vt, "h2", model.beta_v)
+    # data parts: GPU vs reference
     assert rel_l2(s.gradient - reg, g_ref - reg_ref) <= 1e-10
-    assert rel_l2(reg, reg_ref) <= 2e-9
-    assert rel_l2(s.gradient, g_ref) <= 2e-9
     assert rel_l2(hdv, hdv_ref) <= 1e-10
-    assert rel_l2(hv, hv_ref) <= 2e-9
+    # beta_v A terms vs exact: the operator itself, the gradient (data part + beta_v A v) and
+    # the full matvec (data part + beta_v A vt), each GPU vs reference error against exact
+    g_ex = (g_ref - reg_ref) + reg_ex
+    hv_ex = hdv_ref + vt_ex
+    errs = {"reg": (rel_err(reg, reg_ex), rel_err(reg_ref, reg_ex)),
+            "gradient": (rel_err(s.gradient, g_ex), rel_err(g_ref, g_ex)),
+            "matvec": (rel_err(hv, hv_ex), rel_err(hv_ref, hv_ex)),
+            "reg_sampled_max": (sampled_max_err(reg, reg_ex), sampled_max_err(reg_ref, reg_ex))}
+    print("config3 (gpu, reference) error vs exact:", errs)
+    for k, (eg, er) in errs.items():
+        assert no_worse_than_reference(eg, er), (k, eg, er)
     assert o.counters()["pde_solves"] == ro.counters()["pde_solves"]
+
+
+@pytest.mark.parametrize("config", [3, 4])
+def test_fullsize_reg_operator_vs_exact(vr, ref, ctx, config):
+    """beta_v A, (beta_v A)^-1 and (beta_v A)^-1/2 (spectral.cpp:166-184; H2, beta 1e-2) of
+    the config's velocity and of the matvec probe at 256^3 / 512^3: GPU and reference
+    errors against the long-double answer (tests/exact.py); GPU <= 1.5x reference."""
+    from exact import exact_reg, no_worse_than_reference, rel_err
+    from paper_1808_04487_b200 import phantom
+    n = phantom.CONFIGS[config]["n"]
+    c = ctx(n)
+    cfg = phantom.CONFIGS[config]
+    norm = vr.make_norm("h2")
+    for name, f in (("v", phantom.bandlimited_velocity(n, cfg["kmax"], cfg["disp"])),
+                    ("vt", phantom.bandlimited_direction(n))):
+        for mode, code in (("apply", 0), ("inverse", 1), ("inverse_sqrt", 2)):
+            ex = exact_reg(f, "h2", 1e-2, mode)
+            eg = rel_err(np.asarray(vr.apply_reg_operator(c, f, norm, mode, 1e-2)), ex)
+            er = rel_err(ref.apply_reg_operator(f, norm, code, 1e-2), ex)
+            print(f"config{config} {name} {mode}: gpu {eg:.3e} reference {er:.3e}")
+            assert no_worse_than_reference(eg, er), (name, mode, eg, er)
+            del ex
 
 
 def _probe(n, seed):
@@ -70,8 +112,8 @@ def _probe(n, seed):
 def test_fullsize_gn_properties(vr, ctx, config):
     """test_objective.cpp:186-215 at full size: exact symmetry / PSD at v = 0 (1e-6), the
     O(discretization) optimize-then-discretize asymmetry at a generic v (< 5e-3, the
-    reference's bound); linearity of the data matvec to round-off (the beta_v A term
-    at the conditioning-scaled 2e-9 (n/256)^4 of test_config3_reference_parity)."""
+    reference's bound); linearity of the data matvec to round-off and of the full matvec
+    within the measured exact-operator error of its beta_v A term."""
     c, n, m_R, m_T, v = _inputs(vr, ctx, config)
     o = vr.Objective(c, m_R, m_T, vr.make_model())
     u, w = c.to_device(_probe(n, 7)), c.to_device(_probe(n, 8))
@@ -83,14 +125,23 @@ def test_fullsize_gn_properties(vr, ctx, config):
         a, b = vr.inner_product(c, Hu, w), vr.inner_product(c, u, Hw)
         assert abs(a - b) <= sym_tol * max(abs(a), abs(b))
         assert vr.inner_product(c, Hu, u) > 0.0
-    # linearity: H(2u - 3w) = 2 Hu - 3 Hw
+    # linearity: H(2u - 3w) = 2 Hu - 3 Hw. The data matvec to round-off; the full matvec up to
+    # its beta_v A term's measured distance from the exact (long-double) operator, which is
+    # linear: |D| <= |D_data| + e(2u - 3w) + 2 e(u) + 3 e(w), e(x) = ||beta A_gpu x - beta A x||
+    from exact import exact_reg
     comb = c.to_device(2.0 * u.numpy() - 3.0 * w.numpy())
     lhs = o.hessian_data_matvec(s, comb).numpy()
     rhs = 2.0 * o.hessian_data_matvec(s, u).numpy() - 3.0 * o.hessian_data_matvec(s, w).numpy()
     assert rel_l2(lhs, rhs) <= 1e-12
+    d_data = np.linalg.norm((lhs - rhs).ravel())
+    bound = d_data
+    for x, k in ((comb, 1.0), (u, 2.0), (w, 3.0)):
+        xa = x.numpy()
+        gx = np.asarray(vr.apply_reg_operator(c, x, vr.make_norm("h2"), "apply", 1e-2).numpy())
+        bound += k * float(np.sqrt(((gx - exact_reg(xa, "h2", 1e-2)) ** 2).sum()))
     lhs = o.hessian_matvec(s, comb).numpy()
     rhs = 2.0 * Hu.numpy() - 3.0 * Hw.numpy()
-    assert rel_l2(lhs, rhs) <= 2e-9 * (n / 256) ** 4  # |k|^4 amplification grows as n^4
+    assert np.linalg.norm((lhs - rhs).ravel()) <= 1.01 * bound + 1e-14 * np.linalg.norm(rhs.ravel())
     # zero in -> zero out
     z = c.to_device(np.zeros((3, n, n, n)))
     assert vr.max_abs(c, o.hessian_matvec(s, z)) == 0.0
@@ -133,23 +184,24 @@ def test_config4_reference_parity(vr, ref, ctx):
     g_ref = ro.compute_gradient(rs)
     hdv_ref = ro.hessian_data_matvec(rs, vt)
     sc = rs.scalars()
+    from exact import exact_reg, no_worse_than_reference, rel_err
     reg = np.asarray(vr.apply_reg_operator(c, v_eval, model.norm, "apply", model.beta_v))
     reg_ref = ref.apply_reg_operator(v_eval, model.norm, 0, model.beta_v)
+    reg_ex = exact_reg(v_eval, "h2", model.beta_v)
     errs = {"objective": abs(s.objective - sc["objective"]) / abs(sc["objective"]),
-            "gradient_data": rel_l2(g - reg, g_ref - reg_ref), "reg": rel_l2(reg, reg_ref),
-            "data_matvec": rel_l2(hdv, hdv_ref)}
+            "gradient_data": rel_l2(g - reg, g_ref - reg_ref), "data_matvec": rel_l2(hdv, hdv_ref),
+            "reg_vs_exact": (rel_err(reg, reg_ex), rel_err(reg_ref, reg_ex))}
     print("config4 parity", errs)
     assert errs["objective"] <= 1e-12
     assert errs["gradient_data"] <= 1e-10 and errs["data_matvec"] <= 1e-10
-    assert errs["reg"] <= 2e-9 * (n / 256) ** 4
+    assert no_worse_than_reference(*errs["reg_vs_exact"])
 
 
-@pytest.mark.skipif(not __import__("os").environ.get("VR_FULLSIZE_SOLVE"),
-                    reason="~10 min of reference CPU time; set VR_FULLSIZE_SOLVE=1")
 def test_config3_solve_vs_reference(vr, ref, ctx):
     """Config 3 end to end: beta continuation 1 -> 1e-1 -> 1e-2 on the GPU
-    and in the reference on the host cores; per level Newton iterations +-1, final mismatch
-    and gradient norm within 1 % (BASELINE north star). On demand; result in DESIGN.md."""
+    and in the reference on the host cores (~6.5 min on 16 cores); per level Newton
+    iterations +-1, final mismatch and gradient norm within 1 % (BASELINE north star;
+    proj/src/solver.cpp:154-269)."""
     c, n, m_R, m_T, v = _inputs(vr, ctx, 3)
     model, params = vr.make_model(), vr.make_params(eps_opt=1e-2)
     v0 = np.zeros((3, n, n, n))
@@ -163,3 +215,24 @@ def test_config3_solve_vs_reference(vr, ref, ctx):
         assert abs(a["outer_iterations"] - b["outer_iterations"]) <= 1
     assert abs(rg[-1]["final_mismatch_rel"] - rr[-1]["final_mismatch_rel"]) <= 1e-2 * rr[-1]["final_mismatch_rel"]
     assert abs(rg[-1]["final_grad_rel"] - rr[-1]["final_grad_rel"]) <= 1e-2 * rr[-1]["final_grad_rel"]
+
+
+def test_config2_solve_vs_reference(vr, ref, ctx):
+    """Config 2 (128^3 section-4.2 problem, proj/src/synthetic.cpp:16-34): full GN-Krylov
+    solve on the GPU and in the reference; Newton iterations +-1, final mismatch and gradient
+    norm within 1 %, same stop reason (proj/src/solver.cpp:154-269)."""
+    n = 128
+    c = ctx(n)
+    m_R, m_T, _ = ref.generate_synthetic((n, n, n), 4)
+    model, params = vr.make_model(), vr.make_params(eps_opt=1e-2)
+    v0 = np.zeros((3, n, n, n))
+    res = vr.gauss_newton_solve(c, m_R, m_T, v0, model, params)
+    vref, rr, _ = ref.gauss_newton_solve(m_R, m_T, v0, model, params)
+    rg = res.report
+    print("config2 solve GPU", rg["outer_iterations"], rg["final_mismatch_rel"], rg["final_grad_rel"],
+          "REF", rr["outer_iterations"], rr["final_mismatch_rel"], rr["final_grad_rel"])
+    assert rg["stop"] == rr["stop"]
+    assert abs(rg["outer_iterations"] - rr["outer_iterations"]) <= 1
+    assert abs(rg["final_mismatch_rel"] - rr["final_mismatch_rel"]) <= 1e-2 * rr["final_mismatch_rel"]
+    assert abs(rg["final_grad_rel"] - rr["final_grad_rel"]) <= 1e-2 * rr["final_grad_rel"]
+    assert rel_l2(res.v, vref) <= 1e-6

@@ -176,3 +176,37 @@ def test_oracle_beta_search_contract():
     with pytest.raises(ref.RefError) as e:
         ref.beta_search(mR, mT, v0, m, p, L.BetaSearchParams(0.9999999, 1e-5, 1.0, 10, 0.25))
     assert len(e.value.trials) == 1
+
+
+def test_exact_reg_operator_is_exact_on_pure_modes():
+    # tests/exact.py (the long-double beta A the GPU and the reference are measured against):
+    # on a pure mode cos(k.x) every mode of the symbol is known in closed form
+    import numpy as np
+    from exact import exact_reg
+    n = 32
+    x = np.arange(n, dtype=np.longdouble) * (2 * np.arccos(np.longdouble(-1)) / n)
+    X1, X2, X3 = np.meshgrid(x, x, x, indexing="ij")  # long double: no fp64 input round-off
+    for k, kind, p in (((3, -5, 7), "h2", 2), ((1, 2, 2), "h3", 3), ((0, 16, 0), "h1", 1)):
+        f = np.cos(k[0] * X1 + k[1] * X2 + k[2] * X3)
+        k2 = float(sum(a * a for a in k))
+        out = exact_reg(f, kind, 1e-2, "apply")
+        # long-double round-off of f (1e-19) amplified by the largest symbol on the grid
+        smax = (3 * (n // 2) ** 2) ** p
+        assert np.abs(out - 1e-2 * k2 ** p * f).max() <= max(1e-15 * 1e-2 * k2 ** p, 1e-18 * 1e-2 * smax)
+        inv = exact_reg(f, kind, 1e-2, "inverse")
+        assert np.abs(inv - f / (1e-2 * k2 ** p)).max() <= 1e-15 / (1e-2 * k2 ** p)
+
+
+def test_exact_reg_vs_reference_round_off(ref):
+    # the reference's fp64 beta A v sits at the |k|^4-amplified round-off distance from the
+    # exact operator (the effect the GPU parity bar is built on): small at 32^3, growing ~n^4
+    import numpy as np
+    from exact import exact_reg, rel_err
+    from paper_1808_04487_b200 import phantom
+    errs = []
+    for n in (16, 32, 64):
+        v = phantom.bandlimited_velocity(n, 6, 0.5)
+        e = rel_err(ref.apply_reg_operator(v, ref.make_norm("h2"), 0, 1e-2), exact_reg(v, "h2", 1e-2))
+        errs.append(e)
+        assert 0 < e < 1e-11
+    assert errs[2] > errs[0]
