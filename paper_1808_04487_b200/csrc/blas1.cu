@@ -125,9 +125,11 @@ void reduce(vr_ctx* ctx, const double* a, const double* b, long long n, int ncom
     VR_LAUNCH(ctx, "reduce", k_finalize<is_max<OP>()><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nb, ctx->red_out););
     VR_CUDA(cudaMemcpyAsync(ctx->red_host, ctx->red_out, sizeof(double) * ncomp,
                             cudaMemcpyDeviceToHost, ctx->stream));
+    flags_enqueue_copy(ctx);  // deferred matvec flags ride on this synchronisation
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int c = 0; c < ncomp; ++c) host_out[c] = ctx->red_host[c];
     if (ctx->dist) ctx->dist->allreduce(ctx, host_out, ncomp, is_max<OP>());  // rank order
+    flags_after_sync(ctx);
 }
 
 unsigned ew_grid(long long n) {
@@ -269,9 +271,11 @@ void finalize_sums(vr_ctx* ctx, int nblocks, int ncomp, double* host_out) {
     VR_LAUNCH(ctx, "blas1", k_finalize<false><<<ncomp, 256, 0, ctx->stream>>>(ctx->red_partials, nblocks, ctx->red_out););
     VR_CUDA(cudaMemcpyAsync(ctx->red_host, ctx->red_out, sizeof(double) * ncomp,
                             cudaMemcpyDeviceToHost, ctx->stream));
+    flags_enqueue_copy(ctx);
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int c = 0; c < ncomp; ++c) host_out[c] = ctx->red_host[c];
     if (ctx->dist) ctx->dist->allreduce(ctx, host_out, ncomp, false);
+    flags_after_sync(ctx);
 }
 
 }  // namespace vr

@@ -957,10 +957,16 @@ int vr_objective_set_beta(vr_objective* obj, double beta_v) {
         obj->model.beta_v = beta_v;
     });
 }
+// every objective entry point first completes pipelined host-buffer matvecs
+// (vr_hessian_matvec_host_async), so their deferred non-finite check cannot be lost
+static void drain_pipe(vr_objective* obj) {
+    if (obj->pipe.issued) vr::objective_pipe_wait(obj);
+}
 int vr_evaluate(vr_objective* obj, const double* v3, vr_state** out_state) {
     return guard([&] {
         need(obj && v3 && out_state, "vr_evaluate");
         set_dev(obj->ctx);
+        drain_pipe(obj);
         *out_state = vr::objective_evaluate(obj, v3);
     });
 }
@@ -1022,6 +1028,7 @@ int vr_compute_gradient(vr_objective* obj, vr_state* s, double* g3) {
     return guard([&] {
         need(obj && s, "vr_compute_gradient");
         set_dev(obj->ctx);
+        drain_pipe(obj);
         vr::objective_gradient(obj, s);
         if (g3)
             VR_CUDA(cudaMemcpyAsync(g3, s->grad, sizeof(double) * 3 * obj->ctx->g.N,
@@ -1032,15 +1039,18 @@ int vr_hessian_matvec(vr_objective* obj, const vr_state* s, const double* vt3, d
     return guard([&] {
         need(obj && s && vt3 && out3, "vr_hessian_matvec");
         set_dev(obj->ctx);
-        if (obj->pipe.issued) vr::objective_pipe_wait(obj);  // drain pipelined calls first
+        drain_pipe(obj);
         vr::objective_matvec(obj, s, vt3, out3, true);
+        vr::drain_flags(obj->ctx);  // the public call reports a non-finite direction itself
     });
 }
 int vr_hessian_data_matvec(vr_objective* obj, const vr_state* s, const double* vt3, double* out3) {
     return guard([&] {
         need(obj && s && vt3 && out3, "vr_hessian_data_matvec");
         set_dev(obj->ctx);
+        drain_pipe(obj);
         vr::objective_matvec(obj, s, vt3, out3, false);
+        vr::drain_flags(obj->ctx);
     });
 }
 int vr_hessian_matvec_host(vr_objective* obj, const vr_state* s, const double* vt3_host,
@@ -1049,21 +1059,16 @@ int vr_hessian_matvec_host(vr_objective* obj, const vr_state* s, const double* v
         need(obj && s && vt3_host && out3_host, "vr_hessian_matvec_host");
         vr_ctx* ctx = obj->ctx;
         set_dev(ctx);
+        drain_pipe(obj);
         const size_t bytes = sizeof(double) * 3 * ctx->g.N;
-        double* vt = vr::dev_alloc(ctx, 3 * ctx->g.N);
-        double* out = vr::dev_alloc(ctx, 3 * ctx->g.N);
-        try {
-            VR_CUDA(cudaMemcpyAsync(vt, vt3_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-            vr::objective_matvec(obj, s, vt, out, true);
-            VR_CUDA(cudaMemcpyAsync(out3_host, out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-            VR_CUDA(cudaStreamSynchronize(ctx->stream));
-        } catch (...) {
-            vr::dev_free(ctx, vt);
-            vr::dev_free(ctx, out);
-            throw;
-        }
-        vr::dev_free(ctx, vt);
-        vr::dev_free(ctx, out);
+        if (!obj->host_vt) obj->host_vt = vr::dev_alloc(ctx, 3 * ctx->g.N);
+        if (!obj->host_out) obj->host_out = vr::dev_alloc(ctx, 3 * ctx->g.N);
+        VR_CUDA(cudaMemcpyAsync(obj->host_vt, vt3_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        vr::objective_matvec(obj, s, obj->host_vt, obj->host_out, true);
+        VR_CUDA(cudaMemcpyAsync(out3_host, obj->host_out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        vr::flags_enqueue_copy(ctx);  // the flags ride on the download's synchronisation
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        vr::flags_after_sync(ctx);
     });
 }
 int vr_hessian_matvec_host_async(vr_objective* obj, const vr_state* s, const double* vt3_host,
@@ -1085,6 +1090,7 @@ int vr_objective_apply_reg(vr_objective* obj, const double* u3, int mode, double
     return guard([&] {
         need(obj && u3 && out3, "vr_objective_apply_reg");
         set_dev(obj->ctx);
+        drain_pipe(obj);
         vr::objective_apply_reg(obj, u3, mode, out3);
     });
 }
@@ -1092,6 +1098,7 @@ int vr_objective_apply_K(vr_objective* obj, const double* u3, double* out3) {
     return guard([&] {
         need(obj && u3 && out3, "vr_objective_apply_K");
         set_dev(obj->ctx);
+        drain_pipe(obj);
         vr::objective_apply_K(obj, u3, out3);
     });
 }
@@ -1110,6 +1117,7 @@ int vr_pcg_solve(vr_objective* obj, const vr_state* s, const double* rhs3, doubl
         need(obj && s && rhs3 && x3 && stats, "vr_pcg_solve");
         vr_ctx* ctx = obj->ctx;
         set_dev(ctx);
+        drain_pipe(obj);
         const long long n3 = 3 * ctx->g.N;
         vr::DevOp op = [&](const double* u, double* out) {
             vr::objective_matvec(obj, s, u, out, true);
@@ -1124,6 +1132,7 @@ int vr_pcg_solve(vr_objective* obj, const vr_state* s, const double* rhs3, doubl
         *stats = precond == VR_PRECOND_SPECTRAL
                      ? vr::pcg_solve_gn(obj, s, rhs3, rel_tol, max_iter, x3)
                      : vr::pcg_solve(ctx, op, rhs3, rel_tol, max_iter, pc, x3);
+        vr::drain_flags(ctx);
     });
 }
 static void copy_records(const vr::GnResult& r, vr_iteration_record* recs, int max_recs,
@@ -1352,10 +1361,12 @@ int vr_split_matvec(vr_objective* obj, const vr_state* state, const double* w3, 
     return guard([&] {
         need(obj && state && w3 && out3, "vr_split_matvec");
         set_dev(obj->ctx);
+        drain_pipe(obj);
         if (!state->has_adjoint_ctx)
             vr::throw_logic("split_matvec: evaluation context is missing the adjoint sweep data "
                             "(compute the gradient first)");
         vr::split_matvec(obj, state, w3, out3);
+        vr::drain_flags(obj->ctx);
     });
 }
 int vr_twolevel_create(const vr_twolevel_options* opts, vr_twolevel** out) {
@@ -1373,6 +1384,7 @@ int vr_twolevel_rebuild(vr_twolevel* tl, vr_objective* obj, const vr_state* stat
     return guard([&] {
         need(tl && obj && state, "vr_twolevel_rebuild");
         set_dev(obj->ctx);
+        drain_pipe(obj);
         tl->tl.rebuild(obj, state, eps_H);
     });
 }
@@ -1381,12 +1393,15 @@ int vr_twolevel_apply(vr_twolevel* tl, vr_ctx* ctx, const double* r3, double* z3
         need(tl && r3 && z3, "vr_twolevel_apply");
         set_dev(ctx);
         tl->tl.apply(ctx, r3, z3);
+        vr::drain_flags(ctx);
+        if (tl->tl.cctx) vr::drain_flags(tl->tl.cctx);
     });
 }
 int vr_twolevel_coarse_matvec(vr_twolevel* tl, const double* u3, double* out3) {
     return guard([&] {
         need(tl && u3 && out3, "vr_twolevel_coarse_matvec");
         tl->tl.coarse_matvec(u3, out3);
+        if (tl->tl.cctx) vr::drain_flags(tl->tl.cctx);
     });
 }
 int vr_twolevel_info(const vr_twolevel* tl, int dims[3], int* lanczos_runs, int* inner_diverged,

@@ -24,7 +24,7 @@ vr_state::~vr_state() {
 
 vr_objective::~vr_objective() {
     if (!ctx) return;
-    for (double* p : {ws_lam, ws_tmp, ws_div, ws_b}) vr::dev_free(ctx, p);
+    for (double* p : {ws_lam, ws_tmp, ws_div, ws_b, host_vt, host_out}) vr::dev_free(ctx, p);
     if (pipe.h2d) {
         cudaStreamSynchronize(pipe.h2d);
         cudaStreamSynchronize(pipe.d2h);
@@ -149,17 +149,47 @@ void exchange(vr_ctx* ctx, double* interior) {
         ctx->dist->halo(ctx, interior, static_cast<size_t>(ctx->g.n2) * ctx->g.n3, ctx->g.L,
                         ctx->g.halo);
 }
-// raise the per-call device flags: [0] non-finite direction, [1] departure beyond halo
-void check_flags(vr_ctx* ctx, const char* what) {
-    VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, 2 * sizeof(int), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+// The per-call device flags: [0] non-finite direction, [1] departure beyond halo. They
+// are sticky and reset whenever they are read. A matvec inside the solver does not
+// synchronise for them: it marks them pending (defer_flags) and the next reduction
+// (PCG's s.Hs) copies them back together with its result, raising the same error one
+// reduction later; public entry points drain them before returning.
+namespace {
+void raise_flags(vr_ctx* ctx, const char* what) {
     double f[2] = {static_cast<double>(ctx->flag_host[0]), static_cast<double>(ctx->flag_host[1])};
     if (ctx->dist) ctx->dist->allreduce(ctx, f, 2, true);
+    if (f[0] != 0.0 || f[1] != 0.0)
+        VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
     if (f[1] != 0.0)
         throw_resource(std::string(what) + ": departure points beyond the x1 halo of " +
                        std::to_string(ctx->g.halo) + " planes (use a wider halo or fewer ranks)");
     if (f[0] != 0.0) throw_numeric(std::string(what) + ": non-finite direction");
+}
+}  // namespace
+
+void check_flags(vr_ctx* ctx, const char* what) {
+    ctx->flags_pending = nullptr;
+    VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    raise_flags(ctx, what);
+}
+void defer_flags(vr_ctx* ctx, const char* what) {
+    if (!ctx->flags_pending) ctx->flags_pending = what;
+}
+void drain_flags(vr_ctx* ctx) {
+    if (ctx->flags_pending) check_flags(ctx, ctx->flags_pending);
+}
+void flags_enqueue_copy(vr_ctx* ctx) {
+    if (ctx->flags_pending)
+        VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, 2 * sizeof(int),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+}
+void flags_after_sync(vr_ctx* ctx) {
+    if (!ctx->flags_pending) return;
+    const char* what = ctx->flags_pending;
+    ctx->flags_pending = nullptr;
+    raise_flags(ctx, what);
 }
 
 vr_state* objective_evaluate(vr_objective* o, const double* v3) {
@@ -173,6 +203,7 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
     s->obj = o;
     s->nt = nt;
     try {
+        drain_flags(ctx);
         VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
         s->v = dev_alloc(ctx, 3 * N);
         s->xb = dev_alloc(ctx, 3 * N);
@@ -253,6 +284,7 @@ static void prepare_adjoint_ctx(vr_objective* o, vr_state* s) {
     if (!s->xf) s->xf = dev_alloc(ctx, 3 * N);
     if (!s->factor) s->factor = dev_alloc(ctx, N);
     if (!s->gradm) s->gradm = dev_alloc(ctx, 3LL * (nt + 1) * N);
+    drain_flags(ctx);
     VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
     if (ctx->dist)
         sl_trace(ctx, pslice(ctx, s->vpad, 0), ctx->hstride, nt, VR_TRACE_FORWARD, s->xf);
@@ -354,7 +386,8 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     const int nt = s->nt;
     const double dt = 1.0 / nt;
     const double hdt = 0.5 / nt;
-    if (check) VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
+    if (check && !ctx->flags_pending)  // stale flags of an unchecked call must not surface here
+        VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
     // beta_v A vt depends only on vt: its FFT passes (HBM-bound) run on the side
     // stream under the L1-bound transport sweeps; only the c2r + add waits for b
     if (add_reg)
@@ -466,7 +499,7 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
         }
     }
     o->counters.hessian_matvecs += 1;
-    if (check) check_flags(ctx, "hessian_matvec");
+    if (check) defer_flags(ctx, "hessian_matvec");  // raised by the next reduction or drain
 }
 
 void objective_matvec_host_async(vr_objective* o, const vr_state* s, const double* vt3_host,
@@ -491,7 +524,10 @@ void objective_matvec_host_async(vr_objective* o, const vr_state* s, const doubl
         }
         VR_CUDA(cudaStreamSynchronize(ctx->stream));  // slots allocated on the compute stream
     }
-    if (P.issued == 0) VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
+    if (P.issued == 0) {
+        drain_flags(ctx);
+        VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
+    }
     const int q = static_cast<int>(P.issued & 1);
     // upload once the compute two calls back has finished reading this slot
     VR_CUDA(cudaStreamWaitEvent(P.h2d, P.done[q], 0));
@@ -644,7 +680,7 @@ vr_pcg_stats pcg_solve_gn(vr_objective* o, const vr_state* s, const double* rhs,
         pcg_direction(ctx, nullptr, u, nullptr, r, 0.0, mean);  // u = beta_v A z
         double rz = dot_l2_vec(ctx, r, z);
         for (int it = 0; it < max_iter; ++it) {
-            objective_matvec(o, s, sd, Hs, false, u);
+            objective_matvec(o, s, sd, Hs, false, u);  // flags checked with the s.Hs reduction
             const double sHs = dot_l2_vec(ctx, sd, Hs);
             if (sHs <= 0.0) {
                 st.negative_curvature = 1;

@@ -40,6 +40,10 @@ struct vr_objective {
     double* ws_tmp = nullptr;  // 2 halo-padded fields
     double* ws_div = nullptr;  // 1 halo-padded field (div v, gathered by the factor)
     double* ws_b = nullptr;    // 3N
+    // device staging of the synchronous host-buffer matvec (vr_hessian_matvec_host),
+    // allocated on first use and kept: no per-call allocation on the e2e path
+    double* host_vt = nullptr;   // 3N
+    double* host_out = nullptr;  // 3N
     // pipelined host-buffer matvecs (vr_hessian_matvec_host_async): two device slots;
     // H2D and D2H on their own streams so step k+1's upload and step k's download
     // overlap step k / k+1 compute on the context's stream

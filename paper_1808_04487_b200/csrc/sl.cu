@@ -757,6 +757,7 @@ void convert_d2f(vr_ctx* ctx, const double* a, float* b, long long n) {
     VR_LAUNCH(ctx, "sl_pointwise", k_d2f<<<grid_1d(n, kThreads), kThreads, 0, ctx->stream>>>(a, b, n));
 }
 bool all_finite_f32(vr_ctx* ctx, const float* a, long long n) {
+    drain_flags(ctx);
     VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, sizeof(int), ctx->stream));
     VR_LAUNCH(ctx, "sl_pointwise", k_nonfinite_f32<<<grid_1d(n, kThreads), kThreads, 0, ctx->stream>>>(a, n, ctx->flag_dev));
     VR_CUDA(cudaMemcpyAsync(ctx->flag_host, ctx->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

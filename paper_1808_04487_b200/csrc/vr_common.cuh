@@ -128,6 +128,9 @@ struct vr_ctx {
     double* red_host = nullptr;      // pinned host, 8 doubles
     int* flag_dev = nullptr;         // device int flags (non-finite detection)
     int* flag_host = nullptr;        // pinned
+    // deferred flag check: the operation that raised flags last (e.g. "hessian_matvec"),
+    // read back by the next host synchronisation (a reduction) instead of its own sync
+    const char* flags_pending = nullptr;
     long long launches = 0;
     // optional per-launch CUDA-event timing (bench / roofline evidence)
     bool profiling = false;
@@ -220,6 +223,13 @@ double sum_sq_diff(vr_ctx* ctx, const double* a, const double* b, long long n);
 double min_value(vr_ctx* ctx, const double* a, long long n);
 double max_value(vr_ctx* ctx, const double* a, long long n);
 void affine(vr_ctx* ctx, const double* x, double* out, long long n, double lo, double s);
+// deferred device-flag checks (objective.cu): `defer_flags` marks the flags raised by an
+// enqueued operation; the next reduction copies them back with its result (no extra
+// synchronisation) and `flags_after_sync` raises them; `drain_flags` checks now
+void defer_flags(vr_ctx* ctx, const char* what);
+void drain_flags(vr_ctx* ctx);
+void flags_enqueue_copy(vr_ctx* ctx);
+void flags_after_sync(vr_ctx* ctx);
 // device-side partial reduction helper: finalize `nblocks` partial sums (ncomp
 // interleaved per block) into red_out[0..ncomp) and copy to host
 void finalize_sums(vr_ctx* ctx, int nblocks, int ncomp, double* host_out);

@@ -1,0 +1,411 @@
+// gather_lab.cu -- standalone micro-benchmark of the semi-Lagrangian tricubic gather
+// (interp.hpp:32-53 arithmetic) at real departure points, comparing:
+//   A  one point per thread through L1 (the shipped sl.cu gather, 1x4x32 tiles)
+//   D  per-tile stencil box staged in shared memory by the bulk-copy engine
+//      (cp.async.bulk row segments + mbarrier, double-buffered persistent CTAs),
+//      gathered with LDS; tiles whose box overflows fall back to A's path
+// Inputs: raw fp64 files written by tools/gather_lab_inputs.py (departure points
+// X (3N) and a field f (N)). Prints one JSON line per variant.
+//
+// build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo
+//        -Xptxas -v tools/gather_lab.cu -o gpurun_out/gather_lab
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+            exit(1);                                                                  \
+        }                                                                             \
+    } while (0)
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+struct G {
+    int n;  // cubic grid n^3 (power of two)
+    double h;
+};
+
+__device__ __forceinline__ void cubic_weights(double s, double* w) {
+    const double sm1 = s - 1.0, sm2 = s - 2.0, sp1 = s + 1.0;
+    w[0] = -s * sm1 * sm2 * (1.0 / 6.0);
+    w[1] = sp1 * sm1 * sm2 * 0.5;
+    w[2] = -sp1 * s * sm2 * 0.5;
+    w[3] = sp1 * s * sm1 * (1.0 / 6.0);
+}
+__device__ __forceinline__ void axis_stencil(double x, double h, int& b, double* w) {
+    double u = x / h;
+    const double r = rint(u);
+    if (fabs(u - r) < 1e-12) u = r;
+    const double fl = floor(u);
+    cubic_weights(u - fl, w);
+    b = static_cast<int>(fl) - 1;
+}
+__device__ __forceinline__ int wrapi(int j, int n) { return j & (n - 1); }
+// base nearest to the point's own index (departure coords are wrapped into [0, 2pi))
+__device__ __forceinline__ int near(int b, int i, int n) {
+    int d = b - i;
+    d = ((d + n / 2) & (n - 1)) - n / 2;
+    return i + d;
+}
+
+// ---------------------------------------------------------------- variant A
+__device__ __forceinline__ double gather_l1(const double* __restrict__ f, int n, const int b[3],
+                                            const double w[3][4]) {
+    const int n23 = n * n;
+    int o12[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int oa = wrapi(b[0] + a, n) * n23;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) o12[a][bb] = oa + wrapi(b[1] + bb, n) * n;
+    }
+    const int b3 = b[2];
+    double acc = 0.0;
+    if (b3 >= 0 && b3 + 3 < n) {
+        const double* f3 = f + b3;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double acc1 = 0.0;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                const double* p = f3 + o12[a][bb];
+                double acc2 = 0.0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc2 += w[2][c] * __ldg(p + c);
+                acc1 += w[1][bb] * acc2;
+            }
+            acc += w[0][a] * acc1;
+        }
+    } else {
+        int i3[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) i3[c] = wrapi(b3 + c, n);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double acc1 = 0.0;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                const double* p = f + o12[a][bb];
+                double acc2 = 0.0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc2 += w[2][c] * __ldg(p + i3[c]);
+                acc1 += w[1][bb] * acc2;
+            }
+            acc += w[0][a] * acc1;
+        }
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(128, 7) k_gather_A(const double* __restrict__ f, const double* __restrict__ X,
+                                                     double* __restrict__ out, G g) {
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int i3 = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int i2 = blockIdx.y * 4 + (threadIdx.x >> 5);
+    const int i1 = blockIdx.z;
+    const long long i = ((long long)i1 * n + i2) * n + i3;
+    int b[3];
+    double w[3][4];
+    axis_stencil(__ldg(X + i), g.h, b[0], w[0]);
+    axis_stencil(__ldg(X + N + i), g.h, b[1], w[1]);
+    axis_stencil(__ldg(X + 2 * N + i), g.h, b[2], w[2]);
+    out[i] = gather_l1(f, n, b, w);
+}
+
+// ---------------------------------------------------------------- tiles / boxes
+template <int T1, int T2>
+struct TileGeo {
+    static constexpr int P = T1 * T2 * 32;
+};
+
+// per tile: box origin (unwrapped, nearest image to the points) and extents;
+// ext.w = -1 when the box does not fit (then the tile is gathered through L1)
+template <int T1, int T2>
+__global__ void k_boxes(const double* __restrict__ X, G g, int4* __restrict__ org, int4* __restrict__ ext,
+                        int rows_max, int pitch) {
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int tiles3 = n / 32, tiles2 = n / T2;
+    const int t = blockIdx.x;
+    const int t3 = t % tiles3, t2 = (t / tiles3) % tiles2, t1 = t / (tiles3 * tiles2);
+    int mn[3] = {1 << 29, 1 << 29, 1 << 29}, mx[3] = {-(1 << 29), -(1 << 29), -(1 << 29)};
+    for (int p = threadIdx.x; p < TileGeo<T1, T2>::P; p += blockDim.x) {
+        const int l3 = p & 31, r = p >> 5;
+        const int i1 = t1 * T1 + r / T2, i2 = t2 * T2 + r % T2, i3 = t3 * 32 + l3;
+        const long long i = ((long long)i1 * n + i2) * n + i3;
+        const int own[3] = {i1, i2, i3};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            int b;
+            double w[4];
+            axis_stencil(__ldg(X + c * N + i), g.h, b, w);
+            b = near(b, own[c], n);
+            mn[c] = min(mn[c], b);
+            mx[c] = max(mx[c], b);
+        }
+    }
+    __shared__ int smn[3][32], smx[3][32];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        int a = mn[c], z = mx[c];
+        for (int o = 16; o; o >>= 1) {
+            a = min(a, __shfl_xor_sync(~0u, a, o));
+            z = max(z, __shfl_xor_sync(~0u, z, o));
+        }
+        if ((threadIdx.x & 31) == 0) smn[c][threadIdx.x >> 5] = a, smx[c][threadIdx.x >> 5] = z;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a[3], z[3];
+        for (int c = 0; c < 3; ++c) {
+            a[c] = smn[c][0], z[c] = smx[c][0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a[c] = min(a[c], smn[c][w]), z[c] = max(z[c], smx[c][w]);
+        }
+        const int E1 = z[0] - a[0] + 4, E2 = z[1] - a[1] + 4;
+        const int o3a = a[2] & ~1;
+        const int W = ((z[2] + 4 - o3a) + 1) & ~1;  // even number of doubles from the even origin
+        const bool ok = E1 * E2 <= rows_max && W <= pitch && W <= n;
+        org[t] = make_int4(a[0], a[1], o3a, 0);
+        ext[t] = make_int4(E1, E2, W, ok ? 1 : -1);
+    }
+}
+
+// ---------------------------------------------------------------- variant D
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.b32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(su32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// issue the row-segment copies of tile t's box into `buf` (warp 0)
+__device__ __forceinline__ void issue_box(const double* __restrict__ f, int n, int4 o, int4 e, double* buf,
+                                          int pitch, unsigned long long* bar) {
+    const int lane = threadIdx.x & 31;
+    const int rows = e.x * e.y;
+    if (lane == 0) mbar_expect(bar, (unsigned)(rows * e.z * 8));
+    __syncwarp();
+    const int s = o.z & (n - 1);  // even
+    const int first = min(e.z, n - s);
+    for (int r = lane; r < rows; r += 32) {
+        const int a = r / e.y, b = r - a * e.y;
+        const double* row = f + ((long long)wrapi(o.x + a, n) * n + wrapi(o.y + b, n)) * n;
+        double* d = buf + r * pitch;
+        bulk_g2s(d, row + s, first * 8, bar);
+        if (first < e.z) bulk_g2s(d + first, row, (e.z - first) * 8, bar);
+    }
+}
+
+template <int T1, int T2, int PITCH, int ROWS, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_gather_D(const double* __restrict__ f, const double* __restrict__ X,
+                                                     double* __restrict__ out, G g, const int4* __restrict__ org,
+                                                     const int4* __restrict__ ext, int ntiles) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* buf[2] = {reinterpret_cast<double*>(smem_raw), reinterpret_cast<double*>(smem_raw) + ROWS * PITCH};
+    __shared__ unsigned long long bar[2];
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int tiles3 = n / 32, tiles2 = n / T2;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned phase[2] = {0, 0};
+    int t = blockIdx.x;
+    if (t < ntiles && threadIdx.x < 32) {
+        int4 e = ext[t];
+        if (e.w > 0) issue_box(f, n, org[t], e, buf[0], PITCH, &bar[0]);
+    }
+    for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+        const int s = k & 1;
+        const int tn = t + gridDim.x;
+        if (tn < ntiles && threadIdx.x < 32) {
+            int4 e = ext[tn];
+            if (e.w > 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_box(f, n, org[tn], e, buf[s ^ 1], PITCH, &bar[s ^ 1]);
+            }
+        }
+        const int4 o = org[t], e = ext[t];
+        const bool staged = e.w > 0;
+        if (staged) {
+            mbar_wait(&bar[s], phase[s]);
+            phase[s] ^= 1;
+        }
+        const int t3 = t % tiles3, t2 = (t / tiles3) % tiles2, t1 = t / (tiles3 * tiles2);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+        for (int r = warp; r < T1 * T2; r += 8) {
+            const int i1 = t1 * T1 + r / T2, i2 = t2 * T2 + r % T2, i3 = t3 * 32 + lane;
+            const long long i = ((long long)i1 * n + i2) * n + i3;
+            int b[3];
+            double w[3][4];
+            axis_stencil(__ldg(X + i), g.h, b[0], w[0]);
+            axis_stencil(__ldg(X + N + i), g.h, b[1], w[1]);
+            axis_stencil(__ldg(X + 2 * N + i), g.h, b[2], w[2]);
+            double acc = 0.0;
+            if (staged) {
+                const int r1 = near(b[0], i1, n) - o.x, r2 = near(b[1], i2, n) - o.y, r3 = near(b[2], i3, n) - o.z;
+                const double* sb = buf[s] + (r1 * e.y + r2) * PITCH + r3;
+                const int rp = e.y * PITCH;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    double acc1 = 0.0;
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const double* p = sb + a * rp + bb * PITCH;
+                        double acc2 = 0.0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc2 += w[2][c] * p[c];
+                        acc1 += w[1][bb] * acc2;
+                    }
+                    acc += w[0][a] * acc1;
+                }
+            } else {
+                acc = gather_l1(f, n, b, w);
+            }
+            out[i] = acc;
+        }
+        __syncthreads();  // everyone is done with buf[s] before it is refilled
+    }
+}
+
+// ---------------------------------------------------------------- driver
+static std::vector<double> readf(const char* p, size_t cnt) {
+    std::vector<double> v(cnt);
+    FILE* fp = fopen(p, "rb");
+    if (!fp || fread(v.data(), 8, cnt, fp) != cnt) {
+        fprintf(stderr, "cannot read %s\n", p);
+        exit(1);
+    }
+    fclose(fp);
+    return v;
+}
+
+template <class L>
+static float time_it(L&& launch, int reps) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    for (int i = 0; i < 3; ++i) launch();
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(a));
+    for (int i = 0; i < reps; ++i) launch();
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms / reps;
+}
+
+static void compare(const char* name, float ms, const std::vector<double>& ref, double* d_out, long long N,
+                    double extra) {
+    std::vector<double> o(N);
+    CK(cudaMemcpy(o.data(), d_out, N * 8, cudaMemcpyDeviceToHost));
+    long long same = 0;
+    double md = 0;
+    for (long long i = 0; i < N; ++i) {
+        if (o[i] == ref[i]) ++same;
+        md = fmax(md, fabs(o[i] - ref[i]));
+    }
+    printf("{\"variant\": \"%s\", \"ms\": %.4f, \"bitwise_equal_frac\": %.6f, \"max_abs_diff\": %.3e, \"extra\": %.4f}\n",
+           name, ms, (double)same / N, md, extra);
+    fflush(stdout);
+}
+
+template <int T1, int T2, int PITCH, int ROWS, int MINB>
+static void run_D(const char* name, const double* d_f, const double* d_X, double* d_out, G g,
+                  const std::vector<double>& ref) {
+    const int ctas_per_sm = MINB;
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int ntiles = (n / T1) * (n / T2) * (n / 32);
+    int4 *org, *ext;
+    CK(cudaMalloc(&org, ntiles * sizeof(int4)));
+    CK(cudaMalloc(&ext, ntiles * sizeof(int4)));
+    auto boxes = [&] { k_boxes<T1, T2><<<ntiles, 256>>>(d_X, g, org, ext, ROWS, PITCH); };
+    float ms_box = time_it(boxes, 5);
+    std::vector<int4> he(ntiles);
+    CK(cudaMemcpy(he.data(), ext, ntiles * sizeof(int4), cudaMemcpyDeviceToHost));
+    int over = 0;
+    double rows = 0, bytes = 0;
+    for (auto& e : he) {
+        if (e.w < 0) ++over;
+        else rows += e.x * e.y, bytes += 8.0 * e.x * e.y * e.z;
+    }
+    const size_t smem = 2ull * ROWS * PITCH * 8;
+    auto kern = k_gather_D<T1, T2, PITCH, ROWS, MINB>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+    const int grid = sms * std::max(1, std::min(occ, ctas_per_sm));
+    auto launch = [&] { kern<<<grid, 256, smem>>>(d_f, d_X, d_out, g, org, ext, ntiles); };
+    CK(cudaMemset(d_out, 0, N * 8));
+    float ms = time_it(launch, 20);
+    CK(cudaGetLastError());
+    char nm[160];
+    snprintf(nm, sizeof nm, "%s T%dx%dx32 pitch%d rows%d occ%d overflow%.3f box_B_per_pt%.1f", name, T1, T2, PITCH,
+             ROWS, occ, (double)over / ntiles, bytes / ((double)(ntiles - over) * T1 * T2 * 32));
+    compare(nm, ms, ref, d_out, N, ms_box);
+    cudaFree(org);
+    cudaFree(ext);
+}
+
+int main(int argc, char** argv) {
+    const int n = argc > 1 ? atoi(argv[1]) : 256;
+    const char* xp = argc > 2 ? argv[2] : "/tmp/lab_X.bin";
+    const char* fp = argc > 3 ? argv[3] : "/tmp/lab_f.bin";
+    const long long N = (long long)n * n * n;
+    auto X = readf(xp, 3 * N);
+    auto F = readf(fp, N);
+    double *d_X, *d_f, *d_out;
+    CK(cudaMalloc(&d_X, 3 * N * 8));
+    CK(cudaMalloc(&d_f, N * 8));
+    CK(cudaMalloc(&d_out, N * 8));
+    CK(cudaMemcpy(d_X, X.data(), 3 * N * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_f, F.data(), N * 8, cudaMemcpyHostToDevice));
+    G g{n, kTwoPi / n};
+    // A
+    auto la = [&] { k_gather_A<<<dim3(n / 32, n / 4, n), 128>>>(d_f, d_X, d_out, g); };
+    float msA = time_it(la, 20);
+    std::vector<double> ref(N);
+    CK(cudaMemcpy(ref.data(), d_out, N * 8, cudaMemcpyDeviceToHost));
+    printf("{\"variant\": \"A l1 1x4x32\", \"ms\": %.4f, \"GBps_alg\": %.1f}\n", msA, 5.0 * 8 * N / (msA * 1e-3) / 1e9);
+    run_D<2, 8, 48, 144, 2>("D bulk", d_f, d_X, d_out, g, ref);
+    run_D<4, 8, 48, 192, 1>("D bulk", d_f, d_X, d_out, g, ref);
+    run_D<1, 8, 48, 96, 3>("D bulk", d_f, d_X, d_out, g, ref);
+    run_D<2, 4, 48, 96, 3>("D bulk", d_f, d_X, d_out, g, ref);
+    run_D<4, 4, 48, 128, 2>("D bulk", d_f, d_X, d_out, g, ref);
+    run_D<2, 8, 64, 144, 2>("D bulk", d_f, d_X, d_out, g, ref);
+    return 0;
+}
