@@ -193,6 +193,7 @@ void flags_after_sync(vr_ctx* ctx) {
 }
 
 vr_state* objective_evaluate(vr_objective* o, const double* v3) {
+    Range nvtx("evaluate");
     vr_ctx* ctx = o->ctx;
     const GridDims& g = ctx->g;
     const long long N = g.N;
@@ -277,6 +278,7 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
 // prepare_adjoint_ctx (objective.cpp:77-84) + the grad m_j cache
 static void prepare_adjoint_ctx(vr_objective* o, vr_state* s) {
     if (s->has_adjoint_ctx) return;
+    Range nvtx("prepare_adjoint_ctx");
     vr_ctx* ctx = o->ctx;
     const long long N = ctx->g.N;
     const int nt = s->nt;
@@ -336,6 +338,7 @@ vr_state* state_from_history(vr_objective* o, const double* v3, const double* mh
 }
 
 void objective_gradient(vr_objective* o, vr_state* s) {
+    Range nvtx("compute_gradient");
     vr_ctx* ctx = o->ctx;
     const long long N = ctx->g.N;
     prepare_adjoint_ctx(o, s);
@@ -378,6 +381,7 @@ void objective_gradient(vr_objective* o, vr_state* s) {
 // hessian_data_matvec (objective.cpp:123-156) [+ beta_v A vt, objective.cpp:114-121]
 void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, double* out3,
                       bool add_reg, const double* reg_given, bool check) {
+    Range nvtx(add_reg || reg_given ? "hessian_matvec" : "hessian_data_matvec");
     vr_ctx* ctx = o->ctx;
     const long long N = ctx->g.N;
     if (!s->has_adjoint_ctx)
@@ -570,6 +574,7 @@ void objective_apply_K(vr_objective* o, const double* u3, double* out3) {
 // ---------------------------------------------------------------------------
 vr_pcg_stats pcg_solve(vr_ctx* ctx, const DevOp& apply, const double* rhs, double rel_tol,
                        int max_iter, const DevOp& precond, double* x) {
+    Range nvtx("pcg_solve");
     const long long n3 = 3 * ctx->g.N;
     vr_pcg_stats st{};
     st.rel_residual = 1.0;
@@ -644,6 +649,7 @@ vr_pcg_stats pcg_solve(vr_ctx* ctx, const DevOp& apply, const double* rhs, doubl
 // The rewrites change rounding only (~1e-15 relative per iteration).
 vr_pcg_stats pcg_solve_gn(vr_objective* o, const vr_state* s, const double* rhs, double rel_tol,
                           int max_iter, double* x) {
+    Range nvtx("pcg_solve_gn");
     vr_ctx* ctx = o->ctx;
     const long long N = ctx->g.N;
     const long long n3 = 3 * N;
@@ -733,6 +739,7 @@ struct LineSearch {
 
 LineSearch armijo_search(vr_objective* o, const vr_state* cur, const double* dir,
                          const vr_solver_params& p) {
+    Range nvtx("armijo_search");
     vr_ctx* ctx = o->ctx;
     const long long n3 = 3 * ctx->g.N;
     if (!cur->has_gradient) throw_logic("armijo_search: current state has no gradient");
@@ -786,6 +793,7 @@ vr_iteration_record make_record(int k, const vr_state* s, double gn, double g0,
 GnResult gauss_newton_solve(vr_ctx* ctx, const double* mR, const double* mT, const double* v0,
                             const vr_model& model, const vr_solver_params& params, int precond,
                             double* v_out, const vr_twolevel_options* tl_opts) {
+    Range nvtx("gauss_newton_solve");
     validate_params(params);
     if (precond != VR_PRECOND_NONE && precond != VR_PRECOND_SPECTRAL &&
         precond != VR_PRECOND_TWO_LEVEL)

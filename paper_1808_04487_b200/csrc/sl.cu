@@ -638,6 +638,7 @@ void sl_tricubic(vr_ctx* ctx, const double* f, int nfields, const double* pts3, 
 
 void sl_trace(vr_ctx* ctx, const double* v3, long long vstride, int nt, int direction,
               double* dep3) {
+    Range nvtx("trace_characteristics");
     if (nt < 1) throw_argument("trace_characteristics: n_t must be >= 1");
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);

@@ -80,6 +80,7 @@ void scalar_multiplier(vr_ctx* ctx, const double* in, double* s, double* out, co
 // r2c: on slabs the result is left in the x1 layout (what the elementwise
 // spectral kernels and fft_c2r expect)
 void fft_r2c(vr_ctx* ctx, const double* in, double* spec) {
+    Range nvtx("fft_r2c");
     if (ctx->dist) {
         double* s = sbuf(ctx, 8);
         pass_rows_forward(ctx, in, s);
@@ -93,6 +94,7 @@ void fft_r2c(vr_ctx* ctx, const double* in, double* spec) {
 }
 
 void fft_c2r(vr_ctx* ctx, double* spec, double* out, double scale, const double* add) {
+    Range nvtx("fft_c2r");
     pass_x1(ctx, spec, spec, +1, nullptr);
     double* s = spec;
     if (ctx->dist) {
@@ -109,6 +111,7 @@ void spectral_scalar_op(vr_ctx* ctx, const double* in, double* out, const MultPa
 }
 
 void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
+    Range nvtx("gradient");
     const GridDims& g = ctx->g;
     if (!ctx->dist && aligned16(f) && aligned16(out3)) {  // d_a f needs only transforms along a
         // (gradient, spectral.cpp:108-122)
@@ -139,6 +142,7 @@ void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
 }
 
 void op_divergence(vr_ctx* ctx, const double* v3, double* out) {
+    Range nvtx("divergence");
     const GridDims& g = ctx->g;
     if (!ctx->dist && aligned16(v3) && aligned16(out)) {  // sum_a d_a v_a with one-axis
         // derivatives (divergence, spectral.cpp:124-140)
@@ -162,6 +166,7 @@ void op_divergence(vr_ctx* ctx, const double* v3, double* out) {
 
 void op_projection(vr_ctx* ctx, const double* in3, double* out3, int kind, double beta_v,
                    double beta_w) {
+    Range nvtx("projection");
     const GridDims& g = ctx->g;
     if (kind == VR_PROJ_IDENTITY) {
         if (in3 != out3)
@@ -197,6 +202,7 @@ double reg_symbol(const vr_regnorm& n, double k2) {
 
 void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm, int mode,
             double beta, const double* add3) {
+    Range nvtx("reg_operator");
     const MultParams mp = reg_mult(norm, mode, beta);
     const long long N = ctx->g.N;
     for (int c = 0; c < 3; ++c)
@@ -205,6 +211,7 @@ void op_reg(vr_ctx* ctx, const double* in3, double* out3, const vr_regnorm& norm
 }
 
 void op_reg_begin(vr_ctx* ctx, const double* in3, const vr_regnorm& norm, int mode, double beta) {
+    Range nvtx("reg_operator_begin");
     const MultParams mp = reg_mult(norm, mode, beta);
     for (int c = 0; c < 3; ++c)
         scalar_multiplier(ctx, in3 + c * ctx->g.N, sbuf(ctx, 4 + c), nullptr, mp, nullptr);
@@ -231,6 +238,7 @@ void op_reg_finish_f32(vr_ctx* ctx, float* out3, const float* add3) {
 }
 
 void op_reg_finish(vr_ctx* ctx, double* out3, const double* add3) {
+    Range nvtx("reg_operator_finish");
     const GridDims& g = ctx->g;
     for (int c = 0; c < 3; ++c)
         pass_rows_inverse(ctx, sbuf(ctx, 4 + c), out3 + c * g.N, inv_n(g),

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -18,6 +19,15 @@
 namespace vr {
 
 constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+// NVTX range per operator / solver phase (visible in nsys / ncu --nvtx timelines; a
+// no-op unless a tool injects the NVTX handler)
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+    Range(const Range&) = delete;
+    Range& operator=(const Range&) = delete;
+};
 
 // ---------------------------------------------------------------------------
 // Errors: mirror veloreg::Error categories (errors.hpp:9-67)

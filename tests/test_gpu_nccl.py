@@ -1,0 +1,80 @@
+"""GPU, >= 2 devices: the x1-slab path over the real NCCL transport (one process per GPU,
+SURVEY 8(e)) against the single-GPU path, which is itself pinned to the reference.
+
+This is the code path a multi-GPU bench run takes (bench.py under torchrun:
+vr_ctx_create_dist, NCCL all-to-all FFT transposes, NCCL halo send/recv, rank-ordered
+reductions). Skipped when fewer than two GPUs are visible; the same protocol is covered on
+one GPU by test_gpu_dist.py (virtual ranks) and on CPU by test_slab_gloo.py.
+"""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _worker(rank, P, uid, dims, arrays, q):
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import paper_1808_04487_b200 as vr
+        mR, mT, v, vt = arrays
+        ctx = vr.DistContext(dims, rank, P, uid, device=rank, halo=8)
+        sl = [ctx.slab(a) for a in (mR, mT, v, vt)]
+        o = vr.Objective(ctx, sl[0], sl[1], vr.make_model())
+        s = o.evaluate(sl[2])
+        o.compute_gradient(s)
+        hv = np.asarray(o.hessian_matvec(s, sl[3]))
+        res = vr.gauss_newton_solve(ctx, sl[0], sl[1], np.zeros_like(sl[2]), vr.make_model(),
+                                    vr.make_params(eps_opt=1e-2))
+        q.put((rank, s.objective, np.asarray(s.gradient), hv, np.asarray(res.v),
+               res.report["outer_iterations"], res.report["final_mismatch_rel"]))
+    except Exception as exc:  # surface the failure in the parent
+        q.put((rank, repr(exc)))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs (the NCCL transport)")
+def test_nccl_slabs_match_single_gpu(vr, ref, ctx):
+    P = 2
+    dims = (32, 32, 32)
+    mR, mT, vs = ref.generate_synthetic(dims, 4)
+    v = 0.8 * vs + 0.05 * ref.random_smooth_vector(dims, 2, 11, 1.0)
+    vt = ref.random_smooth_vector(dims, 2, 142, 1.0)
+    c = ctx(dims)
+    o = vr.Objective(c, mR, mT, vr.make_model())
+    s = o.evaluate(v)
+    o.compute_gradient(s)
+    hv1 = np.asarray(o.hessian_matvec(s, vt))
+    r1 = vr.gauss_newton_solve(c, mR, mT, np.zeros_like(v), vr.make_model(), vr.make_params(eps_opt=1e-2))
+    uid = vr.nccl_unique_id()
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    procs = [mpc.Process(target=_worker, args=(r, P, uid, dims, (mR, mT, v, vt), q)) for r in range(P)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(P)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    for o_ in out:
+        assert len(o_) > 2, o_[1]
+    g = np.concatenate([o_[2] for o_ in out], axis=1)
+    hv = np.concatenate([o_[3] for o_ in out], axis=1)
+    vsol = np.concatenate([o_[4] for o_ in out], axis=1)
+    assert abs(out[0][1] - s.objective) <= 1e-12 * abs(s.objective)
+    assert rel_l2(g, s.gradient) < 1e-12
+    assert rel_l2(hv, hv1) < 1e-12
+    assert out[0][5] == r1.report["outer_iterations"]
+    assert abs(out[0][6] - r1.report["final_mismatch_rel"]) <= 1e-10
+    assert rel_l2(vsol, r1.v) < 1e-10

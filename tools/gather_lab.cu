@@ -121,6 +121,66 @@ __global__ void __launch_bounds__(128, 7) k_gather_A(const double* __restrict__ 
     out[i] = gather_l1(f, n, b, w);
 }
 
+
+// ---------------------------------------------------------------- variant F
+// as A, but each stencil row is fetched with three 16-byte loads from the even-aligned
+// base a = b3 & ~1 ([a, a+6) covers b3..b3+3), the four values picked by the parity of b3
+// (the odd-lane third load is predicated): 3 requests per row instead of 4
+__device__ __forceinline__ double gather_l1_v2(const double* __restrict__ f, int n, const int b[3],
+                                               const double w[3][4]) {
+    const int n23 = n * n;
+    const int b3 = b[2];
+    if (b3 < 0 || b3 + 5 >= n) return gather_l1(f, n, b, w);
+    const int a3 = b3 & ~1;
+    const bool odd = b3 & 1;
+    int o12[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int oa = wrapi(b[0] + a, n) * n23;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) o12[a][bb] = oa + wrapi(b[1] + bb, n) * n + a3;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double acc1 = 0.0;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            const double2* p = reinterpret_cast<const double2*>(f + o12[a][bb]);
+            const double2 v01 = __ldg(p), v23 = __ldg(p + 1);
+            double2 v45 = make_double2(0.0, 0.0);
+            if (odd) v45 = __ldg(p + 2);
+            const double x0 = odd ? v01.y : v01.x, x1 = odd ? v23.x : v01.y;
+            const double x2 = odd ? v23.y : v23.x, x3 = odd ? v45.x : v23.y;
+            double acc2 = 0.0;
+            acc2 += w[2][0] * x0;
+            acc2 += w[2][1] * x1;
+            acc2 += w[2][2] * x2;
+            acc2 += w[2][3] * x3;
+            acc1 += w[1][bb] * acc2;
+        }
+        acc += w[0][a] * acc1;
+    }
+    return acc;
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(128, WARPS / 4) k_gather_F(const double* __restrict__ f, const double* __restrict__ X,
+                                                             double* __restrict__ out, G g) {
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int i3 = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int i2 = blockIdx.y * 4 + (threadIdx.x >> 5);
+    const int i1 = blockIdx.z;
+    const long long i = ((long long)i1 * n + i2) * n + i3;
+    int b[3];
+    double w[3][4];
+    axis_stencil(__ldg(X + i), g.h, b[0], w[0]);
+    axis_stencil(__ldg(X + N + i), g.h, b[1], w[1]);
+    axis_stencil(__ldg(X + 2 * N + i), g.h, b[2], w[2]);
+    out[i] = gather_l1_v2(f, n, b, w);
+}
+
 // ---------------------------------------------------------------- tiles / boxes
 template <int T1, int T2>
 struct TileGeo {
@@ -298,6 +358,111 @@ __global__ void __launch_bounds__(256, MINB) k_gather_D(const double* __restrict
     }
 }
 
+
+// ---------------------------------------------------------------- variant E
+// warp-specialized: one producer warp streams each tile's stencil box AND its departure
+// points into a STAGES-deep ring of shared-memory stages (cp.async.bulk + full/empty
+// mbarriers); CWARPS consumer warps gather from shared memory only
+template <int T1, int T2, int PITCH, int ROWS, int STAGES, int CWARPS, int MINB>
+__global__ void __launch_bounds__(32 * (CWARPS + 1), MINB)
+    k_gather_E(const double* __restrict__ f, const double* __restrict__ X, double* __restrict__ out, G g,
+               const int4* __restrict__ org, const int4* __restrict__ ext, int ntiles) {
+    constexpr int TP = T1 * T2 * 32;                // points per tile
+    constexpr int STAGE = ROWS * PITCH + 3 * TP;    // doubles per stage
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* sm = reinterpret_cast<double*>(smem_raw);
+    __shared__ unsigned long long full[STAGES], empty[STAGES];
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int tiles3 = n / 32, tiles2 = n / T2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CWARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == CWARPS) {  // producer
+        int k = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+            const int s = k % STAGES, u = k / STAGES;
+            if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+            const int4 o = org[t], e = ext[t];
+            const bool staged = e.w > 0;
+            double* box = sm + s * STAGE;
+            double* xs = box + ROWS * PITCH;
+            const unsigned bytes = (staged ? e.x * e.y * e.z * 8 : 0) + 3 * TP * 8;
+            if (lane == 0) mbar_expect(&full[s], bytes);
+            __syncwarp();
+            const int t3 = t % tiles3, t2 = (t / tiles3) % tiles2, t1 = t / (tiles3 * tiles2);
+            for (int q = lane; q < 3 * T1 * T2; q += 32) {  // departure points: 256 B rows
+                const int c = q / (T1 * T2), r = q % (T1 * T2);
+                const int i1 = t1 * T1 + r / T2, i2 = t2 * T2 + r % T2;
+                bulk_g2s(xs + c * TP + r * 32, X + c * N + ((long long)i1 * n + i2) * n + t3 * 32, 256, &full[s]);
+            }
+            if (staged) {
+                const int rows = e.x * e.y;
+                const int s0 = o.z & (n - 1);
+                const int first = min(e.z, n - s0);
+                for (int r = lane; r < rows; r += 32) {
+                    const int a = r / e.y, b = r - a * e.y;
+                    const double* row = f + ((long long)wrapi(o.x + a, n) * n + wrapi(o.y + b, n)) * n;
+                    double* d = box + r * PITCH;
+                    bulk_g2s(d, row + s0, first * 8, &full[s]);
+                    if (first < e.z) bulk_g2s(d + first, row, (e.z - first) * 8, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+    int k = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int s = k % STAGES, u = k / STAGES;
+        const int4 o = org[t], e = ext[t];
+        const bool staged = e.w > 0;
+        mbar_wait(&full[s], u & 1);
+        const double* box = sm + s * STAGE;
+        const double* xs = box + ROWS * PITCH;
+        const int t3 = t % tiles3, t2 = (t / tiles3) % tiles2, t1 = t / (tiles3 * tiles2);
+#pragma unroll 1
+        for (int r = warp; r < T1 * T2; r += CWARPS) {
+            const int i1 = t1 * T1 + r / T2, i2 = t2 * T2 + r % T2, i3 = t3 * 32 + lane;
+            const long long i = ((long long)i1 * n + i2) * n + i3;
+            int b[3];
+            double w[3][4];
+            axis_stencil(xs[r * 32 + lane], g.h, b[0], w[0]);
+            axis_stencil(xs[TP + r * 32 + lane], g.h, b[1], w[1]);
+            axis_stencil(xs[2 * TP + r * 32 + lane], g.h, b[2], w[2]);
+            double acc = 0.0;
+            if (staged) {
+                const int r1 = near(b[0], i1, n) - o.x, r2 = near(b[1], i2, n) - o.y, r3 = near(b[2], i3, n) - o.z;
+                const double* sb = box + (r1 * e.y + r2) * PITCH + r3;
+                const int rp = e.y * PITCH;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    double acc1 = 0.0;
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const double* p = sb + a * rp + bb * PITCH;
+                        double acc2 = 0.0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc2 += w[2][c] * p[c];
+                        acc1 += w[1][bb] * acc2;
+                    }
+                    acc += w[0][a] * acc1;
+                }
+            } else {
+                acc = gather_l1(f, n, b, w);
+            }
+            out[i] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+    }
+}
+
 // ---------------------------------------------------------------- driver
 static std::vector<double> readf(const char* p, size_t cnt) {
     std::vector<double> v(cnt);
@@ -381,6 +546,39 @@ static void run_D(const char* name, const double* d_f, const double* d_X, double
     cudaFree(ext);
 }
 
+
+template <int T1, int T2, int PITCH, int ROWS, int STAGES, int CWARPS, int MINB>
+static void run_E(const double* d_f, const double* d_X, double* d_out, G g, const std::vector<double>& ref) {
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int ntiles = (n / T1) * (n / T2) * (n / 32);
+    int4 *org, *ext;
+    CK(cudaMalloc(&org, ntiles * sizeof(int4)));
+    CK(cudaMalloc(&ext, ntiles * sizeof(int4)));
+    k_boxes<T1, T2><<<ntiles, 256>>>(d_X, g, org, ext, ROWS, PITCH);
+    std::vector<int4> he(ntiles);
+    CK(cudaMemcpy(he.data(), ext, ntiles * sizeof(int4), cudaMemcpyDeviceToHost));
+    int over = 0;
+    for (auto& e : he) over += e.w < 0;
+    const size_t smem = (size_t)STAGES * (ROWS * PITCH + 3 * T1 * T2 * 32) * 8;
+    auto kern = k_gather_E<T1, T2, PITCH, ROWS, STAGES, CWARPS, MINB>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int sms, occ = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * (CWARPS + 1), smem));
+    const int grid = sms * std::max(1, std::min(occ, MINB));
+    auto launch = [&] { kern<<<grid, 32 * (CWARPS + 1), smem>>>(d_f, d_X, d_out, g, org, ext, ntiles); };
+    CK(cudaMemset(d_out, 0, N * 8));
+    float ms = time_it(launch, 20);
+    CK(cudaGetLastError());
+    char nm[160];
+    snprintf(nm, sizeof nm, "E ws T%dx%dx32 pitch%d rows%d stages%d cwarps%d occ%d smemKB%zu overflow%.3f", T1, T2,
+             PITCH, ROWS, STAGES, CWARPS, occ, smem / 1024, (double)over / ntiles);
+    compare(nm, ms, ref, d_out, N, 0.0);
+    cudaFree(org);
+    cudaFree(ext);
+}
+
 int main(int argc, char** argv) {
     const int n = argc > 1 ? atoi(argv[1]) : 256;
     const char* xp = argc > 2 ? argv[2] : "/tmp/lab_X.bin";
@@ -401,11 +599,16 @@ int main(int argc, char** argv) {
     std::vector<double> ref(N);
     CK(cudaMemcpy(ref.data(), d_out, N * 8, cudaMemcpyDeviceToHost));
     printf("{\"variant\": \"A l1 1x4x32\", \"ms\": %.4f, \"GBps_alg\": %.1f}\n", msA, 5.0 * 8 * N / (msA * 1e-3) / 1e9);
-    run_D<2, 8, 48, 144, 2>("D bulk", d_f, d_X, d_out, g, ref);
-    run_D<4, 8, 48, 192, 1>("D bulk", d_f, d_X, d_out, g, ref);
-    run_D<1, 8, 48, 96, 3>("D bulk", d_f, d_X, d_out, g, ref);
-    run_D<2, 4, 48, 96, 3>("D bulk", d_f, d_X, d_out, g, ref);
-    run_D<4, 4, 48, 128, 2>("D bulk", d_f, d_X, d_out, g, ref);
-    run_D<2, 8, 64, 144, 2>("D bulk", d_f, d_X, d_out, g, ref);
+    {
+        auto lf = [&] { k_gather_F<28><<<dim3(n / 32, n / 4, n), 128>>>(d_f, d_X, d_out, g); };
+        CK(cudaMemset(d_out, 0, N * 8));
+        compare("F ldg128x3 28w", time_it(lf, 20), ref, d_out, N, 0);
+        auto lf2 = [&] { k_gather_F<32><<<dim3(n / 32, n / 4, n), 128>>>(d_f, d_X, d_out, g); };
+        CK(cudaMemset(d_out, 0, N * 8));
+        compare("F ldg128x3 32w", time_it(lf2, 20), ref, d_out, N, 0);
+        auto lf3 = [&] { k_gather_F<24><<<dim3(n / 32, n / 4, n), 128>>>(d_f, d_X, d_out, g); };
+        CK(cudaMemset(d_out, 0, N * 8));
+        compare("F ldg128x3 24w", time_it(lf3, 20), ref, d_out, N, 0);
+    }
     return 0;
 }
