@@ -49,8 +49,10 @@ def parse():
     ap.add_argument("--nt", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--ref-budget-s", type=float, default=90.0,
+    ap.add_argument("--ref-budget-s", type=float, default=60.0,
                     help="wall budget for the reference arm's timed matvecs")
+    ap.add_argument("--no-ref-detail", action="store_true",
+                    help="reference arm: skip the FFT split, 1-worker timing and the CPU GN solves")
     ap.add_argument("--no-solve", action="store_true", help="skip the GN solve timings")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-lane gather micro-benchmark")
     ap.add_argument("--no-config2", action="store_true",
@@ -202,6 +204,67 @@ def run_reference_matvecs(m_R, m_T, v, vt, nt, steps, warmup, budget_s):
     total = sum(times)
     return {"value": len(times) / total, "steps": len(times), "seconds": total, "cores": cores,
             "setup_s": setup}
+
+
+def reference_detail(m_T, v, vt, m_R, nt, n, with_solves=True):
+    """BASELINE.md section 3 for the reference CPU arm (same box, same run): the shim-FFT
+    time split at the bench grid, 1-worker vs all-worker matvec at 128^3 (a bounded sample),
+    and the reference's full GN solves at configs 1-3 (config 3: beta continuation)."""
+    from oracle import ref  # the reference only: never maps libveloreg_gpu.so
+    cores = os.cpu_count() or 1
+    out = {"cores": cores}
+    ref.set_workers(cores)
+    t0 = time.perf_counter()
+    spec = ref.fft_forward(m_T)
+    t1 = time.perf_counter()
+    ref.fft_inverse(spec, m_T.shape)
+    t2 = time.perf_counter()
+    out["fft"] = {"grid": n, "r2c_s": t1 - t0, "c2r_s": t2 - t1,
+                  "per_matvec_transforms": 46, "per_matvec_fft_s_estimate": 23 * ((t1 - t0) + (t2 - t1)),
+                  "note": "oracle FFT = the from-scratch FFTW3-API shim (radix-2, long-double twiddles), "
+                          "single-threaded as the reference's plan cache is (fft.cpp:56-83)"}
+    del spec
+    # 1 worker vs all workers on the 128^3 config-2 problem (one matvec each)
+    n2 = 128
+    mR2, mT2, vs2 = ref.generate_synthetic((n2, n2, n2), nt)
+    model = ref.make_model("h2", beta_v=1e-2, nt=nt)
+    vt2 = ref.random_smooth_vector((n2, n2, n2), 2, 142, 1.0)
+    res = {}
+    for w in (cores, 1):
+        ref.set_workers(w)
+        obj = ref.Objective(mR2, mT2, model)
+        st = obj.evaluate(vs2)
+        obj.compute_gradient(st)
+        t0 = time.perf_counter()
+        obj.hessian_matvec(st, vt2)
+        res[w] = time.perf_counter() - t0
+    ref.set_workers(cores)
+    out["matvec_128"] = {"workers_all_s": res[cores], "workers_1_s": res[1], "speedup": res[1] / res[cores]}
+    if with_solves:
+        solves = {}
+        for name, (a, b) in (("config1_64", ref.generate_synthetic((64,) * 3, nt)[:2]),
+                             ("config2_128", (mR2, mT2))):
+            p = _ref_params(ref)
+            t0 = time.perf_counter()
+            _, rep, _ = ref.gauss_newton_solve(a, b, np.zeros((3,) + a.shape), model, p)
+            solves[name] = {"seconds": time.perf_counter() - t0, "newton_iterations": rep["outer_iterations"],
+                            "final_mismatch_rel": rep["final_mismatch_rel"]}
+        p = _ref_params(ref)
+        t0 = time.perf_counter()
+        _, reps, _ = ref.parameter_continuation(m_R, m_T, np.zeros_like(v), model, p)
+        solves[f"config3_{n}_beta_continuation"] = {
+            "seconds": time.perf_counter() - t0, "newton_iterations": [r["outer_iterations"] for r in reps],
+            "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"]}
+        out["gn_solves"] = solves
+    return out
+
+
+def _ref_params(ref):
+    """SolverParams (solver.hpp:13-33) with the configs' eps_opt = 1e-2."""
+    p = ref.SolverParams()
+    p.eps_opt, p.abs_grad_tol, p.max_newton, p.max_krylov = 1e-2, 1e-6, 50, 100
+    p.armijo_c1, p.armijo_backtrack, p.armijo_max_trials, p.squared_norm_stop = 1e-4, 0.5, 20, 1
+    return p
 
 
 def fp32_block(ctx, V, d_v, d_mT, nt, dev, torch):
@@ -415,9 +478,12 @@ def main():
         from oracle import ref  # the reference only: never maps libveloreg_gpu.so
         ref.set_workers(os.cpu_count() or 1)
         m_R = ref.solve_state(m_T, v, nt)[-1]
-        r = run_reference_matvecs(m_R, m_T, v, vt, nt, args.steps, min(args.warmup, 1), args.ref_budget_s)
-        sample = (f"{r['steps']} GN Hessian matvec(s) at {n}^3 after 1 untimed warm-up matvec and an "
-                  f"untimed evaluate+gradient ({r['setup_s']:.1f}s); capped at {args.ref_budget_s:.0f}s")
+        r = run_reference_matvecs(m_R, m_T, v, vt, nt, args.steps, 0, args.ref_budget_s)
+        sample = (f"{r['steps']} GN Hessian matvec(s) at {n}^3 after an untimed evaluate+gradient "
+                  f"({r['setup_s']:.1f}s); capped at {args.ref_budget_s:.0f}s")
+        detail = None
+        if not args.no_ref_detail:
+            detail = reference_detail(m_T, v, vt, m_R, nt, n, with_solves=(world == 1))
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": r["steps"],
                 "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * r["seconds"] / r["steps"],
                 "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
@@ -425,7 +491,8 @@ def main():
                 "config": bench_config(cid, n, nt, world),
                 "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
                                  "sample": sample},
-                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "reference_detail": detail}
         print(json.dumps(line), flush=True)
         return 0
 

@@ -192,6 +192,12 @@ void* vr_ctx_stream(vr_ctx* ctx); /* cudaStream_t */
 int vr_ctx_grid(const vr_ctx* ctx, int dims[3]);
 /* kernels launched on this ctx since creation / last reset (evidence counter) */
 long long vr_ctx_kernel_launches(const vr_ctx* ctx);
+/* device-memory accounting of this context's library allocations (the reference's
+ * FieldAllocStats live / peak, proj/include/veloreg/field.hpp:16-33, in bytes), and the
+ * device's stream-ordered pool high-water mark (may be NULL) */
+int vr_ctx_memory(const vr_ctx* ctx, long long* live_bytes, long long* peak_bytes,
+                  long long* pool_reserved_high);
+int vr_ctx_reset_memory_peak(vr_ctx* ctx); /* FieldAllocStats::reset_peak */
 void vr_ctx_reset_kernel_launches(vr_ctx* ctx);
 
 /* Optional per-launch CUDA-event timing on the ctx stream (bench / roofline
@@ -369,6 +375,10 @@ int vr_objective_apply_K(vr_objective* obj, const double* u3, double* out3);
 
 /* ---- solvers (solver.hpp:78-164; host driver over the device operators) ---- */
 int vr_compute_forcing(double grad_norm, double grad0_norm, double* out); /* solver.cpp:23-27 */
+/* SolveReport::write_csv (solver.cpp:29-47): the reference's CSV of a report and its
+ * records into buf (NUL-terminated; *needed = bytes required, may be NULL; buf NULL to size) */
+int vr_solve_report_csv(const vr_solve_report* report, const vr_iteration_record* records,
+                        const char* comment, char* buf, size_t len, size_t* needed);
 /* pcg_solve on the GN Hessian of (obj, s) with the chosen preconditioner (solver.cpp:51-100) */
 int vr_pcg_solve(vr_objective* obj, const vr_state* s, const double* rhs3, double rel_tol,
                  int max_iter, int precond, double* x3, vr_pcg_stats* stats);

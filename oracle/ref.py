@@ -79,6 +79,7 @@ _SIG = {
     "vref_objective_apply_reg": (I, [P, P, I, P]),
     "vref_objective_apply_K": (I, [P, P, P]),
     "vref_pcg_solve": (I, [P, P, P, D, I, I, P, C.POINTER(PcgStats)]),
+    "vref_gauss_newton_solve_csv": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), C.c_char_p, I]),
     "vref_gauss_newton_solve": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I, P,
                                     C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
     "vref_parameter_continuation": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I,
@@ -491,6 +492,15 @@ def gauss_newton_solve(m_R, m_T, v0, model, params, precond=1, max_records=512):
           C.byref(model), C.byref(params), precond, vout.ctypes.data, C.byref(rep), recs, max_records)
     n = min(rep.n_records, max_records)
     return vout, _report(rep), [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
+
+
+def gauss_newton_solve_csv(m_R, m_T, v0, model, params):
+    """The reference's SolveReport::write_csv (solver.cpp:29-47) of a spectral-precond solve."""
+    r, t, v0 = _a(m_R), _a(m_T), _a(v0)
+    buf = C.create_string_buffer(1 << 16)
+    _call("vref_gauss_newton_solve_csv", _dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data,
+          C.byref(model), C.byref(params), buf, len(buf))
+    return buf.value.decode()
 
 
 def parameter_continuation(m_R, m_T, v0, model, params, precond=1, max_levels=16, max_records=1024):

@@ -12,6 +12,7 @@
 
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -668,6 +669,22 @@ int vref_parameter_continuation_f32(const int* d, const float* mR, const float* 
             if (res.report.stop == StopReason::line_search_failure) break;
         }
         store_f(v, v_out);
+    });
+}
+
+// gauss_newton_solve + the reference's SolveReport::write_csv (solver.cpp:29-47) into buf
+int vref_gauss_newton_solve_csv(const int* d, const double* mR, const double* mT, const double* v0,
+                                const vr_model* m, const vr_solver_params* p, char* buf, int len) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto R = load_scalar(g, mR), T = load_scalar(g, mT);
+        SpectralPreconditioner<double> spec;
+        auto res = gauss_newton_solve(R, T, load_vector(g, v0), to_model(*m), to_params(*p), spec);
+        std::ostringstream os;
+        res.report.write_csv(os, {"reference"});
+        const std::string out = os.str();
+        if (static_cast<int>(out.size()) + 1 > len) throw ArgumentError("csv buffer too small");
+        std::memcpy(buf, out.c_str(), out.size() + 1);
     });
 }
 

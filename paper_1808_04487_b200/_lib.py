@@ -37,6 +37,8 @@ SIGNATURES = {
     "vr_ctx_grid": (I, [P, C.POINTER(C.c_int)]),
     "vr_ctx_kernel_launches": (C.c_longlong, [P]),
     "vr_ctx_reset_kernel_launches": (None, [P]),
+    "vr_ctx_memory": (I, [P, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "vr_ctx_reset_memory_peak": (I, [P]),
     "vr_ctx_set_profiling": (I, [P, I]),
     "vr_ctx_profile_read": (I, [P, C.c_char_p, C.c_size_t]),
     "vr_device_alloc": (I, [P, C.c_size_t, C.POINTER(P)]),
@@ -117,6 +119,8 @@ SIGNATURES = {
     "vr_objective_apply_reg": (I, [P, DP, I, DP]),
     "vr_objective_apply_K": (I, [P, DP, DP]),
     "vr_compute_forcing": (I, [D, D, C.POINTER(D)]),
+    "vr_solve_report_csv": (I, [C.POINTER(SolveReport), C.POINTER(IterationRecord), C.c_char_p, C.c_char_p,
+                                C.c_size_t, C.POINTER(C.c_size_t)]),
     "vr_pcg_solve": (I, [P, P, DP, D, I, I, DP, C.POINTER(PcgStats)]),
     "vr_gauss_newton_solve": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I,
                                   DP, C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),

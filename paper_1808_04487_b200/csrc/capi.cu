@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 #include "objective.cuh"
@@ -68,6 +69,7 @@ double* spec_buf(vr_ctx* ctx, int i) {
     if (!ctx->spec_scratch[i]) {
         void* p = nullptr;
         VR_CUDA(cudaMalloc(&p, sizeof(double) * 2 * ctx->g.NC));
+        mem_track_alloc(ctx, p, static_cast<long long>(sizeof(double)) * 2 * ctx->g.NC);
         ctx->spec_scratch[i] = static_cast<double*>(p);
     }
     return ctx->spec_scratch[i];
@@ -86,6 +88,7 @@ double* field_buf(vr_ctx* ctx, int i) {
     if (!ctx->field_scratch[i]) {
         void* p = nullptr;
         VR_CUDA(cudaMalloc(&p, sizeof(double) * ctx->g.N));
+        mem_track_alloc(ctx, p, static_cast<long long>(sizeof(double)) * ctx->g.N);
         ctx->field_scratch[i] = static_cast<double*>(p);
     }
     return ctx->field_scratch[i];
@@ -389,13 +392,36 @@ int vr_device_alloc(vr_ctx* ctx, size_t bytes, void** out) {
         set_dev(ctx);
         need(out, "out");
         VR_CUDA(cudaMalloc(out, bytes));
+        vr::mem_track_alloc(ctx, *out, static_cast<long long>(bytes));
     });
 }
 int vr_device_free(vr_ctx* ctx, void* p) {
     return guard([&] {
         set_dev(ctx);
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        vr::mem_track_free(ctx, p);
         VR_CUDA(cudaFree(p));
+    });
+}
+int vr_ctx_memory(const vr_ctx* ctx, long long* live_bytes, long long* peak_bytes,
+                  long long* pool_reserved_high) {
+    return guard([&] {
+        need(ctx != nullptr, "vr_ctx_memory");
+        if (live_bytes) *live_bytes = ctx->mem_live;
+        if (peak_bytes) *peak_bytes = ctx->mem_peak;
+        if (pool_reserved_high) {
+            cudaMemPool_t pool;
+            unsigned long long v = 0;
+            VR_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+            VR_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &v));
+            *pool_reserved_high = static_cast<long long>(v);
+        }
+    });
+}
+int vr_ctx_reset_memory_peak(vr_ctx* ctx) {
+    return guard([&] {
+        need(ctx != nullptr, "vr_ctx_reset_memory_peak");
+        ctx->mem_peak = ctx->mem_live;
     });
 }
 int vr_host_alloc_pinned(size_t bytes, void** out) {
@@ -1104,6 +1130,35 @@ int vr_objective_apply_K(vr_objective* obj, const double* u3, double* out3) {
 }
 
 // ---- solvers ----------------------------------------------------------------------
+// SolveReport::write_csv (solver.cpp:29-47): optional "# comment" line, the header, one
+// row per IterationRecord, precision 17 -- so GPU and CPU reports diff column by column
+int vr_solve_report_csv(const vr_solve_report* report, const vr_iteration_record* records,
+                        const char* comment, char* buf, size_t len, size_t* needed) {
+    return guard([&] {
+        need(report != nullptr && (records != nullptr || report->n_records == 0), "vr_solve_report_csv");
+        std::ostringstream os;
+        if (comment) os << "# " << comment << "\n";
+        os << "iter,objective,mismatch_rel,grad_norm,grad_rel,step_length,forcing,"
+              "inner_iterations,fine_matvecs,coarse_matvecs,pde_solves,wall_time_s\n";
+        std::ostringstream row;
+        row.precision(17);
+        for (int i = 0; i < report->n_records; ++i) {
+            const vr_iteration_record& r = records[i];
+            row.str("");
+            row << r.k << ',' << r.objective << ',' << r.mismatch_rel << ',' << r.grad_norm << ','
+                << r.grad_rel << ',' << r.step_length << ',' << r.forcing << ',' << r.inner_iterations
+                << ',' << r.fine_matvecs << ',' << r.coarse_matvecs << ',' << r.pde_solves << ','
+                << r.wall_time_s;
+            os << row.str() << "\n";
+        }
+        const std::string out = os.str();
+        if (needed) *needed = out.size() + 1;
+        if (buf && len > 0) {
+            if (out.size() + 1 > len) vr::throw_argument("vr_solve_report_csv: buffer too small");
+            std::memcpy(buf, out.c_str(), out.size() + 1);
+        }
+    });
+}
 int vr_compute_forcing(double grad_norm, double grad0_norm, double* out) {
     return guard([&] {
         if (grad0_norm <= 0.0)

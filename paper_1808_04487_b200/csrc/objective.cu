@@ -50,10 +50,13 @@ double* dev_alloc(vr_ctx* ctx, long long n) {
         throw_resource("device allocation of " + std::to_string(sizeof(double) * n) +
                        " bytes failed: " + cudaGetErrorString(e));
     }
+    mem_track_alloc(ctx, p, static_cast<long long>(sizeof(double)) * n);
     return static_cast<double*>(p);
 }
 void dev_free(vr_ctx* ctx, double* p) {
-    if (p) cudaFreeAsync(p, ctx->stream);
+    if (!p) return;
+    mem_track_free(ctx, p);
+    cudaFreeAsync(p, ctx->stream);
 }
 
 void validate_model(const vr_model& m) {

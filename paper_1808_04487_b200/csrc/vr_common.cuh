@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "veloreg_gpu.h"
@@ -142,6 +143,10 @@ struct vr_ctx {
     // read back by the next host synchronisation (a reduction) instead of its own sync
     const char* flags_pending = nullptr;
     long long launches = 0;
+    // device-memory accounting (FieldAllocStats analogue, field.hpp:16-33): bytes live in
+    // allocations made by the library for this context, and their peak since the last reset
+    long long mem_live = 0, mem_peak = 0;
+    std::unordered_map<const void*, long long> mem_sizes;
     // optional per-launch CUDA-event timing (bench / roofline evidence)
     bool profiling = false;
     // side-stream overlap of independent spectral work (VR_OVERLAP=1 enables).
@@ -184,6 +189,18 @@ void set_last_error(int cls, const std::string& msg);  // the C ABI's vr_last_er
 double* spec_buf(vr_ctx* ctx, int i);   // NC complex (2*NC doubles)
 double* field_buf(vr_ctx* ctx, int i);  // N doubles
 inline void count_launch(vr_ctx* ctx, int n = 1) { ctx->launches += n; }
+inline void mem_track_alloc(vr_ctx* ctx, const void* p, long long bytes) {
+    if (!p) return;
+    ctx->mem_sizes[p] = bytes;
+    ctx->mem_live += bytes;
+    if (ctx->mem_live > ctx->mem_peak) ctx->mem_peak = ctx->mem_live;
+}
+inline void mem_track_free(vr_ctx* ctx, const void* p) {
+    auto it = ctx->mem_sizes.find(p);
+    if (it == ctx->mem_sizes.end()) return;
+    ctx->mem_live -= it->second;
+    ctx->mem_sizes.erase(it);
+}
 inline void check_launch() { VR_CUDA(cudaGetLastError()); }
 cudaEvent_t prof_event(vr_ctx* ctx);
 // the context that owns the profile (a sibling shares its parent's stream)

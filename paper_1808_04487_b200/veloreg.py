@@ -115,6 +115,16 @@ class Context:
         except Exception:
             pass
 
+    def memory(self) -> dict:
+        """Library device allocations of this context (vr_ctx_memory): live and peak bytes
+        (the reference's FieldAllocStats), plus the device pool's reserved high-water mark."""
+        a, b, c = C.c_longlong(), C.c_longlong(), C.c_longlong()
+        _lib.call("vr_ctx_memory", self._h, C.byref(a), C.byref(b), C.byref(c))
+        return {"live_bytes": a.value, "peak_bytes": b.value, "pool_reserved_high_bytes": c.value}
+
+    def reset_memory_peak(self):
+        _lib.call("vr_ctx_reset_memory_peak", self._h)
+
     # ---- device arrays
     def empty(self, nfields: int, complex_spectrum: bool = False) -> "DeviceArray":
         return DeviceArray(self, nfields, complex_spectrum)
@@ -571,6 +581,17 @@ class SolveResult:
     v: np.ndarray
     report: dict
     records: List[dict] = field(default_factory=list)
+    csv: str = ""  # SolveReport::write_csv (solver.cpp:29-47) of this solve
+
+
+def solve_report_csv(rep, recs, comment: Optional[str] = None) -> str:
+    """The reference's SolveReport CSV (vr_solve_report_csv) of a raw report / records."""
+    need = C.c_size_t()
+    cm = comment.encode() if comment is not None else None
+    _lib.call("vr_solve_report_csv", C.byref(rep), recs, cm, None, 0, C.byref(need))
+    buf = C.create_string_buffer(need.value)
+    _lib.call("vr_solve_report_csv", C.byref(rep), recs, cm, buf, need.value, None)
+    return buf.value.decode()
 
 
 def _report_dict(r: _lib.SolveReport) -> dict:
@@ -611,7 +632,7 @@ def gauss_newton_solve(ctx, m_R, m_T, v0, model=None, params=None, precond="spec
         _lib.call("vr_gauss_newton_solve", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
                   C.byref(params), pc, vout.ptr, C.byref(rep), recs, max_records)
     return SolveResult(_ret(vout, _is_host(m_R, m_T, v0)), _report_dict(rep),
-                       _records(recs, min(rep.n_records, max_records)))
+                       _records(recs, min(rep.n_records, max_records)), solve_report_csv(rep, recs, "gpu"))
 
 
 # ---- two-level preconditioner and grid transfer (precond.hpp, spectral.cpp:228-385) ----

@@ -52,7 +52,7 @@ def test_reference_arm_never_maps_the_product_library():
     from oracle import ref
     if not ref.available():
         pytest.skip("oracle/_ref not built")
-    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--n','16','--steps','1',"
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--n','16','--steps','1','--no-ref-detail',"
             "'--warmup','0'];\ntry:\n runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit:\n pass\n"
             "maps=open('/proc/self/maps').read(); print('MAPS', 'libveloreg_gpu' in maps, 'libveloreg_ref' in maps)")
     out = subprocess.run([sys.executable, "-c", code], cwd=bench.ROOT, capture_output=True, text=True,

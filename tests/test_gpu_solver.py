@@ -93,3 +93,31 @@ def test_parameter_continuation(vr, ref, ctx):
     assert len(reps_g) == len(reps_r) == 3
     for a, b in zip(reps_g, reps_r):
         _compare(a, b)
+
+
+def test_solve_report_csv_matches_reference(vr, ref, ctx):
+    """SolveReport::write_csv (solver.cpp:29-47): the GPU solve's CSV has the reference's
+    header and one row per iteration with the same integer columns (iter, inner iterations,
+    cumulative matvecs / PDE solves) and the same floats to 1e-8 relative; wall time is the
+    only column that differs by construction."""
+    dims = (16, 16, 16)
+    c = ctx(dims)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model("h2", beta_v=1e-2, nt=4), vr.make_params(eps_opt=1e-2)
+    v0 = np.zeros((3,) + dims)
+    res = vr.gauss_newton_solve(c, mR, mT, v0, model, params)
+    cpu = ref.gauss_newton_solve_csv(mR, mT, v0, model, params)
+    g_lines, r_lines = res.csv.strip().splitlines(), cpu.strip().splitlines()
+    assert g_lines[0] == "# gpu" and r_lines[0] == "# reference"
+    assert g_lines[1] == r_lines[1]  # header
+    assert len(g_lines) == len(r_lines)
+    cols = r_lines[1].split(",")
+    for gl, rl in zip(g_lines[2:], r_lines[2:]):
+        for name, a, b in zip(cols, gl.split(","), rl.split(",")):
+            if name == "wall_time_s":
+                continue
+            if name in ("iter", "inner_iterations", "fine_matvecs", "coarse_matvecs", "pde_solves"):
+                assert a == b, (name, a, b)
+            else:
+                fa, fb = float(a), float(b)
+                assert abs(fa - fb) <= 1e-8 * max(abs(fb), 1e-300), (name, fa, fb)
