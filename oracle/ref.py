@@ -79,7 +79,8 @@ _SIG = {
     "vref_objective_apply_reg": (I, [P, P, I, P]),
     "vref_objective_apply_K": (I, [P, P, P]),
     "vref_pcg_solve": (I, [P, P, P, D, I, I, P, C.POINTER(PcgStats)]),
-    "vref_gauss_newton_solve_csv": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), C.c_char_p, I]),
+    "vref_gauss_newton_solve_csv": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams),
+                                        C.POINTER(C.c_char), I]),
     "vref_gauss_newton_solve": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I, P,
                                     C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
     "vref_parameter_continuation": (I, [DIMS, P, P, P, C.POINTER(Model), C.POINTER(SolverParams), I,

@@ -681,7 +681,8 @@ int vref_gauss_newton_solve_csv(const int* d, const double* mR, const double* mT
         SpectralPreconditioner<double> spec;
         auto res = gauss_newton_solve(R, T, load_vector(g, v0), to_model(*m), to_params(*p), spec);
         std::ostringstream os;
-        res.report.write_csv(os, {"reference"});
+        const std::vector<std::string> comments{"reference"};
+        res.report.write_csv(os, comments);
         const std::string out = os.str();
         if (static_cast<int>(out.size()) + 1 > len) throw ArgumentError("csv buffer too small");
         std::memcpy(buf, out.c_str(), out.size() + 1);

@@ -119,8 +119,8 @@ SIGNATURES = {
     "vr_objective_apply_reg": (I, [P, DP, I, DP]),
     "vr_objective_apply_K": (I, [P, DP, DP]),
     "vr_compute_forcing": (I, [D, D, C.POINTER(D)]),
-    "vr_solve_report_csv": (I, [C.POINTER(SolveReport), C.POINTER(IterationRecord), C.c_char_p, C.c_char_p,
-                                C.c_size_t, C.POINTER(C.c_size_t)]),
+    "vr_solve_report_csv": (I, [C.POINTER(SolveReport), C.POINTER(IterationRecord), C.c_char_p,
+                                C.POINTER(C.c_char), C.c_size_t, C.POINTER(C.c_size_t)]),
     "vr_pcg_solve": (I, [P, P, DP, D, I, I, DP, C.POINTER(PcgStats)]),
     "vr_gauss_newton_solve": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I,
                                   DP, C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
