@@ -240,6 +240,14 @@ __device__ __forceinline__ double2 mult_at(const MultDev& m, const GridDims& g, 
     return make_double2(v, 0.0);
 }
 
+// beta * A^{1,-1,-1/2} at |k|^2 = k2 (the Mult::reg branch of mult_at, same arithmetic)
+__device__ __forceinline__ double reg_mult_k2(const MultDev& m, double k2) {
+    const double s = symbol_dev(m, k2);
+    if (m.reg_mode == VR_REGOP_APPLY) return m.beta * s;
+    if (m.reg_mode == VR_REGOP_INVERSE) return 1.0 / (m.beta * (s == 0.0 ? 1.0 : s));
+    return 1.0 / sqrt(m.beta * (s == 0.0 ? 1.0 : s));
+}
+
 __device__ __forceinline__ double2 apply_mult(double2 m, double2 c) {
     // real multipliers: c * m.x (exactly like complex<double> *= double);
     // imaginary (derivative) multipliers: (0, k) * c
@@ -286,6 +294,8 @@ struct AxisCfg {
 // one is transformed; the last butterfly stage stores straight to HBM).
 // MODE 0: transform in direction DIR (src may equal dst)
 // MODE 1: forward -> multiplier -> inverse (x1 pass only), src -> dst (may alias)
+// MODE 3: as MODE 1 for the regularisation multiplier (Mult::reg), applied in the last
+//         forward butterfly stage's stores (no separate multiplier sweep over shared memory)
 // MODE 2: forward -> i deriv_freq(k) * m.beta -> inverse along this axis: the spectral
 //         derivative of a REAL field viewed as complex pairs (x3 = 2j, 2j+1 as re, im);
 //         i k (Nyquist 0) maps real lines to real lines, so the pair never mixes
@@ -341,6 +351,20 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
                 const double2 c = cmul(make_double2(0.0, (double)deriv_freq(i, N)), sm(i));
                 sm(i) = make_double2(c.x * m.beta, c.y * m.beta);
             }
+            __syncthreads();
+            fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
+        } else if constexpr (MODE == 3) {
+            // x1 pass: column cc = i2 * nh + i3; |k|^2 = fft_freq(i1)^2 + kk23 (integers: exact)
+            const int i2 = static_cast<int>(cc / g.nh) + g.k2_off;
+            const int i3 = static_cast<int>(cc % g.nh);
+            const double b2 = fft_freq(i2, g.n2), b3 = fft_freq(i3, g.n3);
+            const double kk23 = b2 * b2 + b3 * b3;
+            auto store_mult = [&](int i, double2 v) {
+                const double a = fft_freq(i, N);
+                const double mk = reg_mult_k2(m, a * a + kk23);
+                sm(i) = make_double2(v.x * mk, v.y * mk);
+            };
+            fft_line<N, -1, true, true>(t, tw, load_sm, store_mult, sm);
             __syncthreads();
             fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
         } else {
@@ -711,7 +735,7 @@ void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inne
     const long long ntiles = (inner + C::TB - 1) / C::TB * outer;
     const unsigned grid =
         persistent_grid(ctx, k_fft_axis<N, DIR, MODE>, C::THREADS, C::SMEM, ntiles, occ);
-    VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : (MODE == 1 ? "fft_x1_mult" : "fft_deriv"),
+    VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : (MODE == 1 || MODE == 3 ? "fft_x1_mult" : "fft_deriv"),
               k_fft_axis<N, DIR, MODE><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
                   src, dst, inner, outer, outer_stride, tw, m, ctx->g));
 }
@@ -893,7 +917,9 @@ void pass_x1(vr_ctx* ctx, const double* src, double* dst, int dir, const MultPar
     auto* d = reinterpret_cast<double2*>(dst);
     const long long inner = (long long)g.n2s * g.nh;
     MultDev none{};
-    if (mult)
+    if (mult && mult->kind == Mult::reg)
+        launch_axis<-1, 3>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, to_dev(*mult));
+    else if (mult)
         launch_axis<-1, 1>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, to_dev(*mult));
     else if (dir < 0)
         launch_axis<-1, 0>(ctx, g.n1, s, d, inner, 1, 0, ctx->fft->tw1, none);
