@@ -201,6 +201,8 @@ void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& 
     g.nh = n3 / 2 + 1;
     g.dist = P > 1;
     g.L = n1 / P;
+    g.z0 = 0;
+    g.zn = g.L;
     g.off1 = rank * g.L;
     g.halo = P > 1 ? halo : 0;
     g.n2s = n2 / P;
@@ -242,9 +244,10 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
     try {
         ctx->device = device;
         VR_CUDA(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+        ctx->dist = P > 1 ? t : nullptr;
+        ctx->overlap = ctx->dist != nullptr;  // slabs: reg-term transposes under the sweeps
         if (const char* e = std::getenv("VR_OVERLAP")) ctx->overlap = std::atoi(e) != 0;
         if (const char* e = std::getenv("VR_FUSE_ACC")) ctx->fuse_acc = std::atoi(e) != 0;
-        ctx->dist = P > 1 ? t : nullptr;
         GridDims& g = ctx->g;
         g = geo;
         ctx->hstride = static_cast<long long>(g.L + 2 * g.halo) * n2 * n3;
@@ -252,6 +255,8 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
         VR_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+        VR_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo_fork, cudaEventDisableTiming));
         // keep freed blocks cached in the stream-ordered pool (no OS round trips)
         cudaMemPool_t pool;
         VR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -317,6 +322,8 @@ int vr_ctx_destroy(vr_ctx* ctx) {
         if (ctx->side) cudaStreamSynchronize(ctx->side);
         if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
         if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+        if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+        if (ctx->ev_halo_fork) cudaEventDestroy(ctx->ev_halo_fork);
         if (ctx->side) cudaStreamDestroy(ctx->side);
         if (ctx->stream && ctx->owns_stream) cudaStreamDestroy(ctx->stream);
         if (ctx->owns_dist) delete ctx->dist;

@@ -35,6 +35,7 @@ struct NcclApi {
     ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
     ncclResult_t (*groupStart)() = nullptr;
     ncclResult_t (*groupEnd)() = nullptr;
     ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -54,6 +55,7 @@ NcclApi& nccl() {
         api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
         api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(api.h, "ncclCommInitRank"));
         api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+        api.commSplit = reinterpret_cast<decltype(api.commSplit)>(dlsym(api.h, "ncclCommSplit"));
         api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(api.h, "ncclGroupStart"));
         api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(api.h, "ncclGroupEnd"));
         api.send = reinterpret_cast<decltype(api.send)>(dlsym(api.h, "ncclSend"));
@@ -74,6 +76,11 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 struct NcclTransport final : Transport {
     ncclComm_t comm = nullptr;
+    // a second communicator for the exchanges issued on the context's side stream (the
+    // beta_v A vt transposes running under the sweeps): two concurrent NCCL operations
+    // must not share a communicator. Null when ncclCommSplit is unavailable (then the
+    // side-stream work stays on the main stream)
+    ncclComm_t comm_side = nullptr;
     double* buf = nullptr;  // device: 8 doubles in, size*8 gathered
 
     NcclTransport(int r, int p, const unsigned char uid[NCCL_UNIQUE_ID_BYTES]) {
@@ -82,11 +89,17 @@ struct NcclTransport final : Transport {
         ncclUniqueId id;
         std::memcpy(id.internal, uid, NCCL_UNIQUE_ID_BYTES);
         nccl_check(nccl().commInitRank(&comm, p, id, r), "commInitRank");
+        if (nccl().commSplit) nccl_check(nccl().commSplit(comm, 0, r, &comm_side, nullptr), "commSplit");
         VR_CUDA(cudaMalloc(&buf, sizeof(double) * 8 * (p + 1)));
     }
     ~NcclTransport() override {
         if (buf) cudaFree(buf);
+        if (comm_side) nccl().commDestroy(comm_side);
         if (comm) nccl().commDestroy(comm);
+    }
+    bool side_stream_ok() const override { return comm_side != nullptr; }
+    ncclComm_t comm_of(const vr_ctx* ctx) const {
+        return (comm_side && ctx->stream == ctx->side) ? comm_side : comm;
     }
     // exchange time as a profile category (library kernels: not counted as our launches);
     // the exchanges run on the context stream, so their time is also the exposed time
@@ -99,25 +112,27 @@ struct NcclTransport final : Transport {
     }
     void alltoall(vr_ctx* ctx, const double* send, double* recv, size_t count) override {
         auto& api = nccl();
+        ncclComm_t cm = comm_of(ctx);
         cudaEvent_t ev = prof_begin(ctx);
         nccl_check(api.groupStart(), "groupStart");
         for (int q = 0; q < size; ++q) {
-            nccl_check(api.send(send + q * count, count, ncclDouble, q, comm, ctx->stream), "send");
-            nccl_check(api.recv(recv + q * count, count, ncclDouble, q, comm, ctx->stream), "recv");
+            nccl_check(api.send(send + q * count, count, ncclDouble, q, cm, ctx->stream), "send");
+            nccl_check(api.recv(recv + q * count, count, ncclDouble, q, cm, ctx->stream), "recv");
         }
         nccl_check(api.groupEnd(), "groupEnd");
         comm_end(ctx, "comm_alltoall", ev);
     }
     void halo(vr_ctx* ctx, double* interior, size_t plane, int L, int H) override {
         auto& api = nccl();
+        ncclComm_t cm = comm_of(ctx);
         const int prev = (rank + size - 1) % size, next = (rank + 1) % size;
         const size_t n = static_cast<size_t>(H) * plane;
         cudaEvent_t ev = prof_begin(ctx);
         nccl_check(api.groupStart(), "groupStart");
-        nccl_check(api.send(interior, n, ncclDouble, prev, comm, ctx->stream), "send");
-        nccl_check(api.recv(interior + L * plane, n, ncclDouble, next, comm, ctx->stream), "recv");
-        nccl_check(api.send(interior + (L - H) * plane, n, ncclDouble, next, comm, ctx->stream), "send");
-        nccl_check(api.recv(interior - n, n, ncclDouble, prev, comm, ctx->stream), "recv");
+        nccl_check(api.send(interior, n, ncclDouble, prev, cm, ctx->stream), "send");
+        nccl_check(api.recv(interior + L * plane, n, ncclDouble, next, cm, ctx->stream), "recv");
+        nccl_check(api.send(interior + (L - H) * plane, n, ncclDouble, next, cm, ctx->stream), "send");
+        nccl_check(api.recv(interior - n, n, ncclDouble, prev, cm, ctx->stream), "recv");
         nccl_check(api.groupEnd(), "groupEnd");
         comm_end(ctx, "comm_halo", ev);
     }

@@ -152,6 +152,46 @@ void exchange(vr_ctx* ctx, double* interior) {
         ctx->dist->halo(ctx, interior, static_cast<size_t>(ctx->g.n2) * ctx->g.n3, ctx->g.L,
                         ctx->g.halo);
 }
+
+// One semi-Lagrangian step whose gather source `src` needs its halo (SURVEY 8(e)
+// "Overlap"): on x1 slabs with a concurrent-capable transport the halo exchange runs on
+// the side stream while the step runs on the interior planes [H, L - H) -- whose stencils
+// stay inside the slab, since H >= the x1 displacement + 4 -- and the two boundary bands
+// run once the halo has arrived. `launch` issues the step on ctx->stream over the plane
+// window in ctx->g (z0, zn). Elsewhere: exchange, then one launch over all planes.
+template <class Launch>
+void step_with_halo(vr_ctx* ctx, double* src, Launch&& launch) {
+    GridDims& g = ctx->g;
+    const int L = g.L, H = g.halo;
+    if (!ctx->dist || !ctx->overlap || !ctx->dist->side_stream_ok() || ctx->profiling || L <= 2 * H) {
+        exchange(ctx, src);
+        launch();
+        return;
+    }
+    VR_CUDA(cudaEventRecord(ctx->ev_halo_fork, ctx->stream));
+    VR_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_halo_fork, 0));
+    cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->side;
+    try {
+        exchange(ctx, src);
+    } catch (...) {
+        ctx->stream = main;
+        throw;
+    }
+    ctx->stream = main;
+    VR_CUDA(cudaEventRecord(ctx->ev_halo, ctx->side));
+    struct Window {  // restores the full plane range on exit
+        GridDims& g;
+        ~Window() { g.z0 = 0, g.zn = g.L; }
+    } restore{g};
+    g.z0 = H, g.zn = L - 2 * H;
+    launch();
+    VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+    g.z0 = 0, g.zn = H;
+    launch();
+    g.z0 = L - H, g.zn = H;
+    launch();
+}
 // The per-call device flags: [0] non-finite direction, [1] departure beyond halo. They
 // are sticky and reset whenever they are read. A matvec inside the solver does not
 // synchronise for them: it marks them pending (defer_flags) and the next reduction
@@ -237,10 +277,10 @@ vr_state* objective_evaluate(vr_objective* o, const double* v3) {
         // solve_state (transport.cpp:72-79)
         VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->mhist, 0), o->mT, sizeof(double) * N,
                                 cudaMemcpyDeviceToDevice, ctx->stream));
-        for (int j = 0; j < nt; ++j) {
-            exchange(ctx, pslice(ctx, s->mhist, j));
-            sl_advect(ctx, pslice(ctx, s->mhist, j), s->xb, pslice(ctx, s->mhist, j + 1));
-        }
+        for (int j = 0; j < nt; ++j)
+            step_with_halo(ctx, pslice(ctx, s->mhist, j), [&] {
+                sl_advect(ctx, pslice(ctx, s->mhist, j), s->xb, pslice(ctx, s->mhist, j + 1));
+            });
         o->counters.pde_solves += 1;
 
         s->mismatch = sum_sq_diff(ctx, pslice(ctx, s->mhist, nt), o->mR, N) * cell_volume(g);
@@ -364,11 +404,11 @@ void objective_gradient(vr_objective* o, vr_state* s) {
     double* b = o->ws_b;
     sl_grad_terminal(ctx, o->mR, pslice(ctx, s->mhist, nt), s->gradm + 3LL * nt * N, 0.5 * dt,
                      pslice(ctx, hist, nt), nullptr);
-    for (int j = nt - 1; j >= 0; --j) {
-        exchange(ctx, pslice(ctx, hist, j + 1));
-        sl_adjoint_step(ctx, pslice(ctx, hist, j + 1), s->xf, s->factor, pslice(ctx, hist, j),
-                        nullptr, 0.0, nullptr);
-    }
+    for (int j = nt - 1; j >= 0; --j)
+        step_with_halo(ctx, pslice(ctx, hist, j + 1), [&] {
+            sl_adjoint_step(ctx, pslice(ctx, hist, j + 1), s->xf, s->factor, pslice(ctx, hist, j),
+                            nullptr, 0.0, nullptr);
+        });
     sl_accumulate(ctx, pslice(ctx, hist, 0), s->gradm, nt, dt, b);
     o->counters.pde_solves += 1;
     if (ctx->dist) check_flags(ctx, "compute_gradient");
@@ -433,14 +473,15 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
     int cur = 0;
     for (int j = 0; j < nt; ++j) {
         const bool last = (j + 1 == nt);
-        exchange(ctx, tmp[cur]);
-        if (last && fused)
-            sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * nt * N, vt3, hdt, lam(1), 2, b,
-                             0.5 * dt);
-        else
-            sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
-                             last ? lam(nt) : tmp[cur ^ 1], last ? 1 : 0, nullptr, 0.0,
-                             full ? fn.mt + (j + 1) * N : nullptr);
+        step_with_halo(ctx, tmp[cur], [&] {
+            if (last && fused)
+                sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * nt * N, vt3, hdt, lam(1), 2, b,
+                                 0.5 * dt);
+            else
+                sl_incstate_step(ctx, tmp[cur], s->xb, s->gradm + 3LL * (j + 1) * N, vt3, hdt,
+                                 last ? lam(nt) : tmp[cur ^ 1], last ? 1 : 0, nullptr, 0.0,
+                                 full ? fn.mt + (j + 1) * N : nullptr);
+        });
         cur ^= 1;
     }
     o->counters.pde_solves += 1;
@@ -473,17 +514,18 @@ void objective_matvec(vr_objective* o, const vr_state* s, const double* vt3, dou
             const double w = (j == 0) ? 0.5 * dt : dt;
             // the last step also adds u = beta_v A vt when it is given (out = b + u)
             const bool fin = (j == 0) && reg_given && identity_K;
-            exchange(ctx, lam(lc));
-            sl_adjoint_step(ctx, lam(lc), s->xf, s->factor, lam(lc ^ 1), s->gradm + 3LL * j * N, w, b,
-                            fin ? reg_given : nullptr, fin ? out3 : b);
+            step_with_halo(ctx, lam(lc), [&] {
+                sl_adjoint_step(ctx, lam(lc), s->xf, s->factor, lam(lc ^ 1), s->gradm + 3LL * j * N, w,
+                                b, fin ? reg_given : nullptr, fin ? out3 : b);
+            });
             lc ^= 1;
             out_done = fin;
         }
     } else {
-        for (int j = nt - 1; j >= 0; --j) {
-            exchange(ctx, lam(j + 1));
-            sl_adjoint_step(ctx, lam(j + 1), s->xf, s->factor, lam(j), nullptr, 0.0, nullptr);
-        }
+        for (int j = nt - 1; j >= 0; --j)
+            step_with_halo(ctx, lam(j + 1), [&] {
+                sl_adjoint_step(ctx, lam(j + 1), s->xf, s->factor, lam(j), nullptr, 0.0, nullptr);
+            });
         if (reg_given && identity_K) {
             sl_accumulate(ctx, lam0, s->gradm, nt, dt, out3, reg_given);  // out = b + u, one pass
             out_done = true;

@@ -170,8 +170,8 @@ __device__ __forceinline__ bool tile_point(const GridDims& g, const Tile& t, int
     }
     i3 = blockIdx.x * T3 + l3;
     i2 = blockIdx.y * T2 + l2;
-    i1 = blockIdx.z * T1 + l1;
-    const bool ok = l1 < T1 && i1 < g.L && i2 < g.n2 && i3 < g.n3;
+    i1 = g.z0 + blockIdx.z * T1 + l1;
+    const bool ok = l1 < T1 && i1 < g.z0 + g.zn && i2 < g.n2 && i3 < g.n3;
     idx = ok ? (static_cast<long long>(i1) * g.n2 + i2) * g.n3 + i3 : 0;
     return ok;
 }
@@ -586,7 +586,7 @@ Tile tile_of(const GridDims& g) {
 }
 dim3 tgrid(const GridDims& g, const Tile& t) {
     return dim3(static_cast<unsigned>(g.n3 / t.t3), static_cast<unsigned>(g.n2 / t.t2),
-                static_cast<unsigned>(g.L / t.t1));
+                static_cast<unsigned>((g.zn + t.t1 - 1) / t.t1));
 }
 unsigned tthreads(const Tile& t) { return static_cast<unsigned>(t.t1 * t.t2 * t.t3); }
 

@@ -82,6 +82,9 @@ struct GridDims {
     long long Ng;       // global points n1*n2*n3 (FFT normalisation)
     double h1, h2, h3;  // two_pi / n_a, exactly as Grid3::spacing
     int* flags;         // device flags: [0] non-finite input, [1] departure beyond halo
+    int z0, zn;         // x1 plane window of the tiled (semi-Lagrangian) kernels: local planes
+                        // [z0, z0 + zn), normally [0, L); narrowed to run a slab's interior
+                        // planes while its halo is in flight
 };
 
 // Signed FFT frequency / odd-derivative frequency (grid.hpp:58-64)
@@ -114,6 +117,9 @@ struct Transport {
     virtual void halo(vr_ctx* ctx, double* interior, size_t plane, int L, int H) = 0;
     // combine k host doubles over ranks in rank order (sum, or max when `max`)
     virtual void allreduce(vr_ctx* ctx, double* vals, int k, bool max) = 0;
+    // exchanges may be issued on the context's side stream concurrently with main-stream
+    // exchanges (every rank issues the same host-ordered sequence either way)
+    virtual bool side_stream_ok() const { return true; }
 };
 
 }  // namespace vr
@@ -125,6 +131,7 @@ struct vr_ctx {
     bool owns_stream = true;         // false for siblings running on a parent's stream
     cudaStream_t side = nullptr;     // internal: overlaps independent spectral work
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_halo = nullptr, ev_halo_fork = nullptr;  // interior / halo overlap on slabs
     vr::GridDims g{};
     vr::FftPlan* fft = nullptr;
     vr::Transport* dist = nullptr;  // null on one GPU
@@ -149,9 +156,11 @@ struct vr_ctx {
     std::unordered_map<const void*, long long> mem_sizes;
     // optional per-launch CUDA-event timing (bench / roofline evidence)
     bool profiling = false;
-    // side-stream overlap of independent spectral work (VR_OVERLAP=1 enables).
-    // Off by default: the FFT kernels' shared memory shrinks the L1 that the
-    // concurrent gather kernels live on (measured 7.7 vs 6.9 ms per matvec).
+    // side-stream overlap of independent spectral work (VR_OVERLAP=1 / 0 forces it).
+    // Off by default on one GPU: the FFT kernels' shared memory shrinks the L1 that the
+    // concurrent gather kernels live on (measured 7.7 vs 6.9 ms per matvec). On by default
+    // on x1 slabs, where the beta_v A vt transposes (all-to-all over NVLink) hide under
+    // the semi-Lagrangian sweeps (SURVEY 8(e) "Overlap").
     bool overlap = false;
     // GN matvec: accumulate b inside the adjoint steps (HBM slack of the
     // L1-bound gathers) instead of a separate pass over all lam_j (VR_FUSE_ACC)
@@ -327,12 +336,13 @@ void op_reg_finish_f32(vr_ctx* ctx, float* out3, const float* add3);  // out = f
 void op_reg_begin_f32(vr_ctx* ctx, const float* in3, const vr_regnorm& norm, int mode, double beta);
 // run `fn` (which launches on ctx->stream) on the side stream, forked from the
 // current point of ctx->stream; join_side() makes ctx->stream wait for it
-// (on x1 slabs the work stays on the main stream: its collectives must keep one
-// order on every rank; while profiling too, so per-kernel event intervals do not
-// include time shared with a concurrent kernel)
+// (on x1 slabs the side-stream exchanges use their own communicator, and every rank
+// issues them in the same host order; while profiling the work stays on the main
+// stream, so per-kernel event intervals do not include time shared with a concurrent
+// kernel)
 template <class Fn>
 void on_side_stream(vr_ctx* ctx, Fn&& fn) {
-    if (ctx->dist || ctx->profiling || !ctx->overlap) {
+    if ((ctx->dist && !ctx->dist->side_stream_ok()) || ctx->profiling || !ctx->overlap) {
         fn();
         return;
     }
@@ -350,7 +360,8 @@ void on_side_stream(vr_ctx* ctx, Fn&& fn) {
     VR_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
 }
 inline void join_side(vr_ctx* ctx) {
-    if (!ctx->dist && !ctx->profiling && ctx->overlap) VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+    if (!(ctx->dist && !ctx->dist->side_stream_ok()) && !ctx->profiling && ctx->overlap)
+        VR_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
 }
 double reg_symbol(const vr_regnorm& n, double k2);
 
