@@ -552,9 +552,18 @@ def main():
         _ = V._lib.call("vr_memcpy_d2d", ctx.handle, d_mR.ptr, hist.field(nt), 8 * ctx.N)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev))
     obj = V.Objective(ctx, d_mR, d_mT, model)
+    mem0 = ctx.memory()
     st = obj.evaluate(d_v)
     obj.compute_gradient(st)
     out = ctx.empty(3)
+    mem1 = ctx.memory()
+    F_bytes = 8.0 * ctx.N
+    memory = {"context_live_GiB": mem1["live_bytes"] / 2 ** 30,
+              "eval_state_fields": (mem1["live_bytes"] - mem0["live_bytes"] - 3 * F_bytes) / F_bytes,
+              "peak_GiB": mem1["peak_bytes"] / 2 ** 30,
+              "pool_reserved_high_GiB": mem1["pool_reserved_high_bytes"] / 2 ** 30,
+              "note": "library device allocations of this rank (vr_ctx_memory): images, objective workspace, "
+                      "EvalState (v, X_bwd, m history, X_fwd, factor, grad m cache, gradient) and scratch"}
 
     for _ in range(max(3, args.warmup)):
         obj.hessian_matvec(st, d_vt, out=out)
@@ -675,9 +684,15 @@ def main():
     comm = None
     if scaling == "strong":
         cats = {k: v for k, v in prof.items() if k.startswith("comm_")}
-        comm = {"exposed_ms_per_matvec": sum(t for c, t in cats.values()) / k_prof,
+        comm_ms = sum(t for c, t in cats.values()) / k_prof
+        compute_ms = sum(t for k, (c, t) in prof.items() if not k.startswith("comm_")) / k_prof
+        comm = {"total_ms_per_matvec": comm_ms,
                 "by_kind_ms_per_matvec": {k: t / k_prof for k, (c, t) in cats.items()},
-                "note": "serialised profile pass (rank 0): NCCL exchange time per matvec", **(comm_info or {})}
+                "compute_ms_per_matvec": compute_ms,
+                "exposed_ms_per_matvec": max(0.0, ms_per_step - compute_ms),
+                "note": "total / by kind from the serialised profile pass (every kernel and exchange "
+                        "bracketed alone); exposed = timed ms per matvec (reg-term transposes and halos "
+                        "overlapped with the sweeps) minus the serialised compute time", **(comm_info or {})}
     # per-matvec HBM bytes over the aggregate HBM bandwidth, plus (slabs) the
     # all-to-all and halo bytes over NVLink (900 GB/s per direction per GPU)
     nvl_bytes = 0.0
@@ -864,7 +879,8 @@ def main():
                 "kernels": kernels, "kernel_profile": {"steps": k_prof, "ms_per_step": ms_prof / k_prof,
                                                         "note": "separate serialised pass, events per kernel"},
                 "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve,
-                "config4_single_gpu": cfg4, "config2": cfg2, "fp32_lane": f32, "comm": comm}
+                "config4_single_gpu": cfg4, "config2": cfg2, "fp32_lane": f32, "comm": comm,
+                "memory": memory}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
