@@ -87,6 +87,7 @@ _SIG = {
                                         P, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
                                         C.POINTER(IterationRecord), I]),
     "vref_generate_synthetic": (I, [DIMS, I, D, P, P, P]),
+    "vref_make_ball_labels": (I, [DIMS, I, P]),
     "vref_det_deformation_gradient": (I, [DIMS, P, I, P]),
     "vref_tricubic_interpolate_f32": (I, [DIMS, P, P, P, I]),
     "vref_objective_f32_create": (I, [DIMS, P, P, C.POINTER(Model), C.POINTER(P)]),
@@ -740,6 +741,12 @@ def det_stats(det, foreground=None, threshold=0.05):
     _call("vref_det_stats", _dims(d.shape), d.ctypes.data, fg.ctypes.data if fg is not None else None,
           float(threshold), out)
     return {"min": out[0], "mean": out[1], "max": out[2]}
+
+
+def make_ball_labels(shape, count):
+    out = np.empty(shape)
+    _call("vref_make_ball_labels", _dims(shape), count, out.ctypes.data)
+    return out
 
 
 def transport_labels(labels, v, nt):

@@ -774,6 +774,10 @@ int vref_det_stats(const int* d, const double* det, const double* fg, double thr
         out3[0] = st.min, out3[1] = st.mean, out3[2] = st.max;
     });
 }
+// make_ball_labels (synthetic.cpp:36-66): the labelled balls of the reference's postprocess tests
+int vref_make_ball_labels(const int* d, int count, double* out) {
+    return guard([&] { store(make_ball_labels<double>(grid_of(d), count), out); });
+}
 int vref_transport_labels(const int* d, const double* labels, const double* v, int nt, double* out) {
     return guard([&] {
         Grid3 g = grid_of(d);

@@ -183,3 +183,76 @@ def test_beta_search(vr, ref, ctx):
     with pytest.raises(vr.NumericError) as e:
         vr.beta_search(c, mR, mT, v0, model, params, search=vr.beta_search_params(eps_J=0.9999999))
     assert len(e.value.trials) == 1 and not e.value.trials[0]["feasible"]
+
+
+def _compressible_velocity(x, y, z):
+    # proj/tests/test_postprocess.cpp:18-25 over synthetic_velocity (synthetic.cpp:10-14)
+    a = 0.3
+    return (np.sin(z) * np.cos(y) * np.sin(y) + a * np.cos(x) * np.sin(y) * np.sin(z),
+            np.sin(x) * np.cos(z) * np.sin(z) + a * np.sin(x) * np.cos(y) * np.sin(z),
+            np.sin(y) * np.cos(x) * np.sin(x) + a * np.sin(x) * np.sin(y) * np.cos(z))
+
+
+def _fd_det_grad(n, eps=1e-4, substeps=100):
+    """fd_det_grad (proj/tests/oracles.hpp:70-91) at every grid point, vectorised: central
+    differences of RK4 backward trajectories (rk4_flow, oracles.hpp:17-35), det3."""
+    h = 2 * np.pi / n
+    g = np.arange(n) * h
+    X = np.stack(np.meshgrid(g, g, g, indexing="ij")).reshape(3, -1)
+
+    def flow(p):
+        dt = 1.0 / substeps
+        p = p.copy()
+        for _ in range(substeps):
+            f = lambda q: -np.array(_compressible_velocity(q[0], q[1], q[2]))  # noqa: E731
+            k1 = f(p)
+            k2 = f(p + 0.5 * dt * k1)
+            k3 = f(p + 0.5 * dt * k2)
+            k4 = f(p + dt * k3)
+            p = p + (dt / 6.0) * (k1 + 2 * k2 + 2 * k3 + k4)
+        return p
+
+    J = np.empty((3, 3, X.shape[1]))
+    for a in range(3):
+        xp, xm = X.copy(), X.copy()
+        xp[a] += eps
+        xm[a] -= eps
+        yp, ym = flow(xp), flow(xm)
+        for c in range(3):
+            J[c, a] = ((yp[c] - xp[c]) - (ym[c] - xm[c])) / (2 * eps) + (1.0 if c == a else 0.0)
+    det = (J[0, 0] * (J[1, 1] * J[2, 2] - J[1, 2] * J[2, 1]) - J[0, 1] * (J[1, 0] * J[2, 2] - J[1, 2] * J[2, 0])
+           + J[0, 2] * (J[1, 0] * J[2, 1] - J[1, 1] * J[2, 0]))
+    return det.reshape(n, n, n)
+
+
+def test_reference_postprocess_failures_are_not_the_fft_shim(vr, ref, ctx):
+    """The compiled reference fails 2 of its own 7 postprocess checks under the oracle build
+    (test_postprocess.cpp:66 and :142). Both failures reproduce identically on the GPU path,
+    whose FFT is independent of the oracle's FFTW shim, so they are properties of the
+    reference's algorithm at the test's sizes, not of the shim:
+    * :66 -- det grad y by continuity transport vs the RK4/FD trajectory oracle exceeds 1e-2
+      at 16^3, n_t = 4; the gap is discretisation error (it shrinks with the grid);
+    * :142 -- smoothing + arg-max of two small balls at v = 0 flips more boundary voxels than
+      the test's ball/20 bound; the GPU flips exactly the same voxels."""
+    errs = {}
+    for n in (16, 32):
+        h = 2 * np.pi / n
+        g = np.arange(n) * h
+        X1, X2, X3 = np.meshgrid(g, g, g, indexing="ij")
+        v = np.stack(_compressible_velocity(X1, X2, X3))
+        fd = _fd_det_grad(n)
+        d_ref = ref.det_deformation_gradient(v, 4)
+        d_gpu = np.asarray(vr.det_deformation_gradient(ctx(n), v, 4))
+        errs[n] = (float(np.abs(d_ref - fd).max()), float(np.abs(d_gpu - fd).max()))
+    print("det grad y vs FD oracle (reference, gpu):", errs)
+    assert errs[16][0] > 1e-2  # the reference's own check (<= 1e-2) fails
+    assert abs(errs[16][1] - errs[16][0]) <= 1e-8  # ... identically with an independent FFT
+    assert errs[32][0] < 0.5 * errs[16][0]  # discretisation error: shrinks with resolution
+    labels = ref.make_ball_labels((32, 32, 32), 2)
+    z = np.zeros((3, 32, 32, 32))
+    same_ref = ref.transport_labels(labels, z, 4)
+    same_gpu = np.asarray(vr.transport_labels(ctx(32), labels, z, 4))
+    ball = int((labels != 0).sum())
+    flips_ref, flips_gpu = int((same_ref != labels).sum()), int((same_gpu != labels).sum())
+    print("label flips at v = 0 (reference, gpu, ball/20):", flips_ref, flips_gpu, ball // 20)
+    assert flips_ref > ball // 20 and np.array_equal(same_gpu, same_ref)
