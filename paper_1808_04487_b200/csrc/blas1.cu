@@ -7,6 +7,8 @@
 // reproducible run to run (though not bitwise equal to the CPU chunk order).
 #include <cfloat>
 
+#include <chrono>
+
 #include "vr_common.cuh"
 
 namespace vr {
@@ -126,7 +128,12 @@ void reduce(vr_ctx* ctx, const double* a, const double* b, long long n, int ncom
     VR_CUDA(cudaMemcpyAsync(ctx->red_host, ctx->red_out, sizeof(double) * ncomp,
                             cudaMemcpyDeviceToHost, ctx->stream));
     flags_enqueue_copy(ctx);  // deferred matvec flags ride on this synchronisation
-    VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    {
+        const auto t0 = std::chrono::steady_clock::now();
+        VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (timing_enabled())
+            slow_op("reduce sync", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
     for (int c = 0; c < ncomp; ++c) host_out[c] = ctx->red_host[c];
     if (ctx->dist) ctx->dist->allreduce(ctx, host_out, ncomp, is_max<OP>());  // rank order
     flags_after_sync(ctx);

@@ -42,9 +42,21 @@ vr_objective::~vr_objective() {
 
 namespace vr {
 
+bool timing_enabled() {
+    static const bool on = std::getenv("VR_TIMING") != nullptr;
+    return on;
+}
+void slow_op(const char* what, double ms) {
+    static const double thr = std::getenv("VR_SLOW_MS") ? std::atof(std::getenv("VR_SLOW_MS")) : 20.0;
+    if (ms > thr) std::fprintf(stderr, "VR_TIMING slow %s: %.1f ms\n", what, ms);
+}
+
 double* dev_alloc(vr_ctx* ctx, long long n) {
     void* p = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMallocAsync(&p, sizeof(double) * static_cast<size_t>(n), ctx->stream);
+    if (timing_enabled())
+        slow_op("cudaMallocAsync", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     if (e != cudaSuccess) {
         cudaGetLastError();
         throw_resource("device allocation of " + std::to_string(sizeof(double) * n) +
@@ -56,7 +68,10 @@ double* dev_alloc(vr_ctx* ctx, long long n) {
 void dev_free(vr_ctx* ctx, double* p) {
     if (!p) return;
     mem_track_free(ctx, p);
+    const auto t0 = std::chrono::steady_clock::now();
     cudaFreeAsync(p, ctx->stream);
+    if (timing_enabled())
+        slow_op("cudaFreeAsync", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
 }
 
 void validate_model(const vr_model& m) {
@@ -798,7 +813,11 @@ LineSearch armijo_search(vr_objective* o, const vr_state* cur, const double* dir
     try {
         for (int t = 0; t < p.armijo_max_trials; ++t) {
             lin_comb(ctx, trial_v, 1.0, cur->v, alpha, dir, n3);
+            const auto t0 = std::chrono::steady_clock::now();
             vr_state* trial = objective_evaluate(o, trial_v);
+            if (timing_enabled())
+                slow_op("armijo trial evaluate",
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
             res.trials = t + 1;
             if (trial->objective <= cur->objective + p.armijo_c1 * alpha * slope) {
                 res.success = true;

@@ -21,6 +21,11 @@ namespace vr {
 
 constexpr double kTwoPi = 6.283185307179586476925286766559;
 
+// VR_TIMING diagnostics: host operations (allocations, synchronisations) that take longer
+// than VR_SLOW_MS (default 20 ms) are reported on stderr with their name
+bool timing_enabled();
+void slow_op(const char* what, double ms);
+
 // NVTX range per operator / solver phase (visible in nsys / ncu --nvtx timelines; a
 // no-op unless a tool injects the NVTX handler)
 struct Range {
