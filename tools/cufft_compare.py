@@ -39,3 +39,17 @@ st = torch.cuda.ExternalStream(ctx.stream)
 res["ours_r2c_us"] = timeit(lambda: V._lib.call("vr_fft_r2c", ctx.handle, f.ptr, spec.ptr), st)
 res["ours_c2r_us"] = timeit(lambda: V._lib.call("vr_fft_c2r", ctx.handle, spec.ptr, out.ptr), st)
 print(json.dumps(res))
+# the fused spectral operator: beta A v (H2) on 3 components, cuFFT r2c * multiplier * c2r vs
+# this library's vr_apply_reg_operator (5 passes per component, multiplier fused in the x1 pass)
+k = torch.fft.fftfreq(n, 1.0 / n, device="cuda", dtype=torch.float64)
+k3 = torch.arange(n // 2 + 1, device="cuda", dtype=torch.float64)
+mult = 1e-2 * (k[:, None, None] ** 2 + k[None, :, None] ** 2 + k3[None, None, :] ** 2) ** 2
+v3 = torch.randn(3, n, n, n, dtype=torch.float64, device="cuda")
+res["cufft_reg_op_3_us"] = timeit(lambda: [torch.fft.irfftn(torch.fft.rfftn(v3[c]) * mult, s=(n, n, n))
+                                           for c in range(3)], s, reps=10)
+dv3 = ctx.to_device(v3.cpu().numpy())
+o3 = ctx.empty(3)
+norm = V.make_norm("h2")
+res["ours_reg_op_3_us"] = timeit(lambda: V._lib.call("vr_apply_reg_operator", ctx.handle, dv3.ptr, o3.ptr,
+                                                     V.C.byref(norm), 0, 1e-2), st, reps=10)
+print(json.dumps(res))
