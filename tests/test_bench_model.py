@@ -26,7 +26,7 @@ def test_measured_peak_source():
 
 def test_profiles_bench_line_contract():
     # the committed bench line carries the keys the driver and the judge read
-    p = os.path.join(bench.ROOT, "profiles", "r01_bench.json")
+    p = os.path.join(bench.ROOT, "profiles", "r02_bench.json")
     if not os.path.exists(p):
         pytest.skip("no committed bench line")
     d = json.load(open(p))
