@@ -311,6 +311,9 @@ int vr_ctx_destroy(vr_ctx* ctx) {
         for (vr_ctx* c : ctx->siblings) vr_ctx_destroy(c);  // they share this stream
         ctx->siblings.clear();
         vr::fft_plan_destroy(ctx);
+        vr::release_cache(ctx);
+        if (ctx->side) cudaStreamSynchronize(ctx->side);
+        cudaStreamSynchronize(ctx->stream);
         for (double* p : ctx->spec_scratch) cudaFree(p);
         for (double* p : ctx->field_scratch) cudaFree(p);
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

@@ -52,6 +52,14 @@ void slow_op(const char* what, double ms) {
 }
 
 double* dev_alloc(vr_ctx* ctx, long long n) {
+    auto range = ctx->free_cache.equal_range(n);
+    for (auto it = range.first; it != range.second; ++it) {
+        if (it->second.second != ctx->stream) continue;
+        double* p = it->second.first;
+        ctx->free_cache.erase(it);
+        mem_track_alloc(ctx, p, static_cast<long long>(sizeof(double)) * n);
+        return p;
+    }
     void* p = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMallocAsync(&p, sizeof(double) * static_cast<size_t>(n), ctx->stream);
@@ -59,19 +67,31 @@ double* dev_alloc(vr_ctx* ctx, long long n) {
         slow_op("cudaMallocAsync", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     if (e != cudaSuccess) {
         cudaGetLastError();
-        throw_resource("device allocation of " + std::to_string(sizeof(double) * n) +
-                       " bytes failed: " + cudaGetErrorString(e));
+        release_cache(ctx);  // give the cached buffers back and retry once
+        e = cudaMallocAsync(&p, sizeof(double) * static_cast<size_t>(n), ctx->stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw_resource("device allocation of " + std::to_string(sizeof(double) * n) +
+                           " bytes failed: " + cudaGetErrorString(e));
+        }
     }
     mem_track_alloc(ctx, p, static_cast<long long>(sizeof(double)) * n);
     return static_cast<double*>(p);
 }
 void dev_free(vr_ctx* ctx, double* p) {
     if (!p) return;
-    mem_track_free(ctx, p);
-    const auto t0 = std::chrono::steady_clock::now();
+    auto it = ctx->mem_sizes.find(p);
+    if (it != ctx->mem_sizes.end()) {
+        const long long n = it->second / static_cast<long long>(sizeof(double));
+        mem_track_free(ctx, p);
+        ctx->free_cache.emplace(n, std::make_pair(p, ctx->stream));
+        return;
+    }
     cudaFreeAsync(p, ctx->stream);
-    if (timing_enabled())
-        slow_op("cudaFreeAsync", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+}
+void release_cache(vr_ctx* ctx) {
+    for (auto& kv : ctx->free_cache) cudaFreeAsync(kv.second.first, kv.second.second);
+    ctx->free_cache.clear();
 }
 
 void validate_model(const vr_model& m) {

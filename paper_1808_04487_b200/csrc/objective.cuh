@@ -61,6 +61,7 @@ namespace vr {
 
 double* dev_alloc(vr_ctx* ctx, long long ndoubles);
 void dev_free(vr_ctx* ctx, double* p);
+void release_cache(vr_ctx* ctx);  // return the context's cached device buffers to the pool
 // halo-padded field helpers (objective.cu)
 long long hoff(const vr_ctx* ctx);
 double* pslice(const vr_ctx* ctx, double* base, int j);

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -159,6 +160,11 @@ struct vr_ctx {
     // allocations made by the library for this context, and their peak since the last reset
     long long mem_live = 0, mem_peak = 0;
     std::unordered_map<const void*, long long> mem_sizes;
+    // freed library buffers kept for reuse by size (and the stream they were freed on, so a
+    // reuse is ordered after every kernel that used the buffer): the solver's per-iterate
+    // states and trial velocities then cost no cudaMallocAsync in steady state, where the
+    // stream-ordered pool's growth stalls the host for 20-800 ms (VR_TIMING)
+    std::multimap<long long, std::pair<double*, cudaStream_t>> free_cache;
     // optional per-launch CUDA-event timing (bench / roofline evidence)
     bool profiling = false;
     // side-stream overlap of independent spectral work (VR_OVERLAP=1 / 0 forces it).
