@@ -19,6 +19,8 @@
 // In-register butterflies are radix-2 DIT networks of size <= 16 with
 // literal twiddles; inter-stage twiddles come from per-axis long-double
 // tables (exactly rounded), so the transform error is O(eps log n).
+#include <cuda.h>  // CUtensorMap types; cuTensorMapEncodeTiled is resolved at run time (no -lcuda)
+
 #include <cmath>
 #include <type_traits>
 
@@ -286,8 +288,46 @@ struct AxisCfg {
     static constexpr int TB = TB0 < 1 ? 1 : (TB0 > 64 ? 64 : TB0);
     static constexpr int THREADS = TB * T;
     static constexpr int STAGE = N * TB;  // one pipeline stage (double2)
-    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + N);  // 2 stages + W_N
+    static constexpr int BOX_ROWS = N < 256 ? N : 256;  // TMA box height (<= 256 per dimension)
+    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + N) + 16;  // 2 stages + W_N + 2 mbarriers
 };
+
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers for the strided passes ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// one 3D box (columns x rows x outer block) global -> shared, completing on `bar`
+__device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* tmap, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(sdst)), "l"(reinterpret_cast<unsigned long long>(tmap)), "r"(x), "r"(y), "r"(z),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+// generic-proxy shared-memory accesses before this fence are ordered before later
+// async-proxy (TMA) writes to the same locations
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Strided-axis pass over tiles of TB adjacent columns x N elements, persistent
 // CTAs with a two-stage cp.async pipeline (the next tile streams in while this
@@ -301,35 +341,40 @@ struct AxisCfg {
 //         i k (Nyquist 0) maps real lines to real lines, so the pair never mixes
 template <int N, int DIR, int MODE>
 __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
-    k_fft_axis(const double2* src, double2* dst, long long inner, long long outer,
+    k_fft_axis(const __grid_constant__ CUtensorMap tmap, double2* dst, long long inner, long long outer,
                long long outer_stride, const double2* __restrict__ tw_g, MultDev m, GridDims g) {
     using C = AxisCfg<N>;
-    extern __shared__ double2 smem[];
+    extern __shared__ __align__(128) double2 smem[];
     double2* tw = smem + 2 * C::STAGE;  // W_N table staged once per CTA (broadcast reads)
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(tw + N);  // one mbarrier per stage
     for (int i = threadIdx.x; i < N; i += C::THREADS) tw[i] = __ldg(tw_g + i);
     const long long ncb = (inner + C::TB - 1) / C::TB;
     const long long ntiles = ncb * outer;
     const int col = threadIdx.x % C::TB;
     const int t = threadIdx.x / C::TB;
-    auto issue = [&](long long tile, double2* stage) {
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        mbar_init(full + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // tile = TB adjacent columns x N rows of block `ob`: one TMA box per 256 rows, issued by
+    // one thread; columns past `inner` are zero-filled by the copy engine
+    auto issue = [&](long long tile, int b) {
         const long long ob = tile / ncb, c0 = (tile - ob * ncb) * C::TB;
-        const double2* s = src + ob * outer_stride + c0;
-#pragma unroll 4
-        for (int e = threadIdx.x; e < C::STAGE; e += C::THREADS) {
-            const int i = e / C::TB, cl = e % C::TB;
-            const bool ok = c0 + cl < inner;
-            cp_async16(stage + e, s + (ok ? static_cast<long long>(i) * inner + cl : 0), ok);
-        }
+        mbar_expect_tx(full + b, static_cast<unsigned>(C::STAGE * sizeof(double2)));
+#pragma unroll
+        for (int r0 = 0; r0 < N; r0 += C::BOX_ROWS)
+            tma_load_3d(smem + b * C::STAGE + r0 * C::TB, &tmap, static_cast<int>(2 * c0), r0,
+                        static_cast<int>(ob), full + b);
     };
     long long tile = blockIdx.x;
-    if (tile < ntiles) issue(tile, smem);
-    cp_async_commit();
-    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
+    if (threadIdx.x == 0 && tile < ntiles) issue(tile, 0);
+    unsigned it = 0;
+    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1, ++it) {
         const long long next = tile + gridDim.x;
-        if (next < ntiles) issue(next, smem + (b ^ 1) * C::STAGE);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
+        if (threadIdx.x == 0 && next < ntiles) issue(next, b ^ 1);
+        mbar_wait(full + b, (it >> 1) & 1);
         double2* buf = smem + b * C::STAGE;
         const long long ob = tile / ncb;
         const long long cc = (tile - ob * ncb) * C::TB + col;
@@ -381,7 +426,8 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
             __syncthreads();
             fft_line<N, +1, true, false>(t, tw, load_sm, store, sm);
         }
-        __syncthreads();  // this stage is refilled by the next iteration's prefetch
+        fence_proxy_async();  // butterfly stages wrote this stage; the next TMA box overwrites it
+        __syncthreads();      // this stage is refilled by the next iteration's prefetch
     }
 }
 
@@ -508,7 +554,8 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
             }
             dstp[e] = X;
         }
-        __syncthreads();  // this stage is refilled by the next iteration's prefetch
+        fence_proxy_async();  // butterfly stages wrote this stage; the next TMA box overwrites it
+        __syncthreads();      // this stage is refilled by the next iteration's prefetch
     }
 }
 
@@ -604,7 +651,8 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
             ot.y = static_cast<TO>(o.y);
             dstp[e] = ot;
         }
-        __syncthreads();  // this stage is refilled by the next iteration's prefetch
+        fence_proxy_async();  // butterfly stages wrote this stage; the next TMA box overwrites it
+        __syncthreads();      // this stage is refilled by the next iteration's prefetch
     }
 }
 
@@ -727,6 +775,43 @@ unsigned persistent_grid(vr_ctx* ctx, K kern, int threads, size_t smem, long lon
     return static_cast<unsigned>(ntiles < g ? ntiles : g);
 }
 
+// Tensor map of one strided pass: (2 inner doubles) x N rows x outer blocks, box = TB columns
+// x min(N, 256) rows. Encoded on the host per launch (the source buffer changes per call).
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+inline TmapEncodeFn tmap_encoder() {
+    static TmapEncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        VR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            throw_resource("fft: the CUDA driver does not export cuTensorMapEncodeTiled");
+        return reinterpret_cast<TmapEncodeFn>(p);
+    }();
+    return fn;
+}
+template <int N>
+CUtensorMap axis_tmap(const double2* src, long long inner, long long outer, long long outer_stride) {
+    using C = AxisCfg<N>;
+    CUtensorMap tm;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * inner), static_cast<cuuint64_t>(N),
+                                static_cast<cuuint64_t>(outer)};
+    // strides of dimensions 1 and 2 in bytes (dimension 0 is contiguous)
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner) * sizeof(double2),
+                                   static_cast<cuuint64_t>(outer > 1 ? outer_stride : inner * N) * sizeof(double2)};
+    const cuuint32_t box[3] = {2u * C::TB, static_cast<cuuint32_t>(C::BOX_ROWS), 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(src), dims,
+                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw_resource("fft: cuTensorMapEncodeTiled failed (code " + std::to_string(static_cast<int>(r)) + ")");
+    return tm;
+}
+
 template <int N, int DIR, int MODE>
 void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inner, long long outer,
                    long long outer_stride, const double2* tw, const MultDev& m) {
@@ -735,9 +820,10 @@ void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inne
     const long long ntiles = (inner + C::TB - 1) / C::TB * outer;
     const unsigned grid =
         persistent_grid(ctx, k_fft_axis<N, DIR, MODE>, C::THREADS, C::SMEM, ntiles, occ);
+    const CUtensorMap tm = axis_tmap<N>(src, inner, outer, outer_stride);
     VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : (MODE == 1 || MODE == 3 ? "fft_x1_mult" : "fft_deriv"),
               k_fft_axis<N, DIR, MODE><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
-                  src, dst, inner, outer, outer_stride, tw, m, ctx->g));
+                  tm, dst, inner, outer, outer_stride, tw, m, ctx->g));
 }
 
 template <int DIR, int MODE>
