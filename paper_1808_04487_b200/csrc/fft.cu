@@ -328,6 +328,20 @@ __device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* tmap,
 // generic-proxy shared-memory accesses before this fence are ordered before later
 // async-proxy (TMA) writes to the same locations
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// contiguous global -> shared bulk copy (bytes: multiple of 16), completing on `bar`
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init_pair(unsigned long long* bars) {
+    if (threadIdx.x == 0) {
+        mbar_init(bars, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
 
 // Strided-axis pass over tiles of TB adjacent columns x N elements, persistent
 // CTAs with a two-stage cp.async pipeline (the next tile streams in while this
@@ -447,8 +461,25 @@ struct RowCfg {
     static constexpr int THREADS = RB * T;
     static constexpr int LD = (M + 1) + ((M + 1) >> 4) + 1;  // padded row length
     static constexpr int STAGE = LD * RB;                     // one pipeline stage (double2)
-    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + 3 * M);  // 2 stages + W_M, W_2M
+    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + 3 * M) + 16;  // 2 stages + W_M, W_2M + 2 mbarriers
 };
+// A tile of RB consecutive rows of W double2 is one contiguous block in global memory: one
+// bulk copy (cp.async.bulk, issued by one thread, completing on an mbarrier) lands it
+// LINEARLY (row pitch W) at the start of the stage. The first butterfly stage reads that
+// linear layout into registers, and after its barrier every later access uses the padded
+// layout (row pitch LD, padi), so the bank-conflict-free exchange layout is kept.
+template <int M, int W>
+__device__ __forceinline__ void bulk_rows(double2* stage, const double2* src, long long tile,
+                                          long long nrows, unsigned long long* bar) {
+    using C = RowCfg<M>;
+    if (threadIdx.x == 0) {
+        const long long rows = nrows - tile * C::RB;
+        const unsigned bytes =
+            static_cast<unsigned>((rows < C::RB ? rows : C::RB) * W * sizeof(double2));
+        mbar_expect_tx(bar, bytes);
+        bulk_load(stage, src + tile * C::RB * W, bytes, bar);
+    }
+}
 // stage the W_M and W_N (N = 2M) twiddle tables in shared memory after the rows
 template <int M>
 __device__ __forceinline__ void stage_row_tables(double2* smem, const double2* twM_g,
@@ -510,24 +541,34 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
     k_r2c_rows(const TI* __restrict__ in, double2* __restrict__ out, long long nrows,
                const double2* __restrict__ twM_g, const double2* __restrict__ twN_g) {
     using C = RowCfg<M>;
-    extern __shared__ double2 smem[];
+    constexpr bool LIN = std::is_same<TI, double>::value;  // fp64 rows arrive by bulk copy
+    extern __shared__ __align__(128) double2 smem[];
     double2 *twM, *twN;
     stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(twN + 2 * M);
+    mbar_init_pair(full);
     const long long ntiles = (nrows + C::RB - 1) / C::RB;
+    auto issue = [&](long long tl, int b) {
+        if constexpr (LIN)
+            bulk_rows<M, M>(smem + b * C::STAGE, reinterpret_cast<const double2*>(in), tl, nrows, full + b);
+        else
+            load_rows_in<M, TI>(smem + b * C::STAGE, in, tl, nrows);
+    };
     long long tile = blockIdx.x;
-    if (tile < ntiles) load_rows_in<M, TI>(smem, in, tile, nrows);
-    cp_async_commit();
-    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
+    if (tile < ntiles) issue(tile, 0);
+    unsigned it = 0;
+    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1, ++it) {
         const long long next = tile + gridDim.x;
-        if (next < ntiles) load_rows_in<M, TI>(smem + (b ^ 1) * C::STAGE, in, next, nrows);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
+        if (next < ntiles) issue(next, b ^ 1);
+        if constexpr (LIN)
+            mbar_wait(full + b, (it >> 1) & 1);
+        else
+            __syncthreads();
         double2* buf = smem + b * C::STAGE;
         {
             const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
             auto sm = [&](int i) -> double2& { return buf[r * C::LD + padi(i)]; };
-            auto load = [&](int i) -> double2 { return sm(i); };
+            auto load = [&](int i) -> double2 { return LIN ? buf[r * M + i] : sm(i); };
             auto store = [&](int i, double2 v) { sm(i) = v; };
             fft_line<M, -1, true, true>(t, twM, load, store, sm);
         }
@@ -572,17 +613,18 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
     using C = RowCfg<M>;
     using TO2 = typename std::conditional<std::is_same<TO, float>::value, float2, double2>::type;
     constexpr int PER = C::RB * M / C::THREADS;  // output double2 per thread per tile
-    extern __shared__ double2 smem[];
+    extern __shared__ __align__(128) double2 smem[];
     double2 *twM, *twN;
     stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(twN + 2 * M);
+    mbar_init_pair(full);
     const long long ntiles = (nrows + C::RB - 1) / C::RB;
     long long tile = blockIdx.x;
-    if (tile < ntiles) load_rows_async<M, M + 1>(smem, in, tile, nrows);
-    cp_async_commit();
-    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
+    if (tile < ntiles) bulk_rows<M, M + 1>(smem, in, tile, nrows, full);
+    unsigned it = 0;
+    for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1, ++it) {
         const long long next = tile + gridDim.x;
-        if (next < ntiles) load_rows_async<M, M + 1>(smem + (b ^ 1) * C::STAGE, in, next, nrows);
-        cp_async_commit();
+        if (next < ntiles) bulk_rows<M, M + 1>(smem + (b ^ 1) * C::STAGE, in, next, nrows, full + (b ^ 1));
         const long long avail_out = (nrows - tile * C::RB) * M;
         TO2* dstp = reinterpret_cast<TO2*>(out) + tile * C::RB * M;
         // the add field's loads are issued now and land while the rows transform
@@ -600,29 +642,29 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
                 }
             }
         }
-        cp_async_wait<1>();
-        __syncthreads();
+        mbar_wait(full + b, (it >> 1) & 1);
         double2* buf = smem + b * C::STAGE;
-        // form Z in place: thread handles the pair (k, M-k), k in [0, M/2]
+        // form Z in place in the linear layout (row pitch M + 1): thread handles the pair
+        // (k, M-k), k in [0, M/2]
         for (int e = threadIdx.x; e < C::RB * (M / 2 + 1); e += C::THREADS) {
             const int r = e / (M / 2 + 1), k = e % (M / 2 + 1);
-            double2* X = buf + r * C::LD;
+            double2* X = buf + r * (M + 1);
             if (k == 0) {
-                const double a = X[0].x, bb = X[padi(M)].x;
+                const double a = X[0].x, bb = X[M].x;
                 X[0] = make_double2(a + bb, a - bb);
             } else {
-                const double2 xk = X[padi(k)], xm = X[padi(M - k)];
+                const double2 xk = X[k], xm = X[M - k];
                 const double2 wk = twN[k];     // exp(+2 pi i k / N)
                 const double2 wm = twN[M - k]; // exp(+2 pi i (M-k) / N)
                 {
                     const double2 E = cadd(xk, cconj(xm));
                     const double2 O = cmul(csub(xk, cconj(xm)), wk);
-                    X[padi(k)] = make_double2(E.x - O.y, E.y + O.x);
+                    X[k] = make_double2(E.x - O.y, E.y + O.x);
                 }
                 if (k != M - k) {
                     const double2 E = cadd(xm, cconj(xk));
                     const double2 O = cmul(csub(xm, cconj(xk)), wm);
-                    X[padi(M - k)] = make_double2(E.x - O.y, E.y + O.x);
+                    X[M - k] = make_double2(E.x - O.y, E.y + O.x);
                 }
             }
         }
@@ -630,7 +672,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
         {
             const int t = threadIdx.x % C::T, r = threadIdx.x / C::T;
             auto sm = [&](int i) -> double2& { return buf[r * C::LD + padi(i)]; };
-            auto load = [&](int i) -> double2 { return sm(i); };
+            auto load = [&](int i) -> double2 { return buf[r * (M + 1) + i]; };  // linear (first stage only)
             auto store = [&](int i, double2 v) { sm(i) = v; };
             fft_line<M, +1, true, true>(t, twM, load, store, sm);
         }
