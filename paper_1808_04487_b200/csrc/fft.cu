@@ -461,7 +461,10 @@ struct RowCfg {
     static constexpr int THREADS = RB * T;
     static constexpr int LD = (M + 1) + ((M + 1) >> 4) + 1;  // padded row length
     static constexpr int STAGE = LD * RB;                     // one pipeline stage (double2)
-    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + 3 * M) + 16;  // 2 stages + W_M, W_2M + 2 mbarriers
+    // 2 stages + W_M, W_2M. At M = 128 three CTAs fill the SM's 228 KB exactly, so the two
+    // mbarriers live in stage 0's last 16 bytes (pad slot LD - 1 of its last row: never a
+    // padded position, and past the end of the linear RB x (M + 1) landing area)
+    static constexpr size_t SMEM = sizeof(double2) * (2 * STAGE + 3 * M);
 };
 // A tile of RB consecutive rows of W double2 is one contiguous block in global memory: one
 // bulk copy (cp.async.bulk, issued by one thread, completing on an mbarrier) lands it
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
     extern __shared__ __align__(128) double2 smem[];
     double2 *twM, *twN;
     stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(twN + 2 * M);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + C::STAGE - 1);
     mbar_init_pair(full);
     const long long ntiles = (nrows + C::RB - 1) / C::RB;
     auto issue = [&](long long tl, int b) {
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
     extern __shared__ __align__(128) double2 smem[];
     double2 *twM, *twN;
     stage_row_tables<M>(smem, twM_g, twN_g, twM, twN);
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(twN + 2 * M);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + C::STAGE - 1);
     mbar_init_pair(full);
     const long long ntiles = (nrows + C::RB - 1) / C::RB;
     long long tile = blockIdx.x;
