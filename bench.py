@@ -59,6 +59,10 @@ def parse():
                     help="skip the 128^3 (config 2) per-operator micro-benchmarks and solve")
     ap.add_argument("--no-config4", action="store_true",
                     help="skip the 512^3 (config 4, one GPU) matvec throughput")
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="run the multi-GPU code path (x1 slabs over the NCCL transport, per-slab input "
+                         "generation, exchange timing) with whatever world size this is, including 1: a "
+                         "one-rank check of the path a torchrun launch takes, not a benchmark")
     return ap.parse_args()
 
 
@@ -518,9 +522,13 @@ def main():
     import paper_1808_04487_b200.veloreg as V
 
     dist = None
-    if world > 1:
+    slabs = world > 1 or args.force_slabs
+    single = not slabs
+    if slabs:
         import torch.distributed as dist
         torch.cuda.set_device(local)
+        if "MASTER_ADDR" not in os.environ:  # --force-slabs outside torchrun: a one-rank group
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = local
@@ -528,7 +536,7 @@ def main():
     model = V.make_model("h2", beta_v=1e-2, nt=nt)
     desc = workload_desc(cid, n, nt)
     scaling, comm_info = "weak", None
-    if world > 1:
+    if slabs:
         # x1 slabs over the ranks (NCCL all-to-all FFT transposes, P2P halos): one global
         # problem split across the GPUs, i.e. strong scaling. No fallback: any failure
         # raises on this rank and torchrun tears the job down.
@@ -747,7 +755,7 @@ def main():
             "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"],
             "stop": reps[-1]["stop_name"], "precond": "spectral", "continuation": "beta_v 1, 1e-1, 1e-2"}
         # the same continuation with the two-level preconditioner; one GPU only
-        if world == 1:
+        if single:
             t2 = []
             for _ in range(6):  # first run: coarse context, plans and pool growth
                 ctx.synchronize()
@@ -764,7 +772,7 @@ def main():
                 "final_mismatch_rel": reps2[-1]["final_mismatch_rel"],
                 "final_grad_rel": reps2[-1]["final_grad_rel"], "stop": reps2[-1]["stop_name"],
                 "precond": "two-level, PCG(0.1) inner on the 128^3 coarse grid"}
-    if not args.no_solve and world == 1:
+    if not args.no_solve and single:
         # config 1: 64^3 analytic problem, GPU vs the reference on the host cores
         ctx1 = vr.Context(64, device=dev)
         mR1, mT1, _ = V.generate_synthetic(ctx1, nt)
@@ -777,7 +785,7 @@ def main():
                             "hessian_matvecs": r1.report["fine"]["hessian_matvecs"],
                             "final_mismatch_rel": r1.report["final_mismatch_rel"],
                             "final_grad_rel": r1.report["final_grad_rel"]}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if rank == 0 and single and not args.no_cpu_baseline:
             try:
                 from oracle import ref
                 ref.set_workers(os.cpu_count() or 1)
@@ -794,7 +802,7 @@ def main():
     # ---- config 4 on one GPU: 512^3 phantom (|k| <= 10), the P = 1 point of the
     # strong-scaling curve; device-resident matvecs timed like the main line -----
     cfg4 = None
-    if world == 1 and not args.no_config4 and n == 256:
+    if single and not args.no_config4 and n == 256:
         from paper_1808_04487_b200 import phantom
         n4 = phantom.CONFIGS[4]["n"]
         m_T4, v4 = phantom.make_config_inputs(4)
@@ -866,17 +874,17 @@ def main():
     # ---- fp32 lane: the same tricubic gathers at the config-3 departure
     # points with fp32 fields / points (fp64 stencil arithmetic), next to the fp64 kernel --
     f32 = None
-    if world == 1 and not args.no_fp32:
+    if single and not args.no_fp32:
         f32 = fp32_block(ctx, V, d_v, d_mT, nt, dev, torch)
 
     # ---- config 2 (128^3 analytic problem): per-operator micro-benchmarks and the full
     # GN solve, GPU (device-resident, CUDA events) next to the reference on the host cores --
     cfg2 = None
-    if world == 1 and not args.no_config2:
+    if single and not args.no_config2:
         cfg2 = config2_block(vr, V, dev, nt, model, torch, with_cpu=not args.no_cpu_baseline)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and single and not args.no_cpu_baseline:
         try:
             m_R_host = d_mR.numpy()
             r = run_reference_matvecs(m_R_host, m_T, v, vt, nt, 1, 0, 60.0)
@@ -897,7 +905,7 @@ def main():
                                                         "note": "separate serialised pass, events per kernel"},
                 "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve,
                 "config4_single_gpu": cfg4, "config2": cfg2, "fp32_lane": f32, "comm": comm,
-                "memory": memory}
+                "memory": memory, "forced_slabs": bool(args.force_slabs)}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -177,7 +177,8 @@ namespace vr {
 // Grid3 checks (grid.hpp:24-31) plus the GPU FFT domain; with a transport of
 // size P > 1 the context owns the x1 slab of rank t->rank
 // x1-slab geometry of rank `rank` of P; host only.
-void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& g) {
+static void slab_geometry_ex(int n1, int n2, int n3, int P, int rank, int halo, GridDims& g,
+                             bool one_rank_slab) {
     const int d[3] = {n1, n2, n3};
     for (int a = 0; a < 3; ++a)
         if (d[a] < 4)
@@ -189,7 +190,8 @@ void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& 
                             std::to_string(n1) + "x" + std::to_string(n2) + "x" +
                             std::to_string(n3));
     if (P < 1 || rank < 0 || rank >= P) throw_argument("x1 slabs: rank must be in [0, nranks)");
-    if (P > 1) {
+    const bool slab = P > 1 || one_rank_slab;  // one-rank slabs: VR_DIST_SINGLE_RANK (self exchanges)
+    if (slab) {
         if (n1 % P != 0 || n2 % P != 0 || n1 / P < 4)
             throw_argument("x1 slabs: n1 and n2 must be divisible by the rank count, >= 4 planes each");
         if (halo < 4 || halo > n1 / P)
@@ -199,12 +201,12 @@ void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& 
     g.n2 = n2;
     g.n3 = n3;
     g.nh = n3 / 2 + 1;
-    g.dist = P > 1;
+    g.dist = slab;
     g.L = n1 / P;
     g.z0 = 0;
     g.zn = g.L;
     g.off1 = rank * g.L;
-    g.halo = P > 1 ? halo : 0;
+    g.halo = slab ? halo : 0;
     g.n2s = n2 / P;
     g.k2_off = rank * g.n2s;
     g.N = static_cast<long long>(g.L) * n2 * n3;
@@ -216,6 +218,10 @@ void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& 
     g.flags = nullptr;
 }
 
+void slab_geometry(int n1, int n2, int n3, int P, int rank, int halo, GridDims& g) {
+    slab_geometry_ex(n1, n2, n3, P, rank, halo, g, false);
+}
+
 int halo_required(double vmax_x1, int nt, int n1) {
     // RK2 departure points move at most dt max|v_1| (+10% for the midpoint
     // interpolant's overshoot) and the stencil reaches 2 planes beyond floor(u) - 1
@@ -224,8 +230,9 @@ int halo_required(double vmax_x1, int nt, int n1) {
 
 vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
     const int P = t ? t->size : 1;
+    const bool slab = t && (P > 1 || std::getenv("VR_DIST_SINGLE_RANK"));
     GridDims geo;
-    slab_geometry(n1, n2, n3, P, P > 1 ? t->rank : 0, halo, geo);
+    slab_geometry_ex(n1, n2, n3, P, slab ? t->rank : 0, halo, geo, slab);
     int count = 0;
     VR_CUDA(cudaGetDeviceCount(&count));
     if (device < 0 || device >= count)
@@ -244,7 +251,7 @@ vr_ctx* ctx_new(int n1, int n2, int n3, int device, Transport* t, int halo) {
     try {
         ctx->device = device;
         VR_CUDA(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
-        ctx->dist = P > 1 ? t : nullptr;
+        ctx->dist = slab ? t : nullptr;
         ctx->overlap = ctx->dist != nullptr;  // slabs: reg-term transposes under the sweeps
         if (const char* e = std::getenv("VR_OVERLAP")) ctx->overlap = std::atoi(e) != 0;
         if (const char* e = std::getenv("VR_FUSE_ACC")) ctx->fuse_acc = std::atoi(e) != 0;

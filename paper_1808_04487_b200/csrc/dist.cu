@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -311,7 +312,9 @@ int vr_ctx_create_dist(int n1, int n2, int n3, int device, int rank, int nranks,
     return dguard([&] {
         if (!out || !uid) vr::throw_argument("vr_ctx_create_dist: null argument");
         if (nranks < 1 || rank < 0 || rank >= nranks) vr::throw_argument("vr_ctx_create_dist: bad rank");
-        if (nranks == 1) {
+        // one rank: a plain context, unless VR_DIST_SINGLE_RANK asks for the slab code over a
+        // one-rank NCCL communicator (self send/recv: a one-GPU check of the multi-GPU plumbing)
+        if (nranks == 1 && !std::getenv("VR_DIST_SINGLE_RANK")) {
             *out = vr::ctx_new(n1, n2, n3, device, nullptr, 0);
             return;
         }

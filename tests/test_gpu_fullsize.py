@@ -6,8 +6,10 @@
   relative L2 <= 1e-10; the beta_v A terms against the exact (long-double) operator, GPU
   error <= 1.5x the reference's (tests/exact.py).
 * the regularisation operator in all three modes at 256^3 and 512^3 against exact.
-* config 2 (128^3) full solve and config 3 (256^3) beta-continuation solve against the
-  reference: Newton iterations +-1, final mismatch and gradient within 1 %.
+* config 2 (128^3) full solve (reference live on the host cores) and config 3 (256^3)
+  beta-continuation solve (reference results from the committed fixture
+  tests/golden/config3_solve.npz; live with VR_LIVE_CONFIG3=1): Newton iterations +-1,
+  final mismatch and gradient within 1 %.
 * config 3 and config 4 (512^3 on one GPU): size-independent properties of the
   GN Hessian -- linearity, symmetry of the Gauss-Newton operator in the weighted
   inner product (test_objective.cpp:186-215), positive semi-definiteness, zero in
@@ -205,24 +207,47 @@ def test_config4_reference_parity(vr, ref, ctx):
     assert no_worse_than_reference(*errs["reg_vs_exact"])
 
 
+def _check_solve_levels(rg, ref_iters, ref_mismatch, ref_grad):
+    assert len(rg) == len(ref_iters)
+    for a, it in zip(rg, ref_iters):
+        assert abs(a["outer_iterations"] - int(it)) <= 1
+    assert abs(rg[-1]["final_mismatch_rel"] - ref_mismatch[-1]) <= 1e-2 * ref_mismatch[-1]
+    assert abs(rg[-1]["final_grad_rel"] - ref_grad[-1]) <= 1e-2 * ref_grad[-1]
+
+
 def test_config3_solve_vs_reference(vr, ref, ctx):
     """Config 3 end to end: beta continuation 1 -> 1e-1 -> 1e-2 on the GPU
-    and in the reference on the host cores (~6.5 min on 16 cores); per level Newton
-    iterations +-1, final mismatch and gradient norm within 1 % (BASELINE north star;
-    proj/src/solver.cpp:154-269)."""
+    against the reference's own solve of the same arrays (proj/src/solver.cpp:154-269): per
+    level Newton iterations +-1, final mismatch and gradient norm within 1 % (BASELINE north
+    star), final velocity equal on the stored sub-grid. The reference solve takes ~6.5 min on
+    16 host cores, so its results are the committed fixture tests/golden/config3_solve.npz
+    (tests/golden/make_config3_solve.py, generated from the compiled reference);
+    VR_LIVE_CONFIG3=1 also runs the reference live on this box's host cores."""
+    import os
     c, n, m_R, m_T, v = _inputs(vr, ctx, 3)
     model, params = vr.make_model(), vr.make_params(eps_opt=1e-2)
     v0 = np.zeros((3, n, n, n))
     vg, rg, _ = vr.parameter_continuation(c, m_R, m_T, v0, model, params)
-    vref, rr, _ = ref.parameter_continuation(m_R, m_T, v0, model, params)
     print("config3 solve GPU", [(r["outer_iterations"], r["final_mismatch_rel"], r["final_grad_rel"]) for r in rg])
-    print("config3 solve REF", [(r["outer_iterations"], r["final_mismatch_rel"], r["final_grad_rel"]) for r in rr])
-    print("config3 solve v rel", rel_l2(vg, vref))
-    assert len(rg) == len(rr)
-    for a, b in zip(rg, rr):
-        assert abs(a["outer_iterations"] - b["outer_iterations"]) <= 1
-    assert abs(rg[-1]["final_mismatch_rel"] - rr[-1]["final_mismatch_rel"]) <= 1e-2 * rr[-1]["final_mismatch_rel"]
-    assert abs(rg[-1]["final_grad_rel"] - rr[-1]["final_grad_rel"]) <= 1e-2 * rr[-1]["final_grad_rel"]
+    gold = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config3_solve.npz"))
+    print("config3 solve REF (fixture)", list(zip(gold["outer_iterations"], gold["final_mismatch_rel"],
+                                                  gold["final_grad_rel"])))
+    # same problem: the reference's transported image equals the GPU's on the stored sub-grid
+    assert rel_l2(m_R[::8, ::8, ::8], gold["m_R_sub8"]) <= 1e-10
+    _check_solve_levels(rg, gold["outer_iterations"], gold["final_mismatch_rel"], gold["final_grad_rel"])
+    for a, st in zip(rg, gold["stop"]):
+        assert a["stop"] == int(st)
+    dv = rel_l2(vg[:, ::8, ::8, ::8], gold["v_sub8"])
+    print("config3 solve v rel (sub-grid)", dv)
+    assert dv <= 1e-8
+    assert abs(np.linalg.norm(vg.ravel()) - float(gold["v_norm"])) <= 1e-8 * float(gold["v_norm"])
+    if os.environ.get("VR_LIVE_CONFIG3"):
+        vref, rr, _ = ref.parameter_continuation(m_R, m_T, v0, model, params)
+        print("config3 solve REF (live)", [(r["outer_iterations"], r["final_mismatch_rel"], r["final_grad_rel"]) for r in rr])
+        print("config3 solve v rel", rel_l2(vg, vref))
+        _check_solve_levels(rg, [r["outer_iterations"] for r in rr], [r["final_mismatch_rel"] for r in rr],
+                            [r["final_grad_rel"] for r in rr])
+        assert rel_l2(vg, vref) <= 1e-8
 
 
 def test_config2_solve_vs_reference(vr, ref, ctx):

@@ -78,3 +78,55 @@ def test_nccl_slabs_match_single_gpu(vr, ref, ctx):
     assert out[0][5] == r1.report["outer_iterations"]
     assert abs(out[0][6] - r1.report["final_mismatch_rel"]) <= 1e-10
     assert rel_l2(vsol, r1.v) < 1e-10
+
+
+def test_nccl_single_rank_slab_matches_single_gpu(vr, ref, ctx, monkeypatch):
+    """One rank over the REAL NCCL transport (runs on a one-GPU box): NCCL loaded with dlopen,
+    communicator from a unique id, the split side-stream communicator, grouped send/recv
+    all-to-all and halo exchange (with itself: the periodic wrap), rank-ordered reductions --
+    the plumbing a multi-GPU launch uses -- against the plain single-GPU context."""
+    dims = (32, 32, 32)
+    mR, mT, vs = ref.generate_synthetic(dims, 4)
+    v = 0.8 * vs + 0.05 * ref.random_smooth_vector(dims, 2, 11, 1.0)
+    vt = ref.random_smooth_vector(dims, 2, 142, 1.0)
+    c = ctx(dims)
+    o = vr.Objective(c, mR, mT, vr.make_model())
+    s = o.evaluate(v)
+    o.compute_gradient(s)
+    hv1 = np.asarray(o.hessian_matvec(s, vt))
+    r1 = vr.gauss_newton_solve(c, mR, mT, np.zeros_like(v), vr.make_model(), vr.make_params(eps_opt=1e-2))
+    monkeypatch.setenv("VR_DIST_SINGLE_RANK", "1")  # keep the slab code + NCCL at one rank
+    d = vr.DistContext(dims, 0, 1, vr.nccl_unique_id(), device=0, halo=8)
+    od = vr.Objective(d, mR, mT, vr.make_model())
+    sd = od.evaluate(v)
+    od.compute_gradient(sd)
+    hvd = np.asarray(od.hessian_matvec(sd, vt))
+    rd = vr.gauss_newton_solve(d, mR, mT, np.zeros_like(v), vr.make_model(), vr.make_params(eps_opt=1e-2))
+    assert abs(sd.objective - s.objective) <= 1e-12 * abs(s.objective)
+    assert rel_l2(np.asarray(sd.gradient), s.gradient) < 1e-12
+    assert rel_l2(hvd, hv1) < 1e-12
+    assert rd.report["outer_iterations"] == r1.report["outer_iterations"]
+    assert rel_l2(np.asarray(rd.v), r1.v) < 1e-10
+
+
+def test_bench_multi_gpu_path_on_one_rank():
+    """bench.py --force-slabs: the code path a torchrun launch takes (torch.distributed NCCL
+    group, per-slab input generation, halo from the velocity, DistContext over NCCL, exchange
+    timing, e2e with host buffers, slab solve) with world size 1 at a small grid."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VR_DIST_SINGLE_RANK="1")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--force-slabs", "--n", "64",
+                        "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["forced_slabs"] and line["scaling"] == "strong" and line["value"] > 0
+    assert line["comm"] is not None and line["comm"]["halo_planes"] >= 4
+    assert line["comm"]["total_ms_per_matvec"] > 0 and "comm_halo" in line["comm"]["by_kind_ms_per_matvec"]
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    assert line["gn_solve"] and line["gn_solve"]["config3"]["newton_iterations"]
