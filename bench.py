@@ -53,6 +53,13 @@ def parse():
                     help="wall budget for the reference arm's timed matvecs")
     ap.add_argument("--no-ref-detail", action="store_true",
                     help="reference arm: skip the FFT split, 1-worker timing and the CPU GN solves")
+    ap.add_argument("--ref-solve3", action="store_true",
+                    help="reference arm: also run the reference's config-3 beta-continuation solve "
+                         "(~6.5 min on 16 cores; its record is profiles/r02_bench_reference.json and "
+                         "the fixture tests/golden/config3_solve.npz)")
+    ap.add_argument("--ref-sample-n", type=int, default=256,
+                    help="reference arm: largest grid the CPU reference is timed on; a larger config is "
+                         "timed on this sub-grid of the same workload and scaled by the point ratio")
     ap.add_argument("--no-solve", action="store_true", help="skip the GN solve timings")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-lane gather micro-benchmark")
     ap.add_argument("--no-config2", action="store_true",
@@ -210,7 +217,7 @@ def run_reference_matvecs(m_R, m_T, v, vt, nt, steps, warmup, budget_s):
             "setup_s": setup}
 
 
-def reference_detail(m_T, v, vt, m_R, nt, n, with_solves=True):
+def reference_detail(m_T, v, vt, m_R, nt, n, with_solves=True, with_config3=False):
     """BASELINE.md section 3 for the reference CPU arm (same box, same run): the shim-FFT
     time split at the bench grid, 1-worker vs all-worker matvec at 128^3 (a bounded sample),
     and the reference's full GN solves at configs 1-3 (config 3: beta continuation)."""
@@ -265,12 +272,18 @@ def reference_detail(m_T, v, vt, m_R, nt, n, with_solves=True):
             _, rep, _ = ref.gauss_newton_solve(a, b, np.zeros((3,) + a.shape), model, p)
             solves[name] = {"seconds": time.perf_counter() - t0, "newton_iterations": rep["outer_iterations"],
                             "final_mismatch_rel": rep["final_mismatch_rel"]}
-        p = _ref_params(ref)
-        t0 = time.perf_counter()
-        _, reps, _ = ref.parameter_continuation(m_R, m_T, np.zeros_like(v), model, p)
-        solves[f"config3_{n}_beta_continuation"] = {
-            "seconds": time.perf_counter() - t0, "newton_iterations": [r["outer_iterations"] for r in reps],
-            "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"]}
+        if with_config3:
+            p = _ref_params(ref)
+            t0 = time.perf_counter()
+            _, reps, _ = ref.parameter_continuation(m_R, m_T, np.zeros_like(v), model, p)
+            solves[f"config3_{n}_beta_continuation"] = {
+                "seconds": time.perf_counter() - t0, "newton_iterations": [r["outer_iterations"] for r in reps],
+                "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"]}
+        else:
+            solves[f"config3_{n}_beta_continuation"] = {
+                "seconds": None, "note": "run with --ref-solve3 (393 s on this pool's 16 host cores: "
+                                         "profiles/r02_bench_reference.json; results pinned in "
+                                         "tests/golden/config3_solve.npz)"}
         out["gn_solves"] = solves
     return out
 
@@ -485,6 +498,11 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
+        # bounded sample: configs larger than --ref-sample-n (config 4 / 5 under torchrun) are
+        # timed on the same workload at that grid and scaled by the point ratio (the reference's
+        # cost is linear in N up to the FFT's log factor, so this favours the reference)
+        n_full, n = n, min(n, args.ref_sample_n)
+        scale = (n / n_full) ** 3
         ok, need, have = ref_memory_ok(n)
         if not ok:
             print(json.dumps({"impl": "reference", "unavailable": f"the reference needs ~{need / 2 ** 30:.0f} GiB of "
@@ -497,9 +515,15 @@ def main():
         r = run_reference_matvecs(m_R, m_T, v, vt, nt, args.steps, 0, args.ref_budget_s)
         sample = (f"{r['steps']} GN Hessian matvec(s) at {n}^3 after an untimed evaluate+gradient "
                   f"({r['setup_s']:.1f}s); capped at {args.ref_budget_s:.0f}s")
+        if n != n_full:
+            sample += (f"; the {n_full}^3 workload sampled at {n}^3 (same phantom / velocity parameters), "
+                       f"matvec/s scaled by ({n}/{n_full})^3 = {scale:.4g}")
+            r["value"] *= scale
+            r["seconds"] /= scale
         detail = None
         if not args.no_ref_detail:
-            detail = reference_detail(m_T, v, vt, m_R, nt, n, with_solves=(world == 1))
+            detail = reference_detail(m_T, v, vt, m_R, nt, n, with_solves=(world == 1),
+                                      with_config3=args.ref_solve3)
             f = detail["fft"]
             s_mv = r["seconds"] / r["steps"]
             detail["matvec_s_measured"] = s_mv
@@ -509,7 +533,7 @@ def main():
                 "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * r["seconds"] / r["steps"],
                 "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic", "impl": "reference",
-                "config": bench_config(cid, n, nt, world),
+                "config": bench_config(cid, n_full, nt, world),
                 "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
                                  "sample": sample},
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -316,12 +316,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         "r"(parity)
         : "memory");
 }
-// one 3D box (columns x rows x outer block) global -> shared, completing on `bar`
-__device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* tmap, int x, int y, int z,
+// one 5D box (columns x rows x row groups x peer blocks x outer block) global -> shared,
+// completing on `bar`
+__device__ __forceinline__ void tma_load_5d(void* sdst, const CUtensorMap* tmap, int x, int outer,
                                             unsigned long long* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-        ::"r"(smem_u32(sdst)), "l"(reinterpret_cast<unsigned long long>(tmap)), "r"(x), "r"(y), "r"(z),
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %3, %3, %4}], [%5];"
+        ::"r"(smem_u32(sdst)), "l"(reinterpret_cast<unsigned long long>(tmap)), "r"(x), "r"(0), "r"(outer),
         "r"(smem_u32(bar))
         : "memory");
 }
@@ -353,10 +354,15 @@ __device__ __forceinline__ void mbar_init_pair(unsigned long long* bars) {
 // MODE 2: forward -> i deriv_freq(k) * m.beta -> inverse along this axis: the spectral
 //         derivative of a REAL field viewed as complex pairs (x3 = 2j, 2j+1 as re, im);
 //         i k (Nyquist 0) maps real lines to real lines, so the pair never mixes
-template <int N, int DIR, int MODE>
+// SC (x1 slabs, forward x2 pass): the last stage stores row i of block `ob` straight into the
+//         all-to-all send layout, dst + (i >> sc_shift) * sc_blk + ((ob << sc_shift) + (i & mask)) * inner
+//         (block q = rows [q n2s, (q+1) n2s) of every plane), so the transpose needs no pack copy.
+//         The matching unpack of the inverse direction is done by the tensor map of the loads.
+template <int N, int DIR, int MODE, bool SC>
 __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
     k_fft_axis(const __grid_constant__ CUtensorMap tmap, double2* dst, long long inner, long long outer,
-               long long outer_stride, const double2* __restrict__ tw_g, MultDev m, GridDims g) {
+               long long outer_stride, const double2* __restrict__ tw_g, MultDev m, GridDims g,
+               int sc_shift, long long sc_blk) {
     using C = AxisCfg<N>;
     extern __shared__ __align__(128) double2 smem[];
     double2* tw = smem + 2 * C::STAGE;  // W_N table staged once per CTA (broadcast reads)
@@ -377,10 +383,7 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
     auto issue = [&](long long tile, int b) {
         const long long ob = tile / ncb, c0 = (tile - ob * ncb) * C::TB;
         mbar_expect_tx(full + b, static_cast<unsigned>(C::STAGE * sizeof(double2)));
-#pragma unroll
-        for (int r0 = 0; r0 < N; r0 += C::BOX_ROWS)
-            tma_load_3d(smem + b * C::STAGE + r0 * C::TB, &tmap, static_cast<int>(2 * c0), r0,
-                        static_cast<int>(ob), full + b);
+        tma_load_5d(smem + b * C::STAGE, &tmap, static_cast<int>(2 * c0), static_cast<int>(ob), full + b);
     };
     long long tile = blockIdx.x;
     if (threadIdx.x == 0 && tile < ntiles) issue(tile, 0);
@@ -393,11 +396,15 @@ __global__ void __launch_bounds__(AxisCfg<N>::THREADS, 1)
         const long long ob = tile / ncb;
         const long long cc = (tile - ob * ncb) * C::TB + col;
         const bool valid = cc < inner;
-        double2* d = dst + ob * outer_stride + (valid ? cc : 0);
+        double2* d = dst + (SC ? (ob << sc_shift) * inner : ob * outer_stride) + (valid ? cc : 0);
         auto sm = [&](int i) -> double2& { return buf[i * C::TB + col]; };
         auto load_sm = [&](int i) -> double2 { return sm(i); };
         auto store = [&](int i, double2 v) {
-            if (valid) d[static_cast<long long>(i) * inner] = v;
+            if (!valid) return;
+            if constexpr (SC)
+                d[(i >> sc_shift) * sc_blk + static_cast<long long>(i & ((1 << sc_shift) - 1)) * inner] = v;
+            else
+                d[static_cast<long long>(i) * inner] = v;
         };
         if constexpr (MODE == 0) {
             fft_line<N, DIR, true, false>(t, tw, load_sm, store, sm);
@@ -837,18 +844,37 @@ inline TmapEncodeFn tmap_encoder() {
     }();
     return fn;
 }
+// Row layout of a strided pass's SOURCE: the N rows of one block are Q2 peer blocks of Q1
+// groups of R rows (R <= 256, the box limit per dimension); row r of group q1 of peer block q2
+// sits at (q2 * q2_stride + q1 * R * inner + r * inner) double2 from the block's base. Plain
+// layout: Q2 = 1. All-to-all receive layout on x1 slabs: Q2 = P peer blocks of n2s = Q1 * R
+// rows each, q2_stride = the block size, and consecutive planes n2s * inner apart.
+struct RowGroups {
+    int rows_per_block = 0;      // 0: plain layout (one block of N rows)
+    long long q2_stride = 0;
+    long long outer_stride = 0;  // of the source blocks (0: same as the destination's)
+};
 template <int N>
-CUtensorMap axis_tmap(const double2* src, long long inner, long long outer, long long outer_stride) {
+CUtensorMap axis_tmap(const double2* src, long long inner, long long outer, long long outer_stride,
+                      RowGroups rg) {
     using C = AxisCfg<N>;
+    const int rows = rg.rows_per_block ? rg.rows_per_block : N;
+    const int R = rows < 256 ? rows : 256, Q1 = rows / R, Q2 = N / rows;
+    if (R * Q1 * Q2 != N || Q1 > 256 || Q2 > 256) throw_logic("fft: bad row grouping for the tensor map");
+    if (rg.outer_stride) outer_stride = rg.outer_stride;
     CUtensorMap tm;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * inner), static_cast<cuuint64_t>(N),
+    const cuuint64_t dims[5] = {static_cast<cuuint64_t>(2 * inner), static_cast<cuuint64_t>(R),
+                                static_cast<cuuint64_t>(Q1), static_cast<cuuint64_t>(Q2),
                                 static_cast<cuuint64_t>(outer)};
-    // strides of dimensions 1 and 2 in bytes (dimension 0 is contiguous)
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner) * sizeof(double2),
-                                   static_cast<cuuint64_t>(outer > 1 ? outer_stride : inner * N) * sizeof(double2)};
-    const cuuint32_t box[3] = {2u * C::TB, static_cast<cuuint32_t>(C::BOX_ROWS), 1u};
-    const cuuint32_t estr[3] = {1u, 1u, 1u};
-    const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(src), dims,
+    // strides of dimensions 1..4 in bytes (dimension 0 is contiguous)
+    const cuuint64_t strides[4] = {
+        static_cast<cuuint64_t>(inner) * sizeof(double2), static_cast<cuuint64_t>(R) * inner * sizeof(double2),
+        static_cast<cuuint64_t>(Q2 > 1 ? rg.q2_stride : static_cast<long long>(rows) * inner) * sizeof(double2),
+        static_cast<cuuint64_t>(outer > 1 ? outer_stride : inner * N) * sizeof(double2)};
+    const cuuint32_t box[5] = {2u * C::TB, static_cast<cuuint32_t>(R), static_cast<cuuint32_t>(Q1),
+                               static_cast<cuuint32_t>(Q2), 1u};
+    const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+    const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(src), dims,
                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -857,18 +883,20 @@ CUtensorMap axis_tmap(const double2* src, long long inner, long long outer, long
     return tm;
 }
 
-template <int N, int DIR, int MODE>
+// sc_blk > 0: scatter the stores into all-to-all blocks of sc_blk double2 (rows per block = 1 << sc_shift)
+template <int N, int DIR, int MODE, bool SC = false>
 void launch_axis_t(vr_ctx* ctx, const double2* src, double2* dst, long long inner, long long outer,
-                   long long outer_stride, const double2* tw, const MultDev& m) {
+                   long long outer_stride, const double2* tw, const MultDev& m, RowGroups rg = {},
+                   int sc_shift = 0, long long sc_blk = 0) {
     using C = AxisCfg<N>;
     static int occ[64] = {0};
     const long long ntiles = (inner + C::TB - 1) / C::TB * outer;
     const unsigned grid =
-        persistent_grid(ctx, k_fft_axis<N, DIR, MODE>, C::THREADS, C::SMEM, ntiles, occ);
-    const CUtensorMap tm = axis_tmap<N>(src, inner, outer, outer_stride);
+        persistent_grid(ctx, k_fft_axis<N, DIR, MODE, SC>, C::THREADS, C::SMEM, ntiles, occ);
+    const CUtensorMap tm = axis_tmap<N>(src, inner, outer, outer_stride, rg);
     VR_LAUNCH(ctx, MODE == 0 ? "fft_axis" : (MODE == 1 || MODE == 3 ? "fft_x1_mult" : "fft_deriv"),
-              k_fft_axis<N, DIR, MODE><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
-                  tm, dst, inner, outer, outer_stride, tw, m, ctx->g));
+              k_fft_axis<N, DIR, MODE, SC><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+                  tm, dst, inner, outer, outer_stride, tw, m, ctx->g, sc_shift, sc_blk));
 }
 
 template <int DIR, int MODE>
@@ -1041,6 +1069,68 @@ void pass_x2(vr_ctx* ctx, double* spec, int dir) {
         launch_axis<-1, 0>(ctx, g.n2, s, s, g.nh, g.L, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
     else
         launch_axis<+1, 0>(ctx, g.n2, s, s, g.nh, g.L, (long long)g.n2 * g.nh, ctx->fft->tw2, none);
+}
+namespace {
+int ilog2(int v) {
+    int s = 0;
+    while ((1 << s) < v) ++s;
+    return s;
+}
+}  // namespace
+// x1 slabs: forward x2 pass of the slab spectrum [L][n2][nh], stored straight into the
+// all-to-all send layout (block q = [L][n2s][nh], the k2 rows of rank q)
+void pass_x2_to_blocks(vr_ctx* ctx, const double* slab, double* send) {
+    const GridDims& g = ctx->g;
+    const auto* s = reinterpret_cast<const double2*>(slab);
+    auto* d = reinterpret_cast<double2*>(send);
+    MultDev none{};
+    const long long blk = static_cast<long long>(g.L) * g.n2s * g.nh;
+    const int sh = ilog2(g.n2s);
+    switch (g.n2) {
+#define VR_CASE(NN)                                                                                  \
+    case NN:                                                                                         \
+        launch_axis_t<NN, -1, 0, true>(ctx, s, d, g.nh, g.L, (long long)g.n2 * g.nh, ctx->fft->tw2, none, \
+                                       RowGroups{}, sh, blk);                                       \
+        break;
+        VR_CASE(4)
+        VR_CASE(8)
+        VR_CASE(16)
+        VR_CASE(32)
+        VR_CASE(64)
+        VR_CASE(128)
+        VR_CASE(256)
+        VR_CASE(512)
+        VR_CASE(1024)
+#undef VR_CASE
+        default: throw_dimension("fft: unsupported axis length " + std::to_string(g.n2));
+    }
+}
+// x1 slabs: inverse x2 pass reading the all-to-all receive layout (block q = [L][n2s][nh] from
+// rank q) through a tensor map whose row groups are the peer blocks, into the slab [L][n2][nh]
+void pass_x2_from_blocks(vr_ctx* ctx, const double* recv, double* slab) {
+    const GridDims& g = ctx->g;
+    const auto* s = reinterpret_cast<const double2*>(recv);
+    auto* d = reinterpret_cast<double2*>(slab);
+    MultDev none{};
+    const long long blk = static_cast<long long>(g.L) * g.n2s * g.nh;
+    const RowGroups rg{g.n2s, blk, static_cast<long long>(g.n2s) * g.nh};
+    switch (g.n2) {
+#define VR_CASE(NN)                                                                                   \
+    case NN:                                                                                          \
+        launch_axis_t<NN, +1, 0>(ctx, s, d, g.nh, g.L, (long long)g.n2 * g.nh, ctx->fft->tw2, none, rg);  \
+        break;
+        VR_CASE(4)
+        VR_CASE(8)
+        VR_CASE(16)
+        VR_CASE(32)
+        VR_CASE(64)
+        VR_CASE(128)
+        VR_CASE(256)
+        VR_CASE(512)
+        VR_CASE(1024)
+#undef VR_CASE
+        default: throw_dimension("fft: unsupported axis length " + std::to_string(g.n2));
+    }
 }
 void pass_x1(vr_ctx* ctx, const double* src, double* dst, int dir, const MultParams* mult) {
     const GridDims& g = ctx->g;

@@ -198,7 +198,13 @@ template <class Launch>
 void step_with_halo(vr_ctx* ctx, double* src, Launch&& launch) {
     GridDims& g = ctx->g;
     const int L = g.L, H = g.halo;
-    if (!ctx->dist || !ctx->overlap || !ctx->dist->side_stream_ok() || ctx->profiling || L <= 2 * H) {
+    // VR_OVERLAP_HALO=0/1 overrides the context's overlap switch for this mechanism alone
+    static const int halo_env = [] {
+        const char* e = std::getenv("VR_OVERLAP_HALO");
+        return e ? std::atoi(e) : -1;
+    }();
+    const bool overlap = halo_env < 0 ? ctx->overlap : halo_env != 0;
+    if (!ctx->dist || !overlap || !ctx->dist->side_stream_ok() || ctx->profiling || L <= 2 * H) {
         exchange(ctx, src);
         launch();
         return;

@@ -6,8 +6,9 @@
 //           needs whole x1 columns, so an all-to-all transposes the slab into the
 //           k2-slab [n1][n2s][nh] (rank r keeps k2 in [r n2s, (r+1) n2s)), the x1
 //           kernel runs there (the multiplier decodes global k2 via k2_off), and a
-//           second all-to-all transposes back. Blocks to/from rank q are packed
-//           with 2D copies (one per peer), so the x1 layout needs no unpacking.
+//           second all-to-all transposes back. The forward x2 pass stores straight into
+//           the send blocks and the inverse x2 pass reads the received blocks through a
+//           tensor map (TMA), so neither direction has a pack / unpack copy.
 #include "vr_common.cuh"
 
 namespace vr {
@@ -20,28 +21,24 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 // doubles in one complex row block [n2s][nh]
 size_t row_block(const GridDims& g) { return static_cast<size_t>(g.n2s) * g.nh * 2; }
 
-// slab [L][n2][nh] -> x1 layout [n1][n2s][nh]
-void transpose_to_x1(vr_ctx* ctx, const double* slab, double* xl) {
+// x1 slabs: forward x2 pass of the slab spectrum `slab` ([L][n2][nh], after the row pass) and
+// the transpose into the x1 layout `xl` ([n1][n2s][nh]). The x2 pass stores straight into the
+// all-to-all send blocks (no pack copy); the received blocks ARE the x1 layout.
+void x2_forward_to_x1(vr_ctx* ctx, const double* slab, double* xl) {
     const GridDims& g = ctx->g;
-    const size_t row = row_block(g), pitch = static_cast<size_t>(g.n2) * g.nh * 2;
     double* send = sbuf(ctx, 7);
-    for (int q = 0; q < ctx->dist->size; ++q)
-        VR_CUDA(cudaMemcpy2DAsync(send + q * g.L * row, row * sizeof(double), slab + q * row,
-                                  pitch * sizeof(double), row * sizeof(double), g.L,
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
-    ctx->dist->alltoall(ctx, send, xl, g.L * row);
+    pass_x2_to_blocks(ctx, slab, send);
+    ctx->dist->alltoall(ctx, send, xl, g.L * row_block(g));
 }
 
-// x1 layout [n1][n2s][nh] -> slab [L][n2][nh]
-void transpose_from_x1(vr_ctx* ctx, const double* xl, double* slab) {
+// x1 layout `xl` -> transpose back -> inverse x2 pass into the slab spectrum `slab`. The x1
+// layout is already the send blocks; the x2 pass reads the received blocks through a tensor
+// map whose row groups are the peer blocks (no unpack copy).
+void x1_to_x2_inverse(vr_ctx* ctx, const double* xl, double* slab) {
     const GridDims& g = ctx->g;
-    const size_t row = row_block(g), pitch = static_cast<size_t>(g.n2) * g.nh * 2;
     double* recv = sbuf(ctx, 7);
-    ctx->dist->alltoall(ctx, xl, recv, g.L * row);
-    for (int q = 0; q < ctx->dist->size; ++q)
-        VR_CUDA(cudaMemcpy2DAsync(slab + q * row, pitch * sizeof(double), recv + q * g.L * row,
-                                  row * sizeof(double), row * sizeof(double), g.L,
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->dist->alltoall(ctx, xl, recv, g.L * row_block(g));
+    pass_x2_from_blocks(ctx, recv, slab);
 }
 
 double inv_n(const GridDims& g) { return 1.0 / static_cast<double>(g.Ng); }
@@ -62,16 +59,16 @@ MultParams reg_mult(const vr_regnorm& norm, int mode, double beta) {
 void scalar_multiplier(vr_ctx* ctx, const double* in, double* s, double* out, const MultParams& mp,
                        const double* add) {
     pass_rows_forward(ctx, in, s);
-    pass_x2(ctx, s, -1);
     if (ctx->dist) {
         double* t = sbuf(ctx, 8);
-        transpose_to_x1(ctx, s, t);
+        x2_forward_to_x1(ctx, s, t);
         pass_x1(ctx, t, t, 0, &mp);
-        transpose_from_x1(ctx, t, s);
+        x1_to_x2_inverse(ctx, t, s);
     } else {
+        pass_x2(ctx, s, -1);
         pass_x1(ctx, s, s, 0, &mp);
+        pass_x2(ctx, s, +1);
     }
-    pass_x2(ctx, s, +1);
     if (out) pass_rows_inverse(ctx, s, out, inv_n(ctx->g), add);
 }
 
@@ -84,8 +81,7 @@ void fft_r2c(vr_ctx* ctx, const double* in, double* spec) {
     if (ctx->dist) {
         double* s = sbuf(ctx, 8);
         pass_rows_forward(ctx, in, s);
-        pass_x2(ctx, s, -1);
-        transpose_to_x1(ctx, s, spec);
+        x2_forward_to_x1(ctx, s, spec);
     } else {
         pass_rows_forward(ctx, in, spec);
         pass_x2(ctx, spec, -1);
@@ -99,9 +95,10 @@ void fft_c2r(vr_ctx* ctx, double* spec, double* out, double scale, const double*
     double* s = spec;
     if (ctx->dist) {
         s = sbuf(ctx, 8);
-        transpose_from_x1(ctx, spec, s);
+        x1_to_x2_inverse(ctx, spec, s);
+    } else {
+        pass_x2(ctx, s, +1);
     }
-    pass_x2(ctx, s, +1);
     pass_rows_inverse(ctx, s, out, scale, add);
 }
 
@@ -121,11 +118,12 @@ void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
     double* s0 = sbuf(ctx, 0);
     double* s1 = sbuf(ctx, 1);
     pass_rows_forward(ctx, f, s0);
-    pass_x2(ctx, s0, -1);
     double* src = s0;
     if (ctx->dist) {
         src = sbuf(ctx, 8);
-        transpose_to_x1(ctx, s0, src);
+        x2_forward_to_x1(ctx, s0, src);
+    } else {
+        pass_x2(ctx, s0, -1);
     }
     for (int a = 0; a < 3; ++a) {
         MultParams mp;
@@ -134,9 +132,10 @@ void op_gradient(vr_ctx* ctx, const double* f, double* out3) {
         double* s = s1;
         if (ctx->dist) {
             s = sbuf(ctx, 2);
-            transpose_from_x1(ctx, s1, s);
+            x1_to_x2_inverse(ctx, s1, s);
+        } else {
+            pass_x2(ctx, s, +1);
         }
-        pass_x2(ctx, s, +1);
         pass_rows_inverse(ctx, s, out3 + a * g.N, inv_n(g), nullptr);
     }
 }

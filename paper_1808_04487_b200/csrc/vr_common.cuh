@@ -315,6 +315,9 @@ void pass_rows_forward(vr_ctx* ctx, const double* in, double* spec);
 void pass_rows_inverse(vr_ctx* ctx, const double* spec, double* out, double scale,
                        const double* add);
 void pass_x2(vr_ctx* ctx, double* spec, int dir);
+// x1 slabs: the x2 passes with the all-to-all pack / unpack fused into their stores / loads
+void pass_x2_to_blocks(vr_ctx* ctx, const double* slab, double* send);
+void pass_x2_from_blocks(vr_ctx* ctx, const double* recv, double* slab);
 // fp32 lane: r2c rows reading fp32; c2r rows writing out = float(add + scale x) (add: fp32 or null)
 void pass_rows_forward_f32(vr_ctx* ctx, const float* in, double* spec);
 void pass_rows_inverse_f32(vr_ctx* ctx, const double* spec, float* out, double scale,

@@ -215,3 +215,17 @@ def test_exact_reg_vs_reference_round_off(ref):
         errs.append(e)
         assert 0 < e < 1e-11
     assert errs[2] > errs[0]
+
+
+def test_config3_solve_fixture():
+    """tests/golden/config3_solve.npz (the reference's config-3 beta continuation, generated by
+    tests/golden/make_config3_solve.py from the compiled reference): three levels, converged,
+    the iteration counts the bench reports for the reference CPU arm."""
+    import os
+    import numpy as np
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config3_solve.npz"))
+    assert int(g["n"]) == 256 and int(g["levels"]) == 3
+    assert g["v_sub8"].shape == (3, 32, 32, 32) and g["m_R_sub8"].shape == (32, 32, 32)
+    assert [int(x) for x in g["outer_iterations"]] == [1, 3, 3]
+    assert 0.5 < float(g["final_mismatch_rel"][-1]) < 0.6 and float(g["final_grad_rel"][-1]) < 0.1
+    assert np.isfinite(g["v_sub8"]).all() and float(g["v_norm"]) > 0
