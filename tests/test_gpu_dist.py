@@ -43,6 +43,23 @@ def test_slab_objective_matches_single_gpu(vr, ref, ctx, P, name, kw):
     assert abs(sc["grad_norm"] - np.linalg.norm(g1)) <= 1e-12 * np.linalg.norm(g1)
 
 
+@pytest.mark.parametrize("dims,P", [((16, 1024, 8), 2), ((32, 512, 4), 4), ((64, 8, 16), 8)])
+def test_slab_transposes_long_and_short_k2_blocks(vr, ref, ctx, dims, P):
+    """The fused all-to-all layouts at their limits: n2/P = 512 rows per peer block (two
+    256-row groups per block in the tensor map of the inverse x2 pass), 128 rows on four
+    ranks, and one row per rank; the regularisation operator and the objective's spectral
+    terms against the single-GPU path."""
+    mR, mT, vs = ref.generate_synthetic(dims, 4)
+    v = 0.5 * vs
+    vt = ref.random_smooth_vector(dims, 2, 142, 1.0)
+    model = vr.make_model()
+    s, g1, hv1, reg1 = _single(vr, ctx(dims), mR, mT, v, vt, model)
+    g, hv, reg, sc = vr.dist_selftest_objective(P, mR, mT, v, vt, model, halo=8)
+    assert rel_l2(reg, reg1) < 1e-13
+    assert rel_l2(g, g1) < 1e-12
+    assert rel_l2(hv, hv1) < 1e-12
+
+
 def test_slab_objective_config3_like(vr, ctx):
     from paper_1808_04487_b200 import phantom
     n = 64

@@ -12,9 +12,12 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-10
 GRIDS = [(16, 16, 16), (8, 16, 32), (32, 8, 16), (64, 64, 64), (4, 4, 4)]
+# the longest supported axis in every position (1024: four 256-row groups per TMA box and
+# 2-column tiles in the strided passes, M = 512 row transforms) and 512 (two row groups)
+LONG_AXES = [(1024, 4, 8), (4, 1024, 8), (8, 4, 1024), (512, 8, 4), (4, 512, 16)]
 
 
-@pytest.mark.parametrize("dims", GRIDS)
+@pytest.mark.parametrize("dims", GRIDS + LONG_AXES)
 def test_fft_r2c_c2r(vr, ref, ctx, dims):
     c = ctx(dims)
     f = ref.random_rough_scalar(dims, 11)
@@ -28,7 +31,7 @@ def test_fft_r2c_c2r(vr, ref, ctx, dims):
     assert rel_l2(back_gpu, f) < 1e-13
 
 
-@pytest.mark.parametrize("dims", [(16, 16, 16), (8, 16, 32), (64, 32, 16)])
+@pytest.mark.parametrize("dims", [(16, 16, 16), (8, 16, 32), (64, 32, 16)] + LONG_AXES)
 def test_gradient_divergence_laplacian(vr, ref, ctx, dims):
     c = ctx(dims)
     f = ref.random_smooth_scalar(dims, 3, 5, 1.0) + 0.1 * ref.random_rough_scalar(dims, 6)
