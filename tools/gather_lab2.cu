@@ -13,6 +13,7 @@
 //
 // build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo
 //        -Xptxas -v tools/gather_lab2.cu -o /tmp/gather_lab2
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -34,6 +35,7 @@ constexpr double kTwoPi = 6.283185307179586476925286766559;
 struct G {
     int n;
     double h;
+    int skip_fallback = 0;
 };
 
 __device__ __forceinline__ void cubic_weights(double s, double* w) {
@@ -217,6 +219,163 @@ __global__ void __launch_bounds__(4 * T2 * T3, MINB)
     if (c == 0) out[i] = acc;
 }
 
+
+// ---------------------------------------------------------------- variant T (TMA stencil box)
+// Persistent CTAs walk T1 x T2 x 32 tiles. Per tile ONE cp.async.bulk.tensor 3D box
+// (BX1 x BX2 x BW doubles at the tile's stencil origin, two stages, mbarrier) stages the
+// union of the tile's stencils in shared memory; the points gather with LDS.64. Tiles whose
+// stencils leave the box or cross the periodic boundary take A's L1 path.
+__device__ __forceinline__ int near_img(int b, int i, int n) {
+    int d = b - i;
+    d = ((d + n / 2) & (n - 1)) - n / 2;
+    return i + d;
+}
+template <int T1, int T2>
+__global__ void k_tile_boxes(const double* __restrict__ X, G g, int4* __restrict__ org, int bx1, int bx2, int bw) {
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int tiles3 = n / 32, tiles2 = n / T2;
+    const int t = blockIdx.x;
+    const int t3 = t % tiles3, t2 = (t / tiles3) % tiles2, t1 = t / (tiles3 * tiles2);
+    int mn[3] = {1 << 29, 1 << 29, 1 << 29}, mx[3] = {-(1 << 29), -(1 << 29), -(1 << 29)};
+    for (int p = threadIdx.x; p < T1 * T2 * 32; p += blockDim.x) {
+        const int l3 = p & 31, r = p >> 5;
+        const int i1 = t1 * T1 + r / T2, i2 = t2 * T2 + r % T2, i3 = t3 * 32 + l3;
+        const long long i = ((long long)i1 * n + i2) * n + i3;
+        const int own[3] = {i1, i2, i3};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            int b;
+            axis_frac(__ldg(X + c * N + i), g.h, b);
+            b = near_img(b, own[c], n);
+            mn[c] = min(mn[c], b);
+            mx[c] = max(mx[c], b);
+        }
+    }
+    __shared__ int smn[3][32], smx[3][32];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        int a = mn[c], z = mx[c];
+        for (int o = 16; o; o >>= 1) {
+            a = min(a, __shfl_xor_sync(~0u, a, o));
+            z = max(z, __shfl_xor_sync(~0u, z, o));
+        }
+        if ((threadIdx.x & 31) == 0) smn[c][threadIdx.x >> 5] = a, smx[c][threadIdx.x >> 5] = z;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a[3], z[3];
+        for (int c = 0; c < 3; ++c) {
+            a[c] = smn[c][0], z[c] = smx[c][0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a[c] = min(a[c], smn[c][w]), z[c] = max(z[c], smx[c][w]);
+        }
+        const int o3 = a[2] & ~1;  // 16-byte aligned box rows
+        const bool fits = z[0] + 4 - a[0] <= bx1 && z[1] + 4 - a[1] <= bx2 && z[2] + 4 - o3 <= bw;
+        const bool inside = a[0] >= 0 && z[0] + 4 <= n && a[1] >= 0 && z[1] + 4 <= n && o3 >= 0 && z[2] + 4 <= n;
+        org[t] = make_int4(a[0], a[1], o3, fits && inside ? 1 : 0);
+    }
+}
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait_t(unsigned long long* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.b32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(su32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+template <int T1, int T2, int BX1, int BX2, int BW, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_gather_T(const __grid_constant__ CUtensorMap tmap, const double* __restrict__ f, const double* __restrict__ X,
+               double* __restrict__ out, G g, const int4* __restrict__ org, int ntiles) {
+    constexpr int STAGE = BX1 * BX2 * BW;  // doubles
+    extern __shared__ __align__(128) double sm[];
+    __shared__ unsigned long long bar[2];
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int tiles3 = n / 32, tiles2 = n / T2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar[s])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int t, int s) {
+        const int4 o = org[t];
+        if (!o.w) return;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bar[s])),
+                     "r"((unsigned)(STAGE * 8))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+            ::"r"(su32(sm + s * STAGE)), "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(o.z), "r"(o.y),
+            "r"(o.x), "r"(su32(&bar[s]))
+            : "memory");
+    };
+    int t = blockIdx.x;
+    if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
+    unsigned ph[2] = {0, 0};
+    for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+        const int s = k & 1;
+        const int tn = t + gridDim.x;
+        if (threadIdx.x == 0 && tn < ntiles) issue(tn, s ^ 1);
+        const int4 o = org[t];
+        if (o.w) {
+            mbar_wait_t(&bar[s], ph[s]);
+            ph[s] ^= 1;
+        }
+        const double* box = sm + s * STAGE;
+        const int t3 = t % tiles3, t2 = (t / tiles3) % tiles2, t1 = t / (tiles3 * tiles2);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+        for (int r = warp; r < T1 * T2; r += THREADS / 32) {
+            const int i1 = t1 * T1 + r / T2, i2 = t2 * T2 + r % T2, i3 = t3 * 32 + lane;
+            const long long i = ((long long)i1 * n + i2) * n + i3;
+            int b[3];
+            double w[3][4];
+            axis_stencil(__ldg(X + i), g.h, b[0], w[0]);
+            axis_stencil(__ldg(X + N + i), g.h, b[1], w[1]);
+            axis_stencil(__ldg(X + 2 * N + i), g.h, b[2], w[2]);
+            double acc = 0.0;
+            if (o.w) {
+                const int r1 = near_img(b[0], i1, n) - o.x, r2 = near_img(b[1], i2, n) - o.y,
+                          r3 = near_img(b[2], i3, n) - o.z;
+                const double* sb = box + (r1 * BX2 + r2) * BW + r3;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    double acc1 = 0.0;
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const double* p = sb + (a * BX2 + bb) * BW;
+                        double acc2 = 0.0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc2 += w[2][c] * p[c];
+                        acc1 += w[1][bb] * acc2;
+                    }
+                    acc += w[0][a] * acc1;
+                }
+            } else {
+                if (g.skip_fallback) continue;  // lab: time the staged tiles alone
+                acc = gather_l1(f, n, b, w);
+            }
+            out[i] = acc;
+        }
+        __syncthreads();  // everyone is done with this stage before the copy engine refills it
+    }
+}
+
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encoder() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    return reinterpret_cast<TmapEncodeFn>(p);
+}
+
 // ---------------------------------------------------------------- driver
 static std::vector<double> readf(const char* p, size_t cnt) {
     std::vector<double> v(cnt);
@@ -283,6 +442,55 @@ static void run_H4(const double* d_f, const double* d_X, double* d_out, G g, con
     compare(nm, time_it(l, 20), ref, d_out, N);
 }
 
+
+template <int T1, int T2, int BX1, int BX2, int BW, int THREADS, int MINB>
+static void run_T(const double* d_f, const double* d_X, double* d_out, G g, const std::vector<double>& ref) {
+    const int n = g.n;
+    const long long N = (long long)n * n * n;
+    const int ntiles = (n / T1) * (n / T2) * (n / 32);
+    int4* org;
+    CK(cudaMalloc(&org, ntiles * sizeof(int4)));
+    auto boxes = [&] { k_tile_boxes<T1, T2><<<ntiles, 256>>>(d_X, g, org, BX1, BX2, BW); };
+    float ms_box = time_it(boxes, 5);
+    std::vector<int4> ho(ntiles);
+    CK(cudaMemcpy(ho.data(), org, ntiles * sizeof(int4), cudaMemcpyDeviceToHost));
+    int staged = 0;
+    for (auto& o : ho) staged += o.w;
+    CUtensorMap tm;
+    const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)n};
+    const cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)n * n * 8};
+    const cuuint32_t box[3] = {BW, BX2, BX1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)d_f, dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        fprintf(stderr, "tensor map encode failed %d\n", (int)r);
+        exit(1);
+    }
+    const size_t smem = 2ull * BX1 * BX2 * BW * 8;
+    auto kern = k_gather_T<T1, T2, BX1, BX2, BW, THREADS, MINB>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int sms, occ = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, smem));
+    const int grid = sms * std::max(1, std::min(occ, MINB));
+    auto launch = [&] { kern<<<grid, THREADS, smem>>>(tm, d_f, d_X, d_out, g, org, ntiles); };
+    CK(cudaMemset(d_out, 0, N * 8));
+    char nm[200];
+    float ms = time_it(launch, 20);
+    snprintf(nm, sizeof nm, "T tma-box T%dx%dx32 box%dx%dx%d thr%d occ%d smemKB%zu staged%.3f boxes_ms%.3f", T1, T2,
+             BX1, BX2, BW, THREADS, occ, smem / 1024, (double)staged / ntiles, ms_box);
+    compare(nm, ms, ref, d_out, N);
+    G g2 = g;
+    g2.skip_fallback = 1;
+    auto launch2 = [&] { kern<<<grid, THREADS, smem>>>(tm, d_f, d_X, d_out, g2, org, ntiles); };
+    float ms2 = time_it(launch2, 20);
+    printf("{\"variant\": \"%s staged tiles only\", \"ms\": %.4f, \"ms_per_full_grid_equiv\": %.4f}\n", nm, ms2,
+           ms2 / ((double)staged / ntiles));
+    cudaFree(org);
+}
+
 int main(int argc, char** argv) {
     const int n = argc > 1 ? atoi(argv[1]) : 256;
     const char* xp = argc > 2 ? argv[2] : "/tmp/lab_X.bin";
@@ -309,6 +517,17 @@ int main(int argc, char** argv) {
     std::vector<double> ref(N);
     CK(cudaMemcpy(ref.data(), d_out, N * 8, cudaMemcpyDeviceToHost));
     printf("{\"variant\": \"A l1 1x4x32\", \"ms\": %.4f}\n", msA);
+    if (getenv("LAB_T")) {
+        run_T<2, 4, 8, 12, 48, 256, 3>(d_f, d_X, d_out, g, ref);
+        run_T<1, 4, 8, 12, 48, 128, 3>(d_f, d_X, d_out, g, ref);
+        run_T<1, 4, 6, 10, 48, 128, 4>(d_f, d_X, d_out, g, ref);
+        run_T<2, 2, 8, 8, 48, 128, 4>(d_f, d_X, d_out, g, ref);
+        run_T<2, 4, 8, 10, 48, 256, 3>(d_f, d_X, d_out, g, ref);
+        run_T<2, 4, 7, 10, 40, 256, 4>(d_f, d_X, d_out, g, ref);
+        run_T<2, 4, 8, 12, 48, 128, 3>(d_f, d_X, d_out, g, ref);
+        run_T<4, 4, 10, 10, 48, 512, 2>(d_f, d_X, d_out, g, ref);
+        return 0;
+    }
     // 2 lanes per point: tile / occupancy / split / lane-map sweep
     run_H<4, 32, 4, 0, 0>(d_f, d_X, d_out, g, ref);
     run_H<4, 32, 4, 1, 0>(d_f, d_X, d_out, g, ref);
