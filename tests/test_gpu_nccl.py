@@ -96,7 +96,11 @@ def test_nccl_single_rank_slab_matches_single_gpu(vr, ref, ctx, monkeypatch):
     hv1 = np.asarray(o.hessian_matvec(s, vt))
     r1 = vr.gauss_newton_solve(c, mR, mT, np.zeros_like(v), vr.make_model(), vr.make_params(eps_opt=1e-2))
     monkeypatch.setenv("VR_DIST_SINGLE_RANK", "1")  # keep the slab code + NCCL at one rank
-    d = vr.DistContext(dims, 0, 1, vr.nccl_unique_id(), device=0, halo=8)
+    try:
+        d = vr.DistContext(dims, 0, 1, vr.nccl_unique_id(), device=0, halo=8)
+    except vr.ResourceError as exc:  # no usable NCCL on this box: environmental, not a parity failure
+        pytest.skip(f"NCCL communicator unavailable: {exc}")
+    assert (d.rank, d.nranks, d.planes, d.halo) == (0, 1, dims[0], 8)
     od = vr.Objective(d, mR, mT, vr.make_model())
     sd = od.evaluate(v)
     od.compute_gradient(sd)
@@ -123,8 +127,11 @@ def test_bench_multi_gpu_path_on_one_rank():
     p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--force-slabs", "--n", "64",
                         "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
                        capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    if p.returncode != 0 and "NCCL" in p.stderr and ("unhandled system error" in p.stderr or
+                                                      "not loadable" in p.stderr):
+        pytest.skip("NCCL unavailable on this box: " + p.stderr[-300:])
     assert p.returncode == 0, p.stderr[-2000:]
-    line = json.loads(p.stdout.strip().splitlines()[-1])
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith('{"metric"')][-1])
     assert line["forced_slabs"] and line["scaling"] == "strong" and line["value"] > 0
     assert line["comm"] is not None and line["comm"]["halo_planes"] >= 4
     assert line["comm"]["total_ms_per_matvec"] > 0 and "comm_halo" in line["comm"]["by_kind_ms_per_matvec"]
