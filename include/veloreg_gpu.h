@@ -538,6 +538,14 @@ int vr_dist_selftest_solve(int P, int n1, int n2, int n3, int device, int halo,
                            const vr_model* model, const vr_solver_params* params,
                            const double* m_R, const double* m_T, const double* v0, double* v_out,
                            vr_solve_report* report);
+/* The same with a preconditioner choice (VR_PRECOND_*; tl_opts may be NULL): the two-level
+ * preconditioner on slabs (precond.cpp:153-249 with the coarse grid on a sibling slab context
+ * and the coarse band exchanged between the ranks' k2 slabs) */
+int vr_dist_selftest_solve_precond(int P, int n1, int n2, int n3, int device, int halo,
+                                   const vr_model* model, const vr_solver_params* params, int precond,
+                                   const vr_twolevel_options* tl_opts, const double* m_R,
+                                   const double* m_T, const double* v0, double* v_out,
+                                   vr_solve_report* report);
 
 /* ---- synthetic inputs (synthetic.cpp:10-34) -------------------------------- */
 /* m_T, v* analytic on the grid; m_R = solve_state(m_T, v*, nt).final() on the GPU */

@@ -95,11 +95,22 @@ double* field_buf(vr_ctx* ctx, int i) {
 }
 
 vr_ctx* ctx_new_sibling(vr_ctx* parent, int n1, int n2, int n3) {
-    vr_ctx* c = ctx_new(n1, n2, n3, parent->device, nullptr, 0);
+    // x1 slabs: the sibling is the same ranks' slab of the other grid on the parent's
+    // transport; its halo covers the parent's halo in physical units (+2 planes of slack)
+    int halo = 0;
+    if (parent->dist) {
+        const int L = n1 / parent->dist->size;
+        halo = (parent->g.halo * n1 + parent->g.n1 - 1) / parent->g.n1 + 2;
+        halo = halo < 4 ? 4 : halo;
+        halo = halo > L ? L : halo;
+    }
+    vr_ctx* c = ctx_new(n1, n2, n3, parent->device, parent->dist, halo);
     VR_CUDA(cudaStreamDestroy(c->stream));
     c->stream = parent->stream;
     c->owns_stream = false;
-    c->overlap = parent->overlap;
+    // slab siblings keep every exchange on the shared stream (the side-stream communicator
+    // belongs to the parent's overlapped work)
+    c->overlap = parent->dist ? false : parent->overlap;
     c->fuse_acc = parent->fuse_acc;
     c->parent = parent;
     return c;

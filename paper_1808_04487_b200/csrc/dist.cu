@@ -410,6 +410,15 @@ int vr_dist_selftest_solve(int P, int n1, int n2, int n3, int device, int halo,
                            const vr_model* model, const vr_solver_params* params,
                            const double* mR, const double* mT, const double* v0, double* v_out,
                            vr_solve_report* report) {
+    return vr_dist_selftest_solve_precond(P, n1, n2, n3, device, halo, model, params, VR_PRECOND_SPECTRAL,
+                                          nullptr, mR, mT, v0, v_out, report);
+}
+
+int vr_dist_selftest_solve_precond(int P, int n1, int n2, int n3, int device, int halo,
+                                   const vr_model* model, const vr_solver_params* params, int precond,
+                                   const vr_twolevel_options* tl_opts, const double* mR,
+                                   const double* mT, const double* v0, double* v_out,
+                                   vr_solve_report* report) {
     return dguard([&] {
         const vr_model m = vr::model_or_default(model);
         vr_solver_params p;
@@ -429,7 +438,7 @@ int vr_dist_selftest_solve(int P, int n1, int n2, int n3, int device, int halo,
             for (int c = 0; c < 3; ++c)
                 VR_CUDA(cudaMemcpyAsync(dv + c * N, v0 + c * Ng + off, sizeof(double) * N,
                                         cudaMemcpyHostToDevice, ctx->stream));
-            vr::GnResult r = vr::gauss_newton_solve(ctx, dR, dT, dv, m, p, VR_PRECOND_SPECTRAL, dout);
+            vr::GnResult r = vr::gauss_newton_solve(ctx, dR, dT, dv, m, p, precond, dout, tl_opts);
             for (int c = 0; c < 3; ++c)
                 VR_CUDA(cudaMemcpyAsync(v_out + c * Ng + off, dout + c * N, sizeof(double) * N,
                                         cudaMemcpyDeviceToHost, ctx->stream));

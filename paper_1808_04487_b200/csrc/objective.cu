@@ -392,12 +392,13 @@ static void prepare_adjoint_ctx(vr_objective* o, vr_state* s) {
 vr_state* state_from_history(vr_objective* o, const double* v3, const double* mhist, int nt,
                              const double* lamhist) {
     vr_ctx* ctx = o->ctx;
-    if (ctx->dist) throw_argument("state_from_history: one GPU only");
     const long long N = ctx->g.N;
     auto* s = new vr_state();
     s->obj = o;
     s->nt = nt;
     try {
+        drain_flags(ctx);
+        VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
         s->v = dev_alloc(ctx, 3 * N);
         s->xb = dev_alloc(ctx, 3 * N);
         s->mhist = dev_alloc(ctx, (nt + 1) * ctx->hstride);
@@ -406,7 +407,22 @@ vr_state* state_from_history(vr_objective* o, const double* v3, const double* mh
         for (int j = 0; j <= nt; ++j)
             VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->mhist, j), mhist + j * N, sizeof(double) * N,
                                     cudaMemcpyDeviceToDevice, ctx->stream));
-        sl_trace(ctx, s->v, N, nt, VR_TRACE_BACKWARD, s->xb);
+        if (ctx->dist) {  // as objective_evaluate: halo check, halo-padded gather copy of v
+            const double vmax = max_abs(ctx, v3, N);
+            const int need = halo_required(vmax, nt, ctx->g.n1);
+            if (need > ctx->g.halo)
+                throw_resource("state_from_history: x1 displacement needs a halo of " +
+                               std::to_string(need) + " planes, ctx has " + std::to_string(ctx->g.halo));
+            s->vpad = dev_alloc(ctx, 3 * ctx->hstride);
+            for (int c = 0; c < 3; ++c) {
+                VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->vpad, c), v3 + c * N, sizeof(double) * N,
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+                exchange(ctx, pslice(ctx, s->vpad, c));
+            }
+            sl_trace(ctx, pslice(ctx, s->vpad, 0), ctx->hstride, nt, VR_TRACE_BACKWARD, s->xb);
+        } else {
+            sl_trace(ctx, s->v, N, nt, VR_TRACE_BACKWARD, s->xb);
+        }
         prepare_adjoint_ctx(o, s);
         if (lamhist) {
             s->lamhist = dev_alloc(ctx, (nt + 1) * ctx->hstride);
@@ -414,6 +430,7 @@ vr_state* state_from_history(vr_objective* o, const double* v3, const double* mh
                 VR_CUDA(cudaMemcpyAsync(pslice(ctx, s->lamhist, j), lamhist + j * N,
                                         sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
         }
+        if (ctx->dist) check_flags(ctx, "state_from_history");
     } catch (...) {
         delete s;
         throw;

@@ -12,8 +12,9 @@
 // reference's p -> q -> r order when restricting), plus the existing FFT,
 // transport and BLAS-1 kernels on a coarse sibling context (n/2 per axis) that
 // shares the fine context's stream. The Krylov / Lanczos / Chebyshev control
-// flow is host C++ with the reference's constants. One GPU only (the slab
-// layout does not carry the coarse-band exchange).
+// flow is host C++ with the reference's constants. On x1 slabs the coarse sibling
+// is a slab context on the same transport and the grid transfers exchange the
+// coarse band between the ranks' k2 slabs (resample_scalar_slabs).
 #include <algorithm>
 #include <cmath>
 #include <random>
@@ -135,6 +136,113 @@ void launch_prolong(vr_ctx* ctx, const double* in, SpecGrid s, double* out, Spec
 
 SpecGrid grid_of(const vr_ctx* c) { return spec_grid(c->g.n1, c->g.n2, c->g.n3); }
 
+// ---- x1 slabs: the spectra live in the x1 layout [n1][n2s][nh] (rank r holds the k2 rows
+// [r n2s, (r+1) n2s)), and the coarse rows a rank needs sit on other ranks (coarse row j2 is
+// fine row j2 or j2 + m2, i.e. on the lowest or highest quarter of the fine ranks).
+struct SlabSpec {
+    int n1, n2, n3, nh, n2s, k2_off;
+};
+SlabSpec slab_of(const vr_ctx* c) {
+    return {c->g.n1, c->g.n2, c->g.n3, c->g.nh, c->g.n2s, c->g.k2_off};
+}
+
+// Restriction, sender side: for every coarse bin of every destination rank q, the partial
+// alias sum over the fine bins THIS rank holds (zero when it holds none); the receiver adds
+// the P blocks in rank order. Same alias sets as k_spec_restrict.
+__global__ void k_slab_restrict_pack(const double2* __restrict__ in, SlabSpec s, double2* __restrict__ send,
+                                     SlabSpec d, int P, double scale) {
+    const long long blk = static_cast<long long>(d.n1) * d.n2s * d.nh;
+    const long long nb = blk * P;
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb;
+         b += (long long)gridDim.x * blockDim.x) {
+        const int q = static_cast<int>(b / blk);
+        const long long l = b - q * blk;
+        const int j3 = static_cast<int>(l % d.nh);
+        const int j2 = static_cast<int>((l / d.nh) % d.n2s) + q * d.n2s;
+        const int j1 = static_cast<int>(l / (static_cast<long long>(d.nh) * d.n2s));
+        int k1[2], k2[2], k3[2], c1 = 1, c2 = 1, c3 = 1;
+        const int q1 = sfreq(j1, d.n1), q2 = sfreq(j2, d.n2);
+        k1[0] = q1, k2[0] = q2, k3[0] = j3;
+        if (d.n1 != s.n1 && d.n1 % 2 == 0 && abs(q1) == d.n1 / 2) k1[0] = d.n1 / 2, k1[1] = -d.n1 / 2, c1 = 2;
+        if (d.n2 != s.n2 && d.n2 % 2 == 0 && abs(q2) == d.n2 / 2) k2[0] = d.n2 / 2, k2[1] = -d.n2 / 2, c2 = 2;
+        if (d.n3 != s.n3 && d.n3 % 2 == 0 && j3 == d.n3 / 2) k3[0] = d.n3 / 2, k3[1] = -d.n3 / 2, c3 = 2;
+        double vr = 0.0, vi = 0.0;
+        for (int p = 0; p < c1; ++p)
+            for (int qq = 0; qq < c2; ++qq)
+                for (int r = 0; r < c3; ++r) {
+                    const bool img = k3[r] < 0;  // Hermitian image conj(spec(-k))
+                    const int i1 = wrap_k(img ? -k1[p] : k1[p], s.n1);
+                    const int i2 = wrap_k(img ? -k2[qq] : k2[qq], s.n2) - s.k2_off;
+                    const int i3 = img ? -k3[r] : k3[r];
+                    if (i2 < 0 || i2 >= s.n2s) continue;  // another rank's row
+                    const double2 m = in[(static_cast<long long>(i1) * s.n2s + i2) * s.nh + i3];
+                    vr += m.x;
+                    vi += img ? -m.y : m.y;
+                }
+        send[b] = make_double2(vr * scale, vi * scale);
+    }
+}
+__global__ void k_slab_sum_blocks(const double2* __restrict__ recv, long long blk, int P,
+                                  double2* __restrict__ out) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < blk;
+         b += (long long)gridDim.x * blockDim.x) {
+        double2 a = recv[b];
+        for (int q = 1; q < P; ++q) {
+            const double2 v = recv[q * blk + b];
+            a.x += v.x, a.y += v.y;
+        }
+        out[b] = a;
+    }
+}
+// Prolongation, receiver side: `all` = every rank's coarse slab spectrum in rank order
+// (block t = [m1][m2s][mh]); fine bin k of this rank's k2 rows takes the coarse bin whose
+// alias set contains k. Same rule as k_spec_prolong.
+__global__ void k_slab_prolong(const double2* __restrict__ all, SlabSpec s, double2* __restrict__ out,
+                               SlabSpec d, double scale) {
+    const long long nb = static_cast<long long>(d.n1) * d.n2s * d.nh;
+    const long long blk = static_cast<long long>(s.n1) * s.n2s * s.nh;
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb;
+         b += (long long)gridDim.x * blockDim.x) {
+        const int i3 = static_cast<int>(b % d.nh);
+        const int i2 = static_cast<int>((b / d.nh) % d.n2s) + d.k2_off;
+        const int i1 = static_cast<int>(b / (static_cast<long long>(d.nh) * d.n2s));
+        const int k[3] = {sfreq(i1, d.n1), sfreq(i2, d.n2), i3};
+        const int m[3] = {s.n1, s.n2, s.n3};
+        const int n[3] = {d.n1, d.n2, d.n3};
+        int qi[3], cnt = 1;
+        bool hit = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int ak = abs(k[a]);
+            const int direct = a < 2 ? wrap_k(k[a], m[a]) : k[a];
+            if (m[a] == n[a]) {
+                qi[a] = direct;
+            } else if (m[a] % 2 == 0) {
+                if (ak < m[a] / 2) {
+                    qi[a] = direct;
+                } else if (ak == m[a] / 2) {
+                    qi[a] = m[a] / 2;
+                    cnt *= 2;
+                } else {
+                    hit = false;
+                }
+            } else if (ak <= m[a] / 2) {
+                qi[a] = direct;
+            } else {
+                hit = false;
+            }
+        }
+        double2 v = make_double2(0.0, 0.0);
+        if (hit) {
+            const double w = scale / cnt;
+            const int t = qi[1] / s.n2s, row = qi[1] - t * s.n2s;
+            const double2 c = all[t * blk + (static_cast<long long>(qi[0]) * s.n2s + row) * s.nh + qi[2]];
+            v = make_double2(0.0 + c.x * w, 0.0 + c.y * w);
+        }
+        out[b] = v;
+    }
+}
+
 void need_single(const vr_ctx* c, const char* what) {
     if (c->dist) throw_argument(std::string(what) + ": one GPU only (not on x1 slabs)");
 }
@@ -150,9 +258,64 @@ void order_after(vr_ctx* a, vr_ctx* b) {
 
 // ---------------------------------------------------------------------------
 // spectral_resample (spectral.cpp:340-356), one scalar field per call
+// x1 slabs (both contexts on the same transport): r2c on the source slabs, exchange of the
+// coarse band, c2r on the destination slabs. Restriction: every rank packs, per destination
+// rank, the partial alias sums of the fine rows it holds; one all-to-all; the receiver adds the
+// blocks in rank order. Prolongation: the coarse slab spectra are all-gathered (an all-to-all of
+// P copies; the coarse spectrum is 1/8 of the fine one) and every rank fills its fine rows.
+static void resample_scalar_slabs(vr_ctx* src, const double* in, vr_ctx* dst, double* out) {
+    if (!src->dist || !dst->dist || src->dist != dst->dist)
+        throw_argument("spectral_resample: both contexts must be slabs of one rank group");
+    if (src->stream != dst->stream) throw_argument("spectral_resample: slab contexts must share a stream");
+    const int P = src->dist->size;
+    if (src->g.n1 == dst->g.n1 && src->g.n2 == dst->g.n2 && src->g.n3 == dst->g.n3) {
+        VR_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * src->g.N, cudaMemcpyDeviceToDevice, src->stream));
+        return;
+    }
+    const bool down = dst->g.n1 <= src->g.n1 && dst->g.n2 <= src->g.n2 && dst->g.n3 <= src->g.n3;
+    const bool up = dst->g.n1 >= src->g.n1 && dst->g.n2 >= src->g.n2 && dst->g.n3 >= src->g.n3;
+    if (!down && !up)
+        throw_dimension("spectral_resample: target must be coarser or finer on every axis");
+    double* cs = spec_buf(src, 0);
+    double* cd = spec_buf(dst, 0);
+    fft_r2c(src, in, cs);
+    const double scale = static_cast<double>(dst->g.Ng) / static_cast<double>(src->g.Ng);
+    const vr_ctx* coarse = down ? dst : src;
+    const long long blk = coarse->g.NC;  // complex bins of one coarse slab spectrum
+    double* send = dev_alloc(src, 2 * blk * P);
+    double* recv = dev_alloc(src, 2 * blk * P);
+    try {
+        if (down) {
+            VR_LAUNCH(src, "spec_transfer", k_slab_restrict_pack<<<grid_for(blk * P), 256, 0, src->stream>>>(
+                reinterpret_cast<const double2*>(cs), slab_of(src), reinterpret_cast<double2*>(send),
+                slab_of(dst), P, scale));
+            src->dist->alltoall(src, send, recv, static_cast<size_t>(2 * blk));
+            VR_LAUNCH(src, "spec_transfer", k_slab_sum_blocks<<<grid_for(blk), 256, 0, src->stream>>>(
+                reinterpret_cast<const double2*>(recv), blk, P, reinterpret_cast<double2*>(cd)));
+        } else {
+            for (int q = 0; q < P; ++q)
+                VR_CUDA(cudaMemcpyAsync(send + 2 * blk * q, cs, sizeof(double) * 2 * blk,
+                                        cudaMemcpyDeviceToDevice, src->stream));
+            src->dist->alltoall(src, send, recv, static_cast<size_t>(2 * blk));
+            VR_LAUNCH(src, "spec_transfer", k_slab_prolong<<<grid_for(dst->g.NC), 256, 0, src->stream>>>(
+                reinterpret_cast<const double2*>(recv), slab_of(src), reinterpret_cast<double2*>(cd),
+                slab_of(dst), scale));
+        }
+    } catch (...) {
+        dev_free(src, send);
+        dev_free(src, recv);
+        throw;
+    }
+    dev_free(src, send);
+    dev_free(src, recv);
+    fft_c2r(dst, cd, out, 1.0 / static_cast<double>(dst->g.Ng), nullptr);
+}
+
 void resample_scalar(vr_ctx* src, const double* in, vr_ctx* dst, double* out) {
-    need_single(src, "spectral_resample");
-    need_single(dst, "spectral_resample");
+    if (src->dist || dst->dist) {
+        resample_scalar_slabs(src, in, dst, out);
+        return;
+    }
     if (src->device != dst->device)
         throw_argument("spectral_resample: both contexts must be on one device");
     if (src->g.n1 == dst->g.n1 && src->g.n2 == dst->g.n2 && src->g.n3 == dst->g.n3) {
@@ -292,10 +455,21 @@ std::pair<double, double> lanczos_bounds(vr_ctx* ctx, const DevOp& op, int itera
                                          unsigned long long seed) {
     const long long n3 = 3 * ctx->g.N;
     // seeded start vector, drawn on the host in the reference's order (component, point)
+    // (x1 slabs: every rank draws the global sequence and keeps its planes)
     std::vector<double> h(static_cast<size_t>(n3));
     std::mt19937_64 rng(seed);
     std::uniform_real_distribution<double> uni(-1.0, 1.0);
-    for (auto& x : h) x = uni(rng);
+    if (!ctx->dist) {
+        for (auto& x : h) x = uni(rng);
+    } else {
+        const long long N = ctx->g.N, Ng = ctx->g.Ng;
+        const long long first = static_cast<long long>(ctx->g.off1) * ctx->g.n2 * ctx->g.n3;
+        for (int c = 0; c < 3; ++c)
+            for (long long i = 0; i < Ng; ++i) {
+                const double x = uni(rng);
+                if (i >= first && i < first + N) h[static_cast<size_t>(c * N + (i - first))] = x;
+            }
+    }
     double* q = dev_alloc(ctx, n3);
     double* qp = dev_alloc(ctx, n3);
     double* w = dev_alloc(ctx, n3);
@@ -426,7 +600,6 @@ void TwoLevel::resample_vec(vr_ctx* src, const double* in, vr_ctx* dst, double* 
 
 void TwoLevel::rebuild(vr_objective* fine_obj, const vr_state* fine_state, double eps_H) {
     vr_ctx* f = fine_obj->ctx;
-    need_single(f, "two-level preconditioner");
     const int d[3] = {f->g.n1, f->g.n2, f->g.n3};
     for (int a = 0; a < 3; ++a)
         if (d[a] % 2 != 0 || d[a] / 2 < 4)

@@ -1174,15 +1174,17 @@ def dist_selftest_objective(P, m_R, m_T, v, vt, model=None, halo=8, device=0):
                            vt_H_vt=sc[4])
 
 
-def dist_selftest_solve(P, m_R, m_T, v0, model=None, params=None, halo=8, device=0):
-    """A full GN solve on P virtual slab ranks on one GPU."""
+def dist_selftest_solve(P, m_R, m_T, v0, model=None, params=None, halo=8, device=0, precond="spectral",
+                        two_level=None):
+    """A full GN solve on P virtual slab ranks on one GPU (precond: none / spectral / two_level)."""
     dims = tuple(np.shape(m_R))
     model = model if model is not None else make_model()
     params = params if params is not None else make_params()
     a = [np.ascontiguousarray(x, dtype=np.float64) for x in (m_R, m_T, v0)]
     vout = np.empty((3,) + dims)
     rep = _lib.SolveReport()
-    _lib.call("vr_dist_selftest_solve", P, dims[0], dims[1], dims[2], device, halo,
-              C.byref(model), C.byref(params), *[x.ctypes.data for x in a], vout.ctypes.data,
-              C.byref(rep))
+    pc = {"none": 0, "spectral": 1, "two_level": 2}[precond]
+    _lib.call("vr_dist_selftest_solve_precond", P, dims[0], dims[1], dims[2], device, halo,
+              C.byref(model), C.byref(params), pc, C.byref(two_level) if two_level is not None else None,
+              *[x.ctypes.data for x in a], vout.ctypes.data, C.byref(rep))
     return vout, _report_dict(rep)

@@ -171,3 +171,46 @@ def test_gauss_newton_two_level_solve(vr, ref, ctx, n, inner):
         for a, b in zip(res.records, recs_r):
             assert a["inner_iterations"] == b["inner_iterations"]
             assert a["coarse_matvecs"] == b["coarse_matvecs"]
+
+
+@pytest.mark.parametrize("n,P,inner", [(32, 2, "pcg"), (32, 2, "cheb"), (64, 4, "pcg")])
+def test_two_level_solve_on_slabs_matches_single_gpu(vr, ref, ctx, n, P, inner):
+    """The two-level preconditioner on x1 slabs (P virtual ranks on one GPU): the coarse grid
+    on a sibling slab context, the coarse band exchanged between the ranks' k2 slabs
+    (restriction: per-destination partial alias sums + all-to-all; prolongation: all-gathered
+    coarse spectra), the Lanczos start vector cut from the global seeded sequence -- against
+    the single-GPU two-level solve, itself pinned to the reference (precond.cpp:153-249)."""
+    dims = (n, n, n)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model = vr.make_model("h2", beta_v=1e-2, nt=4)
+    params = vr.make_params(eps_opt=1e-2)
+    opts = vr.make_twolevel_options(inner=inner)
+    v0 = np.zeros((3,) + dims)
+    one = vr.gauss_newton_solve(ctx(dims), mR, mT, v0, model, params, precond="two_level", twolevel=opts)
+    vsol, rep = vr.dist_selftest_solve(P, mR, mT, v0, model, params, halo=8, precond="two_level",
+                                       two_level=opts)
+    g = one.report
+    assert rep["stop"] == g["stop"] and rep["success"]
+    assert rep["outer_iterations"] == g["outer_iterations"]
+    assert rep["fine"]["hessian_matvecs"] == g["fine"]["hessian_matvecs"]
+    assert rep["coarse"]["hessian_matvecs"] == g["coarse"]["hessian_matvecs"] > 0
+    assert abs(rep["final_mismatch_rel"] - g["final_mismatch_rel"]) <= 1e-9
+    assert rel_l2(vsol, one.v) < 1e-8
+
+
+def test_two_level_solve_on_one_rank_nccl_slab(vr, ref, ctx, monkeypatch):
+    """The same through the real NCCL transport at one rank (VR_DIST_SINGLE_RANK)."""
+    dims = (32, 32, 32)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model("h2", beta_v=1e-2, nt=4), vr.make_params(eps_opt=1e-2)
+    v0 = np.zeros((3,) + dims)
+    one = vr.gauss_newton_solve(ctx(dims), mR, mT, v0, model, params, precond="two_level")
+    monkeypatch.setenv("VR_DIST_SINGLE_RANK", "1")
+    try:
+        d = vr.DistContext(dims, 0, 1, vr.nccl_unique_id(), device=0, halo=8)
+    except vr.ResourceError as exc:
+        pytest.skip(f"NCCL communicator unavailable: {exc}")
+    res = vr.gauss_newton_solve(d, mR, mT, v0, model, params, precond="two_level")
+    assert res.report["outer_iterations"] == one.report["outer_iterations"]
+    assert res.report["coarse"]["hessian_matvecs"] == one.report["coarse"]["hessian_matvecs"]
+    assert rel_l2(np.asarray(res.v), one.v) < 1e-8
