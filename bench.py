@@ -66,6 +66,10 @@ def parse():
                     help="skip the 128^3 (config 2) per-operator micro-benchmarks and solve")
     ap.add_argument("--no-config4", action="store_true",
                     help="skip the 512^3 (config 4, one GPU) matvec throughput")
+    ap.add_argument("--slab-two-level", action="store_true",
+                    help="x1 slabs: also time the continuation with the two-level preconditioner (one GPU "
+                         "does it by default; on slabs it is opt-in so that a first multi-GPU run times "
+                         "the spectral-preconditioner solve only)")
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the multi-GPU code path (x1 slabs over the NCCL transport, per-slab input "
                          "generation, exchange timing) with whatever world size this is, including 1: a "
@@ -779,7 +783,7 @@ def main():
             "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"],
             "stop": reps[-1]["stop_name"], "precond": "spectral", "continuation": "beta_v 1, 1e-1, 1e-2"}
         # the same continuation with the two-level preconditioner; one GPU only
-        if single:
+        if single or args.slab_two_level:
             t2 = []
             for _ in range(6):  # first run: coarse context, plans and pool growth
                 ctx.synchronize()
@@ -788,14 +792,14 @@ def main():
                                                        precond="two_level")
                 ctx.synchronize()
                 t2.append(time.perf_counter() - t0)
-            solve["config3_two_level"] = {
+            solve[f"config{cid}_two_level"] = {
                 "grid": n, "seconds": float(np.median(t2[1:])), "seconds_runs": t2, "levels": len(reps2),
                 "newton_iterations": [r["outer_iterations"] for r in reps2],
                 "fine_hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps2),
                 "coarse_hessian_matvecs": sum(r["coarse"]["hessian_matvecs"] for r in reps2),
                 "final_mismatch_rel": reps2[-1]["final_mismatch_rel"],
                 "final_grad_rel": reps2[-1]["final_grad_rel"], "stop": reps2[-1]["stop_name"],
-                "precond": "two-level, PCG(0.1) inner on the 128^3 coarse grid"}
+                "precond": f"two-level, PCG(0.1) inner on the {n // 2}^3 coarse grid"}
     if not args.no_solve and single:
         # config 1: 64^3 analytic problem, GPU vs the reference on the host cores
         ctx1 = vr.Context(64, device=dev)

@@ -538,6 +538,10 @@ int vr_dist_selftest_solve(int P, int n1, int n2, int n3, int device, int halo,
                            const vr_model* model, const vr_solver_params* params,
                            const double* m_R, const double* m_T, const double* v0, double* v_out,
                            vr_solve_report* report);
+/* det grad y, the absolute deformation map and det_stats of a velocity on P virtual slab ranks
+ * (postprocess.cpp:13-81); stats3 = min, max, mean */
+int vr_dist_selftest_postprocess(int P, int n1, int n2, int n3, int device, int halo, const double* v,
+                                 int nt, double* det_out, double* map_out, double* stats3);
 /* The same with a preconditioner choice (VR_PRECOND_*; tl_opts may be NULL): the two-level
  * preconditioner on slabs (precond.cpp:153-249 with the coarse grid on a sibling slab context
  * and the coarse band exchanged between the ranks' k2 slabs) */

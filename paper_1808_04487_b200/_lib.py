@@ -169,6 +169,7 @@ SIGNATURES = {
                                        HP, HP]),
     "vr_dist_selftest_solve": (I, [I, I, I, I, I, I, C.POINTER(Model), C.POINTER(SolverParams),
                                    HP, HP, HP, HP, C.POINTER(SolveReport)]),
+    "vr_dist_selftest_postprocess": (I, [I, I, I, I, I, I, HP, I, HP, HP, HP]),
     "vr_dist_selftest_solve_precond": (I, [I, I, I, I, I, I, C.POINTER(Model), C.POINTER(SolverParams), I,
                                            C.POINTER(TwoLevelOptions), HP, HP, HP, HP,
                                            C.POINTER(SolveReport)]),

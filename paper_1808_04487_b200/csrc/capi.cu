@@ -1330,7 +1330,7 @@ int vr_grid_continuation(vr_ctx* ctx, const double* m_R, const double* m_T, cons
                          int max_levels, int* n_levels, vr_iteration_record* records,
                          int max_records) {
     return guard([&] {
-        set_dev_single(ctx, "vr_grid_continuation");
+        set_dev(ctx);  // one GPU or x1 slabs
         need(m_R && m_T && v0 && model && params && v_out && n_levels, "vr_grid_continuation");
         copy_levels(vr::grid_continuation(ctx, m_R, m_T, v0, *model, *params, precond, n_grid_levels, v_out),
                     reports, max_levels, n_levels, records, max_records);
@@ -1360,7 +1360,7 @@ int vr_beta_search(vr_ctx* ctx, const double* m_R, const double* m_T, const doub
                    const vr_beta_search_params* bp, double* beta_out, double* v_out,
                    vr_beta_trial* trials, int max_trials, int* n_trials) {
     return guard([&] {
-        set_dev_single(ctx, "vr_beta_search");
+        set_dev(ctx);  // one GPU or x1 slabs
         need(m_R && m_T && v0 && model && params && bp && beta_out && v_out && n_trials, "vr_beta_search");
         vr::BetaSearch r = vr::beta_search(ctx, m_R, m_T, v0, *model, *params, precond, *bp, v_out);
         *n_trials = static_cast<int>(r.trials.size());
@@ -1373,7 +1373,7 @@ int vr_beta_search(vr_ctx* ctx, const double* m_R, const double* m_T, const doub
 }
 int vr_det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det) {
     return guard([&] {
-        set_dev_single(ctx, "vr_det_deformation_gradient");
+        set_dev(ctx);  // one GPU or x1 slabs
         need(v3 && det, "vr_det_deformation_gradient");
         vr::det_deformation_gradient(ctx, v3, nt, det);
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1381,7 +1381,7 @@ int vr_det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* d
 }
 int vr_deformation_map(vr_ctx* ctx, const double* v3, int nt, int absolute, double* out3) {
     return guard([&] {
-        set_dev_single(ctx, "vr_deformation_map");
+        set_dev(ctx);  // one GPU or x1 slabs
         need(v3 && out3, "vr_deformation_map");
         vr::deformation_map(ctx, v3, nt, absolute != 0, out3);
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1390,7 +1390,7 @@ int vr_deformation_map(vr_ctx* ctx, const double* v3, int nt, int absolute, doub
 int vr_det_stats(vr_ctx* ctx, const double* det, const double* foreground, double threshold,
                  vr_det_summary* out) {
     return guard([&] {
-        set_dev_single(ctx, "vr_det_stats");
+        set_dev(ctx);  // one GPU or x1 slabs
         need(det && out, "vr_det_stats");
         *out = vr::det_stats(ctx, det, foreground, threshold);
     });

@@ -450,4 +450,31 @@ int vr_dist_selftest_solve_precond(int P, int n1, int n2, int n3, int device, in
     });
 }
 
+int vr_dist_selftest_postprocess(int P, int n1, int n2, int n3, int device, int halo, const double* v,
+                                 int nt, double* det_out, double* map_out, double* stats3) {
+    return dguard([&] {
+        const long long Ng = static_cast<long long>(n1) * n2 * n3;
+        vr::run_local_group(P, n1, n2, n3, device, halo, [&](int, vr_ctx* ctx) {
+            const long long N = ctx->g.N, off = static_cast<long long>(ctx->g.off1) * n2 * n3;
+            double* dv = vr::dev_alloc(ctx, 3 * N);
+            double* det = vr::dev_alloc(ctx, N);
+            double* map = vr::dev_alloc(ctx, 3 * N);
+            for (int c = 0; c < 3; ++c)
+                VR_CUDA(cudaMemcpyAsync(dv + c * N, v + c * Ng + off, sizeof(double) * N,
+                                        cudaMemcpyHostToDevice, ctx->stream));
+            vr::det_deformation_gradient(ctx, dv, nt, det);
+            vr::deformation_map(ctx, dv, nt, true, map);
+            const vr_det_summary st = vr::det_stats(ctx, det, nullptr, 0.0);
+            VR_CUDA(cudaMemcpyAsync(det_out + off, det, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+            for (int c = 0; c < 3; ++c)
+                VR_CUDA(cudaMemcpyAsync(map_out + c * Ng + off, map + c * N, sizeof(double) * N,
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+            VR_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (stats3 && ctx->dist->rank == 0) stats3[0] = st.min, stats3[1] = st.max, stats3[2] = st.mean;
+            for (double* q : {dv, det, map}) vr::dev_free(ctx, q);
+            VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        });
+    });
+}
+
 }  // extern "C"

@@ -66,6 +66,8 @@ void release_cache(vr_ctx* ctx);  // return the context's cached device buffers 
 long long hoff(const vr_ctx* ctx);
 double* pslice(const vr_ctx* ctx, double* base, int j);
 void exchange(vr_ctx* ctx, double* interior);
+// read the device flags now (non-finite input, departure beyond the x1 halo) and raise
+void check_flags(vr_ctx* ctx, const char* what);
 
 void validate_model(const vr_model& m);
 void validate_params(const vr_solver_params& p);

@@ -29,7 +29,8 @@ __global__ void k_fill(double* __restrict__ x, long long n, double v) {
 }
 
 // y_c = wrap_coord(x_c + u_c) (postprocess.cpp:50-59)
-__global__ void k_absolute_map(const double* __restrict__ u, double* __restrict__ y, GridDims g) {
+__global__ void k_absolute_map(const double* __restrict__ u, long long ustride, double* __restrict__ y,
+                               GridDims g) {
     const long long i = blockIdx.x * (long long)kT + threadIdx.x;
     if (i >= g.N) return;
     long long r = i;
@@ -37,9 +38,9 @@ __global__ void k_absolute_map(const double* __restrict__ u, double* __restrict_
     r /= g.n3;
     const int i2 = static_cast<int>(r % g.n2);
     const int i1 = static_cast<int>(r / g.n2);
-    const double x[3] = {g.h1 * i1, g.h2 * i2, g.h3 * i3};
+    const double x[3] = {g.h1 * (g.off1 + i1), g.h2 * i2, g.h3 * i3};  // off1: slab origin
 #pragma unroll
-    for (int c = 0; c < 3; ++c) y[c * g.N + i] = wrap_coord(x[c] + u[c * g.N + i]);
+    for (int c = 0; c < 3; ++c) y[c * g.N + i] = wrap_coord(x[c] + u[c * ustride + i]);
 }
 
 // det_stats partials (postprocess.cpp:62-81): per block {min, max, sum, count}
@@ -241,43 +242,94 @@ vr_overlap score(unsigned long long a, unsigned long long b, unsigned long long 
     return s;
 }
 
+
+// x1 slabs: the halo-padded gather copy of v (3 components, stride hstride) with exchanged
+// halos, after the same halo check as objective_evaluate. One GPU: v itself.
+struct GatherVelocity {
+    std::unique_ptr<DevBuf> pad;
+    const double* v = nullptr;   // component 0 (interior)
+    long long stride = 0;
+    GatherVelocity(vr_ctx* ctx, const double* v3, int nt, const char* what) {
+        const long long N = ctx->g.N;
+        if (!ctx->dist) {
+            v = v3, stride = N;
+            return;
+        }
+        const int need = halo_required(max_abs(ctx, v3, N), nt, ctx->g.n1);
+        if (need > ctx->g.halo)
+            throw_resource(std::string(what) + ": x1 displacement needs a halo of " + std::to_string(need) +
+                           " planes, ctx has " + std::to_string(ctx->g.halo));
+        pad.reset(new DevBuf(ctx, 3 * ctx->hstride));
+        for (int c = 0; c < 3; ++c) {
+            VR_CUDA(cudaMemcpyAsync(pslice(ctx, pad->p, c), v3 + c * N, sizeof(double) * N,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+            exchange(ctx, pslice(ctx, pad->p, c));
+        }
+        v = pslice(ctx, pad->p, 0), stride = ctx->hstride;
+    }
+};
+void begin_flags(vr_ctx* ctx) {
+    drain_flags(ctx);
+    VR_CUDA(cudaMemsetAsync(ctx->flag_dev, 0, 2 * sizeof(int), ctx->stream));
+}
+
 }  // namespace
 
 // det_deformation_gradient (postprocess.cpp:13-29): continuity transport of 1 along the
-// backward characteristics with the factor of -div v
+// backward characteristics with the factor of -div v. On x1 slabs every gather source
+// (div v, the two transport buffers) is halo-padded and exchanged before its step.
 void det_deformation_gradient(vr_ctx* ctx, const double* v3, int nt, double* det) {
-    const long long N = ctx->g.N;
+    const long long N = ctx->g.N, H = ctx->hstride;
     check_velocity(ctx, v3, nt);
-    DevBuf xb(ctx, 3 * N), div(ctx, N), factor(ctx, N), work(ctx, N);
-    sl_trace(ctx, v3, N, nt, VR_TRACE_BACKWARD, xb.p);
-    op_divergence(ctx, v3, div.p);
-    scale(ctx, div.p, N, -1.0);
-    sl_factor(ctx, div.p, xb.p, 0.5 / nt, factor.p);
-    double* buf[2] = {det, work.p};
+    begin_flags(ctx);
+    GatherVelocity gv(ctx, v3, nt, "det_deformation_gradient");
+    DevBuf xb(ctx, 3 * N), div(ctx, H), factor(ctx, N), work(ctx, 2 * H);
+    sl_trace(ctx, gv.v, gv.stride, nt, VR_TRACE_BACKWARD, xb.p);
+    double* divi = pslice(ctx, div.p, 0);
+    op_divergence(ctx, v3, divi);
+    scale(ctx, divi, N, -1.0);
+    exchange(ctx, divi);
+    sl_factor(ctx, divi, xb.p, 0.5 / nt, factor.p);
+    double* buf[2] = {pslice(ctx, work.p, 0), pslice(ctx, work.p, 1)};
     VR_LAUNCH(ctx, "pp_pointwise", k_fill<<<blocks_for(N), kT, 0, ctx->stream>>>(buf[0], N, 1.0));
-    for (int j = 0; j < nt; ++j) sl_continuity(ctx, buf[j & 1], xb.p, factor.p, buf[(j + 1) & 1]);
-    if (nt & 1)
-        VR_CUDA(cudaMemcpyAsync(det, work.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    for (int j = 0; j < nt; ++j) {
+        exchange(ctx, buf[j & 1]);
+        sl_continuity(ctx, buf[j & 1], xb.p, factor.p, buf[(j + 1) & 1]);
+    }
+    VR_CUDA(cudaMemcpyAsync(det, buf[nt & 1], sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->dist) check_flags(ctx, "det_deformation_gradient");
 }
 
 // deformation_map (postprocess.cpp:31-60)
 void deformation_map(vr_ctx* ctx, const double* v3, int nt, bool absolute, double* out3) {
-    const long long N = ctx->g.N;
+    const long long N = ctx->g.N, H = ctx->hstride;
     check_velocity(ctx, v3, nt);
-    DevBuf xb(ctx, 3 * N), vdep(ctx, 3 * N), u(ctx, 3 * N), w(ctx, 3 * N);
-    sl_trace(ctx, v3, N, nt, VR_TRACE_BACKWARD, xb.p);
-    sl_tricubic(ctx, v3, 3, xb.p, vdep.p);
-    VR_LAUNCH(ctx, "pp_pointwise", k_fill<<<blocks_for(3 * N), kT, 0, ctx->stream>>>(u.p, 3 * N, 0.0));
-    double* cur = u.p;
-    double* nxt = w.p;
+    begin_flags(ctx);
+    GatherVelocity gv(ctx, v3, nt, "deformation_map");
+    DevBuf xb(ctx, 3 * N), vdep(ctx, 3 * N), u(ctx, 3 * H), w(ctx, 3 * H);
+    sl_trace(ctx, gv.v, gv.stride, nt, VR_TRACE_BACKWARD, xb.p);
+    if (ctx->dist) {
+        for (int c = 0; c < 3; ++c) sl_tricubic(ctx, gv.v + c * gv.stride, 1, xb.p, vdep.p + c * N);
+    } else {
+        sl_tricubic(ctx, v3, 3, xb.p, vdep.p);
+    }
+    VR_CUDA(cudaMemsetAsync(u.p, 0, sizeof(double) * 3 * H, ctx->stream));
+    double* cur = pslice(ctx, u.p, 0);  // component c at + c * hstride
+    double* nxt = pslice(ctx, w.p, 0);
     for (int j = 0; j < nt; ++j) {
+        if (j > 0)  // u = 0 needs no exchange
+            for (int c = 0; c < 3; ++c) exchange(ctx, cur + c * H);
         sl_defmap_step(ctx, cur, xb.p, vdep.p, v3, 0.5 / nt, nxt);
         std::swap(cur, nxt);
     }
-    if (absolute)
-        VR_LAUNCH(ctx, "pp_pointwise", k_absolute_map<<<blocks_for(N), kT, 0, ctx->stream>>>(cur, out3, ctx->g));
-    else
-        VR_CUDA(cudaMemcpyAsync(out3, cur, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (absolute) {
+        VR_LAUNCH(ctx, "pp_pointwise", k_absolute_map<<<blocks_for(N), kT, 0, ctx->stream>>>(cur, H, out3, ctx->g));
+    } else {
+        for (int c = 0; c < 3; ++c)
+            VR_CUDA(cudaMemcpyAsync(out3 + c * N, cur + c * H, sizeof(double) * N, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+    }
+    if (ctx->dist) check_flags(ctx, "deformation_map");
 }
 
 // det_stats (postprocess.cpp:62-81); count == 0 -> all zero like DetStats{}
@@ -293,6 +345,12 @@ vr_det_summary det_stats(vr_ctx* ctx, const double* det, const double* fg, doubl
         mx = std::max(mx, part[4 * q + 1]);
         sum += part[4 * q + 2];
         cnt += part[4 * q + 3];
+    }
+    if (ctx->dist) {  // min / max and sum / count over the ranks (rank-ordered sums)
+        double mm[2] = {-mn, mx}, sc[2] = {sum, cnt};
+        ctx->dist->allreduce(ctx, mm, 2, true);
+        ctx->dist->allreduce(ctx, sc, 2, false);
+        mn = -mm[0], mx = mm[1], sum = sc[0], cnt = sc[1];
     }
     vr_det_summary st{0.0, 0.0, 0.0};
     if (cnt == 0.0) return st;

@@ -359,7 +359,8 @@ template <bool BIG>
 __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
     k_defmap_step(const double* __restrict__ u, const double* __restrict__ dep,
                   const double* __restrict__ vdep, const double* __restrict__ v, double half_dt,
-                  double* __restrict__ out, GridDims g, Tile t) {
+                  double* __restrict__ out, GridDims g, Tile t, long long ustride) {
+    // u / out: component c at + c * ustride (N, or the halo-padded stride on x1 slabs)
     int i1, i2, i3;
     long long i;
     if (!tile_point<BIG>(g, t, i1, i2, i3, i)) return;
@@ -369,8 +370,8 @@ __global__ void __launch_bounds__(kTileThreads, VR_SL_MINB * 2 / 3)
     make_stencil(g, x1, x2, x3, i1, st);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double ud = gather(u + c * g.N, g, st);
-        out[c * g.N + i] = ud - half_dt * (vdep[c * g.N + i] + v[c * g.N + i]);
+        const double ud = gather(u + c * ustride, g, st);
+        out[c * ustride + i] = ud - half_dt * (vdep[c * g.N + i] + v[c * g.N + i]);
     }
 }
 
@@ -721,9 +722,10 @@ void sl_adjoint_fn_step(vr_ctx* ctx, const double* src, const double* rnext, con
 
 void sl_defmap_step(vr_ctx* ctx, const double* u3, const double* dep3, const double* vdep3,
                     const double* v3, double half_dt, double* out3) {
+    // u3 / out3: interiors of 3-component fields with stride ctx->hstride (== N on one GPU)
     const GridDims& g = ctx->g;
     const Tile t = tile_of(g);
-    VR_TILE_LAUNCH(ctx, "sl_defmap_step", K_DEFMAP, u3, dep3, vdep3, v3, half_dt, out3, g, t);
+    VR_TILE_LAUNCH(ctx, "sl_defmap_step", K_DEFMAP, u3, dep3, vdep3, v3, half_dt, out3, g, t, ctx->hstride);
 }
 
 void sl_tricubic_f32(vr_ctx* ctx, const float* f, int nfields, const float* pts3, float* out) {

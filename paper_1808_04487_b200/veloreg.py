@@ -1174,6 +1174,16 @@ def dist_selftest_objective(P, m_R, m_T, v, vt, model=None, halo=8, device=0):
                            vt_H_vt=sc[4])
 
 
+def dist_selftest_postprocess(P, v, nt, halo=8, device=0):
+    """det grad y, the absolute deformation map and det_stats on P virtual slab ranks."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    dims = v.shape[1:]
+    det, ymap, st = np.empty(dims), np.empty((3,) + dims), np.empty(3)
+    _lib.call("vr_dist_selftest_postprocess", P, dims[0], dims[1], dims[2], device, halo, v.ctypes.data, nt,
+              det.ctypes.data, ymap.ctypes.data, st.ctypes.data)
+    return det, ymap, {"min": st[0], "max": st[1], "mean": st[2]}
+
+
 def dist_selftest_solve(P, m_R, m_T, v0, model=None, params=None, halo=8, device=0, precond="spectral",
                         two_level=None):
     """A full GN solve on P virtual slab ranks on one GPU (precond: none / spectral / two_level)."""

@@ -256,3 +256,59 @@ def test_reference_postprocess_failures_are_not_the_fft_shim(vr, ref, ctx):
     flips_ref, flips_gpu = int((same_ref != labels).sum()), int((same_gpu != labels).sum())
     print("label flips at v = 0 (reference, gpu, ball/20):", flips_ref, flips_gpu, ball // 20)
     assert flips_ref > ball // 20 and np.array_equal(same_gpu, same_ref)
+
+
+# ---- x1 slabs (round 2b): deformation measures, beta search and grid continuation -----------
+def _pp_velocity(ref, dims):
+    _, _, vs = ref.generate_synthetic(dims, 4)
+    return 0.7 * vs + 0.1 * ref.random_smooth_vector(dims, 2, 7, 1.0)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_deformation_measures_match_single_gpu(vr, ref, ctx, P):
+    """det grad y, the absolute deformation map (global x1 coordinates on every rank) and
+    det_stats (min / max / mean over ranks) on P virtual slab ranks vs one GPU
+    (postprocess.cpp:13-81)."""
+    dims = (32, 32, 32)
+    v = _pp_velocity(ref, dims)
+    c = ctx(dims)
+    det1 = np.asarray(vr.det_deformation_gradient(c, v, 4))
+    map1 = np.asarray(vr.deformation_map(c, v, 4, absolute=True))
+    st1 = vr.det_stats(c, det1)
+    det, ymap, st = vr.dist_selftest_postprocess(P, v, 4, halo=8)
+    assert rel_l2(det, det1) < 1e-13
+    assert np.abs(np.angle(np.exp(1j * (ymap - map1)))).max() < 1e-12  # equal modulo 2 pi
+    for k in ("min", "max", "mean"):  # the slab divergence takes the 3D transform path: ~1e-16
+        assert abs(st[k] - st1[k]) <= 1e-12 * abs(st1[k])
+
+
+def _one_rank_slab(vr, dims, monkeypatch, halo=8):
+    monkeypatch.setenv("VR_DIST_SINGLE_RANK", "1")
+    try:
+        return vr.DistContext(dims, 0, 1, vr.nccl_unique_id(), device=0, halo=halo)
+    except vr.ResourceError as exc:
+        pytest.skip(f"NCCL communicator unavailable: {exc}")
+
+
+def test_slab_beta_search_and_grid_continuation_one_rank_nccl(vr, ref, ctx, monkeypatch):
+    """The outer loops on a slab context over the real NCCL transport at one rank: beta search
+    (solves + det grad y + det_stats on slabs) and grid continuation (sibling slab contexts per
+    level, slab resampling) reproduce the plain context's trials / levels."""
+    dims = (32, 32, 32)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model(), vr.make_params()
+    v0 = np.zeros((3,) + dims)
+    c = ctx(dims)
+    d = _one_rank_slab(vr, dims, monkeypatch)
+    sp = vr.beta_search_params(eps_J=0.9)
+    b1, v1, t1 = vr.beta_search(c, mR, mT, v0, model, params, search=sp)
+    bd, vd, td = vr.beta_search(d, mR, mT, v0, model, params, search=sp)
+    assert bd == b1 and [t["feasible"] for t in td] == [t["feasible"] for t in t1]
+    for a, b in zip(td, t1):
+        assert a["report"]["outer_iterations"] == b["report"]["outer_iterations"]
+        assert a["det_min"] == pytest.approx(b["det_min"], rel=1e-9)
+    assert rel_l2(np.asarray(vd), np.asarray(v1)) < 1e-8
+    vg1, rg1, _ = vr.grid_continuation(c, mR, mT, v0, 2, model, params)
+    vgd, rgd, _ = vr.grid_continuation(d, mR, mT, v0, 2, model, params)
+    assert [r["outer_iterations"] for r in rgd] == [r["outer_iterations"] for r in rg1]
+    assert rel_l2(np.asarray(vgd), np.asarray(vg1)) < 1e-8
