@@ -542,6 +542,11 @@ int vr_dist_selftest_solve(int P, int n1, int n2, int n3, int device, int halo,
  * (postprocess.cpp:13-81); stats3 = min, max, mean */
 int vr_dist_selftest_postprocess(int P, int n1, int n2, int n3, int device, int halo, const double* v,
                                  int nt, double* det_out, double* map_out, double* stats3);
+/* transport_labels of `labels` by v and overlap_scores(labels, warped) on P virtual slab ranks
+ * (postprocess.cpp:83-165) */
+int vr_dist_selftest_labels(int P, int n1, int n2, int n3, int device, int halo, const double* labels,
+                            const double* v, int nt, double* warped_out, int max_labels, int* n_labels,
+                            int* codes, vr_overlap* per_label, vr_overlap* union_scores);
 /* The same with a preconditioner choice (VR_PRECOND_*; tl_opts may be NULL): the two-level
  * preconditioner on slabs (precond.cpp:153-249 with the coarse grid on a sibling slab context
  * and the coarse band exchanged between the ranks' k2 slabs) */

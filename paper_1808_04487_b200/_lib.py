@@ -170,6 +170,8 @@ SIGNATURES = {
     "vr_dist_selftest_solve": (I, [I, I, I, I, I, I, C.POINTER(Model), C.POINTER(SolverParams),
                                    HP, HP, HP, HP, C.POINTER(SolveReport)]),
     "vr_dist_selftest_postprocess": (I, [I, I, I, I, I, I, HP, I, HP, HP, HP]),
+    "vr_dist_selftest_labels": (I, [I, I, I, I, I, I, HP, HP, I, HP, I, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(Overlap), C.POINTER(Overlap)]),
     "vr_dist_selftest_solve_precond": (I, [I, I, I, I, I, I, C.POINTER(Model), C.POINTER(SolverParams), I,
                                            C.POINTER(TwoLevelOptions), HP, HP, HP, HP,
                                            C.POINTER(SolveReport)]),

@@ -1398,7 +1398,7 @@ int vr_det_stats(vr_ctx* ctx, const double* det, const double* foreground, doubl
 int vr_transport_labels(vr_ctx* ctx, const double* labels, const double* v3, int nt,
                         double* out) {
     return guard([&] {
-        set_dev_single(ctx, "vr_transport_labels");
+        set_dev(ctx);  // one GPU or x1 slabs
         need(labels && v3 && out, "vr_transport_labels");
         vr::transport_labels(ctx, labels, v3, nt, out);
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1408,7 +1408,7 @@ int vr_overlap_scores(vr_ctx* ctx, const double* reference, const double* test,
                       const double* mask, int max_labels, int* n_labels, int* codes,
                       vr_overlap* per_label, vr_overlap* union_scores) {
     return guard([&] {
-        set_dev_single(ctx, "vr_overlap_scores");
+        set_dev(ctx);  // one GPU or x1 slabs
         need(reference && test && n_labels, "vr_overlap_scores");
         *n_labels = vr::overlap_scores(ctx, reference, test, mask, max_labels, codes, per_label,
                                        union_scores);

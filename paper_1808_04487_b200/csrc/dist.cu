@@ -138,11 +138,15 @@ struct NcclTransport final : Transport {
         comm_end(ctx, "comm_halo", ev);
     }
     void allreduce(vr_ctx* ctx, double* vals, int k, bool max) override {
-        VR_CUDA(cudaMemcpyAsync(buf, vals, sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
-        nccl_check(nccl().allGather(buf, buf + 8, k, ncclDouble, comm, ctx->stream), "allGather");
+        double* b = buf;  // 8 in, 8 * size gathered; larger tables (label codes) get a temporary
+        const size_t in = k <= 8 ? 8 : static_cast<size_t>(k);
+        if (k > 8) VR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b), sizeof(double) * in * (size + 1), ctx->stream));
+        VR_CUDA(cudaMemcpyAsync(b, vals, sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
+        nccl_check(nccl().allGather(b, b + in, k, ncclDouble, comm, ctx->stream), "allGather");
         std::vector<double> all(static_cast<size_t>(k) * size);
-        VR_CUDA(cudaMemcpyAsync(all.data(), buf + 8, sizeof(double) * k * size,
+        VR_CUDA(cudaMemcpyAsync(all.data(), b + in, sizeof(double) * k * size,
                                 cudaMemcpyDeviceToHost, ctx->stream));
+        if (k > 8) VR_CUDA(cudaFreeAsync(b, ctx->stream));
         VR_CUDA(cudaStreamSynchronize(ctx->stream));
         for (int i = 0; i < k; ++i) {
             double acc = all[i];
@@ -472,6 +476,42 @@ int vr_dist_selftest_postprocess(int P, int n1, int n2, int n3, int device, int 
             VR_CUDA(cudaStreamSynchronize(ctx->stream));
             if (stats3 && ctx->dist->rank == 0) stats3[0] = st.min, stats3[1] = st.max, stats3[2] = st.mean;
             for (double* q : {dv, det, map}) vr::dev_free(ctx, q);
+            VR_CUDA(cudaStreamSynchronize(ctx->stream));
+        });
+    });
+}
+
+int vr_dist_selftest_labels(int P, int n1, int n2, int n3, int device, int halo, const double* labels,
+                            const double* v, int nt, double* warped_out, int max_labels, int* n_labels,
+                            int* codes, vr_overlap* per_label, vr_overlap* union_scores) {
+    return dguard([&] {
+        const long long Ng = static_cast<long long>(n1) * n2 * n3;
+        vr::run_local_group(P, n1, n2, n3, device, halo, [&](int, vr_ctx* ctx) {
+            const long long N = ctx->g.N, off = static_cast<long long>(ctx->g.off1) * n2 * n3;
+            double* dv = vr::dev_alloc(ctx, 3 * N);
+            double* dl = vr::dev_alloc(ctx, N);
+            double* dw = vr::dev_alloc(ctx, N);
+            VR_CUDA(cudaMemcpyAsync(dl, labels + off, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+            for (int c = 0; c < 3; ++c)
+                VR_CUDA(cudaMemcpyAsync(dv + c * N, v + c * Ng + off, sizeof(double) * N,
+                                        cudaMemcpyHostToDevice, ctx->stream));
+            vr::transport_labels(ctx, dl, dv, nt, dw);
+            VR_CUDA(cudaMemcpyAsync(warped_out + off, dw, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+            const bool r0 = ctx->dist->rank == 0;
+            std::vector<int> cd(max_labels > 0 ? max_labels : 1);
+            std::vector<vr_overlap> pl(max_labels > 0 ? max_labels : 1);
+            vr_overlap un{};
+            const int ns = vr::overlap_scores(ctx, dl, dw, nullptr, max_labels, cd.data(), pl.data(), &un);
+            VR_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (r0) {
+                if (n_labels) *n_labels = ns;
+                for (int s = 0; s < ns && s < max_labels; ++s) {
+                    if (codes) codes[s] = cd[s];
+                    if (per_label) per_label[s] = pl[s];
+                }
+                if (union_scores) *union_scores = un;
+            }
+            for (double* q : {dv, dl, dw}) vr::dev_free(ctx, q);
             VR_CUDA(cudaStreamSynchronize(ctx->stream));
         });
     });

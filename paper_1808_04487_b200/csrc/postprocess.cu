@@ -214,6 +214,13 @@ std::vector<long long> label_codes(vr_ctx* ctx, const double* a, const double* b
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
     double mn = 1e300, mx = -1e300;
     for (int q = 0; q < kRedBlocks; ++q) mn = std::min(mn, part[2 * q]), mx = std::max(mx, part[2 * q + 1]);
+    if (ctx->dist) {  // the code range of all ranks
+        double mm[2] = {-mn, mx};
+        ctx->dist->allreduce(ctx, mm, 2, true);
+        mn = -mm[0], mx = mm[1];
+        if (!(mx - mn < static_cast<double>(1 << 20)))
+            throw_argument("label codes must span fewer than 2^20 values on x1 slabs");
+    }
     if (!(mx - mn < static_cast<double>(1 << 24)))
         throw_argument("label codes must span fewer than 2^24 values");
     cmin = static_cast<long long>(mn);
@@ -228,6 +235,11 @@ std::vector<long long> label_codes(vr_ctx* ctx, const double* a, const double* b
                             ctx->stream));
     VR_CUDA(cudaFreeAsync(dp, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->dist) {  // a code is present if any rank holds it
+        std::vector<double> pd(present.begin(), present.end());
+        ctx->dist->allreduce(ctx, pd.data(), static_cast<int>(pd.size()), true);
+        for (size_t q = 0; q < pd.size(); ++q) present[q] = pd[q] != 0.0;
+    }
     std::vector<long long> codes;
     for (long long q = 0; q < range; ++q)
         if (present[q] && q + cmin != 0) codes.push_back(q + cmin);
@@ -370,21 +382,26 @@ void transport_labels(vr_ctx* ctx, const double* labels, const double* v3, int n
         throw_resource("transport_labels: more than 64 distinct labels (" +
                        std::to_string(codes.size()) + ")");
     check_velocity(ctx, v3, nt);
-    DevBuf xb(ctx, 3 * N), best(ctx, N), mask(ctx, N), next(ctx, N);
-    sl_trace(ctx, v3, N, nt, VR_TRACE_BACKWARD, xb.p);
+    begin_flags(ctx);
+    GatherVelocity gv(ctx, v3, nt, "transport_labels");
+    // mask / next are gather sources: halo-padded and exchanged before each step on x1 slabs
+    DevBuf xb(ctx, 3 * N), best(ctx, N), work(ctx, 2 * ctx->hstride);
+    sl_trace(ctx, gv.v, gv.stride, nt, VR_TRACE_BACKWARD, xb.p);
     VR_LAUNCH(ctx, "pp_pointwise", k_fill<<<blocks_for(N), kT, 0, ctx->stream>>>(out, N, 0.0));
     VR_LAUNCH(ctx, "pp_pointwise", k_fill<<<blocks_for(N), kT, 0, ctx->stream>>>(best.p, N, 0.0));
     for (long long code : codes) {
-        VR_LAUNCH(ctx, "pp_pointwise", k_label_mask<<<blocks_for(N), kT, 0, ctx->stream>>>(labels, N, code, mask.p));
-        gaussian(ctx, mask.p, mask.p, 1.0);
-        double* cur = mask.p;
-        double* nxt = next.p;
+        double* cur = pslice(ctx, work.p, 0);
+        double* nxt = pslice(ctx, work.p, 1);
+        VR_LAUNCH(ctx, "pp_pointwise", k_label_mask<<<blocks_for(N), kT, 0, ctx->stream>>>(labels, N, code, cur));
+        gaussian(ctx, cur, cur, 1.0);
         for (int j = 0; j < nt; ++j) {
+            exchange(ctx, cur);
             sl_advect(ctx, cur, xb.p, nxt);
             std::swap(cur, nxt);
         }
         VR_LAUNCH(ctx, "pp_pointwise", k_label_update<<<blocks_for(N), kT, 0, ctx->stream>>>(cur, best.p, out, N, static_cast<double>(code)));
     }
+    if (ctx->dist) check_flags(ctx, "transport_labels");
 }
 
 // overlap_scores (postprocess.cpp:122-165)
@@ -412,6 +429,11 @@ int overlap_scores(vr_ctx* ctx, const double* ref, const double* test, const dou
     VR_CUDA(cudaFreeAsync(dslot, ctx->stream));
     VR_CUDA(cudaFreeAsync(dcnt, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->dist) {  // voxel counts of all ranks (integers below 2^53: exact as doubles)
+        std::vector<double> cd(cnt.begin(), cnt.end());
+        ctx->dist->allreduce(ctx, cd.data(), static_cast<int>(cd.size()), false);
+        for (size_t q = 0; q < cd.size(); ++q) cnt[q] = static_cast<unsigned long long>(cd[q]);
+    }
     for (int s = 0; s < ns && s < max_labels; ++s) {
         if (codes_out) codes_out[s] = static_cast<int>(codes[s]);
         if (per_label) per_label[s] = score(cnt[3 * s], cnt[3 * s + 1], cnt[3 * s + 2]);

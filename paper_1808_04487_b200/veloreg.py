@@ -1184,6 +1184,23 @@ def dist_selftest_postprocess(P, v, nt, halo=8, device=0):
     return det, ymap, {"min": st[0], "max": st[1], "mean": st[2]}
 
 
+def dist_selftest_labels(P, labels, v, nt, halo=8, device=0, max_labels=256):
+    """transport_labels + overlap_scores(labels, warped) on P virtual slab ranks."""
+    labels = np.ascontiguousarray(labels, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    dims = labels.shape
+    warped = np.empty(dims)
+    n = C.c_int()
+    codes = (C.c_int * max_labels)()
+    per = (_lib.Overlap * max_labels)()
+    uni = _lib.Overlap()
+    _lib.call("vr_dist_selftest_labels", P, dims[0], dims[1], dims[2], device, halo, labels.ctypes.data,
+              v.ctypes.data, nt, warped.ctypes.data, max_labels, C.byref(n), codes, per, C.byref(uni))
+    k = min(n.value, max_labels)
+    return warped, {"per_label": {codes[i]: _ov(per[i]) for i in range(k)}, "union": _ov(uni),
+                    "n_labels": n.value}
+
+
 def dist_selftest_solve(P, m_R, m_T, v0, model=None, params=None, halo=8, device=0, precond="spectral",
                         two_level=None):
     """A full GN solve on P virtual slab ranks on one GPU (precond: none / spectral / two_level)."""

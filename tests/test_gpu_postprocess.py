@@ -312,3 +312,19 @@ def test_slab_beta_search_and_grid_continuation_one_rank_nccl(vr, ref, ctx, monk
     vgd, rgd, _ = vr.grid_continuation(d, mR, mT, v0, 2, model, params)
     assert [r["outer_iterations"] for r in rgd] == [r["outer_iterations"] for r in rg1]
     assert rel_l2(np.asarray(vgd), np.asarray(vg1)) < 1e-8
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_label_transport_and_overlap_match_single_gpu(vr, ref, ctx, P):
+    """transport_labels (code table and per-code advection with halo exchanges) and
+    overlap_scores (voxel counts summed over ranks) on P virtual slab ranks vs one GPU:
+    labels equal voxel for voxel, scores equal (postprocess.cpp:83-165)."""
+    dims = (32, 32, 32)
+    lab, vs = _labels(ref, dims)
+    c = ctx(dims)
+    w1 = np.asarray(vr.transport_labels(c, lab, vs, 4))
+    s1 = vr.overlap_scores(c, lab, w1)
+    w, s = vr.dist_selftest_labels(P, lab, vs, 4, halo=8)
+    assert np.array_equal(w, w1)
+    assert s["n_labels"] == s1["n_labels"] and s["union"] == s1["union"]
+    assert s["per_label"] == s1["per_label"]
