@@ -1,6 +1,6 @@
 // objective_f32.cu -- the fp32 lane of the objective: the reference's
-// Objective<float> (proj/src/objective.cpp:35-156 with T = float) and its Gauss-Newton /
-// PCG / Armijo driver (proj/src/solver.cpp:23-269), one GPU.
+// Objective<float> (proj/src/objective.cpp:35-156 with T = float, Gauss-Newton and full
+// Newton) and its Newton / PCG / Armijo driver (proj/src/solver.cpp:23-269), one GPU.
 //
 // Every field is stored in fp32 exactly where the reference stores a ScalarField<float>
 // (state history, departure points, continuity factor, grad m_j, adjoint / incremental
@@ -44,6 +44,50 @@ __global__ void k_factor_f(float* factor, const float* div, const float* at_dep,
     if (i < n)
         factor[i] = static_cast<float>(
             exp(half_dt * (static_cast<double>(div[i]) + static_cast<double>(at_dep[i]))));
+}
+// ---- full Newton (gauss_newton = false; transport.cpp:150-226, objective.cpp:135-149) ----
+// gradient_dot<float>: q = float(q + d_a m * w_a), a = 0, 1, 2 (transport.cpp:143-145)
+__global__ void k_graddot_f(float* q, const float* gm, const float* vt, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i >= n) return;
+    float o = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        o = static_cast<float>(static_cast<double>(o) +
+                               static_cast<double>(gm[a * n + i]) * static_cast<double>(vt[a * n + i]));
+    q[i] = o;
+}
+// lv_c = float(lam * vt_c) (transport.cpp:203-207)
+__global__ void k_scale_vec_f(float* lv, const float* lam, const float* vt, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i >= n) return;
+    const float l = lam[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) lv[c * n + i] = l * vt[c * n + i];
+}
+// cur = float(lam_interp * factor + half_dt * (r_cur + src_interp)) with the float product and
+// the float sum of the reference's expression (transport.cpp:217-220)
+__global__ void k_fn_step_f(float* cur, const float* li, const float* factor, const float* rc,
+                            const float* si, double half_dt, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i >= n) return;
+    const float a = li[i] * factor[i];
+    const float b = rc[i] + si[i];
+    cur[i] = static_cast<float>(static_cast<double>(a) + half_dt * static_cast<double>(b));
+}
+// the full-Newton observer at slice j (objective.cpp:143-148):
+// b_a = float(b_a + (w lam~_j) d_a m_j); b_a = float(b_a + (w lam_j) d_a mt_j)
+__global__ void k_observe_fn_f(float* b, double w, const float* lamt, const float* gm, const float* lam,
+                               const float* gmt, long long n) {
+    const long long i = blockIdx.x * (long long)kT + threadIdx.x;
+    if (i >= n) return;
+    const double w1 = w * static_cast<double>(lamt[i]), w2 = w * static_cast<double>(lam[i]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float v = static_cast<float>(static_cast<double>(b[a * n + i]) + w1 * static_cast<double>(gm[a * n + i]));
+        v = static_cast<float>(static_cast<double>(v) + w2 * static_cast<double>(gmt[a * n + i]));
+        b[a * n + i] = v;
+    }
 }
 float* falloc(vr_ctx* ctx, long long n) { return reinterpret_cast<float*>(dev_alloc(ctx, (n + 1) / 2)); }
 void ffree(vr_ctx* ctx, float* p) { dev_free(ctx, reinterpret_cast<double*>(p)); }
@@ -102,19 +146,18 @@ struct StateF32 {
     ObjF32* obj = nullptr;
     int nt = 0;
     float *v = nullptr, *xb = nullptr, *mhist = nullptr, *xf = nullptr, *factor = nullptr,
-          *gradm = nullptr, *grad = nullptr;
+          *gradm = nullptr, *grad = nullptr, *lamhist = nullptr;  // lamhist: full Newton only
     double objective = 0.0, mismatch = 0.0, mismatch_rel = 0.0;
     bool has_gradient = false;
     ~StateF32() {
         if (!obj) return;
-        for (float* p : {v, xb, mhist, xf, factor, gradm, grad}) ffree(obj->ctx, p);
+        for (float* p : {v, xb, mhist, xf, factor, gradm, grad, lamhist}) ffree(obj->ctx, p);
     }
 };
 
 ObjF32* objf32_create(vr_ctx* ctx, const float* mR, const float* mT, const vr_model& model) {
     validate_model(model);
     if (ctx->dist) throw_argument("fp32 objective: one GPU only");
-    if (!model.gauss_newton) throw_argument("fp32 objective: Gauss-Newton only (full Newton is fp64)");
     auto o = std::make_unique<ObjF32>();
     o->ctx = ctx;
     o->mR = mR;
@@ -201,7 +244,12 @@ void objf32_gradient(ObjF32* o, StateF32* s) {
     for (int j = nt - 1; j >= 0; --j)  // sweep_continuity (transport.cpp:88-113)
         sl_continuity_f32(ctx, lamh + (j + 1) * N, s->xf, s->factor, lamh + j * N);
     sl_accumulate_f32(ctx, lamh, s->gradm, nt, dt, b);
-    ffree(ctx, lamh);
+    if (!o->model.gauss_newton) {  // s.lambda_history (objective.cpp:100-102)
+        ffree(ctx, s->lamhist);
+        s->lamhist = lamh;
+    } else {
+        ffree(ctx, lamh);
+    }
     o->counters.pde_solves += 1;
     if (o->model.projection != VR_PROJ_IDENTITY)
         spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
@@ -225,6 +273,58 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
                     "(compute the gradient first)");
     const int nt = s->nt;
     const double dt = 1.0 / nt, hdt = 0.5 / nt;
+    if (!o->model.gauss_newton) {
+        if (!s->lamhist) throw_logic("hessian_matvec: full Newton mode needs the adjoint history");
+        // solve_inc_state keeping the mt history (transport.cpp:150-173), step by step with the
+        // reference's rounding points
+        float* mt = falloc(ctx, (nt + 1) * N);
+        float *q[2] = {falloc(ctx, N), falloc(ctx, N)}, *tmp = falloc(ctx, N);
+        VR_CUDA(cudaMemsetAsync(mt, 0, sizeof(float) * N, ctx->stream));
+        VR_LAUNCH(ctx, "f32_pointwise", k_graddot_f<<<blocks(N), kT, 0, ctx->stream>>>(q[0], s->gradm, vt3, N));
+        for (int j = 0; j < nt; ++j) {
+            VR_LAUNCH(ctx, "f32_pointwise", k_graddot_f<<<blocks(N), kT, 0, ctx->stream>>>(
+                q[(j + 1) & 1], s->gradm + 3LL * (j + 1) * N, vt3, N));
+            lincomb(ctx, tmp, 1.0, mt + j * N, -hdt, q[j & 1], N);
+            sl_tricubic_f32(ctx, tmp, 1, s->xb, mt + (j + 1) * N);
+            axpy(ctx, mt + (j + 1) * N, -hdt, q[(j + 1) & 1], N);
+        }
+        o->counters.pde_solves += 1;
+        // solve_inc_adjoint, full Newton (transport.cpp:192-226), with the observer
+        float *cur = falloc(ctx, N), *li = falloc(ctx, N), *si = falloc(ctx, N), *lv = falloc(ctx, 3 * N);
+        float *r[2] = {falloc(ctx, N), falloc(ctx, N)}, *gmt = falloc(ctx, 3 * N);
+        auto source = [&](int j, float* out) {  // r_j = div(lambda_j vt)
+            VR_LAUNCH(ctx, "f32_pointwise", k_scale_vec_f<<<blocks(N), kT, 0, ctx->stream>>>(lv, s->lamhist + j * N, vt3, N));
+            spectral_f(ctx, lv, 3, out, 1, [&](const double* i, double* d) { op_divergence(ctx, i, d); });
+        };
+        float* b = out3;
+        VR_CUDA(cudaMemsetAsync(b, 0, sizeof(float) * 3 * N, ctx->stream));
+        auto observe = [&](int j) {
+            const double w = (j == 0 || j == nt) ? 0.5 * dt : dt;
+            spectral_f(ctx, mt + j * N, 1, gmt, 3, [&](const double* i, double* d) { op_gradient(ctx, i, d); });
+            VR_LAUNCH(ctx, "f32_pointwise", k_observe_fn_f<<<blocks(N), kT, 0, ctx->stream>>>(
+                b, w, cur, s->gradm + 3LL * j * N, s->lamhist + j * N, gmt, N));
+        };
+        lincomb(ctx, cur, -1.0, mt + nt * N, 0.0, nullptr, N);  // terminal = -mt_nt
+        source(nt, r[nt & 1]);
+        observe(nt);
+        for (int j = nt - 1; j >= 0; --j) {
+            source(j, r[j & 1]);
+            sl_tricubic_f32(ctx, cur, 1, s->xf, li);
+            sl_tricubic_f32(ctx, r[(j + 1) & 1], 1, s->xf, si);
+            VR_LAUNCH(ctx, "f32_pointwise", k_fn_step_f<<<blocks(N), kT, 0, ctx->stream>>>(cur, li, s->factor, r[j & 1], si, hdt, N));
+            observe(j);
+        }
+        o->counters.pde_solves += 1;
+        for (float* p : {mt, q[0], q[1], tmp, cur, li, si, lv, r[0], r[1], gmt}) ffree(ctx, p);
+        if (o->model.projection != VR_PROJ_IDENTITY)
+            spectral_f(ctx, b, 3, b, 3, [&](const double* i, double* out) {
+                op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
+            });
+        o->counters.hessian_matvecs += 1;
+        op_reg_begin_f32(ctx, vt3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+        op_reg_finish_f32(ctx, out3, out3);
+        return;
+    }
     // incremental state (transport.cpp:150-173) fused per step; the last step writes the
     // inc-adjoint terminal -mt_nt into the history, whose sweep then keeps every lambda~_j
     float* lamh = falloc(ctx, (nt + 1) * N);

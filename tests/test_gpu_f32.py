@@ -83,7 +83,7 @@ def test_spectral_f32(vr, ref, ctx, n):
 
 
 @pytest.mark.parametrize("n", [16, 32])
-@pytest.mark.parametrize("kind", ["h2", "h1div"])
+@pytest.mark.parametrize("kind", ["h2", "h1div", "h2_full_newton"])
 def test_objective_f32(vr, ref, ctx, n, kind):
     # Objective<float> (objective.cpp:35-156, T = float): J, mismatch, reduced gradient and
     # GN Hessian matvec against the reference's float instantiation, same PDE-solve counts
@@ -92,6 +92,8 @@ def test_objective_f32(vr, ref, ctx, n, kind):
     mR, mT, vs = ref.generate_synthetic(dims, 4)
     if kind == "h2":
         model = vr.make_model()
+    elif kind == "h2_full_newton":  # transport.cpp:192-226, objective.cpp:143-148 with T = float
+        model = vr.make_model(gauss_newton=False)
     else:
         model = vr.make_model("h1", beta_v=1e-3, nt=4, div_penalty=True, beta_w=1e-4,
                               projection="near_incompressible")
@@ -118,13 +120,14 @@ def test_objective_f32(vr, ref, ctx, n, kind):
     assert rel_l2(o.hessian_matvec(s32, vt), o64.hessian_matvec(s64, vt)) <= 1e-4
 
 
-@pytest.mark.parametrize("n", [16, 32])
-def test_gn_solve_f32(vr, ref, ctx, n):
-    # gauss_newton_solve<float>: Newton iterations +-1, final mismatch and |g| within 1 %
+@pytest.mark.parametrize("n,gn", [(16, True), (32, True), (16, False)])
+def test_gn_solve_f32(vr, ref, ctx, n, gn):
+    # gauss_newton_solve<float> (gn = False: the full-Newton Hessian): Newton iterations +-1,
+    # final mismatch and |g| within 1 %
     dims = (n, n, n)
     c = ctx(dims)
     mR, mT, _ = ref.generate_synthetic(dims, 4)
-    model, params = vr.make_model(), vr.make_params(eps_opt=1e-2)
+    model, params = vr.make_model(gauss_newton=gn), vr.make_params(eps_opt=1e-2)
     v0 = np.zeros((3,) + dims)
     res = vr.gauss_newton_solve_f32(c, mR, mT, v0, model, params)
     v_ref, rep, _ = ref.gauss_newton_solve_f32(mR, mT, v0, model, params)
