@@ -156,6 +156,15 @@ class Clocks:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+        # nvidia-smi needs ~0.2 s before its first line: wait for it here, outside the timed
+        # region, so that even a short region (K x 6 ms) is covered by the 100 ms samples that
+        # follow; the pre-roll line itself is only reported when no later sample exists
+        self.pre = None
+        if self.proc is not None:
+            try:
+                self.pre = self.proc.stdout.readline()
+            except Exception:
+                self.pre = None
         return self
 
     def __exit__(self, *a):
@@ -182,8 +191,16 @@ class Clocks:
             for nm, val in zip(names, p[3:7]):
                 if val.lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+               "samples": len(sm), "reasons": sorted(reasons)}
+        if not sm and getattr(self, "pre", None):  # region shorter than one sampling interval
+            p = [x.strip() for x in self.pre.split(",")]
+            try:
+                out.update(sm_mhz=float(p[0]), sm_max_mhz=float(p[1]), pre_roll_sample=True,
+                           reasons=sorted(nm for nm, val in zip(names, p[3:7]) if val.lower() == "active"))
+            except (ValueError, IndexError):
+                pass
+        return out
 
 
 def measured_peak():

@@ -6,9 +6,10 @@ mkdir -p gpurun_out
 (nproc; lscpu | grep "Model name"; free -g | head -2; nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv) > gpurun_out/r2b_host.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 > gpurun_out/r2b_gputest.log 2>&1
 echo "rc=$?" >> gpurun_out/r2b_gputest.log
+python __graft_entry__.py > gpurun_out/r2b_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r2b_smoke.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2b_bench.json 2> gpurun_out/r2b_bench.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2b_bench_ref.json 2> gpurun_out/r2b_bench_ref.err
-VR_DIST_SINGLE_RANK=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29544 bench.py --gpus 1 --steps 10 --warmup 3 --force-slabs > gpurun_out/r2b_forced_slabs_256.json 2> gpurun_out/r2b_forced_slabs_256.err
+VR_DIST_SINGLE_RANK=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29544 bench.py --gpus 1 --steps 10 --warmup 3 --force-slabs --slab-two-level > gpurun_out/r2b_forced_slabs_256.json 2> gpurun_out/r2b_forced_slabs_256.err
 Q="--no-solve --no-fp32 --no-config2 --no-config4 --no-e2e --no-cpu-baseline"
 timeout 600 python bench.py --steps 2 --warmup 3 $Q > gpurun_out/r2b_launch_cmd.json 2> gpurun_out/r2b_launch_cmd.err && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2b_launches.csv python bench.py --steps 2 --warmup 3 $Q > gpurun_out/r2b_ncu_launches.log 2>&1
