@@ -153,11 +153,11 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
         # nvidia-smi needs ~0.2 s before its first line: wait for it here, outside the timed
-        # region, so that even a short region (K x 6 ms) is covered by the 100 ms samples that
+        # region, so that even a short region (K x 6 ms) is covered by the 25 ms samples that
         # follow; the pre-roll line itself is only reported when no later sample exists
         self.pre = None
         if self.proc is not None:
