@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=256, help="grid size (default: config 3, 256^3)")
+    ap.add_argument("--n", type=int, default=None,
+                    help="grid size (default: the config's own: 256^3 on one GPU, 512^3 on 2-7, 1024^3 on 8)")
     ap.add_argument("--nt", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

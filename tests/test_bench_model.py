@@ -95,3 +95,16 @@ def test_slab_inputs_match_the_global_generators(P):
     assert np.abs(raw - gm).max() <= 1e-9  # x1 kernel truncation: see ellipsoid_phantom_slab
     _, vmax1 = ph.bandlimited_velocity_slab(n, kmax, disp, 0, n)
     assert abs(vmax1 - np.abs(gv[0]).max()) <= 1e-14
+
+
+def test_default_grid_follows_the_world_size(monkeypatch):
+    """No --n: config 3 (256^3) on one GPU, config 4 (512^3) on 2-7, config 5 (1024^3) on 8
+    (BASELINE configs; the driver launches `bench.py --gpus N --steps K --warmup W` only)."""
+    import sys
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "8", "--steps", "5", "--warmup", "3"])
+    args = bench.parse()
+    assert args.n is None
+    assert bench.config_for(1, args.n) == (3, 256)
+    assert bench.config_for(2, args.n) == (4, 512) and bench.config_for(4, args.n) == (4, 512)
+    assert bench.config_for(8, args.n) == (5, 1024)
+    assert bench.config_for(8, 64) == (5, 64)  # --n overrides the grid only
