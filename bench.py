@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None,
                     help="grid size (default: the config's own: 256^3 on one GPU, 512^3 on 2-7, 1024^3 on 8)")
+    ap.add_argument("--config", type=int, default=None, choices=[3, 4, 5],
+                    help="BASELINE config whose phantom / velocity parameters to use (default: by world size)")
     ap.add_argument("--nt", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -85,10 +87,10 @@ def dist_env():
     return rank, world, local
 
 
-def config_for(world, n_arg):
+def config_for(world, n_arg, cid_arg=None):
     """BASELINE config id and grid: config 3 (256^3) on one GPU, config 4 (512^3) on 2-7
-    GPUs, config 5 (1024^3) on 8; --n overrides the grid."""
-    cid = 3 if world == 1 else (5 if world >= 8 else 4)
+    GPUs, config 5 (1024^3) on 8; --n overrides the grid, --config the parameters."""
+    cid = cid_arg or (3 if world == 1 else (5 if world >= 8 else 4))
     from paper_1808_04487_b200 import phantom  # numpy only; does not load the product library
     return cid, (n_arg or phantom.CONFIGS[cid]["n"])
 
@@ -515,7 +517,7 @@ def main():
     args = parse()
     rank, world, local = dist_env()
     nt = args.nt
-    cid, n = config_for(world, args.n)
+    cid, n = config_for(world, args.n, args.config)
 
     if args.impl == "reference":
         if rank != 0:
