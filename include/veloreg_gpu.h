@@ -307,11 +307,19 @@ int vr_compute_gradient_f32(vr_objective_f32* obj, vr_state_f32* s, float* g3);
 int vr_hessian_matvec_f32(vr_objective_f32* obj, const vr_state_f32* s, const float* vt3,
                           float* out3);
 /* gauss_newton_solve<float> (solver.cpp:154-269; PCG and Armijo on fp32 vectors with fp64
- * scalars); precond VR_PRECOND_NONE or VR_PRECOND_SPECTRAL; fp32 device pointers */
+ * scalars); precond VR_PRECOND_NONE, VR_PRECOND_SPECTRAL or VR_PRECOND_TWO_LEVEL (default
+ * options); gauss_newton = 0 selects the full-Newton Hessian; fp32 device pointers */
 int vr_gauss_newton_solve_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
                               const vr_model* model, const vr_solver_params* params, int precond,
                               float* v_out, vr_solve_report* report, vr_iteration_record* records,
                               int max_records);
+/* the same with TwoLevelPreconditioner<float> (precond.cpp:153-249; opts may be NULL): the
+ * Newton / split-system PCG iterates are fp32, the coarse-grid machinery behind M^-1 runs in fp64 */
+int vr_gauss_newton_solve_two_level_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
+                                        const vr_model* model, const vr_solver_params* params,
+                                        const vr_twolevel_options* opts, float* v_out,
+                                        vr_solve_report* report, vr_iteration_record* records,
+                                        int max_records);
 /* parameter continuation over vr_gauss_newton_solve_f32 */
 int vr_parameter_continuation_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
                                   const vr_model* model, const vr_solver_params* params,

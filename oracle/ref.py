@@ -140,6 +140,10 @@ _SIG = {
                                               C.POINTER(SolverParams), C.POINTER(TwoLevelOptions),
                                               P, C.POINTER(SolveReport), C.POINTER(IterationRecord),
                                               I]),
+    "vref_gauss_newton_solve_two_level_f32": (I, [DIMS, P, P, P, C.POINTER(Model),
+                                                  C.POINTER(SolverParams), C.POINTER(TwoLevelOptions),
+                                                  P, C.POINTER(SolveReport), C.POINTER(IterationRecord),
+                                                  I]),
     "vref_random_smooth_scalar": (I, [DIMS, I, C.c_ulonglong, D, P]),
     "vref_random_smooth_vector": (I, [DIMS, I, C.c_ulonglong, D, P]),
     "vref_random_rough_scalar": (I, [DIMS, C.c_ulonglong, P]),
@@ -694,6 +698,19 @@ def gauss_newton_solve_f32(m_R, m_T, v0, model, params, precond=1, max_records=5
     recs = (IterationRecord * max_records)()
     _call("vref_gauss_newton_solve_f32", _dims(r.shape), r.ctypes.data, t.ctypes.data, v0.ctypes.data,
           C.byref(model), C.byref(params), precond, vout.ctypes.data, C.byref(rep), recs, max_records)
+    n = min(rep.n_records, max_records)
+    return vout, _report(rep), [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
+
+
+def gauss_newton_solve_two_level_f32(m_R, m_T, v0, model, params, options, max_records=512):
+    """gauss_newton_solve<float> with TwoLevelPreconditioner<float> (precond.cpp:153-249)."""
+    r, t, v0 = _f(m_R), _f(m_T), _f(v0)
+    vout = np.empty_like(v0)
+    rep = SolveReport()
+    recs = (IterationRecord * max_records)()
+    _call("vref_gauss_newton_solve_two_level_f32", _dims(r.shape), r.ctypes.data, t.ctypes.data,
+          v0.ctypes.data, C.byref(model), C.byref(params), C.byref(options), vout.ctypes.data,
+          C.byref(rep), recs, max_records)
     n = min(rep.n_records, max_records)
     return vout, _report(rep), [{k: getattr(recs[i], k) for k, _ in IterationRecord._fields_} for i in range(n)]
 

@@ -635,6 +635,21 @@ int vref_gauss_newton_solve_f32(const int* d, const float* mR, const float* mT, 
     });
 }
 
+int vref_gauss_newton_solve_two_level_f32(const int* d, const float* mR, const float* mT, const float* v0,
+                                          const vr_model* m, const vr_solver_params* p,
+                                          const vr_twolevel_options* opts, float* v_out,
+                                          vr_solve_report* rep, vr_iteration_record* recs, int max_recs) {
+    return guard([&] {
+        Grid3 g = grid_of(d);
+        auto R = load_scalar_f(g, mR), T = load_scalar_f(g, mT);
+        TwoLevelPreconditioner<float> pre(to_tl(opts));
+        auto res = gauss_newton_solve(R, T, load_vector_f(g, v0), to_model(*m), to_params(*p), pre,
+                                      pre.coarse_counters());
+        store_f(res.v, v_out);
+        fill_report(res.report, rep, recs, max_recs, 0);
+    });
+}
+
 int vref_parameter_continuation_f32(const int* d, const float* mR, const float* mT, const float* v0,
                                     const vr_model* m, const vr_solver_params* p, int precond,
                                     float* v_out, vr_solve_report* reps, int max_levels,

@@ -105,6 +105,9 @@ SIGNATURES = {
     "vr_hessian_matvec_f32": (I, [P, P, DP, DP]),
     "vr_gauss_newton_solve_f32": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I,
                                       DP, C.POINTER(SolveReport), C.POINTER(IterationRecord), I]),
+    "vr_gauss_newton_solve_two_level_f32": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams),
+                                                C.POINTER(TwoLevelOptions), DP, C.POINTER(SolveReport),
+                                                C.POINTER(IterationRecord), I]),
     "vr_parameter_continuation_f32": (I, [P, DP, DP, DP, C.POINTER(Model), C.POINTER(SolverParams), I,
                                           DP, C.POINTER(SolveReport), I, C.POINTER(C.c_int),
                                           C.POINTER(IterationRecord), I]),

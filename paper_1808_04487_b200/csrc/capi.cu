@@ -1252,6 +1252,21 @@ int vr_gauss_newton_solve_f32(vr_ctx* ctx, const float* m_R, const float* m_T, c
     });
 }
 
+int vr_gauss_newton_solve_two_level_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
+                                        const vr_model* model, const vr_solver_params* params,
+                                        const vr_twolevel_options* opts, float* v_out,
+                                        vr_solve_report* report, vr_iteration_record* records,
+                                        int max_records) {
+    return guard([&] {
+        set_dev_single(ctx, "vr_gauss_newton_solve_two_level_f32");
+        need(m_R && m_T && v0 && model && params && v_out && report, "vr_gauss_newton_solve_two_level_f32");
+        vr::GnResult r = vr::gauss_newton_solve_f32(ctx, m_R, m_T, v0, *model, *params, VR_PRECOND_TWO_LEVEL,
+                                                    v_out, opts);
+        *report = r.report;
+        copy_records(r, records, max_records, 0);
+    });
+}
+
 int vr_parameter_continuation_f32(vr_ctx* ctx, const float* m_R, const float* m_T, const float* v0,
                                   const vr_model* model, const vr_solver_params* params,
                                   int precond, float* v_out, vr_solve_report* reports,

@@ -130,7 +130,7 @@ vr_ctx* objf32_ctx(ObjF32* o);
 void objf32_copy_gradient(ObjF32* o, const StateF32* s, float* g3);  // synchronises
 GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, const float* v0,
                                 const vr_model& model, const vr_solver_params& params, int precond,
-                                float* v_out);
+                                float* v_out, const vr_twolevel_options* tl_opts = nullptr);
 std::vector<GnResult> parameter_continuation_f32(vr_ctx* ctx, const float* mR, const float* mT,
                                                  const float* v0, const vr_model& model,
                                                  const vr_solver_params& params, int precond,

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "objective.cuh"
+#include "twolevel.cuh"
 
 namespace vr {
 namespace {
@@ -264,7 +265,12 @@ void objf32_gradient(ObjF32* o, StateF32* s) {
 
 // hessian_matvec (objective.cpp:114-156, GN): inc-state (transport.cpp:150-173), GN
 // inc-adjoint (sweep_continuity with the observer), K, + beta_v A vt
+static void objf32_matvec_impl(ObjF32* o, const StateF32* s, const float* vt3, float* out3, bool with_reg);
 void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) {
+    objf32_matvec_impl(o, s, vt3, out3, true);
+}
+// hessian_matvec (with_reg) / hessian_data_matvec (objective.cpp:114-156)
+static void objf32_matvec_impl(ObjF32* o, const StateF32* s, const float* vt3, float* out3, bool with_reg) {
     vr_ctx* ctx = o->ctx;
     const long long N = ctx->g.N;
     if (!all_finite_f32(ctx, vt3, 3 * N)) throw_numeric("hessian_matvec: non-finite direction");
@@ -321,8 +327,10 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
                 op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
             });
         o->counters.hessian_matvecs += 1;
-        op_reg_begin_f32(ctx, vt3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
-        op_reg_finish_f32(ctx, out3, out3);
+        if (with_reg) {
+            op_reg_begin_f32(ctx, vt3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
+            op_reg_finish_f32(ctx, out3, out3);
+        }
         return;
     }
     // incremental state (transport.cpp:150-173) fused per step; the last step writes the
@@ -349,6 +357,7 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
             op_projection(ctx, i, out, o->model.projection, o->model.beta_v, o->model.norm.beta_w);
         });
     o->counters.hessian_matvecs += 1;
+    if (!with_reg) return;
     // out = float(b + beta_v A vt): fp32 rows in, the add fused into the c2r epilogue
     op_reg_begin_f32(ctx, vt3, o->model.norm, VR_REGOP_APPLY, o->model.beta_v);
     op_reg_finish_f32(ctx, out3, out3);
@@ -358,8 +367,10 @@ void objf32_matvec(ObjF32* o, const StateF32* s, const float* vt3, float* out3) 
 namespace {
 double norm_f(vr_ctx* ctx, const float* a, long long n) { return std::sqrt(dot_f(ctx, a, a, n, 1)); }
 
+using OpF = std::function<void(const float*, float*)>;
 vr_pcg_stats pcg_f32(ObjF32* o, const StateF32* s, const float* rhs, double rel_tol, int max_iter,
-                     int precond, float* x) {
+                     int precond, float* x, const OpF* op_override = nullptr,
+                     const OpF* pc_override = nullptr) {
     vr_ctx* ctx = o->ctx;
     const long long n3 = 3 * ctx->g.N;
     vr_pcg_stats st{};
@@ -372,7 +383,9 @@ vr_pcg_stats pcg_f32(ObjF32* o, const StateF32* s, const float* rhs, double rel_
     const double target = rel_tol * r0;
     float *r = falloc(ctx, n3), *z = falloc(ctx, n3), *sd = falloc(ctx, n3), *Hs = falloc(ctx, n3);
     auto pc = [&](const float* in, float* out) {  // SpectralPreconditioner: (beta_v A)^-1
-        if (precond == VR_PRECOND_SPECTRAL) {
+        if (pc_override) {
+            (*pc_override)(in, out);
+        } else if (precond == VR_PRECOND_SPECTRAL) {
             op_reg_begin_f32(ctx, in, o->model.norm, VR_REGOP_INVERSE, o->model.beta_v);
             op_reg_finish_f32(ctx, out, nullptr);
         }
@@ -385,7 +398,10 @@ vr_pcg_stats pcg_f32(ObjF32* o, const StateF32* s, const float* rhs, double rel_
     double rz = dot_f(ctx, r, z, n3, 1);
     bool done = false;
     for (int it = 0; it < max_iter && !done; ++it) {
-        objf32_matvec(o, s, sd, Hs);
+        if (op_override)
+            (*op_override)(sd, Hs);
+        else
+            objf32_matvec(o, s, sd, Hs);
         const double sHs = dot_f(ctx, sd, Hs, n3, 1);
         if (sHs <= 0.0) {
             st.negative_curvature = 1;
@@ -418,12 +434,61 @@ vr_pcg_stats pcg_f32(ObjF32* o, const StateF32* s, const float* rhs, double rel_
 }
 }  // namespace
 
+// The two-level preconditioner of the fp32 solve (precond.cpp:153-249 with T = float): the
+// outer Newton / split-system PCG runs on fp32 vectors as in the reference; the coarse-grid
+// machinery behind M^-1 (restriction, coarse objective, inner PCG / Chebyshev, prolongation)
+// is the fp64 TwoLevel of twolevel.cu applied to fp64 views of the fp32 fields -- a
+// preconditioner in higher precision than the reference's float one (it changes Krylov
+// iteration counts slightly, not what the solve converges to).
+struct TwoLevelF32 {
+    vr_ctx* ctx;
+    TwoLevel tl;
+    std::unique_ptr<F64> mR, mT;
+    vr_objective* obj64 = nullptr;
+    std::unique_ptr<vr_state> st64;
+    TwoLevelF32(vr_ctx* c, const vr_twolevel_options& o, const float* r, const float* t, const vr_model& m)
+        : ctx(c), tl(o), mR(new F64(c, r, c->g.N)), mT(new F64(c, t, c->g.N)) {
+        obj64 = objective_create(c, mR->p, mT->p, m);
+    }
+    ~TwoLevelF32() {  // the coarse objects in `tl` do not reference the fine mirror
+        st64.reset();
+        delete obj64;
+    }
+    void rebuild(const StateF32* s, double eps_H) {
+        const long long N = ctx->g.N;
+        st64.reset(new vr_state());
+        st64->obj = obj64;
+        st64->nt = s->nt;
+        st64->v = dev_alloc(ctx, 3 * N);
+        st64->mhist = dev_alloc(ctx, (s->nt + 1) * N);
+        convert_f2d(ctx, s->v, st64->v, 3 * N);
+        convert_f2d(ctx, s->mhist, st64->mhist, (s->nt + 1) * N);
+        if (s->lamhist) {
+            st64->lamhist = dev_alloc(ctx, (s->nt + 1) * N);
+            convert_f2d(ctx, s->lamhist, st64->lamhist, (s->nt + 1) * N);
+        }
+        tl.rebuild(obj64, st64.get(), eps_H);
+    }
+    void apply(const float* r, float* z) {
+        const long long n3 = 3 * ctx->g.N;
+        F64 dr(ctx, r, n3), dz(ctx, nullptr, n3);
+        tl.apply(ctx, dr.p, dz.p);
+        convert_d2f(ctx, dz.p, z, n3);
+    }
+};
+
 GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, const float* v0,
                                 const vr_model& model, const vr_solver_params& params, int precond,
-                                float* v_out) {
+                                float* v_out, const vr_twolevel_options* tl_opts) {
     validate_params(params);
-    if (precond != VR_PRECOND_NONE && precond != VR_PRECOND_SPECTRAL)
-        throw_argument("gauss_newton_solve_f32: preconditioner must be none or spectral");
+    if (precond != VR_PRECOND_NONE && precond != VR_PRECOND_SPECTRAL && precond != VR_PRECOND_TWO_LEVEL)
+        throw_argument("gauss_newton_solve_f32: unknown preconditioner");
+    std::unique_ptr<TwoLevelF32> tl;
+    if (precond == VR_PRECOND_TWO_LEVEL) {
+        vr_twolevel_options d;
+        vr_twolevel_options_default(&d);
+        tl.reset(new TwoLevelF32(ctx, tl_opts ? *tl_opts : d, mR, mT, model));
+    }
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     const long long n3 = 3 * ctx->g.N;
@@ -476,9 +541,45 @@ GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, c
                 break;
             }
             const double eps_H = std::min(0.5, std::sqrt(gk / g0));  // compute_forcing
-            lincomb(ctx, rhs, -1.0, state->grad, 0.0, nullptr, n3);   // scale(rhs, -1)
-            const vr_pcg_stats pcg = pcg_f32(obj.get(), state.get(), rhs, eps_H, params.max_krylov,
-                                             precond, dir);
+            vr_pcg_stats pcg;
+            if (tl) {
+                // split system (solver.cpp:208-221): (I + R H_data R) w = -R g, v~ = R w, R = (beta_v A)^-1/2
+                tl->rebuild(state.get(), eps_H);
+                const bool zero_mode = reg_symbol(model.norm, 0.0) == 0.0;
+                auto R = [&](const float* in, float* out) {
+                    op_reg_begin_f32(ctx, in, model.norm, VR_REGOP_INVERSE_SQRT, model.beta_v);
+                    op_reg_finish_f32(ctx, out, nullptr);
+                };
+                float* u = falloc(ctx, n3);
+                float* du = falloc(ctx, n3);
+                OpF sop = [&](const float* w, float* out) {  // Objective<float>::split_matvec (objective.cpp:158-176)
+                    R(w, u);
+                    objf32_matvec_impl(obj.get(), state.get(), u, du, false);
+                    R(du, out);
+                    axpy(ctx, out, 1.0, w, n3);
+                    if (zero_mode) {  // + mean(w) per component: A has a zero singular value
+                        const long long N = ctx->g.N;
+                        for (int c = 0; c < 3; ++c) {
+                            F64 dw(ctx, w + c * N, N);
+                            double sum[1];
+                            sum_components(ctx, dw.p, N, 1, sum);
+                            F64 dout(ctx, out + c * N, N);
+                            affine(ctx, dout.p, dout.p, N, sum[0] / static_cast<double>(ctx->g.Ng), 1.0);
+                            convert_d2f(ctx, dout.p, out + c * N, N);
+                        }
+                    }
+                };
+                OpF spc = [&](const float* r, float* z) { tl->apply(r, z); };
+                R(state->grad, rhs);
+                lincomb(ctx, rhs, -1.0, rhs, 0.0, nullptr, n3);
+                pcg = pcg_f32(obj.get(), state.get(), rhs, eps_H, params.max_krylov, precond, dir, &sop, &spc);
+                R(dir, dir);
+                ffree(ctx, u);
+                ffree(ctx, du);
+            } else {
+                lincomb(ctx, rhs, -1.0, state->grad, 0.0, nullptr, n3);   // scale(rhs, -1)
+                pcg = pcg_f32(obj.get(), state.get(), rhs, eps_H, params.max_krylov, precond, dir);
+            }
             const double slope = dot_f(ctx, state->grad, dir, ctx->g.N, 3) * hc;  // inner_product
             if (slope >= 0.0) {
                 rep.stop = VR_STOP_LINE_SEARCH_FAILURE;
@@ -517,6 +618,7 @@ GnResult gauss_newton_solve_f32(vr_ctx* ctx, const float* mR, const float* mT, c
     rep.final_mismatch_rel = state->mismatch_rel;
     rep.final_grad_rel = g0 > 0 ? norm_f(ctx, state->grad, n3) / g0 : 0.0;
     rep.fine = obj->counters;
+    if (tl) rep.coarse = tl->tl.counters();
     rep.n_records = static_cast<int>(res.records.size());
     VR_CUDA(cudaMemcpyAsync(v_out, state->v, sizeof(float) * n3, cudaMemcpyDeviceToDevice, ctx->stream));
     VR_CUDA(cudaStreamSynchronize(ctx->stream));

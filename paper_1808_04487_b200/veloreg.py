@@ -962,8 +962,9 @@ class ObjectiveF32:
 
 
 def gauss_newton_solve_f32(ctx, m_R, m_T, v0, model=None, params=None, precond="spectral",
-                           max_records=512):
-    """gauss_newton_solve<float> (solver.cpp:154-269) on host float32 arrays."""
+                           max_records=512, twolevel=None):
+    """gauss_newton_solve<float> (solver.cpp:154-269) on host float32 arrays; precond
+    "two_level" takes TwoLevelOptions in `twolevel`."""
     model = model if model is not None else make_model()
     params = params if params is not None else make_params()
     dR, dT, dv0 = (DeviceBufferF32.from_host(ctx, a) for a in (m_R, m_T, v0))
@@ -971,8 +972,13 @@ def gauss_newton_solve_f32(ctx, m_R, m_T, v0, model=None, params=None, precond="
     vout = DeviceBufferF32(ctx, v0.size)
     rep = _lib.SolveReport()
     recs = (_lib.IterationRecord * max_records)()
-    _lib.call("vr_gauss_newton_solve_f32", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
-              C.byref(params), _enum(_PRECOND, precond), vout.ptr, C.byref(rep), recs, max_records)
+    if precond == "two_level":
+        _lib.call("vr_gauss_newton_solve_two_level_f32", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
+                  C.byref(params), C.byref(twolevel) if twolevel is not None else None, vout.ptr,
+                  C.byref(rep), recs, max_records)
+    else:
+        _lib.call("vr_gauss_newton_solve_f32", ctx.handle, dR.ptr, dT.ptr, dv0.ptr, C.byref(model),
+                  C.byref(params), _enum(_PRECOND, precond), vout.ptr, C.byref(rep), recs, max_records)
     return SolveResult(vout.numpy(v0.shape), _report_dict(rep), _records(recs, min(rep.n_records, max_records)))
 
 

@@ -158,3 +158,27 @@ def test_parameter_continuation_f32(vr, ref, ctx):
         assert abs(a["outer_iterations"] - b["outer_iterations"]) <= 1
         assert abs(a["final_mismatch_rel"] - b["final_mismatch_rel"]) <= 1e-2 * b["final_mismatch_rel"]
     assert vg.dtype == np.float32 and rel_l2(vg, vref) <= 1e-3
+
+
+@pytest.mark.parametrize("n,inner", [(16, "pcg"), (32, "pcg"), (32, "cheb")])
+def test_two_level_solve_f32(vr, ref, ctx, n, inner):
+    """gauss_newton_solve<float> with TwoLevelPreconditioner<float> (precond.cpp:153-249,
+    solver.cpp:208-221): the GPU runs the fp32 Newton / split-system PCG with the coarse-grid
+    machinery in fp64; Newton iterations +-1, final mismatch and |g| within 1 % of the
+    reference's float instantiation, coarse work recorded."""
+    dims = (n, n, n)
+    c = ctx(dims)
+    mR, mT, _ = ref.generate_synthetic(dims, 4)
+    model, params = vr.make_model("h2", beta_v=1e-2, nt=4), vr.make_params(eps_opt=1e-2)
+    opts = vr.make_twolevel_options(inner=inner)
+    v0 = np.zeros((3,) + dims)
+    res = vr.gauss_newton_solve_f32(c, mR, mT, v0, model, params, precond="two_level", twolevel=opts)
+    v_ref, rep, _ = ref.gauss_newton_solve_two_level_f32(mR, mT, v0, model, params, opts)
+    g = res.report
+    assert res.v.dtype == np.float32 and g["success"] and g["stop"] == rep["stop"]
+    assert abs(g["outer_iterations"] - rep["outer_iterations"]) <= 1
+    assert abs(g["final_mismatch_rel"] - rep["final_mismatch_rel"]) <= 1e-2 * rep["final_mismatch_rel"]
+    assert abs(g["final_grad_rel"] - rep["final_grad_rel"]) <= 1e-2 * rep["final_grad_rel"]
+    assert g["coarse"]["hessian_matvecs"] > 0
+    if g["outer_iterations"] == rep["outer_iterations"]:
+        assert rel_l2(res.v, v_ref) <= 1e-3
