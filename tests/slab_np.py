@@ -13,6 +13,8 @@ oracle (oracle/veloreg_np.py):
                            image nearest the point's own plane, then made
                            slab-relative and read from the halo-padded slab
   * reductions          -- per-rank partials gathered and summed in rank order
+  * grid transfer       -- the coarse-band exchange of the two-level preconditioner
+                           (twolevel.cu resample_scalar_slabs)
 
 The compute itself is numpy (the oracle's arithmetic); only the decomposition
 is under test here. The CUDA slab path is checked on the GPU
@@ -120,6 +122,70 @@ class Slab:
                             for r in range(self.P)])
         a = np.concatenate([c[0] + 1j * c[1] for c in re], axis=1)
         return np.fft.irfft(np.fft.ifft(a, axis=1), n=self.shape[2], axis=2)
+
+    # ---- two-level grid transfer (twolevel.cu resample_scalar_slabs) ----------------
+    # The x1-layout spectra hold the k2 rows [k2_off, k2_off + n2s) of every rank. Coarse row
+    # j2 (of m2 = n2 / 2) is fine row j2 (j2 < m2 / 2) or j2 + m2 (j2 > m2 / 2), the Nyquist
+    # row m2 / 2 folds the fine rows m2 / 2 and 3 m2 / 2: the band a coarse rank needs lives on
+    # the lowest / highest quarter of the fine ranks. Restriction: per destination rank the
+    # partial alias sums of the rows this rank holds, one all-to-all, blocks added in rank
+    # order. Prolongation: all-gathered coarse slabs, every rank fills its own fine rows.
+    # (x3 Nyquist-plane images are left to the GPU tests; inputs here stay below them.)
+    @staticmethod
+    def _fine_rows(j, m):
+        """fine indices (axis length 2 m) aliasing onto coarse index j (axis length m)"""
+        if 2 * j < m:
+            return [j]
+        if 2 * j == m:
+            return [m // 2, 2 * m - m // 2]
+        return [j + m]
+
+    def restrict_to(self, spec, coarse: "Slab"):
+        """fine x1-layout spectrum (n1, n2s, nh) of this slab -> coarse (m1, m2s, mh)."""
+        (n1, n2, n3), (m1, m2, m3) = self.shape, coarse.shape
+        assert (n1, n2, n3) == (2 * m1, 2 * m2, 2 * m3) and coarse.P == self.P
+        scale = (m1 * m2 * m3) / (n1 * n2 * n3)
+        mh = coarse.nh
+        blocks = []
+        for q in range(self.P):
+            blk = np.zeros((m1, coarse.n2s, mh), dtype=complex)
+            for jl in range(coarse.n2s):
+                for i2 in self._fine_rows(q * coarse.n2s + jl, m2):
+                    l2 = i2 - self.k2_off
+                    if not 0 <= l2 < self.n2s:
+                        continue  # another rank's row
+                    for j1 in range(m1):
+                        for i1 in self._fine_rows(j1, m1):
+                            blk[j1, jl, :] += spec[i1, l2, :mh]
+            blocks.append(np.stack([blk.real, blk.imag]) * scale)
+        got = self.alltoall(blocks)
+        out = np.zeros((m1, coarse.n2s, mh), dtype=complex)
+        for c in got:  # rank order
+            out = out + (c[0] + 1j * c[1])
+        return out
+
+    def prolong_to(self, spec_c, fine: "Slab"):
+        """coarse x1-layout spectrum (m1, m2s, mh) of this slab -> fine (n1, n2s, nh)."""
+        (m1, m2, m3), (n1, n2, n3) = self.shape, fine.shape
+        assert (n1, n2, n3) == (2 * m1, 2 * m2, 2 * m3)
+        scale = (n1 * n2 * n3) / (m1 * m2 * m3)
+        own = np.stack([spec_c.real, spec_c.imag])
+        allc = self.alltoall([own for _ in range(self.P)])  # all-gather of the coarse slabs
+        full = np.concatenate([c[0] + 1j * c[1] for c in allc], axis=1)  # (m1, m2, mh)
+        out = np.zeros((n1, fine.n2s, fine.nh), dtype=complex)
+        mh = self.nh
+        for j2 in range(m2):
+            rows2 = self._fine_rows(j2, m2)
+            for i2 in rows2:
+                l2 = i2 - fine.k2_off
+                if not 0 <= l2 < fine.n2s:
+                    continue
+                for j1 in range(m1):
+                    rows1 = self._fine_rows(j1, m1)
+                    for i1 in rows1:
+                        out[i1, l2, :mh] = full[j1, j2, :] * (scale / (len(rows1) * len(rows2)))
+        out[:, :, mh - 1] *= 0.5  # the coarse x3 Nyquist bin folds onto +-m3/2
+        return out
 
     def kgrids(self, deriv=False):
         f = O.deriv_freq if deriv else O.fft_freq
