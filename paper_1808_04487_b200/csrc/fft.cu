@@ -615,11 +615,19 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
 // O = (X[k] - conj X[M-k]) exp(+2 pi i k / N); z = IFFT_M(Z); x[2m] = Re, x[2m+1] = Im.
 // Imaginary parts of the self-conjugate bins X[0], X[M] are ignored (c2r semantics).
 // TO = output / add element type (float for the fp32 lane: out = float(add + scale x))
-template <int M, class TO>
-__global__ void __launch_bounds__(RowCfg<M>::THREADS)
+// ADD = false (plain transform: no prefetched add field) is built for 3 CTAs/SM where the
+// stages allow three (M <= 128: 76.8 KB each); with the add field's 64 prefetch registers
+// that cap spills and measured slower (104 vs 89 us at 256^3), so ADD = true keeps 2.
+template <int M, bool ADD>
+struct C2rOcc {
+    static constexpr int MINB = (!ADD && 3 * (RowCfg<M>::SMEM + 1024) <= 233472) ? 3 : 2;
+};
+template <int M, class TO, bool ADD>
+__global__ void __launch_bounds__(RowCfg<M>::THREADS, C2rOcc<M, ADD>::MINB)
     k_c2r_rows(const double2* __restrict__ in, TO* __restrict__ out, long long nrows,
                const double2* __restrict__ twM_g, const double2* __restrict__ twN_g, double scale,
-               const TO* __restrict__ add) {
+               const TO* __restrict__ add_in) {
+    const TO* __restrict__ add = ADD ? add_in : nullptr;
     using C = RowCfg<M>;
     using TO2 = typename std::conditional<std::is_same<TO, float>::value, float2, double2>::type;
     constexpr int PER = C::RB * M / C::THREADS;  // output double2 per thread per tile
@@ -638,8 +646,8 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
         const long long avail_out = (nrows - tile * C::RB) * M;
         TO2* dstp = reinterpret_cast<TO2*>(out) + tile * C::RB * M;
         // the add field's loads are issued now and land while the rows transform
-        double2 addv[PER];
-        if (add) {
+        double2 addv[ADD ? PER : 1];
+        if constexpr (ADD) {
             const TO2* addp = reinterpret_cast<const TO2*>(add) + tile * C::RB * M;
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
@@ -694,7 +702,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS)
             const int r = e / M, i = e % M;
             const double2 z = buf[r * C::LD + padi(i)];
             double2 o;
-            if (add)
+            if constexpr (ADD)
                 o = make_double2(addv[j].x + scale * z.x, addv[j].y + scale * z.y);
             else
                 o = make_double2(z.x * scale, z.y * scale);
@@ -935,10 +943,17 @@ void launch_rows_f32out(vr_ctx* ctx, const void* in, float* out, double scale, c
     using C = RowCfg<M>;
     const long long nrows = static_cast<long long>(ctx->g.L) * ctx->g.n2;
     const long long ntiles = (nrows + C::RB - 1) / C::RB;
-    static int occ[64] = {0};
-    const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, float>, C::THREADS, C::SMEM, ntiles, occ);
-    VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, float><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
-        static_cast<const double2*>(in), out, nrows, ctx->fft->tw3h, ctx->fft->tw3, scale, add));
+    if (add) {
+        static int occ[64] = {0};
+        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, float, true>, C::THREADS, C::SMEM, ntiles, occ);
+        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, float, true><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+            static_cast<const double2*>(in), out, nrows, ctx->fft->tw3h, ctx->fft->tw3, scale, add));
+    } else {
+        static int occ[64] = {0};
+        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, float, false>, C::THREADS, C::SMEM, ntiles, occ);
+        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, float, false><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+            static_cast<const double2*>(in), out, nrows, ctx->fft->tw3h, ctx->fft->tw3, scale, nullptr));
+    }
 }
 
 template <int M>
@@ -953,12 +968,18 @@ void launch_rows_t(vr_ctx* ctx, bool forward, const void* in, void* out, double 
         VR_LAUNCH(ctx, "fft_x3_r2c", k_r2c_rows<M, double><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double*>(in), static_cast<double2*>(out), nrows, ctx->fft->tw3h,
             ctx->fft->tw3));
-    } else {
+    } else if (add) {
         static int occ[64] = {0};
-        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, double>, C::THREADS, C::SMEM, ntiles, occ);
-        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, double><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, double, true>, C::THREADS, C::SMEM, ntiles, occ);
+        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, double, true><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
             static_cast<const double2*>(in), static_cast<double*>(out), nrows, ctx->fft->tw3h,
             ctx->fft->tw3, scale, add));
+    } else {
+        static int occ[64] = {0};
+        const unsigned grid = persistent_grid(ctx, k_c2r_rows<M, double, false>, C::THREADS, C::SMEM, ntiles, occ);
+        VR_LAUNCH(ctx, "fft_x3_c2r", k_c2r_rows<M, double, false><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(
+            static_cast<const double2*>(in), static_cast<double*>(out), nrows, ctx->fft->tw3h,
+            ctx->fft->tw3, scale, nullptr));
     }
 }
 
