@@ -10,7 +10,7 @@ OUT=$ROOT/variants/$NAME
 mkdir -p "$OUT"
 FLAGS="-O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -I$ROOT/include -I$PKG/csrc --expt-relaxed-constexpr $EXTRA"
 pids=()
-for s in blas1 fft fft_axis spectral sl objective objective_f32 twolevel postprocess dist capi; do
+for s in blas1 fft fft_axis fft_axis_fused spectral sl objective objective_f32 twolevel postprocess dist capi; do
   /usr/local/cuda/bin/nvcc $FLAGS -c "$PKG/csrc/$s.cu" -o "$OUT/$s.o" -Xptxas -v 2> "$OUT/$s.log" &
   pids+=($!)
 done
