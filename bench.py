@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=None,
-                    help="grid size (default: the config's own: 256^3 on one GPU, 512^3 on 2-7, 1024^3 on 8)")
+    ap.add_argument("--n", "--grid", dest="n", type=int, default=None,
+                    help="grid size (default: the config's own: 256^3 on one GPU, 512^3 on 2-7, 1024^3 on 8); "
+                         "under torchrun spell it --grid (its parser rejects the abbreviation-like --n)")
     ap.add_argument("--config", type=int, default=None, choices=[3, 4, 5],
                     help="BASELINE config whose phantom / velocity parameters to use (default: by world size)")
     ap.add_argument("--nt", type=int, default=4)

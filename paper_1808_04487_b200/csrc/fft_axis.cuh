@@ -2,6 +2,9 @@
 // (plain transforms, slab variants) and fft_axis_fused.cu (fused x1 multiplier / derivative
 // passes): two translation units so that their instantiations compile in parallel.
 #pragma once
+#ifdef VR_AXIS_RMAX  // tuning: a smaller radix for the strided passes only (more threads per column)
+#define VR_FFT_RMAX VR_AXIS_RMAX
+#endif
 #include "fft_core.cuh"
 
 namespace vr {

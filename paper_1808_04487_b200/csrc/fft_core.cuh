@@ -94,7 +94,11 @@ __device__ __forceinline__ void dft_reg(double2* x) {
     }
 }
 
-__host__ __device__ constexpr int rmax_of(int n) { return n < 16 ? n : 16; }
+// largest in-register radix of this translation unit (elements per thread per stage)
+#ifndef VR_FFT_RMAX
+#define VR_FFT_RMAX 16
+#endif
+__host__ __device__ constexpr int rmax_of(int n) { return n < VR_FFT_RMAX ? n : VR_FFT_RMAX; }
 
 // One Stockham stage of radix R for a length-N transform with Ns = product of
 // previous radices; this thread handles butterflies j = t + b*T, b < RMAX/R.
@@ -147,8 +151,8 @@ __device__ __forceinline__ void fft_line(int t, const double2* __restrict__ tw, 
     bool first = true;
     while (Ns < N) {
         const int rem = N / Ns;
-        const bool last = rem <= 16;
-        const int R = rem >= 16 ? 16 : rem;
+        const bool last = rem <= VR_FFT_RMAX;
+        const int R = rem >= VR_FFT_RMAX ? VR_FFT_RMAX : rem;
         const bool reads_sm = !first || SRC_SM;
         const bool writes_sm = !last || DST_SM;
         const bool sync_between = reads_sm && writes_sm;
@@ -164,8 +168,8 @@ __device__ __forceinline__ void fft_line(int t, const double2* __restrict__ tw, 
         else                                                                                   \
             stockham_stage<N, RR, DIR>(Ns, t, tw, sm_src, sm_dst, sync_between);               \
     }
-        if constexpr (N >= 16) { VR_STAGE(16) }
-        if constexpr (N >= 8) { VR_STAGE(8) }
+        if constexpr (N >= 16 && VR_FFT_RMAX >= 16) { VR_STAGE(16) }
+        if constexpr (N >= 8 && VR_FFT_RMAX >= 8) { VR_STAGE(8) }
         if constexpr (N >= 4) { VR_STAGE(4) }
         VR_STAGE(2)
 #undef VR_STAGE
