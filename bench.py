@@ -750,7 +750,8 @@ def main():
             traffic = None
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
-                "limiter": "L1/LSU wavefronts of the 64-node fp64 gathers (ncu: L1/TEX 85 %, DRAM 29 %)"
+                "limiter": "L1 return path of the 64-node fp64 gathers: 64 B/clk/SM, 512 B per point = 0.46 ms "
+                           "floor per gather at 256^3 (ncu: data-pipe wavefronts 79-85 %, DRAM 29 %)"
                            if dom.startswith("sl_") and "step" in dom else None,
                 "bytes_per_launch": per_launch[dom], "avg_launch_ms": t / c}
     # x1 slabs: NCCL exchange time per matvec (all-to-all transposes + halos run on the
