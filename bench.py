@@ -600,7 +600,9 @@ def main():
         m_T, v, vt, vmax1 = phantom.make_config_inputs_slab(
             cid, first, planes, n=n, allreduce_max=lambda x: _red(x, dist.ReduceOp.MAX),
             allreduce_min=lambda x: _red(x, dist.ReduceOp.MIN))
-        halo = V.slab_halo_required(vmax1, nt, n)
+        # the halo covers the generating velocity with 30 % headroom: the solve's Armijo trials may
+        # overshoot it, and a trial that needs more planes raises ResourceError (never clamps)
+        halo = min(planes, max(V.slab_halo_required(vmax1, nt, n), V.slab_halo_required(1.3 * vmax1, nt, n)))
         uid = [V.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx = V.DistContext(n, rank, world, uid[0], device=dev, halo=halo)
@@ -789,23 +791,34 @@ def main():
         # initial guess and result device resident (host I/O is not solver time)
         params = V.make_params(eps_opt=1e-2)
         d_v0 = ctx.to_device(np.zeros((3,) + ctx.local_dims))  # device-resident initial guess
-        t_runs = []
-        for _ in range(6):  # the first run also grows the stream-ordered memory pool
-            ctx.synchronize()
-            t0 = time.perf_counter()
-            vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, d_v0, model, params)
-            ctx.synchronize()
-            t_runs.append(time.perf_counter() - t0)
-        t_solve = float(np.median(t_runs[1:]))  # median of the 5 steady runs (host jitter)
-        solve[f"config{cid}"] = {
-            "grid": n, "seconds": t_solve, "seconds_runs": t_runs, "levels": len(reps),
-            "newton_iterations": [r["outer_iterations"] for r in reps],
-            "hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps),
-            "pde_solves": sum(r["fine"]["pde_solves"] for r in reps),
-            "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"],
-            "stop": reps[-1]["stop_name"], "precond": "spectral", "continuation": "beta_v 1, 1e-1, 1e-2"}
+        t_runs, reps, solve_error = [], None, None
+        try:
+            for _ in range(6):  # the first run also grows the stream-ordered memory pool
+                ctx.synchronize()
+                t0 = time.perf_counter()
+                vsol, reps, _ = V.parameter_continuation(ctx, d_mR, d_mT, d_v0, model, params)
+                ctx.synchronize()
+                t_runs.append(time.perf_counter() - t0)
+        except vr.VelouregError as exc:
+            # library errors are raised from rank-consistent data (all-reduced flags and norms), so
+            # every rank lands here together; the matvec line above is still reported
+            if single:
+                raise
+            solve_error = f"{type(exc).__name__}: {exc}"
+        if solve_error is not None or reps is None:
+            solve[f"config{cid}"] = {"grid": n, "error": solve_error, "seconds_runs": t_runs}
+            reps = None
+        t_solve = float(np.median(t_runs[1:])) if len(t_runs) > 1 else None  # median of the steady runs
+        if reps is not None:
+            solve[f"config{cid}"] = {
+                "grid": n, "seconds": t_solve, "seconds_runs": t_runs, "levels": len(reps),
+                "newton_iterations": [r["outer_iterations"] for r in reps],
+                "hessian_matvecs": sum(r["fine"]["hessian_matvecs"] for r in reps),
+                "pde_solves": sum(r["fine"]["pde_solves"] for r in reps),
+                "final_mismatch_rel": reps[-1]["final_mismatch_rel"], "final_grad_rel": reps[-1]["final_grad_rel"],
+                "stop": reps[-1]["stop_name"], "precond": "spectral", "continuation": "beta_v 1, 1e-1, 1e-2"}
         # the same continuation with the two-level preconditioner; one GPU only
-        if single or args.slab_two_level:
+        if (single or args.slab_two_level) and reps is not None:
             t2 = []
             for _ in range(6):  # first run: coarse context, plans and pool growth
                 ctx.synchronize()
