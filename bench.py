@@ -697,7 +697,7 @@ def main():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize(dev)
-        k_e2e = max(3, min(args.steps, 10))
+        k_e2e = max(3, min(args.steps, 50))  # enough steps for a stable pipelined rate
         # (1) synchronous calls: upload, matvec, download, one after the other
         e0.record(stream)
         for _ in range(k_e2e):
