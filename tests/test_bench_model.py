@@ -24,9 +24,10 @@ def test_measured_peak_source():
         assert kind == "measured"
 
 
-def test_profiles_bench_line_contract():
-    # the committed bench line carries the keys the driver and the judge read
-    p = os.path.join(bench.ROOT, "profiles", "r02_bench.json")
+@pytest.mark.parametrize("name", ["r02_bench.json", "r02b_bench.json"])
+def test_profiles_bench_line_contract(name):
+    # the committed bench lines carry the keys the driver and the judge read
+    p = os.path.join(bench.ROOT, "profiles", name)
     if not os.path.exists(p):
         pytest.skip("no committed bench line")
     d = json.load(open(p))
