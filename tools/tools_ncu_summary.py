@@ -51,6 +51,10 @@ for (kid, name), lines in kern.items():
     wr = f(d["dram__bytes_write.sum"]) * scale.get(units[rh.index("dram__bytes_write.sum")], 1)
     print(f"   dram read {rd / 1e9:.4f} GB, write {wr / 1e9:.4f} GB, traffic {(rd + wr) / 1e9:.4f} GB")
     for h in ["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
-              "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum"]:
+              "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum",
+              # the L1 return path (64 B per wavefront and cycle per SM): the gathers' bound
+              "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+              "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg",
+              "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum", "sm__cycles_elapsed.max"]:
         if h in d:
             print(f"   {h} {d[h]}")
