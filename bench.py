@@ -577,7 +577,11 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local)
         if "MASTER_ADDR" not in os.environ:  # --force-slabs outside torchrun: a one-rank group
-            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
+            import socket
+            with socket.socket() as sk:  # any free port
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = local
