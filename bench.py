@@ -733,6 +733,36 @@ def main():
         V._lib.call("vr_host_free_pinned", hp_in)
         V._lib.call("vr_host_free_pinned", hp_out)
 
+    # ---- x1 slabs: 10 PCG iterations of the first Newton step ----
+    pcg10 = None
+    if slabs and not args.no_solve:
+        d_zero = ctx.to_device(np.zeros((3,) + ctx.local_dims))
+        s_zero = obj.evaluate(d_zero)
+        obj.compute_gradient(s_zero)
+        rhs = s_zero.get(V._lib.STATE_GRADIENT, host=False)
+        V._lib.call("vr_scale", ctx.handle, rhs.ptr, 3, -1.0)
+        V.pcg_solve(obj, s_zero, rhs, 1e-30, 2)  # warm-up
+        ctx.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0.record(stream)
+        _, pst = V.pcg_solve(obj, s_zero, rhs, 1e-30, 10)
+        e1.record(stream)
+        e1.synchronize()
+        ms_pcg = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms_pcg], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_pcg = float(t.item())
+        b_pcg = 148.0 * 8 * n ** 3  # B_mv + 39 F + 6 F_c ~ 148 F per PCG iteration
+        its = max(1, pst["iterations"])
+        peak_pcg, _ = measured_peak()
+        pcg10 = {"ms": ms_pcg, "iterations": pst["iterations"], "ms_per_iteration": ms_pcg / its,
+                 "bytes_per_iteration": b_pcg,
+                 "frac_of_aggregate_hbm": b_pcg / (ms_pcg / its / 1e3) / 1e9 / (peak_pcg * world),
+                 "note": "first Newton step (v = 0), spectral preconditioner; device events, max over ranks"}
+        s_zero.close()
+
     # ---- roofline of the dominant kernel ------------------------------------
     peak, peak_kind = measured_peak()
     per_matvec_bytes, per_launch = bytes_model(n, nt)
@@ -972,7 +1002,7 @@ def main():
                                                         "note": "separate serialised pass, events per kernel"},
                 "cpu_baseline": cpu, "clocks": clk.summary(), "gn_solve": solve,
                 "config4_single_gpu": cfg4, "config2": cfg2, "fp32_lane": f32, "comm": comm,
-                "memory": memory, "forced_slabs": bool(args.force_slabs)}
+                "memory": memory, "forced_slabs": bool(args.force_slabs), "pcg_10_iterations": pcg10}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
